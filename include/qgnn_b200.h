@@ -1,0 +1,234 @@
+/*
+ * qgnn_b200.h — C-ABI of the B200-native AdaQP boundary-message path.
+ *
+ * The reference (qgnn, /root/reference/proj) has no FFI: its operator API is
+ * a set of inline C++ functions called by trainer/engine.hpp.  Each entry
+ * point below replaces one of them; the citation names the function and
+ * file:line (relative to proj/include/qgnn/).  All signatures are plain C:
+ * pointers, sizes, enums.  Device pointers are marked [dev]; everything is
+ * asynchronous on the caller's cudaStream_t (passed as void*), and
+ * device-detected errors (non-finite input, corrupt chunk) are latched in the
+ * context's error word and reported by qgnn_ctx_check() at the phase
+ * boundary, mapped onto the reference's exception taxonomy below.
+ *
+ * There is no CPU fallback: every compute entry point launches sm_100a
+ * kernels and fails with QGNN_ECUDA when no device is present.
+ */
+#ifndef QGNN_B200_H
+#define QGNN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: common/errors.hpp:8-36 --------------------------------- */
+enum {
+  QGNN_OK = 0,
+  QGNN_EINVAL = 1,    /* std::invalid_argument (bad width, empty, non-finite, shape) */
+  QGNN_EDECODE = 2,   /* DecodeError (corrupt chunk / index mismatch) */
+  QGNN_EPROTOCOL = 3, /* ProtocolError (routing, plan version, buffer size) */
+  QGNN_ERESOURCE = 4, /* ResourceLimitError (brute-force solver limit) */
+  QGNN_EDIVERGED = 5, /* DivergedError (non-finite loss) */
+  QGNN_EIO = 6,       /* IoError */
+  QGNN_ECUDA = 7,     /* CUDA runtime failure / no device */
+  QGNN_ENCCL = 8      /* NCCL failure */
+};
+
+enum { QGNN_F32 = 0, QGNN_F64 = 1 };            /* element type of a dense buffer */
+enum { QGNN_WIRE_GPU = 0, QGNN_WIRE_REF = 1 };  /* chunk layout, see qgnn_chunk_wire_bytes */
+
+/* Message of the last failing call on this thread. */
+const char* qgnn_last_error(void);
+const char* qgnn_version(void);
+
+/* ---- context ---------------------------------------------------------------- */
+typedef struct qgnn_ctx qgnn_ctx;
+/* Binds `device`, allocates the device error word and split-K scratch. */
+int qgnn_ctx_create(int device, qgnn_ctx** out);
+int qgnn_ctx_destroy(qgnn_ctx* ctx);
+/* Synchronizes `stream`, reads and clears the device error word; returns the
+ * status of the first latched error (QGNN_EINVAL for non-finite quantize input,
+ * QGNN_EDECODE for a corrupt chunk) or QGNN_OK. */
+int qgnn_ctx_check(qgnn_ctx* ctx, void* stream);
+
+/* ---- RngStream: quantcodec/rng.hpp:13-61 ------------------------------------- */
+uint64_t qgnn_rng_seed_key(uint64_t seed);               /* RngStream(seed) key, rng.hpp:15 */
+uint64_t qgnn_rng_fork(uint64_t key, uint64_t coord);    /* fork(coord) key, rng.hpp:17-22 */
+uint64_t qgnn_rng_u64(uint64_t key, uint64_t counter);   /* next_u64 at counter, rng.hpp:30 */
+
+/* ---- sizes: quant.hpp:16-18, 103-107; plan.hpp:90-100 ------------------------ */
+uint64_t qgnn_packed_bytes(uint64_t count, int bits);
+/* QGNN_WIRE_REF: 25 + ceil(count*bits/8)  (byte-identical to append_chunk).
+ * QGNN_WIRE_GPU: 16-byte header {f32 scale, f32 zero, u32 count, u8 bits, 3 pad}
+ *                + payload padded to a 16-byte multiple.
+ * bits == 0 denotes a raw full-precision row (BitMode::kFp): count * elem bytes. */
+uint64_t qgnn_chunk_wire_bytes(uint64_t count, int bits, int layout, int dtype);
+
+/* encode_message_set's wire order (codec.hpp:56-69): width groups 2,4,8, caller
+ * order inside each.  Host helper.  wire_pos[k] = caller index of chunk k;
+ * offsets[i] = byte offset of caller message i; *total = set bytes. */
+int qgnn_wire_layout(const int32_t* bits, int64_t n, int64_t dim, int layout, int dtype,
+                     int64_t* wire_pos, uint64_t* offsets, uint64_t* total);
+
+/* ---- K1 quantize + pack: quant.hpp:60-90 via codec.hpp:41-72 ------------------
+ * Message i quantizes row rows[i] of `values` (dtype, row stride ld, dim
+ * columns) at width bits[i] with RNG stream fork(set_keys[set_of[i]], ids[i])
+ * and writes its chunk at out + offsets[i].  bits[i] == 0 copies the raw row
+ * (fp mode, engine.hpp:473-481).  win_lo/win_hi (optional, dtype, [n]) fold
+ * the row extrema into the message's trace window (trace.hpp:86-91).
+ * set_of == NULL means every message belongs to set 0.  [dev] for all arrays. */
+int qgnn_quantize_pack(qgnn_ctx* ctx, const void* values, int dtype, int64_t ld, int64_t dim,
+                       int64_t n, const int32_t* rows, const uint32_t* ids, const uint8_t* bits,
+                       const uint64_t* offsets, const uint16_t* set_of, const uint64_t* set_keys,
+                       int layout, uint8_t* out, void* win_lo, void* win_hi, void* stream);
+
+/* ---- K3 unpack + dequantize + scatter: quant.hpp:92-99, codec.hpp:80-96 --------
+ * Decodes message i's chunk at in + offsets[i] (validating width and count
+ * against bits[i] / dim — DecodeError semantics) and stores (accumulate == 0,
+ * engine.hpp:607-618) or adds (accumulate == 1, engine.hpp:729-733) the values
+ * into row dst_rows[i] of `out` (dst_rows == NULL: row i). */
+int qgnn_dequant_scatter(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int64_t dim,
+                         const uint8_t* bits, const uint64_t* offsets, int layout,
+                         const int32_t* dst_rows, int accumulate, void* out, int dtype,
+                         int64_t ld, void* stream);
+
+/* ---- K4 CSR aggregation: aggregate.hpp:94-165 ----------------------------------
+ * For each listed row r (rows != NULL: rows[k]; else row_begin + k):
+ *   out[r] = self_alpha[r] * x[r]                    (self_alpha may be NULL -> 0)
+ *          + sum_{e in [ptr_a[r], ptr_a[r+1])} alpha_a[e] * x[col_a[e]]
+ *          + sum_{e in [ptr_b[r], ptr_b[r+1])} alpha_b[e] * y[col_b[e]]   (ptr_b may be NULL)
+ * in that order.  aggregate_rows = (self, local CSR over h, remote CSR over
+ * the halo); aggregate_backward_local = (self, local CSR with alpha_bwd);
+ * backward_remote_partials = (no self, slot->marginal-row transpose CSR).
+ * F64 reproduces the reference's mul-then-add order bit for bit; F32 uses FMA. */
+int qgnn_csr_aggregate(qgnn_ctx* ctx, int dtype, int64_t dim, const void* x, int64_t ld_x,
+                       const void* y, int64_t ld_y, const void* self_alpha, const int64_t* ptr_a,
+                       const int32_t* col_a, const void* alpha_a, const int64_t* ptr_b,
+                       const int32_t* col_b, const void* alpha_b, const int32_t* rows,
+                       int64_t row_begin, int64_t n_rows, void* out, int64_t ld_out, void* stream);
+
+/* ---- K5 dense transform: model.hpp:90-170, matrix.hpp:51-65 --------------------
+ * forward:      out[r] = act(A[r] W)            W: din x dout row-major (layer_forward_rows)
+ * input grad:   out[r] = A[r] W^T               (input_grad_rows)
+ * weight grad:  out (+)= A[rows]^T B[rows]      (matmul_transa; deterministic split-K) */
+int qgnn_dense_forward(qgnn_ctx* ctx, int dtype, const void* A, int64_t lda, const void* W,
+                       int64_t din, int64_t dout, const int32_t* rows, int64_t row_begin,
+                       int64_t n_rows, int relu, void* out, int64_t ld_out, void* stream);
+int qgnn_dense_input_grad(qgnn_ctx* ctx, int dtype, const void* A, int64_t lda, const void* W,
+                          int64_t din, int64_t dout, const int32_t* rows, int64_t row_begin,
+                          int64_t n_rows, void* out, int64_t ld_out, void* stream);
+int qgnn_dense_weight_grad(qgnn_ctx* ctx, int dtype, const void* A, int64_t lda, const void* B,
+                           int64_t ldb, int64_t m, int64_t n, const int32_t* rows,
+                           int64_t row_begin, int64_t n_rows, int accumulate, void* out,
+                           void* stream);
+/* layer_backward_rows (model.hpp:128-153), ReLU only: dz = act > 0 ? dh : 0 */
+int qgnn_relu_backward(qgnn_ctx* ctx, int dtype, const void* act, int64_t ld_act, const void* dh,
+                       int64_t ld_dh, int64_t dim, int64_t row_begin, int64_t n_rows, void* dz,
+                       int64_t ld_dz, void* stream);
+/* masked_ce_partial (model.hpp:175-200) + count_correct (:216-227): writes grad
+ * rows of the listed rows, adds the scaled loss into *loss_acc [dev, f64] and
+ * argmax hits of the rows in correct_rows into *correct_acc [dev, u64]. */
+int qgnn_masked_ce(qgnn_ctx* ctx, int dtype, const void* logits, int64_t ld, int64_t classes,
+                   const int32_t* labels, const int32_t* rows, int64_t n_rows, double inv_denom,
+                   void* grad, int64_t ld_grad, double* loss_acc, void* stream);
+int qgnn_count_correct(qgnn_ctx* ctx, int dtype, const void* logits, int64_t ld, int64_t classes,
+                       const int32_t* labels, const int32_t* rows, int64_t n_rows,
+                       unsigned long long* correct_acc, void* stream);
+/* optimizer_step Adam branch (optim.hpp:47-62); bc1/bc2 = 1 - beta^t from the host. */
+int qgnn_adam_step(qgnn_ctx* ctx, int dtype, void* p, void* m, void* v, const void* g, int64_t n,
+                   double lr, double beta1, double beta2, double eps, double bc1, double bc2,
+                   void* stream);
+
+/* ---- host: graph / partition / coefficients (graphcore/{partition,coeffs}.hpp) ------------------ */
+/* partition_graph (partition.hpp:90-135): seeded BFS region growing -> owner[n]. */
+int qgnn_partition_graph(const int64_t* adj_ptr, const int32_t* adj, int64_t n, int64_t n_parts,
+                         uint64_t seed, uint32_t* owner);
+/* compute_coeffs (coeffs.hpp:30-45): alpha per CSR slot + self alpha (f64). */
+int qgnn_compute_coeffs(const int64_t* adj_ptr, const int32_t* adj, int64_t n, int sage,
+                        double* alpha, double* self_alpha);
+
+/* ---- host: assigner (assigner/solve.hpp) ---------------------------------------
+ * One instance = one tensor key across device pairs.  Messages are flat,
+ * grouped by pair: pair p has pair_count[p] messages (id, dim, lo, hi,
+ * sum_alpha_sq).  Runs group_and_order (solve.hpp:24-52) then the exact
+ * solve_assignment (solve.hpp:264-309), or brute_force_assignment
+ * (solve.hpp:220-258) when brute != 0; writes per-message bits (input order)
+ * and eval = {objective, variance_term, z_seconds}. */
+int qgnn_solve_instance(int64_t n_pairs, const uint32_t* pair_src, const uint32_t* pair_dst,
+                        const uint64_t* pair_count, const uint32_t* m_id, const uint64_t* m_dim,
+                        const double* m_lo, const double* m_hi, const double* m_asq,
+                        int64_t n_devices, const double* theta, const double* gamma,
+                        double lambda, int64_t group_size, int brute, int32_t* out_bits,
+                        double* eval);
+/* fit_cost_model (cost_model.hpp:78-109) for one pair: least squares on
+ * (bits, seconds) samples with clamp-to-zero. */
+int qgnn_fit_affine(const double* bits, const double* seconds, int64_t n, double* theta,
+                    double* gamma);
+
+/* ---- engine: trainer/engine.hpp:95-884 ------------------------------------------ */
+typedef struct qgnn_engine qgnn_engine;
+
+typedef struct {
+  int32_t sage;            /* AggMode: 0 GCN, 1 SAGE-mean */
+  int32_t n_dims;          /* dims = feature, hidden..., classes */
+  int64_t dims[8];
+  int32_t bit_mode;        /* BitMode: 0 fp, 1 fixed, 2 uniform, 3 adaptive */
+  int32_t fixed_bits;
+  double lambda;
+  int64_t group_size;
+  int64_t period;
+  uint64_t seed;
+  int64_t n_parts;         /* simulated devices = graph partitions (all ranks) */
+  double lr;
+  double theta, gamma;     /* uniform affine cost model (CostModel::uniform) */
+  int32_t dtype;           /* QGNN_F32 production, QGNN_F64 reference-order parity */
+  int32_t layout;          /* QGNN_WIRE_GPU or QGNN_WIRE_REF */
+  int32_t rank, world;     /* process rank / count; parts are split contiguously */
+  int32_t device;          /* CUDA device of this rank */
+  int32_t overlap;         /* 1: central compute on its own stream during the exchange */
+} qgnn_settings;
+
+typedef struct {
+  uint64_t epoch;
+  double train_loss, val_acc, test_acc;
+  uint64_t bytes_total;      /* actual wire bytes this epoch (all pairs) */
+  uint64_t ref_bytes_total;  /* reference-layout-equivalent bytes (25 + ceil(Db/8)) */
+  uint64_t msgs_b2, msgs_b4, msgs_b8, msgs_fp;
+  uint64_t plan_version;
+  double ms_total;           /* device time of the epoch (CUDA events) */
+  double ms_quant, ms_exchange, ms_central, ms_marginal, ms_backward, ms_step;
+  double resolve_seconds;    /* host solver time if a re-solve ran */
+} qgnn_epoch_metrics;
+
+/* Graph: symmetric sorted CSR without self loops (graph.hpp:20-56) + node
+ * features (f32 or f64 per settings dtype, n x dims[0]), labels and masks.
+ * owner == NULL partitions with partition_graph(g, n_parts, seed) like the
+ * reference engine (engine.hpp:212); otherwise partitions_from_owner. */
+int qgnn_engine_create(const qgnn_settings* s, int64_t n_nodes, const int64_t* adj_ptr,
+                       const int32_t* adj, const void* features, const int32_t* labels,
+                       const uint8_t* train, const uint8_t* val, const uint8_t* test,
+                       const uint32_t* owner, const void* nccl_unique_id, qgnn_engine** out);
+int qgnn_engine_destroy(qgnn_engine* e);
+/* One epoch (run_epoch, engine.hpp:384-426). */
+int qgnn_engine_run_epoch(qgnn_engine* e, qgnn_epoch_metrics* out);
+/* Re-upload node features of this rank's parts from host memory (f32/f64). */
+int qgnn_engine_set_features(qgnn_engine* e, const void* features);
+/* Weights of layer l (din x dout, settings dtype) to host memory. */
+int qgnn_engine_get_weights(qgnn_engine* e, int layer, void* out);
+int qgnn_engine_set_weights(qgnn_engine* e, int layer, const void* in);
+/* Static facts: [num_messages_per_tensor, n_parts, parts_on_rank, max_owned, max_halo]. */
+int qgnn_engine_info(qgnn_engine* e, int64_t* out5);
+/* Average device time (ms) of the named kernel class over the last epoch. */
+int qgnn_engine_kernel_stats(qgnn_engine* e, double* out, int n);
+
+/* NCCL bootstrap for world > 1: rank 0 creates the id, every rank passes it to
+ * qgnn_engine_create.  128 bytes. */
+int qgnn_nccl_unique_id(void* out128);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QGNN_B200_H */

@@ -1,0 +1,343 @@
+// codec.cu — K1 (stochastic quantize + LSB-first pack + trace window) and
+// K3 (unpack + dequantize + scatter/accumulate) for sm_100a.
+//
+// Work decomposition: one warp per message (row, destination).  The row is
+// read once for the extrema (warp-shuffle min/max), then each lane produces
+// whole 32-bit payload words (32/b codes each), so the payload store of a
+// warp is a contiguous, coalesced run.  Every element draws its own uniform
+// from the counter-based generator, u_i = mix(key + (i+1)*phi) >> 11, so the
+// draws are embarrassingly parallel and bit-identical to the reference's
+// sequential stream (quant.hpp:81-87).  The per-element arithmetic is the
+// reference's fp64 sequence x=(h-lo)/S, floor, frac, u<frac, clamp.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "rng.cuh"
+
+namespace qgnn_b200 {
+
+constexpr int kHdrGpu = 16;
+constexpr int kHdrRef = 25;
+
+__host__ __device__ inline uint64_t packed_bytes(uint64_t count, int b) {
+  return (count * static_cast<uint64_t>(b) + 7) / 8;
+}
+__host__ __device__ inline uint64_t chunk_bytes(uint64_t count, int b, int layout, int elem) {
+  if (b == 0) return count * static_cast<uint64_t>(elem);
+  if (layout == QGNN_WIRE_REF) return kHdrRef + packed_bytes(count, b);
+  return kHdrGpu + ((packed_bytes(count, b) + 15) / 16) * 16;
+}
+
+template <typename T>
+__device__ __forceinline__ bool is_finite_t(T v) {
+  return isfinite(v);
+}
+
+// Warp-wide first-occurrence fix-up for signed zeros: the reference's
+// sequential std::min/std::max keep the FIRST element equal to the extremum
+// (quant.hpp:63-68), which only matters for +0.0 vs -0.0.
+template <typename T>
+__device__ __forceinline__ T first_zero(const T* row, int dim, int lane) {
+  for (int base = 0; base < dim; base += 32) {
+    const int j = base + lane;
+    const bool z = j < dim && row[j] == T(0);
+    const unsigned mask = __ballot_sync(0xffffffffu, z);
+    if (mask) return row[base + __ffs(mask) - 1];
+  }
+  return T(0);
+}
+
+template <typename T>
+__device__ __forceinline__ void row_extrema(const T* __restrict__ row, int dim, int lane, T& lo,
+                                            T& hi, bool& finite) {
+  lo = INFINITY;
+  hi = -INFINITY;
+  finite = true;
+  for (int j = lane; j < dim; j += 32) {
+    const T v = row[j];
+    finite &= is_finite_t(v);
+    lo = v < lo ? v : lo;
+    hi = hi < v ? v : hi;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const T l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+    const T h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = l2 < lo ? l2 : lo;
+    hi = hi < h2 ? h2 : hi;
+  }
+  finite = __all_sync(0xffffffffu, finite);
+  if (lo == T(0)) lo = first_zero(row, dim, lane);
+  if (hi == T(0)) hi = first_zero(row, dim, lane);
+}
+
+__device__ __forceinline__ void store_u64_bytes(uint8_t* p, uint64_t v, int lane_byte, int base) {
+  // writes byte (lane_byte - base) of v when in range
+  const int k = lane_byte - base;
+  if (k >= 0 && k < 8) p[lane_byte] = static_cast<uint8_t>(v >> (8 * k));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_quantize_pack(
+    const T* __restrict__ values, int64_t ld, int dim, int64_t n, const int32_t* __restrict__ rows,
+    const uint32_t* __restrict__ ids, const uint8_t* __restrict__ bits,
+    const uint64_t* __restrict__ offsets, const uint16_t* __restrict__ set_of,
+    const uint64_t* __restrict__ set_keys, int layout, uint8_t* __restrict__ out,
+    T* __restrict__ win_lo, T* __restrict__ win_hi, int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t m = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (m >= n) return;
+  const T* row = values + static_cast<int64_t>(rows[m]) * ld;
+  const int b = bits[m];
+  uint8_t* chunk = out + offsets[m];
+
+  T lo, hi;
+  bool finite;
+  row_extrema(row, dim, lane, lo, hi, finite);
+  if (lane == 0 && win_lo) {  // trace.hpp:86-91 (update precedes encode, engine.hpp:487)
+    const T wl = win_lo[m], wh = win_hi[m];
+    win_lo[m] = lo < wl ? lo : wl;
+    win_hi[m] = wh < hi ? hi : wh;
+  }
+  if (b == 0) {  // BitMode::kFp: raw row (engine.hpp:473-481)
+    T* dst = reinterpret_cast<T*>(chunk);
+    for (int j = lane; j < dim; j += 32) dst[j] = row[j];
+    return;
+  }
+  if (b != 2 && b != 4 && b != 8) {
+    if (lane == 0) atomicOr(err, kErrBadWidth);
+    return;
+  }
+  if (!finite) {
+    if (lane == 0) atomicOr(err, kErrNonFinite);
+    return;
+  }
+  const double lo_d = static_cast<double>(lo), hi_d = static_cast<double>(hi);
+  const uint32_t levels = (1u << b) - 1;
+  const bool constant = hi_d == lo_d;
+  const double scale = constant ? 0.0 : (hi_d - lo_d) / static_cast<double>(levels);
+
+  uint8_t* payload;
+  if (layout == QGNN_WIRE_GPU) {
+    if (lane == 0) {
+      uint4 h;
+      h.x = __float_as_uint(static_cast<float>(scale));
+      h.y = __float_as_uint(static_cast<float>(lo_d));
+      h.z = static_cast<uint32_t>(dim);
+      h.w = static_cast<uint32_t>(b);
+      *reinterpret_cast<uint4*>(chunk) = h;
+    }
+    payload = chunk + kHdrGpu;
+  } else {  // quant.hpp:109-119, byte-identical
+    if (lane < kHdrRef) {
+      if (lane == 0) chunk[0] = static_cast<uint8_t>(b);
+      store_u64_bytes(chunk, static_cast<uint64_t>(dim), lane, 1);
+      store_u64_bytes(chunk, __double_as_longlong(scale), lane, 9);
+      store_u64_bytes(chunk, __double_as_longlong(lo_d), lane, 17);
+    }
+    payload = chunk + kHdrRef;
+  }
+
+  const int nbytes = static_cast<int>(packed_bytes(dim, b));
+  const int epw = 32 / b;
+  const int nwords =
+      layout == QGNN_WIRE_GPU ? ((nbytes + 15) / 16) * 4 : (nbytes + 3) / 4;
+  const uint64_t key = rng_fork(set_keys[set_of ? set_of[m] : 0], ids[m]);
+  const double lv = static_cast<double>(levels);
+
+  for (int w = lane; w < nwords; w += 32) {
+    uint32_t word = 0;
+    if (!constant) {
+      const int e0 = w * epw;
+      const int e1 = min(e0 + epw, dim);
+      for (int e = e0; e < e1; ++e) {
+        const double x = __ddiv_rn(__dsub_rn(static_cast<double>(row[e]), lo_d), scale);
+        double base = floor(x);
+        const double frac = __dsub_rn(x, base);
+        const double u = static_cast<double>(rng_u53(key, static_cast<uint64_t>(e) + 1)) *
+                         0x1.0p-53;
+        if (u < frac) base = __dadd_rn(base, 1.0);
+        const uint32_t code = static_cast<uint32_t>(base < lv ? base : lv);
+        word |= code << ((e - e0) * b);
+      }
+    }
+    if (layout == QGNN_WIRE_GPU) {
+      reinterpret_cast<uint32_t*>(payload)[w] = word;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (4 * w + k < nbytes) payload[4 * w + k] = static_cast<uint8_t>(word >> (8 * k));
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t load_u64_bytes(const uint8_t* p) {
+  uint64_t v = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v |= static_cast<uint64_t>(p[k]) << (8 * k);
+  return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_dequant_scatter(
+    const uint8_t* __restrict__ in, int64_t n, int dim, const uint8_t* __restrict__ bits,
+    const uint64_t* __restrict__ offsets, int layout, const int32_t* __restrict__ dst_rows,
+    int accumulate, T* __restrict__ out, int64_t ld, int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t m = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (m >= n) return;
+  const uint8_t* chunk = in + offsets[m];
+  const int b = bits[m];
+  T* dst = out + (dst_rows ? static_cast<int64_t>(dst_rows[m]) : m) * ld;
+  if (b == 0) {
+    const T* src = reinterpret_cast<const T*>(chunk);
+    for (int j = lane; j < dim; j += 32) dst[j] = accumulate ? dst[j] + src[j] : src[j];
+    return;
+  }
+  int hb;
+  uint64_t count;
+  double scale_d, zero_d;
+  float scale_f = 0.f, zero_f = 0.f;
+  const uint8_t* payload;
+  if (layout == QGNN_WIRE_GPU) {
+    const uint4 h = *reinterpret_cast<const uint4*>(chunk);
+    scale_f = __uint_as_float(h.x);
+    zero_f = __uint_as_float(h.y);
+    scale_d = scale_f;
+    zero_d = zero_f;
+    count = h.z;
+    hb = static_cast<int>(h.w & 0xff);
+    payload = chunk + kHdrGpu;
+  } else {
+    hb = chunk[0];
+    count = load_u64_bytes(chunk + 1);
+    scale_d = __longlong_as_double(load_u64_bytes(chunk + 9));
+    zero_d = __longlong_as_double(load_u64_bytes(chunk + 17));
+    payload = chunk + kHdrRef;
+  }
+  if (hb != b || count != static_cast<uint64_t>(dim)) {  // codec.hpp:88-89
+    if (lane == 0) atomicOr(err, kErrDecode);
+    return;
+  }
+  const int nbytes = static_cast<int>(packed_bytes(dim, b));
+  const int epw = 32 / b;
+  const uint32_t mask = (1u << b) - 1;
+  const int nwords = (nbytes + 3) / 4;
+  for (int w = lane; w < nwords; w += 32) {
+    uint32_t word;
+    if (layout == QGNN_WIRE_GPU) {
+      word = reinterpret_cast<const uint32_t*>(payload)[w];
+    } else {
+      word = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (4 * w + k < nbytes) word |= static_cast<uint32_t>(payload[4 * w + k]) << (8 * k);
+    }
+    const int e0 = w * epw;
+    const int e1 = min(e0 + epw, dim);
+    for (int e = e0; e < e1; ++e) {
+      const uint32_t code = (word >> ((e - e0) * b)) & mask;
+      T v;
+      if (sizeof(T) == 4 && layout == QGNN_WIRE_GPU) {
+        v = static_cast<T>(fmaf(static_cast<float>(code), scale_f, zero_f));
+      } else {  // quant.hpp:97: code*S then +Z, both rounded
+        v = static_cast<T>(__dadd_rn(__dmul_rn(static_cast<double>(code), scale_d), zero_d));
+      }
+      if (accumulate) {
+        if (sizeof(T) == 8)
+          dst[e] = static_cast<T>(__dadd_rn(static_cast<double>(dst[e]), static_cast<double>(v)));
+        else
+          dst[e] = dst[e] + v;
+      } else {
+        dst[e] = v;
+      }
+    }
+  }
+}
+
+}  // namespace qgnn_b200
+
+using namespace qgnn_b200;
+
+extern "C" {
+
+uint64_t qgnn_packed_bytes(uint64_t count, int bits) { return packed_bytes(count, bits); }
+
+uint64_t qgnn_chunk_wire_bytes(uint64_t count, int bits, int layout, int dtype) {
+  return chunk_bytes(count, bits, layout, dtype == QGNN_F64 ? 8 : 4);
+}
+
+int qgnn_wire_layout(const int32_t* bits, int64_t n, int64_t dim, int layout, int dtype,
+                     int64_t* wire_pos, uint64_t* offsets, uint64_t* total) {
+  QGNN_API_BEGIN
+  const int elem = dtype == QGNN_F64 ? 8 : 4;
+  uint64_t off = 0;
+  int64_t k = 0;
+  for (int64_t i = 0; i < n; ++i)
+    QGNN_REQUIRE(bits[i] == 0 || bits[i] == 2 || bits[i] == 4 || bits[i] == 8, QGNN_EINVAL,
+                 "encode_message_set: bit width must be 2, 4, or 8");
+  for (int b : {0, 2, 4, 8}) {
+    for (int64_t i = 0; i < n; ++i) {
+      if (bits[i] != b) continue;
+      if (wire_pos) wire_pos[k] = i;
+      ++k;
+      offsets[i] = off;
+      off += chunk_bytes(static_cast<uint64_t>(dim), b, layout, elem);
+    }
+  }
+  *total = off;
+  QGNN_API_END
+}
+
+int qgnn_quantize_pack(qgnn_ctx* ctx, const void* values, int dtype, int64_t ld, int64_t dim,
+                       int64_t n, const int32_t* rows, const uint32_t* ids, const uint8_t* bits,
+                       const uint64_t* offsets, const uint16_t* set_of, const uint64_t* set_keys,
+                       int layout, uint8_t* out, void* win_lo, void* win_hi, void* stream) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(ctx, QGNN_EINVAL, "quantize_pack: null context");
+  QGNN_REQUIRE(dim > 0, QGNN_EINVAL, "quantize: empty input");
+  if (n == 0) return QGNN_OK;
+  const int threads = 256;
+  const int64_t blocks = ceil_div(n * 32, threads);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == QGNN_F64)
+    k_quantize_pack<double><<<blocks, threads, 0, s>>>(
+        static_cast<const double*>(values), ld, static_cast<int>(dim), n, rows, ids, bits, offsets,
+        set_of, set_keys, layout, out, static_cast<double*>(win_lo), static_cast<double*>(win_hi),
+        ctx->d_err);
+  else
+    k_quantize_pack<float><<<blocks, threads, 0, s>>>(
+        static_cast<const float*>(values), ld, static_cast<int>(dim), n, rows, ids, bits, offsets,
+        set_of, set_keys, layout, out, static_cast<float*>(win_lo), static_cast<float*>(win_hi),
+        ctx->d_err);
+  check_launch("k_quantize_pack");
+  QGNN_API_END
+}
+
+int qgnn_dequant_scatter(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int64_t dim,
+                         const uint8_t* bits, const uint64_t* offsets, int layout,
+                         const int32_t* dst_rows, int accumulate, void* out, int dtype,
+                         int64_t ld, void* stream) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(ctx, QGNN_EINVAL, "dequant_scatter: null context");
+  if (n == 0) return QGNN_OK;
+  const int threads = 256;
+  const int64_t blocks = ceil_div(n * 32, threads);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == QGNN_F64)
+    k_dequant_scatter<double><<<blocks, threads, 0, s>>>(in, n, static_cast<int>(dim), bits,
+                                                         offsets, layout, dst_rows, accumulate,
+                                                         static_cast<double*>(out), ld, ctx->d_err);
+  else
+    k_dequant_scatter<float><<<blocks, threads, 0, s>>>(in, n, static_cast<int>(dim), bits,
+                                                        offsets, layout, dst_rows, accumulate,
+                                                        static_cast<float*>(out), ld, ctx->d_err);
+  check_launch("k_dequant_scatter");
+  QGNN_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// common.cuh — shared helpers for the sm_100a boundary-message kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "qgnn_b200.h"
+#include "status.hpp"
+
+namespace qgnn_b200 {
+
+// Device error word bits (latched by kernels, read by qgnn_ctx_check).
+enum : int {
+  kErrNonFinite = 1,   // quantize: non-finite input       -> QGNN_EINVAL   (quant.hpp:64)
+  kErrDecode = 2,      // chunk width/count/index mismatch -> QGNN_EDECODE  (codec.hpp:82-95)
+  kErrBadWidth = 4,    // bit width not in {2,4,8}         -> QGNN_EINVAL   (quant.hpp:61)
+  kErrLabel = 8,       // label out of range               -> QGNN_EINVAL   (model.hpp:185)
+};
+
+#define QGNN_CUDA(call)                                                                  \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw ::qgnn_b200::Status(QGNN_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// Launch check: catches configuration errors synchronously.
+inline void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Status(QGNN_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// ---- arithmetic policy ------------------------------------------------------
+// F64 reproduces the reference's x86-64 arithmetic (mul rounded, then add
+// rounded, no contraction); F32 is the production path and contracts.
+template <typename T>
+struct Arith;
+template <>
+struct Arith<double> {
+  __device__ __forceinline__ static double madd(double a, double x, double acc) {
+    return __dadd_rn(acc, __dmul_rn(a, x));
+  }
+  __device__ __forceinline__ static double mul(double a, double x) { return __dmul_rn(a, x); }
+};
+template <>
+struct Arith<float> {
+  __device__ __forceinline__ static float madd(float a, float x, float acc) {
+    return fmaf(a, x, acc);
+  }
+  __device__ __forceinline__ static float mul(float a, float x) { return a * x; }
+};
+
+struct Ctx;  // defined in ctx.cu
+
+}  // namespace qgnn_b200
+
+struct qgnn_ctx {
+  int device = 0;
+  int* d_err = nullptr;          // device error word
+  void* scratch = nullptr;       // split-K workspace
+  size_t scratch_bytes = 0;
+  int num_sms = 148;
+};
+
+namespace qgnn_b200 {
+// Grows ctx->scratch to at least `bytes` (synchronous; call outside capture).
+void* ctx_scratch(qgnn_ctx* ctx, size_t bytes);
+}  // namespace qgnn_b200

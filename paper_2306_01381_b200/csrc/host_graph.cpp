@@ -1,0 +1,531 @@
+// host_graph.cpp — partitioning, coefficients, GPU aggregation views and the
+// synthetic planted-block graph generator (host setup for the GPU engine).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <numeric>
+#include <thread>
+
+#include "host.hpp"
+#include "qgnn_b200.h"
+#include "rng.cuh"
+#include "status.hpp"
+
+namespace qgnn_b200 {
+
+namespace {
+template <typename F>
+void parallel_for(int64_t n, F&& f, int max_threads = 0) {
+  int64_t t = std::max(1u, std::thread::hardware_concurrency());
+  if (max_threads > 0) t = std::min<int64_t>(t, max_threads);
+  t = std::min<int64_t>(t, std::max<int64_t>(1, n));
+  if (t <= 1) {
+    for (int64_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  const int64_t chunk = (n + t - 1) / t;
+  for (int64_t w = 0; w < t; ++w)
+    th.emplace_back([&, w] {
+      for (int64_t i = w * chunk; i < std::min(n, (w + 1) * chunk); ++i) f(i);
+    });
+  for (auto& x : th) x.join();
+}
+}  // namespace
+
+// partition.hpp:90-135 — identical claim order, quotas and RNG draws.
+std::vector<uint32_t> partition_owner_bfs(const int64_t* ptr, const int32_t* adj, int64_t n,
+                                          int64_t n_parts, uint64_t seed) {
+  QGNN_REQUIRE(n_parts >= 1 && n_parts <= n, QGNN_EINVAL,
+               "partition_graph: n_parts must be in [1, num_nodes]");
+  std::vector<uint32_t> owner(n, UINT32_MAX);
+  std::vector<int64_t> quota(n_parts, n / n_parts);
+  for (int64_t p = 0; p < n % n_parts; ++p) ++quota[p];
+  const uint64_t key = rng_fork(rng_seed_key(seed), 0x9a27);
+  uint64_t ctr = 0;
+  std::vector<std::deque<uint32_t>> frontier(n_parts);
+  std::vector<char> rooted(n, 0);
+  for (int64_t p = 0; p < n_parts; ++p) {
+    uint32_t r = static_cast<uint32_t>(rng_next_below(key, ctr, n));
+    while (rooted[r]) r = static_cast<uint32_t>(rng_next_below(key, ctr, n));
+    rooted[r] = 1;
+    frontier[p].push_back(r);
+  }
+  std::vector<int64_t> owned(n_parts, 0);
+  uint32_t next_unclaimed = 0;
+  int64_t assigned = 0;
+  while (assigned < n) {
+    for (int64_t p = 0; p < n_parts && assigned < n; ++p) {
+      if (owned[p] >= quota[p]) continue;
+      uint32_t v = UINT32_MAX;
+      while (!frontier[p].empty()) {
+        const uint32_t c = frontier[p].front();
+        frontier[p].pop_front();
+        if (owner[c] == UINT32_MAX) {
+          v = c;
+          break;
+        }
+      }
+      if (v == UINT32_MAX) {
+        while (next_unclaimed < n && owner[next_unclaimed] != UINT32_MAX) ++next_unclaimed;
+        v = next_unclaimed;
+      }
+      owner[v] = static_cast<uint32_t>(p);
+      ++owned[p];
+      ++assigned;
+      for (int64_t e = ptr[v]; e < ptr[v + 1]; ++e)
+        if (owner[adj[e]] == UINT32_MAX) frontier[p].push_back(static_cast<uint32_t>(adj[e]));
+    }
+  }
+  return owner;
+}
+
+// partition.hpp:39-84 — consumer sets as per-node bitmasks (P <= 64).
+std::vector<Part> partitions_from_owner(const int64_t* ptr, const int32_t* adj, int64_t n,
+                                        const uint32_t* owner, int64_t n_parts) {
+  QGNN_REQUIRE(n_parts >= 1 && n_parts <= 64, QGNN_EINVAL, "partitions: 1..64 parts supported");
+  std::vector<Part> parts(n_parts);
+  for (int64_t p = 0; p < n_parts; ++p) {
+    parts[p].id = static_cast<uint32_t>(p);
+    parts[p].remote_in.resize(n_parts);
+    parts[p].remote_out.resize(n_parts);
+  }
+  for (int64_t v = 0; v < n; ++v) {
+    QGNN_REQUIRE(owner[v] < n_parts, QGNN_EINVAL, "owner id out of range");
+    parts[owner[v]].owned.push_back(static_cast<uint32_t>(v));
+  }
+  std::vector<uint64_t> consumers(n, 0);
+  parallel_for(n, [&](int64_t v) {
+    uint64_t m = 0;
+    for (int64_t e = ptr[v]; e < ptr[v + 1]; ++e) {
+      const uint32_t q = owner[adj[e]];
+      if (q != owner[v]) m |= uint64_t{1} << q;
+    }
+    consumers[v] = m;
+  });
+  parallel_for(n_parts, [&](int64_t p) {
+    Part& P = parts[p];
+    for (uint32_t v : P.owned) (consumers[v] ? P.marginal : P.central).push_back(v);
+    for (int64_t q = 0; q < n_parts; ++q) {
+      if (q == p) continue;
+      for (uint32_t v : P.owned)
+        if (consumers[v] >> q & 1) P.remote_out[q].push_back(v);
+      for (uint32_t u : parts[q].owned)
+        if (consumers[u] >> p & 1) P.remote_in[q].push_back(u);
+    }
+  });
+  return parts;
+}
+
+// coeffs.hpp:30-45
+void compute_coeffs(const int64_t* ptr, const int32_t* adj, int64_t n, bool sage,
+                    std::vector<double>& alpha, std::vector<double>& self_alpha) {
+  alpha.assign(ptr[n], 0.0);
+  self_alpha.assign(n, 0.0);
+  parallel_for(n, [&](int64_t v) {
+    const double dv1 = static_cast<double>(ptr[v + 1] - ptr[v]) + 1.0;
+    self_alpha[v] = 1.0 / dv1;
+    for (int64_t e = ptr[v]; e < ptr[v + 1]; ++e) {
+      const int64_t u = adj[e];
+      const double du1 = static_cast<double>(ptr[u + 1] - ptr[u]) + 1.0;
+      alpha[e] = sage ? 1.0 / dv1 : 1.0 / std::sqrt(du1 * dv1);
+    }
+  });
+}
+
+int32_t View::gpu_row(uint32_t node) const {
+  auto it = std::lower_bound(owned_sorted.begin(), owned_sorted.end(), node);
+  if (it == owned_sorted.end() || *it != node) return -1;
+  return owned_gpu_row[it - owned_sorted.begin()];
+}
+
+// aggregate.hpp:41-89 in GPU row order (central block then marginal block).
+View build_view(const int64_t* ptr, const int32_t* adj, int64_t n, const Part& part,
+                int64_t n_parts, const std::vector<double>& alpha,
+                const std::vector<double>& self_alpha, bool sage) {
+  (void)n;
+  View v;
+  v.num_owned = static_cast<int64_t>(part.owned.size());
+  v.n_central = static_cast<int64_t>(part.central.size());
+  v.n_marginal = static_cast<int64_t>(part.marginal.size());
+  v.owned_sorted = part.owned;
+  v.owned_gpu_row.assign(v.num_owned, -1);
+  v.row_node.reserve(v.num_owned);
+  for (uint32_t x : part.central) v.row_node.push_back(x);
+  for (uint32_t x : part.marginal) v.row_node.push_back(x);
+  v.ref_row.assign(v.num_owned, 0);
+  v.gpu_row_of_ref.assign(v.num_owned, 0);
+  // owned ids ascending == reference row order; central/marginal are sorted subsets
+  {
+    size_t ic = 0, im = 0;
+    for (int64_t r = 0; r < v.num_owned; ++r) {
+      const uint32_t node = part.owned[r];
+      int32_t g;
+      if (ic < part.central.size() && part.central[ic] == node)
+        g = static_cast<int32_t>(ic++);
+      else
+        g = static_cast<int32_t>(v.n_central + static_cast<int64_t>(im++));
+      v.owned_gpu_row[r] = g;
+      v.ref_row[g] = static_cast<int32_t>(r);
+      v.gpu_row_of_ref[r] = g;
+    }
+  }
+  // halo slots: remote_in lists by ascending source (aggregate.hpp:45-56)
+  v.device_slot_offset.assign(n_parts + 1, 0);
+  for (int64_t q = 0; q < n_parts; ++q) {
+    v.device_slot_offset[q] = static_cast<int64_t>(v.slot_node.size());
+    for (uint32_t k : part.remote_in[q]) v.slot_node.push_back(k);
+  }
+  v.device_slot_offset[n_parts] = static_cast<int64_t>(v.slot_node.size());
+  v.num_remote = static_cast<int64_t>(v.slot_node.size());
+  // slot lookup: (owner q, index in remote_in[q]) via binary search per source list
+  auto slot_of = [&](uint32_t node, uint32_t q) -> int32_t {
+    const auto& lst = part.remote_in[q];
+    auto it = std::lower_bound(lst.begin(), lst.end(), node);
+    return static_cast<int32_t>(v.device_slot_offset[q] + (it - lst.begin()));
+  };
+  // owner lookup for remote neighbours: a node not owned here is in exactly one remote_in list
+  std::vector<std::pair<uint32_t, uint32_t>> remote_owner;  // (node, q) sorted by node
+  for (int64_t q = 0; q < n_parts; ++q)
+    for (uint32_t k : part.remote_in[q]) remote_owner.emplace_back(k, static_cast<uint32_t>(q));
+  std::sort(remote_owner.begin(), remote_owner.end());
+
+  v.self_alpha.assign(v.num_owned, 0.0);
+  v.local_ptr.assign(v.num_owned + 1, 0);
+  v.remote_ptr.assign(v.num_owned + 1, 0);
+  for (int64_t g = 0; g < v.num_owned; ++g) {
+    const uint32_t node = v.row_node[g];
+    v.self_alpha[g] = self_alpha[node];
+    for (int64_t e = ptr[node]; e < ptr[node + 1]; ++e) {
+      const uint32_t u = static_cast<uint32_t>(adj[e]);
+      const int32_t lr = v.gpu_row(u);
+      if (lr >= 0) {
+        v.local_col.push_back(lr);
+        v.local_afwd.push_back(alpha[e]);
+        v.local_abwd.push_back(sage ? self_alpha[u] : alpha[e]);  // coeffs.of(g, v, u)
+      } else {
+        auto it = std::lower_bound(remote_owner.begin(), remote_owner.end(),
+                                   std::make_pair(u, uint32_t{0}));
+        QGNN_REQUIRE(it != remote_owner.end() && it->first == u, QGNN_EINVAL,
+                     "view: remote neighbour missing from remote_in");
+        v.remote_slot.push_back(slot_of(u, it->second));
+        v.remote_alpha.push_back(alpha[e]);
+      }
+    }
+    v.local_ptr[g + 1] = static_cast<int64_t>(v.local_col.size());
+    v.remote_ptr[g + 1] = static_cast<int64_t>(v.remote_slot.size());
+  }
+  // transpose of the remote CSR, contributions in ascending reference-row order
+  v.slot_ptr.assign(v.num_remote + 1, 0);
+  for (int32_t s : v.remote_slot) ++v.slot_ptr[s + 1];
+  for (int64_t k = 0; k < v.num_remote; ++k) v.slot_ptr[k + 1] += v.slot_ptr[k];
+  v.slot_row.assign(v.remote_slot.size(), 0);
+  v.slot_alpha.assign(v.remote_slot.size(), 0.0);
+  {
+    std::vector<int64_t> fill(v.slot_ptr.begin(), v.slot_ptr.end() - 1);
+    for (int64_t r = 0; r < v.num_owned; ++r) {  // reference row order
+      const int32_t g = v.gpu_row_of_ref[r];
+      for (int64_t e = v.remote_ptr[g]; e < v.remote_ptr[g + 1]; ++e) {
+        const int32_t s = v.remote_slot[e];
+        v.slot_row[fill[s]] = g;
+        v.slot_alpha[fill[s]] = v.remote_alpha[e];
+        ++fill[s];
+      }
+    }
+  }
+  // engine.hpp:262-273: squared consumption weights of incoming messages
+  v.rx_alpha_sq.assign(n_parts, {});
+  for (int64_t p = 0; p < n_parts; ++p) v.rx_alpha_sq[p].assign(part.remote_in[p].size(), 0.0);
+  {
+    std::vector<uint32_t> slot_src(v.num_remote);
+    for (int64_t q = 0; q < n_parts; ++q)
+      for (int64_t k = v.device_slot_offset[q]; k < v.device_slot_offset[q + 1]; ++k)
+        slot_src[k] = static_cast<uint32_t>(q);
+    for (int64_t r = 0; r < v.num_owned; ++r) {
+      const int32_t g = v.gpu_row_of_ref[r];
+      for (int64_t e = v.remote_ptr[g]; e < v.remote_ptr[g + 1]; ++e) {
+        const int32_t s = v.remote_slot[e];
+        const uint32_t src = slot_src[s];
+        const double a = v.remote_alpha[e];
+        v.rx_alpha_sq[src][s - v.device_slot_offset[src]] += a * a;
+      }
+    }
+  }
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// Planted-block power-law generator.
+//
+// Nodes are split into `blocks` contiguous id ranges (the planted partition:
+// owner = block).  Node u emits k_u undirected edges with k_u drawn from a
+// discrete Pareto law (mean avg_degree/2, exponent `gamma`).  A fraction
+// `cross_frac` of them lands in another block on a node picked with
+// probability proportional to its own Pareto weight (hubs attract cut edges,
+// as in real co-purchase/social graphs); the rest stay in the block at a
+// log-uniform id distance (community locality as left by a locality-
+// preserving node order such as METIS/RCM).  Pairs are de-duplicated, self
+// loops dropped and the count is trimmed/topped up to exactly n_edges.
+// Labels follow 256-node communities; features are sep*mu_class + N(0,1)
+// (synth.hpp:112-124 recipe) drawn from per-node RngStream forks.
+// ---------------------------------------------------------------------------
+struct PlantedSpec {
+  int64_t nodes, n_edges, feat, classes, blocks;
+  double cross_frac, gamma, sep;
+  uint64_t seed;
+};
+
+static double u01(uint64_t key, uint64_t ctr) {
+  return static_cast<double>(rng_u53(key, ctr)) * 0x1.0p-53;
+}
+
+static void gen_planted(const PlantedSpec& s, int64_t* adj_ptr, int32_t* adj, float* features,
+                        int32_t* labels, uint8_t* train, uint8_t* val, uint8_t* test) {
+  const int64_t n = s.nodes;
+  const int64_t bsz = (n + s.blocks - 1) / s.blocks;
+  const uint64_t root = rng_seed_key(s.seed);
+  // Pareto weights w_u >= 1, tail exponent gamma; k_u ~ w_u * scale
+  std::vector<double> w(n);
+  const uint64_t kw = rng_fork(root, 0x61);
+  parallel_for(n, [&](int64_t u) {
+    const double x = u01(kw, static_cast<uint64_t>(u) + 1);
+    w[u] = std::pow(1.0 - x, -1.0 / (s.gamma - 1.0));
+  });
+  // cumulative weights per block for preferential cross targets
+  std::vector<double> cum(n + 1, 0.0);
+  for (int64_t u = 0; u < n; ++u) cum[u + 1] = cum[u] + w[u];
+  const double wsum = cum[n];
+  const double target_pairs = static_cast<double>(s.n_edges) * 1.03;
+  const double scale = target_pairs / wsum;
+
+  const int nt = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  std::vector<std::vector<uint64_t>> buckets(nt);
+  const uint64_t ke = rng_fork(root, 0x62);
+  {
+    std::vector<std::thread> th;
+    const int64_t chunk = (n + nt - 1) / nt;
+    for (int t = 0; t < nt; ++t)
+      th.emplace_back([&, t] {
+        auto& out = buckets[t];
+        for (int64_t u = t * chunk; u < std::min(n, (t + 1) * chunk); ++u) {
+          const uint64_t k = rng_fork(ke, static_cast<uint64_t>(u));
+          uint64_t c = 0;
+          const double lam = w[u] * scale;
+          int64_t ku = static_cast<int64_t>(lam);
+          if (u01(k, ++c) < lam - static_cast<double>(ku)) ++ku;
+          const int64_t b = u / bsz;
+          const int64_t b0 = b * bsz, b1 = std::min(n, b0 + bsz);
+          for (int64_t e = 0; e < ku; ++e) {
+            int64_t v;
+            if (s.blocks > 1 && u01(k, ++c) < s.cross_frac) {
+              // other block, preferential by weight
+              int64_t ob = static_cast<int64_t>(u01(k, ++c) * (s.blocks - 1));
+              if (ob >= b) ++ob;
+              const int64_t o0 = ob * bsz, o1 = std::min(n, o0 + bsz);
+              const double t2 = cum[o0] + u01(k, ++c) * (cum[o1] - cum[o0]);
+              v = std::upper_bound(cum.begin() + o0, cum.begin() + o1 + 1, t2) - cum.begin() - 1;
+              v = std::clamp<int64_t>(v, o0, o1 - 1);
+            } else {
+              const double span = static_cast<double>(b1 - b0);
+              const double dist = std::floor(std::exp(u01(k, ++c) * std::log(span)));
+              const int64_t d = static_cast<int64_t>(dist);
+              v = u01(k, ++c) < 0.5 ? u + d : u - d;
+              const int64_t len = b1 - b0;
+              v = b0 + (((v - b0) % len) + len) % len;
+            }
+            if (v == u) continue;
+            const uint64_t a = static_cast<uint64_t>(std::min(u, v)),
+                           bb = static_cast<uint64_t>(std::max(u, v));
+            out.push_back(a << 32 | bb);
+          }
+        }
+      });
+    for (auto& x : th) x.join();
+  }
+  // global radix by high node id range, sort + unique per range
+  std::vector<std::vector<uint64_t>> ranges(nt);
+  const int64_t rchunk = (n + nt - 1) / nt;
+  {
+    std::vector<std::vector<size_t>> counts(nt, std::vector<size_t>(nt, 0));
+    for (int t = 0; t < nt; ++t)
+      for (uint64_t x : buckets[t]) ++counts[t][static_cast<int64_t>(x >> 32) / rchunk];
+    for (int r = 0; r < nt; ++r) {
+      size_t tot = 0;
+      for (int t = 0; t < nt; ++t) tot += counts[t][r];
+      ranges[r].reserve(tot);
+    }
+    for (int t = 0; t < nt; ++t) {
+      for (uint64_t x : buckets[t]) ranges[static_cast<int64_t>(x >> 32) / rchunk].push_back(x);
+      std::vector<uint64_t>().swap(buckets[t]);
+    }
+  }
+  parallel_for(nt, [&](int64_t r) {
+    auto& v = ranges[r];
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+  });
+  std::vector<uint64_t> pairs;
+  {
+    size_t tot = 0;
+    for (auto& r : ranges) tot += r.size();
+    pairs.reserve(tot);
+    for (auto& r : ranges) {
+      pairs.insert(pairs.end(), r.begin(), r.end());
+      std::vector<uint64_t>().swap(r);
+    }
+  }
+  // exact edge count: drop a deterministic random subset, or top up with
+  // extra local edges (rare; the 3% overshoot normally covers duplicates)
+  const int64_t want = s.n_edges;
+  if (static_cast<int64_t>(pairs.size()) > want) {
+    const uint64_t kd = rng_fork(root, 0x63);
+    std::vector<std::pair<uint64_t, uint64_t>> keyed(pairs.size());
+    parallel_for(static_cast<int64_t>(pairs.size()), [&](int64_t i) {
+      keyed[i] = {rng_u64(kd, pairs[i]), pairs[i]};
+    });
+    std::nth_element(keyed.begin(), keyed.begin() + want, keyed.end());
+    keyed.resize(want);
+    pairs.resize(want);
+    for (int64_t i = 0; i < want; ++i) pairs[i] = keyed[i].second;
+    std::vector<std::pair<uint64_t, uint64_t>>().swap(keyed);
+    std::sort(pairs.begin(), pairs.end());
+  } else {
+    uint64_t c = 0;
+    const uint64_t kt = rng_fork(root, 0x64);
+    std::vector<uint64_t> extra;
+    while (static_cast<int64_t>(pairs.size() + extra.size()) < want) {
+      const int64_t u = static_cast<int64_t>(rng_u64(kt, ++c) % static_cast<uint64_t>(n));
+      const int64_t b0 = (u / bsz) * bsz, b1 = std::min(n, b0 + bsz);
+      const int64_t v = b0 + static_cast<int64_t>(rng_u64(kt, ++c) % static_cast<uint64_t>(b1 - b0));
+      if (u == v) continue;
+      const uint64_t key = static_cast<uint64_t>(std::min(u, v)) << 32 |
+                           static_cast<uint64_t>(std::max(u, v));
+      if (std::binary_search(pairs.begin(), pairs.end(), key)) continue;
+      extra.push_back(key);
+      if (static_cast<int64_t>(pairs.size() + extra.size()) == want) {
+        std::sort(extra.begin(), extra.end());
+        extra.erase(std::unique(extra.begin(), extra.end()), extra.end());
+      }
+    }
+    pairs.insert(pairs.end(), extra.begin(), extra.end());
+    std::sort(pairs.begin(), pairs.end());
+  }
+  // symmetric CSR
+  std::vector<int64_t> deg(n + 1, 0);
+  for (uint64_t x : pairs) {
+    ++deg[(x >> 32) + 1];
+    ++deg[(x & 0xffffffffu) + 1];
+  }
+  adj_ptr[0] = 0;
+  for (int64_t v = 0; v < n; ++v) adj_ptr[v + 1] = adj_ptr[v] + deg[v + 1];
+  {
+    std::vector<int64_t> fill(adj_ptr, adj_ptr + n);
+    for (uint64_t x : pairs) {
+      const int64_t a = static_cast<int64_t>(x >> 32), b = static_cast<int64_t>(x & 0xffffffffu);
+      adj[fill[a]++] = static_cast<int32_t>(b);
+      adj[fill[b]++] = static_cast<int32_t>(a);
+    }
+  }
+  std::vector<uint64_t>().swap(pairs);
+  parallel_for(n, [&](int64_t v) { std::sort(adj + adj_ptr[v], adj + adj_ptr[v + 1]); });
+  // labels: 256-node communities mapped to classes by a hash
+  const uint64_t kl = rng_fork(root, 0x51);
+  parallel_for(n, [&](int64_t v) {
+    labels[v] = static_cast<int32_t>(rng_u64(kl, static_cast<uint64_t>(v / 256)) %
+                                     static_cast<uint64_t>(s.classes));
+  });
+  // class means (synth.hpp:127-131) then per-node noise (:132-137)
+  std::vector<double> means(s.classes * s.feat);
+  {
+    const uint64_t km = rng_fork(root, 0x54);
+    uint64_t c = 0;
+    for (auto& x : means) {
+      double a = u01(km, ++c);
+      while (a <= 0.0) a = u01(km, ++c);
+      const double b = u01(km, ++c);
+      x = std::sqrt(-2.0 * std::log(a)) * std::cos(6.283185307179586476925286766559 * b);
+    }
+  }
+  const uint64_t kf = rng_fork(root, 0x55);
+  parallel_for(n, [&](int64_t v) {
+    const uint64_t k = rng_fork(kf, static_cast<uint64_t>(v));
+    uint64_t c = 0;
+    for (int64_t j = 0; j < s.feat; ++j) {
+      double a = u01(k, ++c);
+      while (a <= 0.0) a = u01(k, ++c);
+      const double b = u01(k, ++c);
+      const double gz = std::sqrt(-2.0 * std::log(a)) * std::cos(6.283185307179586476925286766559 * b);
+      features[v * s.feat + j] = static_cast<float>(s.sep * means[labels[v] * s.feat + j] + gz);
+    }
+  });
+  // 60/20/20 split by a per-node draw
+  const uint64_t ks = rng_fork(root, 0x56);
+  parallel_for(n, [&](int64_t v) {
+    const double x = u01(ks, static_cast<uint64_t>(v) + 1);
+    train[v] = x < 0.6;
+    val[v] = x >= 0.6 && x < 0.8;
+    test[v] = x >= 0.8;
+  });
+}
+
+}  // namespace qgnn_b200
+
+using namespace qgnn_b200;
+
+extern "C" {
+
+int qgnn_partition_graph(const int64_t* adj_ptr, const int32_t* adj, int64_t n, int64_t n_parts,
+                         uint64_t seed, uint32_t* owner) {
+  QGNN_API_BEGIN
+  const auto o = partition_owner_bfs(adj_ptr, adj, n, n_parts, seed);
+  std::memcpy(owner, o.data(), o.size() * sizeof(uint32_t));
+  QGNN_API_END
+}
+
+int qgnn_compute_coeffs(const int64_t* adj_ptr, const int32_t* adj, int64_t n, int sage,
+                        double* alpha, double* self_alpha) {
+  QGNN_API_BEGIN
+  std::vector<double> a, sa;
+  compute_coeffs(adj_ptr, adj, n, sage != 0, a, sa);
+  std::memcpy(alpha, a.data(), a.size() * sizeof(double));
+  std::memcpy(self_alpha, sa.data(), sa.size() * sizeof(double));
+  QGNN_API_END
+}
+
+// Planted-block generator (see gen_planted).  adj must hold 2 * n_edges entries.
+int qgnn_generate_planted(int64_t nodes, int64_t n_edges, int64_t feat, int64_t classes,
+                          int64_t blocks, double cross_frac, double gamma, double sep,
+                          uint64_t seed, int64_t* adj_ptr, int32_t* adj, float* features,
+                          int32_t* labels, uint8_t* train, uint8_t* val, uint8_t* test) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(nodes > 1 && n_edges > 0 && blocks >= 1 && blocks <= nodes, QGNN_EINVAL,
+               "generate_planted: bad sizes");
+  QGNN_REQUIRE(n_edges < nodes * (nodes - 1) / 4, QGNN_EINVAL, "generate_planted: too dense");
+  PlantedSpec s{nodes, n_edges, feat, classes, blocks, cross_frac, gamma, sep, seed};
+  gen_planted(s, adj_ptr, adj, features, labels, train, val, test);
+  QGNN_API_END
+}
+
+// Partition statistics for an owner map: per part [owned, central, marginal,
+// halo (num_remote), sum_q |remote_out[q]|].  out has 5 * n_parts entries.
+int qgnn_partition_stats(const int64_t* adj_ptr, const int32_t* adj, int64_t n,
+                         const uint32_t* owner, int64_t n_parts, int64_t* out) {
+  QGNN_API_BEGIN
+  const auto parts = partitions_from_owner(adj_ptr, adj, n, owner, n_parts);
+  for (int64_t p = 0; p < n_parts; ++p) {
+    int64_t halo = 0, outm = 0;
+    for (int64_t q = 0; q < n_parts; ++q) {
+      halo += static_cast<int64_t>(parts[p].remote_in[q].size());
+      outm += static_cast<int64_t>(parts[p].remote_out[q].size());
+    }
+    out[5 * p + 0] = static_cast<int64_t>(parts[p].owned.size());
+    out[5 * p + 1] = static_cast<int64_t>(parts[p].central.size());
+    out[5 * p + 2] = static_cast<int64_t>(parts[p].marginal.size());
+    out[5 * p + 3] = halo;
+    out[5 * p + 4] = outm;
+  }
+  QGNN_API_END
+}
+
+}  // extern "C"

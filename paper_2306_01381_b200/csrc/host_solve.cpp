@@ -1,0 +1,395 @@
+// host_solve.cpp — the adaptive bit-width assigner kept on the host
+// (north star (6)): variance weights, grouping, the canonical bi-objective,
+// the exact per-pair knapsack solver and the brute-force oracle
+// (assigner/trace.hpp:71-74, assigner/solve.hpp:24-363), and the affine
+// cost-model fit (commsim/cost_model.hpp:78-109).
+//
+// Floating-point expressions are evaluated in the reference's order and the
+// TU is built with -ffp-contract=off, so plans, objectives and tie-breaks are
+// identical to the reference's solve_assignment.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <numeric>
+#include <optional>
+
+#include "host.hpp"
+#include "qgnn_b200.h"
+#include "status.hpp"
+
+namespace qgnn_b200 {
+
+namespace {
+constexpr int kBits[3] = {2, 4, 8};
+constexpr size_t kBruteLimit = 16;  // solve.hpp:20
+
+double variance_at(double beta, int bits) {  // solve.hpp:60-63
+  const double levels = static_cast<double>((1u << bits) - 1);
+  return beta / (levels * levels);
+}
+
+struct Eval {
+  double objective = 0, variance = 0, z = 0;
+};
+
+Eval evaluate(const SolveResult& plan, const Cost& cm, double lambda) {  // solve.hpp:68-81
+  Eval ev;
+  for (const PlanPairG& pp : plan.pairs) {
+    uint64_t pair_bits = 0;
+    for (const Group& g : pp.groups) {
+      ev.variance += variance_at(g.beta, g.bits);
+      pair_bits += g.dim_sum() * static_cast<uint64_t>(g.bits);
+    }
+    ev.z = std::max(ev.z, cm.seconds(pp.src, pp.dst, static_cast<double>(pair_bits)));
+  }
+  ev.objective = lambda * ev.variance + (1.0 - lambda) * ev.z;
+  return ev;
+}
+
+void validate(const SolveResult& plan, const Cost& cm, double lambda) {  // solve.hpp:85-101
+  QGNN_REQUIRE(lambda >= 0.0 && lambda <= 1.0, QGNN_EINVAL, "solve: lambda must be in [0, 1]");
+  QGNN_REQUIRE(!plan.pairs.empty(), QGNN_EINVAL, "solve: no device pairs");
+  for (const PlanPairG& pp : plan.pairs) {
+    QGNN_REQUIRE(pp.src < cm.n && pp.dst < cm.n, QGNN_EINVAL, "solve: pair outside cost model");
+    QGNN_REQUIRE(!pp.groups.empty(), QGNN_EINVAL, "solve: empty groups");
+    for (const Group& g : pp.groups) {
+      QGNN_REQUIRE(!g.ids.empty() && g.ids.size() == g.dims.size(), QGNN_EINVAL,
+                   "solve: malformed group");
+      QGNN_REQUIRE(g.dim_sum() != 0, QGNN_EINVAL, "solve: zero-dim group");
+      QGNN_REQUIRE(g.beta >= 0.0 && std::isfinite(g.beta), QGNN_EINVAL,
+                   "solve: beta must be finite and >= 0");
+    }
+  }
+}
+
+std::vector<int> flat_bits(const SolveResult& p) {
+  std::vector<int> b;
+  for (const auto& pp : p.pairs)
+    for (const auto& g : pp.groups) b.push_back(g.bits);
+  return b;
+}
+void set_bits(SolveResult& p, const std::vector<int>& b) {
+  size_t i = 0;
+  for (auto& pp : p.pairs)
+    for (auto& g : pp.groups) g.bits = b[i++];
+}
+// objective, then variance, then lexicographically larger bit vector (solve.hpp:116-121)
+bool better(const Eval& a, const std::vector<int>& ba, const Eval& b, const std::vector<int>& bb) {
+  if (a.objective != b.objective) return a.objective < b.objective;
+  if (a.variance != b.variance) return a.variance < b.variance;
+  return ba > bb;
+}
+
+// Per-pair knapsack over scaled bit totals (solve.hpp:125-194).  minvar is
+// stored flat, row j = groups j.. with capacity c.
+struct Table {
+  double theta = 0, gamma = 0;
+  uint64_t unit = 1, smax = 0;
+  size_t n = 0;
+  std::vector<uint64_t> w;  // [j*3 + bi]
+  std::vector<double> minvar;  // [(j) * (smax+1) + c], j in [0, n]
+  std::vector<char> reachable;
+  double mv(size_t j, uint64_t c) const { return minvar[j * (smax + 1) + c]; }
+  double time_at(uint64_t s) const { return theta * static_cast<double>(s * unit) + gamma; }
+  std::optional<uint64_t> cap_for(double z) const {
+    if (time_at(0) > z) return std::nullopt;
+    uint64_t lo = 0, hi = smax;
+    while (lo < hi) {
+      const uint64_t mid = lo + (hi - lo + 1) / 2;
+      if (time_at(mid) <= z)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    return lo;
+  }
+};
+
+Table build_table(const PlanPairG& pp, const Cost& cm) {
+  Table t;
+  t.theta = cm.theta[pp.src * cm.n + pp.dst];
+  t.gamma = cm.gamma[pp.src * cm.n + pp.dst];
+  uint64_t base = 0;
+  for (const Group& g : pp.groups) base = std::gcd(base, g.dim_sum());
+  t.unit = 2 * base;
+  t.n = pp.groups.size();
+  t.w.resize(t.n * 3);
+  for (size_t j = 0; j < t.n; ++j) {
+    for (int bi = 0; bi < 3; ++bi) t.w[j * 3 + bi] = pp.groups[j].dim_sum() * kBits[bi] / t.unit;
+    t.smax += t.w[j * 3 + 2];
+  }
+  QGNN_REQUIRE((t.n + 1) * (t.smax + 1) <= (uint64_t{1} << 31), QGNN_ERESOURCE,
+               "solve_assignment: knapsack table too large (raise group_size)");
+  const double inf = std::numeric_limits<double>::infinity();
+  const size_t W = t.smax + 1;
+  t.minvar.assign((t.n + 1) * W, inf);
+  std::fill(t.minvar.begin() + t.n * W, t.minvar.end(), 0.0);
+  for (size_t j = t.n; j-- > 0;) {
+    const double* below = &t.minvar[(j + 1) * W];
+    double* row = &t.minvar[j * W];
+    double var[3];
+    for (int bi = 0; bi < 3; ++bi) var[bi] = variance_at(pp.groups[j].beta, kBits[bi]);
+    for (uint64_t c = 0; c <= t.smax; ++c) {
+      double best = inf;
+      for (int bi = 2; bi >= 0; --bi) {  // prefer larger bits on ties
+        const uint64_t wt = t.w[j * 3 + bi];
+        if (wt > c) continue;
+        const double b = below[c - wt];
+        if (b == inf) continue;
+        const double v = var[bi] + b;
+        if (v < best) best = v;
+      }
+      row[c] = best;
+    }
+  }
+  t.reachable.assign(W, 0);
+  t.reachable[0] = 1;
+  std::vector<char> next(W);
+  for (size_t j = 0; j < t.n; ++j) {
+    std::fill(next.begin(), next.end(), 0);
+    for (uint64_t s = 0; s <= t.smax; ++s) {
+      if (!t.reachable[s]) continue;
+      for (int bi = 0; bi < 3; ++bi) next[s + t.w[j * 3 + bi]] = 1;
+    }
+    t.reachable.swap(next);
+  }
+  return t;
+}
+
+// greedy largest-bits walk consistent with the minima (solve.hpp:197-214)
+void reconstruct(const Table& t, const PlanPairG& pp, uint64_t cap, std::vector<int>& out) {
+  uint64_t c = cap;
+  const double inf = std::numeric_limits<double>::infinity();
+  for (size_t j = 0; j < pp.groups.size(); ++j) {
+    int pick = 0;
+    for (int bi = 2; bi >= 0; --bi) {
+      const uint64_t wt = t.w[j * 3 + bi];
+      if (wt > c) continue;
+      const double b = t.mv(j + 1, c - wt);
+      if (b == inf) continue;
+      if (variance_at(pp.groups[j].beta, kBits[bi]) + b == t.mv(j, c)) {
+        pick = kBits[bi];
+        c -= wt;
+        break;
+      }
+    }
+    out.push_back(pick);
+  }
+}
+}  // namespace
+
+uint64_t Group::dim_sum() const { return std::accumulate(dims.begin(), dims.end(), uint64_t{0}); }
+
+double compute_beta(const MsgStat& m) {  // trace.hpp:71-74
+  const double range = m.hi - m.lo;
+  return m.asq * static_cast<double>(m.dim) * range * range / 6.0;
+}
+
+SolveResult group_and_order(const std::vector<PairStat>& pairs, int64_t group_size) {
+  QGNN_REQUIRE(group_size > 0, QGNN_EINVAL, "group_and_order: group_size must be > 0");
+  for (const PairStat& p : pairs) {  // trace.hpp:58-67
+    QGNN_REQUIRE(p.src != p.dst, QGNN_EINVAL, "stats: src == dst");
+    for (const MsgStat& m : p.msgs) {
+      QGNN_REQUIRE(m.dim != 0, QGNN_EINVAL, "stats: zero dim");
+      QGNN_REQUIRE(!(m.hi < m.lo), QGNN_EINVAL, "stats: hi < lo");
+      QGNN_REQUIRE(m.asq > 0.0, QGNN_EINVAL, "stats: sum_alpha_sq must be > 0");
+    }
+  }
+  SolveResult plan;
+  for (const PairStat& p : pairs) {
+    if (p.msgs.empty()) continue;
+    std::vector<std::pair<double, const MsgStat*>> order;
+    order.reserve(p.msgs.size());
+    for (const MsgStat& m : p.msgs) order.emplace_back(compute_beta(m), &m);
+    std::stable_sort(order.begin(), order.end(), [](const auto& a, const auto& b) {
+      if (a.first != b.first) return a.first > b.first;
+      return a.second->id < b.second->id;
+    });
+    PlanPairG pp;
+    pp.src = p.src;
+    pp.dst = p.dst;
+    for (size_t i = 0; i < order.size(); i += static_cast<size_t>(group_size)) {
+      Group g;
+      for (size_t j = i; j < std::min(order.size(), i + static_cast<size_t>(group_size)); ++j) {
+        g.ids.push_back(order[j].second->id);
+        g.dims.push_back(order[j].second->dim);
+        g.beta += order[j].first;
+      }
+      pp.groups.push_back(std::move(g));
+    }
+    plan.pairs.push_back(std::move(pp));
+  }
+  return plan;
+}
+
+void solve_exact(SolveResult& plan, const Cost& cm, double lambda) {
+  validate(plan, cm, lambda);
+  std::vector<Table> tables;
+  tables.reserve(plan.pairs.size());
+  for (const PlanPairG& pp : plan.pairs) tables.push_back(build_table(pp, cm));
+  std::vector<double> cand;
+  for (const Table& t : tables)
+    for (uint64_t s = 0; s <= t.smax; ++s)
+      if (t.reachable[s]) cand.push_back(t.time_at(s));
+  std::sort(cand.begin(), cand.end());
+  cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+
+  // The pair assignment is a function of its cap only: memoize per pair.
+  std::vector<std::optional<uint64_t>> last_cap(tables.size());
+  std::vector<std::vector<int>> last_bits(tables.size());
+  std::vector<int> best_bits, bits;
+  Eval best;
+  bool have = false;
+  SolveResult work = plan;
+  const double inf = std::numeric_limits<double>::infinity();
+  for (double z : cand) {
+    bits.clear();
+    bool feasible = true;
+    for (size_t i = 0; i < tables.size(); ++i) {
+      const auto cap = tables[i].cap_for(z);
+      if (!cap || tables[i].mv(0, *cap) == inf) {
+        feasible = false;
+        break;
+      }
+      if (!last_cap[i] || *last_cap[i] != *cap) {
+        last_bits[i].clear();
+        reconstruct(tables[i], plan.pairs[i], *cap, last_bits[i]);
+        last_cap[i] = cap;
+      }
+      bits.insert(bits.end(), last_bits[i].begin(), last_bits[i].end());
+    }
+    if (!feasible) continue;
+    set_bits(work, bits);
+    const Eval ev = evaluate(work, cm, lambda);
+    if (!have || better(ev, bits, best, best_bits)) {
+      best = ev;
+      best_bits = bits;
+      have = true;
+    }
+  }
+  QGNN_REQUIRE(have, QGNN_EINVAL, "solve_assignment: no feasible assignment");
+  set_bits(plan, best_bits);
+  plan.objective = best.objective;
+  plan.variance = best.variance;
+  plan.z = best.z;
+}
+
+void solve_brute(SolveResult& plan, const Cost& cm, double lambda) {
+  validate(plan, cm, lambda);
+  size_t n = 0;
+  for (const auto& pp : plan.pairs) n += pp.groups.size();
+  QGNN_REQUIRE(n <= kBruteLimit, QGNN_ERESOURCE, "brute_force_assignment: too many groups");
+  std::vector<int> idx(n, 0), bits(n, 2), best_bits;
+  Eval best;
+  bool have = false;
+  SolveResult work = plan;
+  for (;;) {
+    set_bits(work, bits);
+    const Eval ev = evaluate(work, cm, lambda);
+    if (!have || better(ev, bits, best, best_bits)) {
+      best = ev;
+      best_bits = bits;
+      have = true;
+    }
+    size_t j = 0;
+    while (j < n) {
+      if (++idx[j] < 3) {
+        bits[j] = kBits[idx[j]];
+        break;
+      }
+      idx[j] = 0;
+      bits[j] = 2;
+      ++j;
+    }
+    if (j == n) break;
+  }
+  set_bits(plan, best_bits);
+  plan.objective = best.objective;
+  plan.variance = best.variance;
+  plan.z = best.z;
+}
+
+double uniform_expected_variance(const std::vector<PairStat>& pairs) {  // solve.hpp:313-326
+  double mean_inv = 0.0;
+  for (int b : kBits) {
+    const double levels = static_cast<double>((1u << b) - 1);
+    mean_inv += 1.0 / (levels * levels);
+  }
+  mean_inv /= 3.0;
+  double total = 0.0;
+  for (const auto& p : pairs)
+    for (const auto& m : p.msgs) total += compute_beta(m) * mean_inv;
+  return total;
+}
+
+}  // namespace qgnn_b200
+
+using namespace qgnn_b200;
+
+extern "C" {
+
+int qgnn_solve_instance(int64_t n_pairs, const uint32_t* pair_src, const uint32_t* pair_dst,
+                        const uint64_t* pair_count, const uint32_t* m_id, const uint64_t* m_dim,
+                        const double* m_lo, const double* m_hi, const double* m_asq,
+                        int64_t n_devices, const double* theta, const double* gamma,
+                        double lambda, int64_t group_size, int brute, int32_t* out_bits,
+                        double* eval) {
+  QGNN_API_BEGIN
+  std::vector<PairStat> pairs(n_pairs);
+  uint64_t o = 0;
+  for (int64_t p = 0; p < n_pairs; ++p) {
+    pairs[p].src = pair_src[p];
+    pairs[p].dst = pair_dst[p];
+    for (uint64_t i = 0; i < pair_count[p]; ++i, ++o)
+      pairs[p].msgs.push_back({m_id[o], m_dim[o], m_lo[o], m_hi[o], m_asq[o]});
+  }
+  Cost cm;
+  cm.n = n_devices;
+  cm.theta.assign(theta, theta + n_devices * n_devices);
+  cm.gamma.assign(gamma, gamma + n_devices * n_devices);
+  SolveResult plan = group_and_order(pairs, group_size);
+  if (brute)
+    solve_brute(plan, cm, lambda);
+  else
+    solve_exact(plan, cm, lambda);
+  eval[0] = plan.objective;
+  eval[1] = plan.variance;
+  eval[2] = plan.z;
+  // map back to input order
+  std::map<std::pair<uint32_t, uint32_t>, std::map<uint32_t, int>> bits;
+  for (const auto& pp : plan.pairs)
+    for (const auto& g : pp.groups)
+      for (uint32_t id : g.ids) bits[{pp.src, pp.dst}][id] = g.bits;
+  o = 0;
+  for (int64_t p = 0; p < n_pairs; ++p)
+    for (uint64_t i = 0; i < pair_count[p]; ++i, ++o)
+      out_bits[o] = bits[{pair_src[p], pair_dst[p]}][m_id[o]];
+  QGNN_API_END
+}
+
+// cost_model.hpp:78-109, one pair
+int qgnn_fit_affine(const double* x, const double* y, int64_t n, double* theta, double* gamma) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(n >= 2, QGNN_EINVAL, "fit_cost_model: need at least 2 samples per pair");
+  double mx = 0, my = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    mx += x[i];
+    my += y[i];
+  }
+  mx /= static_cast<double>(n);
+  my /= static_cast<double>(n);
+  double sxx = 0, sxy = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    sxx += (x[i] - mx) * (x[i] - mx);
+    sxy += (x[i] - mx) * (y[i] - my);
+  }
+  QGNN_REQUIRE(sxx != 0.0, QGNN_EINVAL, "fit_cost_model: need at least 2 distinct sizes per pair");
+  const double th = sxy / sxx;
+  const double ga = my - th * mx;
+  *theta = std::max(0.0, th);
+  *gamma = std::max(0.0, ga);
+  QGNN_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,214 @@
+"""Host mirror of the reference operator API over the C-ABI (torch tensors for device memory).
+
+Each function names the reference function it stands in for.  Arguments are
+CUDA tensors; the kernels run on the current torch stream and the context's
+device error word is checked before returning, so failures surface as the
+reference's exception types (``DecodeError``, ``InvalidArgument`` ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import F32, F64, WIRE_GPU, WIRE_REF, check, lib
+
+_CTX = {}
+
+
+def ctx(device: Optional[int] = None):
+    """Per-device qgnn_ctx (error word + scratch)."""
+    if device is None:
+        device = torch.cuda.current_device()
+    if device not in _CTX:
+        h = C.c_void_p()
+        check(lib.qgnn_ctx_create(device, C.byref(h)))
+        _CTX[device] = h
+    return _CTX[device]
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _dtype(t: torch.Tensor) -> int:
+    if t.dtype == torch.float64:
+        return F64
+    if t.dtype == torch.float32:
+        return F32
+    raise _lib.InvalidArgument(f"unsupported dtype {t.dtype}")
+
+
+def sync_check(device: Optional[int] = None) -> None:
+    check(lib.qgnn_ctx_check(ctx(device), _stream()))
+
+
+# ---- rng.hpp ------------------------------------------------------------------
+def rng_key(seed: int, *coords: int) -> int:
+    """Key of RngStream(seed).fork(c0).fork(c1)... (rng.hpp:15-28)."""
+    k = lib.qgnn_rng_seed_key(seed & (2**64 - 1))
+    for c in coords:
+        k = lib.qgnn_rng_fork(k, c & (2**64 - 1))
+    return k
+
+
+def chunk_wire_bytes(count: int, bits: int, layout: int = WIRE_GPU, dtype: int = F32) -> int:
+    return int(lib.qgnn_chunk_wire_bytes(count, bits, layout, dtype))
+
+
+def wire_layout(bits: np.ndarray, dim: int, layout: int = WIRE_GPU, dtype: int = F32):
+    """encode_message_set wire order (codec.hpp:56-69): (wire_pos, offsets, total)."""
+    bits = np.ascontiguousarray(bits, np.int32)
+    n = len(bits)
+    pos = np.zeros(max(1, n), np.int64)
+    off = np.zeros(max(1, n), np.uint64)
+    tot = C.c_uint64()
+    check(lib.qgnn_wire_layout(bits.ctypes.data, n, dim, layout, dtype, pos.ctypes.data,
+                               off.ctypes.data, C.byref(tot)))
+    return pos[:n], off[:n], tot.value
+
+
+# ---- codec.hpp / quant.hpp ----------------------------------------------------------
+def quantize_pack(values, rows, ids, bits, offsets, set_keys, out, layout=WIRE_GPU, set_of=None,
+                  win_lo=None, win_hi=None, check_errors=True):
+    """K1 over arbitrary (row, id, width, offset) message lists."""
+    dim = values.shape[1]
+    check(lib.qgnn_quantize_pack(ctx(), _ptr(values), _dtype(values), values.stride(0), dim,
+                                 rows.numel(), _ptr(rows), _ptr(ids), _ptr(bits), _ptr(offsets),
+                                 _ptr(set_of), _ptr(set_keys), layout, _ptr(out), _ptr(win_lo),
+                                 _ptr(win_hi), _stream()))
+    if check_errors:
+        sync_check()
+    return out
+
+
+def encode_message_set(values: torch.Tensor, rows, ids, bits, set_key: int,
+                       layout: int = WIRE_GPU):
+    """encode_message_set (codec.hpp:41-72) on the GPU.
+
+    ``rows``/``ids``/``bits`` are host arrays in caller order.  Returns the wire
+    bytes (CUDA uint8 tensor) and the retrieval index (wire order) as numpy
+    arrays: (pos -> caller index, bits, offset).
+    """
+    dev = values.device
+    ids_np = np.ascontiguousarray(ids, np.uint32)
+    if len(np.unique(ids_np)) != len(ids_np):
+        raise _lib.InvalidArgument("encode_message_set: duplicate message ids")
+    bits_np = np.ascontiguousarray(bits, np.int32)
+    pos, off, total = wire_layout(bits_np, values.shape[1], layout, _dtype(values))
+    out = torch.zeros(max(total, 16), dtype=torch.uint8, device=dev)
+    rows_t = torch.as_tensor(np.ascontiguousarray(rows, np.int32), device=dev)
+    ids_t = torch.as_tensor(ids_np.view(np.int32), device=dev)
+    bits_t = torch.as_tensor(bits_np.astype(np.uint8), device=dev)
+    off_t = torch.as_tensor(off.view(np.int64), device=dev)
+    keys = torch.as_tensor(np.array([set_key], np.uint64).view(np.int64), device=dev)
+    quantize_pack(values, rows_t, ids_t, bits_t, off_t, keys, out, layout=layout)
+    return out[:total], dict(pos=pos, bits=bits_np[pos], off=off[pos], total=total)
+
+
+def dequant_scatter(wire, bits, offsets, dim, out, dst_rows=None, accumulate=False,
+                    layout=WIRE_GPU, check_errors=True):
+    """K3: decode_message_set (codec.hpp:80-96) fused with the halo scatter."""
+    n = bits.numel()
+    check(lib.qgnn_dequant_scatter(ctx(), _ptr(wire), n, dim, _ptr(bits), _ptr(offsets), layout,
+                                   _ptr(dst_rows), int(accumulate), _ptr(out), _dtype(out),
+                                   out.stride(0), _stream()))
+    if check_errors:
+        sync_check()
+    return out
+
+
+def decode_message_set(wire: torch.Tensor, bits, offsets, dim: int, dtype=torch.float32,
+                       layout: int = WIRE_GPU):
+    """decode_message_set: rows in index (wire) order."""
+    dev = wire.device
+    n = len(bits)
+    out = torch.zeros((max(1, n), dim), dtype=dtype, device=dev)
+    bits_t = torch.as_tensor(np.ascontiguousarray(bits, np.uint8), device=dev)
+    off_t = torch.as_tensor(np.ascontiguousarray(offsets, np.uint64).view(np.int64), device=dev)
+    dequant_scatter(wire, bits_t, off_t, dim, out, layout=layout)
+    return out[:n]
+
+
+# ---- aggregate.hpp ---------------------------------------------------------------
+def csr_aggregate(x, ptr_a, col_a, alpha_a, out, self_alpha=None, y=None, ptr_b=None, col_b=None,
+                  alpha_b=None, rows=None, row_begin=0, n_rows=None):
+    """K4 (see qgnn_csr_aggregate)."""
+    dim = x.shape[1]
+    if n_rows is None:
+        n_rows = rows.numel() if rows is not None else out.shape[0] - row_begin
+    check(lib.qgnn_csr_aggregate(ctx(), _dtype(x), dim, _ptr(x), x.stride(0), _ptr(y),
+                                 y.stride(0) if y is not None else 0, _ptr(self_alpha),
+                                 _ptr(ptr_a), _ptr(col_a), _ptr(alpha_a), _ptr(ptr_b),
+                                 _ptr(col_b), _ptr(alpha_b), _ptr(rows), row_begin, n_rows,
+                                 _ptr(out), out.stride(0), _stream()))
+    return out
+
+
+# ---- model.hpp / matrix.hpp ---------------------------------------------------------
+def dense_forward(a, w, out, relu=True, rows=None, row_begin=0, n_rows=None):
+    if n_rows is None:
+        n_rows = rows.numel() if rows is not None else a.shape[0] - row_begin
+    check(lib.qgnn_dense_forward(ctx(), _dtype(a), _ptr(a), a.stride(0), _ptr(w), w.shape[0],
+                                 w.shape[1], _ptr(rows), row_begin, n_rows, int(relu), _ptr(out),
+                                 out.stride(0), _stream()))
+    return out
+
+
+def dense_input_grad(dz, w, out, rows=None, row_begin=0, n_rows=None):
+    if n_rows is None:
+        n_rows = rows.numel() if rows is not None else dz.shape[0] - row_begin
+    check(lib.qgnn_dense_input_grad(ctx(), _dtype(dz), _ptr(dz), dz.stride(0), _ptr(w),
+                                    w.shape[0], w.shape[1], _ptr(rows), row_begin, n_rows,
+                                    _ptr(out), out.stride(0), _stream()))
+    return out
+
+
+def dense_weight_grad(a, b, out, rows=None, row_begin=0, n_rows=None, accumulate=False):
+    if n_rows is None:
+        n_rows = rows.numel() if rows is not None else a.shape[0] - row_begin
+    check(lib.qgnn_dense_weight_grad(ctx(), _dtype(a), _ptr(a), a.stride(0), _ptr(b),
+                                     b.stride(0), a.shape[1], b.shape[1], _ptr(rows), row_begin,
+                                     n_rows, int(accumulate), _ptr(out), _stream()))
+    return out
+
+
+def relu_backward(act, dh, dz, row_begin=0, n_rows=None):
+    if n_rows is None:
+        n_rows = act.shape[0] - row_begin
+    check(lib.qgnn_relu_backward(ctx(), _dtype(act), _ptr(act), act.stride(0), _ptr(dh),
+                                 dh.stride(0), act.shape[1], row_begin, n_rows, _ptr(dz),
+                                 dz.stride(0), _stream()))
+    return dz
+
+
+def masked_ce(logits, labels, rows, inv_denom, grad):
+    acc = torch.zeros(1, dtype=torch.float64, device=logits.device)
+    check(lib.qgnn_masked_ce(ctx(), _dtype(logits), _ptr(logits), logits.stride(0),
+                             logits.shape[1], _ptr(labels), _ptr(rows), rows.numel(), inv_denom,
+                             _ptr(grad), grad.stride(0), _ptr(acc), _stream()))
+    sync_check()
+    return float(acc.item())
+
+
+def count_correct(logits, labels, rows):
+    acc = torch.zeros(1, dtype=torch.int64, device=logits.device)
+    check(lib.qgnn_count_correct(ctx(), _dtype(logits), _ptr(logits), logits.stride(0),
+                                 logits.shape[1], _ptr(labels), _ptr(rows), rows.numel(),
+                                 _ptr(acc), _stream()))
+    return int(acc.item())
+
+
+def adam_step(p, m, v, g, t, lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8):
+    bc1 = 1.0 - beta1 ** t
+    bc2 = 1.0 - beta2 ** t
+    check(lib.qgnn_adam_step(ctx(), _dtype(p), _ptr(p), _ptr(m), _ptr(v), _ptr(g), p.numel(), lr,
+                             beta1, beta2, eps, bc1, bc2, _stream()))
+    return p

@@ -1,0 +1,204 @@
+"""CPU tests of the C-ABI library: it loads, exports every declared symbol, and
+its host-side logic (RNG, wire layout, partitioning, coefficients, solver,
+cost fit) matches the oracle / reference.  No kernels are launched here."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import port, ref_available
+from paper_2306_01381_b200 import _lib
+from paper_2306_01381_b200._lib import check, lib
+
+GOLDEN = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
+
+
+def _declared_symbols():
+    text = open(_lib.HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(qgnn_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    syms = _declared_symbols()
+    assert len(syms) > 30
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.HEADER_SYMBOLS)
+
+
+def test_compute_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    h = C.c_void_p()
+    st = lib.qgnn_ctx_create(0, C.byref(h))
+    assert st == _lib.ECUDA
+    assert b"no CUDA device" in lib.qgnn_last_error()
+
+
+def test_rng_matches_oracle():
+    rs = np.random.default_rng(1)
+    for _ in range(50):
+        seed = int(rs.integers(0, 2**63))
+        coords = [int(x) for x in rs.integers(0, 2**63, 4)]
+        k = lib.qgnn_rng_seed_key(seed)
+        for c in coords:
+            k = lib.qgnn_rng_fork(k, c)
+        assert k == port.stream(seed, *coords)
+        for ctr in (1, 2, 1000):
+            assert lib.qgnn_rng_u64(k, ctr) == port.draw_u64(k, ctr)
+
+
+def test_chunk_sizes_ref_and_gpu_layout():
+    assert lib.qgnn_chunk_wire_bytes(10, 8, _lib.WIRE_REF, 1) == 35
+    assert lib.qgnn_chunk_wire_bytes(64, 2, _lib.WIRE_REF, 1) == 41
+    assert lib.qgnn_chunk_wire_bytes(5, 4, _lib.WIRE_REF, 1) == 28
+    assert lib.qgnn_chunk_wire_bytes(256, 8, _lib.WIRE_GPU, 0) == 16 + 256
+    assert lib.qgnn_chunk_wire_bytes(100, 2, _lib.WIRE_GPU, 0) == 16 + 32
+    assert lib.qgnn_chunk_wire_bytes(100, 0, _lib.WIRE_GPU, 0) == 400
+    assert lib.qgnn_chunk_wire_bytes(100, 0, _lib.WIRE_REF, 1) == 800
+
+
+def test_wire_layout_matches_encode_order():  # codec.hpp:56-69, test_quantcodec.cpp:293-315
+    from paper_2306_01381_b200.ops import wire_layout
+    pos, off, total = wire_layout(np.array([8, 2, 4, 2]), 5, _lib.WIRE_REF, 1)
+    assert pos.tolist() == [1, 3, 2, 0]
+    G = GOLDEN
+    pos, off, total = wire_layout(G["enc_bits"], 96, _lib.WIRE_REF, 1)
+    assert (G["enc_ids"][pos] == G["enc_idx_id"]).all()
+    assert (off[pos] == G["enc_idx_off"]).all()
+    assert total == len(G["enc_wire"])
+    with pytest.raises(_lib.InvalidArgument):
+        wire_layout(np.array([8, 3]), 5)
+
+
+def test_partition_graph_matches_reference():
+    G = GOLDEN
+    ptr, adj = G["g_adj_ptr"], G["g_adj"]
+    owner = np.zeros(len(ptr) - 1, np.uint32)
+    check(lib.qgnn_partition_graph(ptr.ctypes.data, adj.ctypes.data, len(owner), 4, 11,
+                                   owner.ctypes.data))
+    assert (owner == G["g_owner_p4_s11"]).all()
+
+
+@pytest.mark.skipif(not ref_available(), reason="compiled reference not present")
+def test_partition_graph_matches_reference_cite():
+    from oracle import ref
+    g = ref.generate_dataset("cite", nodes=3000, classes=8, feature_dim=4, attach_edges=6, seed=3)
+    for parts, seed in ((2, 7), (3, 1), (8, 99)):
+        owner = np.zeros(3000, np.uint32)
+        check(lib.qgnn_partition_graph(g["adj_ptr"].ctypes.data, g["adj"].ctypes.data, 3000,
+                                       parts, seed, owner.ctypes.data))
+        assert (owner == ref.partition_owner(g["adj_ptr"], g["adj"], parts, seed)).all()
+
+
+def test_compute_coeffs_matches_reference():
+    G = GOLDEN
+    ptr, adj = G["g_adj_ptr"], G["g_adj"]
+    n = len(ptr) - 1
+    for sage, key in ((0, "g_alpha_gcn"), (1, "g_alpha_sage")):
+        a = np.zeros(len(adj))
+        sa = np.zeros(n)
+        check(lib.qgnn_compute_coeffs(ptr.ctypes.data, adj.ctypes.data, n, sage, a.ctypes.data,
+                                      sa.ctypes.data))
+        assert (a == G[key]).all() and (sa == G["g_self_alpha"]).all()
+
+
+def _solve(pairs, n_dev, theta, gamma, lam, gs, brute=False):
+    src = np.array([p[0] for p in pairs], np.uint32)
+    dst = np.array([p[1] for p in pairs], np.uint32)
+    cnt = np.array([len(p[2]) for p in pairs], np.uint64)
+    msgs = [m for p in pairs for m in p[2]]
+    mid = np.array([m[0] for m in msgs], np.uint32)
+    mdim = np.array([m[1] for m in msgs], np.uint64)
+    mlo = np.array([m[2] for m in msgs])
+    mhi = np.array([m[3] for m in msgs])
+    masq = np.array([m[4] for m in msgs])
+    th = np.ascontiguousarray(theta, np.float64)
+    ga = np.ascontiguousarray(gamma, np.float64)
+    bits = np.zeros(len(msgs), np.int32)
+    ev = np.zeros(3)
+    check(lib.qgnn_solve_instance(len(pairs), src.ctypes.data, dst.ctypes.data, cnt.ctypes.data,
+                                  mid.ctypes.data, mdim.ctypes.data, mlo.ctypes.data,
+                                  mhi.ctypes.data, masq.ctypes.data, n_dev, th.ctypes.data,
+                                  ga.ctypes.data, lam, gs, int(brute), bits.ctypes.data,
+                                  ev.ctypes.data))
+    return bits, ev
+
+
+def _random_instance(rs, n_dev, n_msgs, dims=(4, 8, 16)):
+    pairs = []
+    for s in range(n_dev):
+        for d in range(n_dev):
+            if s == d or rs.random() < 0.3:
+                continue
+            ids = np.sort(rs.choice(1000, int(rs.integers(1, n_msgs + 1)), replace=False))
+            msgs = []
+            for i in ids:
+                lo = float(rs.normal())
+                msgs.append((int(i), int(rs.choice(dims)), lo, lo + float(rs.exponential()),
+                             float(rs.uniform(0.1, 2.0))))
+            pairs.append((s, d, msgs))
+    return pairs
+
+
+@pytest.mark.skipif(not ref_available(), reason="compiled reference not present")
+def test_solver_matches_reference_and_brute_force():  # test_assigner.cpp:228-245
+    from oracle import ref
+    rs = np.random.default_rng(2024)
+    n_checked = 0
+    for trial in range(60):
+        n_dev = int(rs.integers(2, 4))
+        pairs = _random_instance(rs, n_dev, 6)
+        if not pairs:
+            continue
+        theta = rs.uniform(1e-4, 1e-2, n_dev * n_dev)
+        gamma = rs.uniform(0, 1e-2, n_dev * n_dev)
+        lam = float(rs.choice([0.0, 0.3, 0.5, 0.9, 1.0]))
+        gs = int(rs.integers(1, 4))
+        bits, ev = _solve(pairs, n_dev, theta, gamma, lam, gs)
+        rbits, rev = ref.solve_instance(pairs, n_dev, theta, gamma, lam, gs)
+        assert (bits == rbits).all() and (ev == rev).all(), trial
+        n_groups = sum(-(-len(p[2]) // gs) for p in pairs)
+        if n_groups <= 10:
+            bb, bev = _solve(pairs, n_dev, theta, gamma, lam, gs, brute=True)
+            rb, rbev = ref.solve_instance(pairs, n_dev, theta, gamma, lam, gs, brute=True)
+            assert (bb == rb).all() and (bev == rbev).all()
+            assert bev[0] == ev[0]  # exact solver reaches the exhaustive optimum
+            n_checked += 1
+    assert n_checked > 10
+
+
+def test_solver_rejects_bad_instances():  # test_assigner.cpp:265-297
+    pairs = [(0, 1, [(1, 4, 0.0, 1.0, 1.0)])]
+    with pytest.raises(_lib.InvalidArgument):
+        _solve(pairs, 2, [0] * 4, [0] * 4, 1.5, 1)
+    with pytest.raises(_lib.InvalidArgument):
+        _solve(pairs, 2, [0] * 4, [0] * 4, 0.5, 0)
+    big = [(0, 1, [(i, 4, 0.0, 1.0, 1.0) for i in range(20)])]
+    with pytest.raises(_lib.ResourceLimitError):
+        _solve(big, 2, [1e-3] * 4, [0] * 4, 0.5, 1, brute=True)
+
+
+def test_pure_variance_weighting_is_all_eight():  # test_assigner.cpp:192-205
+    rs = np.random.default_rng(3)
+    pairs = _random_instance(rs, 3, 5)
+    bits, _ = _solve(pairs, 3, [1e-3] * 9, [1e-3] * 9, 1.0, 2)
+    assert (bits == 8).all()
+
+
+def test_fit_affine():  # cost_model.hpp:78-109, test_commsim.cpp:65-99
+    th, ga = C.c_double(), C.c_double()
+    x = np.array([1e6, 2e6])
+    y = np.array([1e-3 + 1e6 * 2e-9, 1e-3 + 2e6 * 2e-9])
+    check(lib.qgnn_fit_affine(x.ctypes.data, y.ctypes.data, 2, C.byref(th), C.byref(ga)))
+    assert abs(th.value - 2e-9) < 1e-18 and abs(ga.value - 1e-3) < 1e-12
+    y2 = np.array([5.0, 1.0])  # negative slope clamps to zero
+    check(lib.qgnn_fit_affine(x.ctypes.data, y2.ctypes.data, 2, C.byref(th), C.byref(ga)))
+    assert th.value == 0.0
+    with pytest.raises(_lib.InvalidArgument):
+        x1 = np.array([1.0, 1.0])
+        check(lib.qgnn_fit_affine(x1.ctypes.data, y.ctypes.data, 2, C.byref(th), C.byref(ga)))

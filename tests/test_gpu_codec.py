@@ -1,0 +1,178 @@
+"""K1/K3 parity: GPU quantize+pack and unpack+dequantize vs the oracle and the
+reference's golden vectors.  Integer/byte outputs must be bit-exact."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import port
+from paper_2306_01381_b200 import DecodeError, InvalidArgument, WIRE_GPU, WIRE_REF, ops
+
+pytestmark = pytest.mark.gpu
+GOLDEN = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
+DIMS = [100, 128, 200, 256, 300, 602]
+
+
+def _gpu_quantize_one(h, b, key, layout, dtype=torch.float64):
+    v = torch.as_tensor(np.asarray(h)[None, :], dtype=dtype, device="cuda")
+    wire, idx = ops.encode_message_set(v, [0], [0], [b], ops.lib.qgnn_rng_fork(key, 0) if False
+                                       else key, layout=layout)
+    return wire.cpu().numpy(), idx
+
+
+def test_encode_golden_byte_identical(cuda):
+    G = GOLDEN
+    c = [int(x) for x in G["enc_coords"]]
+    key = port.stream(c[0], *c[1:])
+    vals = torch.as_tensor(G["enc_vals"], device=cuda)
+    wire, idx = ops.encode_message_set(vals, G["enc_rows"], G["enc_ids"], G["enc_bits"], key,
+                                       layout=WIRE_REF)
+    assert wire.cpu().numpy().tobytes() == G["enc_wire"].tobytes()
+    assert (G["enc_ids"][idx["pos"]] == G["enc_idx_id"]).all()
+    dec = ops.decode_message_set(wire, idx["bits"], idx["off"], 96, dtype=torch.float64,
+                                 layout=WIRE_REF)
+    assert (dec.cpu().numpy() == G["enc_decoded"]).all()
+
+
+def test_quantize_golden_vectors(cuda):
+    """Every reference golden row (dims 1..602, b 2/4/8, gauss/relu/const)."""
+    for i in range(int(GOLDEN["n_quant"])):
+        meta = GOLDEN[f"q{i}_meta"].astype(np.uint64)
+        b, seed, coords = int(meta[0]), int(meta[1]), [int(x) for x in meta[2:]]
+        h = GOLDEN[f"q{i}_h"]
+        # message key = fork(set_key, id): use set = stream(seed, coords[:-1]), id = coords[-1]
+        set_key = port.stream(seed, *coords[:-1])
+        v = torch.as_tensor(h[None, :], device=cuda)
+        wire, idx = ops.encode_message_set(v, [0], [coords[-1]], [b], set_key, layout=WIRE_REF)
+        w = wire.cpu().numpy()
+        assert w[0] == b
+        s = w[9:17].view(np.float64)[0]
+        z = w[17:25].view(np.float64)[0]
+        es, ez = GOLDEN[f"q{i}_sz"]
+        assert s == es and z == ez, i
+        assert (w[25:] == GOLDEN[f"q{i}_payload"]).all(), i
+
+
+def _random_rows(rs, n, d, kind):
+    x = rs.standard_normal((n, d)) * rs.uniform(0.05, 5.0, (n, 1))
+    if kind == "relu":
+        x = np.maximum(x, 0.0)
+        x[:: 17] = 0.0  # all-zero rows -> S = 0 path
+    elif kind == "const":
+        x[:] = rs.standard_normal((n, 1))
+    return x
+
+
+@pytest.mark.parametrize("d", DIMS)
+def test_random_sets_f64_reference_layout_bit_exact(cuda, d):
+    rs = np.random.default_rng(d)
+    for kind in ("gauss", "relu", "const"):
+        n = 257
+        x = _random_rows(rs, n, d, kind)
+        rows = rs.permutation(n)[:200]
+        ids = (rs.permutation(100000)[:200] * 3 + 1).astype(np.uint32)
+        bits = rs.choice([2, 4, 8], 200).astype(np.int32)
+        key = port.stream(7, 2, 3, 1, 0, 2)
+        exp_wire, pos, off = port.encode_message_set(x, rows, ids, bits, key)
+        wire, idx = ops.encode_message_set(torch.as_tensor(x, device=cuda), rows, ids, bits, key,
+                                           layout=WIRE_REF)
+        assert wire.cpu().numpy().tobytes() == exp_wire.tobytes()
+        dec = ops.decode_message_set(wire, idx["bits"], idx["off"], d, dtype=torch.float64,
+                                     layout=WIRE_REF)
+        exp = port.decode_message_set(exp_wire, bits[pos], np.full(200, d, np.uint64), off,
+                                      len(exp_wire))
+        assert (dec.cpu().numpy() == exp).all()
+
+
+@pytest.mark.parametrize("d", DIMS)
+def test_random_sets_f32_gpu_layout(cuda, d):
+    """fp32 buffers: codes bit-exact with the oracle fed the same fp32 values as
+    doubles; headers are (float)S, (float)Z; dequant within fp32 rounding."""
+    rs = np.random.default_rng(1000 + d)
+    for kind in ("gauss", "relu"):
+        n = 300
+        x32 = _random_rows(rs, n, d, kind).astype(np.float32)
+        x = x32.astype(np.float64)
+        rows = np.arange(n)
+        ids = np.arange(n, dtype=np.uint32) * 5
+        bits = rs.choice([2, 4, 8], n).astype(np.int32)
+        key = port.stream(3, 2, 1, 0, 0, 1)
+        wire, idx = ops.encode_message_set(torch.as_tensor(x32, device=cuda), rows, ids, bits,
+                                           key, layout=WIRE_GPU)
+        w = wire.cpu().numpy()
+        for k in range(n):
+            i = idx["pos"][k]
+            o = int(idx["off"][k])
+            b = int(bits[i])
+            s, z, p = port.quantize(x[rows[i]], b, port.fork(key, int(ids[i])))
+            hdr = w[o:o + 16]
+            assert hdr[:4].view(np.float32)[0] == np.float32(s)
+            assert hdr[4:8].view(np.float32)[0] == np.float32(z)
+            assert hdr[8:12].view(np.uint32)[0] == d and hdr[12] == b
+            nb = len(p)
+            assert (w[o + 16:o + 16 + nb] == p).all(), (k, b)
+            assert (w[o + 16 + nb:o + 16 + ((nb + 15) // 16) * 16] == 0).all()
+        dec = ops.decode_message_set(wire, idx["bits"], idx["off"], d, dtype=torch.float32)
+        got = dec.cpu().numpy().astype(np.float64)
+        for k in range(0, n, 7):
+            i = idx["pos"][k]
+            b = int(bits[i])
+            s, z, p = port.quantize(x[rows[i]], b, port.fork(key, int(ids[i])))
+            exp = port.dequantize(p, b, d, s, z)
+            assert np.allclose(got[k], exp, rtol=2e-6, atol=2e-6 * (abs(s) * 255 + abs(z)))
+
+
+def test_scatter_and_accumulate(cuda):
+    rs = np.random.default_rng(4)
+    d, n = 64, 100
+    x = rs.standard_normal((n, d)).astype(np.float32)
+    bits = np.full(n, 8, np.int32)
+    wire, idx = ops.encode_message_set(torch.as_tensor(x, device=cuda), np.arange(n),
+                                       np.arange(n), bits, 123)
+    out = torch.ones((2 * n, d), dtype=torch.float32, device=cuda)
+    dst = torch.as_tensor((np.arange(n) * 2 + 1).astype(np.int32), device=cuda)
+    b_t = torch.as_tensor(idx["bits"].astype(np.uint8), device=cuda)
+    o_t = torch.as_tensor(idx["off"].view(np.int64), device=cuda)
+    ops.dequant_scatter(wire, b_t, o_t, d, out, dst_rows=dst, accumulate=True)
+    o = out.cpu().numpy()
+    assert (o[0::2] == 1).all()
+    dec = ops.decode_message_set(wire, idx["bits"], idx["off"], d).cpu().numpy()
+    assert np.allclose(o[1::2], dec + 1, atol=1e-6)
+    step = (x.max(1) - x.min(1)) / 255
+    assert (np.abs(dec - x) <= step[:, None] * 1.0001 + 1e-6).all()  # within one step
+
+
+def test_nonfinite_input_raises_invalid_argument(cuda):
+    x = torch.zeros((2, 16), dtype=torch.float32, device=cuda)
+    x[1, 3] = float("nan")
+    with pytest.raises(InvalidArgument):
+        ops.encode_message_set(x, [0, 1], [0, 1], [4, 4], 5)
+    ops.encode_message_set(x, [0], [0], [4], 5)  # error word was cleared
+
+
+def test_corrupt_chunk_raises_decode_error(cuda):
+    x = torch.randn((3, 16), device=cuda)
+    wire, idx = ops.encode_message_set(x, [0, 1, 2], [0, 1, 2], [4, 4, 8], 5)
+    with pytest.raises(DecodeError):
+        ops.decode_message_set(wire, np.array([4, 8, 8]), idx["off"], 16)
+    bad = wire.clone()
+    bad[int(idx["off"][0]) + 8] = 15  # count field
+    with pytest.raises(DecodeError):
+        ops.decode_message_set(bad, idx["bits"], idx["off"], 16)
+
+
+def test_unbiased_at_scale(cuda):
+    """Size-independent property at a large size: E[dequant] = x within 4 SE."""
+    rs = np.random.default_rng(8)
+    d, n = 256, 20000
+    base = rs.standard_normal(d).astype(np.float32)
+    x = np.tile(base, (n, 1))
+    for b in (2, 8):
+        wire, idx = ops.encode_message_set(torch.as_tensor(x, device=cuda), np.arange(n),
+                                           np.arange(n), np.full(n, b), 77)
+        dec = ops.decode_message_set(wire, idx["bits"], idx["off"], d).cpu().numpy()
+        s = (base.max() - base.min()) / ((1 << b) - 1)
+        mean = dec.mean(0)
+        se = s / 2 / np.sqrt(n)
+        assert (np.abs(mean - base) < 4 * se + 1e-6).mean() > 0.99
