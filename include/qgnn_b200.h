@@ -189,6 +189,7 @@ typedef struct {
   int32_t rank, world;     /* process rank / count; parts are split contiguously */
   int32_t device;          /* CUDA device of this rank */
   int32_t overlap;         /* 1: central compute on its own stream during the exchange */
+  int32_t kstats;          /* 1: time every kernel class with CUDA events (bench roofline) */
 } qgnn_settings;
 
 typedef struct {
@@ -221,7 +222,15 @@ int qgnn_engine_get_weights(qgnn_engine* e, int layer, void* out);
 int qgnn_engine_set_weights(qgnn_engine* e, int layer, const void* in);
 /* Static facts: [num_messages_per_tensor, n_parts, parts_on_rank, max_owned, max_halo]. */
 int qgnn_engine_info(qgnn_engine* e, int64_t* out5);
-/* Average device time (ms) of the named kernel class over the last epoch. */
+/* Per kernel class k (QGNN_K_*), accumulated since the last call (needs
+ * settings.kstats): out[3k] = total device ms, out[3k+1] = launches,
+ * out[3k+2] = algorithmic bytes (SURVEY.md §8d model).  Returns the number
+ * of classes written (<= n). */
+enum {
+  QGNN_K_QUANT = 0, QGNN_K_DEQUANT, QGNN_K_SPMM_FWD, QGNN_K_SPMM_BWD, QGNN_K_PARTIALS,
+  QGNN_K_GEMM_FWD, QGNN_K_GEMM_DGRAD, QGNN_K_GEMM_WGRAD, QGNN_K_ELEMWISE, QGNN_K_EXCHANGE,
+  QGNN_K_COUNT
+};
 int qgnn_engine_kernel_stats(qgnn_engine* e, double* out, int n);
 
 /* NCCL bootstrap for world > 1: rank 0 creates the id, every rank passes it to

@@ -67,7 +67,7 @@ class Settings(C.Structure):
                 ("n_parts", C.c_int64), ("lr", C.c_double), ("theta", C.c_double),
                 ("gamma", C.c_double), ("dtype", C.c_int32), ("layout", C.c_int32),
                 ("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32),
-                ("overlap", C.c_int32)]
+                ("overlap", C.c_int32), ("kstats", C.c_int32)]
 
 
 class EpochMetrics(C.Structure):

@@ -1,15 +1,1353 @@
-// engine.cu — placeholder; replaced by the GPU engine.
+// engine.cu — the GPU engine: the reference's per-epoch phase schedule
+// (trainer/engine.hpp:384-426) over partitions resident in HBM.
+//
+// One process per GPU hosts a contiguous range of the P graph partitions
+// ("devices" in the reference).  Per layer and direction the boundary path is
+//   K1 quantize+pack (all destinations of a partition in one launch)
+//   -> exchange: partitions on the same GPU are zero-copy (the receiver's
+//      decode reads the sender's send region in place); partitions on other
+//      GPUs move through grouped ncclSend/ncclRecv on a dedicated stream
+//   || central-row SpMM + GEMM on the compute stream (overlaps the exchange)
+//   -> K3 dequant+scatter into the halo (fwd) / accumulate into dh (bwd)
+//   -> marginal-row SpMM + GEMM.
+// Central rows are laid out first in every partition, so the central and
+// marginal subsets are contiguous row ranges for SpMM/GEMM.  Per-message
+// metadata (source row, id, bit width, wire offset) is built on the host per
+// plan version and uploaded once; RNG stream keys are uploaded per epoch.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <future>
+#include <memory>
+#include <numeric>
+#include <vector>
+
 #include "common.cuh"
-extern "C" {
-int qgnn_engine_create(const qgnn_settings*, int64_t, const int64_t*, const int32_t*, const void*,
-                       const int32_t*, const uint8_t*, const uint8_t*, const uint8_t*,
-                       const uint32_t*, const void*, qgnn_engine**) { return QGNN_EINVAL; }
-int qgnn_engine_destroy(qgnn_engine*) { return QGNN_OK; }
-int qgnn_engine_run_epoch(qgnn_engine*, qgnn_epoch_metrics*) { return QGNN_EINVAL; }
-int qgnn_engine_set_features(qgnn_engine*, const void*) { return QGNN_EINVAL; }
-int qgnn_engine_get_weights(qgnn_engine*, int, void*) { return QGNN_EINVAL; }
-int qgnn_engine_set_weights(qgnn_engine*, int, const void*) { return QGNN_EINVAL; }
-int qgnn_engine_info(qgnn_engine*, int64_t*) { return QGNN_EINVAL; }
-int qgnn_engine_kernel_stats(qgnn_engine*, double*, int) { return QGNN_EINVAL; }
-int qgnn_nccl_unique_id(void*) { return QGNN_ENCCL; }
+#include "host.hpp"
+#include "rng.cuh"
+
+namespace qgnn_b200 {
+
+// ------------------------------------------------------------------ NCCL ---
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  if (api.h) return api;
+  // prefer the NCCL already loaded into the process (torch's), else the system one
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  QGNN_REQUIRE(h, QGNN_ENCCL, "cannot load libnccl.so.2");
+  auto sym = [&](const char* n) {
+    void* p = dlsym(h, n);
+    QGNN_REQUIRE(p, QGNN_ENCCL, std::string("NCCL symbol missing: ") + n);
+    return p;
+  };
+  api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+  api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+  api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+  api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+  api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+  api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+  api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+  api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+  api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+  api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  api.h = h;
+  return api;
 }
+
+#define QGNN_NCCL(call)                                                                  \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess)                                                               \
+      throw ::qgnn_b200::Status(QGNN_ENCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
+  } while (0)
+
+// ---------------------------------------------------------- device buffer ---
+template <typename X>
+struct DBuf {
+  X* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    return *this;
+  }
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t count, bool zero = true) {
+    if (count <= n && p) {
+      if (zero) QGNN_CUDA(cudaMemset(p, 0, count * sizeof(X)));
+      QGNN_CUDA(cudaDeviceSynchronize());
+      return;
+    }
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = count;
+    QGNN_CUDA(cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(X)));
+    if (zero) QGNN_CUDA(cudaMemset(p, 0, std::max<size_t>(1, count) * sizeof(X)));
+    // legacy-stream memsets/copies do not order against our non-blocking streams
+    QGNN_CUDA(cudaDeviceSynchronize());
+  }
+  void upload(const std::vector<X>& v) {
+    alloc(v.size(), false);
+    if (!v.empty()) QGNN_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(X), cudaMemcpyHostToDevice));
+    QGNN_CUDA(cudaDeviceSynchronize());
+  }
+};
+
+// ------------------------------------------------------ small kernels ----
+template <typename T>
+__global__ void k_sum_parts(const T* __restrict__ all, int parts, int64_t n, T* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  T s = T(0);
+  for (int p = 0; p < parts; ++p) {  // ascending device order, engine.hpp:786-788
+    if constexpr (sizeof(T) == 8)
+      s = __dadd_rn(s, all[static_cast<int64_t>(p) * n + i]);
+    else
+      s += all[static_cast<int64_t>(p) * n + i];
+  }
+  out[i] = s;
+}
+
+template <typename T>
+__global__ void k_fill2(T* __restrict__ a, T va, T* __restrict__ b, T vb, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) {
+    a[i] = va;
+    b[i] = vb;
+  }
+}
+
+// ------------------------------------------------------------ engine ----
+enum BitMode { kFp = 0, kFixed = 1, kUniform = 2, kAdaptive = 3 };
+constexpr int kChoices[3] = {2, 4, 8};
+
+struct KeyInfo {
+  int t;
+  bool bwd;
+  int64_t dim;
+  uint64_t code;  // engine.hpp:455-457
+};
+
+// Messages of one ordered pair for one key (codec wire order within the set).
+struct PairMsgs {
+  std::vector<uint32_t> ids;  // caller order (ascending id)
+  std::vector<uint8_t> bits;
+  std::vector<uint64_t> off;  // byte offset inside the set
+  uint64_t bytes = 0, ref_bytes = 0;
+};
+
+struct KStat {
+  double ms = 0;
+  double launches = 0;
+  double bytes = 0;
+};
+
+class EngineBase {
+ public:
+  virtual ~EngineBase() = default;
+  virtual void run_epoch(qgnn_epoch_metrics* m) = 0;
+  virtual void set_features(const void* f) = 0;
+  virtual void get_weights(int l, void* out) = 0;
+  virtual void set_weights(int l, const void* in) = 0;
+  virtual void info(int64_t* out) = 0;
+  virtual int kernel_stats(double* out, int n) = 0;
+};
+
+template <typename T>
+class Engine final : public EngineBase {
+ public:
+  Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const int32_t* adj,
+         const void* features, const int32_t* labels, const uint8_t* train, const uint8_t* val,
+         const uint8_t* test, const uint32_t* owner, const void* nccl_id);
+  ~Engine() override;
+  void run_epoch(qgnn_epoch_metrics* m) override;
+  void set_features(const void* f) override;
+  void get_weights(int l, void* out) override;
+  void set_weights(int l, const void* in) override;
+  void info(int64_t* out) override;
+  int kernel_stats(double* out, int n) override;
+
+ private:
+  struct PartDev {
+    int id = 0;
+    View view;
+    // static graph arrays
+    DBuf<int64_t> lptr, rptr, sptr;
+    DBuf<int32_t> lcol, rslot, srow;
+    DBuf<T> lafwd, labwd, ralpha, salpha, self_alpha;
+    DBuf<int32_t> labels, train_rows, val_rows, test_rows, ref_order;
+    int64_t n_train = 0, n_val = 0, n_test = 0;
+    // activations
+    std::vector<DBuf<T>> h, hagg;  // h[0..L], hagg[0..L-1]
+    DBuf<T> halo, partials, dh, dh_next, dz, gbar;
+    // per key: sender metadata
+    struct SendMeta {
+      DBuf<int32_t> rows;
+      DBuf<uint32_t> ids;
+      DBuf<uint8_t> bits;
+      DBuf<uint64_t> off;
+      DBuf<uint16_t> set;
+      DBuf<uint64_t> keys;  // [P]
+      DBuf<T> wlo, whi;
+      int64_t n = 0;
+      std::vector<int64_t> q_begin;  // [P+1] message ranges per destination
+    };
+    struct RecvMeta {
+      DBuf<int32_t> dst;
+      DBuf<uint8_t> bits;
+      DBuf<uint64_t> off;
+      int64_t n = 0;
+      std::vector<int64_t> p_begin;  // [P+1] message ranges per source
+    };
+    std::vector<SendMeta> snd;
+    std::vector<RecvMeta> rcv;
+    DBuf<double> loss;                  // [1]
+    DBuf<unsigned long long> correct;   // [2]
+    DBuf<double> ce_terms;
+  };
+
+  int64_t ld_of(int64_t d) const { return round_up(d, 8); }
+  void build_messages();
+  void layout_pair(int k, int p, int q);
+  void upload_key_meta(int k);
+  void compute_bits_uniform();
+  void prepare_epoch();
+  void quantize(PartDev& P, int k, const T* src, int64_t ld);
+  void exchange(int k);
+  void forward_layer(int l);
+  void loss_phase();
+  void backward_layer(int l);
+  void backward_last();
+  void step();
+  void adaptive_round(qgnn_epoch_metrics* m);
+  uint64_t msg_offset_send(int k, int p, int q) const { return send_base_[k][p][q]; }
+  void arena_layout();
+  // profiling
+  void kbegin(int cls);
+  void kend(int cls, double bytes, cudaStream_t s);
+  void flush_kstats();
+
+  qgnn_settings s_;
+  int64_t P_ = 0, L_ = 0, p0_ = 0, p1_ = 0;
+  std::vector<int64_t> dims_;
+  uint64_t root_ = 0;
+  uint64_t epoch_ = 0;
+  qgnn_ctx* ctx_ = nullptr;
+  cudaStream_t s_main_ = nullptr, s_comm_ = nullptr;
+  cudaEvent_t ev_a_ = nullptr, ev_b_ = nullptr, ev_x_ = nullptr, ev_q_ = nullptr;
+  ncclComm_t comm_ = nullptr;
+  int dtype_ = QGNN_F32;
+
+  // host graph facts
+  int64_t n_nodes_ = 0;
+  std::vector<uint32_t> owner_;
+  std::vector<Part> parts_;
+  std::vector<KeyInfo> keys_;
+  // msgs_[k][p][q]
+  std::vector<std::vector<std::vector<PairMsgs>>> msgs_;
+  std::vector<std::vector<std::vector<uint64_t>>> send_base_, recv_base_;
+  DBuf<uint8_t> arena_;
+  size_t arena_bytes_ = 0;
+  std::vector<std::unique_ptr<PartDev>> parts_dev_;
+  // adaptive plan
+  uint64_t plan_version_ = 0;
+  std::vector<std::vector<std::vector<double>>> rx_asq_;  // [p][q][i] fwd stats
+  // weights
+  std::vector<int64_t> woff_;  // offsets of layer l in the flat parameter vector
+  int64_t nparams_ = 0;
+  DBuf<T> w_, adam_m_, adam_v_, wgrad_all_, wsum_;
+  uint64_t adam_t_ = 0;
+  int64_t global_train_ = 0, global_val_ = 0, global_test_ = 0;
+  // profiling
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool_;
+  std::vector<std::tuple<int, size_t, double>> ev_used_;  // (class, pool index, bytes)
+  size_t ev_next_ = 0;
+  KStat kst_[QGNN_K_COUNT];
+  int cur_cls_ = -1;
+  // per-epoch message counters
+  uint64_t msgs_b_[4] = {0, 0, 0, 0};
+  double resolve_seconds_ = 0;
+};
+
+// ------------------------------------------------------------ profiling ---
+template <typename T>
+void Engine<T>::kbegin(int cls) {
+  if (!s_.kstats) return;
+  if (ev_next_ == ev_pool_.size()) {
+    cudaEvent_t a, b;
+    QGNN_CUDA(cudaEventCreate(&a));
+    QGNN_CUDA(cudaEventCreate(&b));
+    ev_pool_.emplace_back(a, b);
+  }
+  cur_cls_ = cls;
+  QGNN_CUDA(cudaEventRecord(ev_pool_[ev_next_].first, s_main_));
+}
+
+template <typename T>
+void Engine<T>::kend(int cls, double bytes, cudaStream_t s) {
+  if (!s_.kstats) return;
+  QGNN_CUDA(cudaEventRecord(ev_pool_[ev_next_].second, s));
+  ev_used_.emplace_back(cls, ev_next_, bytes);
+  ++ev_next_;
+}
+
+template <typename T>
+void Engine<T>::flush_kstats() {
+  if (!s_.kstats) return;
+  for (auto& [cls, idx, bytes] : ev_used_) {
+    float ms = 0;
+    QGNN_CUDA(cudaEventElapsedTime(&ms, ev_pool_[idx].first, ev_pool_[idx].second));
+    kst_[cls].ms += ms;
+    kst_[cls].launches += 1;
+    kst_[cls].bytes += bytes;
+  }
+  ev_used_.clear();
+  ev_next_ = 0;
+}
+
+// ---------------------------------------------------------------- setup ---
+template <typename T>
+Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const int32_t* adj,
+                  const void* features, const int32_t* labels, const uint8_t* train,
+                  const uint8_t* val, const uint8_t* test, const uint32_t* owner,
+                  const void* nccl_id)
+    : s_(s) {
+  dtype_ = sizeof(T) == 8 ? QGNN_F64 : QGNN_F32;
+  QGNN_REQUIRE(s.n_dims >= 2 && s.n_dims <= 8, QGNN_EINVAL, "engine: dims must list in and out");
+  QGNN_REQUIRE(s.n_parts >= 1, QGNN_EINVAL, "engine: n_parts must be >= 1");
+  QGNN_REQUIRE(s.world >= 1 && s.rank >= 0 && s.rank < s.world, QGNN_EINVAL, "engine: bad rank");
+  QGNN_REQUIRE(s.n_parts % s.world == 0, QGNN_EINVAL, "engine: n_parts must divide by world");
+  QGNN_REQUIRE(s.bit_mode >= 0 && s.bit_mode <= 3, QGNN_EINVAL, "engine: bad bit mode");
+  if (s.bit_mode == kFixed)
+    QGNN_REQUIRE(s.fixed_bits == 2 || s.fixed_bits == 4 || s.fixed_bits == 8, QGNN_EINVAL,
+                 "engine: fixed bit width must be 2, 4, or 8");
+  QGNN_REQUIRE(labels && train && val && test, QGNN_EINVAL, "engine: missing labels");
+  P_ = s.n_parts;
+  L_ = s.n_dims - 1;
+  dims_.assign(s.dims, s.dims + s.n_dims);
+  p0_ = s.rank * (P_ / s.world);
+  p1_ = p0_ + P_ / s.world;
+  n_nodes_ = n;
+  root_ = rng_seed_key(s.seed);
+  QGNN_CUDA(cudaSetDevice(s.device));
+  QGNN_REQUIRE(qgnn_ctx_create(s.device, &ctx_) == QGNN_OK, QGNN_ECUDA, qgnn_last_error());
+  int lo_pri = 0, hi_pri = 0;
+  QGNN_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+  QGNN_CUDA(cudaStreamCreateWithPriority(&s_main_, cudaStreamNonBlocking, lo_pri));
+  QGNN_CUDA(cudaStreamCreateWithPriority(&s_comm_, cudaStreamNonBlocking, hi_pri));
+  QGNN_CUDA(cudaEventCreate(&ev_a_));
+  QGNN_CUDA(cudaEventCreate(&ev_b_));
+  QGNN_CUDA(cudaEventCreateWithFlags(&ev_x_, cudaEventDisableTiming));
+  QGNN_CUDA(cudaEventCreateWithFlags(&ev_q_, cudaEventDisableTiming));
+  if (s.world > 1) {
+    QGNN_REQUIRE(nccl_id, QGNN_EINVAL, "engine: world > 1 needs an NCCL unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    QGNN_NCCL(nccl().CommInitRank(&comm_, s.world, id, s.rank));
+  }
+
+  // partition (engine.hpp:212) and coefficients (:213)
+  if (owner)
+    owner_.assign(owner, owner + n);
+  else
+    owner_ = partition_owner_bfs(ptr, adj, n, P_, s.seed);
+  parts_ = partitions_from_owner(ptr, adj, n, owner_.data(), P_);
+  std::vector<double> alpha, self_alpha;
+  compute_coeffs(ptr, adj, n, s.sage != 0, alpha, self_alpha);
+
+  for (int64_t v = 0; v < n; ++v) {
+    global_train_ += train[v] != 0;
+    global_val_ += val[v] != 0;
+    global_test_ += test[v] != 0;
+  }
+  QGNN_REQUIRE(global_train_ > 0, QGNN_EINVAL, "engine: empty train mask");
+
+  // keys: forward t = 0..L-1, backward t = 1..L-1 (engine.hpp:345-352)
+  for (int64_t t = 0; t < L_; ++t) keys_.push_back({int(t), false, dims_[t], uint64_t(2 * t)});
+  for (int64_t t = 1; t < L_; ++t) keys_.push_back({int(t), true, dims_[t], uint64_t(2 * t + 1)});
+
+  // views of hosted partitions (parallel)
+  parts_dev_.resize(p1_ - p0_);
+  {
+    std::vector<std::future<View>> futs;
+    for (int64_t p = p0_; p < p1_; ++p)
+      futs.push_back(std::async(std::launch::async, [&, p] {
+        return build_view(ptr, adj, n, parts_[p], P_, alpha, self_alpha, s.sage != 0);
+      }));
+    for (int64_t i = 0; i < p1_ - p0_; ++i) {
+      parts_dev_[i] = std::make_unique<PartDev>();
+      parts_dev_[i]->id = int(p0_ + i);
+      parts_dev_[i]->view = futs[i].get();
+    }
+  }
+
+  // forward-statistics weights of every pair (engine.hpp:262-273), for adaptive
+  if (s.bit_mode == kAdaptive) {
+    rx_asq_.assign(P_, std::vector<std::vector<double>>(P_));
+    for (int64_t p = 0; p < P_; ++p)
+      for (int64_t q = 0; q < P_; ++q) {
+        if (p == q) continue;
+        const auto& ids = parts_[p].remote_out[q];
+        auto& out = rx_asq_[p][q];
+        out.assign(ids.size(), 0.0);
+        for (size_t i = 0; i < ids.size(); ++i) {
+          const uint32_t u = ids[i];
+          double acc = 0.0;
+          for (int64_t e = ptr[u]; e < ptr[u + 1]; ++e) {  // ascending v == receiver row order
+            const uint32_t v = static_cast<uint32_t>(adj[e]);
+            if (owner_[v] != static_cast<uint32_t>(q)) continue;
+            const double a = s.sage ? self_alpha[v] : alpha[e];
+            acc += a * a;
+          }
+          out[i] = acc;
+        }
+      }
+  }
+
+  // device state per hosted partition
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    const View& V = D.view;
+    auto tocast = [](const std::vector<double>& v) { return std::vector<T>(v.begin(), v.end()); };
+    D.lptr.upload(V.local_ptr);
+    D.lcol.upload(V.local_col);
+    D.lafwd.upload(tocast(V.local_afwd));
+    D.labwd.upload(tocast(V.local_abwd));
+    D.rptr.upload(V.remote_ptr);
+    D.rslot.upload(V.remote_slot);
+    D.ralpha.upload(tocast(V.remote_alpha));
+    D.sptr.upload(V.slot_ptr);
+    D.srow.upload(V.slot_row);
+    D.salpha.upload(tocast(V.slot_alpha));
+    D.self_alpha.upload(tocast(V.self_alpha));
+    std::vector<int32_t> lab(V.num_owned), tr, va, te;
+    for (int64_t g = 0; g < V.num_owned; ++g) {
+      const uint32_t node = V.row_node[g];
+      lab[g] = labels[node];
+    }
+    for (int64_t r = 0; r < V.num_owned; ++r) {  // reference row order
+      const int32_t g = V.gpu_row_of_ref[r];
+      const uint32_t node = V.row_node[g];
+      if (train[node]) tr.push_back(g);
+      if (val[node]) va.push_back(g);
+      if (test[node]) te.push_back(g);
+    }
+    D.labels.upload(lab);
+    D.train_rows.upload(tr);
+    D.val_rows.upload(va);
+    D.test_rows.upload(te);
+    D.n_train = int64_t(tr.size());
+    D.n_val = int64_t(va.size());
+    D.n_test = int64_t(te.size());
+    D.ref_order.upload(V.gpu_row_of_ref);
+    const int64_t no = V.num_owned, nr = V.num_remote;
+    int64_t maxd = 0;
+    for (int64_t d : dims_) maxd = std::max(maxd, ld_of(d));
+    D.h.resize(L_ + 1);
+    D.hagg.resize(L_);
+    for (int64_t l = 0; l <= L_; ++l) D.h[l].alloc(no * ld_of(dims_[l]));
+    for (int64_t t = 0; t < L_; ++t) D.hagg[t].alloc(no * ld_of(dims_[t]));
+    D.halo.alloc(std::max<int64_t>(1, nr) * maxd);
+    D.partials.alloc(std::max<int64_t>(1, nr) * maxd);
+    D.dh.alloc(no * maxd);
+    D.dh_next.alloc(no * maxd);
+    D.dz.alloc(no * maxd);
+    D.gbar.alloc(no * maxd);
+    D.loss.alloc(1);
+    D.correct.alloc(2);
+    D.ce_terms.alloc(std::max<int64_t>(1, D.n_train));
+    D.snd.resize(keys_.size());
+    D.rcv.resize(keys_.size());
+  }
+  set_features(features);
+
+  // weights: GnnModel::init (model.hpp:27-41), replicated on every rank
+  woff_.assign(L_ + 1, 0);
+  for (int64_t l = 0; l < L_; ++l) woff_[l + 1] = woff_[l] + dims_[l] * dims_[l + 1];
+  nparams_ = woff_[L_];
+  {
+    std::vector<T> w(nparams_);
+    for (int64_t l = 0; l < L_; ++l) {
+      const double a = std::sqrt(6.0 / static_cast<double>(dims_[l] + dims_[l + 1]));
+      const uint64_t key = rng_fork(rng_fork(rng_seed_key(s.seed), 0x77), uint64_t(l));
+      for (int64_t i = 0; i < dims_[l] * dims_[l + 1]; ++i) {
+        const double u = static_cast<double>(rng_u53(key, uint64_t(i) + 1)) * 0x1.0p-53;
+        w[woff_[l] + i] = static_cast<T>((2.0 * u - 1.0) * a);
+      }
+    }
+    w_.upload(w);
+  }
+  adam_m_.alloc(nparams_);
+  adam_v_.alloc(nparams_);
+  wgrad_all_.alloc(P_ * nparams_);
+  wsum_.alloc(nparams_);
+
+  plan_version_ = s.bit_mode == kAdaptive ? 1 : 0;
+  build_messages();
+  for (size_t k = 0; k < keys_.size(); ++k) upload_key_meta(int(k));
+  QGNN_CUDA(cudaDeviceSynchronize());
+}
+
+template <typename T>
+Engine<T>::~Engine() {
+  cudaDeviceSynchronize();
+  parts_dev_.clear();
+  for (auto& e : ev_pool_) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  if (comm_) nccl().CommDestroy(comm_);
+  if (ev_a_) cudaEventDestroy(ev_a_);
+  if (ev_b_) cudaEventDestroy(ev_b_);
+  if (ev_x_) cudaEventDestroy(ev_x_);
+  if (ev_q_) cudaEventDestroy(ev_q_);
+  if (s_main_) cudaStreamDestroy(s_main_);
+  if (s_comm_) cudaStreamDestroy(s_comm_);
+  if (ctx_) qgnn_ctx_destroy(ctx_);
+}
+
+template <typename T>
+void Engine<T>::set_features(const void* f) {
+  const int64_t F = dims_[0];
+  const T* src = static_cast<const T*>(f);
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    const int64_t no = D.view.num_owned, ld = ld_of(F);
+    std::vector<T> buf(no * ld, T(0));
+    for (int64_t g = 0; g < no; ++g)
+      std::memcpy(&buf[g * ld], src + static_cast<int64_t>(D.view.row_node[g]) * F, F * sizeof(T));
+    QGNN_CUDA(cudaMemcpyAsync(D.h[0].p, buf.data(), buf.size() * sizeof(T), cudaMemcpyHostToDevice,
+                              s_main_));
+    QGNN_CUDA(cudaStreamSynchronize(s_main_));
+  }
+}
+
+// Message lists of every ordered pair and key (engine.hpp:142-143, 585-587, 683-687);
+// bit widths from the mode, offsets from the codec wire order.
+template <typename T>
+void Engine<T>::build_messages() {
+  msgs_.assign(keys_.size(), std::vector<std::vector<PairMsgs>>(P_, std::vector<PairMsgs>(P_)));
+  for (size_t k = 0; k < keys_.size(); ++k)
+    for (int64_t p = 0; p < P_; ++p)
+      for (int64_t q = 0; q < P_; ++q) {
+        if (p == q) continue;
+        PairMsgs& m = msgs_[k][p][q];
+        m.ids = keys_[k].bwd ? parts_[p].remote_in[q] : parts_[p].remote_out[q];
+        const uint8_t b = s_.bit_mode == kFp ? 0 : s_.bit_mode == kFixed ? uint8_t(s_.fixed_bits) : 8;
+        m.bits.assign(m.ids.size(), b);  // adaptive: initial all-8 plan (plan.hpp:104-126)
+      }
+  if (s_.bit_mode == kUniform) compute_bits_uniform();
+  for (size_t k = 0; k < keys_.size(); ++k)
+    for (int64_t p = 0; p < P_; ++p)
+      for (int64_t q = 0; q < P_; ++q)
+        if (p != q) layout_pair(int(k), int(p), int(q));
+  arena_layout();
+}
+
+template <typename T>
+void Engine<T>::layout_pair(int k, int p, int q) {
+  PairMsgs& m = msgs_[k][p][q];
+  const int64_t n = int64_t(m.ids.size());
+  const int64_t dim = keys_[k].dim;
+  m.off.assign(n, 0);
+  uint64_t off = 0, ref = 0;
+  for (int b : {0, 2, 4, 8}) {
+    for (int64_t i = 0; i < n; ++i) {
+      if (m.bits[i] != b) continue;
+      m.off[i] = off;
+      off += qgnn_chunk_wire_bytes(dim, b, s_.layout, dtype_);
+      ref += b == 0 ? uint64_t(dim) * 8 : qgnn_chunk_wire_bytes(dim, b, QGNN_WIRE_REF, QGNN_F64);
+    }
+  }
+  m.bytes = off;
+  m.ref_bytes = ref;
+}
+
+// engine.hpp:443-446: a random width per message per epoch
+template <typename T>
+void Engine<T>::compute_bits_uniform() {
+  for (size_t k = 0; k < keys_.size(); ++k)
+    for (int64_t p = 0; p < P_; ++p)
+      for (int64_t q = 0; q < P_; ++q) {
+        if (p == q) continue;
+        PairMsgs& m = msgs_[k][p][q];
+        for (size_t i = 0; i < m.ids.size(); ++i) {
+          uint64_t key = root_;
+          for (uint64_t c : {uint64_t(0x3), epoch_, keys_[k].code, uint64_t(p), uint64_t(q),
+                             uint64_t(m.ids[i])})
+            key = rng_fork(key, c);
+          uint64_t ctr = 0;
+          m.bits[i] = uint8_t(kChoices[rng_next_below(key, ctr, 3)]);
+        }
+      }
+}
+
+// Arena: per key, send regions of hosted senders (per destination) followed by
+// receive regions of hosted receivers for remote sources.  All keys reuse the
+// same arena (they are processed one after another on the same streams).
+template <typename T>
+void Engine<T>::arena_layout() {
+  send_base_.assign(keys_.size(), std::vector<std::vector<uint64_t>>(P_, std::vector<uint64_t>(P_, 0)));
+  recv_base_ = send_base_;
+  size_t need = 0;
+  for (size_t k = 0; k < keys_.size(); ++k) {
+    uint64_t o = 0;
+    auto al = [](uint64_t x) { return (x + 255) / 256 * 256; };
+    for (int64_t p = p0_; p < p1_; ++p)
+      for (int64_t q = 0; q < P_; ++q) {
+        if (q == p) continue;
+        send_base_[k][p][q] = o;
+        o = al(o + msgs_[k][p][q].bytes);
+      }
+    for (int64_t q = p0_; q < p1_; ++q)
+      for (int64_t p = 0; p < P_; ++p) {
+        if (p == q) continue;
+        if (p >= p0_ && p < p1_)
+          recv_base_[k][q][p] = send_base_[k][p][q];  // zero copy on the same GPU
+        else {
+          recv_base_[k][q][p] = o;
+          o = al(o + msgs_[k][p][q].bytes);
+        }
+      }
+    need = std::max<size_t>(need, o);
+  }
+  if (need > arena_bytes_ || !arena_.p) {
+    arena_.alloc(std::max<size_t>(need, 256), true);
+    arena_bytes_ = std::max<size_t>(need, 256);
+  }
+}
+
+template <typename T>
+void Engine<T>::upload_key_meta(int k) {
+  const KeyInfo& K = keys_[k];
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    const int64_t p = D.id;
+    const View& V = D.view;
+    auto& S = D.snd[k];
+    std::vector<int32_t> rows;
+    std::vector<uint32_t> ids;
+    std::vector<uint8_t> bits;
+    std::vector<uint64_t> off;
+    std::vector<uint16_t> set;
+    S.q_begin.assign(P_ + 1, 0);
+    for (int64_t q = 0; q < P_; ++q) {
+      S.q_begin[q] = int64_t(ids.size());
+      if (q == p) continue;
+      const PairMsgs& m = msgs_[k][p][q];
+      for (size_t i = 0; i < m.ids.size(); ++i) {
+        rows.push_back(K.bwd ? int32_t(V.device_slot_offset[q] + int64_t(i)) : V.gpu_row(m.ids[i]));
+        ids.push_back(m.ids[i]);
+        bits.push_back(m.bits[i]);
+        off.push_back(send_base_[k][p][q] + m.off[i]);
+        set.push_back(uint16_t(q));
+      }
+    }
+    S.q_begin[P_] = int64_t(ids.size());
+    const bool fresh = S.n != int64_t(ids.size()) || !S.rows.p;
+    S.n = int64_t(ids.size());
+    if (fresh) {
+      S.rows.upload(rows);
+      S.ids.upload(ids);
+      S.set.upload(set);
+      S.keys.alloc(P_);
+      S.wlo.alloc(std::max<int64_t>(1, S.n), false);
+      S.whi.alloc(std::max<int64_t>(1, S.n), false);
+      if (S.n)
+        k_fill2<T><<<unsigned(ceil_div(S.n, 256)), 256, 0, s_main_>>>(
+            S.wlo.p, T(INFINITY), S.whi.p, T(-INFINITY), S.n);
+    }
+    S.bits.upload(bits);
+    S.off.upload(off);
+
+    auto& R = D.rcv[k];
+    std::vector<int32_t> dst;
+    std::vector<uint8_t> rb;
+    std::vector<uint64_t> ro;
+    R.p_begin.assign(P_ + 1, 0);
+    for (int64_t src = 0; src < P_; ++src) {
+      R.p_begin[src] = int64_t(dst.size());
+      if (src == p) continue;
+      const PairMsgs& m = msgs_[k][src][p];
+      for (size_t i = 0; i < m.ids.size(); ++i) {
+        dst.push_back(K.bwd ? V.gpu_row(m.ids[i]) : int32_t(V.device_slot_offset[src] + int64_t(i)));
+        rb.push_back(m.bits[i]);
+        ro.push_back(recv_base_[k][p][src] + m.off[i]);
+      }
+    }
+    R.p_begin[P_] = int64_t(dst.size());
+    if (R.n != int64_t(dst.size()) || !R.dst.p) R.dst.upload(dst);
+    R.n = int64_t(dst.size());
+    R.bits.upload(rb);
+    R.off.upload(ro);
+  }
+}
+
+template <typename T>
+void Engine<T>::prepare_epoch() {
+  if (s_.bit_mode == kUniform) {
+    compute_bits_uniform();
+    for (size_t k = 0; k < keys_.size(); ++k)
+      for (int64_t p = 0; p < P_; ++p)
+        for (int64_t q = 0; q < P_; ++q)
+          if (p != q) layout_pair(int(k), int(p), int(q));
+    arena_layout();
+    for (size_t k = 0; k < keys_.size(); ++k) upload_key_meta(int(k));
+  }
+  // RNG stream of each encoded set: root.fork({0x2, epoch, key_code, src, dst}) (engine.hpp:497)
+  for (size_t k = 0; k < keys_.size(); ++k)
+    for (auto& up : parts_dev_) {
+      std::vector<uint64_t> ks(P_, 0);
+      for (int64_t q = 0; q < P_; ++q) {
+        uint64_t key = root_;
+        for (uint64_t c : {uint64_t(0x2), epoch_, keys_[k].code, uint64_t(up->id), uint64_t(q)})
+          key = rng_fork(key, c);
+        ks[q] = key;
+      }
+      QGNN_CUDA(cudaMemcpyAsync(up->snd[k].keys.p, ks.data(), P_ * sizeof(uint64_t),
+                                cudaMemcpyHostToDevice, s_main_));
+    }
+  msgs_b_[0] = msgs_b_[1] = msgs_b_[2] = msgs_b_[3] = 0;
+  for (size_t k = 0; k < keys_.size(); ++k)
+    for (int64_t p = 0; p < P_; ++p)
+      for (int64_t q = 0; q < P_; ++q) {
+        if (p == q) continue;
+        for (uint8_t b : msgs_[k][p][q].bits) ++msgs_b_[b == 0 ? 3 : b == 2 ? 0 : b == 4 ? 1 : 2];
+      }
+}
+
+// ------------------------------------------------------------ data path ---
+template <typename T>
+void Engine<T>::quantize(PartDev& D, int k, const T* src, int64_t ld) {
+  auto& S = D.snd[k];
+  if (S.n == 0) return;
+  const int64_t dim = keys_[k].dim;
+  kbegin(QGNN_K_QUANT);
+  const int st = qgnn_quantize_pack(ctx_, src, dtype_, ld, dim, S.n, S.rows.p, S.ids.p, S.bits.p,
+                                    S.off.p, S.set.p, S.keys.p, s_.layout, arena_.p, S.wlo.p,
+                                    S.whi.p, s_main_);
+  if (st) throw Status(st, qgnn_last_error());
+  // algorithmic bytes: rows read once per message + packed chunks + metadata
+  double bytes = 0;
+  for (int64_t q = 0; q < P_; ++q)
+    if (q != D.id) bytes += double(msgs_[k][D.id][q].bytes);
+  bytes += double(S.n) * (double(dim) * sizeof(T) + 4 + 4 + 1 + 8 + 2 + 2 * sizeof(T));
+  kend(QGNN_K_QUANT, bytes, s_main_);
+}
+
+// Grouped point-to-point exchange of the remote pairs on the comm stream.
+template <typename T>
+void Engine<T>::exchange(int k) {
+  if (s_.world == 1) return;  // every pair is on this GPU: zero-copy
+  QGNN_CUDA(cudaEventRecord(ev_q_, s_main_));
+  QGNN_CUDA(cudaStreamWaitEvent(s_comm_, ev_q_, 0));
+  const int64_t ppr = P_ / s_.world;
+  if (s_.kstats) {
+    kbegin(QGNN_K_EXCHANGE);
+    QGNN_CUDA(cudaEventRecord(ev_pool_[ev_next_].first, s_comm_));
+  }
+  double bytes = 0;
+  QGNN_NCCL(nccl().GroupStart());
+  for (int64_t p = p0_; p < p1_; ++p)
+    for (int64_t q = 0; q < P_; ++q) {
+      if (q == p || (q >= p0_ && q < p1_)) continue;
+      const uint64_t nb = msgs_[k][p][q].bytes;
+      if (!nb) continue;
+      QGNN_NCCL(nccl().Send(arena_.p + send_base_[k][p][q], nb, ncclUint8, int(q / ppr), comm_,
+                            s_comm_));
+      bytes += double(nb);
+    }
+  for (int64_t q = p0_; q < p1_; ++q)
+    for (int64_t p = 0; p < P_; ++p) {
+      if (p == q || (p >= p0_ && p < p1_)) continue;
+      const uint64_t nb = msgs_[k][p][q].bytes;
+      if (!nb) continue;
+      QGNN_NCCL(nccl().Recv(arena_.p + recv_base_[k][q][p], nb, ncclUint8, int(p / ppr), comm_,
+                            s_comm_));
+    }
+  QGNN_NCCL(nccl().GroupEnd());
+  kend(QGNN_K_EXCHANGE, bytes, s_comm_);
+  QGNN_CUDA(cudaEventRecord(ev_x_, s_comm_));
+}
+
+#define QGNN_CALL(x)                                 \
+  do {                                               \
+    const int st_ = (x);                             \
+    if (st_) throw Status(st_, qgnn_last_error());   \
+  } while (0)
+
+template <typename T>
+void Engine<T>::forward_layer(int l) {
+  const int t = l - 1;
+  const int k = t;  // forward key index
+  const int64_t din = dims_[t], dout = dims_[l];
+  const int64_t ldi = ld_of(din), ldo = ld_of(dout);
+  const int relu = l < L_ ? 1 : 0;
+  // fwd_send (engine.hpp:566-588)
+  for (auto& up : parts_dev_) quantize(*up, k, up->h[t].p, ldi);
+  exchange(k);
+  // central rows while the exchange is in flight (engine.hpp:598-605)
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    const int64_t nc = D.view.n_central;
+    if (!nc) continue;
+    kbegin(QGNN_K_SPMM_FWD);
+    QGNN_CALL(qgnn_csr_aggregate(ctx_, dtype_, din, D.h[t].p, ldi, nullptr, 0, D.self_alpha.p,
+                                 D.lptr.p, D.lcol.p, D.lafwd.p, nullptr, nullptr, nullptr, nullptr,
+                                 0, nc, D.hagg[t].p, ldi, s_main_));
+    const double nnz = double(D.view.local_ptr[nc]);
+    kend(QGNN_K_SPMM_FWD, nc * (16.0 + 2 * din * sizeof(T)) + nnz * (4 + sizeof(T)) +
+                              double(D.view.num_owned) * din * sizeof(T), s_main_);
+    kbegin(QGNN_K_GEMM_FWD);
+    QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
+                                 nullptr, 0, nc, relu, D.h[l].p, ldo, s_main_));
+    kend(QGNN_K_GEMM_FWD, double(nc) * (din + dout) * sizeof(T), s_main_);
+  }
+  if (s_.world > 1) QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_x_, 0));
+  // receive (engine.hpp:607-618): decode every source straight into the halo
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    auto& R = D.rcv[k];
+    if (!R.n) continue;
+    kbegin(QGNN_K_DEQUANT);
+    QGNN_CALL(qgnn_dequant_scatter(ctx_, arena_.p, R.n, din, R.bits.p, R.off.p, s_.layout,
+                                   R.dst.p, 0, D.halo.p, dtype_, ldi, s_main_));
+    double bytes = double(R.n) * (din * sizeof(T) + 4 + 1 + 8);
+    for (int64_t src = 0; src < P_; ++src)
+      if (src != D.id) bytes += double(msgs_[k][src][D.id].bytes);
+    kend(QGNN_K_DEQUANT, bytes, s_main_);
+  }
+  // marginal rows (engine.hpp:622-623)
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    const int64_t nc = D.view.n_central, nm = D.view.n_marginal;
+    if (!nm) continue;
+    kbegin(QGNN_K_SPMM_FWD);
+    QGNN_CALL(qgnn_csr_aggregate(ctx_, dtype_, din, D.h[t].p, ldi, D.halo.p, ldi, D.self_alpha.p,
+                                 D.lptr.p, D.lcol.p, D.lafwd.p, D.rptr.p, D.rslot.p, D.ralpha.p,
+                                 nullptr, nc, nm, D.hagg[t].p, ldi, s_main_));
+    const double nnz = double(D.view.local_ptr[nc + nm] - D.view.local_ptr[nc]) +
+                       double(D.view.remote_nnz());
+    kend(QGNN_K_SPMM_FWD, nm * (24.0 + 2 * din * sizeof(T)) + nnz * (4 + sizeof(T)) +
+                              double(D.view.num_remote) * din * sizeof(T), s_main_);
+    kbegin(QGNN_K_GEMM_FWD);
+    QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
+                                 nullptr, nc, nm, relu, D.h[l].p, ldo, s_main_));
+    kend(QGNN_K_GEMM_FWD, double(nm) * (din + dout) * sizeof(T), s_main_);
+  }
+}
+
+// loss_phase (engine.hpp:647-659)
+template <typename T>
+void Engine<T>::loss_phase() {
+  const int64_t C = dims_[L_], ldc = ld_of(C);
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    QGNN_CUDA(cudaMemsetAsync(D.dh.p, 0, D.view.num_owned * ldc * sizeof(T), s_main_));
+    QGNN_CUDA(cudaMemsetAsync(D.loss.p, 0, sizeof(double), s_main_));
+    QGNN_CUDA(cudaMemsetAsync(D.correct.p, 0, 2 * sizeof(unsigned long long), s_main_));
+    kbegin(QGNN_K_ELEMWISE);
+    if (D.n_train)
+      QGNN_CALL(qgnn_masked_ce(ctx_, dtype_, D.h[L_].p, ldc, C, D.labels.p, D.train_rows.p,
+                               D.n_train, 1.0 / double(global_train_), D.dh.p, ldc, D.loss.p,
+                               s_main_));
+    if (D.n_val)
+      QGNN_CALL(qgnn_count_correct(ctx_, dtype_, D.h[L_].p, ldc, C, D.labels.p, D.val_rows.p,
+                                   D.n_val, D.correct.p, s_main_));
+    if (D.n_test)
+      QGNN_CALL(qgnn_count_correct(ctx_, dtype_, D.h[L_].p, ldc, C, D.labels.p, D.test_rows.p,
+                                   D.n_test, D.correct.p + 1, s_main_));
+    kend(QGNN_K_ELEMWISE, double(D.view.num_owned) * C * sizeof(T) * 2, s_main_);
+  }
+}
+
+template <typename T>
+void Engine<T>::backward_layer(int l) {
+  const int t = l - 1;
+  const int k = int(L_) + t - 1;  // backward key index (keys: fwd 0..L-1, bwd 1..L-1)
+  const int64_t din = dims_[t], dout = dims_[l];
+  const int64_t ldi = ld_of(din), ldo = ld_of(dout);
+  const bool relu = l < L_;
+  const T* W = w_.p + woff_[t];
+  // bwd_send (engine.hpp:661-688): marginal chain, remote partials, encode
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    const int64_t nc = D.view.n_central, nm = D.view.n_marginal;
+    const T* dz = D.dh.p;
+    if (relu) {
+      kbegin(QGNN_K_ELEMWISE);
+      QGNN_CALL(qgnn_relu_backward(ctx_, dtype_, D.h[l].p, ldo, D.dh.p, ldo, dout, nc, nm, D.dz.p,
+                                   ldo, s_main_));
+      kend(QGNN_K_ELEMWISE, double(nm) * dout * sizeof(T) * 3, s_main_);
+      dz = D.dz.p;
+    }
+    kbegin(QGNN_K_GEMM_DGRAD);
+    QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, dz, ldo, W, din, dout, nullptr, nc, nm, D.gbar.p,
+                                    ldi, s_main_));
+    kend(QGNN_K_GEMM_DGRAD, double(nm) * (din + dout) * sizeof(T), s_main_);
+    if (D.view.num_remote) {
+      kbegin(QGNN_K_PARTIALS);
+      QGNN_CALL(qgnn_csr_aggregate(ctx_, dtype_, din, D.gbar.p, ldi, nullptr, 0, nullptr, D.sptr.p,
+                                   D.srow.p, D.salpha.p, nullptr, nullptr, nullptr, nullptr, 0,
+                                   D.view.num_remote, D.partials.p, ldi, s_main_));
+      kend(QGNN_K_PARTIALS, double(D.view.num_remote) * (8 + din * sizeof(T)) +
+                                double(D.view.remote_nnz()) * (4 + sizeof(T) + din * sizeof(T)),
+           s_main_);
+    }
+    quantize(D, k, D.partials.p, ldi);
+  }
+  exchange(k);
+  // bwd_finish (engine.hpp:690-740)
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    const int64_t nc = D.view.n_central, no = D.view.num_owned;
+    const T* dz = D.dh.p;
+    if (relu) {
+      kbegin(QGNN_K_ELEMWISE);
+      QGNN_CALL(qgnn_relu_backward(ctx_, dtype_, D.h[l].p, ldo, D.dh.p, ldo, dout, 0, nc, D.dz.p,
+                                   ldo, s_main_));
+      kend(QGNN_K_ELEMWISE, double(nc) * dout * sizeof(T) * 3, s_main_);
+      dz = D.dz.p;
+    }
+    kbegin(QGNN_K_GEMM_DGRAD);
+    QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, dz, ldo, W, din, dout, nullptr, 0, nc, D.gbar.p,
+                                    ldi, s_main_));
+    kend(QGNN_K_GEMM_DGRAD, double(nc) * (din + dout) * sizeof(T), s_main_);
+    kbegin(QGNN_K_GEMM_WGRAD);
+    T* wg = wgrad_all_.p + D.id * nparams_ + woff_[t];
+    QGNN_CALL(qgnn_dense_weight_grad(ctx_, dtype_, D.hagg[t].p, ldi, dz, ldo, din, dout,
+                                     dtype_ == QGNN_F64 ? D.ref_order.p : nullptr, 0, no, 0, wg,
+                                     s_main_));
+    kend(QGNN_K_GEMM_WGRAD, double(no) * (din + dout) * sizeof(T), s_main_);
+    kbegin(QGNN_K_SPMM_BWD);
+    QGNN_CALL(qgnn_csr_aggregate(ctx_, dtype_, din, D.gbar.p, ldi, nullptr, 0, D.self_alpha.p,
+                                 D.lptr.p, D.lcol.p, D.labwd.p, nullptr, nullptr, nullptr, nullptr,
+                                 0, no, D.dh_next.p, ldi, s_main_));
+    kend(QGNN_K_SPMM_BWD, no * (16.0 + 2 * din * sizeof(T)) +
+                              double(D.view.local_nnz()) * (4 + sizeof(T)) +
+                              double(no) * din * sizeof(T), s_main_);
+  }
+  if (s_.world > 1) QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_x_, 0));
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    auto& R = D.rcv[k];
+    for (int64_t src = 0; src < P_; ++src) {  // ascending source (engine.hpp:720-734)
+      const int64_t b = R.p_begin[src], e = R.p_begin[src + 1];
+      if (e == b) continue;
+      kbegin(QGNN_K_DEQUANT);
+      QGNN_CALL(qgnn_dequant_scatter(ctx_, arena_.p, e - b, din, R.bits.p + b, R.off.p + b,
+                                     s_.layout, R.dst.p + b, 1, D.dh_next.p, dtype_, ldi,
+                                     s_main_));
+      kend(QGNN_K_DEQUANT, double(e - b) * (2 * din * sizeof(T) + 13) +
+                               double(msgs_[k][src][D.id].bytes), s_main_);
+    }
+    std::swap(D.dh, D.dh_next);
+  }
+}
+
+// bwd_last (engine.hpp:743-765): layer-1 weight gradient only
+template <typename T>
+void Engine<T>::backward_last() {
+  const int64_t din = dims_[0], dout = dims_[1];
+  const int64_t ldi = ld_of(din), ldo = ld_of(dout);
+  const bool relu = L_ > 1;
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    const int64_t no = D.view.num_owned;
+    const T* dz = D.dh.p;
+    if (relu) {
+      kbegin(QGNN_K_ELEMWISE);
+      QGNN_CALL(qgnn_relu_backward(ctx_, dtype_, D.h[1].p, ldo, D.dh.p, ldo, dout, 0, no, D.dz.p,
+                                   ldo, s_main_));
+      kend(QGNN_K_ELEMWISE, double(no) * dout * sizeof(T) * 3, s_main_);
+      dz = D.dz.p;
+    }
+    kbegin(QGNN_K_GEMM_WGRAD);
+    QGNN_CALL(qgnn_dense_weight_grad(ctx_, dtype_, D.hagg[0].p, ldi, dz, ldo, din, dout,
+                                     dtype_ == QGNN_F64 ? D.ref_order.p : nullptr, 0, no, 0,
+                                     wgrad_all_.p + D.id * nparams_ + woff_[0], s_main_));
+    kend(QGNN_K_GEMM_WGRAD, double(no) * (din + dout) * sizeof(T), s_main_);
+  }
+}
+
+// allreduce_and_step (engine.hpp:782-801): fixed-order sum, then Adam
+template <typename T>
+void Engine<T>::step() {
+  kbegin(QGNN_K_ELEMWISE);
+  if (s_.world > 1) {
+    const int64_t ppr = P_ / s_.world;
+    T* base = wgrad_all_.p;
+    QGNN_NCCL(nccl().AllGather(base + p0_ * nparams_, base, size_t(ppr * nparams_),
+                               sizeof(T) == 8 ? ncclFloat64 : ncclFloat32, comm_, s_main_));
+  }
+  k_sum_parts<T><<<unsigned(ceil_div(nparams_, 256)), 256, 0, s_main_>>>(wgrad_all_.p, int(P_),
+                                                                         nparams_, wsum_.p);
+  ++adam_t_;
+  const double b1 = 0.9, b2 = 0.999;
+  const double bc1 = 1.0 - std::pow(b1, double(adam_t_));
+  const double bc2 = 1.0 - std::pow(b2, double(adam_t_));
+  QGNN_CALL(qgnn_adam_step(ctx_, dtype_, w_.p, adam_m_.p, adam_v_.p, wsum_.p, nparams_, s_.lr, b1,
+                           b2, 1e-8, bc1, bc2, s_main_));
+  kend(QGNN_K_ELEMWISE, double(nparams_) * sizeof(T) * (P_ + 6), s_main_);
+}
+
+template <typename T>
+void Engine<T>::run_epoch(qgnn_epoch_metrics* m) {
+  ++epoch_;
+  QGNN_CUDA(cudaSetDevice(s_.device));
+  prepare_epoch();
+  QGNN_CUDA(cudaEventRecord(ev_a_, s_main_));
+  for (int64_t l = 1; l <= L_; ++l) forward_layer(int(l));
+  loss_phase();
+  for (int64_t l = L_; l >= 2; --l) backward_layer(int(l));
+  backward_last();
+  step();
+  QGNN_CUDA(cudaEventRecord(ev_b_, s_main_));
+  QGNN_CUDA(cudaEventSynchronize(ev_b_));
+  float ms = 0;
+  QGNN_CUDA(cudaEventElapsedTime(&ms, ev_a_, ev_b_));
+  QGNN_CALL(qgnn_ctx_check(ctx_, s_main_));
+  flush_kstats();
+
+  // loss / accuracy (engine.hpp:393-397, 803-849)
+  std::vector<double> loss(P_, 0.0);
+  std::vector<unsigned long long> corr(2 * P_, 0);
+  for (auto& up : parts_dev_) {
+    QGNN_CUDA(cudaMemcpy(&loss[up->id], up->loss.p, sizeof(double), cudaMemcpyDeviceToHost));
+    QGNN_CUDA(cudaMemcpy(&corr[2 * up->id], up->correct.p, 2 * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost));
+  }
+  if (s_.world > 1) {
+    DBuf<double> dl;
+    DBuf<unsigned long long> dc;
+    dl.upload(loss);
+    dc.upload(corr);
+    QGNN_NCCL(nccl().AllReduce(dl.p, dl.p, size_t(P_), ncclFloat64, ncclSum, comm_, s_main_));
+    QGNN_NCCL(nccl().AllReduce(dc.p, dc.p, size_t(2 * P_), ncclUint64, ncclSum, comm_, s_main_));
+    QGNN_CUDA(cudaStreamSynchronize(s_main_));
+    QGNN_CUDA(cudaMemcpy(loss.data(), dl.p, P_ * sizeof(double), cudaMemcpyDeviceToHost));
+    QGNN_CUDA(cudaMemcpy(corr.data(), dc.p, 2 * P_ * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost));
+  }
+  double total = 0.0;
+  unsigned long long vc = 0, tc = 0;
+  for (int64_t p = 0; p < P_; ++p) {
+    total += loss[p];
+    vc += corr[2 * p];
+    tc += corr[2 * p + 1];
+  }
+  if (!std::isfinite(total))
+    throw Status(QGNN_EDIVERGED, "epoch " + std::to_string(epoch_) + ": loss diverged");
+  qgnn_epoch_metrics em{};
+  em.epoch = epoch_;
+  em.train_loss = total;
+  em.val_acc = global_val_ ? double(vc) / double(global_val_) : 0.0;
+  em.test_acc = global_test_ ? double(tc) / double(global_test_) : 0.0;
+  for (size_t k = 0; k < keys_.size(); ++k)
+    for (int64_t p = 0; p < P_; ++p)
+      for (int64_t q = 0; q < P_; ++q)
+        if (p != q) {
+          em.bytes_total += msgs_[k][p][q].bytes;
+          em.ref_bytes_total += msgs_[k][p][q].ref_bytes;
+        }
+  em.msgs_b2 = msgs_b_[0];
+  em.msgs_b4 = msgs_b_[1];
+  em.msgs_b8 = msgs_b_[2];
+  em.msgs_fp = msgs_b_[3];
+  em.ms_total = ms;
+  em.ms_quant = kst_[QGNN_K_QUANT].ms;
+  resolve_seconds_ = 0;
+  if (s_.bit_mode == kAdaptive) adaptive_round(&em);
+  em.plan_version = plan_version_;
+  em.resolve_seconds = resolve_seconds_;
+  *m = em;
+}
+
+// gather_stats (engine.hpp:135-165) + reassignment_round (solve.hpp:337-363) + adopt_plan (:851-861)
+template <typename T>
+void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
+  if (s_.period <= 0 || epoch_ % uint64_t(s_.period) != 0) return;
+  const auto t0 = std::chrono::steady_clock::now();
+  // windows of every sender partition (all ranks)
+  std::vector<std::vector<std::vector<double>>> wlo(keys_.size()), whi(keys_.size());
+  for (size_t k = 0; k < keys_.size(); ++k) {
+    wlo[k].assign(P_, {});
+    whi[k].assign(P_, {});
+    int64_t maxn = 0;
+    for (int64_t p = 0; p < P_; ++p) {
+      int64_t n = 0;
+      for (int64_t q = 0; q < P_; ++q)
+        if (q != p) n += int64_t(msgs_[k][p][q].ids.size());
+      maxn = std::max(maxn, n);
+    }
+    const int64_t ppr = P_ / s_.world;
+    std::vector<T> lo_all(P_ * std::max<int64_t>(1, maxn)), hi_all(lo_all.size());
+    DBuf<T> dlo, dhi;
+    dlo.alloc(lo_all.size());
+    dhi.alloc(lo_all.size());
+    const int64_t stride = std::max<int64_t>(1, maxn);
+    for (auto& up : parts_dev_) {
+      auto& S = up->snd[k];
+      if (S.n) {
+        QGNN_CUDA(cudaMemcpyAsync(dlo.p + up->id * stride, S.wlo.p, S.n * sizeof(T),
+                                  cudaMemcpyDeviceToDevice, s_main_));
+        QGNN_CUDA(cudaMemcpyAsync(dhi.p + up->id * stride, S.whi.p, S.n * sizeof(T),
+                                  cudaMemcpyDeviceToDevice, s_main_));
+      }
+    }
+    if (s_.world > 1) {
+      const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
+      QGNN_NCCL(nccl().AllGather(dlo.p + p0_ * stride, dlo.p, size_t(ppr * stride), dt, comm_,
+                                 s_main_));
+      QGNN_NCCL(nccl().AllGather(dhi.p + p0_ * stride, dhi.p, size_t(ppr * stride), dt, comm_,
+                                 s_main_));
+    }
+    QGNN_CUDA(cudaStreamSynchronize(s_main_));
+    QGNN_CUDA(cudaMemcpy(lo_all.data(), dlo.p, lo_all.size() * sizeof(T), cudaMemcpyDeviceToHost));
+    QGNN_CUDA(cudaMemcpy(hi_all.data(), dhi.p, hi_all.size() * sizeof(T), cudaMemcpyDeviceToHost));
+    for (int64_t p = 0; p < P_; ++p) {
+      wlo[k][p].assign(lo_all.begin() + p * stride, lo_all.begin() + (p + 1) * stride);
+      whi[k][p].assign(hi_all.begin() + p * stride, hi_all.begin() + (p + 1) * stride);
+    }
+  }
+  // per key: stats -> group_and_order -> solve_assignment, concurrently (solve.hpp:343-350)
+  Cost cm;
+  cm.n = P_;
+  cm.theta.assign(P_ * P_, s_.theta);
+  cm.gamma.assign(P_ * P_, s_.gamma);
+  std::vector<std::future<SolveResult>> jobs(keys_.size());
+  std::vector<char> has(keys_.size(), 0);
+  for (size_t k = 0; k < keys_.size(); ++k) {
+    std::vector<PairStat> pairs;
+    for (int64_t p = 0; p < P_; ++p) {
+      int64_t base = 0;
+      for (int64_t q = 0; q < P_; ++q) {
+        if (p == q) continue;
+        const PairMsgs& m = msgs_[k][p][q];
+        if (m.ids.empty()) continue;
+        PairStat ps;
+        ps.src = uint32_t(p);
+        ps.dst = uint32_t(q);
+        int64_t mb = 0;
+        for (int64_t qq = 0; qq < q; ++qq)
+          if (qq != p) mb += int64_t(msgs_[k][p][qq].ids.size());
+        (void)base;
+        for (size_t i = 0; i < m.ids.size(); ++i) {
+          const double lo = double(wlo[k][p][mb + i]), hi = double(whi[k][p][mb + i]);
+          if (!(hi >= lo)) continue;  // traced (trace.hpp:93)
+          MsgStat st;
+          st.id = m.ids[i];
+          st.dim = uint64_t(keys_[k].dim);
+          st.lo = lo;
+          st.hi = hi;
+          st.asq = keys_[k].bwd ? 1.0 : rx_asq_[p][q][i];
+          ps.msgs.push_back(st);
+        }
+        if (!ps.msgs.empty()) pairs.push_back(std::move(ps));
+      }
+    }
+    if (pairs.empty()) continue;
+    has[k] = 1;
+    jobs[k] = std::async(std::launch::async, [pairs = std::move(pairs), &cm, this]() {
+      SolveResult r = group_and_order(pairs, s_.group_size);
+      solve_exact(r, cm, s_.lambda);
+      return r;
+    });
+  }
+  // adopt: new bits for every message (all-8 default for untraced / absent pairs)
+  ++plan_version_;
+  for (size_t k = 0; k < keys_.size(); ++k) {
+    for (int64_t p = 0; p < P_; ++p)
+      for (int64_t q = 0; q < P_; ++q)
+        if (p != q) std::fill(msgs_[k][p][q].bits.begin(), msgs_[k][p][q].bits.end(), uint8_t(8));
+    if (!has[k]) continue;
+    SolveResult r = jobs[k].get();
+    for (const PlanPairG& pp : r.pairs) {
+      PairMsgs& m = msgs_[k][pp.src][pp.dst];
+      for (const Group& g : pp.groups)
+        for (uint32_t id : g.ids) {
+          auto it = std::lower_bound(m.ids.begin(), m.ids.end(), id);
+          m.bits[it - m.ids.begin()] = uint8_t(g.bits);
+        }
+    }
+  }
+  for (size_t k = 0; k < keys_.size(); ++k)
+    for (int64_t p = 0; p < P_; ++p)
+      for (int64_t q = 0; q < P_; ++q)
+        if (p != q) layout_pair(int(k), int(p), int(q));
+  arena_layout();
+  for (size_t k = 0; k < keys_.size(); ++k) {
+    upload_key_meta(int(k));
+    for (auto& up : parts_dev_) {  // reset windows (engine.hpp:855-860)
+      auto& S = up->snd[k];
+      if (S.n)
+        k_fill2<T><<<unsigned(ceil_div(S.n, 256)), 256, 0, s_main_>>>(S.wlo.p, T(INFINITY), S.whi.p,
+                                                                      T(-INFINITY), S.n);
+    }
+  }
+  QGNN_CUDA(cudaStreamSynchronize(s_main_));
+  resolve_seconds_ =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+template <typename T>
+void Engine<T>::get_weights(int l, void* out) {
+  QGNN_REQUIRE(l >= 0 && l < L_, QGNN_EINVAL, "get_weights: bad layer");
+  QGNN_CUDA(cudaMemcpy(out, w_.p + woff_[l], dims_[l] * dims_[l + 1] * sizeof(T),
+                       cudaMemcpyDeviceToHost));
+}
+
+template <typename T>
+void Engine<T>::set_weights(int l, const void* in) {
+  QGNN_REQUIRE(l >= 0 && l < L_, QGNN_EINVAL, "set_weights: bad layer");
+  QGNN_CUDA(cudaMemcpy(w_.p + woff_[l], in, dims_[l] * dims_[l + 1] * sizeof(T),
+                       cudaMemcpyHostToDevice));
+}
+
+template <typename T>
+void Engine<T>::info(int64_t* out) {
+  int64_t msgs = 0, max_owned = 0, max_halo = 0;
+  for (int64_t p = 0; p < P_; ++p)
+    for (int64_t q = 0; q < P_; ++q)
+      if (p != q) msgs += int64_t(parts_[p].remote_out[q].size());
+  for (auto& up : parts_dev_) {
+    max_owned = std::max(max_owned, up->view.num_owned);
+    max_halo = std::max(max_halo, up->view.num_remote);
+  }
+  out[0] = msgs;
+  out[1] = P_;
+  out[2] = p1_ - p0_;
+  out[3] = max_owned;
+  out[4] = max_halo;
+}
+
+template <typename T>
+int Engine<T>::kernel_stats(double* out, int n) {
+  const int m = std::min<int>(n / 3, QGNN_K_COUNT);
+  for (int c = 0; c < m; ++c) {
+    out[3 * c] = kst_[c].ms;
+    out[3 * c + 1] = kst_[c].launches;
+    out[3 * c + 2] = kst_[c].bytes;
+    kst_[c] = KStat{};
+  }
+  return m;
+}
+
+}  // namespace qgnn_b200
+
+using namespace qgnn_b200;
+
+struct qgnn_engine {
+  std::unique_ptr<EngineBase> impl;
+};
+
+extern "C" {
+
+int qgnn_engine_create(const qgnn_settings* s, int64_t n_nodes, const int64_t* adj_ptr,
+                       const int32_t* adj, const void* features, const int32_t* labels,
+                       const uint8_t* train, const uint8_t* val, const uint8_t* test,
+                       const uint32_t* owner, const void* nccl_unique_id, qgnn_engine** out) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(s && out && adj_ptr && adj && features, QGNN_EINVAL, "engine: null argument");
+  int count = 0;
+  QGNN_REQUIRE(cudaGetDeviceCount(&count) == cudaSuccess && count > 0, QGNN_ECUDA,
+               "no CUDA device: the B200 path has no CPU fallback");
+  auto* e = new qgnn_engine;
+  try {
+    if (s->dtype == QGNN_F64)
+      e->impl = std::make_unique<Engine<double>>(*s, n_nodes, adj_ptr, adj, features, labels, train,
+                                                 val, test, owner, nccl_unique_id);
+    else
+      e->impl = std::make_unique<Engine<float>>(*s, n_nodes, adj_ptr, adj, features, labels, train,
+                                                val, test, owner, nccl_unique_id);
+  } catch (...) {
+    delete e;
+    throw;
+  }
+  *out = e;
+  QGNN_API_END
+}
+
+int qgnn_engine_destroy(qgnn_engine* e) {
+  QGNN_API_BEGIN
+  delete e;
+  QGNN_API_END
+}
+
+int qgnn_engine_run_epoch(qgnn_engine* e, qgnn_epoch_metrics* m) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(e && m, QGNN_EINVAL, "null engine");
+  e->impl->run_epoch(m);
+  QGNN_API_END
+}
+
+int qgnn_engine_set_features(qgnn_engine* e, const void* f) {
+  QGNN_API_BEGIN
+  e->impl->set_features(f);
+  QGNN_API_END
+}
+
+int qgnn_engine_get_weights(qgnn_engine* e, int layer, void* out) {
+  QGNN_API_BEGIN
+  e->impl->get_weights(layer, out);
+  QGNN_API_END
+}
+
+int qgnn_engine_set_weights(qgnn_engine* e, int layer, const void* in) {
+  QGNN_API_BEGIN
+  e->impl->set_weights(layer, in);
+  QGNN_API_END
+}
+
+int qgnn_engine_info(qgnn_engine* e, int64_t* out5) {
+  QGNN_API_BEGIN
+  e->impl->info(out5);
+  QGNN_API_END
+}
+
+int qgnn_engine_kernel_stats(qgnn_engine* e, double* out, int n) {
+  try {
+    return e->impl->kernel_stats(out, n);
+  } catch (...) {
+    return -status_from_exception();
+  }
+}
+
+int qgnn_nccl_unique_id(void* out128) {
+  QGNN_API_BEGIN
+  ncclUniqueId id;
+  QGNN_NCCL(nccl().GetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof(id));
+  QGNN_API_END
+}
+
+}  // extern "C"

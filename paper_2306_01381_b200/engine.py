@@ -1,0 +1,172 @@
+"""Python handle on the C++ GPU engine (trainer/engine.hpp's Engine, B200 edition).
+
+    eng = Engine(graph, dims=[F, 256, 256, C], n_parts=8, bit_mode="adaptive")
+    m = eng.run_epoch()          # dict: train_loss, val_acc, ..., ms_total
+
+``graph`` is a dict with CSR ``adj_ptr`` (int64), ``adj`` (int32), ``features``
+(float32/float64, n x F), ``labels`` (int32) and ``train``/``val``/``test``
+masks (uint8), as produced by :func:`generate_planted` or the oracle's
+reference generator.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import F32, F64, WIRE_GPU, WIRE_REF, check, lib
+
+BIT_MODES = {"fp": 0, "fixed": 1, "uniform": 2, "adaptive": 3}
+KCLASSES = ["quant", "dequant", "spmm_fwd", "spmm_bwd", "partials", "gemm_fwd", "gemm_dgrad",
+            "gemm_wgrad", "elemwise", "exchange"]
+
+
+def generate_planted(nodes: int, n_edges: int, feat: int, classes: int, blocks: int,
+                     cross_frac: float, gamma: float = 2.5, sep: float = 1.0, seed: int = 1):
+    """Planted-block power-law graph (host C++, csrc/host_graph.cpp:gen_planted)."""
+    g = dict(adj_ptr=np.zeros(nodes + 1, np.int64), adj=np.zeros(2 * n_edges, np.int32),
+             features=np.zeros((nodes, feat), np.float32), labels=np.zeros(nodes, np.int32),
+             train=np.zeros(nodes, np.uint8), val=np.zeros(nodes, np.uint8),
+             test=np.zeros(nodes, np.uint8))
+    check(lib.qgnn_generate_planted(nodes, n_edges, feat, classes, blocks, cross_frac, gamma, sep,
+                                    seed, g["adj_ptr"].ctypes.data, g["adj"].ctypes.data,
+                                    g["features"].ctypes.data, g["labels"].ctypes.data,
+                                    g["train"].ctypes.data, g["val"].ctypes.data,
+                                    g["test"].ctypes.data))
+    g["owner"] = (np.arange(nodes, dtype=np.int64) // (-(-nodes // blocks))).astype(np.uint32)
+    return g
+
+
+def partition_stats(g, owner, n_parts):
+    out = np.zeros((n_parts, 5), np.int64)
+    ptr, adj = g["adj_ptr"], g["adj"]
+    own = np.ascontiguousarray(owner, np.uint32)
+    check(lib.qgnn_partition_stats(ptr.ctypes.data, adj.ctypes.data, len(ptr) - 1,
+                                   own.ctypes.data, n_parts, out.ctypes.data))
+    return out  # per part: owned, central, marginal, halo, sum |remote_out|
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    check(lib.qgnn_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class Engine:
+    def __init__(self, graph, dims: Sequence[int], n_parts: int, bit_mode: str = "fixed",
+                 fixed_bits: int = 8, seed: int = 7, sage: bool = False, lam: float = 0.5,
+                 group_size: int = 4, period: int = 50, lr: float = 0.01, theta: float = 3e-9,
+                 gamma: float = 5e-5, dtype: str = "f32", layout: Optional[int] = None,
+                 owner=None, rank: int = 0, world: int = 1, device: int = 0,
+                 nccl_id: Optional[bytes] = None, kstats: bool = False):
+        s = _lib.Settings()
+        s.sage = int(sage)
+        s.n_dims = len(dims)
+        for i, d in enumerate(dims):
+            s.dims[i] = int(d)
+        s.bit_mode = BIT_MODES[bit_mode]
+        s.fixed_bits = fixed_bits
+        s.lambda_ = lam
+        s.group_size = group_size
+        s.period = period
+        s.seed = seed
+        s.n_parts = n_parts
+        s.lr = lr
+        s.theta = theta
+        s.gamma = gamma
+        s.dtype = F64 if dtype == "f64" else F32
+        s.layout = (WIRE_REF if dtype == "f64" else WIRE_GPU) if layout is None else layout
+        s.rank, s.world, s.device = rank, world, device
+        s.overlap = 1
+        s.kstats = int(kstats)
+        self.settings = s
+        self.dims = list(dims)
+        self.np_dtype = np.float64 if dtype == "f64" else np.float32
+        feats = np.ascontiguousarray(graph["features"], self.np_dtype)
+        self._keep = dict(
+            ptr=np.ascontiguousarray(graph["adj_ptr"], np.int64),
+            adj=np.ascontiguousarray(graph["adj"], np.int32), feats=feats,
+            labels=np.ascontiguousarray(graph["labels"], np.int32),
+            train=np.ascontiguousarray(graph["train"], np.uint8),
+            val=np.ascontiguousarray(graph["val"], np.uint8),
+            test=np.ascontiguousarray(graph["test"], np.uint8),
+            owner=None if owner is None else np.ascontiguousarray(owner, np.uint32))
+        k = self._keep
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = (C.c_char * 128).from_buffer_copy(nccl_id)
+        h = C.c_void_p()
+        check(lib.qgnn_engine_create(
+            C.byref(s), len(k["ptr"]) - 1, k["ptr"].ctypes.data, k["adj"].ctypes.data,
+            feats.ctypes.data, k["labels"].ctypes.data, k["train"].ctypes.data,
+            k["val"].ctypes.data, k["test"].ctypes.data,
+            None if k["owner"] is None else k["owner"].ctypes.data,
+            None if idbuf is None else C.cast(idbuf, C.c_void_p), C.byref(h)))
+        self._h = h
+        del self._keep["adj"]  # the engine keeps its own copies
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.qgnn_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def run_epoch(self) -> dict:
+        m = _lib.EpochMetrics()
+        check(lib.qgnn_engine_run_epoch(self._h, C.byref(m)))
+        return m.as_dict()
+
+    def set_features(self, feats: np.ndarray):
+        f = np.ascontiguousarray(feats, self.np_dtype)
+        check(lib.qgnn_engine_set_features(self._h, f.ctypes.data))
+
+    def weights(self):
+        out = []
+        for l in range(len(self.dims) - 1):
+            w = np.zeros((self.dims[l], self.dims[l + 1]), self.np_dtype)
+            check(lib.qgnn_engine_get_weights(self._h, l, w.ctypes.data))
+            out.append(w)
+        return out
+
+    def set_weights(self, ws):
+        for l, w in enumerate(ws):
+            w = np.ascontiguousarray(w, self.np_dtype)
+            check(lib.qgnn_engine_set_weights(self._h, l, w.ctypes.data))
+
+    def info(self) -> dict:
+        out = np.zeros(5, np.int64)
+        check(lib.qgnn_engine_info(self._h, out.ctypes.data))
+        return dict(messages_per_tensor=int(out[0]), n_parts=int(out[1]),
+                    parts_on_rank=int(out[2]), max_owned=int(out[3]), max_halo=int(out[4]))
+
+    def kernel_stats(self) -> dict:
+        out = np.zeros(3 * len(KCLASSES))
+        n = lib.qgnn_engine_kernel_stats(self._h, out.ctypes.data, len(out))
+        if n < 0:
+            check(-n)
+        return {KCLASSES[i]: dict(ms=out[3 * i], launches=int(out[3 * i + 1]),
+                                  bytes=out[3 * i + 2]) for i in range(n)}
+
+
+def smoke_epoch():
+    """Tiny fp32 engine run (2 partitions, quantized 8-bit exchange) on cuda:0."""
+    from oracle import port  # checker only
+    g = generate_planted(2000, 12000, 16, 4, 2, 0.05, seed=3)
+    eng = Engine(g, [16, 32, 32, 4], n_parts=2, bit_mode="fixed", fixed_bits=8, seed=5)
+    m1 = eng.run_epoch()
+    m2 = eng.run_epoch()
+    assert np.isfinite(m1["train_loss"]) and m2["train_loss"] < m1["train_loss"] * 1.5
+    assert m1["bytes_total"] > 0 and m1["msgs_b8"] > 0
+    # initial weights follow GnnModel::init (model.hpp:27-41) exactly
+    eng2 = Engine(g, [16, 32, 32, 4], n_parts=2, bit_mode="fixed", seed=5)
+    w0 = eng2.weights()[0]
+    key = port.stream(5, 0x77, 0)
+    a = np.sqrt(6.0 / 48)
+    exp = np.array([(2.0 * port.draw_double(key, i + 1) - 1.0) * a for i in range(16 * 32)])
+    assert np.allclose(w0.reshape(-1), exp.astype(np.float32))
+    eng.close()
+    eng2.close()
