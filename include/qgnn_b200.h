@@ -220,8 +220,9 @@ int qgnn_engine_set_features(qgnn_engine* e, const void* features);
 /* Weights of layer l (din x dout, settings dtype) to host memory. */
 int qgnn_engine_get_weights(qgnn_engine* e, int layer, void* out);
 int qgnn_engine_set_weights(qgnn_engine* e, int layer, const void* in);
-/* Static facts: [num_messages_per_tensor, n_parts, parts_on_rank, max_owned, max_halo]. */
-int qgnn_engine_info(qgnn_engine* e, int64_t* out5);
+/* Facts: [fwd messages per tensor (all pairs), n_parts, parts_on_rank, max_owned,
+ * max_halo, kernels of ours launched in the last epoch]. */
+int qgnn_engine_info(qgnn_engine* e, int64_t* out6);
 /* Per kernel class k (QGNN_K_*), accumulated since the last call (needs
  * settings.kstats): out[3k] = total device ms, out[3k+1] = launches,
  * out[3k+2] = algorithmic bytes (SURVEY.md §8d model).  Returns the number

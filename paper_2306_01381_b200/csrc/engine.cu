@@ -253,7 +253,7 @@ class Engine final : public EngineBase {
   void arena_layout();
   // profiling
   void kbegin(int cls);
-  void kend(int cls, double bytes, cudaStream_t s);
+  void kend(int cls, double bytes, cudaStream_t s, int nk = 1);
   void flush_kstats();
 
   qgnn_settings s_;
@@ -293,6 +293,9 @@ class Engine final : public EngineBase {
   size_t ev_next_ = 0;
   KStat kst_[QGNN_K_COUNT];
   int cur_cls_ = -1;
+  int64_t launches_ = 0, launches_last_ = 0;
+  T* pinned_ = nullptr;
+  size_t pinned_elems_ = 0;
   // per-epoch message counters
   uint64_t msgs_b_[4] = {0, 0, 0, 0};
   double resolve_seconds_ = 0;
@@ -313,7 +316,8 @@ void Engine<T>::kbegin(int cls) {
 }
 
 template <typename T>
-void Engine<T>::kend(int cls, double bytes, cudaStream_t s) {
+void Engine<T>::kend(int cls, double bytes, cudaStream_t s, int nk) {
+  launches_ += nk;  // kernels of ours inside the region (always counted)
   if (!s_.kstats) return;
   QGNN_CUDA(cudaEventRecord(ev_pool_[ev_next_].second, s));
   ev_used_.emplace_back(cls, ev_next_, bytes);
@@ -526,6 +530,7 @@ Engine<T>::~Engine() {
     cudaEventDestroy(e.second);
   }
   if (comm_) nccl().CommDestroy(comm_);
+  if (pinned_) cudaFreeHost(pinned_);
   if (ev_a_) cudaEventDestroy(ev_a_);
   if (ev_b_) cudaEventDestroy(ev_b_);
   if (ev_x_) cudaEventDestroy(ev_x_);
@@ -537,18 +542,38 @@ Engine<T>::~Engine() {
 
 template <typename T>
 void Engine<T>::set_features(const void* f) {
-  const int64_t F = dims_[0];
+  const int64_t F = dims_[0], ld = ld_of(F);
   const T* src = static_cast<const T*>(f);
-  for (auto& up : parts_dev_) {
-    PartDev& D = *up;
-    const int64_t no = D.view.num_owned, ld = ld_of(F);
-    std::vector<T> buf(no * ld, T(0));
-    for (int64_t g = 0; g < no; ++g)
-      std::memcpy(&buf[g * ld], src + static_cast<int64_t>(D.view.row_node[g]) * F, F * sizeof(T));
-    QGNN_CUDA(cudaMemcpyAsync(D.h[0].p, buf.data(), buf.size() * sizeof(T), cudaMemcpyHostToDevice,
-                              s_main_));
-    QGNN_CUDA(cudaStreamSynchronize(s_main_));
+  size_t total = 0;
+  for (auto& up : parts_dev_) total += size_t(up->view.num_owned * ld);
+  if (total > pinned_elems_) {
+    if (pinned_) cudaFreeHost(pinned_);
+    QGNN_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&pinned_), total * sizeof(T), cudaHostAllocDefault));
+    std::memset(pinned_, 0, total * sizeof(T));
+    pinned_elems_ = total;
   }
+  // gather rows into partition order (threads), then one pinned H2D per partition
+  std::vector<std::future<void>> jobs;
+  size_t o = 0;
+  for (auto& up : parts_dev_) {
+    PartDev* D = up.get();
+    T* dst = pinned_ + o;
+    o += size_t(D->view.num_owned * ld);
+    jobs.push_back(std::async(std::launch::async, [D, dst, src, F, ld] {
+      const int64_t no = D->view.num_owned;
+      for (int64_t g = 0; g < no; ++g)
+        std::memcpy(dst + g * ld, src + int64_t(D->view.row_node[g]) * F, F * sizeof(T));
+    }));
+  }
+  o = 0;
+  for (size_t i = 0; i < parts_dev_.size(); ++i) {
+    jobs[i].get();
+    PartDev& D = *parts_dev_[i];
+    QGNN_CUDA(cudaMemcpyAsync(D.h[0].p, pinned_ + o, D.view.num_owned * ld * sizeof(T),
+                              cudaMemcpyHostToDevice, s_main_));
+    o += size_t(D.view.num_owned * ld);
+  }
+  QGNN_CUDA(cudaStreamSynchronize(s_main_));
 }
 
 // Message lists of every ordered pair and key (engine.hpp:142-143, 585-587, 683-687);
@@ -795,7 +820,7 @@ void Engine<T>::exchange(int k) {
                             s_comm_));
     }
   QGNN_NCCL(nccl().GroupEnd());
-  kend(QGNN_K_EXCHANGE, bytes, s_comm_);
+  kend(QGNN_K_EXCHANGE, bytes, s_comm_, 0);
   QGNN_CUDA(cudaEventRecord(ev_x_, s_comm_));
 }
 
@@ -886,7 +911,8 @@ void Engine<T>::loss_phase() {
     if (D.n_test)
       QGNN_CALL(qgnn_count_correct(ctx_, dtype_, D.h[L_].p, ldc, C, D.labels.p, D.test_rows.p,
                                    D.n_test, D.correct.p + 1, s_main_));
-    kend(QGNN_K_ELEMWISE, double(D.view.num_owned) * C * sizeof(T) * 2, s_main_);
+    kend(QGNN_K_ELEMWISE, double(D.view.num_owned) * C * sizeof(T) * 2, s_main_,
+         (D.n_train ? 2 : 0) + (D.n_val ? 1 : 0) + (D.n_test ? 1 : 0));
   }
 }
 
@@ -947,7 +973,8 @@ void Engine<T>::backward_layer(int l) {
     QGNN_CALL(qgnn_dense_weight_grad(ctx_, dtype_, D.hagg[t].p, ldi, dz, ldo, din, dout,
                                      dtype_ == QGNN_F64 ? D.ref_order.p : nullptr, 0, no, 0, wg,
                                      s_main_));
-    kend(QGNN_K_GEMM_WGRAD, double(no) * (din + dout) * sizeof(T), s_main_);
+    kend(QGNN_K_GEMM_WGRAD, double(no) * (din + dout) * sizeof(T), s_main_,
+         dtype_ == QGNN_F64 ? 1 : 2);
     kbegin(QGNN_K_SPMM_BWD);
     QGNN_CALL(qgnn_csr_aggregate(ctx_, dtype_, din, D.gbar.p, ldi, nullptr, 0, D.self_alpha.p,
                                  D.lptr.p, D.lcol.p, D.labwd.p, nullptr, nullptr, nullptr, nullptr,
@@ -995,7 +1022,8 @@ void Engine<T>::backward_last() {
     QGNN_CALL(qgnn_dense_weight_grad(ctx_, dtype_, D.hagg[0].p, ldi, dz, ldo, din, dout,
                                      dtype_ == QGNN_F64 ? D.ref_order.p : nullptr, 0, no, 0,
                                      wgrad_all_.p + D.id * nparams_ + woff_[0], s_main_));
-    kend(QGNN_K_GEMM_WGRAD, double(no) * (din + dout) * sizeof(T), s_main_);
+    kend(QGNN_K_GEMM_WGRAD, double(no) * (din + dout) * sizeof(T), s_main_,
+         dtype_ == QGNN_F64 ? 1 : 2);
   }
 }
 
@@ -1017,13 +1045,14 @@ void Engine<T>::step() {
   const double bc2 = 1.0 - std::pow(b2, double(adam_t_));
   QGNN_CALL(qgnn_adam_step(ctx_, dtype_, w_.p, adam_m_.p, adam_v_.p, wsum_.p, nparams_, s_.lr, b1,
                            b2, 1e-8, bc1, bc2, s_main_));
-  kend(QGNN_K_ELEMWISE, double(nparams_) * sizeof(T) * (P_ + 6), s_main_);
+  kend(QGNN_K_ELEMWISE, double(nparams_) * sizeof(T) * (P_ + 6), s_main_, 2);
 }
 
 template <typename T>
 void Engine<T>::run_epoch(qgnn_epoch_metrics* m) {
   ++epoch_;
   QGNN_CUDA(cudaSetDevice(s_.device));
+  launches_ = 0;
   prepare_epoch();
   QGNN_CUDA(cudaEventRecord(ev_a_, s_main_));
   for (int64_t l = 1; l <= L_; ++l) forward_layer(int(l));
@@ -1037,6 +1066,7 @@ void Engine<T>::run_epoch(qgnn_epoch_metrics* m) {
   QGNN_CUDA(cudaEventElapsedTime(&ms, ev_a_, ev_b_));
   QGNN_CALL(qgnn_ctx_check(ctx_, s_main_));
   flush_kstats();
+  launches_last_ = launches_;
 
   // loss / accuracy (engine.hpp:393-397, 803-849)
   std::vector<double> loss(P_, 0.0);
@@ -1248,6 +1278,7 @@ void Engine<T>::info(int64_t* out) {
   out[2] = p1_ - p0_;
   out[3] = max_owned;
   out[4] = max_halo;
+  out[5] = launches_last_;
 }
 
 template <typename T>

@@ -138,10 +138,11 @@ class Engine:
             check(lib.qgnn_engine_set_weights(self._h, l, w.ctypes.data))
 
     def info(self) -> dict:
-        out = np.zeros(5, np.int64)
+        out = np.zeros(6, np.int64)
         check(lib.qgnn_engine_info(self._h, out.ctypes.data))
         return dict(messages_per_tensor=int(out[0]), n_parts=int(out[1]),
-                    parts_on_rank=int(out[2]), max_owned=int(out[3]), max_halo=int(out[4]))
+                    parts_on_rank=int(out[2]), max_owned=int(out[3]), max_halo=int(out[4]),
+                    launches_last_epoch=int(out[5]))
 
     def kernel_stats(self) -> dict:
         out = np.zeros(3 * len(KCLASSES))
