@@ -65,10 +65,21 @@ struct qgnn_ctx {
   int* d_err = nullptr;          // device error word
   void* scratch = nullptr;       // split-K workspace
   size_t scratch_bytes = 0;
+  void* gemm_b = nullptr;        // pre-split weight operand of the tcgen05 GEMM
+  size_t gemm_b_bytes = 0;
   int num_sms = 148;
 };
 
 namespace qgnn_b200 {
 // Grows ctx->scratch to at least `bytes` (synchronous; call outside capture).
 void* ctx_scratch(qgnn_ctx* ctx, size_t bytes);
+void* ctx_gemm_b(qgnn_ctx* ctx, size_t bytes);
+// tcgen05 GEMMs (gemm_tc.cu)
+void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int wcols, int N,
+                  int K, int transpose_w, int64_t n_rows, int relu, float* out, int64_t ldo,
+                  cudaStream_t s);
+float* tc_gemm_wgrad_partials(qgnn_ctx* ctx, const float* A, int64_t lda, const float* B,
+                              int64_t ldb, int M, int N, int64_t n_rows, int* splits_out,
+                              cudaStream_t s);
+bool use_tc_gemm();
 }  // namespace qgnn_b200

@@ -1,6 +1,7 @@
 // ctx.cu — context, error word, thread-local error messages, RNG entry points.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -44,6 +45,25 @@ void* ctx_scratch(qgnn_ctx* ctx, size_t bytes) {
   QGNN_CUDA(cudaMalloc(&ctx->scratch, bytes));
   ctx->scratch_bytes = bytes;
   return ctx->scratch;
+}
+
+void* ctx_gemm_b(qgnn_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->gemm_b_bytes) return ctx->gemm_b;
+  if (ctx->gemm_b) QGNN_CUDA(cudaFree(ctx->gemm_b));
+  ctx->gemm_b = nullptr;
+  ctx->gemm_b_bytes = 0;
+  QGNN_CUDA(cudaMalloc(&ctx->gemm_b, bytes));
+  ctx->gemm_b_bytes = bytes;
+  return ctx->gemm_b;
+}
+
+// tcgen05 GEMM unless QGNN_GEMM=simt (debug / A-B comparison switch)
+bool use_tc_gemm() {
+  static const bool tc = [] {
+    const char* e = std::getenv("QGNN_GEMM");
+    return !(e && std::string(e) == "simt");
+  }();
+  return tc;
 }
 
 // Maps a latched device error word onto the reference's exception taxonomy.
@@ -103,6 +123,7 @@ int qgnn_ctx_destroy(qgnn_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->d_err) cudaFree(ctx->d_err);
   if (ctx->scratch) cudaFree(ctx->scratch);
+  if (ctx->gemm_b) cudaFree(ctx->gemm_b);
   delete ctx;
   QGNN_API_END
 }

@@ -319,6 +319,10 @@ int qgnn_dense_forward(qgnn_ctx* ctx, int dtype, const void* A, int64_t lda, con
     k_dfwd_exact<<<grid1(n_rows * dout, 256), 256, 0, s>>>(
         static_cast<const double*>(A), lda, static_cast<const double*>(W), int(din), int(dout),
         rows, row_begin, n_rows, relu, static_cast<double*>(out), ld_out);
+  } else if (!rows && use_tc_gemm() && dout <= 256) {
+    tc_gemm_rows(ctx, static_cast<const float*>(A) + row_begin * lda, lda,
+                 static_cast<const float*>(W), int(dout), int(dout), int(din), 1, n_rows, relu,
+                 static_cast<float*>(out) + row_begin * ld_out, ld_out, s);
   } else {
     dim3 g(static_cast<unsigned>(ceil_div(n_rows, BM)), static_cast<unsigned>(ceil_div(dout, BN)), 1);
     k_sgemm<false, false><<<g, 256, 0, s>>>(int(n_rows), int(dout), int(din),
@@ -342,6 +346,10 @@ int qgnn_dense_input_grad(qgnn_ctx* ctx, int dtype, const void* A, int64_t lda, 
     k_dgrad_exact<<<grid1(n_rows * din, 256), 256, 0, s>>>(
         static_cast<const double*>(A), lda, static_cast<const double*>(W), int(din), int(dout),
         rows, row_begin, n_rows, static_cast<double*>(out), ld_out);
+  } else if (!rows && use_tc_gemm() && din <= 256) {
+    tc_gemm_rows(ctx, static_cast<const float*>(A) + row_begin * lda, lda,
+                 static_cast<const float*>(W), int(dout), int(din), int(dout), 0, n_rows, 0,
+                 static_cast<float*>(out) + row_begin * ld_out, ld_out, s);
   } else {
     dim3 g(static_cast<unsigned>(ceil_div(n_rows, BM)), static_cast<unsigned>(ceil_div(din, BN)), 1);
     k_sgemm<false, true><<<g, 256, 0, s>>>(int(n_rows), int(din), int(dout),
@@ -365,6 +373,13 @@ int qgnn_dense_weight_grad(qgnn_ctx* ctx, int dtype, const void* A, int64_t lda,
     k_wgrad_exact<<<grid1(m * n, 128), 128, 0, s>>>(
         static_cast<const double*>(A), lda, static_cast<const double*>(B), ldb, int(m), int(n),
         rows, row_begin, n_rows, accumulate, static_cast<double*>(out));
+  } else if (!rows && use_tc_gemm() && n <= 256 && (lda * 4) % 16 == 0 && (ldb * 4) % 16 == 0) {
+    int splits = 0;
+    const float* part = tc_gemm_wgrad_partials(
+        ctx, static_cast<const float*>(A) + row_begin * lda, lda,
+        static_cast<const float*>(B) + row_begin * ldb, ldb, int(m), int(n), n_rows, &splits, s);
+    k_splitk_reduce<<<grid1(m * n, 256), 256, 0, s>>>(part, splits, m * n,
+                                                       static_cast<float*>(out), accumulate);
   } else {
     // split K (rows) so that tiles x splits ~ 4 waves of the SMs
     const int64_t tiles = ceil_div(m, BM) * ceil_div(n, BN);

@@ -1,0 +1,484 @@
+// gemm_tc.cu — K5 dense transform on the 5th-gen tensor cores (tcgen05, sm_100a).
+//
+// fp32-faithful GEMM via the 3xTF32 split: every operand x = hi + lo with
+// hi = x with the low 13 mantissa bits cleared (exactly representable in
+// TF32) and lo = x - hi; D = Ahi*Bhi + Ahi*Blo + Alo*Bhi accumulated in fp32
+// in TMEM (relative error ~2^-21, vs ~2^-11 for plain TF32).
+//
+// Pipeline (one persistent CTA per SM, 12 warps):
+//   warp 0      TMA producer: A tile (and, for the weight gradient, B tile)
+//               for each 32-deep K chunk into a 2-stage smem ring (SW128)
+//   warp 1      MMA issuer: one elected thread issues 4 k-steps x 3 products of
+//               tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=BN) per chunk
+//   warp 2      TMEM allocator (2 x BN fp32 accumulator columns, double buffer)
+//   warps 4-7   epilogue: tcgen05.ld 32x32b -> ReLU -> global stores, while the
+//               MMA warp already accumulates the next tile in the other buffer
+//   warps 8-11  converters: split the landed fp32 tile into hi (in place) and
+//               lo (second buffer), fence.proxy.async, release the stage
+// Shapes: forward z = A W (A rows x din, K-major), input gradient dz W^T
+// (K-major), weight gradient A^T B over rows (both operands MN-major, split-K
+// over rows with a fixed-order reduction).  B for the first two is the small
+// weight matrix, pre-split into padded hi/lo K-major copies by k_prep_b.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace qgnn_b200 {
+namespace tc {
+
+constexpr int kBM = 128;
+constexpr int kBK = 32;  // fp32 elements per 128-byte swizzle row
+constexpr int kStages = 2;
+constexpr int kThreads = 384;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LAB_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra LAB_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// SW128 shared-memory matrix descriptor (tcgen05 "version 1")
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t{1} << 46;  // version
+  d |= uint64_t{2} << 61;  // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+
+// in-place hi + separate lo for `n16` 16-byte vectors, strided over `nthr` threads
+__device__ __forceinline__ void split_tile(float4* buf, float4* lo, int n16, int t, int nthr) {
+  for (int i = t; i < n16; i += nthr) {
+    float4 v = buf[i];
+    float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+    buf[i] = h;
+    lo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+  }
+}
+
+struct Params {
+  int M, N, K;          // logical GEMM (C[M x N] = A[M x K] B[K x N])
+  int BN;               // N tile (multiple of 16 / 32 for MN-major B), <= 256
+  int tmem_cols;        // columns per accumulator buffer (pow2 >= BN)
+  int m_tiles, splits, k_chunks, chunks_per_split;
+  float* out;
+  int64_t ldo;
+  int relu;
+};
+
+// kMN = false: A K-major (tmA box {32, 128}), B/Blo K-major prepared (box {32, BN})
+// kMN = true : A MN-major (box {32 m, 32 k}), B MN-major (box {32 n, 32 k}); both split here
+template <bool kMN>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmBlo, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int a_bytes = kBM * kBK * 4;        // 16 KB
+  const int b_bytes = p.BN * kBK * 4;       // BN x 128 B
+  const int stage_bytes = 2 * a_bytes + 2 * b_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * stage_bytes);
+  uint64_t* full = bars;                 // [kStages]
+  uint64_t* conv = bars + kStages;       // [kStages]
+  uint64_t* empty = bars + 2 * kStages;  // [kStages]
+  uint64_t* tfull = bars + 3 * kStages;  // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n_tiles = p.m_tiles * p.splits;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(2 * p.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto tile_chunks = [&](int tile, int& m0, int& kc0, int& kc1, int& split) {
+    const int mt = tile % p.m_tiles;
+    split = tile / p.m_tiles;
+    m0 = mt * kBM;
+    kc0 = split * p.chunks_per_split;
+    kc1 = min(p.k_chunks, kc0 + p.chunks_per_split);
+  };
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        int m0, kc0, kc1, split;
+        tile_chunks(tile, m0, kc0, kc1, split);
+        for (int kc = kc0; kc < kc1; ++kc) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * stage_bytes;
+          uint8_t* A = st;
+          uint8_t* B = st + 2 * a_bytes;
+          uint8_t* Blo = B + b_bytes;
+          const int k0 = kc * kBK;
+          if (!kMN) {
+            mbar_expect_tx(&full[s], a_bytes + 2 * b_bytes);
+            tma_load_2d(A, &tmA, &full[s], k0, m0);
+            tma_load_2d(B, &tmB, &full[s], k0, 0);
+            tma_load_2d(Blo, &tmBlo, &full[s], k0, 0);
+          } else {
+            mbar_expect_tx(&full[s], a_bytes + b_bytes);
+            for (int j = 0; j < kBM / 32; ++j) tma_load_2d(A + j * 4096, &tmA, &full[s], m0 + 32 * j, k0);
+            for (int j = 0; j < p.BN / 32; ++j) tma_load_2d(B + j * 4096, &tmB, &full[s], 32 * j, k0);
+          }
+          if (++s == kStages) s = 0, ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((kMN ? 1u : 0u) << 15) |
+                           ((kMN ? 1u : 0u) << 16) | (uint32_t(p.BN >> 3) << 17) |
+                           (uint32_t(kBM >> 4) << 24);
+    int s = 0;
+    uint32_t ph = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+      int m0, kc0, kc1, split;
+      tile_chunks(tile, m0, kc0, kc1, split);
+      const int acc = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      mbar_wait(&tempty[acc], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + uint32_t(acc * p.tmem_cols);
+      bool first = true;
+      for (int kc = kc0; kc < kc1; ++kc) {
+        mbar_wait(&full[s], ph);
+        mbar_wait(&conv[s], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          uint8_t* st = smem + s * stage_bytes;
+          const uint32_t aH = smem_u32(st), aL = smem_u32(st + a_bytes);
+          const uint32_t bH = smem_u32(st + 2 * a_bytes), bL = smem_u32(st + 2 * a_bytes + b_bytes);
+#pragma unroll
+          for (int j = 0; j < kBK / 8; ++j) {
+            uint64_t dAh, dAl, dBh, dBl;
+            if (!kMN) {  // K-major: advance 8 fp32 = 32 B inside the 128 B swizzle row
+              dAh = sdesc(aH + 32 * j, 16, 1024);
+              dAl = sdesc(aL + 32 * j, 16, 1024);
+              dBh = sdesc(bH + 32 * j, 16, 1024);
+              dBl = sdesc(bL + 32 * j, 16, 1024);
+            } else {  // MN-major: 8 K rows = one 1024 B atom; 32-element MN groups 4 KB apart
+              dAh = sdesc(aH + 1024 * j, 4096, 1024);
+              dAl = sdesc(aL + 1024 * j, 4096, 1024);
+              dBh = sdesc(bH + 1024 * j, 4096, 1024);
+              dBl = sdesc(bL + 1024 * j, 4096, 1024);
+            }
+            tc_mma(d, dAh, dBh, idesc, first ? 0u : 1u);
+            first = false;
+            tc_mma(d, dAh, dBl, idesc, 1u);
+            tc_mma(d, dAl, dBh, idesc, 1u);
+          }
+          tc_commit(&empty[s]);
+        }
+        __syncwarp();
+        if (++s == kStages) s = 0, ph ^= 1;
+      }
+      if (lane == 0) tc_commit(&tfull[acc]);
+      __syncwarp();
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------- epilogue
+    const int q = warp & 3;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+      int m0, kc0, kc1, split;
+      tile_chunks(tile, m0, kc0, kc1, split);
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + 32 * q + lane;
+      float* orow = p.out + (kMN ? int64_t(split) * p.M * p.N : 0) + int64_t(row) * p.ldo;
+      for (int c = 0; c < p.BN; c += 16) {
+        float v[16];
+        tmem_ld16(tmem_base + uint32_t(acc * p.tmem_cols + c) + (uint32_t(32 * q) << 16), v);
+        if (row < p.M) {
+          if (p.relu) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = v[i] > 0.f ? v[i] : 0.f;
+          }
+          if (c + 16 <= p.N && (p.ldo & 3) == 0) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+              *reinterpret_cast<float4*>(orow + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          } else {
+            for (int i = 0; i < 16 && c + i < p.N; ++i) orow[c + i] = v[i];
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  } else if (warp >= 8) {
+    // ---------------- converters
+    const int t = threadIdx.x - 256;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      int m0, kc0, kc1, split;
+      tile_chunks(tile, m0, kc0, kc1, split);
+      for (int kc = kc0; kc < kc1; ++kc) {
+        mbar_wait(&full[s], ph);
+        uint8_t* st = smem + s * stage_bytes;
+        split_tile(reinterpret_cast<float4*>(st), reinterpret_cast<float4*>(st + a_bytes),
+                   a_bytes / 16, t, 128);
+        if (kMN)
+          split_tile(reinterpret_cast<float4*>(st + 2 * a_bytes),
+                     reinterpret_cast<float4*>(st + 2 * a_bytes + b_bytes), b_bytes / 16, t, 128);
+        fence_proxy_async();
+        mbar_arrive(&conv[s]);
+        if (++s == kStages) s = 0, ph ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(2 * p.tmem_cols));
+  }
+}
+
+// B(n, k) for the K-major paths, padded to Kp columns and split into hi / lo:
+//   transpose == 1: B(n, k) = W[k][n]  (forward: W is K x N)
+//   transpose == 0: B(n, k) = W[n][k]  (input gradient: W is N x K)
+__global__ void k_prep_b(const float* __restrict__ W, int wcols, int N, int K, int Kp, int transpose,
+                         float* __restrict__ bhi, float* __restrict__ blo) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= int64_t(N) * Kp) return;
+  const int n = int(i / Kp), k = int(i % Kp);
+  float x = 0.f;
+  if (k < K) x = transpose ? W[int64_t(k) * wcols + n] : W[int64_t(n) * wcols + k];
+  const float h = tf32_hi(x);
+  bhi[i] = h;
+  blo[i] = x - h;
+}
+
+}  // namespace tc
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  QGNN_REQUIRE(fn, QGNN_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 2D fp32 tensor map: inner (contiguous) extent x outer extent, row pitch in elements
+CUtensorMap make_map(const float* base, uint64_t inner, uint64_t outer, uint64_t pitch_elems,
+                     uint32_t box_inner, uint32_t box_outer) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {pitch_elems * 4};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  QGNN_REQUIRE((pitch_elems * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(base) & 15) == 0,
+               QGNN_EINVAL, "tensor map: 16-byte aligned base/pitch required");
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base),
+                                 dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  QGNN_REQUIRE(r == CUDA_SUCCESS, QGNN_ECUDA, "cuTensorMapEncodeTiled failed");
+  return m;
+}
+
+int pow2_cols(int bn) {
+  int c = 32;
+  while (c < bn) c <<= 1;
+  return c;
+}
+
+size_t smem_bytes(int BN) {
+  return size_t(tc::kStages) * (2 * tc::kBM * tc::kBK * 4 + 2 * BN * tc::kBK * 4) + 1024 + 256;
+}
+
+template <bool kMN>
+void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo, const tc::Params& p,
+            int num_sms, cudaStream_t s) {
+  const size_t sm = smem_bytes(p.BN);
+  static bool attr_set = false;
+  if (!attr_set) {
+    QGNN_CUDA(cudaFuncSetAttribute(tc::k_tc_gemm<kMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem_bytes(256))));
+    attr_set = true;
+  }
+  const int tiles = p.m_tiles * p.splits;
+  const int grid = std::max(1, std::min(tiles, num_sms));
+  tc::k_tc_gemm<kMN><<<grid, tc::kThreads, sm, s>>>(a, b, blo, p);
+  check_launch("k_tc_gemm");
+}
+}  // namespace
+
+// C[rows x N] = A[rows x K] B  with B(n,k) from W (see k_prep_b); relu optional.
+void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int wcols, int N,
+                  int K, int transpose_w, int64_t n_rows, int relu, float* out, int64_t ldo,
+                  cudaStream_t s) {
+  QGNN_REQUIRE(N <= 256 && K <= 4096, QGNN_EINVAL, "tc_gemm: N must be <= 256");
+  const int BN = int(round_up(N, 16));
+  const int Kp = int(round_up(K, 4));
+  float* bhi = static_cast<float*>(ctx_gemm_b(ctx, size_t(2) * BN * Kp * sizeof(float)));
+  float* blo = bhi + size_t(BN) * Kp;
+  tc::k_prep_b<<<unsigned(ceil_div(int64_t(N) * Kp, 256)), 256, 0, s>>>(W, wcols, N, K, Kp,
+                                                                        transpose_w, bhi, blo);
+  const CUtensorMap ta = make_map(A, uint64_t(K), uint64_t(n_rows), uint64_t(lda), 32, tc::kBM);
+  const CUtensorMap tb = make_map(bhi, uint64_t(Kp), uint64_t(N), uint64_t(Kp), 32, uint32_t(BN));
+  const CUtensorMap tbl = make_map(blo, uint64_t(Kp), uint64_t(N), uint64_t(Kp), 32, uint32_t(BN));
+  tc::Params p{};
+  p.M = int(n_rows);
+  p.N = N;
+  p.K = K;
+  p.BN = BN;
+  p.tmem_cols = pow2_cols(BN);
+  p.m_tiles = int(ceil_div(n_rows, tc::kBM));
+  p.splits = 1;
+  p.k_chunks = int(ceil_div(K, tc::kBK));
+  p.chunks_per_split = p.k_chunks;
+  p.out = out;
+  p.ldo = ldo;
+  p.relu = relu;
+  launch<false>(ta, tb, tbl, p, ctx->num_sms, s);
+}
+
+// Partial tiles of out[M x N] = A[rows x M]^T B[rows x N], split-K over rows:
+// returns the workspace holding *splits consecutive M x N partial products
+// (the caller reduces them in fixed order).
+float* tc_gemm_wgrad_partials(qgnn_ctx* ctx, const float* A, int64_t lda, const float* B,
+                              int64_t ldb, int M, int N, int64_t n_rows, int* splits_out,
+                              cudaStream_t s) {
+  QGNN_REQUIRE(N <= 256, QGNN_EINVAL, "tc_gemm_wgrad: N must be <= 256");
+  const int BN = int(round_up(N, 32));
+  const int m_tiles = int(ceil_div(M, tc::kBM));
+  const int k_chunks = int(ceil_div(std::max<int64_t>(n_rows, 1), tc::kBK));
+  int splits = std::max(1, std::min(k_chunks, ctx->num_sms / std::max(1, m_tiles)));
+  const int cps = int(ceil_div(k_chunks, splits));
+  splits = int(ceil_div(k_chunks, cps));
+  float* part = static_cast<float*>(ctx_scratch(ctx, sizeof(float) * size_t(splits) * M * N));
+  const CUtensorMap ta = make_map(A, uint64_t(M), uint64_t(n_rows), uint64_t(lda), 32, 32);
+  const CUtensorMap tb = make_map(B, uint64_t(N), uint64_t(n_rows), uint64_t(ldb), 32, 32);
+  tc::Params p{};
+  p.M = M;
+  p.N = N;
+  p.K = int(n_rows);
+  p.BN = BN;
+  p.tmem_cols = pow2_cols(BN);
+  p.m_tiles = m_tiles;
+  p.splits = splits;
+  p.k_chunks = k_chunks;
+  p.chunks_per_split = cps;
+  p.out = part;
+  p.ldo = N;
+  p.relu = 0;
+  launch<true>(ta, tb, tb, p, ctx->num_sms, s);
+  *splits_out = splits;
+  return part;
+}
+
+}  // namespace qgnn_b200
