@@ -16,8 +16,10 @@
 //   warps 8-11  converters: split the landed fp32 tile into hi (in place) and
 //               lo (second buffer), fence.proxy.async, release the stage
 // Shapes: forward z = A W (A rows x din, K-major), input gradient dz W^T
-// (K-major), weight gradient A^T B over rows (both operands MN-major, split-K
-// over rows with a fixed-order reduction).  B for the first two is the small
+// (K-major, SWIZZLE_128B), weight gradient A^T B over rows (both operands
+// MN-major; 32-bit MN-major operands require the 128B swizzle with 32-byte
+// atoms, TMA SWIZZLE_128B_ATOM_32B / UMMA SWIZZLE_128B_BASE32B; split-K over
+// rows with a fixed-order reduction).  B for the first two is the small
 // weight matrix, pre-split into padded hi/lo K-major copies by k_prep_b.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -107,13 +109,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 }
 
 // SW128 shared-memory matrix descriptor (tcgen05 "version 1")
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                          uint32_t layout = 2) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
   d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
   d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
   d |= uint64_t{1} << 46;  // version
-  d |= uint64_t{2} << 61;  // SWIZZLE_128B
+  d |= uint64_t(layout) << 61;  // 2 = SWIZZLE_128B, 1 = SWIZZLE_128B_BASE32B
   return d;
 }
 
@@ -218,6 +221,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(Blo, &tmBlo, &full[s], k0, 0);
           } else {
             mbar_expect_tx(&full[s], a_bytes + b_bytes);
+            // 32-bit MN-major operands must use the 128B swizzle with 32-byte atoms
+            // (TMA SWIZZLE_128B_ATOM_32B <-> UMMA SWIZZLE_128B_BASE32B): one box per
+            // 32-wide MN group, 32 K rows of 128 B, groups 4 KB apart
             for (int j = 0; j < kBM / 32; ++j) tma_load_2d(A + j * 4096, &tmA, &full[s], m0 + 32 * j, k0);
             for (int j = 0; j < p.BN / 32; ++j) tma_load_2d(B + j * 4096, &tmB, &full[s], 32 * j, k0);
           }
@@ -258,11 +264,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               dAl = sdesc(aL + 32 * j, 16, 1024);
               dBh = sdesc(bH + 32 * j, 16, 1024);
               dBl = sdesc(bL + 32 * j, 16, 1024);
-            } else {  // MN-major: 8 K rows = one 1024 B atom; 32-element MN groups 4 KB apart
-              dAh = sdesc(aH + 1024 * j, 4096, 1024);
-              dAl = sdesc(aL + 1024 * j, 4096, 1024);
-              dBh = sdesc(bH + 1024 * j, 4096, 1024);
-              dBl = sdesc(bL + 1024 * j, 4096, 1024);
+            } else {  // MN-major BASE32B: 4-row K atoms (SBO 512 B), MN groups 4 KB (LBO)
+              dAh = sdesc(aH + 1024 * j, 4096, 512, 1);
+              dAl = sdesc(aL + 1024 * j, 4096, 512, 1);
+              dBh = sdesc(bH + 1024 * j, 4096, 512, 1);
+              dBl = sdesc(bL + 1024 * j, 4096, 512, 1);
             }
             tc_mma(d, dAh, dBh, idesc, first ? 0u : 1u);
             first = false;
@@ -374,7 +380,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2D fp32 tensor map: inner (contiguous) extent x outer extent, row pitch in elements
 CUtensorMap make_map(const float* base, uint64_t inner, uint64_t outer, uint64_t pitch_elems,
-                     uint32_t box_inner, uint32_t box_outer) {
+                     uint32_t box_inner, uint32_t box_outer,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {pitch_elems * 4};
@@ -384,7 +391,7 @@ CUtensorMap make_map(const float* base, uint64_t inner, uint64_t outer, uint64_t
                QGNN_EINVAL, "tensor map: 16-byte aligned base/pitch required");
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base),
                                  dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   QGNN_REQUIRE(r == CUDA_SUCCESS, QGNN_ECUDA, "cuTensorMapEncodeTiled failed");
   return m;
@@ -461,8 +468,10 @@ float* tc_gemm_wgrad_partials(qgnn_ctx* ctx, const float* A, int64_t lda, const 
   const int cps = int(ceil_div(k_chunks, splits));
   splits = int(ceil_div(k_chunks, cps));
   float* part = static_cast<float*>(ctx_scratch(ctx, sizeof(float) * size_t(splits) * M * N));
-  const CUtensorMap ta = make_map(A, uint64_t(M), uint64_t(n_rows), uint64_t(lda), 32, 32);
-  const CUtensorMap tb = make_map(B, uint64_t(N), uint64_t(n_rows), uint64_t(ldb), 32, 32);
+  const CUtensorMap ta = make_map(A, uint64_t(M), uint64_t(n_rows), uint64_t(lda), 32, 32,
+                                  CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  const CUtensorMap tb = make_map(B, uint64_t(N), uint64_t(n_rows), uint64_t(ldb), 32, 32,
+                                  CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   tc::Params p{};
   p.M = M;
   p.N = N;
