@@ -82,4 +82,10 @@ float* tc_gemm_wgrad_partials(qgnn_ctx* ctx, const float* A, int64_t lda, const 
                               int64_t ldb, int M, int N, int64_t n_rows, int* splits_out,
                               cudaStream_t s);
 bool use_tc_gemm();
+// fp32 row-range SpMM with hub-row splitting (spmm.cu)
+void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y, int64_t ldy,
+              const float* sa, const int64_t* pa, const int32_t* ca, const float* aa,
+              const int64_t* pb, const int32_t* cb, const float* ab, int64_t row_begin,
+              int64_t n_rows, float* out, int64_t ldo, const int32_t* hubs, int64_t n_hubs,
+              int64_t hub_deg, cudaStream_t s);
 }  // namespace qgnn_b200

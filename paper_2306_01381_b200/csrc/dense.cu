@@ -302,6 +302,12 @@ __global__ void k_adam(T* __restrict__ p, T* __restrict__ m, T* __restrict__ v,
 
 inline dim3 grid1(int64_t n, int t) { return dim3(static_cast<unsigned>(ceil_div(n, t))); }
 
+// TMA needs a 16-byte aligned base and row pitch
+inline bool tma_ok(const void* base, int64_t ld, int64_t row_begin) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(static_cast<const float*>(base) + row_begin * ld);
+  return (a & 15) == 0 && (ld * 4) % 16 == 0;
+}
+
 }  // namespace qgnn_b200
 
 using namespace qgnn_b200;
@@ -319,7 +325,7 @@ int qgnn_dense_forward(qgnn_ctx* ctx, int dtype, const void* A, int64_t lda, con
     k_dfwd_exact<<<grid1(n_rows * dout, 256), 256, 0, s>>>(
         static_cast<const double*>(A), lda, static_cast<const double*>(W), int(din), int(dout),
         rows, row_begin, n_rows, relu, static_cast<double*>(out), ld_out);
-  } else if (!rows && use_tc_gemm() && dout <= 256) {
+  } else if (!rows && use_tc_gemm() && dout <= 256 && tma_ok(A, lda, row_begin)) {
     tc_gemm_rows(ctx, static_cast<const float*>(A) + row_begin * lda, lda,
                  static_cast<const float*>(W), int(dout), int(dout), int(din), 1, n_rows, relu,
                  static_cast<float*>(out) + row_begin * ld_out, ld_out, s);
@@ -346,7 +352,7 @@ int qgnn_dense_input_grad(qgnn_ctx* ctx, int dtype, const void* A, int64_t lda, 
     k_dgrad_exact<<<grid1(n_rows * din, 256), 256, 0, s>>>(
         static_cast<const double*>(A), lda, static_cast<const double*>(W), int(din), int(dout),
         rows, row_begin, n_rows, static_cast<double*>(out), ld_out);
-  } else if (!rows && use_tc_gemm() && din <= 256) {
+  } else if (!rows && use_tc_gemm() && din <= 256 && tma_ok(A, lda, row_begin)) {
     tc_gemm_rows(ctx, static_cast<const float*>(A) + row_begin * lda, lda,
                  static_cast<const float*>(W), int(dout), int(din), int(dout), 0, n_rows, 0,
                  static_cast<float*>(out) + row_begin * ld_out, ld_out, s);
@@ -373,7 +379,8 @@ int qgnn_dense_weight_grad(qgnn_ctx* ctx, int dtype, const void* A, int64_t lda,
     k_wgrad_exact<<<grid1(m * n, 128), 128, 0, s>>>(
         static_cast<const double*>(A), lda, static_cast<const double*>(B), ldb, int(m), int(n),
         rows, row_begin, n_rows, accumulate, static_cast<double*>(out));
-  } else if (!rows && use_tc_gemm() && n <= 256 && (lda * 4) % 16 == 0 && (ldb * 4) % 16 == 0) {
+  } else if (!rows && use_tc_gemm() && n <= 256 && tma_ok(A, lda, row_begin) &&
+             tma_ok(B, ldb, row_begin)) {
     int splits = 0;
     const float* part = tc_gemm_wgrad_partials(
         ctx, static_cast<const float*>(A) + row_begin * lda, lda,

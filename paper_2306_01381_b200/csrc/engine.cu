@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <future>
 #include <memory>
@@ -233,9 +234,32 @@ class Engine final : public EngineBase {
     DBuf<double> loss;                  // [1]
     DBuf<unsigned long long> correct;   // [2]
     DBuf<double> ce_terms;
+    // rows (slots) with more than kHubDeg neighbours, per SpMM call site
+    DBuf<int32_t> hub_fc, hub_fm, hub_bwd, hub_part;
+    int64_t n_hub_fc = 0, n_hub_fm = 0, n_hub_bwd = 0, n_hub_part = 0;
   };
 
   int64_t ld_of(int64_t d) const { return round_up(d, 8); }
+  // rows with more neighbours than this are split across a CTA (QGNN_HUB_DEG overrides)
+  int64_t kHubDeg = 1024;
+  // K4 dispatch: fp32 -> nnz-balanced row-range kernel with hub splitting (all
+  // feature buffers are zero-padded to a multiple of 4 columns); fp64 -> the
+  // reference-order kernel.  Returns the number of kernels launched.
+  int spmm(int64_t dim, const T* x, int64_t ldx, const T* y, int64_t ldy, const T* sa,
+           const int64_t* pa, const int32_t* ca, const T* aa, const int64_t* pb,
+           const int32_t* cb, const T* ab, int64_t r0, int64_t n, T* out, int64_t ldo,
+           const int32_t* hubs, int64_t n_hubs) {
+    if constexpr (sizeof(T) == 4) {
+      spmm_f32(ctx_, int(round_up(dim, 4)), x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, r0, n, out,
+               ldo, hubs, n_hubs, kHubDeg, s_main_);
+      return 1 + (n_hubs > 0 ? 1 : 0);
+    } else {
+      const int st = qgnn_csr_aggregate(ctx_, dtype_, dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb,
+                                        ab, nullptr, r0, n, out, ldo, s_main_);
+      if (st) throw Status(st, qgnn_last_error());
+      return 1;
+    }
+  }
   void build_messages();
   void layout_pair(int k, int p, int q);
   void upload_key_meta(int k);
@@ -357,6 +381,7 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
   QGNN_REQUIRE(labels && train && val && test, QGNN_EINVAL, "engine: missing labels");
   P_ = s.n_parts;
   L_ = s.n_dims - 1;
+  if (const char* e = std::getenv("QGNN_HUB_DEG")) kHubDeg = std::max<int64_t>(1, std::atoll(e));
   dims_.assign(s.dims, s.dims + s.n_dims);
   p0_ = s.rank * (P_ / s.world);
   p1_ = p0_ + P_ / s.world;
@@ -489,6 +514,26 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
     D.loss.alloc(1);
     D.correct.alloc(2);
     D.ce_terms.alloc(std::max<int64_t>(1, D.n_train));
+    {
+      std::vector<int32_t> fc, fm, bw, pt;
+      for (int64_t g = 0; g < no; ++g) {
+        const int64_t ld = V.local_ptr[g + 1] - V.local_ptr[g];
+        const int64_t rd = V.remote_ptr[g + 1] - V.remote_ptr[g];
+        if (g < V.n_central && ld > kHubDeg) fc.push_back(int32_t(g));
+        if (g >= V.n_central && ld + rd > kHubDeg) fm.push_back(int32_t(g));
+        if (ld > kHubDeg) bw.push_back(int32_t(g));
+      }
+      for (int64_t k = 0; k < nr; ++k)
+        if (V.slot_ptr[k + 1] - V.slot_ptr[k] > kHubDeg) pt.push_back(int32_t(k));
+      D.hub_fc.upload(fc);
+      D.hub_fm.upload(fm);
+      D.hub_bwd.upload(bw);
+      D.hub_part.upload(pt);
+      D.n_hub_fc = int64_t(fc.size());
+      D.n_hub_fm = int64_t(fm.size());
+      D.n_hub_bwd = int64_t(bw.size());
+      D.n_hub_part = int64_t(pt.size());
+    }
     D.snd.resize(keys_.size());
     D.rcv.resize(keys_.size());
   }
@@ -846,12 +891,12 @@ void Engine<T>::forward_layer(int l) {
     const int64_t nc = D.view.n_central;
     if (!nc) continue;
     kbegin(QGNN_K_SPMM_FWD);
-    QGNN_CALL(qgnn_csr_aggregate(ctx_, dtype_, din, D.h[t].p, ldi, nullptr, 0, D.self_alpha.p,
-                                 D.lptr.p, D.lcol.p, D.lafwd.p, nullptr, nullptr, nullptr, nullptr,
-                                 0, nc, D.hagg[t].p, ldi, s_main_));
+    const int nk = spmm(din, D.h[t].p, ldi, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
+                        D.lafwd.p, nullptr, nullptr, nullptr, 0, nc, D.hagg[t].p, ldi, D.hub_fc.p,
+                        D.n_hub_fc);
     const double nnz = double(D.view.local_ptr[nc]);
     kend(QGNN_K_SPMM_FWD, nc * (16.0 + 2 * din * sizeof(T)) + nnz * (4 + sizeof(T)) +
-                              double(D.view.num_owned) * din * sizeof(T), s_main_);
+                              double(D.view.num_owned) * din * sizeof(T), s_main_, nk);
     kbegin(QGNN_K_GEMM_FWD);
     QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
                                  nullptr, 0, nc, relu, D.h[l].p, ldo, s_main_));
@@ -877,13 +922,13 @@ void Engine<T>::forward_layer(int l) {
     const int64_t nc = D.view.n_central, nm = D.view.n_marginal;
     if (!nm) continue;
     kbegin(QGNN_K_SPMM_FWD);
-    QGNN_CALL(qgnn_csr_aggregate(ctx_, dtype_, din, D.h[t].p, ldi, D.halo.p, ldi, D.self_alpha.p,
-                                 D.lptr.p, D.lcol.p, D.lafwd.p, D.rptr.p, D.rslot.p, D.ralpha.p,
-                                 nullptr, nc, nm, D.hagg[t].p, ldi, s_main_));
+    const int nk = spmm(din, D.h[t].p, ldi, D.halo.p, ldi, D.self_alpha.p, D.lptr.p, D.lcol.p,
+                        D.lafwd.p, D.rptr.p, D.rslot.p, D.ralpha.p, nc, nm, D.hagg[t].p, ldi,
+                        D.hub_fm.p, D.n_hub_fm);
     const double nnz = double(D.view.local_ptr[nc + nm] - D.view.local_ptr[nc]) +
                        double(D.view.remote_nnz());
     kend(QGNN_K_SPMM_FWD, nm * (24.0 + 2 * din * sizeof(T)) + nnz * (4 + sizeof(T)) +
-                              double(D.view.num_remote) * din * sizeof(T), s_main_);
+                              double(D.view.num_remote) * din * sizeof(T), s_main_, nk);
     kbegin(QGNN_K_GEMM_FWD);
     QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
                                  nullptr, nc, nm, relu, D.h[l].p, ldo, s_main_));
@@ -942,12 +987,12 @@ void Engine<T>::backward_layer(int l) {
     kend(QGNN_K_GEMM_DGRAD, double(nm) * (din + dout) * sizeof(T), s_main_);
     if (D.view.num_remote) {
       kbegin(QGNN_K_PARTIALS);
-      QGNN_CALL(qgnn_csr_aggregate(ctx_, dtype_, din, D.gbar.p, ldi, nullptr, 0, nullptr, D.sptr.p,
-                                   D.srow.p, D.salpha.p, nullptr, nullptr, nullptr, nullptr, 0,
-                                   D.view.num_remote, D.partials.p, ldi, s_main_));
+      const int nk = spmm(din, D.gbar.p, ldi, nullptr, 0, nullptr, D.sptr.p, D.srow.p, D.salpha.p,
+                          nullptr, nullptr, nullptr, 0, D.view.num_remote, D.partials.p, ldi,
+                          D.hub_part.p, D.n_hub_part);
       kend(QGNN_K_PARTIALS, double(D.view.num_remote) * (8 + din * sizeof(T)) +
                                 double(D.view.remote_nnz()) * (4 + sizeof(T) + din * sizeof(T)),
-           s_main_);
+           s_main_, nk);
     }
     quantize(D, k, D.partials.p, ldi);
   }
@@ -976,12 +1021,12 @@ void Engine<T>::backward_layer(int l) {
     kend(QGNN_K_GEMM_WGRAD, double(no) * (din + dout) * sizeof(T), s_main_,
          dtype_ == QGNN_F64 ? 1 : 2);
     kbegin(QGNN_K_SPMM_BWD);
-    QGNN_CALL(qgnn_csr_aggregate(ctx_, dtype_, din, D.gbar.p, ldi, nullptr, 0, D.self_alpha.p,
-                                 D.lptr.p, D.lcol.p, D.labwd.p, nullptr, nullptr, nullptr, nullptr,
-                                 0, no, D.dh_next.p, ldi, s_main_));
+    const int nk = spmm(din, D.gbar.p, ldi, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
+                        D.labwd.p, nullptr, nullptr, nullptr, 0, no, D.dh_next.p, ldi, D.hub_bwd.p,
+                        D.n_hub_bwd);
     kend(QGNN_K_SPMM_BWD, no * (16.0 + 2 * din * sizeof(T)) +
                               double(D.view.local_nnz()) * (4 + sizeof(T)) +
-                              double(no) * din * sizeof(T), s_main_);
+                              double(no) * din * sizeof(T), s_main_, nk);
   }
   if (s_.world > 1) QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_x_, 0));
   for (auto& up : parts_dev_) {

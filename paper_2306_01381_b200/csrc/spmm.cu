@@ -10,6 +10,8 @@
 // and the transposed-CSR form of backward_remote_partials; F32 contracts to FMA.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace qgnn_b200 {
@@ -182,6 +184,151 @@ void launch_csr(int nv, int dim, const T* x, int64_t ldx, const T* y, int64_t ld
   check_launch("k_csr_aggregate");
 }
 
+// ----------------------------------------------------------------- F32 v2 ---
+// Production fp32 SpMM over a contiguous row range.  Each CTA owns an
+// nnz-balanced contiguous slice of rows and its 8 warps walk it in lock-step
+// (rows r, r+1, ..., r+7 in flight), so neighbour rows shared by nearby rows
+// (graph locality) are served from L1 instead of L2.  Rows with more than
+// `hub_deg` neighbours are skipped here and finished by k_spmm_hubs, where a
+// whole CTA splits the row's edge list (no single-warp tail on power-law hubs).
+template <int NV>
+__device__ __forceinline__ void row_gather4(float (&acc)[NV][4], const float* __restrict__ src,
+                                            int64_t ld, int64_t beg, int64_t end,
+                                            const int32_t* __restrict__ col,
+                                            const float* __restrict__ alpha, int lane, int nvec) {
+  gather_edges<float, 4, NV>(acc, src, ld, beg, end, col, alpha, lane, nvec);
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256, 3) k_spmm_f32(
+    int dim, const float* __restrict__ x, int64_t ldx, const float* __restrict__ y, int64_t ldy,
+    const float* __restrict__ self_alpha, const int64_t* __restrict__ pa,
+    const int32_t* __restrict__ ca, const float* __restrict__ aa, const int64_t* __restrict__ pb,
+    const int32_t* __restrict__ cb, const float* __restrict__ ab, int64_t r0, int64_t n_rows,
+    float* __restrict__ out, int64_t ldo, int64_t hub_deg) {
+  __shared__ int64_t range[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r1 = r0 + n_rows;
+  if (threadIdx.x < 2) {
+    // weight = edges + 2 per row (self term + output row)
+    auto key = [&](int64_t r) { return pa[r] + (pb ? pb[r] : 0) + 2 * (r - r0); };
+    const int64_t k0 = key(r0), tot = key(r1) - k0;
+    const int64_t target = k0 + tot * (blockIdx.x + threadIdx.x) / gridDim.x;
+    int64_t lo = r0, hi = r1;  // first r with key(r) >= target
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (key(mid) < target) lo = mid + 1; else hi = mid;
+    }
+    range[threadIdx.x] = lo;
+  }
+  __syncthreads();
+  const int64_t start = range[0], end = blockIdx.x + 1 == gridDim.x ? r1 : range[1];
+  const int nvec = dim >> 2;
+  for (int64_t r = start + warp; r < end; r += 8) {
+    const int64_t ea0 = pa[r], ea1 = pa[r + 1];
+    const int64_t eb0 = pb ? pb[r] : 0, eb1 = pb ? pb[r + 1] : 0;
+    if ((ea1 - ea0) + (eb1 - eb0) > hub_deg) continue;  // k_spmm_hubs
+    float acc[NV][4];
+    if (self_alpha) {
+      const float sa = self_alpha[r];
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int cv = lane + 32 * i;
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (cv < nvec) vload<float, 4>(x + r * ldx + cv * 4, v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q] = sa * v[q];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NV; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q] = 0.f;
+    }
+    row_gather4<NV>(acc, x, ldx, ea0, ea1, ca, aa, lane, nvec);
+    if (pb) row_gather4<NV>(acc, y, ldy, eb0, eb1, cb, ab, lane, nvec);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int cv = lane + 32 * i;
+      if (cv < nvec) vstore<float, 4>(out + r * ldo + cv * 4, acc[i]);
+    }
+  }
+}
+
+// One CTA per hub row: 8 warps take contiguous eighths of the edge lists,
+// partial sums meet in shared memory and are added in warp order (deterministic).
+template <int NV>
+__global__ void __launch_bounds__(256) k_spmm_hubs(
+    int dim, const float* __restrict__ x, int64_t ldx, const float* __restrict__ y, int64_t ldy,
+    const float* __restrict__ self_alpha, const int64_t* __restrict__ pa,
+    const int32_t* __restrict__ ca, const float* __restrict__ aa, const int64_t* __restrict__ pb,
+    const int32_t* __restrict__ cb, const float* __restrict__ ab, const int32_t* __restrict__ hubs,
+    float* __restrict__ out, int64_t ldo) {
+  extern __shared__ float part[];  // [8][NV * 128]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r = hubs[blockIdx.x];
+  const int nvec = dim >> 2;
+  float acc[NV][4];
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[i][q] = 0.f;
+  {
+    const int64_t e0 = pa[r], e1 = pa[r + 1], len = e1 - e0;
+    const int64_t b = e0 + len * warp / 8, e = e0 + len * (warp + 1) / 8;
+    row_gather4<NV>(acc, x, ldx, b, e, ca, aa, lane, nvec);
+  }
+  if (pb) {
+    const int64_t e0 = pb[r], e1 = pb[r + 1], len = e1 - e0;
+    const int64_t b = e0 + len * warp / 8, e = e0 + len * (warp + 1) / 8;
+    row_gather4<NV>(acc, y, ldy, b, e, cb, ab, lane, nvec);
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) part[warp * NV * 128 + (lane + 32 * i) * 4 + q] = acc[i][q];
+  __syncthreads();
+  const float sa = self_alpha ? self_alpha[r] : 0.f;
+  for (int c = threadIdx.x; c < nvec * 4; c += blockDim.x) {
+    float v = self_alpha ? sa * x[r * ldx + c] : 0.f;
+    for (int w = 0; w < 8; ++w) v += part[w * NV * 128 + c];
+    out[r * ldo + c] = v;
+  }
+}
+
+// fp32 row-range SpMM with optional hub list (rows with > hub_deg neighbours).
+void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y, int64_t ldy,
+              const float* sa, const int64_t* pa, const int32_t* ca, const float* aa,
+              const int64_t* pb, const int32_t* cb, const float* ab, int64_t row_begin,
+              int64_t n_rows, float* out, int64_t ldo, const int32_t* hubs, int64_t n_hubs,
+              int64_t hub_deg, cudaStream_t s) {
+  if (n_rows <= 0) return;
+  const int nv = int(ceil_div(dim / 4, 32));
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_rows, 8),
+                                                              int64_t(ctx->num_sms) * 3 * 4));
+  const int64_t hd = hubs ? hub_deg : (int64_t(1) << 62);
+#define QGNN_SPMM_CASE(NVV)                                                                    \
+  case NVV:                                                                                    \
+    k_spmm_f32<NVV><<<unsigned(blocks), 256, 0, s>>>(dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, \
+                                                     ab, row_begin, n_rows, out, ldo, hd);       \
+    if (hubs && n_hubs > 0)                                                                    \
+      k_spmm_hubs<NVV><<<unsigned(n_hubs), 256, 8 * NVV * 128 * sizeof(float), s>>>(           \
+          dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, hubs, out, ldo);                    \
+    break;
+  switch (nv) {
+    QGNN_SPMM_CASE(1)
+    QGNN_SPMM_CASE(2)
+    QGNN_SPMM_CASE(3)
+    QGNN_SPMM_CASE(4)
+    QGNN_SPMM_CASE(5)
+    QGNN_SPMM_CASE(8)
+    default:
+      throw Status(QGNN_EINVAL, "spmm_f32: feature dim too large");
+  }
+#undef QGNN_SPMM_CASE
+  check_launch("k_spmm_f32");
+}
+
 inline int pick_nv(int64_t nvec) {
   const int64_t need = ceil_div(nvec, 32);
   for (int c : {1, 2, 3, 4, 5, 8, 16, 32})
@@ -219,7 +366,13 @@ extern "C" int qgnn_csr_aggregate(qgnn_ctx* ctx, int dtype, int64_t dim, const v
   } else {
     const bool vec4 = dim % 4 == 0 && ld_x % 4 == 0 && ld_out % 4 == 0 && aligned16(x) &&
                       aligned16(out) && (!ptr_b || (ld_y % 4 == 0 && aligned16(y)));
-    if (vec4) {
+    if (vec4 && !rows && pick_nv(dim / 4) <= 5) {
+      spmm_f32(ctx, d, static_cast<const float*>(x), ld_x, static_cast<const float*>(y), ld_y,
+               static_cast<const float*>(self_alpha), ptr_a, col_a,
+               static_cast<const float*>(alpha_a), ptr_b, col_b,
+               static_cast<const float*>(alpha_b), row_begin, n_rows, static_cast<float*>(out),
+               ld_out, nullptr, 0, 0, s);
+    } else if (vec4) {
       const int nv = pick_nv(dim / 4);
       launch_csr<float, 4>(nv, d, static_cast<const float*>(x), ld_x,
                            static_cast<const float*>(y), ld_y,

@@ -89,3 +89,13 @@ def test_engine_partition_count_invariance_lossless(cuda):
         else:
             assert max(_rel(a, b) for a, b in zip(losses, base)) < 1e-10
             assert np.abs(w - wb).max() < 1e-10
+
+
+def test_engine_hub_split_matches(cuda, monkeypatch):
+    """Hub rows split across a CTA (k_spmm_hubs) give the same training run."""
+    base, wb = _run("fixed", 8, 3, "f32")
+    monkeypatch.setenv("QGNN_HUB_DEG", "3")
+    hub, wh = _run("fixed", 8, 3, "f32")
+    for a, b in zip(base, hub):
+        assert _rel(a["train_loss"], b["train_loss"]) < 1e-5
+    assert np.abs(wb - wh).max() < 1e-4
