@@ -185,12 +185,12 @@ void launch_csr(int nv, int dim, const T* x, int64_t ldx, const T* y, int64_t ld
 }
 
 // ----------------------------------------------------------------- F32 v2 ---
-// Production fp32 SpMM over a contiguous row range.  Each CTA owns an
-// nnz-balanced contiguous slice of rows and its 8 warps walk it in lock-step
-// (rows r, r+1, ..., r+7 in flight), so neighbour rows shared by nearby rows
-// (graph locality) are served from L1 instead of L2.  Rows with more than
-// `hub_deg` neighbours are skipped here and finished by k_spmm_hubs, where a
-// whole CTA splits the row's edge list (no single-warp tail on power-law hubs).
+// Production fp32 SpMM over a contiguous row range.  Warp w of block b owns
+// row r0 + 8b + w, so at any instant the resident warps of the whole GPU sweep
+// one window of consecutive rows: with the graph's locality their neighbour
+// rows overlap and are served from L2.  Rows with more than `hub_deg`
+// neighbours are skipped here and finished by k_spmm_hubs, where a whole CTA
+// splits the row's edge list (no single-warp tail on power-law hubs).
 template <int NV>
 __device__ __forceinline__ void row_gather4(float (&acc)[NV][4], const float* __restrict__ src,
                                             int64_t ld, int64_t beg, int64_t end,
@@ -200,34 +200,20 @@ __device__ __forceinline__ void row_gather4(float (&acc)[NV][4], const float* __
 }
 
 template <int NV>
-__global__ void __launch_bounds__(256, 3) k_spmm_f32(
+__global__ void __launch_bounds__(256, (NV <= 2 ? 3 : 1)) k_spmm_f32(
     int dim, const float* __restrict__ x, int64_t ldx, const float* __restrict__ y, int64_t ldy,
     const float* __restrict__ self_alpha, const int64_t* __restrict__ pa,
     const int32_t* __restrict__ ca, const float* __restrict__ aa, const int64_t* __restrict__ pb,
     const int32_t* __restrict__ cb, const float* __restrict__ ab, int64_t r0, int64_t n_rows,
     float* __restrict__ out, int64_t ldo, int64_t hub_deg) {
-  __shared__ int64_t range[2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t r1 = r0 + n_rows;
-  if (threadIdx.x < 2) {
-    // weight = edges + 2 per row (self term + output row)
-    auto key = [&](int64_t r) { return pa[r] + (pb ? pb[r] : 0) + 2 * (r - r0); };
-    const int64_t k0 = key(r0), tot = key(r1) - k0;
-    const int64_t target = k0 + tot * (blockIdx.x + threadIdx.x) / gridDim.x;
-    int64_t lo = r0, hi = r1;  // first r with key(r) >= target
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (key(mid) < target) lo = mid + 1; else hi = mid;
-    }
-    range[threadIdx.x] = lo;
-  }
-  __syncthreads();
-  const int64_t start = range[0], end = blockIdx.x + 1 == gridDim.x ? r1 : range[1];
   const int nvec = dim >> 2;
-  for (int64_t r = start + warp; r < end; r += 8) {
+  {
+    const int64_t r = r0 + int64_t(blockIdx.x) * 8 + warp;
+    if (r >= r0 + n_rows) return;
     const int64_t ea0 = pa[r], ea1 = pa[r + 1];
     const int64_t eb0 = pb ? pb[r] : 0, eb1 = pb ? pb[r + 1] : 0;
-    if ((ea1 - ea0) + (eb1 - eb0) > hub_deg) continue;  // k_spmm_hubs
+    if ((ea1 - ea0) + (eb1 - eb0) > hub_deg) return;  // k_spmm_hubs
     float acc[NV][4];
     if (self_alpha) {
       const float sa = self_alpha[r];
@@ -304,8 +290,7 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
               int64_t hub_deg, cudaStream_t s) {
   if (n_rows <= 0) return;
   const int nv = int(ceil_div(dim / 4, 32));
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_rows, 8),
-                                                              int64_t(ctx->num_sms) * 3 * 4));
+  const int64_t blocks = ceil_div(n_rows, 8);
   const int64_t hd = hubs ? hub_deg : (int64_t(1) << 62);
 #define QGNN_SPMM_CASE(NVV)                                                                    \
   case NVV:                                                                                    \
