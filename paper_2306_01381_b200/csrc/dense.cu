@@ -200,12 +200,31 @@ template <typename T>
 __global__ void k_relu_backward(const T* __restrict__ act, int64_t lda, const T* __restrict__ dh,
                                 int64_t ldh, int dim, int64_t rb, int64_t n, T* __restrict__ dz,
                                 int64_t ldz) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= n * dim) return;
-  const int64_t r = rb + t / dim;
-  const int j = static_cast<int>(t % dim);
-  const T a = act[r * lda + j];
-  dz[r * ldz + j] = a <= T(0) ? T(0) : dh[r * ldh + j];
+  // 2D grid: blockIdx.y walks rows, x covers the row (no 64-bit div/mod per element)
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= dim) return;
+  for (int64_t k = blockIdx.y; k < n; k += gridDim.y) {
+    const int64_t r = rb + k;
+    const T a = act[r * lda + j];
+    dz[r * ldz + j] = a <= T(0) ? T(0) : dh[r * ldh + j];
+  }
+}
+
+// float4 variant (dim, leading dims and bases multiples of 4 floats)
+__global__ void k_relu_backward4(const float4* __restrict__ act, int64_t lda4,
+                                 const float4* __restrict__ dh, int64_t ldh4, int dim4, int64_t rb,
+                                 int64_t n, float4* __restrict__ dz, int64_t ldz4) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t total = n * dim4;
+  for (int64_t i = t; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t k = i / dim4;
+    const int j = int(i - k * dim4);
+    const int64_t r = rb + k;
+    const float4 a = act[r * lda4 + j];
+    const float4 g = dh[r * ldh4 + j];
+    dz[r * ldz4 + j] = make_float4(a.x <= 0.f ? 0.f : g.x, a.y <= 0.f ? 0.f : g.y,
+                                   a.z <= 0.f ? 0.f : g.z, a.w <= 0.f ? 0.f : g.w);
+  }
 }
 
 // One warp per listed row: softmax CE (model.hpp:175-200); loss term per row to `terms`.
@@ -414,14 +433,27 @@ int qgnn_relu_backward(qgnn_ctx* ctx, int dtype, const void* act, int64_t ld_act
   QGNN_REQUIRE(ctx, QGNN_EINVAL, "relu_backward: null context");
   if (n_rows == 0) return QGNN_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (dtype == QGNN_F64)
-    k_relu_backward<double><<<grid1(n_rows * dim, 256), 256, 0, s>>>(
+  const dim3 g2(static_cast<unsigned>(ceil_div(dim, 128)),
+                static_cast<unsigned>(std::min<int64_t>(n_rows, 65535)));
+  const bool v4 = dtype == QGNN_F32 && dim % 4 == 0 && ld_act % 4 == 0 && ld_dh % 4 == 0 &&
+                  ld_dz % 4 == 0 && (reinterpret_cast<uintptr_t>(act) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(dh) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(dz) & 15) == 0;
+  if (v4) {
+    const int64_t total = n_rows * (dim / 4);
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(total, 256), 148 * 16));
+    k_relu_backward4<<<blocks, 256, 0, s>>>(
+        static_cast<const float4*>(act), ld_act / 4, static_cast<const float4*>(dh), ld_dh / 4,
+        int(dim / 4), row_begin, n_rows, static_cast<float4*>(dz), ld_dz / 4);
+  } else if (dtype == QGNN_F64) {
+    k_relu_backward<double><<<g2, 128, 0, s>>>(
         static_cast<const double*>(act), ld_act, static_cast<const double*>(dh), ld_dh, int(dim),
         row_begin, n_rows, static_cast<double*>(dz), ld_dz);
-  else
-    k_relu_backward<float><<<grid1(n_rows * dim, 256), 256, 0, s>>>(
+  } else {
+    k_relu_backward<float><<<g2, 128, 0, s>>>(
         static_cast<const float*>(act), ld_act, static_cast<const float*>(dh), ld_dh, int(dim),
         row_begin, n_rows, static_cast<float*>(dz), ld_dz);
+  }
   check_launch("relu_backward");
   QGNN_API_END
 }

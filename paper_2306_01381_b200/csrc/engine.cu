@@ -210,6 +210,7 @@ class Engine final : public EngineBase {
     // activations
     std::vector<DBuf<T>> h, hagg;  // h[0..L], hagg[0..L-1]
     DBuf<T> halo, partials, dh, dh_next, dz, gbar;
+    DBuf<T> gpart;  // transform-first last layer: backward_remote_partials of dz
     // per key: sender metadata
     struct SendMeta {
       DBuf<int32_t> rows;
@@ -268,6 +269,10 @@ class Engine final : public EngineBase {
   void quantize(PartDev& P, int k, const T* src, int64_t ld);
   void exchange(int k);
   void forward_layer(int l);
+  void forward_last_tf(int l);
+  void backward_last_tf(int l);
+  bool tf_last_ = false;  // last layer aggregates after the transform (fp32, dout < din)
+  int gemm_nk() const { return (sizeof(T) == 4 && use_tc_gemm()) ? 2 : 1; }
   void loss_phase();
   void backward_layer(int l);
   void backward_last();
@@ -381,6 +386,10 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
   QGNN_REQUIRE(labels && train && val && test, QGNN_EINVAL, "engine: missing labels");
   P_ = s.n_parts;
   L_ = s.n_dims - 1;
+  // z = A(hW) for the last layer when it narrows (e.g. 256 -> 47 classes): the
+  // exchanged tensors are unchanged, the SpMMs gather dout- instead of din-wide rows
+  tf_last_ = sizeof(T) == 4 && L_ >= 2 && s.dims[L_] < s.dims[L_ - 1];
+  if (const char* e = std::getenv("QGNN_TF_LAST")) tf_last_ = tf_last_ && std::atoi(e) != 0;
   if (const char* e = std::getenv("QGNN_HUB_DEG")) kHubDeg = std::max<int64_t>(1, std::atoll(e));
   dims_.assign(s.dims, s.dims + s.n_dims);
   p0_ = s.rank * (P_ / s.world);
@@ -511,6 +520,7 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
     D.dh_next.alloc(no * maxd);
     D.dz.alloc(no * maxd);
     D.gbar.alloc(no * maxd);
+    if (tf_last_) D.gpart.alloc(std::max<int64_t>(1, nr) * ld_of(dims_[L_]));
     D.loss.alloc(1);
     D.correct.alloc(2);
     D.ce_terms.alloc(std::max<int64_t>(1, D.n_train));
@@ -900,7 +910,7 @@ void Engine<T>::forward_layer(int l) {
     kbegin(QGNN_K_GEMM_FWD);
     QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
                                  nullptr, 0, nc, relu, D.h[l].p, ldo, s_main_));
-    kend(QGNN_K_GEMM_FWD, double(nc) * (din + dout) * sizeof(T), s_main_);
+    kend(QGNN_K_GEMM_FWD, double(nc) * (din + dout) * sizeof(T), s_main_, gemm_nk());
   }
   if (s_.world > 1) QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_x_, 0));
   // receive (engine.hpp:607-618): decode every source straight into the halo
@@ -932,7 +942,7 @@ void Engine<T>::forward_layer(int l) {
     kbegin(QGNN_K_GEMM_FWD);
     QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
                                  nullptr, nc, nm, relu, D.h[l].p, ldo, s_main_));
-    kend(QGNN_K_GEMM_FWD, double(nm) * (din + dout) * sizeof(T), s_main_);
+    kend(QGNN_K_GEMM_FWD, double(nm) * (din + dout) * sizeof(T), s_main_, gemm_nk());
   }
 }
 
@@ -984,7 +994,7 @@ void Engine<T>::backward_layer(int l) {
     kbegin(QGNN_K_GEMM_DGRAD);
     QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, dz, ldo, W, din, dout, nullptr, nc, nm, D.gbar.p,
                                     ldi, s_main_));
-    kend(QGNN_K_GEMM_DGRAD, double(nm) * (din + dout) * sizeof(T), s_main_);
+    kend(QGNN_K_GEMM_DGRAD, double(nm) * (din + dout) * sizeof(T), s_main_, gemm_nk());
     if (D.view.num_remote) {
       kbegin(QGNN_K_PARTIALS);
       const int nk = spmm(din, D.gbar.p, ldi, nullptr, 0, nullptr, D.sptr.p, D.srow.p, D.salpha.p,
@@ -1012,7 +1022,7 @@ void Engine<T>::backward_layer(int l) {
     kbegin(QGNN_K_GEMM_DGRAD);
     QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, dz, ldo, W, din, dout, nullptr, 0, nc, D.gbar.p,
                                     ldi, s_main_));
-    kend(QGNN_K_GEMM_DGRAD, double(nc) * (din + dout) * sizeof(T), s_main_);
+    kend(QGNN_K_GEMM_DGRAD, double(nc) * (din + dout) * sizeof(T), s_main_, gemm_nk());
     kbegin(QGNN_K_GEMM_WGRAD);
     T* wg = wgrad_all_.p + D.id * nparams_ + woff_[t];
     QGNN_CALL(qgnn_dense_weight_grad(ctx_, dtype_, D.hagg[t].p, ldi, dz, ldo, din, dout,
@@ -1033,6 +1043,139 @@ void Engine<T>::backward_layer(int l) {
     PartDev& D = *up;
     auto& R = D.rcv[k];
     for (int64_t src = 0; src < P_; ++src) {  // ascending source (engine.hpp:720-734)
+      const int64_t b = R.p_begin[src], e = R.p_begin[src + 1];
+      if (e == b) continue;
+      kbegin(QGNN_K_DEQUANT);
+      QGNN_CALL(qgnn_dequant_scatter(ctx_, arena_.p, e - b, din, R.bits.p + b, R.off.p + b,
+                                     s_.layout, R.dst.p + b, 1, D.dh_next.p, dtype_, ldi,
+                                     s_main_));
+      kend(QGNN_K_DEQUANT, double(e - b) * (2 * din * sizeof(T) + 13) +
+                               double(msgs_[k][src][D.id].bytes), s_main_);
+    }
+    std::swap(D.dh, D.dh_next);
+  }
+}
+
+// Last layer, transform first (fp32 engine, dout < din): y = h W on owned and
+// halo rows, then z = A y (dout-wide gathers).  Messages: the same quantized
+// rows of h as forward_layer (engine.hpp:566-588).
+template <typename T>
+void Engine<T>::forward_last_tf(int l) {
+  const int t = l - 1;
+  const int k = t;
+  const int64_t din = dims_[t], dout = dims_[l];
+  const int64_t ldi = ld_of(din), ldo = ld_of(dout);
+  const T* W = w_.p + woff_[t];
+  for (auto& up : parts_dev_) quantize(*up, k, up->h[t].p, ldi);
+  exchange(k);
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    const int64_t no = D.view.num_owned, nc = D.view.n_central;
+    kbegin(QGNN_K_GEMM_FWD);
+    QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.h[t].p, ldi, W, din, dout, nullptr, 0, no, 0,
+                                 D.dz.p, ldo, s_main_));
+    kend(QGNN_K_GEMM_FWD, double(no) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+    if (!nc) continue;
+    kbegin(QGNN_K_SPMM_FWD);
+    const int nk = spmm(dout, D.dz.p, ldo, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
+                        D.lafwd.p, nullptr, nullptr, nullptr, 0, nc, D.h[l].p, ldo, D.hub_fc.p,
+                        D.n_hub_fc);
+    kend(QGNN_K_SPMM_FWD, nc * (16.0 + 2 * dout * sizeof(T)) +
+                              double(D.view.local_ptr[nc]) * (4 + sizeof(T)) +
+                              double(no) * dout * sizeof(T), s_main_, nk);
+  }
+  if (s_.world > 1) QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_x_, 0));
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    auto& R = D.rcv[k];
+    if (!R.n) continue;
+    kbegin(QGNN_K_DEQUANT);
+    QGNN_CALL(qgnn_dequant_scatter(ctx_, arena_.p, R.n, din, R.bits.p, R.off.p, s_.layout,
+                                   R.dst.p, 0, D.halo.p, dtype_, ldi, s_main_));
+    double bytes = double(R.n) * (din * sizeof(T) + 4 + 1 + 8);
+    for (int64_t src = 0; src < P_; ++src)
+      if (src != D.id) bytes += double(msgs_[k][src][D.id].bytes);
+    kend(QGNN_K_DEQUANT, bytes, s_main_);
+  }
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    const int64_t nc = D.view.n_central, nm = D.view.n_marginal, nr = D.view.num_remote;
+    if (!nm) continue;
+    if (nr) {
+      kbegin(QGNN_K_GEMM_FWD);
+      QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.halo.p, ldi, W, din, dout, nullptr, 0, nr, 0,
+                                   D.partials.p, ldo, s_main_));
+      kend(QGNN_K_GEMM_FWD, double(nr) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+    }
+    kbegin(QGNN_K_SPMM_FWD);
+    const int nk = spmm(dout, D.dz.p, ldo, D.partials.p, ldo, D.self_alpha.p, D.lptr.p, D.lcol.p,
+                        D.lafwd.p, D.rptr.p, D.rslot.p, D.ralpha.p, nc, nm, D.h[l].p, ldo,
+                        D.hub_fm.p, D.n_hub_fm);
+    const double nnz = double(D.view.local_ptr[nc + nm] - D.view.local_ptr[nc]) +
+                       double(D.view.remote_nnz());
+    kend(QGNN_K_SPMM_FWD, nm * (24.0 + 2 * dout * sizeof(T)) + nnz * (4 + sizeof(T)) +
+                              double(nr) * dout * sizeof(T), s_main_, nk);
+  }
+}
+
+// Backward of the transform-first last layer: g = A^T dz (dout-wide), then
+// partials = g_halo W^T (the same rows backward_remote_partials(dz W^T) gives,
+// aggregate.hpp:152-165), dh_next = g_local W^T, dW = h^T g_local + halo^T g_halo.
+template <typename T>
+void Engine<T>::backward_last_tf(int l) {
+  const int t = l - 1;
+  const int k = int(L_) + t - 1;
+  const int64_t din = dims_[t], dout = dims_[l];
+  const int64_t ldi = ld_of(din), ldo = ld_of(dout);
+  const T* W = w_.p + woff_[t];
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    const int64_t nr = D.view.num_remote;
+    if (nr) {
+      kbegin(QGNN_K_PARTIALS);
+      const int nk = spmm(dout, D.dh.p, ldo, nullptr, 0, nullptr, D.sptr.p, D.srow.p, D.salpha.p,
+                          nullptr, nullptr, nullptr, 0, nr, D.gpart.p, ldo, D.hub_part.p,
+                          D.n_hub_part);
+      kend(QGNN_K_PARTIALS, double(nr) * (8 + dout * sizeof(T)) +
+                                double(D.view.remote_nnz()) * (4 + sizeof(T) + dout * sizeof(T)),
+           s_main_, nk);
+      kbegin(QGNN_K_GEMM_DGRAD);
+      QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, D.gpart.p, ldo, W, din, dout, nullptr, 0, nr,
+                                      D.partials.p, ldi, s_main_));
+      kend(QGNN_K_GEMM_DGRAD, double(nr) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+    }
+    quantize(D, k, D.partials.p, ldi);
+  }
+  exchange(k);
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    const int64_t no = D.view.num_owned, nr = D.view.num_remote;
+    kbegin(QGNN_K_SPMM_BWD);
+    const int nk = spmm(dout, D.dh.p, ldo, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
+                        D.labwd.p, nullptr, nullptr, nullptr, 0, no, D.gbar.p, ldo, D.hub_bwd.p,
+                        D.n_hub_bwd);
+    kend(QGNN_K_SPMM_BWD, no * (16.0 + 2 * dout * sizeof(T)) +
+                              double(D.view.local_nnz()) * (4 + sizeof(T)) +
+                              double(no) * dout * sizeof(T), s_main_, nk);
+    kbegin(QGNN_K_GEMM_DGRAD);
+    QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, D.gbar.p, ldo, W, din, dout, nullptr, 0, no,
+                                    D.dh_next.p, ldi, s_main_));
+    kend(QGNN_K_GEMM_DGRAD, double(no) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+    kbegin(QGNN_K_GEMM_WGRAD);
+    T* wg = wgrad_all_.p + D.id * nparams_ + woff_[t];
+    QGNN_CALL(qgnn_dense_weight_grad(ctx_, dtype_, D.h[t].p, ldi, D.gbar.p, ldo, din, dout, nullptr,
+                                     0, no, 0, wg, s_main_));
+    if (nr)
+      QGNN_CALL(qgnn_dense_weight_grad(ctx_, dtype_, D.halo.p, ldi, D.gpart.p, ldo, din, dout,
+                                       nullptr, 0, nr, 1, wg, s_main_));
+    kend(QGNN_K_GEMM_WGRAD, double(no + nr) * (din + dout) * sizeof(T), s_main_,
+         (dtype_ == QGNN_F64 ? 1 : 2) * (nr ? 2 : 1));
+  }
+  if (s_.world > 1) QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_x_, 0));
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    auto& R = D.rcv[k];
+    for (int64_t src = 0; src < P_; ++src) {
       const int64_t b = R.p_begin[src], e = R.p_begin[src + 1];
       if (e == b) continue;
       kbegin(QGNN_K_DEQUANT);
@@ -1100,9 +1243,19 @@ void Engine<T>::run_epoch(qgnn_epoch_metrics* m) {
   launches_ = 0;
   prepare_epoch();
   QGNN_CUDA(cudaEventRecord(ev_a_, s_main_));
-  for (int64_t l = 1; l <= L_; ++l) forward_layer(int(l));
+  for (int64_t l = 1; l <= L_; ++l) {
+    if (l == L_ && tf_last_)
+      forward_last_tf(int(l));
+    else
+      forward_layer(int(l));
+  }
   loss_phase();
-  for (int64_t l = L_; l >= 2; --l) backward_layer(int(l));
+  for (int64_t l = L_; l >= 2; --l) {
+    if (l == L_ && tf_last_)
+      backward_last_tf(int(l));
+    else
+      backward_layer(int(l));
+  }
   backward_last();
   step();
   QGNN_CUDA(cudaEventRecord(ev_b_, s_main_));

@@ -99,3 +99,14 @@ def test_engine_hub_split_matches(cuda, monkeypatch):
     for a, b in zip(base, hub):
         assert _rel(a["train_loss"], b["train_loss"]) < 1e-5
     assert np.abs(wb - wh).max() < 1e-4
+
+
+def test_engine_transform_first_last_layer(cuda, monkeypatch):
+    """z = A(hW) for the narrowing last layer matches aggregate-then-transform (fp32)."""
+    tf, wt = _run("fixed", 4, 4, "f32")
+    monkeypatch.setenv("QGNN_TF_LAST", "0")
+    ag, wa = _run("fixed", 4, 4, "f32")
+    for a, b in zip(tf, ag):
+        assert _rel(a["train_loss"], b["train_loss"]) < 1e-5
+        assert a["ref_bytes_total"] == b["ref_bytes_total"]
+    assert np.abs(wt - wa).max() < 1e-4
