@@ -259,6 +259,177 @@ __global__ void __launch_bounds__(256) k_dequant_scatter(
   }
 }
 
+
+// ------------------------------------------------------------------ fast path ---
+// fp32 rows, GPU wire layout: lane l owns the float4 chunks c = l + 32 i of the
+// row, held in registers for both the extrema and the encode (one row read).
+// Chunk c's 4 codes occupy 4b bits at payload byte c*b/2, so a lane stores 1, 2
+// or 4 bytes per chunk and a warp instruction writes a contiguous run.  The
+// draw counter of element e is e + 1; consecutive elements advance the
+// generator input by +phi (64-bit add) instead of a multiply.
+__device__ __forceinline__ uint32_t quant_code(float h, double lo_d, double scale, double lv,
+                                               uint64_t z) {
+  // z = key + (e + 1) * phi, i.e. the input of rng_mix for counter e + 1
+  const double x = __ddiv_rn(__dsub_rn(static_cast<double>(h), lo_d), scale);
+  double base = floor(x);
+  const double frac = __dsub_rn(x, base);
+  const double u = static_cast<double>(rng_mix(z) >> 11) * 0x1.0p-53;
+  if (u < frac) base = __dadd_rn(base, 1.0);
+  return static_cast<uint32_t>(base < lv ? base : lv);
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256) k_quantize_pack_f32(
+    const float* __restrict__ values, int64_t ld, int dim, int64_t n,
+    const int32_t* __restrict__ rows, const uint32_t* __restrict__ ids,
+    const uint8_t* __restrict__ bits, const uint64_t* __restrict__ offsets,
+    const uint16_t* __restrict__ set_of, const uint64_t* __restrict__ set_keys,
+    uint8_t* __restrict__ out, float* __restrict__ win_lo, float* __restrict__ win_hi,
+    int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t m = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (m >= n) return;
+  const float* row = values + static_cast<int64_t>(rows[m]) * ld;
+  const int b = bits[m];
+  uint8_t* chunk = out + offsets[m];
+  const int nchunk = (dim + 3) >> 2;
+  float v[NV][4];
+  float lo = INFINITY, hi = -INFINITY;
+  bool finite = true;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + 32 * i;
+    if (c < nchunk) {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(row) + c);
+      v[i][0] = t.x, v[i][1] = t.y, v[i][2] = t.z, v[i][3] = t.w;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (4 * c + q < dim) {
+          finite &= isfinite(v[i][q]);
+          lo = v[i][q] < lo ? v[i][q] : lo;
+          hi = hi < v[i][q] ? v[i][q] : hi;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+    const float h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = l2 < lo ? l2 : lo;
+    hi = hi < h2 ? h2 : hi;
+  }
+  finite = __all_sync(0xffffffffu, finite);
+  if (lo == 0.f) lo = first_zero(row, dim, lane);  // signed-zero first occurrence
+  if (hi == 0.f) hi = first_zero(row, dim, lane);
+  if (lane == 0 && win_lo) {
+    const float wl = win_lo[m], wh = win_hi[m];
+    win_lo[m] = lo < wl ? lo : wl;
+    win_hi[m] = wh < hi ? hi : wh;
+  }
+  if (b == 0) {
+    float* dst = reinterpret_cast<float*>(chunk);
+    for (int j = lane; j < dim; j += 32) dst[j] = row[j];
+    return;
+  }
+  if (b != 2 && b != 4 && b != 8) {
+    if (lane == 0) atomicOr(err, kErrBadWidth);
+    return;
+  }
+  if (!finite) {
+    if (lane == 0) atomicOr(err, kErrNonFinite);
+    return;
+  }
+  const double lo_d = lo, hi_d = hi;
+  const uint32_t levels = (1u << b) - 1;
+  const bool constant = hi_d == lo_d;
+  const double scale = constant ? 0.0 : (hi_d - lo_d) / static_cast<double>(levels);
+  if (lane == 0) {
+    uint4 h;
+    h.x = __float_as_uint(static_cast<float>(scale));
+    h.y = __float_as_uint(lo);
+    h.z = static_cast<uint32_t>(dim);
+    h.w = static_cast<uint32_t>(b);
+    *reinterpret_cast<uint4*>(chunk) = h;
+  }
+  uint8_t* payload = chunk + kHdrGpu;
+  const int padded = static_cast<int>(((packed_bytes(dim, b) + 15) / 16) * 16);
+  const int units = padded * 2 / b;  // chunk-sized store units incl. zero padding
+  const uint64_t key = rng_fork(set_keys[set_of ? set_of[m] : 0], ids[m]);
+  const double lv = static_cast<double>(levels);
+#pragma unroll
+  for (int i = 0; i < NV + 1; ++i) {
+    const int c = lane + 32 * i;
+    if (c >= units) break;
+    uint32_t word = 0;
+    if (i < NV && c < nchunk && !constant) {
+      uint64_t z = key + static_cast<uint64_t>(4 * c + 1) * kPhi;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (4 * c + q < dim) word |= quant_code(v[i][q], lo_d, scale, lv, z) << (q * b);
+        z += kPhi;
+      }
+    }
+    if (b == 8)
+      reinterpret_cast<uint32_t*>(payload)[c] = word;
+    else if (b == 4)
+      reinterpret_cast<uint16_t*>(payload)[c] = static_cast<uint16_t>(word);
+    else
+      payload[c] = static_cast<uint8_t>(word);
+  }
+}
+
+// Decode counterpart: lane l writes the float4 chunks c = l + 32 i of the row.
+__global__ void __launch_bounds__(256) k_dequant_f32(
+    const uint8_t* __restrict__ in, int64_t n, int dim, const uint8_t* __restrict__ bits,
+    const uint64_t* __restrict__ offsets, const int32_t* __restrict__ dst_rows, int accumulate,
+    float* __restrict__ out, int64_t ld, int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t m = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (m >= n) return;
+  const uint8_t* chunk = in + offsets[m];
+  const int b = bits[m];
+  float* dst = out + (dst_rows ? static_cast<int64_t>(dst_rows[m]) : m) * ld;
+  const int nchunk = (dim + 3) >> 2;
+  if (b == 0) {
+    const float* src = reinterpret_cast<const float*>(chunk);
+    for (int j = lane; j < dim; j += 32) dst[j] = accumulate ? dst[j] + src[j] : src[j];
+    return;
+  }
+  const uint4 h = *reinterpret_cast<const uint4*>(chunk);
+  if (static_cast<int>(h.w & 0xff) != b || h.z != static_cast<uint32_t>(dim)) {
+    if (lane == 0) atomicOr(err, kErrDecode);
+    return;
+  }
+  const float sc = __uint_as_float(h.x), zp = __uint_as_float(h.y);
+  const uint8_t* payload = chunk + kHdrGpu;
+  const uint32_t mask = (1u << b) - 1;
+  for (int c = lane; c < nchunk; c += 32) {
+    uint32_t word;
+    if (b == 8)
+      word = reinterpret_cast<const uint32_t*>(payload)[c];
+    else if (b == 4)
+      word = reinterpret_cast<const uint16_t*>(payload)[c];
+    else
+      word = payload[c];
+    float r[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) r[q] = fmaf(static_cast<float>((word >> (q * b)) & mask), sc, zp);
+    if (4 * c + 3 < dim) {
+      float4* d4 = reinterpret_cast<float4*>(dst) + c;
+      if (accumulate) {
+        const float4 o = *d4;
+        *d4 = make_float4(o.x + r[0], o.y + r[1], o.z + r[2], o.w + r[3]);
+      } else {
+        *d4 = make_float4(r[0], r[1], r[2], r[3]);
+      }
+    } else {
+      for (int q = 0; q < 4 && 4 * c + q < dim; ++q)
+        dst[4 * c + q] = accumulate ? dst[4 * c + q] + r[q] : r[q];
+    }
+  }
+}
+
 }  // namespace qgnn_b200
 
 using namespace qgnn_b200;
@@ -304,7 +475,27 @@ int qgnn_quantize_pack(qgnn_ctx* ctx, const void* values, int dtype, int64_t ld,
   const int threads = 256;
   const int64_t blocks = ceil_div(n * 32, threads);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (dtype == QGNN_F64)
+  const bool fast = dtype == QGNN_F32 && layout == QGNN_WIRE_GPU && ld % 4 == 0 &&
+                    (reinterpret_cast<uintptr_t>(values) & 15) == 0 && dim <= 1024;
+  if (fast) {
+    const int nv = static_cast<int>(ceil_div(ceil_div(dim, 4), 32));
+    auto* v = static_cast<const float*>(values);
+    auto* wl = static_cast<float*>(win_lo);
+    auto* wh = static_cast<float*>(win_hi);
+    const int d = static_cast<int>(dim);
+    if (nv <= 1)
+      k_quantize_pack_f32<1><<<blocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,
+                                                        set_of, set_keys, out, wl, wh, ctx->d_err);
+    else if (nv <= 2)
+      k_quantize_pack_f32<2><<<blocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,
+                                                        set_of, set_keys, out, wl, wh, ctx->d_err);
+    else if (nv <= 4)
+      k_quantize_pack_f32<4><<<blocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,
+                                                        set_of, set_keys, out, wl, wh, ctx->d_err);
+    else
+      k_quantize_pack_f32<8><<<blocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,
+                                                        set_of, set_keys, out, wl, wh, ctx->d_err);
+  } else if (dtype == QGNN_F64)
     k_quantize_pack<double><<<blocks, threads, 0, s>>>(
         static_cast<const double*>(values), ld, static_cast<int>(dim), n, rows, ids, bits, offsets,
         set_of, set_keys, layout, out, static_cast<double*>(win_lo), static_cast<double*>(win_hi),
@@ -328,7 +519,12 @@ int qgnn_dequant_scatter(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int64_t di
   const int threads = 256;
   const int64_t blocks = ceil_div(n * 32, threads);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (dtype == QGNN_F64)
+  const bool fast = dtype == QGNN_F32 && layout == QGNN_WIRE_GPU && ld % 4 == 0 &&
+                    (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  if (fast)
+    k_dequant_f32<<<blocks, threads, 0, s>>>(in, n, static_cast<int>(dim), bits, offsets, dst_rows,
+                                             accumulate, static_cast<float*>(out), ld, ctx->d_err);
+  else if (dtype == QGNN_F64)
     k_dequant_scatter<double><<<blocks, threads, 0, s>>>(in, n, static_cast<int>(dim), bits,
                                                          offsets, layout, dst_rows, accumulate,
                                                          static_cast<double*>(out), ld, ctx->d_err);
