@@ -42,7 +42,7 @@ def launches(path):
         if len(r) <= mi:
             continue
         v = float(r[mi].replace(",", ""))
-        v *= {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}.get(r[ui], 1.0)
+        v *= {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}.get(r[ui], 1.0)
         name = r[ki].split("(")[0]
         agg[name][0] += 1
         agg[name][1] += v
