@@ -287,8 +287,9 @@ __global__ void __launch_bounds__(256) k_quantize_pack_f32(
     uint8_t* __restrict__ out, float* __restrict__ win_lo, float* __restrict__ win_hi,
     int* __restrict__ err) {
   const int lane = threadIdx.x & 31;
-  const int64_t m = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (m >= n) return;
+  const int64_t wstride = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t m = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; m < n;
+       m += wstride) {
   const float* row = values + static_cast<int64_t>(rows[m]) * ld;
   const int b = bits[m];
   uint8_t* chunk = out + offsets[m];
@@ -330,15 +331,15 @@ __global__ void __launch_bounds__(256) k_quantize_pack_f32(
   if (b == 0) {
     float* dst = reinterpret_cast<float*>(chunk);
     for (int j = lane; j < dim; j += 32) dst[j] = row[j];
-    return;
+    continue;
   }
   if (b != 2 && b != 4 && b != 8) {
     if (lane == 0) atomicOr(err, kErrBadWidth);
-    return;
+    continue;
   }
   if (!finite) {
     if (lane == 0) atomicOr(err, kErrNonFinite);
-    return;
+    continue;
   }
   const double lo_d = lo, hi_d = hi;
   const uint32_t levels = (1u << b) - 1;
@@ -377,6 +378,7 @@ __global__ void __launch_bounds__(256) k_quantize_pack_f32(
     else
       payload[c] = static_cast<uint8_t>(word);
   }
+  }
 }
 
 // Decode counterpart: lane l writes the float4 chunks c = l + 32 i of the row.
@@ -385,8 +387,9 @@ __global__ void __launch_bounds__(256) k_dequant_f32(
     const uint64_t* __restrict__ offsets, const int32_t* __restrict__ dst_rows, int accumulate,
     float* __restrict__ out, int64_t ld, int* __restrict__ err) {
   const int lane = threadIdx.x & 31;
-  const int64_t m = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (m >= n) return;
+  const int64_t wstride = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t m = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; m < n;
+       m += wstride) {
   const uint8_t* chunk = in + offsets[m];
   const int b = bits[m];
   float* dst = out + (dst_rows ? static_cast<int64_t>(dst_rows[m]) : m) * ld;
@@ -394,12 +397,12 @@ __global__ void __launch_bounds__(256) k_dequant_f32(
   if (b == 0) {
     const float* src = reinterpret_cast<const float*>(chunk);
     for (int j = lane; j < dim; j += 32) dst[j] = accumulate ? dst[j] + src[j] : src[j];
-    return;
+    continue;
   }
   const uint4 h = *reinterpret_cast<const uint4*>(chunk);
   if (static_cast<int>(h.w & 0xff) != b || h.z != static_cast<uint32_t>(dim)) {
     if (lane == 0) atomicOr(err, kErrDecode);
-    return;
+    continue;
   }
   const float sc = __uint_as_float(h.x), zp = __uint_as_float(h.y);
   const uint8_t* payload = chunk + kHdrGpu;
@@ -427,6 +430,7 @@ __global__ void __launch_bounds__(256) k_dequant_f32(
       for (int q = 0; q < 4 && 4 * c + q < dim; ++q)
         dst[4 * c + q] = accumulate ? dst[4 * c + q] + r[q] : r[q];
     }
+  }
   }
 }
 
@@ -478,22 +482,23 @@ int qgnn_quantize_pack(qgnn_ctx* ctx, const void* values, int dtype, int64_t ld,
   const bool fast = dtype == QGNN_F32 && layout == QGNN_WIRE_GPU && ld % 4 == 0 &&
                     (reinterpret_cast<uintptr_t>(values) & 15) == 0 && dim <= 1024;
   if (fast) {
+    const int64_t fblocks = std::min<int64_t>(blocks, int64_t(ctx->num_sms) * 16);
     const int nv = static_cast<int>(ceil_div(ceil_div(dim, 4), 32));
     auto* v = static_cast<const float*>(values);
     auto* wl = static_cast<float*>(win_lo);
     auto* wh = static_cast<float*>(win_hi);
     const int d = static_cast<int>(dim);
     if (nv <= 1)
-      k_quantize_pack_f32<1><<<blocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,
+      k_quantize_pack_f32<1><<<fblocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,
                                                         set_of, set_keys, out, wl, wh, ctx->d_err);
     else if (nv <= 2)
-      k_quantize_pack_f32<2><<<blocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,
+      k_quantize_pack_f32<2><<<fblocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,
                                                         set_of, set_keys, out, wl, wh, ctx->d_err);
     else if (nv <= 4)
-      k_quantize_pack_f32<4><<<blocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,
+      k_quantize_pack_f32<4><<<fblocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,
                                                         set_of, set_keys, out, wl, wh, ctx->d_err);
     else
-      k_quantize_pack_f32<8><<<blocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,
+      k_quantize_pack_f32<8><<<fblocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,
                                                         set_of, set_keys, out, wl, wh, ctx->d_err);
   } else if (dtype == QGNN_F64)
     k_quantize_pack<double><<<blocks, threads, 0, s>>>(
@@ -522,7 +527,7 @@ int qgnn_dequant_scatter(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int64_t di
   const bool fast = dtype == QGNN_F32 && layout == QGNN_WIRE_GPU && ld % 4 == 0 &&
                     (reinterpret_cast<uintptr_t>(out) & 15) == 0;
   if (fast)
-    k_dequant_f32<<<blocks, threads, 0, s>>>(in, n, static_cast<int>(dim), bits, offsets, dst_rows,
+    k_dequant_f32<<<std::min<int64_t>(blocks, int64_t(ctx->num_sms) * 16), threads, 0, s>>>(in, n, static_cast<int>(dim), bits, offsets, dst_rows,
                                              accumulate, static_cast<float*>(out), ld, ctx->d_err);
   else if (dtype == QGNN_F64)
     k_dequant_scatter<double><<<blocks, threads, 0, s>>>(in, n, static_cast<int>(dim), bits,

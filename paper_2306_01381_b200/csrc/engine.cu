@@ -211,6 +211,7 @@ class Engine final : public EngineBase {
     std::vector<DBuf<T>> h, hagg;  // h[0..L], hagg[0..L-1]
     DBuf<T> halo, partials, dh, dh_next, dz, gbar;
     DBuf<T> gpart;  // transform-first last layer: backward_remote_partials of dz
+    DBuf<int32_t> row_node_d;  // GPU row -> node id (feature gather)
     // per key: sender metadata
     struct SendMeta {
       DBuf<int32_t> rows;
@@ -325,6 +326,7 @@ class Engine final : public EngineBase {
   int64_t launches_ = 0, launches_last_ = 0;
   T* pinned_ = nullptr;
   size_t pinned_elems_ = 0;
+  DBuf<T> feat_all_;  // node-ordered features (pinned-input fast path)
   // per-epoch message counters
   uint64_t msgs_b_[4] = {0, 0, 0, 0};
   double resolve_seconds_ = 0;
@@ -507,6 +509,10 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
     D.n_val = int64_t(va.size());
     D.n_test = int64_t(te.size());
     D.ref_order.upload(V.gpu_row_of_ref);
+    {
+      std::vector<int32_t> rn(V.row_node.begin(), V.row_node.end());
+      D.row_node_d.upload(rn);
+    }
     const int64_t no = V.num_owned, nr = V.num_remote;
     int64_t maxd = 0;
     for (int64_t d : dims_) maxd = std::max(maxd, ld_of(d));
@@ -595,10 +601,42 @@ Engine<T>::~Engine() {
   if (ctx_) qgnn_ctx_destroy(ctx_);
 }
 
+// h0[g] = feats[row_node[g]] for every partition row (zero padding untouched)
+template <typename T>
+__global__ void k_gather_rows(const T* __restrict__ feats, int64_t F, const int32_t* __restrict__ node,
+                              int64_t n, T* __restrict__ out, int64_t ld) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t g = t / F;
+  if (g >= n) return;
+  const int64_t j = t - g * F;
+  out[g * ld + j] = feats[int64_t(node[g]) * F + j];
+}
+
 template <typename T>
 void Engine<T>::set_features(const void* f) {
   const int64_t F = dims_[0], ld = ld_of(F);
   const T* src = static_cast<const T*>(f);
+  cudaPointerAttributes attr{};
+  const bool pinned = cudaPointerGetAttributes(&attr, f) == cudaSuccess &&
+                      (attr.type == cudaMemoryTypeHost || attr.type == cudaMemoryTypeDevice);
+  cudaGetLastError();
+  if (pinned) {
+    // one async copy of the node-ordered matrix from pinned (or device) memory,
+    // then a gather into partition row order on the GPU
+    if (!feat_all_.p || feat_all_.n < size_t(n_nodes_ * F)) feat_all_.alloc(n_nodes_ * F, false);
+    QGNN_CUDA(cudaMemcpyAsync(feat_all_.p, src, n_nodes_ * F * sizeof(T), cudaMemcpyDefault,
+                              s_main_));
+    for (auto& up : parts_dev_) {
+      PartDev& D = *up;
+      const int64_t no = D.view.num_owned;
+      k_gather_rows<T><<<unsigned(ceil_div(no * F, 256)), 256, 0, s_main_>>>(
+          feat_all_.p, F, D.row_node_d.p, no, D.h[0].p, ld);
+      ++launches_;
+    }
+    check_launch("k_gather_rows");
+    QGNN_CUDA(cudaStreamSynchronize(s_main_));
+    return;
+  }
   size_t total = 0;
   for (auto& up : parts_dev_) total += size_t(up->view.num_owned * ld);
   if (total > pinned_elems_) {
@@ -607,7 +645,8 @@ void Engine<T>::set_features(const void* f) {
     std::memset(pinned_, 0, total * sizeof(T));
     pinned_elems_ = total;
   }
-  // gather rows into partition order (threads), then one pinned H2D per partition
+  // pageable input: gather rows into partition order on host threads, then one
+  // pinned H2D per partition
   std::vector<std::future<void>> jobs;
   size_t o = 0;
   for (auto& up : parts_dev_) {

@@ -120,7 +120,14 @@ class Engine:
         check(lib.qgnn_engine_run_epoch(self._h, C.byref(m)))
         return m.as_dict()
 
-    def set_features(self, feats: np.ndarray):
+    def set_features(self, feats):
+        """Upload node features (n x F).  A pinned torch tensor (or a CUDA
+        tensor) takes the fast path: one async copy + a GPU gather into
+        partition order; a numpy array is staged through pinned memory."""
+        if hasattr(feats, "data_ptr"):
+            assert feats.is_contiguous() and feats.element_size() == np.dtype(self.np_dtype).itemsize
+            check(lib.qgnn_engine_set_features(self._h, C.c_void_p(feats.data_ptr())))
+            return
         f = np.ascontiguousarray(feats, self.np_dtype)
         check(lib.qgnn_engine_set_features(self._h, f.ctypes.data))
 
