@@ -237,6 +237,12 @@ int qgnn_engine_kernel_stats(qgnn_engine* e, double* out, int n);
 /* NCCL bootstrap for world > 1: rank 0 creates the id, every rank passes it to
  * qgnn_engine_create.  128 bytes. */
 int qgnn_nccl_unique_id(void* out128);
+/* In-process loopback transport (tests, one device): every rank of `group` runs
+ * its engine in its own host thread of one process and passes this id instead
+ * of an NCCL id; exchanges and all-gathers become device copies between the
+ * ranks' buffers over the same routing as the NCCL path (the analogue of the
+ * reference's in-process mailbox, engine.hpp:331,502,528-529). */
+int qgnn_loopback_id(uint64_t group, void* out128);
 
 #ifdef __cplusplus
 }

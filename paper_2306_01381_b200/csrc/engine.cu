@@ -23,7 +23,10 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
 #include <future>
+#include <map>
+#include <mutex>
 #include <memory>
 #include <numeric>
 #include <vector>
@@ -146,6 +149,36 @@ __global__ void k_fill2(T* __restrict__ a, T va, T* __restrict__ b, T vb, int64_
     b[i] = vb;
   }
 }
+
+// ------------------------------------------------------- loopback comm ----
+// In-process transport for world > 1 on ONE device (tests): every rank is an
+// Engine in its own host thread; collectives publish device pointers / events
+// in a shared group and copy with cudaMemcpyAsync between the ranks' buffers.
+// It exercises the same routing (arena offsets, remote pairs, rank slices) as
+// the NCCL path — the analogue of the reference's in-process mailbox.
+struct LoopGroup {
+  int world = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<void*> engines, ptr;
+  std::vector<cudaEvent_t> ev, ev2;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+static std::mutex g_loop_mu;
+static std::map<uint64_t, std::shared_ptr<LoopGroup>> g_loops;
+constexpr char kLoopMagic[8] = {'Q', 'G', 'N', 'N', 'L', 'O', 'O', 'P'};
 
 // ------------------------------------------------------------ engine ----
 enum BitMode { kFp = 0, kFixed = 1, kUniform = 2, kAdaptive = 3 };
@@ -295,6 +328,14 @@ class Engine final : public EngineBase {
   cudaStream_t s_main_ = nullptr, s_comm_ = nullptr;
   cudaEvent_t ev_a_ = nullptr, ev_b_ = nullptr, ev_x_ = nullptr, ev_q_ = nullptr;
   ncclComm_t comm_ = nullptr;
+  std::shared_ptr<LoopGroup> loop_;     // loopback transport (tests), else NCCL
+  cudaEvent_t ev_c_ = nullptr, ev_d_ = nullptr;
+  std::vector<cudaEvent_t> peer_x_;     // loopback: peers' exchange-done events
+  DBuf<double> dloss_;
+  DBuf<unsigned long long> dcorr_;
+  template <typename X>
+  void allgather_dev(X* base, int64_t slice, cudaStream_t s);
+  void wait_exchange();
   int dtype_ = QGNN_F32;
 
   // host graph facts
@@ -408,11 +449,32 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
   QGNN_CUDA(cudaEventCreate(&ev_b_));
   QGNN_CUDA(cudaEventCreateWithFlags(&ev_x_, cudaEventDisableTiming));
   QGNN_CUDA(cudaEventCreateWithFlags(&ev_q_, cudaEventDisableTiming));
+  QGNN_CUDA(cudaEventCreateWithFlags(&ev_c_, cudaEventDisableTiming));
+  QGNN_CUDA(cudaEventCreateWithFlags(&ev_d_, cudaEventDisableTiming));
   if (s.world > 1) {
     QGNN_REQUIRE(nccl_id, QGNN_EINVAL, "engine: world > 1 needs an NCCL unique id");
-    ncclUniqueId id;
-    std::memcpy(&id, nccl_id, sizeof(id));
-    QGNN_NCCL(nccl().CommInitRank(&comm_, s.world, id, s.rank));
+    if (std::memcmp(nccl_id, kLoopMagic, 8) == 0) {
+      uint64_t key;
+      std::memcpy(&key, static_cast<const char*>(nccl_id) + 8, 8);
+      std::lock_guard<std::mutex> lk(g_loop_mu);
+      auto& g = g_loops[key];
+      if (!g) {
+        g = std::make_shared<LoopGroup>();
+        g->world = s.world;
+        g->engines.assign(s.world, nullptr);
+        g->ptr.assign(s.world, nullptr);
+        g->ev.assign(s.world, nullptr);
+        g->ev2.assign(s.world, nullptr);
+      }
+      QGNN_REQUIRE(g->world == s.world && !g->engines[s.rank], QGNN_EPROTOCOL,
+                   "loopback group: world mismatch or rank already registered");
+      g->engines[s.rank] = this;
+      loop_ = g;
+    } else {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      QGNN_NCCL(nccl().CommInitRank(&comm_, s.world, id, s.rank));
+    }
   }
 
   // partition (engine.hpp:212) and coefficients (:213)
@@ -591,6 +653,20 @@ Engine<T>::~Engine() {
     cudaEventDestroy(e.second);
   }
   if (comm_) nccl().CommDestroy(comm_);
+  if (loop_) {
+    std::lock_guard<std::mutex> lk(g_loop_mu);
+    loop_->engines[s_.rank] = nullptr;
+    bool empty = true;
+    for (void* e : loop_->engines) empty &= e == nullptr;
+    if (empty)
+      for (auto it = g_loops.begin(); it != g_loops.end(); ++it)
+        if (it->second == loop_) {
+          g_loops.erase(it);
+          break;
+        }
+  }
+  if (ev_c_) cudaEventDestroy(ev_c_);
+  if (ev_d_) cudaEventDestroy(ev_d_);
   if (pinned_) cudaFreeHost(pinned_);
   if (ev_a_) cudaEventDestroy(ev_a_);
   if (ev_b_) cudaEventDestroy(ev_b_);
@@ -895,6 +971,32 @@ void Engine<T>::exchange(int k) {
     QGNN_CUDA(cudaEventRecord(ev_pool_[ev_next_].first, s_comm_));
   }
   double bytes = 0;
+  if (loop_) {
+    LoopGroup& G = *loop_;
+    G.ev[s_.rank] = ev_q_;
+    G.barrier();  // every rank's K1 enqueued; its receive regions free after ev_q_
+    for (int r = 0; r < s_.world; ++r)
+      if (r != s_.rank) QGNN_CUDA(cudaStreamWaitEvent(s_comm_, G.ev[r], 0));
+    for (int64_t p = p0_; p < p1_; ++p)
+      for (int64_t q = 0; q < P_; ++q) {
+        if (q == p || (q >= p0_ && q < p1_)) continue;
+        const uint64_t nb = msgs_[k][p][q].bytes;
+        if (!nb) continue;
+        auto* peer = static_cast<Engine<T>*>(G.engines[q / ppr]);
+        QGNN_CUDA(cudaMemcpyAsync(peer->arena_.p + peer->recv_base_[k][q][p],
+                                  arena_.p + send_base_[k][p][q], nb, cudaMemcpyDeviceToDevice,
+                                  s_comm_));
+        bytes += double(nb);
+      }
+    QGNN_CUDA(cudaEventRecord(ev_x_, s_comm_));
+    G.ev2[s_.rank] = ev_x_;
+    G.barrier();  // all copies enqueued
+    peer_x_.clear();
+    for (int r = 0; r < s_.world; ++r)
+      if (r != s_.rank) peer_x_.push_back(G.ev2[r]);
+    kend(QGNN_K_EXCHANGE, bytes, s_comm_, 0);
+    return;
+  }
   QGNN_NCCL(nccl().GroupStart());
   for (int64_t p = p0_; p < p1_; ++p)
     for (int64_t q = 0; q < P_; ++q) {
@@ -916,6 +1018,48 @@ void Engine<T>::exchange(int k) {
   QGNN_NCCL(nccl().GroupEnd());
   kend(QGNN_K_EXCHANGE, bytes, s_comm_, 0);
   QGNN_CUDA(cudaEventRecord(ev_x_, s_comm_));
+}
+
+// Receivers wait for the exchange of the current key: NCCL completes on our comm
+// stream; loopback copies were issued on the senders' comm streams.
+template <typename T>
+void Engine<T>::wait_exchange() {
+  if (s_.world == 1) return;
+  if (loop_) {
+    for (cudaEvent_t e : peer_x_) QGNN_CUDA(cudaStreamWaitEvent(s_main_, e, 0));
+    return;
+  }
+  QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_x_, 0));
+}
+
+// In-place all-gather: rank r contributes base[r * slice, (r + 1) * slice).
+template <typename T>
+template <typename X>
+void Engine<T>::allgather_dev(X* base, int64_t slice, cudaStream_t st) {
+  if (s_.world == 1 || slice == 0) return;
+  if (!loop_) {
+    ncclDataType_t dt = ncclUint8;
+    size_t count = size_t(slice) * sizeof(X);
+    QGNN_NCCL(nccl().AllGather(base + s_.rank * slice, base, count, dt, comm_, st));
+    return;
+  }
+  LoopGroup& G = *loop_;
+  QGNN_CUDA(cudaEventRecord(ev_c_, st));
+  G.ptr[s_.rank] = base;
+  G.ev[s_.rank] = ev_c_;
+  G.barrier();
+  for (int r = 0; r < s_.world; ++r)
+    if (r != s_.rank) QGNN_CUDA(cudaStreamWaitEvent(s_comm_, G.ev[r], 0));
+  QGNN_CUDA(cudaStreamWaitEvent(s_comm_, ev_c_, 0));
+  for (int r = 0; r < s_.world; ++r)
+    if (r != s_.rank)
+      QGNN_CUDA(cudaMemcpyAsync(static_cast<X*>(G.ptr[r]) + s_.rank * slice, base + s_.rank * slice,
+                                size_t(slice) * sizeof(X), cudaMemcpyDeviceToDevice, s_comm_));
+  QGNN_CUDA(cudaEventRecord(ev_d_, s_comm_));
+  G.ev2[s_.rank] = ev_d_;
+  G.barrier();
+  for (int r = 0; r < s_.world; ++r)
+    if (r != s_.rank) QGNN_CUDA(cudaStreamWaitEvent(st, G.ev2[r], 0));
 }
 
 #define QGNN_CALL(x)                                 \
@@ -951,7 +1095,7 @@ void Engine<T>::forward_layer(int l) {
                                  nullptr, 0, nc, relu, D.h[l].p, ldo, s_main_));
     kend(QGNN_K_GEMM_FWD, double(nc) * (din + dout) * sizeof(T), s_main_, gemm_nk());
   }
-  if (s_.world > 1) QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_x_, 0));
+  wait_exchange();
   // receive (engine.hpp:607-618): decode every source straight into the halo
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
@@ -1077,7 +1221,7 @@ void Engine<T>::backward_layer(int l) {
                               double(D.view.local_nnz()) * (4 + sizeof(T)) +
                               double(no) * din * sizeof(T), s_main_, nk);
   }
-  if (s_.world > 1) QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_x_, 0));
+  wait_exchange();
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
     auto& R = D.rcv[k];
@@ -1123,7 +1267,7 @@ void Engine<T>::forward_last_tf(int l) {
                               double(D.view.local_ptr[nc]) * (4 + sizeof(T)) +
                               double(no) * dout * sizeof(T), s_main_, nk);
   }
-  if (s_.world > 1) QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_x_, 0));
+  wait_exchange();
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
     auto& R = D.rcv[k];
@@ -1210,7 +1354,7 @@ void Engine<T>::backward_last_tf(int l) {
     kend(QGNN_K_GEMM_WGRAD, double(no + nr) * (din + dout) * sizeof(T), s_main_,
          (dtype_ == QGNN_F64 ? 1 : 2) * (nr ? 2 : 1));
   }
-  if (s_.world > 1) QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_x_, 0));
+  wait_exchange();
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
     auto& R = D.rcv[k];
@@ -1258,12 +1402,7 @@ void Engine<T>::backward_last() {
 template <typename T>
 void Engine<T>::step() {
   kbegin(QGNN_K_ELEMWISE);
-  if (s_.world > 1) {
-    const int64_t ppr = P_ / s_.world;
-    T* base = wgrad_all_.p;
-    QGNN_NCCL(nccl().AllGather(base + p0_ * nparams_, base, size_t(ppr * nparams_),
-                               sizeof(T) == 8 ? ncclFloat64 : ncclFloat32, comm_, s_main_));
-  }
+  allgather_dev(wgrad_all_.p, (P_ / s_.world) * nparams_, s_main_);
   k_sum_parts<T><<<unsigned(ceil_div(nparams_, 256)), 256, 0, s_main_>>>(wgrad_all_.p, int(P_),
                                                                          nparams_, wsum_.p);
   ++adam_t_;
@@ -1313,16 +1452,21 @@ void Engine<T>::run_epoch(qgnn_epoch_metrics* m) {
     QGNN_CUDA(cudaMemcpy(&corr[2 * up->id], up->correct.p, 2 * sizeof(unsigned long long),
                          cudaMemcpyDeviceToHost));
   }
-  if (s_.world > 1) {
-    DBuf<double> dl;
-    DBuf<unsigned long long> dc;
-    dl.upload(loss);
-    dc.upload(corr);
-    QGNN_NCCL(nccl().AllReduce(dl.p, dl.p, size_t(P_), ncclFloat64, ncclSum, comm_, s_main_));
-    QGNN_NCCL(nccl().AllReduce(dc.p, dc.p, size_t(2 * P_), ncclUint64, ncclSum, comm_, s_main_));
+  if (s_.world > 1) {  // every rank fills its partitions' slots, then all-gather
+    if (!dloss_.p) {
+      dloss_.alloc(P_);
+      dcorr_.alloc(2 * P_);
+    }
+    QGNN_CUDA(cudaMemcpyAsync(dloss_.p, loss.data(), P_ * sizeof(double), cudaMemcpyHostToDevice,
+                              s_main_));
+    QGNN_CUDA(cudaMemcpyAsync(dcorr_.p, corr.data(), 2 * P_ * sizeof(unsigned long long),
+                              cudaMemcpyHostToDevice, s_main_));
+    const int64_t ppr = P_ / s_.world;
+    allgather_dev(dloss_.p, ppr, s_main_);
+    allgather_dev(dcorr_.p, 2 * ppr, s_main_);
     QGNN_CUDA(cudaStreamSynchronize(s_main_));
-    QGNN_CUDA(cudaMemcpy(loss.data(), dl.p, P_ * sizeof(double), cudaMemcpyDeviceToHost));
-    QGNN_CUDA(cudaMemcpy(corr.data(), dc.p, 2 * P_ * sizeof(unsigned long long),
+    QGNN_CUDA(cudaMemcpy(loss.data(), dloss_.p, P_ * sizeof(double), cudaMemcpyDeviceToHost));
+    QGNN_CUDA(cudaMemcpy(corr.data(), dcorr_.p, 2 * P_ * sizeof(unsigned long long),
                          cudaMemcpyDeviceToHost));
   }
   double total = 0.0;
@@ -1391,13 +1535,8 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
                                   cudaMemcpyDeviceToDevice, s_main_));
       }
     }
-    if (s_.world > 1) {
-      const ncclDataType_t dt = sizeof(T) == 8 ? ncclFloat64 : ncclFloat32;
-      QGNN_NCCL(nccl().AllGather(dlo.p + p0_ * stride, dlo.p, size_t(ppr * stride), dt, comm_,
-                                 s_main_));
-      QGNN_NCCL(nccl().AllGather(dhi.p + p0_ * stride, dhi.p, size_t(ppr * stride), dt, comm_,
-                                 s_main_));
-    }
+    allgather_dev(dlo.p, ppr * stride, s_main_);
+    allgather_dev(dhi.p, ppr * stride, s_main_);
     QGNN_CUDA(cudaStreamSynchronize(s_main_));
     QGNN_CUDA(cudaMemcpy(lo_all.data(), dlo.p, lo_all.size() * sizeof(T), cudaMemcpyDeviceToHost));
     QGNN_CUDA(cudaMemcpy(hi_all.data(), dhi.p, hi_all.size() * sizeof(T), cudaMemcpyDeviceToHost));
@@ -1608,6 +1747,14 @@ int qgnn_engine_kernel_stats(qgnn_engine* e, double* out, int n) {
   } catch (...) {
     return -status_from_exception();
   }
+}
+
+int qgnn_loopback_id(uint64_t group, void* out128) {
+  QGNN_API_BEGIN
+  std::memset(out128, 0, 128);
+  std::memcpy(out128, kLoopMagic, 8);
+  std::memcpy(static_cast<char*>(out128) + 8, &group, 8);
+  QGNN_API_END
 }
 
 int qgnn_nccl_unique_id(void* out128) {

@@ -54,6 +54,13 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def loopback_id(group: int) -> bytes:
+    """Id for the in-process loopback transport (one thread per rank, one GPU)."""
+    buf = (C.c_char * 128)()
+    check(lib.qgnn_loopback_id(group, buf))
+    return bytes(buf)
+
+
 class Engine:
     def __init__(self, graph, dims: Sequence[int], n_parts: int, bit_mode: str = "fixed",
                  fixed_bits: int = 8, seed: int = 7, sage: bool = False, lam: float = 0.5,
