@@ -267,13 +267,28 @@ __global__ void __launch_bounds__(256) k_dequant_scatter(
 // or 4 bytes per chunk and a warp instruction writes a contiguous run.  The
 // draw counter of element e is e + 1; consecutive elements advance the
 // generator input by +phi (64-bit add) instead of a multiply.
-__device__ __forceinline__ uint32_t quant_code(float h, double lo_d, double scale, double lv,
-                                               uint64_t z) {
-  // z = key + (e + 1) * phi, i.e. the input of rng_mix for counter e + 1
-  const double x = __ddiv_rn(__dsub_rn(static_cast<double>(h), lo_d), scale);
-  double base = floor(x);
-  const double frac = __dsub_rn(x, base);
+__device__ __forceinline__ uint32_t quant_code(float h, double lo_d, double scale, double rcp,
+                                               double lv, uint64_t z) {
+  // z = key + (e + 1) * phi, i.e. the input of rng_mix for counter e + 1.
+  // Reference: x = RN((h - lo) / S), base = floor(x), frac = x - base,
+  // base += (u < frac), clamp (quant.hpp:81-87).  Fast path: x' = RN(a * RN(1/S))
+  // satisfies |x' - x| < 2^-43 for x <= 255, so floor(x') == floor(x) and
+  // (u < frac') == (u < frac) whenever frac' and u - frac' stay 2^-40 away from
+  // the decision boundaries; otherwise (probability ~1e-12, and each row's
+  // extremum) the exact division decides.  Codes are identical either way.
+  const double a = __dsub_rn(static_cast<double>(h), lo_d);
   const double u = static_cast<double>(rng_mix(z) >> 11) * 0x1.0p-53;
+  if (a == 0.0) return 0u;  // x = 0 exactly, frac = 0, u < 0 false
+  constexpr double tol = 0x1.0p-40;
+  double x = __dmul_rn(a, rcp);
+  double base = floor(x);
+  double frac = __dsub_rn(x, base);
+  const double d = u - frac;
+  if (!(frac >= tol && frac <= 1.0 - tol && (d > tol || d < -tol))) {
+    x = __ddiv_rn(a, scale);
+    base = floor(x);
+    frac = __dsub_rn(x, base);
+  }
   if (u < frac) base = __dadd_rn(base, 1.0);
   return static_cast<uint32_t>(base < lv ? base : lv);
 }
@@ -358,6 +373,7 @@ __global__ void __launch_bounds__(256) k_quantize_pack_f32(
   const int units = padded * 2 / b;  // chunk-sized store units incl. zero padding
   const uint64_t key = rng_fork(set_keys[set_of ? set_of[m] : 0], ids[m]);
   const double lv = static_cast<double>(levels);
+  const double rcp = constant ? 0.0 : __drcp_rn(scale);
 #pragma unroll
   for (int i = 0; i < NV + 1; ++i) {
     const int c = lane + 32 * i;
@@ -367,7 +383,7 @@ __global__ void __launch_bounds__(256) k_quantize_pack_f32(
       uint64_t z = key + static_cast<uint64_t>(4 * c + 1) * kPhi;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        if (4 * c + q < dim) word |= quant_code(v[i][q], lo_d, scale, lv, z) << (q * b);
+        if (4 * c + q < dim) word |= quant_code(v[i][q], lo_d, scale, rcp, lv, z) << (q * b);
         z += kPhi;
       }
     }

@@ -176,3 +176,42 @@ def test_unbiased_at_scale(cuda):
         mean = dec.astype(np.float64).mean(0)  # fp32 axis-0 means accumulate naively
         se = s / 2 / np.sqrt(n)
         assert (np.abs(mean - base) < 4 * se + 1e-6).mean() > 0.99
+
+
+def test_fast_path_codes_exact_on_adversarial_rows(cuda):
+    """K1's reciprocal fast path must reproduce the exact-division codes: lattice
+    rows (x exactly integral), near-lattice rows, constant and post-ReLU rows."""
+    rs = np.random.default_rng(77)
+    rows = []
+    for k in range(3000):
+        b = (2, 4, 8)[k % 3]
+        lv = (1 << b) - 1
+        kind = k % 6
+        if kind == 0:
+            x = rs.standard_normal(256)
+        elif kind == 1:  # exact lattice: (h - lo) / S integral
+            x = rs.integers(0, lv + 1, 256).astype(np.float64) * 0.375 - 1.5
+        elif kind == 2:  # lattice plus one-ulp-scale noise
+            x = rs.integers(0, lv + 1, 256) * 0.25 + rs.standard_normal(256) * 1e-7
+        elif kind == 3:
+            x = np.maximum(rs.standard_normal(256), 0)
+        elif kind == 4:
+            x = rs.standard_normal(256) * 1e-30
+        else:
+            x = rs.uniform(-1e4, 1e4, 256)
+        rows.append((x.astype(np.float32), b))
+    X = np.stack([r[0] for r in rows])
+    bits = np.array([r[1] for r in rows], np.int32)
+    n = len(rows)
+    ids = np.arange(n, dtype=np.uint32) * 7 + 1
+    key = port.stream(9, 2, 4, 1, 2, 3)
+    wire, idx = ops.encode_message_set(torch.as_tensor(X, device=cuda), np.arange(n), ids, bits,
+                                       key, layout=WIRE_GPU)
+    w = wire.cpu().numpy()
+    bad = 0
+    for k in range(n):
+        i = idx["pos"][k]
+        o = int(idx["off"][k])
+        s_, z_, p = port.quantize(X[i].astype(np.float64), int(bits[i]), port.fork(key, int(ids[i])))
+        bad += int(not (w[o + 16:o + 16 + len(p)] == p).all())
+    assert bad == 0
