@@ -7,8 +7,8 @@
 //
 // Pipeline (one persistent CTA per SM, 12 warps):
 //   warp 0      TMA producer: A tile (and, for the weight gradient, B tile)
-//               for each 32-deep K chunk into a 2-stage smem ring (SW128)
-//   warp 1      MMA issuer: one elected thread issues 4 k-steps x 3 products of
+//               for each 16-deep K chunk into a 2..6-stage smem ring
+//   warp 1      MMA issuer: one elected thread issues 2 k-steps x 3 products of
 //               tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=BN) per chunk
 //   warp 2      TMEM allocator (2 x BN fp32 accumulator columns, double buffer)
 //   warps 4-7   epilogue: tcgen05.ld 32x32b -> ReLU -> global stores, while the
@@ -33,8 +33,8 @@ namespace qgnn_b200 {
 namespace tc {
 
 constexpr int kBM = 128;
-constexpr int kBK = 32;  // fp32 elements per 128-byte swizzle row
-constexpr int kStages = 2;
+constexpr int kBK = 16;         // fp32 K elements per chunk (64-byte K-major rows)
+constexpr int kMaxStages = 6;   // ring depth is chosen per launch from the smem budget
 constexpr int kThreads = 384;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -116,7 +116,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
   d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
   d |= uint64_t{1} << 46;  // version
-  d |= uint64_t(layout) << 61;  // 2 = SWIZZLE_128B, 1 = SWIZZLE_128B_BASE32B
+  d |= uint64_t(layout) << 61;  // 2 = SW128, 4 = SW64, 1 = SW128_BASE32B
   return d;
 }
 
@@ -139,6 +139,7 @@ struct Params {
   int BN;               // N tile (multiple of 16 / 32 for MN-major B), <= 256
   int tmem_cols;        // columns per accumulator buffer (pow2 >= BN)
   int m_tiles, splits, k_chunks, chunks_per_split;
+  int stages;
   float* out;
   int64_t ldo;
   int relu;
@@ -153,14 +154,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  const int a_bytes = kBM * kBK * 4;        // 16 KB
-  const int b_bytes = p.BN * kBK * 4;       // BN x 128 B
+  const int a_bytes = kBM * kBK * 4;        // 8 KB
+  const int b_bytes = p.BN * kBK * 4;       // BN x 64 B
   const int stage_bytes = 2 * a_bytes + 2 * b_bytes;
+  const int kStages = p.stages;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * stage_bytes);
-  uint64_t* full = bars;                 // [kStages]
-  uint64_t* conv = bars + kStages;       // [kStages]
-  uint64_t* empty = bars + 2 * kStages;  // [kStages]
-  uint64_t* tfull = bars + 3 * kStages;  // [2]
+  uint64_t* full = bars;                    // [kMaxStages]
+  uint64_t* conv = bars + kMaxStages;       // [kMaxStages]
+  uint64_t* empty = bars + 2 * kMaxStages;  // [kMaxStages]
+  uint64_t* tfull = bars + 3 * kMaxStages;  // [2]
   uint64_t* tempty = tfull + 2;          // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -223,9 +225,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_expect_tx(&full[s], a_bytes + b_bytes);
             // 32-bit MN-major operands must use the 128B swizzle with 32-byte atoms
             // (TMA SWIZZLE_128B_ATOM_32B <-> UMMA SWIZZLE_128B_BASE32B): one box per
-            // 32-wide MN group, 32 K rows of 128 B, groups 4 KB apart
-            for (int j = 0; j < kBM / 32; ++j) tma_load_2d(A + j * 4096, &tmA, &full[s], m0 + 32 * j, k0);
-            for (int j = 0; j < p.BN / 32; ++j) tma_load_2d(B + j * 4096, &tmB, &full[s], 32 * j, k0);
+            // 32-wide MN group, kBK K rows of 128 B, groups 2 KB apart
+            for (int j = 0; j < kBM / 32; ++j) tma_load_2d(A + j * 2048, &tmA, &full[s], m0 + 32 * j, k0);
+            for (int j = 0; j < p.BN / 32; ++j) tma_load_2d(B + j * 2048, &tmB, &full[s], 32 * j, k0);
           }
           if (++s == kStages) s = 0, ph ^= 1;
         }
@@ -259,16 +261,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < kBK / 8; ++j) {
             uint64_t dAh, dAl, dBh, dBl;
-            if (!kMN) {  // K-major: advance 8 fp32 = 32 B inside the 128 B swizzle row
-              dAh = sdesc(aH + 32 * j, 16, 1024);
-              dAl = sdesc(aL + 32 * j, 16, 1024);
-              dBh = sdesc(bH + 32 * j, 16, 1024);
-              dBl = sdesc(bL + 32 * j, 16, 1024);
-            } else {  // MN-major BASE32B: 4-row K atoms (SBO 512 B), MN groups 4 KB (LBO)
-              dAh = sdesc(aH + 1024 * j, 4096, 512, 1);
-              dAl = sdesc(aL + 1024 * j, 4096, 512, 1);
-              dBh = sdesc(bH + 1024 * j, 4096, 512, 1);
-              dBl = sdesc(bL + 1024 * j, 4096, 512, 1);
+            if (!kMN) {  // K-major SWIZZLE_64B: 8-row atoms of 64 B (SBO 512), +32 B per k-step
+              dAh = sdesc(aH + 32 * j, 16, 512, 4);
+              dAl = sdesc(aL + 32 * j, 16, 512, 4);
+              dBh = sdesc(bH + 32 * j, 16, 512, 4);
+              dBl = sdesc(bL + 32 * j, 16, 512, 4);
+            } else {  // MN-major BASE32B: 4-row K atoms (SBO 512 B), MN groups 2 KB (LBO)
+              dAh = sdesc(aH + 1024 * j, 2048, 512, 1);
+              dAl = sdesc(aL + 1024 * j, 2048, 512, 1);
+              dBh = sdesc(bH + 1024 * j, 2048, 512, 1);
+              dBl = sdesc(bL + 1024 * j, 2048, 512, 1);
             }
             tc_mma(d, dAh, dBh, idesc, first ? 0u : 1u);
             first = false;
@@ -403,8 +405,14 @@ int pow2_cols(int bn) {
   return c;
 }
 
+constexpr size_t kSmemBudget = 200 * 1024;
+int stages_for(int BN) {
+  const size_t stage = 2 * tc::kBM * tc::kBK * 4 + 2 * size_t(BN) * tc::kBK * 4;
+  return int(std::max<size_t>(2, std::min<size_t>(tc::kMaxStages, kSmemBudget / stage)));
+}
 size_t smem_bytes(int BN) {
-  return size_t(tc::kStages) * (2 * tc::kBM * tc::kBK * 4 + 2 * BN * tc::kBK * 4) + 1024 + 256;
+  const size_t stage = 2 * tc::kBM * tc::kBK * 4 + 2 * size_t(BN) * tc::kBK * 4;
+  return size_t(stages_for(BN)) * stage + 1024 + 256;
 }
 
 template <bool kMN>
@@ -414,7 +422,7 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo, 
   static bool attr_set = false;
   if (!attr_set) {
     QGNN_CUDA(cudaFuncSetAttribute(tc::k_tc_gemm<kMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(smem_bytes(256))));
+                                   int(kSmemBudget + 1024 + 256)));
     attr_set = true;
   }
   const int tiles = p.m_tiles * p.splits;
@@ -435,9 +443,12 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
   float* blo = bhi + size_t(BN) * Kp;
   tc::k_prep_b<<<unsigned(ceil_div(int64_t(N) * Kp, 256)), 256, 0, s>>>(W, wcols, N, K, Kp,
                                                                         transpose_w, bhi, blo);
-  const CUtensorMap ta = make_map(A, uint64_t(K), uint64_t(n_rows), uint64_t(lda), 32, tc::kBM);
-  const CUtensorMap tb = make_map(bhi, uint64_t(Kp), uint64_t(N), uint64_t(Kp), 32, uint32_t(BN));
-  const CUtensorMap tbl = make_map(blo, uint64_t(Kp), uint64_t(N), uint64_t(Kp), 32, uint32_t(BN));
+  const CUtensorMap ta = make_map(A, uint64_t(K), uint64_t(n_rows), uint64_t(lda), tc::kBK, tc::kBM,
+                                  CU_TENSOR_MAP_SWIZZLE_64B);
+  const CUtensorMap tb = make_map(bhi, uint64_t(Kp), uint64_t(N), uint64_t(Kp), tc::kBK, uint32_t(BN),
+                                  CU_TENSOR_MAP_SWIZZLE_64B);
+  const CUtensorMap tbl = make_map(blo, uint64_t(Kp), uint64_t(N), uint64_t(Kp), tc::kBK,
+                                   uint32_t(BN), CU_TENSOR_MAP_SWIZZLE_64B);
   tc::Params p{};
   p.M = int(n_rows);
   p.N = N;
@@ -451,6 +462,7 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
   p.out = out;
   p.ldo = ldo;
   p.relu = relu;
+  p.stages = stages_for(BN);
   launch<false>(ta, tb, tbl, p, ctx->num_sms, s);
 }
 
@@ -468,9 +480,9 @@ float* tc_gemm_wgrad_partials(qgnn_ctx* ctx, const float* A, int64_t lda, const 
   const int cps = int(ceil_div(k_chunks, splits));
   splits = int(ceil_div(k_chunks, cps));
   float* part = static_cast<float*>(ctx_scratch(ctx, sizeof(float) * size_t(splits) * M * N));
-  const CUtensorMap ta = make_map(A, uint64_t(M), uint64_t(n_rows), uint64_t(lda), 32, 32,
+  const CUtensorMap ta = make_map(A, uint64_t(M), uint64_t(n_rows), uint64_t(lda), 32, tc::kBK,
                                   CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-  const CUtensorMap tb = make_map(B, uint64_t(N), uint64_t(n_rows), uint64_t(ldb), 32, 32,
+  const CUtensorMap tb = make_map(B, uint64_t(N), uint64_t(n_rows), uint64_t(ldb), 32, tc::kBK,
                                   CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   tc::Params p{};
   p.M = M;
@@ -485,6 +497,7 @@ float* tc_gemm_wgrad_partials(qgnn_ctx* ctx, const float* A, int64_t lda, const 
   p.out = part;
   p.ldo = N;
   p.relu = 0;
+  p.stages = stages_for(BN);
   launch<true>(ta, tb, tb, p, ctx->num_sms, s);
   *splits_out = splits;
   return part;
