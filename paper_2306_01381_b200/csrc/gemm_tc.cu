@@ -94,8 +94,8 @@ __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t
       "}\n" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
+// 16 consecutive accumulator columns of this thread's TMEM lane (no wait)
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
       "%12, %13, %14, %15}, [%16];"
@@ -103,9 +103,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
         "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
         "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 // SW128 shared-memory matrix descriptor (tcgen05 "version 1")
@@ -297,13 +297,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int row = m0 + 32 * q + lane;
       float* orow = p.out + (kMN ? int64_t(split) * p.M * p.N : 0) + int64_t(row) * p.ldo;
-      for (int c = 0; c < p.BN; c += 16) {
-        float v[16];
-        tmem_ld16(tmem_base + uint32_t(acc * p.tmem_cols + c) + (uint32_t(32 * q) << 16), v);
-        if (row < p.M) {
-          if (p.relu) {
+      // 4 TMEM loads (64 columns) in flight per wait, then ReLU + 16-byte stores
+      for (int c0 = 0; c0 < p.BN; c0 += 64) {
+        uint32_t r[4][16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = v[i] > 0.f ? v[i] : 0.f;
+        for (int u = 0; u < 4; ++u)
+          if (c0 + 16 * u < p.BN)
+            tmem_ld16_nowait(tmem_base + uint32_t(acc * p.tmem_cols + c0 + 16 * u) +
+                                 (uint32_t(32 * q) << 16),
+                             r[u]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + 16 * u;
+          if (c >= p.BN || row >= p.M) continue;
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            v[i] = __uint_as_float(r[u][i]);
+            if (p.relu) v[i] = v[i] > 0.f ? v[i] : 0.f;
           }
           if (c + 16 <= p.N && (p.ldo & 3) == 0) {
 #pragma unroll
