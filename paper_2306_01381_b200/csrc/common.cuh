@@ -82,10 +82,19 @@ float* tc_gemm_wgrad_partials(qgnn_ctx* ctx, const float* A, int64_t lda, const 
                               int64_t ldb, int M, int N, int64_t n_rows, int* splits_out,
                               cudaStream_t s);
 bool use_tc_gemm();
-// fp32 row-range SpMM with hub-row splitting (spmm.cu)
+// Hub rows of one SpMM call site, split into 256-edge segments (device arrays).
+struct HubPlan {
+  int64_t hub_deg = 0;        // rows with more neighbours than this are hubs
+  int64_t n_hubs = 0, n_segs = 0;
+  const int32_t* hubs = nullptr;     // [n_hubs] rows
+  const int32_t* seg_ptr = nullptr;  // [n_hubs + 1] segment range per hub
+  const int64_t* seg = nullptr;      // [n_segs][4] = a_begin, a_end, b_begin, b_end
+  float* part = nullptr;             // [n_segs][ldp] partial rows (workspace)
+  int64_t ldp = 0;
+};
+// fp32 row-range SpMM with segmented hub rows (spmm.cu)
 void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y, int64_t ldy,
               const float* sa, const int64_t* pa, const int32_t* ca, const float* aa,
               const int64_t* pb, const int32_t* cb, const float* ab, int64_t row_begin,
-              int64_t n_rows, float* out, int64_t ldo, const int32_t* hubs, int64_t n_hubs,
-              int64_t hub_deg, cudaStream_t s);
+              int64_t n_rows, float* out, int64_t ldo, const HubPlan* hp, cudaStream_t s);
 }  // namespace qgnn_b200

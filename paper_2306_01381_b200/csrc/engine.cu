@@ -269,9 +269,13 @@ class Engine final : public EngineBase {
     DBuf<double> loss;                  // [1]
     DBuf<unsigned long long> correct;   // [2]
     DBuf<double> ce_terms;
-    // rows (slots) with more than kHubDeg neighbours, per SpMM call site
-    DBuf<int32_t> hub_fc, hub_fm, hub_bwd, hub_part;
-    int64_t n_hub_fc = 0, n_hub_fm = 0, n_hub_bwd = 0, n_hub_part = 0;
+    // hub rows (slots) per SpMM call site, segmented (spmm.cu:k_spmm_hubseg)
+    struct Hubs {
+      DBuf<int32_t> rows, seg_ptr;
+      DBuf<int64_t> seg;
+      DBuf<float> part;
+      HubPlan plan;
+    } hub_fc, hub_fm, hub_bwd, hub_part;
   };
 
   int64_t ld_of(int64_t d) const { return round_up(d, 8); }
@@ -280,14 +284,52 @@ class Engine final : public EngineBase {
   // K4 dispatch: fp32 -> nnz-balanced row-range kernel with hub splitting (all
   // feature buffers are zero-padded to a multiple of 4 columns); fp64 -> the
   // reference-order kernel.  Returns the number of kernels launched.
+  // rows [r0, r1) whose (a + b) degree exceeds kHubDeg -> 256-edge segments
+  template <typename H>
+  void build_hubs(H& h, const std::vector<int64_t>& pa, const std::vector<int64_t>* pb, int64_t r0,
+                  int64_t r1, int64_t maxd) {
+    constexpr int64_t kSeg = 256;
+    std::vector<int32_t> rows, sptr{0};
+    std::vector<int64_t> seg;
+    for (int64_t r = r0; r < r1; ++r) {
+      const int64_t a0 = pa[r], a1 = pa[r + 1];
+      const int64_t b0 = pb ? (*pb)[r] : 0, b1 = pb ? (*pb)[r + 1] : 0;
+      const int64_t deg = (a1 - a0) + (b1 - b0);
+      if (deg <= kHubDeg) continue;
+      rows.push_back(int32_t(r));
+      for (int64_t e = 0; e < deg; e += kSeg) {  // edge positions in the (a ++ b) list
+        const int64_t f = std::min(deg, e + kSeg);
+        const int64_t la = a1 - a0;
+        seg.push_back(a0 + std::min(e, la));
+        seg.push_back(a0 + std::min(f, la));
+        seg.push_back(b0 + std::max<int64_t>(0, e - la));
+        seg.push_back(b0 + std::max<int64_t>(0, f - la));
+      }
+      sptr.push_back(int32_t(seg.size() / 4));
+    }
+    h.rows.upload(rows);
+    h.seg_ptr.upload(sptr);
+    h.seg.upload(seg);
+    const int64_t n_segs = int64_t(seg.size() / 4);
+    if constexpr (sizeof(T) == 4) h.part.alloc(std::max<int64_t>(1, n_segs) * maxd, false);
+    h.plan.hub_deg = kHubDeg;
+    h.plan.n_hubs = int64_t(rows.size());
+    h.plan.n_segs = n_segs;
+    h.plan.hubs = h.rows.p;
+    h.plan.seg_ptr = h.seg_ptr.p;
+    h.plan.seg = h.seg.p;
+    h.plan.part = reinterpret_cast<float*>(h.part.p);
+    h.plan.ldp = maxd;
+  }
+
   int spmm(int64_t dim, const T* x, int64_t ldx, const T* y, int64_t ldy, const T* sa,
            const int64_t* pa, const int32_t* ca, const T* aa, const int64_t* pb,
            const int32_t* cb, const T* ab, int64_t r0, int64_t n, T* out, int64_t ldo,
-           const int32_t* hubs, int64_t n_hubs) {
+           const HubPlan* hubs) {
     if constexpr (sizeof(T) == 4) {
       spmm_f32(ctx_, int(round_up(dim, 4)), x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, r0, n, out,
-               ldo, hubs, n_hubs, kHubDeg, s_main_);
-      return 1 + (n_hubs > 0 ? 1 : 0);
+               ldo, hubs, s_main_);
+      return 1 + (hubs && hubs->n_hubs > 0 ? 2 : 0);
     } else {
       const int st = qgnn_csr_aggregate(ctx_, dtype_, dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb,
                                         ab, nullptr, r0, n, out, ldo, s_main_);
@@ -592,25 +634,11 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
     D.loss.alloc(1);
     D.correct.alloc(2);
     D.ce_terms.alloc(std::max<int64_t>(1, D.n_train));
-    {
-      std::vector<int32_t> fc, fm, bw, pt;
-      for (int64_t g = 0; g < no; ++g) {
-        const int64_t ld = V.local_ptr[g + 1] - V.local_ptr[g];
-        const int64_t rd = V.remote_ptr[g + 1] - V.remote_ptr[g];
-        if (g < V.n_central && ld > kHubDeg) fc.push_back(int32_t(g));
-        if (g >= V.n_central && ld + rd > kHubDeg) fm.push_back(int32_t(g));
-        if (ld > kHubDeg) bw.push_back(int32_t(g));
-      }
-      for (int64_t k = 0; k < nr; ++k)
-        if (V.slot_ptr[k + 1] - V.slot_ptr[k] > kHubDeg) pt.push_back(int32_t(k));
-      D.hub_fc.upload(fc);
-      D.hub_fm.upload(fm);
-      D.hub_bwd.upload(bw);
-      D.hub_part.upload(pt);
-      D.n_hub_fc = int64_t(fc.size());
-      D.n_hub_fm = int64_t(fm.size());
-      D.n_hub_bwd = int64_t(bw.size());
-      D.n_hub_part = int64_t(pt.size());
+    if constexpr (sizeof(T) == 4) {
+      build_hubs(D.hub_fc, V.local_ptr, nullptr, 0, V.n_central, maxd);
+      build_hubs(D.hub_fm, V.local_ptr, &V.remote_ptr, V.n_central, no, maxd);
+      build_hubs(D.hub_bwd, V.local_ptr, nullptr, 0, no, maxd);
+      build_hubs(D.hub_part, V.slot_ptr, nullptr, 0, nr, maxd);
     }
     D.snd.resize(keys_.size());
     D.rcv.resize(keys_.size());
@@ -1085,8 +1113,7 @@ void Engine<T>::forward_layer(int l) {
     if (!nc) continue;
     kbegin(QGNN_K_SPMM_FWD);
     const int nk = spmm(din, D.h[t].p, ldi, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
-                        D.lafwd.p, nullptr, nullptr, nullptr, 0, nc, D.hagg[t].p, ldi, D.hub_fc.p,
-                        D.n_hub_fc);
+                        D.lafwd.p, nullptr, nullptr, nullptr, 0, nc, D.hagg[t].p, ldi, &D.hub_fc.plan);
     const double nnz = double(D.view.local_ptr[nc]);
     kend(QGNN_K_SPMM_FWD, nc * (16.0 + 2 * din * sizeof(T)) + nnz * (4 + sizeof(T)) +
                               double(D.view.num_owned) * din * sizeof(T), s_main_, nk);
@@ -1117,7 +1144,7 @@ void Engine<T>::forward_layer(int l) {
     kbegin(QGNN_K_SPMM_FWD);
     const int nk = spmm(din, D.h[t].p, ldi, D.halo.p, ldi, D.self_alpha.p, D.lptr.p, D.lcol.p,
                         D.lafwd.p, D.rptr.p, D.rslot.p, D.ralpha.p, nc, nm, D.hagg[t].p, ldi,
-                        D.hub_fm.p, D.n_hub_fm);
+                        &D.hub_fm.plan);
     const double nnz = double(D.view.local_ptr[nc + nm] - D.view.local_ptr[nc]) +
                        double(D.view.remote_nnz());
     kend(QGNN_K_SPMM_FWD, nm * (24.0 + 2 * din * sizeof(T)) + nnz * (4 + sizeof(T)) +
@@ -1182,7 +1209,7 @@ void Engine<T>::backward_layer(int l) {
       kbegin(QGNN_K_PARTIALS);
       const int nk = spmm(din, D.gbar.p, ldi, nullptr, 0, nullptr, D.sptr.p, D.srow.p, D.salpha.p,
                           nullptr, nullptr, nullptr, 0, D.view.num_remote, D.partials.p, ldi,
-                          D.hub_part.p, D.n_hub_part);
+                          &D.hub_part.plan);
       kend(QGNN_K_PARTIALS, double(D.view.num_remote) * (8 + din * sizeof(T)) +
                                 double(D.view.remote_nnz()) * (4 + sizeof(T) + din * sizeof(T)),
            s_main_, nk);
@@ -1215,8 +1242,7 @@ void Engine<T>::backward_layer(int l) {
          dtype_ == QGNN_F64 ? 1 : 2);
     kbegin(QGNN_K_SPMM_BWD);
     const int nk = spmm(din, D.gbar.p, ldi, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
-                        D.labwd.p, nullptr, nullptr, nullptr, 0, no, D.dh_next.p, ldi, D.hub_bwd.p,
-                        D.n_hub_bwd);
+                        D.labwd.p, nullptr, nullptr, nullptr, 0, no, D.dh_next.p, ldi, &D.hub_bwd.plan);
     kend(QGNN_K_SPMM_BWD, no * (16.0 + 2 * din * sizeof(T)) +
                               double(D.view.local_nnz()) * (4 + sizeof(T)) +
                               double(no) * din * sizeof(T), s_main_, nk);
@@ -1261,8 +1287,7 @@ void Engine<T>::forward_last_tf(int l) {
     if (!nc) continue;
     kbegin(QGNN_K_SPMM_FWD);
     const int nk = spmm(dout, D.dz.p, ldo, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
-                        D.lafwd.p, nullptr, nullptr, nullptr, 0, nc, D.h[l].p, ldo, D.hub_fc.p,
-                        D.n_hub_fc);
+                        D.lafwd.p, nullptr, nullptr, nullptr, 0, nc, D.h[l].p, ldo, &D.hub_fc.plan);
     kend(QGNN_K_SPMM_FWD, nc * (16.0 + 2 * dout * sizeof(T)) +
                               double(D.view.local_ptr[nc]) * (4 + sizeof(T)) +
                               double(no) * dout * sizeof(T), s_main_, nk);
@@ -1293,7 +1318,7 @@ void Engine<T>::forward_last_tf(int l) {
     kbegin(QGNN_K_SPMM_FWD);
     const int nk = spmm(dout, D.dz.p, ldo, D.partials.p, ldo, D.self_alpha.p, D.lptr.p, D.lcol.p,
                         D.lafwd.p, D.rptr.p, D.rslot.p, D.ralpha.p, nc, nm, D.h[l].p, ldo,
-                        D.hub_fm.p, D.n_hub_fm);
+                        &D.hub_fm.plan);
     const double nnz = double(D.view.local_ptr[nc + nm] - D.view.local_ptr[nc]) +
                        double(D.view.remote_nnz());
     kend(QGNN_K_SPMM_FWD, nm * (24.0 + 2 * dout * sizeof(T)) + nnz * (4 + sizeof(T)) +
@@ -1317,8 +1342,7 @@ void Engine<T>::backward_last_tf(int l) {
     if (nr) {
       kbegin(QGNN_K_PARTIALS);
       const int nk = spmm(dout, D.dh.p, ldo, nullptr, 0, nullptr, D.sptr.p, D.srow.p, D.salpha.p,
-                          nullptr, nullptr, nullptr, 0, nr, D.gpart.p, ldo, D.hub_part.p,
-                          D.n_hub_part);
+                          nullptr, nullptr, nullptr, 0, nr, D.gpart.p, ldo, &D.hub_part.plan);
       kend(QGNN_K_PARTIALS, double(nr) * (8 + dout * sizeof(T)) +
                                 double(D.view.remote_nnz()) * (4 + sizeof(T) + dout * sizeof(T)),
            s_main_, nk);
@@ -1335,8 +1359,7 @@ void Engine<T>::backward_last_tf(int l) {
     const int64_t no = D.view.num_owned, nr = D.view.num_remote;
     kbegin(QGNN_K_SPMM_BWD);
     const int nk = spmm(dout, D.dh.p, ldo, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
-                        D.labwd.p, nullptr, nullptr, nullptr, 0, no, D.gbar.p, ldo, D.hub_bwd.p,
-                        D.n_hub_bwd);
+                        D.labwd.p, nullptr, nullptr, nullptr, 0, no, D.gbar.p, ldo, &D.hub_bwd.plan);
     kend(QGNN_K_SPMM_BWD, no * (16.0 + 2 * dout * sizeof(T)) +
                               double(D.view.local_nnz()) * (4 + sizeof(T)) +
                               double(no) * dout * sizeof(T), s_main_, nk);

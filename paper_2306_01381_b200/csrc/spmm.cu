@@ -282,23 +282,75 @@ __global__ void __launch_bounds__(256) k_spmm_hubs(
   }
 }
 
+// Hub rows, segmented: each 256-edge segment of a hub row's (local, then
+// remote) edge list is one warp's work; partial rows are then added in segment
+// order with the self term (deterministic).  A 17k-neighbour hub becomes ~70
+// independent warps instead of one CTA.
+template <int NV>
+__global__ void __launch_bounds__(256) k_spmm_hubseg(
+    int dim, const float* __restrict__ x, int64_t ldx, const float* __restrict__ y, int64_t ldy,
+    const int32_t* __restrict__ ca, const float* __restrict__ aa, const int32_t* __restrict__ cb,
+    const float* __restrict__ ab, const int64_t* __restrict__ seg, int64_t n_segs,
+    float* __restrict__ part, int64_t ldp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (g >= n_segs) return;
+  const int nvec = dim >> 2;
+  const int64_t* sg = seg + 4 * g;  // [a0, a1, b0, b1]
+  float acc[NV][4];
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[i][q] = 0.f;
+  row_gather4<NV>(acc, x, ldx, sg[0], sg[1], ca, aa, lane, nvec);
+  if (sg[3] > sg[2]) row_gather4<NV>(acc, y, ldy, sg[2], sg[3], cb, ab, lane, nvec);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int cv = lane + 32 * i;
+    if (cv < nvec) vstore<float, 4>(part + g * ldp + cv * 4, acc[i]);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_spmm_hubred(
+    int dim, const float* __restrict__ x, int64_t ldx, const float* __restrict__ self_alpha,
+    const int32_t* __restrict__ hubs, const int32_t* __restrict__ seg_ptr, int64_t n_hubs,
+    const float* __restrict__ part, int64_t ldp, float* __restrict__ out, int64_t ldo) {
+  const int lane = threadIdx.x & 31;
+  const int64_t h = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (h >= n_hubs) return;
+  const int64_t r = hubs[h];
+  const float sa = self_alpha ? self_alpha[r] : 0.f;
+  for (int c = lane * 4; c < dim; c += 128) {
+    float4 v = self_alpha ? *reinterpret_cast<const float4*>(x + r * ldx + c) : make_float4(0, 0, 0, 0);
+    v.x *= sa, v.y *= sa, v.z *= sa, v.w *= sa;
+    for (int s = seg_ptr[h]; s < seg_ptr[h + 1]; ++s) {
+      const float4 p = *reinterpret_cast<const float4*>(part + int64_t(s) * ldp + c);
+      v.x += p.x, v.y += p.y, v.z += p.z, v.w += p.w;
+    }
+    *reinterpret_cast<float4*>(out + r * ldo + c) = v;
+  }
+}
+
 // fp32 row-range SpMM with optional hub list (rows with > hub_deg neighbours).
 void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y, int64_t ldy,
               const float* sa, const int64_t* pa, const int32_t* ca, const float* aa,
               const int64_t* pb, const int32_t* cb, const float* ab, int64_t row_begin,
-              int64_t n_rows, float* out, int64_t ldo, const int32_t* hubs, int64_t n_hubs,
-              int64_t hub_deg, cudaStream_t s) {
+              int64_t n_rows, float* out, int64_t ldo, const HubPlan* hp, cudaStream_t s) {
   if (n_rows <= 0) return;
   const int nv = int(ceil_div(dim / 4, 32));
   const int64_t blocks = ceil_div(n_rows, 8);
-  const int64_t hd = hubs ? hub_deg : (int64_t(1) << 62);
+  const bool hubs = hp && hp->n_hubs > 0;
+  const int64_t hd = hubs ? hp->hub_deg : (int64_t(1) << 62);
 #define QGNN_SPMM_CASE(NVV)                                                                    \
   case NVV:                                                                                    \
     k_spmm_f32<NVV><<<unsigned(blocks), 256, 0, s>>>(dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, \
                                                      ab, row_begin, n_rows, out, ldo, hd);       \
-    if (hubs && n_hubs > 0)                                                                    \
-      k_spmm_hubs<NVV><<<unsigned(n_hubs), 256, 8 * NVV * 128 * sizeof(float), s>>>(           \
-          dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, hubs, out, ldo);                    \
+    if (hubs) {                                                                                \
+      k_spmm_hubseg<NVV><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(             \
+          dim, x, ldx, y, ldy, ca, aa, cb, ab, hp->seg, hp->n_segs, hp->part, hp->ldp);        \
+      k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 256)), 256, 0, s>>>(                  \
+          dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo);    \
+    }                                                                                          \
     break;
   switch (nv) {
     QGNN_SPMM_CASE(1)
@@ -356,7 +408,7 @@ extern "C" int qgnn_csr_aggregate(qgnn_ctx* ctx, int dtype, int64_t dim, const v
                static_cast<const float*>(self_alpha), ptr_a, col_a,
                static_cast<const float*>(alpha_a), ptr_b, col_b,
                static_cast<const float*>(alpha_b), row_begin, n_rows, static_cast<float*>(out),
-               ld_out, nullptr, 0, 0, s);
+               ld_out, nullptr, s);
     } else if (vec4) {
       const int nv = pick_nv(dim / 4);
       launch_csr<float, 4>(nv, d, static_cast<const float*>(x), ld_x,
