@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -241,6 +242,85 @@ __global__ void __launch_bounds__(256, (NV <= 2 ? 3 : 1)) k_spmm_f32(
   }
 }
 
+// Narrow rows (dim <= 128, one float4 per lane): the full-row kernel would
+// keep only 4 gathers of <= 400 B per warp in flight and leave lanes idle for
+// dim < 128.  Here G = dim/4 lanes cover one row and E = 32/G lane groups take
+// consecutive edges round-robin, 8 steps per round, so every lane has 8
+// independent 16-byte gathers in flight (the L2 gather ceiling needs ~8,
+// profiles/gather_probe.cu).  Groups meet in a fixed order at the end
+// (deterministic); self term first, then the local and remote lists.
+__device__ __forceinline__ void grp_gather(float4& acc, const float* __restrict__ src, int64_t ld,
+                                           int64_t beg, int64_t end,
+                                           const int32_t* __restrict__ col,
+                                           const float* __restrict__ alpha, int lane, int grp,
+                                           int E, bool act) {
+  for (int64_t e0 = beg; e0 < end; e0 += 32) {
+    const int cnt = end - e0 < 32 ? static_cast<int>(end - e0) : 32;
+    int my_c = 0;
+    float my_a = 0.f;
+    if (lane < cnt) {
+      my_c = __ldg(col + e0 + lane);
+      my_a = __ldg(alpha + e0 + lane);
+    }
+    for (int j = 0; j < cnt; j += 8 * E) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = j + u * E + grp;
+        const int c = __shfl_sync(0xffffffffu, my_c, k & 31);
+        v[u] = (act && k < cnt) ? __ldg(reinterpret_cast<const float4*>(src + int64_t(c) * ld))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float a = __shfl_sync(0xffffffffu, my_a, (j + u * E + grp) & 31);
+        acc.x = fmaf(a, v[u].x, acc.x);
+        acc.y = fmaf(a, v[u].y, acc.y);
+        acc.z = fmaf(a, v[u].z, acc.z);
+        acc.w = fmaf(a, v[u].w, acc.w);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 4) k_spmm_f32g(
+    int dim, const float* __restrict__ x, int64_t ldx, const float* __restrict__ y, int64_t ldy,
+    const float* __restrict__ self_alpha, const int64_t* __restrict__ pa,
+    const int32_t* __restrict__ ca, const float* __restrict__ aa, const int64_t* __restrict__ pb,
+    const int32_t* __restrict__ cb, const float* __restrict__ ab, int64_t r0, int64_t n_rows,
+    float* __restrict__ out, int64_t ldo, int64_t hub_deg) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = dim >> 2, E = 32 / G;
+  const int grp = lane / G, sub = lane - grp * G;
+  const bool act = grp < E;
+  const int64_t r = r0 + int64_t(blockIdx.x) * 8 + warp;
+  if (r >= r0 + n_rows) return;
+  const int64_t ea0 = pa[r], ea1 = pa[r + 1];
+  const int64_t eb0 = pb ? pb[r] : 0, eb1 = pb ? pb[r + 1] : 0;
+  if ((ea1 - ea0) + (eb1 - eb0) > hub_deg) return;  // k_spmm_hubseg + k_spmm_hubred
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  grp_gather(acc, x + sub * 4, ldx, ea0, ea1, ca, aa, lane, grp, E, act);
+  if (pb) grp_gather(acc, y + sub * 4, ldy, eb0, eb1, cb, ab, lane, grp, E, act);
+  const float4 mine = acc;  // group g's partial -> group 0, g ascending
+  for (int g = 1; g < E; ++g) {
+    const int sl = (lane + g * G) & 31;
+    acc.x += __shfl_sync(0xffffffffu, mine.x, sl);
+    acc.y += __shfl_sync(0xffffffffu, mine.y, sl);
+    acc.z += __shfl_sync(0xffffffffu, mine.z, sl);
+    acc.w += __shfl_sync(0xffffffffu, mine.w, sl);
+  }
+  if (grp == 0) {
+    float4 o = acc;
+    if (self_alpha) {
+      const float sa = self_alpha[r];
+      const float4 xv = __ldg(reinterpret_cast<const float4*>(x + r * ldx + sub * 4));
+      o = make_float4(fmaf(sa, xv.x, acc.x), fmaf(sa, xv.y, acc.y), fmaf(sa, xv.z, acc.z),
+                      fmaf(sa, xv.w, acc.w));
+    }
+    *reinterpret_cast<float4*>(out + r * ldo + sub * 4) = o;
+  }
+}
+
 // One CTA per hub row: 8 warps take contiguous eighths of the edge lists,
 // partial sums meet in shared memory and are added in warp order (deterministic).
 template <int NV>
@@ -331,6 +411,14 @@ __global__ void __launch_bounds__(256) k_spmm_hubred(
   }
 }
 
+static bool grouped_narrow() {  // QGNN_SPMM_GROUPED=0 selects the one-row-per-warp kernel
+  static const bool on = [] {
+    const char* e = std::getenv("QGNN_SPMM_GROUPED");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 // fp32 row-range SpMM with optional hub list (rows with > hub_deg neighbours).
 void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y, int64_t ldy,
               const float* sa, const int64_t* pa, const int32_t* ca, const float* aa,
@@ -352,6 +440,18 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
           dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo);    \
     }                                                                                          \
     break;
+  if (nv == 1 && grouped_narrow()) {
+    k_spmm_f32g<<<unsigned(blocks), 256, 0, s>>>(dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab,
+                                                 row_begin, n_rows, out, ldo, hd);
+    if (hubs) {
+      k_spmm_hubseg<1><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(
+          dim, x, ldx, y, ldy, ca, aa, cb, ab, hp->seg, hp->n_segs, hp->part, hp->ldp);
+      k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 256)), 256, 0, s>>>(
+          dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo);
+    }
+    check_launch("k_spmm_f32g");
+    return;
+  }
   switch (nv) {
     QGNN_SPMM_CASE(1)
     QGNN_SPMM_CASE(2)
