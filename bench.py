@@ -237,6 +237,17 @@ def impl_ours(args):
     # pinned host memory, one epoch, loss/accuracy read back to the host
     feats = torch.from_numpy(np.ascontiguousarray(g["features"], np.float32)).pin_memory()
     h2d = feats.numel() * feats.element_size()
+    # raw pinned H2D bandwidth of this box (context for the e2e number)
+    dev_copy = torch.empty_like(feats, device="cuda")
+    dev_copy.copy_(feats, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    dev_copy.copy_(feats, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    h2d_gbs = h2d / (e0.elapsed_time(e1) / 1e3) / 1e9
+    del dev_copy
     barrier(world)
     t0 = time.time()
     for _ in range(max(3, args.steps // 2)):
@@ -285,7 +296,7 @@ def impl_ours(args):
             "data": "synthetic", "config": config_dict(world, bit_mode),
             "wall_s_per_step": wall_s,
             "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": 8 * 3},
+                    "d2h_bytes_per_step": 8 * 3, "h2d_gbs_raw": h2d_gbs},
             "gpu_launches": launches * args.steps,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,

@@ -215,7 +215,12 @@ int qgnn_engine_create(const qgnn_settings* s, int64_t n_nodes, const int64_t* a
 int qgnn_engine_destroy(qgnn_engine* e);
 /* One epoch (run_epoch, engine.hpp:384-426). */
 int qgnn_engine_run_epoch(qgnn_engine* e, qgnn_epoch_metrics* out);
-/* Re-upload node features of this rank's parts from host memory (f32/f64). */
+/* Re-upload node features (n_nodes x F, f32/f64, node order).  From pinned
+ * (or device) memory the copy is asynchronous: node-range chunks stream in on a
+ * copy stream and the next run_epoch gathers each partition as soon as its
+ * chunk has landed, overlapping the upload with the first layer; `features`
+ * must stay valid until that run_epoch returns.  From pageable memory the call
+ * stages through pinned memory and returns after the upload. */
 int qgnn_engine_set_features(qgnn_engine* e, const void* features);
 /* Weights of layer l (din x dout, settings dtype) to host memory. */
 int qgnn_engine_get_weights(qgnn_engine* e, int layer, void* out);

@@ -267,30 +267,62 @@ __global__ void __launch_bounds__(256) k_dequant_scatter(
 // or 4 bytes per chunk and a warp instruction writes a contiguous run.  The
 // draw counter of element e is e + 1; consecutive elements advance the
 // generator input by +phi (64-bit add) instead of a multiply.
-__device__ __forceinline__ uint32_t quant_code(float h, double lo_d, double scale, double rcp,
-                                               double lv, uint64_t z) {
-  // z = key + (e + 1) * phi, i.e. the input of rng_mix for counter e + 1.
-  // Reference: x = RN((h - lo) / S), base = floor(x), frac = x - base,
-  // base += (u < frac), clamp (quant.hpp:81-87).  Fast path: x' = RN(a * RN(1/S))
-  // satisfies |x' - x| < 2^-43 for x <= 255, so floor(x') == floor(x) and
-  // (u < frac') == (u < frac) whenever frac' and u - frac' stay 2^-40 away from
-  // the decision boundaries; otherwise (probability ~1e-12, and each row's
-  // extremum) the exact division decides.  Codes are identical either way.
+// Element math.  Reference: x = RN((h - lo) / S), base = floor(x),
+// frac = x - base, base += (u < frac), code = min(base, levels) (quant.hpp:81-87).
+// Fast path: x' = RN(a * RN(1/S)) satisfies |x' - x| < 2^-43 for x <= 255, so
+// floor(x') == floor(x) and (u < frac') == (u < frac) whenever frac' and
+// u - frac' stay 2^-40 away from the decision boundaries.  h == lo gives x = 0
+// exactly (code 0); h == hi uses x_hi = RN((hi - lo) / S), computed once per
+// message with the exact division.  Anything else within 2^-40 of a boundary
+// (probability ~1e-12 per element) is flagged and recomputed by quant_exact.
+// The draw u = (mix(z) >> 11) * 2^-53 with z = key + (e + 1) * phi.
+struct QRow {
+  double lo, scale, rcp, x_hi;
+  float hi;
+  uint32_t levels;
+};
+
+__device__ __forceinline__ uint32_t quant_fast(float h, const QRow& R, uint64_t z, bool& slow) {
+  constexpr double tol = 0x1.0p-40;
+  const double a = __dsub_rn(static_cast<double>(h), R.lo);
+  const double u = static_cast<double>(rng_mix(z) >> 11) * 0x1.0p-53;
+  const bool top = h == R.hi;
+  const double x = top ? R.x_hi : __dmul_rn(a, R.rcp);
+  const double base = floor(x);
+  const double frac = __dsub_rn(x, base);
+  const double d = fabs(u - frac);
+  slow = !top && a != 0.0 && !(frac >= tol && frac <= 1.0 - tol && d > tol);
+  const uint32_t code = static_cast<uint32_t>(base) + (u < frac ? 1u : 0u);
+  return code < R.levels ? code : R.levels;
+}
+
+__device__ __noinline__ uint32_t quant_exact(float h, double lo_d, double scale, double lv,
+                                             uint64_t z) {
   const double a = __dsub_rn(static_cast<double>(h), lo_d);
   const double u = static_cast<double>(rng_mix(z) >> 11) * 0x1.0p-53;
-  if (a == 0.0) return 0u;  // x = 0 exactly, frac = 0, u < 0 false
-  constexpr double tol = 0x1.0p-40;
-  double x = __dmul_rn(a, rcp);
+  const double x = __ddiv_rn(a, scale);
   double base = floor(x);
-  double frac = __dsub_rn(x, base);
-  const double d = u - frac;
-  if (!(frac >= tol && frac <= 1.0 - tol && (d > tol || d < -tol))) {
-    x = __ddiv_rn(a, scale);
-    base = floor(x);
-    frac = __dsub_rn(x, base);
-  }
+  const double frac = __dsub_rn(x, base);
   if (u < frac) base = __dadd_rn(base, 1.0);
   return static_cast<uint32_t>(base < lv ? base : lv);
+}
+
+// First-occurrence signed zero from registers (quant.hpp:63-68 keeps the FIRST
+// element equal to the extremum; only +0.0 vs -0.0 can differ): the lowest
+// element index holding a zero, warp-wide, and that element's sign.
+template <int NV>
+__device__ __forceinline__ float first_zero_reg(const float (&v)[NV][4], int lane, int dim) {
+  int key = 0x7fffffff;  // (index << 1) | sign
+#pragma unroll
+  for (int i = NV - 1; i >= 0; --i)
+#pragma unroll
+    for (int q = 3; q >= 0; --q) {
+      const int e = 4 * (lane + 32 * i) + q;
+      if (e < dim && v[i][q] == 0.f) key = (e << 1) | int(__float_as_uint(v[i][q]) >> 31);
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
+  return (key & 1) ? -0.f : 0.f;
 }
 
 template <int NV>
@@ -336,8 +368,11 @@ __global__ void __launch_bounds__(256) k_quantize_pack_f32(
     hi = hi < h2 ? h2 : hi;
   }
   finite = __all_sync(0xffffffffu, finite);
-  if (lo == 0.f) lo = first_zero(row, dim, lane);  // signed-zero first occurrence
-  if (hi == 0.f) hi = first_zero(row, dim, lane);
+  if (lo == 0.f || hi == 0.f) {  // signed-zero first occurrence, from registers
+    const float z0 = first_zero_reg<NV>(v, lane, dim);
+    if (lo == 0.f) lo = z0;
+    if (hi == 0.f) hi = z0;
+  }
   if (lane == 0 && win_lo) {
     const float wl = win_lo[m], wh = win_hi[m];
     win_lo[m] = lo < wl ? lo : wl;
@@ -372,19 +407,39 @@ __global__ void __launch_bounds__(256) k_quantize_pack_f32(
   const int padded = static_cast<int>(((packed_bytes(dim, b) + 15) / 16) * 16);
   const int units = padded * 2 / b;  // chunk-sized store units incl. zero padding
   const uint64_t key = rng_fork(set_keys[set_of ? set_of[m] : 0], ids[m]);
-  const double lv = static_cast<double>(levels);
-  const double rcp = constant ? 0.0 : __drcp_rn(scale);
+  QRow R;
+  R.lo = lo_d;
+  R.scale = scale;
+  R.rcp = constant ? 0.0 : __drcp_rn(scale);
+  R.x_hi = constant ? 0.0 : __ddiv_rn(__dsub_rn(hi_d, lo_d), scale);
+  R.hi = hi;
+  R.levels = levels;
 #pragma unroll
   for (int i = 0; i < NV + 1; ++i) {
     const int c = lane + 32 * i;
     if (c >= units) break;
     uint32_t word = 0;
     if (i < NV && c < nchunk && !constant) {
-      uint64_t z = key + static_cast<uint64_t>(4 * c + 1) * kPhi;
+      const uint64_t z0 = key + static_cast<uint64_t>(4 * c + 1) * kPhi;
+      uint64_t z = z0;
+      uint32_t slow_mask = 0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        if (4 * c + q < dim) word |= quant_code(v[i][q], lo_d, scale, rcp, lv, z) << (q * b);
+        bool sl;
+        const uint32_t code = quant_fast(v[i][q], R, z, sl);
+        if (4 * c + q < dim) {
+          word |= code << (q * b);
+          slow_mask |= uint32_t(sl) << q;
+        }
         z += kPhi;
+      }
+      if (slow_mask) {  // ~1e-12 per element: exact division for the flagged ones
+        const double lv = static_cast<double>(levels);
+        for (int q = 0; q < 4; ++q)
+          if (slow_mask >> q & 1) {
+            const uint32_t code = quant_exact(v[i][q], lo_d, scale, lv, z0 + uint64_t(q) * kPhi);
+            word = (word & ~(((1u << b) - 1) << (q * b))) | (code << (q * b));
+          }
       }
     }
     if (b == 8)

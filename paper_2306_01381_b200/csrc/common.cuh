@@ -58,6 +58,11 @@ struct Arith<float> {
 
 struct Ctx;  // defined in ctx.cu
 
+// fp32 loss phase for the engine: CE over train rows + val/test hit counts (dense.cu)
+void loss_f32(qgnn_ctx* ctx, const float* logits, int64_t ld, int classes, const int32_t* labels,
+              const int32_t* rows, int64_t n_train, int64_t n_val, int64_t n_test,
+              double inv_denom, float* grad, int64_t ldg, double* loss_acc,
+              unsigned long long* correct, cudaStream_t s);
 }  // namespace qgnn_b200
 
 struct qgnn_ctx {
@@ -97,4 +102,9 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
               const float* sa, const int64_t* pa, const int32_t* ca, const float* aa,
               const int64_t* pb, const int32_t* cb, const float* ab, int64_t row_begin,
               int64_t n_rows, float* out, int64_t ldo, const HubPlan* hp, cudaStream_t s);
+// fp32 loss phase for the engine: CE over train rows + val/test hit counts (dense.cu)
+void loss_f32(qgnn_ctx* ctx, const float* logits, int64_t ld, int classes, const int32_t* labels,
+              const int32_t* rows, int64_t n_train, int64_t n_val, int64_t n_test,
+              double inv_denom, float* grad, int64_t ldg, double* loss_acc,
+              unsigned long long* correct, cudaStream_t s);
 }  // namespace qgnn_b200

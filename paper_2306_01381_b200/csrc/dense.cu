@@ -293,6 +293,93 @@ __global__ void k_count_correct(const T* __restrict__ logits, int64_t ld, int cl
   if ((threadIdx.x & 31) == 0 && total) atomicAdd(acc, static_cast<unsigned long long>(total));
 }
 
+// Production fp32 loss phase in one launch per partition (model.hpp:172-227):
+// rows = [train | val | test] of the partition; warp per row.  Train rows:
+// softmax cross-entropy in fp32 (max, sum of expf, logf), the loss term in
+// fp64 and the gradient (softmax - onehot) / n_train_global written to grad;
+// val / test rows: first-argmax hit counts.  Each block adds its 8 warp terms
+// in warp order into block_part[blockIdx.x] (a fixed-order tree over blocks
+// follows), so the loss is deterministic.
+__global__ void __launch_bounds__(256) k_loss_f32(
+    const float* __restrict__ logits, int64_t ld, int classes, const int32_t* __restrict__ labels,
+    const int32_t* __restrict__ rows, int64_t n_train, int64_t n_val, int64_t n_test,
+    double inv_denom, float* __restrict__ grad, int64_t ldg, double* __restrict__ block_part,
+    unsigned long long* __restrict__ correct, int* __restrict__ err) {
+  __shared__ double wterm[8];
+  __shared__ unsigned whit[8][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t k = int64_t(blockIdx.x) * 8 + warp;
+  const int64_t n_all = n_train + n_val + n_test;
+  double term = 0.0;
+  unsigned hit_v = 0, hit_t = 0;
+  if (k < n_all) {
+    const int64_t r = rows[k];
+    const float* row = logits + r * ld;
+    const int y = labels[r];
+    if (y < 0 || y >= classes) {
+      if (lane == 0) atomicOr(err, kErrLabel);
+    } else if (k < n_train) {
+      float hi = -INFINITY;
+      for (int c = lane; c < classes; c += 32) hi = fmaxf(hi, row[c]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      float sum = 0.f;
+      for (int c = lane; c < classes; c += 32) sum += expf(row[c] - hi);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      const float lse = hi + logf(sum);
+      term = (static_cast<double>(lse) - static_cast<double>(row[y])) * inv_denom;
+      const float sc = static_cast<float>(inv_denom);
+      float* g = grad + r * ldg;
+      for (int c = lane; c < classes; c += 32)
+        g[c] = (expf(row[c] - lse) - (c == y ? 1.f : 0.f)) * sc;
+    } else {
+      // first argmax (model.hpp:216-227): larger value wins, ties -> lower index
+      float best = -INFINITY;
+      int bi = 0x7fffffff;
+      for (int c = lane; c < classes; c += 32)
+        if (row[c] > best) best = row[c], bi = c;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) best = ob, bi = oi;
+      }
+      const unsigned hit = bi == y;
+      if (k < n_train + n_val) hit_v = hit; else hit_t = hit;
+    }
+  }
+  if (lane == 0) {
+    wterm[warp] = term;
+    whit[warp][0] = hit_v;
+    whit[warp][1] = hit_t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    unsigned hv = 0, ht = 0;
+    for (int w = 0; w < 8; ++w) t += wterm[w], hv += whit[w][0], ht += whit[w][1];
+    block_part[blockIdx.x] = t;
+    if (hv) atomicAdd(correct, static_cast<unsigned long long>(hv));
+    if (ht) atomicAdd(correct + 1, static_cast<unsigned long long>(ht));
+  }
+}
+
+void loss_f32(qgnn_ctx* ctx, const float* logits, int64_t ld, int classes, const int32_t* labels,
+              const int32_t* rows, int64_t n_train, int64_t n_val, int64_t n_test,
+              double inv_denom, float* grad, int64_t ldg, double* loss_acc,
+              unsigned long long* correct, cudaStream_t s) {
+  const int64_t n_all = n_train + n_val + n_test;
+  if (!n_all) return;
+  const int64_t blocks = ceil_div(n_all, 8);
+  double* part = static_cast<double*>(ctx_scratch(ctx, sizeof(double) * blocks));
+  k_loss_f32<<<unsigned(blocks), 256, 0, s>>>(logits, ld, classes, labels, rows, n_train, n_val,
+                                              n_test, inv_denom, grad, ldg, part, correct,
+                                              ctx->d_err);
+  k_sum_fixed<<<1, 1024, 0, s>>>(part, blocks, loss_acc);
+  check_launch("loss_f32");
+}
+
 // optim.hpp:47-62
 template <typename T>
 __global__ void k_adam(T* __restrict__ p, T* __restrict__ m, T* __restrict__ v,

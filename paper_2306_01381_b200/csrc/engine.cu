@@ -238,7 +238,7 @@ class Engine final : public EngineBase {
     DBuf<int64_t> lptr, rptr, sptr;
     DBuf<int32_t> lcol, rslot, srow;
     DBuf<T> lafwd, labwd, ralpha, salpha, self_alpha;
-    DBuf<int32_t> labels, train_rows, val_rows, test_rows, ref_order;
+    DBuf<int32_t> labels, train_rows, val_rows, test_rows, loss_rows, ref_order;
     int64_t n_train = 0, n_val = 0, n_test = 0;
     // activations
     std::vector<DBuf<T>> h, hagg;  // h[0..L], hagg[0..L-1]
@@ -410,6 +410,17 @@ class Engine final : public EngineBase {
   T* pinned_ = nullptr;
   size_t pinned_elems_ = 0;
   DBuf<T> feat_all_;  // node-ordered features (pinned-input fast path)
+  // async feature upload: node-range chunks on s_copy_, one event per chunk;
+  // partition p's gather waits for the chunk holding its largest node id
+  cudaStream_t s_copy_ = nullptr;
+  cudaEvent_t ev_main_done_ = nullptr;
+  std::vector<int64_t> feat_bounds_;    // chunk c = nodes [bounds[c], bounds[c + 1])
+  std::vector<cudaEvent_t> ev_feat_;    // per chunk
+  std::vector<int> part_chunk_;         // local partition -> chunk it waits for
+  bool feat_pending_ = false;
+  void gather_features(PartDev& D);
+  bool bits_dirty_ = true;
+  void recount_bits();
   // per-epoch message counters
   uint64_t msgs_b_[4] = {0, 0, 0, 0};
   double resolve_seconds_ = 0;
@@ -493,6 +504,8 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
   QGNN_CUDA(cudaEventCreateWithFlags(&ev_q_, cudaEventDisableTiming));
   QGNN_CUDA(cudaEventCreateWithFlags(&ev_c_, cudaEventDisableTiming));
   QGNN_CUDA(cudaEventCreateWithFlags(&ev_d_, cudaEventDisableTiming));
+  QGNN_CUDA(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking));
+  QGNN_CUDA(cudaEventCreateWithFlags(&ev_main_done_, cudaEventDisableTiming));
   if (s.world > 1) {
     QGNN_REQUIRE(nccl_id, QGNN_EINVAL, "engine: world > 1 needs an NCCL unique id");
     if (std::memcmp(nccl_id, kLoopMagic, 8) == 0) {
@@ -609,6 +622,12 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
     D.train_rows.upload(tr);
     D.val_rows.upload(va);
     D.test_rows.upload(te);
+    {
+      std::vector<int32_t> all(tr);
+      all.insert(all.end(), va.begin(), va.end());
+      all.insert(all.end(), te.begin(), te.end());
+      D.loss_rows.upload(all);
+    }
     D.n_train = int64_t(tr.size());
     D.n_val = int64_t(va.size());
     D.n_test = int64_t(te.size());
@@ -643,7 +662,34 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
     D.snd.resize(keys_.size());
     D.rcv.resize(keys_.size());
   }
+  {  // feature-upload chunks: boundaries at each local partition's largest node id
+    std::vector<int64_t> ends;
+    for (auto& up : parts_dev_) {
+      int64_t mx = -1;
+      for (uint32_t nd : up->view.row_node) mx = std::max<int64_t>(mx, nd);
+      ends.push_back(mx + 1);
+    }
+    std::vector<int64_t> b = ends;
+    b.push_back(n_nodes_);
+    std::sort(b.begin(), b.end());
+    b.erase(std::unique(b.begin(), b.end()), b.end());
+    feat_bounds_.assign(1, 0);
+    for (int64_t x : b)
+      if (x > feat_bounds_.back()) feat_bounds_.push_back(x);
+    ev_feat_.assign(feat_bounds_.size() - 1, nullptr);
+    for (auto& e : ev_feat_) QGNN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    part_chunk_.clear();
+    for (int64_t e : ends) {
+      int c = 0;
+      while (c + 1 < int(ev_feat_.size()) && feat_bounds_[c + 1] < e) ++c;
+      part_chunk_.push_back(c);
+    }
+  }
   set_features(features);
+  if (feat_pending_) {  // construction consumes the features right away
+    for (auto& up : parts_dev_) gather_features(*up);
+    feat_pending_ = false;
+  }
 
   // weights: GnnModel::init (model.hpp:27-41), replicated on every rank
   woff_.assign(L_ + 1, 0);
@@ -702,6 +748,10 @@ Engine<T>::~Engine() {
   if (ev_q_) cudaEventDestroy(ev_q_);
   if (s_main_) cudaStreamDestroy(s_main_);
   if (s_comm_) cudaStreamDestroy(s_comm_);
+  if (s_copy_) cudaStreamDestroy(s_copy_);
+  for (auto e : ev_feat_)
+    if (e) cudaEventDestroy(e);
+  if (ev_main_done_) cudaEventDestroy(ev_main_done_);
   if (ctx_) qgnn_ctx_destroy(ctx_);
 }
 
@@ -725,20 +775,21 @@ void Engine<T>::set_features(const void* f) {
                       (attr.type == cudaMemoryTypeHost || attr.type == cudaMemoryTypeDevice);
   cudaGetLastError();
   if (pinned) {
-    // one async copy of the node-ordered matrix from pinned (or device) memory,
-    // then a gather into partition row order on the GPU
+    // node-range chunks copied asynchronously on s_copy_ (after the previous
+    // epoch's readers of feat_all_); the epoch's first layer gathers partition
+    // p into row order as soon as p's chunk has landed (gather_features), so
+    // the upload overlaps the first layer's work.  The caller keeps `f` alive
+    // until the next run_epoch returns.
     if (!feat_all_.p || feat_all_.n < size_t(n_nodes_ * F)) feat_all_.alloc(n_nodes_ * F, false);
-    QGNN_CUDA(cudaMemcpyAsync(feat_all_.p, src, n_nodes_ * F * sizeof(T), cudaMemcpyDefault,
-                              s_main_));
-    for (auto& up : parts_dev_) {
-      PartDev& D = *up;
-      const int64_t no = D.view.num_owned;
-      k_gather_rows<T><<<unsigned(ceil_div(no * F, 256)), 256, 0, s_main_>>>(
-          feat_all_.p, F, D.row_node_d.p, no, D.h[0].p, ld);
-      ++launches_;
+    QGNN_CUDA(cudaEventRecord(ev_main_done_, s_main_));
+    QGNN_CUDA(cudaStreamWaitEvent(s_copy_, ev_main_done_, 0));
+    for (size_t c = 0; c + 1 < feat_bounds_.size(); ++c) {
+      const int64_t a = feat_bounds_[c], b = feat_bounds_[c + 1];
+      QGNN_CUDA(cudaMemcpyAsync(feat_all_.p + a * F, src + a * F, size_t(b - a) * F * sizeof(T),
+                                cudaMemcpyDefault, s_copy_));
+      QGNN_CUDA(cudaEventRecord(ev_feat_[c], s_copy_));
     }
-    check_launch("k_gather_rows");
-    QGNN_CUDA(cudaStreamSynchronize(s_main_));
+    feat_pending_ = true;
     return;
   }
   size_t total = 0;
@@ -774,6 +825,46 @@ void Engine<T>::set_features(const void* f) {
   QGNN_CUDA(cudaStreamSynchronize(s_main_));
 }
 
+// warp per row, 16-byte vectors (rows of F % 4 == 0 fp32 features)
+__global__ void k_gather_rows4(const float4* __restrict__ feats, int64_t f4,
+                               const int32_t* __restrict__ node, int64_t n, float4* __restrict__ out,
+                               int64_t ld4) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; g < n; g += wstride) {
+    const float4* src = feats + int64_t(node[g]) * f4;
+    for (int64_t j = lane; j < f4; j += 32) out[g * ld4 + j] = __ldg(src + j);
+  }
+}
+
+template <typename T>
+void Engine<T>::gather_features(PartDev& D) {
+  const int64_t F = dims_[0], ld = ld_of(F), no = D.view.num_owned;
+  QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_feat_[part_chunk_[D.id - p0_]], 0));
+  if (sizeof(T) == 4 && F % 4 == 0)
+    k_gather_rows4<<<unsigned(std::min<int64_t>(ceil_div(no, 8), int64_t(ctx_->num_sms) * 16)), 256,
+                     0, s_main_>>>(reinterpret_cast<const float4*>(feat_all_.p), F / 4,
+                                   D.row_node_d.p, no, reinterpret_cast<float4*>(D.h[0].p), ld / 4);
+  else
+    k_gather_rows<T><<<unsigned(ceil_div(no * F, 256)), 256, 0, s_main_>>>(feat_all_.p, F,
+                                                                          D.row_node_d.p, no,
+                                                                          D.h[0].p, ld);
+  check_launch("k_gather_rows");
+  ++launches_;
+}
+
+template <typename T>
+void Engine<T>::recount_bits() {
+  msgs_b_[0] = msgs_b_[1] = msgs_b_[2] = msgs_b_[3] = 0;
+  for (size_t k = 0; k < keys_.size(); ++k)
+    for (int64_t p = 0; p < P_; ++p)
+      for (int64_t q = 0; q < P_; ++q) {
+        if (p == q) continue;
+        for (uint8_t b : msgs_[k][p][q].bits) ++msgs_b_[b == 0 ? 3 : b == 2 ? 0 : b == 4 ? 1 : 2];
+      }
+  bits_dirty_ = false;
+}
+
 // Message lists of every ordered pair and key (engine.hpp:142-143, 585-587, 683-687);
 // bit widths from the mode, offsets from the codec wire order.
 template <typename T>
@@ -794,6 +885,7 @@ void Engine<T>::build_messages() {
       for (int64_t q = 0; q < P_; ++q)
         if (p != q) layout_pair(int(k), int(p), int(q));
   arena_layout();
+  bits_dirty_ = true;
 }
 
 template <typename T>
@@ -832,6 +924,7 @@ void Engine<T>::compute_bits_uniform() {
           m.bits[i] = uint8_t(kChoices[rng_next_below(key, ctr, 3)]);
         }
       }
+  bits_dirty_ = true;
 }
 
 // Arena: per key, send regions of hosted senders (per destination) followed by
@@ -959,13 +1052,7 @@ void Engine<T>::prepare_epoch() {
       QGNN_CUDA(cudaMemcpyAsync(up->snd[k].keys.p, ks.data(), P_ * sizeof(uint64_t),
                                 cudaMemcpyHostToDevice, s_main_));
     }
-  msgs_b_[0] = msgs_b_[1] = msgs_b_[2] = msgs_b_[3] = 0;
-  for (size_t k = 0; k < keys_.size(); ++k)
-    for (int64_t p = 0; p < P_; ++p)
-      for (int64_t q = 0; q < P_; ++q) {
-        if (p == q) continue;
-        for (uint8_t b : msgs_[k][p][q].bits) ++msgs_b_[b == 0 ? 3 : b == 2 ? 0 : b == 4 ? 1 : 2];
-      }
+  if (bits_dirty_) recount_bits();  // widths change only with the plan (or per epoch, uniform)
 }
 
 // ------------------------------------------------------------ data path ---
@@ -1103,14 +1190,10 @@ void Engine<T>::forward_layer(int l) {
   const int64_t din = dims_[t], dout = dims_[l];
   const int64_t ldi = ld_of(din), ldo = ld_of(dout);
   const int relu = l < L_ ? 1 : 0;
-  // fwd_send (engine.hpp:566-588)
-  for (auto& up : parts_dev_) quantize(*up, k, up->h[t].p, ldi);
-  exchange(k);
-  // central rows while the exchange is in flight (engine.hpp:598-605)
-  for (auto& up : parts_dev_) {
-    PartDev& D = *up;
+  // central rows (engine.hpp:598-605): during the exchange
+  auto central = [&](PartDev& D) {
     const int64_t nc = D.view.n_central;
-    if (!nc) continue;
+    if (!nc) return;
     kbegin(QGNN_K_SPMM_FWD);
     const int nk = spmm(din, D.h[t].p, ldi, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
                         D.lafwd.p, nullptr, nullptr, nullptr, 0, nc, D.hagg[t].p, ldi, &D.hub_fc.plan);
@@ -1121,6 +1204,24 @@ void Engine<T>::forward_layer(int l) {
     QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
                                  nullptr, 0, nc, relu, D.h[l].p, ldo, s_main_));
     kend(QGNN_K_GEMM_FWD, double(nc) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+  };
+  // With features still in flight (first layer after set_features) or with no
+  // remote exchange (one GPU), each partition's encode and central rows run as
+  // soon as its rows exist; otherwise every encode precedes the exchange, which
+  // the central rows then overlap.
+  const bool feats = t == 0 && feat_pending_;
+  if (feats || s_.world == 1) {
+    for (auto& up : parts_dev_) {
+      if (feats) gather_features(*up);
+      quantize(*up, k, up->h[t].p, ldi);  // fwd_send (engine.hpp:566-588)
+      central(*up);
+    }
+    feat_pending_ = false;
+    exchange(k);
+  } else {
+    for (auto& up : parts_dev_) quantize(*up, k, up->h[t].p, ldi);  // fwd_send
+    exchange(k);
+    for (auto& up : parts_dev_) central(*up);
   }
   wait_exchange();
   // receive (engine.hpp:607-618): decode every source straight into the halo
@@ -1166,6 +1267,12 @@ void Engine<T>::loss_phase() {
     QGNN_CUDA(cudaMemsetAsync(D.loss.p, 0, sizeof(double), s_main_));
     QGNN_CUDA(cudaMemsetAsync(D.correct.p, 0, 2 * sizeof(unsigned long long), s_main_));
     kbegin(QGNN_K_ELEMWISE);
+    if constexpr (sizeof(T) == 4) {
+      loss_f32(ctx_, D.h[L_].p, ldc, int(C), D.labels.p, D.loss_rows.p, D.n_train, D.n_val,
+               D.n_test, 1.0 / double(global_train_), D.dh.p, ldc, D.loss.p, D.correct.p, s_main_);
+      kend(QGNN_K_ELEMWISE, double(D.view.num_owned) * C * sizeof(T) * 2, s_main_, 2);
+      continue;
+    }
     if (D.n_train)
       QGNN_CALL(qgnn_masked_ce(ctx_, dtype_, D.h[L_].p, ldc, C, D.labels.p, D.train_rows.p,
                                D.n_train, 1.0 / double(global_train_), D.dh.p, ldc, D.loss.p,
@@ -1629,6 +1736,7 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
         }
     }
   }
+  bits_dirty_ = true;
   for (size_t k = 0; k < keys_.size(); ++k)
     for (int64_t p = 0; p < P_; ++p)
       for (int64_t q = 0; q < P_; ++q)

@@ -129,8 +129,10 @@ class Engine:
 
     def set_features(self, feats):
         """Upload node features (n x F).  A pinned torch tensor (or a CUDA
-        tensor) takes the fast path: one async copy + a GPU gather into
-        partition order; a numpy array is staged through pinned memory."""
+        tensor) takes the fast path: asynchronous node-range copies that the
+        next run_epoch consumes partition by partition as they land (keep the
+        tensor alive until then); a numpy array is staged through pinned
+        memory synchronously."""
         if hasattr(feats, "data_ptr"):
             assert feats.is_contiguous() and feats.element_size() == np.dtype(self.np_dtype).itemsize
             check(lib.qgnn_engine_set_features(self._h, C.c_void_p(feats.data_ptr())))

@@ -1,5 +1,5 @@
 # A/B helper: bash profiles/ab.sh "ENV=a" "ENV=b" ...  (runs gpu tests first, then bench per env)
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2 | tee gpurun_out/ab_tests.log
 i=0
 for cfg in "$@"; do i=$((i+1))
   env $cfg timeout 300 python bench.py --steps ${STEPS:-3} --no-cpu > gpurun_out/ab_$i.log 2>&1
