@@ -456,7 +456,8 @@ __global__ void __launch_bounds__(256) k_quantize_pack_f32(
 __global__ void __launch_bounds__(256) k_dequant_f32(
     const uint8_t* __restrict__ in, int64_t n, int dim, const uint8_t* __restrict__ bits,
     const uint64_t* __restrict__ offsets, const int32_t* __restrict__ dst_rows, int accumulate,
-    float* __restrict__ out, int64_t ld, int* __restrict__ err) {
+    float* __restrict__ out, int64_t ld, int* __restrict__ err, const float* __restrict__ mask,
+    int64_t ldm) {
   const int lane = threadIdx.x & 31;
   const int64_t wstride = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   for (int64_t m = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; m < n;
@@ -467,7 +468,11 @@ __global__ void __launch_bounds__(256) k_dequant_f32(
   const int nchunk = (dim + 3) >> 2;
   if (b == 0) {
     const float* src = reinterpret_cast<const float*>(chunk);
-    for (int j = lane; j < dim; j += 32) dst[j] = accumulate ? dst[j] + src[j] : src[j];
+    const float* hm = mask ? mask + (dst_rows ? static_cast<int64_t>(dst_rows[m]) : m) * ldm : nullptr;
+    for (int j = lane; j < dim; j += 32) {
+      const float v = hm && !(hm[j] > 0.f) ? 0.f : src[j];
+      dst[j] = accumulate ? dst[j] + v : v;
+    }
     continue;
   }
   const uint4 h = *reinterpret_cast<const uint4*>(chunk);
@@ -477,7 +482,7 @@ __global__ void __launch_bounds__(256) k_dequant_f32(
   }
   const float sc = __uint_as_float(h.x), zp = __uint_as_float(h.y);
   const uint8_t* payload = chunk + kHdrGpu;
-  const uint32_t mask = (1u << b) - 1;
+  const uint32_t cmask = (1u << b) - 1;
   for (int c = lane; c < nchunk; c += 32) {
     uint32_t word;
     if (b == 8)
@@ -488,7 +493,15 @@ __global__ void __launch_bounds__(256) k_dequant_f32(
       word = payload[c];
     float r[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) r[q] = fmaf(static_cast<float>((word >> (q * b)) & mask), sc, zp);
+    for (int q = 0; q < 4; ++q) r[q] = fmaf(static_cast<float>((word >> (q * b)) & cmask), sc, zp);
+    if (mask) {  // ReLU backward folded into the scatter-add (see spmm.cu:relu_mask4)
+      const float4 hm = __ldg(reinterpret_cast<const float4*>(
+          mask + (dst_rows ? static_cast<int64_t>(dst_rows[m]) : m) * ldm + 4 * c));
+      r[0] = hm.x > 0.f ? r[0] : 0.f;
+      r[1] = hm.y > 0.f ? r[1] : 0.f;
+      r[2] = hm.z > 0.f ? r[2] : 0.f;
+      r[3] = hm.w > 0.f ? r[3] : 0.f;
+    }
     if (4 * c + 3 < dim) {
       float4* d4 = reinterpret_cast<float4*>(dst) + c;
       if (accumulate) {
@@ -598,8 +611,9 @@ int qgnn_dequant_scatter(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int64_t di
   const bool fast = dtype == QGNN_F32 && layout == QGNN_WIRE_GPU && ld % 4 == 0 &&
                     (reinterpret_cast<uintptr_t>(out) & 15) == 0;
   if (fast)
-    k_dequant_f32<<<std::min<int64_t>(blocks, int64_t(ctx->num_sms) * 16), threads, 0, s>>>(in, n, static_cast<int>(dim), bits, offsets, dst_rows,
-                                             accumulate, static_cast<float*>(out), ld, ctx->d_err);
+    k_dequant_f32<<<std::min<int64_t>(blocks, int64_t(ctx->num_sms) * 16), threads, 0, s>>>(
+        in, n, static_cast<int>(dim), bits, offsets, dst_rows, accumulate, static_cast<float*>(out),
+        ld, ctx->d_err, nullptr, 0);
   else if (dtype == QGNN_F64)
     k_dequant_scatter<double><<<blocks, threads, 0, s>>>(in, n, static_cast<int>(dim), bits,
                                                          offsets, layout, dst_rows, accumulate,
@@ -613,3 +627,16 @@ int qgnn_dequant_scatter(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int64_t di
 }
 
 }  // extern "C"
+
+namespace qgnn_b200 {
+// fp32 GPU-layout decode + scatter-add with the ReLU-backward mask (engine)
+void dequant_add_masked_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int dim,
+                            const uint8_t* bits, const uint64_t* offsets, const int32_t* dst_rows,
+                            float* out, int64_t ld, const float* mask, int64_t ldm, cudaStream_t s) {
+  if (n == 0) return;
+  const int64_t blocks = ceil_div(n * 32, 256);
+  k_dequant_f32<<<std::min<int64_t>(blocks, int64_t(ctx->num_sms) * 16), 256, 0, s>>>(
+      in, n, dim, bits, offsets, dst_rows, 1, out, ld, ctx->d_err, mask, ldm);
+  check_launch("k_dequant_f32");
+}
+}  // namespace qgnn_b200

@@ -58,6 +58,15 @@ struct Arith<float> {
 
 struct Ctx;  // defined in ctx.cu
 
+// fp32 GPU-layout decode + scatter-add, ReLU-backward mask by h (codec.cu)
+void dequant_add_masked_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int dim,
+                            const uint8_t* bits, const uint64_t* offsets, const int32_t* dst_rows,
+                            float* out, int64_t ld, const float* mask, int64_t ldm, cudaStream_t s);
+// fp32 input gradient out = A W^T for rows [row_begin, row_begin + n_rows) with the
+// ReLU-backward mask by h folded into the epilogue (dense.cu)
+void input_grad_masked_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int64_t din,
+                           int64_t dout, int64_t row_begin, int64_t n_rows, float* out,
+                           int64_t ldo, const float* mask, int64_t ldm, cudaStream_t s);
 // fp32 loss phase for the engine: CE over train rows + val/test hit counts (dense.cu)
 void loss_f32(qgnn_ctx* ctx, const float* logits, int64_t ld, int classes, const int32_t* labels,
               const int32_t* rows, int64_t n_train, int64_t n_val, int64_t n_test,
@@ -82,7 +91,7 @@ void* ctx_gemm_b(qgnn_ctx* ctx, size_t bytes);
 // tcgen05 GEMMs (gemm_tc.cu)
 void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int wcols, int N,
                   int K, int transpose_w, int64_t n_rows, int relu, float* out, int64_t ldo,
-                  cudaStream_t s);
+                  cudaStream_t s, const float* mask = nullptr, int64_t ldm = 0);
 float* tc_gemm_wgrad_partials(qgnn_ctx* ctx, const float* A, int64_t lda, const float* B,
                               int64_t ldb, int M, int N, int64_t n_rows, int* splits_out,
                               cudaStream_t s);
@@ -101,7 +110,17 @@ struct HubPlan {
 void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y, int64_t ldy,
               const float* sa, const int64_t* pa, const int32_t* ca, const float* aa,
               const int64_t* pb, const int32_t* cb, const float* ab, int64_t row_begin,
-              int64_t n_rows, float* out, int64_t ldo, const HubPlan* hp, cudaStream_t s);
+              int64_t n_rows, float* out, int64_t ldo, const HubPlan* hp, cudaStream_t s,
+              const float* mask = nullptr, int64_t ldm = 0);
+// fp32 GPU-layout decode + scatter-add, ReLU-backward mask by h (codec.cu)
+void dequant_add_masked_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int dim,
+                            const uint8_t* bits, const uint64_t* offsets, const int32_t* dst_rows,
+                            float* out, int64_t ld, const float* mask, int64_t ldm, cudaStream_t s);
+// fp32 input gradient out = A W^T for rows [row_begin, row_begin + n_rows) with the
+// ReLU-backward mask by h folded into the epilogue (dense.cu)
+void input_grad_masked_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int64_t din,
+                           int64_t dout, int64_t row_begin, int64_t n_rows, float* out,
+                           int64_t ldo, const float* mask, int64_t ldm, cudaStream_t s);
 // fp32 loss phase for the engine: CE over train rows + val/test hit counts (dense.cu)
 void loss_f32(qgnn_ctx* ctx, const float* logits, int64_t ld, int classes, const int32_t* labels,
               const int32_t* rows, int64_t n_train, int64_t n_val, int64_t n_test,

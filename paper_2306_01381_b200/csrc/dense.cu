@@ -605,3 +605,24 @@ int qgnn_adam_step(qgnn_ctx* ctx, int dtype, void* p, void* m, void* v, const vo
 }
 
 }  // extern "C"
+
+namespace qgnn_b200 {
+void input_grad_masked_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int64_t din,
+                           int64_t dout, int64_t row_begin, int64_t n_rows, float* out,
+                           int64_t ldo, const float* mask, int64_t ldm, cudaStream_t s) {
+  if (n_rows == 0) return;
+  if (use_tc_gemm() && din <= 256 && tma_ok(A, lda, row_begin)) {
+    tc_gemm_rows(ctx, A + row_begin * lda, lda, W, int(dout), int(din), int(dout), 0, n_rows, 0,
+                 out + row_begin * ldo, ldo, s, mask ? mask + row_begin * ldm : nullptr, ldm);
+    return;
+  }
+  const int st = qgnn_dense_input_grad(ctx, QGNN_F32, A, lda, W, din, dout, nullptr, row_begin,
+                                       n_rows, out, ldo, s);
+  if (st) throw Status(st, qgnn_last_error());
+  if (mask) {
+    const int st2 = qgnn_relu_backward(ctx, QGNN_F32, mask, ldm, out, ldo, din, row_begin, n_rows,
+                                       out, ldo, s);
+    if (st2) throw Status(st2, qgnn_last_error());
+  }
+}
+}  // namespace qgnn_b200

@@ -280,7 +280,7 @@ class Engine final : public EngineBase {
 
   int64_t ld_of(int64_t d) const { return round_up(d, 8); }
   // rows with more neighbours than this are split across a CTA (QGNN_HUB_DEG overrides)
-  int64_t kHubDeg = 1024;
+  int64_t kHubDeg = 128;
   // K4 dispatch: fp32 -> nnz-balanced row-range kernel with hub splitting (all
   // feature buffers are zero-padded to a multiple of 4 columns); fp64 -> the
   // reference-order kernel.  Returns the number of kernels launched.
@@ -325,10 +325,10 @@ class Engine final : public EngineBase {
   int spmm(int64_t dim, const T* x, int64_t ldx, const T* y, int64_t ldy, const T* sa,
            const int64_t* pa, const int32_t* ca, const T* aa, const int64_t* pb,
            const int32_t* cb, const T* ab, int64_t r0, int64_t n, T* out, int64_t ldo,
-           const HubPlan* hubs) {
+           const HubPlan* hubs, const T* mask = nullptr, int64_t ldm = 0) {
     if constexpr (sizeof(T) == 4) {
       spmm_f32(ctx_, int(round_up(dim, 4)), x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, r0, n, out,
-               ldo, hubs, s_main_);
+               ldo, hubs, s_main_, mask, ldm);
       return 1 + (hubs && hubs->n_hubs > 0 ? 2 : 0);
     } else {
       const int st = qgnn_csr_aggregate(ctx_, dtype_, dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb,
@@ -348,10 +348,27 @@ class Engine final : public EngineBase {
   void forward_last_tf(int l);
   void backward_last_tf(int l);
   bool tf_last_ = false;  // last layer aggregates after the transform (fp32, dout < din)
+  // fp32 + GPU wire layout: ReLU backward folded into the producers of dh (masked by h)
+  bool relu_fused() const { return sizeof(T) == 4 && s_.layout == QGNN_WIRE_GPU; }
+  bool dh_masked_ = false;  // dh already carries the ReLU-backward mask of its layer
   int gemm_nk() const { return (sizeof(T) == 4 && use_tc_gemm()) ? 2 : 1; }
   void loss_phase();
   void backward_layer(int l);
   void backward_last();
+  // ascending-source scatter-add of decoded rows [b, e) of R into dh_next (mask: fp32 ReLU bwd)
+  template <typename R_>
+  void dequant_add(PartDev& D, R_& R, int64_t b, int64_t e, int64_t din, int64_t ldi, const T* mask) {
+    if constexpr (sizeof(T) == 4) {
+      if (s_.layout == QGNN_WIRE_GPU) {
+        dequant_add_masked_f32(ctx_, arena_.p, e - b, int(din), R.bits.p + b, R.off.p + b,
+                               R.dst.p + b, D.dh_next.p, ldi, mask, ldi, s_main_);
+        return;
+      }
+    }
+    const int st = qgnn_dequant_scatter(ctx_, arena_.p, e - b, din, R.bits.p + b, R.off.p + b,
+                                        s_.layout, R.dst.p + b, 1, D.dh_next.p, dtype_, ldi, s_main_);
+    if (st) throw Status(st, qgnn_last_error());
+  }
   void step();
   void adaptive_round(qgnn_epoch_metrics* m);
   uint64_t msg_offset_send(int k, int p, int q) const { return send_base_[k][p][q]; }
@@ -1294,7 +1311,10 @@ void Engine<T>::backward_layer(int l) {
   const int k = int(L_) + t - 1;  // backward key index (keys: fwd 0..L-1, bwd 1..L-1)
   const int64_t din = dims_[t], dout = dims_[l];
   const int64_t ldi = ld_of(din), ldo = ld_of(dout);
-  const bool relu = l < L_;
+  // fp32: the ReLU backward of this layer was folded into whoever produced dh,
+  // and this layer's producers of dh_next are masked by h[t] (relu_mask4)
+  const bool relu = l < L_ && !dh_masked_;
+  const bool mk = relu_fused() && t >= 1;
   const T* W = w_.p + woff_[t];
   // bwd_send (engine.hpp:661-688): marginal chain, remote partials, encode
   for (auto& up : parts_dev_) {
@@ -1349,7 +1369,8 @@ void Engine<T>::backward_layer(int l) {
          dtype_ == QGNN_F64 ? 1 : 2);
     kbegin(QGNN_K_SPMM_BWD);
     const int nk = spmm(din, D.gbar.p, ldi, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
-                        D.labwd.p, nullptr, nullptr, nullptr, 0, no, D.dh_next.p, ldi, &D.hub_bwd.plan);
+                        D.labwd.p, nullptr, nullptr, nullptr, 0, no, D.dh_next.p, ldi, &D.hub_bwd.plan,
+                        mk ? D.h[t].p : nullptr, ldi);
     kend(QGNN_K_SPMM_BWD, no * (16.0 + 2 * din * sizeof(T)) +
                               double(D.view.local_nnz()) * (4 + sizeof(T)) +
                               double(no) * din * sizeof(T), s_main_, nk);
@@ -1362,14 +1383,13 @@ void Engine<T>::backward_layer(int l) {
       const int64_t b = R.p_begin[src], e = R.p_begin[src + 1];
       if (e == b) continue;
       kbegin(QGNN_K_DEQUANT);
-      QGNN_CALL(qgnn_dequant_scatter(ctx_, arena_.p, e - b, din, R.bits.p + b, R.off.p + b,
-                                     s_.layout, R.dst.p + b, 1, D.dh_next.p, dtype_, ldi,
-                                     s_main_));
+      dequant_add(D, R, b, e, din, ldi, mk ? D.h[t].p : nullptr);
       kend(QGNN_K_DEQUANT, double(e - b) * (2 * din * sizeof(T) + 13) +
                                double(msgs_[k][src][D.id].bytes), s_main_);
     }
     std::swap(D.dh, D.dh_next);
   }
+  dh_masked_ = mk;
 }
 
 // Last layer, transform first (fp32 engine, dout < din): y = h W on owned and
@@ -1492,14 +1512,15 @@ void Engine<T>::backward_last_tf(int l) {
       const int64_t b = R.p_begin[src], e = R.p_begin[src + 1];
       if (e == b) continue;
       kbegin(QGNN_K_DEQUANT);
-      QGNN_CALL(qgnn_dequant_scatter(ctx_, arena_.p, e - b, din, R.bits.p + b, R.off.p + b,
-                                     s_.layout, R.dst.p + b, 1, D.dh_next.p, dtype_, ldi,
-                                     s_main_));
+      dequant_add(D, R, b, e, din, ldi, nullptr);
       kend(QGNN_K_DEQUANT, double(e - b) * (2 * din * sizeof(T) + 13) +
                                double(msgs_[k][src][D.id].bytes), s_main_);
     }
     std::swap(D.dh, D.dh_next);
   }
+  // dh_next comes from a GEMM whose row-per-thread epilogue makes a fused mask
+  // read expensive: the next layer applies its ReLU backward itself
+  dh_masked_ = false;
 }
 
 // bwd_last (engine.hpp:743-765): layer-1 weight gradient only
@@ -1507,7 +1528,7 @@ template <typename T>
 void Engine<T>::backward_last() {
   const int64_t din = dims_[0], dout = dims_[1];
   const int64_t ldi = ld_of(din), ldo = ld_of(dout);
-  const bool relu = L_ > 1;
+  const bool relu = L_ > 1 && !dh_masked_;  // fp32: usually folded into dh's producers
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
     const int64_t no = D.view.num_owned;

@@ -143,6 +143,8 @@ struct Params {
   float* out;
   int64_t ldo;
   int relu;
+  const float* mask;  // optional ReLU-backward mask: out = v * 1[mask > 0] (same row/col layout)
+  int64_t ldm;
 };
 
 // kMN = false: A K-major (tmA box {32, 128}), B/Blo K-major prepared (box {32, BN})
@@ -317,6 +319,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             v[i] = __uint_as_float(r[u][i]);
             if (p.relu) v[i] = v[i] > 0.f ? v[i] : 0.f;
           }
+          if (p.mask) {
+            const float* mrow = p.mask + int64_t(row) * p.ldm + c;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (c + i < p.N && !(mrow[i] > 0.f)) v[i] = 0.f;
+          }
           if (c + 16 <= p.N && (p.ldo & 3) == 0) {
 #pragma unroll
             for (int i = 0; i < 16; i += 4)
@@ -447,7 +455,7 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo, 
 // C[rows x N] = A[rows x K] B  with B(n,k) from W (see k_prep_b); relu optional.
 void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int wcols, int N,
                   int K, int transpose_w, int64_t n_rows, int relu, float* out, int64_t ldo,
-                  cudaStream_t s) {
+                  cudaStream_t s, const float* mask, int64_t ldm) {
   QGNN_REQUIRE(N <= 256 && K <= 4096, QGNN_EINVAL, "tc_gemm: N must be <= 256");
   const int BN = int(round_up(N, 16));
   const int Kp = int(round_up(K, 4));
@@ -474,6 +482,8 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
   p.out = out;
   p.ldo = ldo;
   p.relu = relu;
+  p.mask = mask;
+  p.ldm = ldm;
   p.stages = stages_for(BN);
   launch<false>(ta, tb, tbl, p, ctx->num_sms, s);
 }
@@ -509,6 +519,8 @@ float* tc_gemm_wgrad_partials(qgnn_ctx* ctx, const float* A, int64_t lda, const 
   p.out = part;
   p.ldo = N;
   p.relu = 0;
+  p.mask = nullptr;
+  p.ldm = 0;
   p.stages = stages_for(BN);
   launch<true>(ta, tb, tb, p, ctx->num_sms, s);
   *splits_out = splits;

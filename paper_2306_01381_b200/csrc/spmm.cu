@@ -185,6 +185,23 @@ void launch_csr(int nv, int dim, const T* x, int64_t ldx, const T* y, int64_t ld
   check_launch("k_csr_aggregate");
 }
 
+// ReLU backward folded into the producer of dh: dz = dh * 1[h > 0] is linear in
+// dh, so every contribution to dh (SpMM rows, decoded remote partials, the
+// transform-first input gradient) can be masked by the layer's activation h
+// before it is stored or added (model.hpp:128-153).
+__device__ __forceinline__ void relu_mask4(float (&v)[4], const float* __restrict__ m) {
+  const float4 h = __ldg(reinterpret_cast<const float4*>(m));
+  v[0] = h.x > 0.f ? v[0] : 0.f;
+  v[1] = h.y > 0.f ? v[1] : 0.f;
+  v[2] = h.z > 0.f ? v[2] : 0.f;
+  v[3] = h.w > 0.f ? v[3] : 0.f;
+}
+__device__ __forceinline__ float4 relu_mask4(float4 v, const float* __restrict__ m) {
+  const float4 h = __ldg(reinterpret_cast<const float4*>(m));
+  return make_float4(h.x > 0.f ? v.x : 0.f, h.y > 0.f ? v.y : 0.f, h.z > 0.f ? v.z : 0.f,
+                     h.w > 0.f ? v.w : 0.f);
+}
+
 // ----------------------------------------------------------------- F32 v2 ---
 // Production fp32 SpMM over a contiguous row range.  Warp w of block b owns
 // row r0 + 8b + w, so at any instant the resident warps of the whole GPU sweep
@@ -206,7 +223,8 @@ __global__ void __launch_bounds__(256, (NV <= 2 ? 3 : 1)) k_spmm_f32(
     const float* __restrict__ self_alpha, const int64_t* __restrict__ pa,
     const int32_t* __restrict__ ca, const float* __restrict__ aa, const int64_t* __restrict__ pb,
     const int32_t* __restrict__ cb, const float* __restrict__ ab, int64_t r0, int64_t n_rows,
-    float* __restrict__ out, int64_t ldo, int64_t hub_deg) {
+    float* __restrict__ out, int64_t ldo, int64_t hub_deg, const float* __restrict__ mask,
+    int64_t ldm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nvec = dim >> 2;
   {
@@ -237,7 +255,9 @@ __global__ void __launch_bounds__(256, (NV <= 2 ? 3 : 1)) k_spmm_f32(
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const int cv = lane + 32 * i;
-      if (cv < nvec) vstore<float, 4>(out + r * ldo + cv * 4, acc[i]);
+      if (cv >= nvec) continue;
+      if (mask) relu_mask4(acc[i], mask + r * ldm + cv * 4);
+      vstore<float, 4>(out + r * ldo + cv * 4, acc[i]);
     }
   }
 }
@@ -288,7 +308,8 @@ __global__ void __launch_bounds__(256, 4) k_spmm_f32g(
     const float* __restrict__ self_alpha, const int64_t* __restrict__ pa,
     const int32_t* __restrict__ ca, const float* __restrict__ aa, const int64_t* __restrict__ pb,
     const int32_t* __restrict__ cb, const float* __restrict__ ab, int64_t r0, int64_t n_rows,
-    float* __restrict__ out, int64_t ldo, int64_t hub_deg) {
+    float* __restrict__ out, int64_t ldo, int64_t hub_deg, const float* __restrict__ mask,
+    int64_t ldm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = dim >> 2, E = 32 / G;
   const int grp = lane / G, sub = lane - grp * G;
@@ -317,6 +338,7 @@ __global__ void __launch_bounds__(256, 4) k_spmm_f32g(
       o = make_float4(fmaf(sa, xv.x, acc.x), fmaf(sa, xv.y, acc.y), fmaf(sa, xv.z, acc.z),
                       fmaf(sa, xv.w, acc.w));
     }
+    if (mask) o = relu_mask4(o, mask + r * ldm + sub * 4);
     *reinterpret_cast<float4*>(out + r * ldo + sub * 4) = o;
   }
 }
@@ -394,7 +416,8 @@ __global__ void __launch_bounds__(256) k_spmm_hubseg(
 __global__ void __launch_bounds__(256) k_spmm_hubred(
     int dim, const float* __restrict__ x, int64_t ldx, const float* __restrict__ self_alpha,
     const int32_t* __restrict__ hubs, const int32_t* __restrict__ seg_ptr, int64_t n_hubs,
-    const float* __restrict__ part, int64_t ldp, float* __restrict__ out, int64_t ldo) {
+    const float* __restrict__ part, int64_t ldp, float* __restrict__ out, int64_t ldo,
+    const float* __restrict__ mask, int64_t ldm) {
   const int lane = threadIdx.x & 31;
   const int64_t h = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (h >= n_hubs) return;
@@ -407,6 +430,7 @@ __global__ void __launch_bounds__(256) k_spmm_hubred(
       const float4 p = *reinterpret_cast<const float4*>(part + int64_t(s) * ldp + c);
       v.x += p.x, v.y += p.y, v.z += p.z, v.w += p.w;
     }
+    if (mask) v = relu_mask4(v, mask + r * ldm + c);
     *reinterpret_cast<float4*>(out + r * ldo + c) = v;
   }
 }
@@ -423,7 +447,8 @@ static bool grouped_narrow() {  // QGNN_SPMM_GROUPED=0 selects the one-row-per-w
 void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y, int64_t ldy,
               const float* sa, const int64_t* pa, const int32_t* ca, const float* aa,
               const int64_t* pb, const int32_t* cb, const float* ab, int64_t row_begin,
-              int64_t n_rows, float* out, int64_t ldo, const HubPlan* hp, cudaStream_t s) {
+              int64_t n_rows, float* out, int64_t ldo, const HubPlan* hp, cudaStream_t s,
+              const float* mask, int64_t ldm) {
   if (n_rows <= 0) return;
   const int nv = int(ceil_div(dim / 4, 32));
   const int64_t blocks = ceil_div(n_rows, 8);
@@ -432,22 +457,23 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
 #define QGNN_SPMM_CASE(NVV)                                                                    \
   case NVV:                                                                                    \
     k_spmm_f32<NVV><<<unsigned(blocks), 256, 0, s>>>(dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, \
-                                                     ab, row_begin, n_rows, out, ldo, hd);       \
+                                                     ab, row_begin, n_rows, out, ldo, hd, mask, ldm); \
     if (hubs) {                                                                                \
       k_spmm_hubseg<NVV><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(             \
           dim, x, ldx, y, ldy, ca, aa, cb, ab, hp->seg, hp->n_segs, hp->part, hp->ldp);        \
       k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 256)), 256, 0, s>>>(                  \
-          dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo);    \
+          dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask, ldm); \
     }                                                                                          \
     break;
   if (nv == 1 && grouped_narrow()) {
     k_spmm_f32g<<<unsigned(blocks), 256, 0, s>>>(dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab,
-                                                 row_begin, n_rows, out, ldo, hd);
+                                                 row_begin, n_rows, out, ldo, hd, mask, ldm);
     if (hubs) {
       k_spmm_hubseg<1><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(
           dim, x, ldx, y, ldy, ca, aa, cb, ab, hp->seg, hp->n_segs, hp->part, hp->ldp);
       k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 256)), 256, 0, s>>>(
-          dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo);
+          dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask,
+          ldm);
     }
     check_launch("k_spmm_f32g");
     return;
