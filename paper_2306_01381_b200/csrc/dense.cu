@@ -297,68 +297,69 @@ __global__ void k_count_correct(const T* __restrict__ logits, int64_t ld, int cl
 // rows = [train | val | test] of the partition; warp per row.  Train rows:
 // softmax cross-entropy in fp32 (max, sum of expf, logf), the loss term in
 // fp64 and the gradient (softmax - onehot) / n_train_global written to grad;
-// val / test rows: first-argmax hit counts.  Each block adds its 8 warp terms
-// in warp order into block_part[blockIdx.x] (a fixed-order tree over blocks
+// val / test rows: first-argmax hit counts.  Each block adds its 32 row terms
+// in row order into block_part[blockIdx.x] (a fixed-order tree over blocks
 // follows), so the loss is deterministic.
 __global__ void __launch_bounds__(256) k_loss_f32(
     const float* __restrict__ logits, int64_t ld, int classes, const int32_t* __restrict__ labels,
     const int32_t* __restrict__ rows, int64_t n_train, int64_t n_val, int64_t n_test,
     double inv_denom, float* __restrict__ grad, int64_t ldg, double* __restrict__ block_part,
     unsigned long long* __restrict__ correct, int* __restrict__ err) {
-  __shared__ double wterm[8];
-  __shared__ unsigned whit[8][2];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t k = int64_t(blockIdx.x) * 8 + warp;
+  // 8 lanes per row, 32 rows per block (4 per warp): four independent
+  // index -> label -> logits chains per warp keep the loads in flight
+  __shared__ double rterm[32];
+  __shared__ unsigned rhit[32][2];
+  const int lane = threadIdx.x & 31, sub = lane & 7, slot = threadIdx.x >> 3;
+  const unsigned gm = 0xffu << (lane & 24);  // the row's 8 lanes (groups branch independently)
+  const int64_t k = int64_t(blockIdx.x) * 32 + slot;
   const int64_t n_all = n_train + n_val + n_test;
   double term = 0.0;
   unsigned hit_v = 0, hit_t = 0;
-  if (k < n_all) {
-    const int64_t r = rows[k];
-    const float* row = logits + r * ld;
-    const int y = labels[r];
-    if (y < 0 || y >= classes) {
-      if (lane == 0) atomicOr(err, kErrLabel);
-    } else if (k < n_train) {
-      float hi = -INFINITY;
-      for (int c = lane; c < classes; c += 32) hi = fmaxf(hi, row[c]);
+  const bool live = k < n_all;
+  const int64_t r = live ? rows[k] : 0;
+  const int y = live ? labels[r] : 0;
+  const float* row = logits + r * ld;
+  if (live && (y < 0 || y >= classes)) {
+    if (sub == 0) atomicOr(err, kErrLabel);
+  } else if (live && k < n_train) {
+    float hi = -INFINITY;
+    for (int c = sub; c < classes; c += 8) hi = fmaxf(hi, row[c]);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-      float sum = 0.f;
-      for (int c = lane; c < classes; c += 32) sum += expf(row[c] - hi);
+    for (int o = 4; o > 0; o >>= 1) hi = fmaxf(hi, __shfl_xor_sync(gm, hi, o));
+    float sum = 0.f;
+    for (int c = sub; c < classes; c += 8) sum += expf(row[c] - hi);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      const float lse = hi + logf(sum);
-      term = (static_cast<double>(lse) - static_cast<double>(row[y])) * inv_denom;
-      const float sc = static_cast<float>(inv_denom);
-      float* g = grad + r * ldg;
-      for (int c = lane; c < classes; c += 32)
-        g[c] = (expf(row[c] - lse) - (c == y ? 1.f : 0.f)) * sc;
-    } else {
-      // first argmax (model.hpp:216-227): larger value wins, ties -> lower index
-      float best = -INFINITY;
-      int bi = 0x7fffffff;
-      for (int c = lane; c < classes; c += 32)
-        if (row[c] > best) best = row[c], bi = c;
+    for (int o = 4; o > 0; o >>= 1) sum += __shfl_xor_sync(gm, sum, o);
+    const float lse = hi + logf(sum);
+    term = (static_cast<double>(lse) - static_cast<double>(row[y])) * inv_denom;
+    const float sc = static_cast<float>(inv_denom);
+    float* g = grad + r * ldg;
+    for (int c = sub; c < classes; c += 8) g[c] = (expf(row[c] - lse) - (c == y ? 1.f : 0.f)) * sc;
+  } else if (live) {
+    // first argmax (model.hpp:216-227): larger value wins, ties -> lower index
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int c = sub; c < classes; c += 8)
+      if (row[c] > best) best = row[c], bi = c;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) best = ob, bi = oi;
-      }
-      const unsigned hit = bi == y;
-      if (k < n_train + n_val) hit_v = hit; else hit_t = hit;
+    for (int o = 4; o > 0; o >>= 1) {
+      const float ob = __shfl_xor_sync(gm, best, o);
+      const int oi = __shfl_xor_sync(gm, bi, o);
+      if (ob > best || (ob == best && oi < bi)) best = ob, bi = oi;
     }
+    const unsigned hit = bi == y;
+    if (k < n_train + n_val) hit_v = hit; else hit_t = hit;
   }
-  if (lane == 0) {
-    wterm[warp] = term;
-    whit[warp][0] = hit_v;
-    whit[warp][1] = hit_t;
+  if (sub == 0) {
+    rterm[slot] = term;
+    rhit[slot][0] = hit_v;
+    rhit[slot][1] = hit_t;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
     unsigned hv = 0, ht = 0;
-    for (int w = 0; w < 8; ++w) t += wterm[w], hv += whit[w][0], ht += whit[w][1];
+    for (int w = 0; w < 32; ++w) t += rterm[w], hv += rhit[w][0], ht += rhit[w][1];
     block_part[blockIdx.x] = t;
     if (hv) atomicAdd(correct, static_cast<unsigned long long>(hv));
     if (ht) atomicAdd(correct + 1, static_cast<unsigned long long>(ht));
@@ -371,7 +372,7 @@ void loss_f32(qgnn_ctx* ctx, const float* logits, int64_t ld, int classes, const
               unsigned long long* correct, cudaStream_t s) {
   const int64_t n_all = n_train + n_val + n_test;
   if (!n_all) return;
-  const int64_t blocks = ceil_div(n_all, 8);
+  const int64_t blocks = ceil_div(n_all, 32);
   double* part = static_cast<double*>(ctx_scratch(ctx, sizeof(double) * blocks));
   k_loss_f32<<<unsigned(blocks), 256, 0, s>>>(logits, ld, classes, labels, rows, n_train, n_val,
                                               n_test, inv_denom, grad, ldg, part, correct,

@@ -1463,6 +1463,7 @@ void Engine<T>::backward_last_tf(int l) {
   const int64_t din = dims_[t], dout = dims_[l];
   const int64_t ldi = ld_of(din), ldo = ld_of(dout);
   const T* W = w_.p + woff_[t];
+  const bool mk = relu_fused() && t >= 1;  // ReLU backward of layer t folded into dh_next's producers
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
     const int64_t nr = D.view.num_remote;
@@ -1491,8 +1492,12 @@ void Engine<T>::backward_last_tf(int l) {
                               double(D.view.local_nnz()) * (4 + sizeof(T)) +
                               double(no) * dout * sizeof(T), s_main_, nk);
     kbegin(QGNN_K_GEMM_DGRAD);
-    QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, D.gbar.p, ldo, W, din, dout, nullptr, 0, no,
-                                    D.dh_next.p, ldi, s_main_));
+    if constexpr (sizeof(T) == 4)
+      input_grad_masked_f32(ctx_, D.gbar.p, ldo, W, din, dout, 0, no, D.dh_next.p, ldi,
+                            mk ? D.h[t].p : nullptr, ldi, s_main_);
+    else
+      QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, D.gbar.p, ldo, W, din, dout, nullptr, 0, no,
+                                      D.dh_next.p, ldi, s_main_));
     kend(QGNN_K_GEMM_DGRAD, double(no) * (din + dout) * sizeof(T), s_main_, gemm_nk());
     kbegin(QGNN_K_GEMM_WGRAD);
     T* wg = wgrad_all_.p + D.id * nparams_ + woff_[t];
@@ -1512,15 +1517,13 @@ void Engine<T>::backward_last_tf(int l) {
       const int64_t b = R.p_begin[src], e = R.p_begin[src + 1];
       if (e == b) continue;
       kbegin(QGNN_K_DEQUANT);
-      dequant_add(D, R, b, e, din, ldi, nullptr);
+      dequant_add(D, R, b, e, din, ldi, mk ? D.h[t].p : nullptr);
       kend(QGNN_K_DEQUANT, double(e - b) * (2 * din * sizeof(T) + 13) +
                                double(msgs_[k][src][D.id].bytes), s_main_);
     }
     std::swap(D.dh, D.dh_next);
   }
-  // dh_next comes from a GEMM whose row-per-thread epilogue makes a fused mask
-  // read expensive: the next layer applies its ReLU backward itself
-  dh_masked_ = false;
+  dh_masked_ = mk;
 }
 
 // bwd_last (engine.hpp:743-765): layer-1 weight gradient only

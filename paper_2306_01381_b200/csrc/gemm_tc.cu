@@ -167,6 +167,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = bars + 3 * kMaxStages;  // [2]
   uint64_t* tempty = tfull + 2;          // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  // epilogue staging: per epilogue warp a 32 x 32 fp32 block, row pitch 36 floats
+  float* stage_out = reinterpret_cast<float*>(smem + kStages * stage_bytes + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -297,42 +299,77 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
-      const int row = m0 + 32 * q + lane;
-      float* orow = p.out + (kMN ? int64_t(split) * p.M * p.N : 0) + int64_t(row) * p.ldo;
-      // 4 TMEM loads (64 columns) in flight per wait, then ReLU + 16-byte stores
-      for (int c0 = 0; c0 < p.BN; c0 += 64) {
-        uint32_t r[4][16];
+      const int row0 = m0 + 32 * q;  // this warp's 32 accumulator rows (TMEM lanes 32q..)
+      float* out_base = p.out + (kMN ? int64_t(split) * p.M * p.N : 0);
+      float* st = stage_out + q * (32 * 36);
+      // 32-column groups: TMEM -> registers (thread = row) -> ReLU / mask -> smem
+      // -> registers (8 lanes = one 128-byte row segment) -> coalesced stores
+      for (int c0 = 0; c0 < p.BN; c0 += 32) {
+        const int cc = c0 + 4 * (lane & 7);
+        // ReLU-backward mask of this lane's 8 output segments, loaded up front
+        float4 mk[8];
+        if (p.mask) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (c0 + 16 * u < p.BN)
-            tmem_ld16_nowait(tmem_base + uint32_t(acc * p.tmem_cols + c0 + 16 * u) +
-                                 (uint32_t(32 * q) << 16),
-                             r[u]);
-        tmem_wait_ld();
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int c = c0 + 16 * u;
-          if (c >= p.BN || row >= p.M) continue;
-          float v[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            v[i] = __uint_as_float(r[u][i]);
-            if (p.relu) v[i] = v[i] > 0.f ? v[i] : 0.f;
-          }
-          if (p.mask) {
-            const float* mrow = p.mask + int64_t(row) * p.ldm + c;
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (c + i < p.N && !(mrow[i] > 0.f)) v[i] = 0.f;
-          }
-          if (c + 16 <= p.N && (p.ldo & 3) == 0) {
-#pragma unroll
-            for (int i = 0; i < 16; i += 4)
-              *reinterpret_cast<float4*>(orow + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-          } else {
-            for (int i = 0; i < 16 && c + i < p.N; ++i) orow[c + i] = v[i];
+          for (int j = 0; j < 8; ++j) {
+            const int row = row0 + 4 * j + (lane >> 3);
+            mk[j] = make_float4(1.f, 1.f, 1.f, 1.f);
+            if (row < p.M && cc + 4 <= p.N && (p.ldm & 3) == 0)
+              mk[j] = __ldg(reinterpret_cast<const float4*>(p.mask + int64_t(row) * p.ldm + cc));
+            else if (row < p.M && cc < p.N) {
+              const float* mrow = p.mask + int64_t(row) * p.ldm + cc;
+              mk[j].x = mrow[0];
+              if (cc + 1 < p.N) mk[j].y = mrow[1];
+              if (cc + 2 < p.N) mk[j].z = mrow[2];
+              if (cc + 3 < p.N) mk[j].w = mrow[3];
+            }
           }
         }
+        uint32_t r[2][16];
+        tmem_ld16_nowait(tmem_base + uint32_t(acc * p.tmem_cols + c0) + (uint32_t(32 * q) << 16),
+                         r[0]);
+        if (c0 + 16 < p.BN)
+          tmem_ld16_nowait(tmem_base + uint32_t(acc * p.tmem_cols + c0 + 16) +
+                               (uint32_t(32 * q) << 16),
+                           r[1]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            float4 v = make_float4(__uint_as_float(r[h][i]), __uint_as_float(r[h][i + 1]),
+                                   __uint_as_float(r[h][i + 2]), __uint_as_float(r[h][i + 3]));
+            if (p.relu) {
+              v.x = v.x > 0.f ? v.x : 0.f;
+              v.y = v.y > 0.f ? v.y : 0.f;
+              v.z = v.z > 0.f ? v.z : 0.f;
+              v.w = v.w > 0.f ? v.w : 0.f;
+            }
+            *reinterpret_cast<float4*>(st + lane * 36 + 16 * h + i) = v;
+          }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int rr = 4 * j + (lane >> 3);
+          const int row = row0 + rr;
+          if (row >= p.M || cc >= p.N) continue;
+          float4 v = *reinterpret_cast<const float4*>(st + rr * 36 + 4 * (lane & 7));
+          if (p.mask) {
+            v.x = mk[j].x > 0.f ? v.x : 0.f;
+            v.y = mk[j].y > 0.f ? v.y : 0.f;
+            v.z = mk[j].z > 0.f ? v.z : 0.f;
+            v.w = mk[j].w > 0.f ? v.w : 0.f;
+          }
+          float* o = out_base + int64_t(row) * p.ldo + cc;
+          if (cc + 4 <= p.N && (p.ldo & 3) == 0) {
+            *reinterpret_cast<float4*>(o) = v;
+          } else {
+            o[0] = v.x;
+            if (cc + 1 < p.N) o[1] = v.y;
+            if (cc + 2 < p.N) o[2] = v.z;
+            if (cc + 3 < p.N) o[3] = v.w;
+          }
+        }
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -425,14 +462,14 @@ int pow2_cols(int bn) {
   return c;
 }
 
-constexpr size_t kSmemBudget = 200 * 1024;
+constexpr size_t kSmemBudget = 184 * 1024;  // + 18 KB epilogue staging
 int stages_for(int BN) {
   const size_t stage = 2 * tc::kBM * tc::kBK * 4 + 2 * size_t(BN) * tc::kBK * 4;
   return int(std::max<size_t>(2, std::min<size_t>(tc::kMaxStages, kSmemBudget / stage)));
 }
 size_t smem_bytes(int BN) {
   const size_t stage = 2 * tc::kBM * tc::kBK * 4 + 2 * size_t(BN) * tc::kBK * 4;
-  return size_t(stages_for(BN)) * stage + 1024 + 256;
+  return size_t(stages_for(BN)) * stage + 1024 + 256 + 4 * 32 * 36 * sizeof(float);
 }
 
 template <bool kMN>
@@ -442,7 +479,7 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo, 
   static bool attr_set = false;
   if (!attr_set) {
     QGNN_CUDA(cudaFuncSetAttribute(tc::k_tc_gemm<kMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(kSmemBudget + 1024 + 256)));
+                                   int(kSmemBudget + 1024 + 256 + 4 * 32 * 36 * sizeof(float))));
     attr_set = true;
   }
   const int tiles = p.m_tiles * p.splits;
