@@ -36,6 +36,9 @@ sys.path.insert(0, ROOT)
 WORKLOAD = dict(nodes=2449029, n_edges=61859140, feat=100, hidden=256, classes=47, parts=8,
                 cross_frac=0.0085, gamma=2.8, seed=1)
 METRIC = "full-graph GCN epoch time (s)"
+# random-row gather ceiling measured on B200 by profiles/gather_probe.cu
+# (L2-resident table, 256-512 B rows): the bound of a gather-form SpMM
+GATHER_CEILING_GBS = 15540.0
 CLOCK_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -267,6 +270,19 @@ def impl_ours(args):
             traffic = json.load(open(tp)).get(dom)
         except Exception:
             traffic = None
+    # per class: algorithmic GB/s vs HBM; SpMM classes also gathered-row GB/s vs
+    # the measured random-gather ceiling of this GPU (profiles/gather_probe.cu)
+    per_class = {}
+    for k, v in ks.items():
+        if v["ms"] <= 0:
+            continue
+        e = {"ms_per_epoch": v["ms"] / args.steps, "launches_per_epoch": v["launches"] / args.steps,
+             "gbs": v["bytes"] / (v["ms"] / 1e3) / 1e9}
+        e["frac_hbm"] = e["gbs"] / hbm
+        if v.get("gathered"):
+            e["gather_gbs"] = v["gathered"] / (v["ms"] / 1e3) / 1e9
+            e["frac_gather_ceiling"] = e["gather_gbs"] / GATHER_CEILING_GBS
+        per_class[k] = e
     q = ks["quant"]
     quant_gbs = q["bytes"] / (q["ms"] / 1e3) / 1e9 if q["ms"] > 0 else None
     x = ks.get("exchange", {"ms": 0, "bytes": 0})
@@ -298,6 +314,14 @@ def impl_ours(args):
             "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8 * 3, "h2d_gbs_raw": h2d_gbs},
             "gpu_launches": launches * args.steps,
+            "roofline_gather": ({"kernel": dom, "achieved": per_class[dom].get("gather_gbs"),
+                                 "peak": GATHER_CEILING_GBS, "unit": "GB/s",
+                                 "frac": per_class[dom].get("frac_gather_ceiling"),
+                                 "model": "nnz x dim x 4 B gathered rows per launch",
+                                 "peak_source": "profiles/gather_probe_r1f.txt (L2-resident "
+                                                "random 256-512 B rows, register loads)"}
+                                if "gather_gbs" in per_class.get(dom, {}) else None),
+            "kernels": per_class,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                          "peak_source": src,

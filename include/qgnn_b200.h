@@ -149,6 +149,16 @@ int qgnn_partition_graph(const int64_t* adj_ptr, const int32_t* adj, int64_t n, 
 /* compute_coeffs (coeffs.hpp:30-45): alpha per CSR slot + self alpha (f64). */
 int qgnn_compute_coeffs(const int64_t* adj_ptr, const int32_t* adj, int64_t n, int sage,
                         double* alpha, double* self_alpha);
+/* Exchange schedule of one tensor key for `rank` of `world` GPUs hosting
+ * partitions [rank * P / world, (rank + 1) * P / world) — replaces the
+ * reference's pair_wire_bytes / negotiate_buffers (assigner/plan.hpp:90-154)
+ * for a uniform width `bits` (0 = raw rows): send_bytes[world] / recv_bytes[world]
+ * = bytes this rank sends to / receives from each rank (same-rank pairs are
+ * zero-copy, 0).  bwd selects the backward partial-gradient direction. */
+int qgnn_exchange_plan(const int64_t* adj_ptr, const int32_t* adj, int64_t n,
+                       const uint32_t* owner, int64_t n_parts, int world, int rank, int64_t dim,
+                       int bits, int bwd, int layout, int dtype, uint64_t* send_bytes,
+                       uint64_t* recv_bytes);
 
 /* ---- host: assigner (assigner/solve.hpp) ---------------------------------------
  * One instance = one tensor key across device pairs.  Messages are flat,
@@ -230,8 +240,10 @@ int qgnn_engine_set_weights(qgnn_engine* e, int layer, const void* in);
 int qgnn_engine_info(qgnn_engine* e, int64_t* out6);
 /* Per kernel class k (QGNN_K_*), accumulated since the last call (needs
  * settings.kstats): out[3k] = total device ms, out[3k+1] = launches,
- * out[3k+2] = algorithmic bytes (SURVEY.md §8d model).  Returns the number
- * of classes written (<= n). */
+ * out[3k+2] = algorithmic bytes (SURVEY.md §8d model).  With n >= 4 *
+ * QGNN_K_COUNT the layout is 4 per class and out[4k+3] = gathered row bytes of
+ * the SpMM classes (nnz x dim x elem, the L2 gather model).  Returns the
+ * number of classes written. */
 enum {
   QGNN_K_QUANT = 0, QGNN_K_DEQUANT, QGNN_K_SPMM_FWD, QGNN_K_SPMM_BWD, QGNN_K_PARTIALS,
   QGNN_K_GEMM_FWD, QGNN_K_GEMM_DGRAD, QGNN_K_GEMM_WGRAD, QGNN_K_ELEMWISE, QGNN_K_EXCHANGE,

@@ -117,6 +117,8 @@ _SIGS = {
                                  vp]),
     "qgnn_partition_graph": (C.c_int, [vp, vp, i64, i64, u64, vp]),
     "qgnn_compute_coeffs": (C.c_int, [vp, vp, i64, C.c_int, vp, vp]),
+    "qgnn_exchange_plan": (C.c_int, [vp, vp, i64, vp, i64, C.c_int, C.c_int, i64, C.c_int,
+                                     C.c_int, C.c_int, C.c_int, vp, vp]),
     "qgnn_solve_instance": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, dbl, i64,
                                       C.c_int, vp, vp]),
     "qgnn_fit_affine": (C.c_int, [vp, vp, i64, vp, vp]),

@@ -203,6 +203,7 @@ struct KStat {
   double ms = 0;
   double launches = 0;
   double bytes = 0;
+  double gbytes = 0;  // SpMM classes: gathered row bytes (nnz x dim x elem), the L2 gather model
 };
 
 class EngineBase {
@@ -375,7 +376,7 @@ class Engine final : public EngineBase {
   void arena_layout();
   // profiling
   void kbegin(int cls);
-  void kend(int cls, double bytes, cudaStream_t s, int nk = 1);
+  void kend(int cls, double bytes, cudaStream_t s, int nk = 1, double gbytes = 0);
   void flush_kstats();
 
   qgnn_settings s_;
@@ -458,9 +459,10 @@ void Engine<T>::kbegin(int cls) {
 }
 
 template <typename T>
-void Engine<T>::kend(int cls, double bytes, cudaStream_t s, int nk) {
+void Engine<T>::kend(int cls, double bytes, cudaStream_t s, int nk, double gbytes) {
   launches_ += nk;  // kernels of ours inside the region (always counted)
   if (!s_.kstats) return;
+  kst_[cls].gbytes += gbytes;
   QGNN_CUDA(cudaEventRecord(ev_pool_[ev_next_].second, s));
   ev_used_.emplace_back(cls, ev_next_, bytes);
   ++ev_next_;
@@ -1216,7 +1218,8 @@ void Engine<T>::forward_layer(int l) {
                         D.lafwd.p, nullptr, nullptr, nullptr, 0, nc, D.hagg[t].p, ldi, &D.hub_fc.plan);
     const double nnz = double(D.view.local_ptr[nc]);
     kend(QGNN_K_SPMM_FWD, nc * (16.0 + 2 * din * sizeof(T)) + nnz * (4 + sizeof(T)) +
-                              double(D.view.num_owned) * din * sizeof(T), s_main_, nk);
+                              double(D.view.num_owned) * din * sizeof(T), s_main_, nk,
+         (nnz + nc) * din * sizeof(T));
     kbegin(QGNN_K_GEMM_FWD);
     QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
                                  nullptr, 0, nc, relu, D.h[l].p, ldo, s_main_));
@@ -1266,7 +1269,8 @@ void Engine<T>::forward_layer(int l) {
     const double nnz = double(D.view.local_ptr[nc + nm] - D.view.local_ptr[nc]) +
                        double(D.view.remote_nnz());
     kend(QGNN_K_SPMM_FWD, nm * (24.0 + 2 * din * sizeof(T)) + nnz * (4 + sizeof(T)) +
-                              double(D.view.num_remote) * din * sizeof(T), s_main_, nk);
+                              double(D.view.num_remote) * din * sizeof(T), s_main_, nk,
+         (nnz + nm) * din * sizeof(T));
     kbegin(QGNN_K_GEMM_FWD);
     QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
                                  nullptr, nc, nm, relu, D.h[l].p, ldo, s_main_));
@@ -1339,7 +1343,7 @@ void Engine<T>::backward_layer(int l) {
                           &D.hub_part.plan);
       kend(QGNN_K_PARTIALS, double(D.view.num_remote) * (8 + din * sizeof(T)) +
                                 double(D.view.remote_nnz()) * (4 + sizeof(T) + din * sizeof(T)),
-           s_main_, nk);
+           s_main_, nk, double(D.view.remote_nnz()) * din * sizeof(T));
     }
     quantize(D, k, D.partials.p, ldi);
   }
@@ -1373,7 +1377,8 @@ void Engine<T>::backward_layer(int l) {
                         mk ? D.h[t].p : nullptr, ldi);
     kend(QGNN_K_SPMM_BWD, no * (16.0 + 2 * din * sizeof(T)) +
                               double(D.view.local_nnz()) * (4 + sizeof(T)) +
-                              double(no) * din * sizeof(T), s_main_, nk);
+                              double(no) * din * sizeof(T), s_main_, nk,
+         double(D.view.local_nnz() + no) * din * sizeof(T));
   }
   wait_exchange();
   for (auto& up : parts_dev_) {
@@ -1417,7 +1422,8 @@ void Engine<T>::forward_last_tf(int l) {
                         D.lafwd.p, nullptr, nullptr, nullptr, 0, nc, D.h[l].p, ldo, &D.hub_fc.plan);
     kend(QGNN_K_SPMM_FWD, nc * (16.0 + 2 * dout * sizeof(T)) +
                               double(D.view.local_ptr[nc]) * (4 + sizeof(T)) +
-                              double(no) * dout * sizeof(T), s_main_, nk);
+                              double(no) * dout * sizeof(T), s_main_, nk,
+         double(D.view.local_ptr[nc] + nc) * dout * sizeof(T));
   }
   wait_exchange();
   for (auto& up : parts_dev_) {
@@ -1449,7 +1455,8 @@ void Engine<T>::forward_last_tf(int l) {
     const double nnz = double(D.view.local_ptr[nc + nm] - D.view.local_ptr[nc]) +
                        double(D.view.remote_nnz());
     kend(QGNN_K_SPMM_FWD, nm * (24.0 + 2 * dout * sizeof(T)) + nnz * (4 + sizeof(T)) +
-                              double(nr) * dout * sizeof(T), s_main_, nk);
+                              double(nr) * dout * sizeof(T), s_main_, nk,
+         (nnz + nm) * dout * sizeof(T));
   }
 }
 
@@ -1473,7 +1480,7 @@ void Engine<T>::backward_last_tf(int l) {
                           nullptr, nullptr, nullptr, 0, nr, D.gpart.p, ldo, &D.hub_part.plan);
       kend(QGNN_K_PARTIALS, double(nr) * (8 + dout * sizeof(T)) +
                                 double(D.view.remote_nnz()) * (4 + sizeof(T) + dout * sizeof(T)),
-           s_main_, nk);
+           s_main_, nk, double(D.view.remote_nnz()) * dout * sizeof(T));
       kbegin(QGNN_K_GEMM_DGRAD);
       QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, D.gpart.p, ldo, W, din, dout, nullptr, 0, nr,
                                       D.partials.p, ldi, s_main_));
@@ -1490,7 +1497,8 @@ void Engine<T>::backward_last_tf(int l) {
                         D.labwd.p, nullptr, nullptr, nullptr, 0, no, D.gbar.p, ldo, &D.hub_bwd.plan);
     kend(QGNN_K_SPMM_BWD, no * (16.0 + 2 * dout * sizeof(T)) +
                               double(D.view.local_nnz()) * (4 + sizeof(T)) +
-                              double(no) * dout * sizeof(T), s_main_, nk);
+                              double(no) * dout * sizeof(T), s_main_, nk,
+         double(D.view.local_nnz() + no) * dout * sizeof(T));
     kbegin(QGNN_K_GEMM_DGRAD);
     if constexpr (sizeof(T) == 4)
       input_grad_masked_f32(ctx_, D.gbar.p, ldo, W, din, dout, 0, no, D.dh_next.p, ldi,
@@ -1814,11 +1822,15 @@ void Engine<T>::info(int64_t* out) {
 
 template <typename T>
 int Engine<T>::kernel_stats(double* out, int n) {
-  const int m = std::min<int>(n / 3, QGNN_K_COUNT);
+  // 3 doubles per class (ms, launches, algorithmic bytes); with room for 4 per
+  // class the SpMM gathered-row bytes follow as the 4th
+  const int w = n >= 4 * QGNN_K_COUNT ? 4 : 3;
+  const int m = std::min<int>(n / w, QGNN_K_COUNT);
   for (int c = 0; c < m; ++c) {
-    out[3 * c] = kst_[c].ms;
-    out[3 * c + 1] = kst_[c].launches;
-    out[3 * c + 2] = kst_[c].bytes;
+    out[w * c] = kst_[c].ms;
+    out[w * c + 1] = kst_[c].launches;
+    out[w * c + 2] = kst_[c].bytes;
+    if (w == 4) out[w * c + 3] = kst_[c].gbytes;
     kst_[c] = KStat{};
   }
   return m;

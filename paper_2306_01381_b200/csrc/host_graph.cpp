@@ -493,6 +493,36 @@ int qgnn_compute_coeffs(const int64_t* adj_ptr, const int32_t* adj, int64_t n, i
   QGNN_API_END
 }
 
+// Exchange schedule of one tensor for one rank (plan.hpp:90-154 pair_wire_bytes /
+// negotiate_buffers, engine.hpp:460-505 routing).  Sender and receiver derive
+// each pair's bytes from their own Part (remote_out vs remote_in), so the
+// GPU engine needs no size handshake; tests check the two sides agree.
+int qgnn_exchange_plan(const int64_t* adj_ptr, const int32_t* adj, int64_t n,
+                       const uint32_t* owner, int64_t n_parts, int world, int rank, int64_t dim,
+                       int bits, int bwd, int layout, int dtype, uint64_t* send_bytes,
+                       uint64_t* recv_bytes) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(world >= 1 && rank >= 0 && rank < world && n_parts % world == 0, QGNN_EINVAL,
+               "exchange_plan: n_parts must divide by world, 0 <= rank < world");
+  QGNN_REQUIRE(bits == 0 || bits == 2 || bits == 4 || bits == 8, QGNN_EINVAL,
+               "exchange_plan: bit width must be 0, 2, 4 or 8");
+  const auto parts = partitions_from_owner(adj_ptr, adj, n, owner, n_parts);
+  const int64_t ppr = n_parts / world;
+  const uint64_t chunk = qgnn_chunk_wire_bytes(uint64_t(dim), bits, layout, dtype);
+  for (int r = 0; r < world; ++r) send_bytes[r] = recv_bytes[r] = 0;
+  for (int64_t p = rank * ppr; p < (rank + 1) * ppr; ++p)
+    for (int64_t q = 0; q < n_parts; ++q) {
+      if (q / ppr == rank) continue;  // same GPU: zero copy
+      // forward p -> q: rows of p's owned nodes q consumes; backward: partials of
+      // the halo slots p holds for q's nodes (engine.hpp:566-588, 661-688)
+      const auto& out_ids = bwd ? parts[p].remote_in[q] : parts[p].remote_out[q];
+      const auto& in_ids = bwd ? parts[p].remote_out[q] : parts[p].remote_in[q];
+      send_bytes[q / ppr] += chunk * out_ids.size();
+      recv_bytes[q / ppr] += chunk * in_ids.size();
+    }
+  QGNN_API_END
+}
+
 // Planted-block generator (see gen_planted).  adj must hold 2 * n_edges entries.
 int qgnn_generate_planted(int64_t nodes, int64_t n_edges, int64_t feat, int64_t classes,
                           int64_t blocks, double cross_frac, double gamma, double sep,

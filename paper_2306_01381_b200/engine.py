@@ -48,6 +48,21 @@ def partition_stats(g, owner, n_parts):
     return out  # per part: owned, central, marginal, halo, sum |remote_out|
 
 
+def exchange_plan(g, owner, n_parts: int, world: int, rank: int, dim: int, bits: int = 8,
+                  bwd: bool = False, layout: int = 0, dtype: str = "f32"):
+    """Bytes this rank sends to / receives from every rank for one tensor key
+    (qgnn_exchange_plan; the reference's pair_wire_bytes / negotiate_buffers,
+    assigner/plan.hpp:90-154).  Returns (send[world], recv[world])."""
+    ptr, adj = g["adj_ptr"], g["adj"]
+    own = np.ascontiguousarray(owner, np.uint32)
+    send = np.zeros(world, np.uint64)
+    recv = np.zeros(world, np.uint64)
+    check(lib.qgnn_exchange_plan(ptr.ctypes.data, adj.ctypes.data, len(ptr) - 1, own.ctypes.data,
+                                 n_parts, world, rank, dim, bits, int(bwd), layout,
+                                 1 if dtype == "f64" else 0, send.ctypes.data, recv.ctypes.data))
+    return send, recv
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_char * 128)()
     check(lib.qgnn_nccl_unique_id(buf))
@@ -161,12 +176,13 @@ class Engine:
                     launches_last_epoch=int(out[5]))
 
     def kernel_stats(self) -> dict:
-        out = np.zeros(3 * len(KCLASSES))
+        out = np.zeros(4 * len(KCLASSES))
         n = lib.qgnn_engine_kernel_stats(self._h, out.ctypes.data, len(out))
         if n < 0:
             check(-n)
-        return {KCLASSES[i]: dict(ms=out[3 * i], launches=int(out[3 * i + 1]),
-                                  bytes=out[3 * i + 2]) for i in range(n)}
+        return {KCLASSES[i]: dict(ms=out[4 * i], launches=int(out[4 * i + 1]),
+                                  bytes=out[4 * i + 2], gathered=out[4 * i + 3])
+                for i in range(n)}
 
 
 def smoke_epoch():
