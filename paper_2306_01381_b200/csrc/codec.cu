@@ -13,6 +13,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -325,8 +326,8 @@ __device__ __forceinline__ float first_zero_reg(const float (&v)[NV][4], int lan
   return (key & 1) ? -0.f : 0.f;
 }
 
-template <int NV>
-__global__ void __launch_bounds__(256) k_quantize_pack_f32(
+template <int NV, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_quantize_pack_f32(
     const float* __restrict__ values, int64_t ld, int dim, int64_t n,
     const int32_t* __restrict__ rows, const uint32_t* __restrict__ ids,
     const uint8_t* __restrict__ bits, const uint64_t* __restrict__ offsets,
@@ -572,18 +573,31 @@ int qgnn_quantize_pack(qgnn_ctx* ctx, const void* values, int dtype, int64_t ld,
     auto* wl = static_cast<float*>(win_lo);
     auto* wh = static_cast<float*>(win_hi);
     const int d = static_cast<int>(dim);
-    if (nv <= 1)
-      k_quantize_pack_f32<1><<<fblocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,
-                                                        set_of, set_keys, out, wl, wh, ctx->d_err);
-    else if (nv <= 2)
-      k_quantize_pack_f32<2><<<fblocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,
-                                                        set_of, set_keys, out, wl, wh, ctx->d_err);
-    else if (nv <= 4)
-      k_quantize_pack_f32<4><<<fblocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,
-                                                        set_of, set_keys, out, wl, wh, ctx->d_err);
-    else
-      k_quantize_pack_f32<8><<<fblocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,
-                                                        set_of, set_keys, out, wl, wh, ctx->d_err);
+    static const int minb = [] {
+      const char* e = std::getenv("QGNN_K1_MINB");  // occupancy target (measured best: 4)
+      return e ? std::atoi(e) : 4;
+    }();
+#define QGNN_K1_LAUNCH(NVV, MB)                                                                  \
+  k_quantize_pack_f32<NVV, MB><<<fblocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets, \
+                                                          set_of, set_keys, out, wl, wh, ctx->d_err)
+#define QGNN_K1_NV(NVV)                 \
+  if (minb >= 4)                        \
+    QGNN_K1_LAUNCH(NVV, 4);             \
+  else if (minb == 3)                   \
+    QGNN_K1_LAUNCH(NVV, 3);             \
+  else                                  \
+    QGNN_K1_LAUNCH(NVV, 1);
+    if (nv <= 1) {
+      QGNN_K1_NV(1)
+    } else if (nv <= 2) {
+      QGNN_K1_NV(2)
+    } else if (nv <= 4) {
+      QGNN_K1_NV(4)
+    } else {
+      QGNN_K1_NV(8)
+    }
+#undef QGNN_K1_NV
+#undef QGNN_K1_LAUNCH
   } else if (dtype == QGNN_F64)
     k_quantize_pack<double><<<blocks, threads, 0, s>>>(
         static_cast<const double*>(values), ld, static_cast<int>(dim), n, rows, ids, bits, offsets,

@@ -309,12 +309,17 @@ __global__ void __launch_bounds__(256, 4) k_spmm_f32g(
     const int32_t* __restrict__ ca, const float* __restrict__ aa, const int64_t* __restrict__ pb,
     const int32_t* __restrict__ cb, const float* __restrict__ ab, int64_t r0, int64_t n_rows,
     float* __restrict__ out, int64_t ldo, int64_t hub_deg, const float* __restrict__ mask,
-    int64_t ldm) {
+    int64_t ldm, int parts) {
+  // `parts` > 1: the row is cut into `parts` column ranges of `dim` floats, handled
+  // by the consecutive CTAs blockIdx.x = parts * row_block + part (wide rows keep
+  // 8 gathers per lane in flight at a register budget that allows 32 warps/SM)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = dim >> 2, E = 32 / G;
-  const int grp = lane / G, sub = lane - grp * G;
+  const int grp = lane / G, sub0 = lane - grp * G;
   const bool act = grp < E;
-  const int64_t r = r0 + int64_t(blockIdx.x) * 8 + warp;
+  const int part = int(blockIdx.x % unsigned(parts));
+  const int sub = sub0 + part * G;  // float4 column of this lane in the full row
+  const int64_t r = r0 + int64_t(blockIdx.x / unsigned(parts)) * 8 + warp;
   if (r >= r0 + n_rows) return;
   const int64_t ea0 = pa[r], ea1 = pa[r + 1];
   const int64_t eb0 = pb ? pb[r] : 0, eb1 = pb ? pb[r + 1] : 0;
@@ -324,7 +329,7 @@ __global__ void __launch_bounds__(256, 4) k_spmm_f32g(
   if (pb) grp_gather(acc, y + sub * 4, ldy, eb0, eb1, cb, ab, lane, grp, E, act);
   const float4 mine = acc;  // group g's partial -> group 0, g ascending
   for (int g = 1; g < E; ++g) {
-    const int sl = (lane + g * G) & 31;
+    const int sl = (lane + g * G) & 31;  // same column (sub0) in group g
     acc.x += __shfl_sync(0xffffffffu, mine.x, sl);
     acc.y += __shfl_sync(0xffffffffu, mine.y, sl);
     acc.z += __shfl_sync(0xffffffffu, mine.z, sl);
@@ -435,12 +440,14 @@ __global__ void __launch_bounds__(256) k_spmm_hubred(
   }
 }
 
+static bool split_wide() {  // QGNN_SPMM_SPLIT=1: two warps per 256-wide row (measured slower)
+  const char* e = std::getenv("QGNN_SPMM_SPLIT");
+  return e && std::atoi(e) != 0;
+}
+
 static bool grouped_narrow() {  // QGNN_SPMM_GROUPED=0 selects the one-row-per-warp kernel
-  static const bool on = [] {
-    const char* e = std::getenv("QGNN_SPMM_GROUPED");
-    return !e || std::atoi(e) != 0;
-  }();
-  return on;
+  const char* e = std::getenv("QGNN_SPMM_GROUPED");
+  return !e || std::atoi(e) != 0;
 }
 
 // fp32 row-range SpMM with optional hub list (rows with > hub_deg neighbours).
@@ -465,12 +472,18 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
           dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask, ldm); \
     }                                                                                          \
     break;
-  if (nv == 1 && grouped_narrow()) {
-    k_spmm_f32g<<<unsigned(blocks), 256, 0, s>>>(dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab,
-                                                 row_begin, n_rows, out, ldo, hd, mask, ldm);
+  const int parts = nv == 1 ? 1 : (nv == 2 && dim % 8 == 0 && split_wide()) ? 2 : 0;
+  if (parts && grouped_narrow()) {
+    k_spmm_f32g<<<unsigned(blocks * parts), 256, 0, s>>>(dim / parts, x, ldx, y, ldy, sa, pa, ca,
+                                                         aa, pb, cb, ab, row_begin, n_rows, out,
+                                                         ldo, hd, mask, ldm, parts);
     if (hubs) {
-      k_spmm_hubseg<1><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(
-          dim, x, ldx, y, ldy, ca, aa, cb, ab, hp->seg, hp->n_segs, hp->part, hp->ldp);
+      if (nv == 1)
+        k_spmm_hubseg<1><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(
+            dim, x, ldx, y, ldy, ca, aa, cb, ab, hp->seg, hp->n_segs, hp->part, hp->ldp);
+      else
+        k_spmm_hubseg<2><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(
+            dim, x, ldx, y, ldy, ca, aa, cb, ab, hp->seg, hp->n_segs, hp->part, hp->ldp);
       k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 256)), 256, 0, s>>>(
           dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask,
           ldm);

@@ -101,6 +101,28 @@ def test_engine_hub_split_matches(cuda, monkeypatch):
     assert np.abs(wb - wh).max() < 1e-4
 
 
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_engine_wide_hub_rows_match(cuda, monkeypatch, split):
+    """256-wide hidden layers (two float4 per lane, or two warps per row) with
+    every row above the hub threshold give the same run as without hub splits."""
+    monkeypatch.setenv("QGNN_SPMM_SPLIT", split)
+
+    def run():
+        eng = Engine(GRAPH, [8, 256, 256, 3], n_parts=4, bit_mode="fixed", fixed_bits=8, seed=11,
+                     dtype="f32")
+        out = [eng.run_epoch()["train_loss"] for _ in range(3)]
+        w = np.concatenate([x.reshape(-1) for x in eng.weights()])
+        eng.close()
+        return out, w
+
+    base, wb = run()
+    monkeypatch.setenv("QGNN_HUB_DEG", "2")
+    hub, wh = run()
+    for a, b in zip(base, hub):
+        assert _rel(a, b) < 1e-5, (a, b)
+    assert np.abs(wb - wh).max() < 1e-4
+
+
 def test_engine_transform_first_last_layer(cuda, monkeypatch):
     """z = A(hW) for the narrowing last layer matches aggregate-then-transform (fp32)."""
     tf, wt = _run("fixed", 4, 4, "f32")
