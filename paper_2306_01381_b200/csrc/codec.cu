@@ -643,6 +643,100 @@ int qgnn_dequant_scatter(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int64_t di
 }  // extern "C"
 
 namespace qgnn_b200 {
+// Backward scatter-add, one launch: warp per destination row; the row's
+// incoming chunks (ascending source, engine.hpp:720-734) are decoded and summed
+// in registers, masked by the ReLU of h (when given) and added to out once.
+__global__ void __launch_bounds__(256) k_dequant_rows_f32(
+    const uint8_t* __restrict__ in, int64_t n_rows, const int32_t* __restrict__ rows,
+    const int32_t* __restrict__ ptr, const int32_t* __restrict__ msg, int dim,
+    const uint8_t* __restrict__ bits, const uint64_t* __restrict__ offsets,
+    float* __restrict__ out, int64_t ld, const float* __restrict__ mask, int64_t ldm,
+    int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (g >= n_rows) return;
+  const int nchunk = (dim + 3) >> 2;
+  constexpr int kMaxC = 4;  // float4 chunks per lane: dim <= 512
+  float4 acc[kMaxC];
+#pragma unroll
+  for (int i = 0; i < kMaxC; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int j = ptr[g]; j < ptr[g + 1]; ++j) {
+    const int m = msg[j];
+    const uint8_t* chunk = in + offsets[m];
+    const int b = bits[m];
+    if (b == 0) {  // raw fp32 row (BitMode::kFp)
+      const float4* src = reinterpret_cast<const float4*>(chunk);
+#pragma unroll
+      for (int i = 0; i < kMaxC; ++i) {
+        const int c = lane + 32 * i;
+        if (c < nchunk) {
+          const float4 v = src[c];
+          acc[i].x += v.x, acc[i].y += v.y, acc[i].z += v.z, acc[i].w += v.w;
+        }
+      }
+      continue;
+    }
+    const uint4 h = *reinterpret_cast<const uint4*>(chunk);
+    if (static_cast<int>(h.w & 0xff) != b || h.z != static_cast<uint32_t>(dim)) {
+      if (lane == 0) atomicOr(err, kErrDecode);
+      continue;
+    }
+    const float sc = __uint_as_float(h.x), zp = __uint_as_float(h.y);
+    const uint8_t* payload = chunk + kHdrGpu;
+    const uint32_t cmask = (1u << b) - 1;
+#pragma unroll
+    for (int i = 0; i < kMaxC; ++i) {
+      const int c = lane + 32 * i;
+      if (c >= nchunk) continue;
+      uint32_t word;
+      if (b == 8)
+        word = reinterpret_cast<const uint32_t*>(payload)[c];
+      else if (b == 4)
+        word = reinterpret_cast<const uint16_t*>(payload)[c];
+      else
+        word = payload[c];
+      acc[i].x += fmaf(static_cast<float>(word & cmask), sc, zp);
+      acc[i].y += fmaf(static_cast<float>((word >> b) & cmask), sc, zp);
+      acc[i].z += fmaf(static_cast<float>((word >> (2 * b)) & cmask), sc, zp);
+      acc[i].w += fmaf(static_cast<float>((word >> (3 * b)) & cmask), sc, zp);
+    }
+  }
+  const int64_t r = rows[g];
+#pragma unroll
+  for (int i = 0; i < kMaxC; ++i) {
+    const int c = lane + 32 * i;
+    if (c >= nchunk) continue;
+    float4 a = acc[i];
+    if (mask) {
+      const float4 hm = __ldg(reinterpret_cast<const float4*>(mask + r * ldm + 4 * c));
+      a.x = hm.x > 0.f ? a.x : 0.f;
+      a.y = hm.y > 0.f ? a.y : 0.f;
+      a.z = hm.z > 0.f ? a.z : 0.f;
+      a.w = hm.w > 0.f ? a.w : 0.f;
+    }
+    float* o = out + r * ld + 4 * c;
+    if (4 * c + 3 < dim) {
+      float4 p = *reinterpret_cast<float4*>(o);
+      p.x += a.x, p.y += a.y, p.z += a.z, p.w += a.w;
+      *reinterpret_cast<float4*>(o) = p;
+    } else {
+      const float av[4] = {a.x, a.y, a.z, a.w};
+      for (int q = 0; q < 4 && 4 * c + q < dim; ++q) o[q] += av[q];
+    }
+  }
+}
+
+void dequant_rows_add_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n_rows, const int32_t* rows,
+                          const int32_t* ptr, const int32_t* msg, int dim, const uint8_t* bits,
+                          const uint64_t* offsets, float* out, int64_t ld, const float* mask,
+                          int64_t ldm, cudaStream_t s) {
+  if (n_rows == 0) return;
+  QGNN_REQUIRE(dim <= 512, QGNN_EINVAL, "dequant_rows_add: dim must be <= 512");
+  k_dequant_rows_f32<<<unsigned(ceil_div(n_rows * 32, 256)), 256, 0, s>>>(
+      in, n_rows, rows, ptr, msg, dim, bits, offsets, out, ld, mask, ldm, ctx->d_err);
+  check_launch("k_dequant_rows_f32");
+}
+
 // fp32 GPU-layout decode + scatter-add with the ReLU-backward mask (engine)
 void dequant_add_masked_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int dim,
                             const uint8_t* bits, const uint64_t* offsets, const int32_t* dst_rows,

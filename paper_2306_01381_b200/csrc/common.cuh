@@ -67,6 +67,12 @@ void dequant_add_masked_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int dim
 void input_grad_masked_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int64_t din,
                            int64_t dout, int64_t row_begin, int64_t n_rows, float* out,
                            int64_t ldo, const float* mask, int64_t ldm, cudaStream_t s);
+// backward scatter-add in one launch: destination rows with their incoming
+// messages in ascending source order, decoded + summed per row (codec.cu)
+void dequant_rows_add_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n_rows, const int32_t* rows,
+                          const int32_t* ptr, const int32_t* msg, int dim, const uint8_t* bits,
+                          const uint64_t* offsets, float* out, int64_t ld, const float* mask,
+                          int64_t ldm, cudaStream_t s);
 // fp32 loss phase for the engine: CE over train rows + val/test hit counts (dense.cu)
 void loss_f32(qgnn_ctx* ctx, const float* logits, int64_t ld, int classes, const int32_t* labels,
               const int32_t* rows, int64_t n_train, int64_t n_val, int64_t n_test,
@@ -121,6 +127,12 @@ void dequant_add_masked_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int dim
 void input_grad_masked_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int64_t din,
                            int64_t dout, int64_t row_begin, int64_t n_rows, float* out,
                            int64_t ldo, const float* mask, int64_t ldm, cudaStream_t s);
+// backward scatter-add in one launch: destination rows with their incoming
+// messages in ascending source order, decoded + summed per row (codec.cu)
+void dequant_rows_add_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n_rows, const int32_t* rows,
+                          const int32_t* ptr, const int32_t* msg, int dim, const uint8_t* bits,
+                          const uint64_t* offsets, float* out, int64_t ld, const float* mask,
+                          int64_t ldm, cudaStream_t s);
 // fp32 loss phase for the engine: CE over train rows + val/test hit counts (dense.cu)
 void loss_f32(qgnn_ctx* ctx, const float* logits, int64_t ld, int classes, const int32_t* labels,
               const int32_t* rows, int64_t n_train, int64_t n_val, int64_t n_test,

@@ -264,6 +264,10 @@ class Engine final : public EngineBase {
       DBuf<uint64_t> off;
       int64_t n = 0;
       std::vector<int64_t> p_begin;  // [P+1] message ranges per source
+      // backward keys: destination rows with their incoming messages in ascending
+      // source order (one fused scatter-add launch instead of one per source)
+      DBuf<int32_t> acc_rows, acc_ptr, acc_msg;
+      int64_t n_acc_rows = 0;
     };
     std::vector<SendMeta> snd;
     std::vector<RecvMeta> rcv;
@@ -356,6 +360,34 @@ class Engine final : public EngineBase {
   void loss_phase();
   void backward_layer(int l);
   void backward_last();
+  // bwd_finish scatter-add (engine.hpp:718-738) of every received partial into dh_next.
+  // fp32 + GPU layout: one launch, warp per destination row summing its messages
+  // in ascending source order; otherwise one exact-order launch per source.
+  void scatter_add_all(PartDev& D, int k, int64_t din, int64_t ldi, const T* mask) {
+    auto& R = D.rcv[k];
+    if (!R.n) return;
+    double wire = 0;
+    for (int64_t src = 0; src < P_; ++src)
+      if (src != D.id) wire += double(msgs_[k][src][D.id].bytes);
+    if constexpr (sizeof(T) == 4) {
+      if (s_.layout == QGNN_WIRE_GPU && din <= 512) {
+        kbegin(QGNN_K_DEQUANT);
+        dequant_rows_add_f32(ctx_, arena_.p, R.n_acc_rows, R.acc_rows.p, R.acc_ptr.p, R.acc_msg.p,
+                             int(din), R.bits.p, R.off.p, D.dh_next.p, ldi, mask, ldi, s_main_);
+        kend(QGNN_K_DEQUANT, double(R.n_acc_rows) * 2 * din * sizeof(T) + double(R.n) * 13 + wire,
+             s_main_);
+        return;
+      }
+    }
+    for (int64_t src = 0; src < P_; ++src) {  // ascending source (engine.hpp:720-734)
+      const int64_t b = R.p_begin[src], e = R.p_begin[src + 1];
+      if (e == b) continue;
+      kbegin(QGNN_K_DEQUANT);
+      dequant_add(D, R, b, e, din, ldi, mask);
+      kend(QGNN_K_DEQUANT, double(e - b) * (2 * din * sizeof(T) + 13) +
+                               double(msgs_[k][src][D.id].bytes), s_main_);
+    }
+  }
   // ascending-source scatter-add of decoded rows [b, e) of R into dh_next (mask: fp32 ReLU bwd)
   template <typename R_>
   void dequant_add(PartDev& D, R_& R, int64_t b, int64_t e, int64_t din, int64_t ldi, const T* mask) {
@@ -1040,6 +1072,25 @@ void Engine<T>::upload_key_meta(int k) {
       }
     }
     R.p_begin[P_] = int64_t(dst.size());
+    if (K.bwd && (R.n != int64_t(dst.size()) || !R.acc_ptr.p)) {
+      std::vector<int32_t> order(dst.size());
+      std::iota(order.begin(), order.end(), 0);
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int32_t a, int32_t b) { return dst[a] < dst[b]; });  // keeps source order
+      std::vector<int32_t> rows, ptr{0};
+      for (size_t i = 0; i < order.size(); ++i) {
+        if (i == 0 || dst[order[i]] != dst[order[i - 1]]) {
+          if (i) ptr.push_back(int32_t(i));
+          rows.push_back(dst[order[i]]);
+        }
+      }
+      ptr.push_back(int32_t(order.size()));
+      if (rows.empty()) ptr.assign(1, 0);
+      R.acc_rows.upload(rows);
+      R.acc_ptr.upload(ptr);
+      R.acc_msg.upload(order);
+      R.n_acc_rows = int64_t(rows.size());
+    }
     if (R.n != int64_t(dst.size()) || !R.dst.p) R.dst.upload(dst);
     R.n = int64_t(dst.size());
     R.bits.upload(rb);
@@ -1383,15 +1434,7 @@ void Engine<T>::backward_layer(int l) {
   wait_exchange();
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
-    auto& R = D.rcv[k];
-    for (int64_t src = 0; src < P_; ++src) {  // ascending source (engine.hpp:720-734)
-      const int64_t b = R.p_begin[src], e = R.p_begin[src + 1];
-      if (e == b) continue;
-      kbegin(QGNN_K_DEQUANT);
-      dequant_add(D, R, b, e, din, ldi, mk ? D.h[t].p : nullptr);
-      kend(QGNN_K_DEQUANT, double(e - b) * (2 * din * sizeof(T) + 13) +
-                               double(msgs_[k][src][D.id].bytes), s_main_);
-    }
+    scatter_add_all(D, k, din, ldi, mk ? D.h[t].p : nullptr);
     std::swap(D.dh, D.dh_next);
   }
   dh_masked_ = mk;
@@ -1520,15 +1563,7 @@ void Engine<T>::backward_last_tf(int l) {
   wait_exchange();
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
-    auto& R = D.rcv[k];
-    for (int64_t src = 0; src < P_; ++src) {
-      const int64_t b = R.p_begin[src], e = R.p_begin[src + 1];
-      if (e == b) continue;
-      kbegin(QGNN_K_DEQUANT);
-      dequant_add(D, R, b, e, din, ldi, mk ? D.h[t].p : nullptr);
-      kend(QGNN_K_DEQUANT, double(e - b) * (2 * din * sizeof(T) + 13) +
-                               double(msgs_[k][src][D.id].bytes), s_main_);
-    }
+    scatter_add_all(D, k, din, ldi, mk ? D.h[t].p : nullptr);
     std::swap(D.dh, D.dh_next);
   }
   dh_masked_ = mk;
