@@ -251,15 +251,22 @@ def impl_ours(args):
     torch.cuda.synchronize()
     h2d_gbs = h2d / (e0.elapsed_time(e1) / 1e3) / 1e9
     del dev_copy
+    # the e2e loop a training script would run: every step's inputs are copied
+    # from pinned host memory and its loss / accuracy read back; the copy of
+    # step i+1's inputs is issued while step i runs (double-buffered staging)
+    n_e2e = max(3, args.steps // 2)
     eng.set_features(feats)  # untimed warm-up of the e2e path (staging buffer allocation)
     eng.run_epoch()
     barrier(world)
     t0 = time.time()
-    for _ in range(max(3, args.steps // 2)):
-        eng.set_features(feats)
-        m = eng.run_epoch()
+    eng.set_features(feats)
+    for i in range(n_e2e):
+        eng.launch_epoch()
+        if i + 1 < n_e2e:
+            eng.set_features(feats)
+        m = eng.finish_epoch()
         _ = (m["train_loss"], m["val_acc"])
-    e2e_s = allmax((time.time() - t0) / max(3, args.steps // 2), world)
+    e2e_s = allmax((time.time() - t0) / n_e2e, world)
     hbm, tflops, src = peaks()
     # roofline of the dominant kernel class
     dom = max((k for k in ks if k != "exchange"), key=lambda k: ks[k]["ms"])

@@ -225,6 +225,13 @@ int qgnn_engine_create(const qgnn_settings* s, int64_t n_nodes, const int64_t* a
 int qgnn_engine_destroy(qgnn_engine* e);
 /* One epoch (run_epoch, engine.hpp:384-426). */
 int qgnn_engine_run_epoch(qgnn_engine* e, qgnn_epoch_metrics* out);
+/* run_epoch split in two: launch enqueues the epoch on the engine's streams and
+ * returns; finish waits for it and fills the metrics (loss / accuracy read
+ * back).  In between the caller may stage the next epoch's inputs with
+ * qgnn_engine_set_features (the copy overlaps the running epoch).  Weights
+ * cannot be read or written while an epoch is in flight (QGNN_EPROTOCOL). */
+int qgnn_engine_launch_epoch(qgnn_engine* e);
+int qgnn_engine_finish_epoch(qgnn_engine* e, qgnn_epoch_metrics* out);
 /* Re-upload node features (n_nodes x F, f32/f64, node order).  From pinned
  * (or device) memory the copy is asynchronous: node-range chunks stream in on a
  * copy stream and the next run_epoch gathers each partition as soon as its

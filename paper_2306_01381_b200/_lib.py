@@ -126,6 +126,8 @@ _SIGS = {
                                      vp, C.POINTER(vp)]),
     "qgnn_engine_destroy": (C.c_int, [vp]),
     "qgnn_engine_run_epoch": (C.c_int, [vp, C.POINTER(EpochMetrics)]),
+    "qgnn_engine_launch_epoch": (C.c_int, [vp]),
+    "qgnn_engine_finish_epoch": (C.c_int, [vp, C.POINTER(EpochMetrics)]),
     "qgnn_engine_set_features": (C.c_int, [vp, vp]),
     "qgnn_engine_get_weights": (C.c_int, [vp, C.c_int, vp]),
     "qgnn_engine_set_weights": (C.c_int, [vp, C.c_int, vp]),

@@ -210,6 +210,8 @@ class EngineBase {
  public:
   virtual ~EngineBase() = default;
   virtual void run_epoch(qgnn_epoch_metrics* m) = 0;
+  virtual void launch_epoch() = 0;
+  virtual void finish_epoch(qgnn_epoch_metrics* m) = 0;
   virtual void set_features(const void* f) = 0;
   virtual void get_weights(int l, void* out) = 0;
   virtual void set_weights(int l, const void* in) = 0;
@@ -224,7 +226,13 @@ class Engine final : public EngineBase {
          const void* features, const int32_t* labels, const uint8_t* train, const uint8_t* val,
          const uint8_t* test, const uint32_t* owner, const void* nccl_id);
   ~Engine() override;
-  void run_epoch(qgnn_epoch_metrics* m) override;
+  void run_epoch(qgnn_epoch_metrics* m) override {
+    launch_epoch();
+    finish_epoch(m);
+  }
+  void launch_epoch() override;
+  void finish_epoch(qgnn_epoch_metrics* m) override;
+  bool in_flight_ = false;
   void set_features(const void* f) override;
   void get_weights(int l, void* out) override;
   void set_weights(int l, const void* in) override;
@@ -463,7 +471,7 @@ class Engine final : public EngineBase {
   // async feature upload: node-range chunks on s_copy_, one event per chunk;
   // partition p's gather waits for the chunk holding its largest node id
   cudaStream_t s_copy_ = nullptr;
-  cudaEvent_t ev_main_done_ = nullptr;
+  cudaEvent_t ev_feat_free_ = nullptr;
   std::vector<int64_t> feat_bounds_;    // chunk c = nodes [bounds[c], bounds[c + 1])
   std::vector<cudaEvent_t> ev_feat_;    // per chunk
   std::vector<int> part_chunk_;         // local partition -> chunk it waits for
@@ -556,7 +564,7 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
   QGNN_CUDA(cudaEventCreateWithFlags(&ev_c_, cudaEventDisableTiming));
   QGNN_CUDA(cudaEventCreateWithFlags(&ev_d_, cudaEventDisableTiming));
   QGNN_CUDA(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking));
-  QGNN_CUDA(cudaEventCreateWithFlags(&ev_main_done_, cudaEventDisableTiming));
+  QGNN_CUDA(cudaEventCreateWithFlags(&ev_feat_free_, cudaEventDisableTiming));
   if (s.world > 1) {
     QGNN_REQUIRE(nccl_id, QGNN_EINVAL, "engine: world > 1 needs an NCCL unique id");
     if (std::memcmp(nccl_id, kLoopMagic, 8) == 0) {
@@ -739,6 +747,7 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
   set_features(features);
   if (feat_pending_) {  // construction consumes the features right away
     for (auto& up : parts_dev_) gather_features(*up);
+    QGNN_CUDA(cudaEventRecord(ev_feat_free_, s_main_));
     feat_pending_ = false;
   }
 
@@ -802,7 +811,7 @@ Engine<T>::~Engine() {
   if (s_copy_) cudaStreamDestroy(s_copy_);
   for (auto e : ev_feat_)
     if (e) cudaEventDestroy(e);
-  if (ev_main_done_) cudaEventDestroy(ev_main_done_);
+  if (ev_feat_free_) cudaEventDestroy(ev_feat_free_);
   if (ctx_) qgnn_ctx_destroy(ctx_);
 }
 
@@ -832,8 +841,10 @@ void Engine<T>::set_features(const void* f) {
     // the upload overlaps the first layer's work.  The caller keeps `f` alive
     // until the next run_epoch returns.
     if (!feat_all_.p || feat_all_.n < size_t(n_nodes_ * F)) feat_all_.alloc(n_nodes_ * F, false);
-    QGNN_CUDA(cudaEventRecord(ev_main_done_, s_main_));
-    QGNN_CUDA(cudaStreamWaitEvent(s_copy_, ev_main_done_, 0));
+    // the staging matrix is free once the last epoch's gathers have read it
+    // (ev_feat_free_ is recorded after them), so this copy may overlap the
+    // rest of an epoch that is still in flight
+    QGNN_CUDA(cudaStreamWaitEvent(s_copy_, ev_feat_free_, 0));
     for (size_t c = 0; c + 1 < feat_bounds_.size(); ++c) {
       const int64_t a = feat_bounds_[c], b = feat_bounds_[c + 1];
       QGNN_CUDA(cudaMemcpyAsync(feat_all_.p + a * F, src + a * F, size_t(b - a) * F * sizeof(T),
@@ -1284,6 +1295,8 @@ void Engine<T>::forward_layer(int l) {
   if (feats || s_.world == 1) {
     for (auto& up : parts_dev_) {
       if (feats) gather_features(*up);
+      if (feats && up.get() == parts_dev_.back().get())
+        QGNN_CUDA(cudaEventRecord(ev_feat_free_, s_main_));  // staging matrix consumed
       quantize(*up, k, up->h[t].p, ldi);  // fwd_send (engine.hpp:566-588)
       central(*up);
     }
@@ -1611,8 +1624,12 @@ void Engine<T>::step() {
   kend(QGNN_K_ELEMWISE, double(nparams_) * sizeof(T) * (P_ + 6), s_main_, 2);
 }
 
+// launch_epoch enqueues the whole epoch on the engine's streams and returns;
+// finish_epoch waits for it and reads the loss / accuracy back.  Between the
+// two the host may stage the next epoch's inputs (set_features).
 template <typename T>
-void Engine<T>::run_epoch(qgnn_epoch_metrics* m) {
+void Engine<T>::launch_epoch() {
+  QGNN_REQUIRE(!in_flight_, QGNN_EPROTOCOL, "launch_epoch: previous epoch not finished");
   ++epoch_;
   QGNN_CUDA(cudaSetDevice(s_.device));
   launches_ = 0;
@@ -1634,6 +1651,13 @@ void Engine<T>::run_epoch(qgnn_epoch_metrics* m) {
   backward_last();
   step();
   QGNN_CUDA(cudaEventRecord(ev_b_, s_main_));
+  in_flight_ = true;
+}
+
+template <typename T>
+void Engine<T>::finish_epoch(qgnn_epoch_metrics* m) {
+  QGNN_REQUIRE(in_flight_, QGNN_EPROTOCOL, "finish_epoch: no epoch in flight");
+  in_flight_ = false;
   QGNN_CUDA(cudaEventSynchronize(ev_b_));
   float ms = 0;
   QGNN_CUDA(cudaEventElapsedTime(&ms, ev_a_, ev_b_));
@@ -1825,6 +1849,7 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
 
 template <typename T>
 void Engine<T>::get_weights(int l, void* out) {
+  QGNN_REQUIRE(!in_flight_, QGNN_EPROTOCOL, "get_weights: an epoch is in flight");
   QGNN_REQUIRE(l >= 0 && l < L_, QGNN_EINVAL, "get_weights: bad layer");
   QGNN_CUDA(cudaMemcpy(out, w_.p + woff_[l], dims_[l] * dims_[l + 1] * sizeof(T),
                        cudaMemcpyDeviceToHost));
@@ -1832,6 +1857,7 @@ void Engine<T>::get_weights(int l, void* out) {
 
 template <typename T>
 void Engine<T>::set_weights(int l, const void* in) {
+  QGNN_REQUIRE(!in_flight_, QGNN_EPROTOCOL, "set_weights: an epoch is in flight");
   QGNN_REQUIRE(l >= 0 && l < L_, QGNN_EINVAL, "set_weights: bad layer");
   QGNN_CUDA(cudaMemcpy(w_.p + woff_[l], in, dims_[l] * dims_[l + 1] * sizeof(T),
                        cudaMemcpyHostToDevice));
@@ -1916,6 +1942,20 @@ int qgnn_engine_run_epoch(qgnn_engine* e, qgnn_epoch_metrics* m) {
   QGNN_API_BEGIN
   QGNN_REQUIRE(e && m, QGNN_EINVAL, "null engine");
   e->impl->run_epoch(m);
+  QGNN_API_END
+}
+
+int qgnn_engine_launch_epoch(qgnn_engine* e) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(e, QGNN_EINVAL, "null engine");
+  e->impl->launch_epoch();
+  QGNN_API_END
+}
+
+int qgnn_engine_finish_epoch(qgnn_engine* e, qgnn_epoch_metrics* m) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(e && m, QGNN_EINVAL, "null engine");
+  e->impl->finish_epoch(m);
   QGNN_API_END
 }
 

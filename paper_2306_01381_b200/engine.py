@@ -142,6 +142,16 @@ class Engine:
         check(lib.qgnn_engine_run_epoch(self._h, C.byref(m)))
         return m.as_dict()
 
+    def launch_epoch(self) -> None:
+        """Enqueue one epoch and return (pair with finish_epoch)."""
+        check(lib.qgnn_engine_launch_epoch(self._h))
+
+    def finish_epoch(self) -> dict:
+        """Wait for the launched epoch; returns its metrics (loss read back)."""
+        m = _lib.EpochMetrics()
+        check(lib.qgnn_engine_finish_epoch(self._h, C.byref(m)))
+        return m.as_dict()
+
     def set_features(self, feats):
         """Upload node features (n x F).  A pinned torch tensor (or a CUDA
         tensor) takes the fast path: asynchronous node-range copies that the

@@ -12,7 +12,8 @@ import json
 import os
 import sys
 
-UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "ns": 1e-9,
+         "us": 1e-6, "usecond": 1e-6, "ms": 1e-3,
          "msecond": 1e-3}
 # engine-level launches (kend calls) per class per epoch for the bench workload (P = 8, 3 layers)
 KENDS = {"spmm_fwd": 48, "spmm_bwd": 16, "partials": 16, "quant": 40, "gemm_fwd": 48}

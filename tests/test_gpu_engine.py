@@ -132,3 +132,36 @@ def test_engine_transform_first_last_layer(cuda, monkeypatch):
         assert _rel(a["train_loss"], b["train_loss"]) < 1e-5
         assert a["ref_bytes_total"] == b["ref_bytes_total"]
     assert np.abs(wt - wa).max() < 1e-4
+
+
+def test_overlapped_feature_staging_is_identical(cuda):
+    """launch_epoch / set_features(next) / finish_epoch (inputs of step i+1 copied
+    while step i runs) trains exactly like set_features + run_epoch."""
+    import torch
+    feats = torch.from_numpy(np.ascontiguousarray(GRAPH["features"], np.float32)).pin_memory()
+
+    def make():
+        return Engine(GRAPH, [8, 12, 3], n_parts=4, bit_mode="fixed", fixed_bits=4, seed=11,
+                      dtype="f32")
+
+    a = make()
+    seq = []
+    for _ in range(4):
+        a.set_features(feats)
+        seq.append(a.run_epoch()["train_loss"])
+    wa = np.concatenate([x.reshape(-1) for x in a.weights()])
+    a.close()
+    b = make()
+    ovl = []
+    b.set_features(feats)
+    for i in range(4):
+        b.launch_epoch()
+        if i < 3:
+            b.set_features(feats)
+        ovl.append(b.finish_epoch()["train_loss"])
+    wb = np.concatenate([x.reshape(-1) for x in b.weights()])
+    with pytest.raises(Exception):
+        b.finish_epoch()  # nothing in flight
+    b.close()
+    assert seq == ovl
+    assert (wa == wb).all()
