@@ -260,12 +260,14 @@ def impl_ours(args):
     barrier(world)
     t0 = time.time()
     eng.set_features(feats)
+    e2e_dev = []
     for i in range(n_e2e):
         eng.launch_epoch()
         if i + 1 < n_e2e:
             eng.set_features(feats)
         m = eng.finish_epoch()
         _ = (m["train_loss"], m["val_acc"])
+        e2e_dev.append(m["ms_total"])
     e2e_s = allmax((time.time() - t0) / n_e2e, world)
     hbm, tflops, src = peaks()
     # roofline of the dominant kernel class
@@ -321,7 +323,8 @@ def impl_ours(args):
             "data": "synthetic", "config": config_dict(world, bit_mode),
             "wall_s_per_step": wall_s,
             "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": 8 * 3, "h2d_gbs_raw": h2d_gbs},
+                    "d2h_bytes_per_step": 8 * 3, "h2d_gbs_raw": h2d_gbs,
+                    "device_ms_per_step": float(np.mean(e2e_dev))},
             "gpu_launches": launches * args.steps,
             "roofline_gather": ({"kernel": dom, "achieved": per_class[dom].get("gather_gbs"),
                                  "peak": GATHER_CEILING_GBS, "unit": "GB/s",
