@@ -317,9 +317,13 @@ __global__ void __launch_bounds__(256, 4) k_spmm_f32g(
   const int G = dim >> 2, E = 32 / G;
   const int grp = lane / G, sub0 = lane - grp * G;
   const bool act = grp < E;
-  const int part = int(blockIdx.x % unsigned(parts));
+  // parts > 0: column parts interleaved per row block; parts < 0: part-major
+  // (all rows of column part 0 first: an L2 working set of rows x dim floats)
+  const unsigned np = unsigned(parts < 0 ? -parts : parts);
+  const unsigned rb = parts < 0 ? (gridDim.x / np) : 0;
+  const int part = int(parts < 0 ? blockIdx.x / rb : blockIdx.x % np);
   const int sub = sub0 + part * G;  // float4 column of this lane in the full row
-  const int64_t r = r0 + int64_t(blockIdx.x / unsigned(parts)) * 8 + warp;
+  const int64_t r = r0 + int64_t(parts < 0 ? blockIdx.x % rb : blockIdx.x / np) * 8 + warp;
   if (r >= r0 + n_rows) return;
   const int64_t ea0 = pa[r], ea1 = pa[r + 1];
   const int64_t eb0 = pb ? pb[r] : 0, eb1 = pb ? pb[r + 1] : 0;
@@ -440,9 +444,11 @@ __global__ void __launch_bounds__(256) k_spmm_hubred(
   }
 }
 
-static bool split_wide() {  // QGNN_SPMM_SPLIT=1: two warps per 256-wide row (measured slower)
+// QGNN_SPMM_SPLIT=1: two warps per 256-wide row, interleaved (measured slower);
+// =2: the two column halves as two sweeps over all rows (half the L2 working set)
+static int split_wide() {
   const char* e = std::getenv("QGNN_SPMM_SPLIT");
-  return e && std::atoi(e) != 0;
+  return e ? std::atoi(e) : 0;
 }
 
 static bool grouped_narrow() {  // QGNN_SPMM_GROUPED=0 selects the one-row-per-warp kernel
@@ -472,11 +478,13 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
           dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask, ldm); \
     }                                                                                          \
     break;
-  const int parts = nv == 1 ? 1 : (nv == 2 && dim % 8 == 0 && split_wide()) ? 2 : 0;
+  const int sw = split_wide();
+  const int parts = nv == 1 ? 1 : (nv == 2 && dim % 8 == 0 && sw) ? (sw == 2 ? -2 : 2) : 0;
   if (parts && grouped_narrow()) {
-    k_spmm_f32g<<<unsigned(blocks * parts), 256, 0, s>>>(dim / parts, x, ldx, y, ldy, sa, pa, ca,
-                                                         aa, pb, cb, ab, row_begin, n_rows, out,
-                                                         ldo, hd, mask, ldm, parts);
+    const int np = parts < 0 ? -parts : parts;
+    k_spmm_f32g<<<unsigned(blocks * np), 256, 0, s>>>(dim / np, x, ldx, y, ldy, sa, pa, ca, aa, pb,
+                                                      cb, ab, row_begin, n_rows, out, ldo, hd, mask,
+                                                      ldm, parts);
     if (hubs) {
       if (nv == 1)
         k_spmm_hubseg<1><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(
