@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -145,6 +146,8 @@ struct Params {
   int relu;
   const float* mask;  // optional ReLU-backward mask: out = v * 1[mask > 0] (same row/col layout)
   int64_t ldm;
+  int mh;  // M halves per tile (MN-major path): 2 = 256-row tiles, the two TMEM buffers hold
+           // the two halves, so the N operand is read once per 256 output rows
 };
 
 // kMN = false: A K-major (tmA box {32, 128}), B/Blo K-major prepared (box {32, BN})
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  const int a_bytes = kBM * kBK * 4;        // 8 KB
+  const int a_bytes = kBM * kBK * 4 * p.mh;  // 8 KB per 128-row half
   const int b_bytes = p.BN * kBK * 4;       // BN x 64 B
   const int stage_bytes = 2 * a_bytes + 2 * b_bytes;
   const int kStages = p.stages;
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto tile_chunks = [&](int tile, int& m0, int& kc0, int& kc1, int& split) {
     const int mt = tile % p.m_tiles;
     split = tile / p.m_tiles;
-    m0 = mt * kBM;
+    m0 = mt * kBM * p.mh;
     kc0 = split * p.chunks_per_split;
     kc1 = min(p.k_chunks, kc0 + p.chunks_per_split);
   };
@@ -230,7 +233,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // 32-bit MN-major operands must use the 128B swizzle with 32-byte atoms
             // (TMA SWIZZLE_128B_ATOM_32B <-> UMMA SWIZZLE_128B_BASE32B): one box per
             // 32-wide MN group, kBK K rows of 128 B, groups 2 KB apart
-            for (int j = 0; j < kBM / 32; ++j) tma_load_2d(A + j * 2048, &tmA, &full[s], m0 + 32 * j, k0);
+            for (int j = 0; j < kBM * p.mh / 32; ++j)
+              tma_load_2d(A + j * 2048, &tmA, &full[s], m0 + 32 * j, k0);
             for (int j = 0; j < p.BN / 32; ++j) tma_load_2d(B + j * 2048, &tmB, &full[s], 32 * j, k0);
           }
           if (++s == kStages) s = 0, ph ^= 1;
@@ -248,8 +252,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
       int m0, kc0, kc1, split;
       tile_chunks(tile, m0, kc0, kc1, split);
-      const int acc = it & 1;
-      const uint32_t aph = (it >> 1) & 1;
+      // two accumulator buffers alternate between tiles, or (mh = 2) hold the
+      // two 128-row halves of one tile
+      const int acc = p.mh == 2 ? 0 : it & 1;
+      const uint32_t aph = p.mh == 2 ? (it & 1) : ((it >> 1) & 1);
       mbar_wait(&tempty[acc], aph ^ 1);
       tc_fence_after();
       const uint32_t d = tmem_base + uint32_t(acc * p.tmem_cols);
@@ -276,10 +282,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               dBh = sdesc(bH + 1024 * j, 2048, 512, 1);
               dBl = sdesc(bL + 1024 * j, 2048, 512, 1);
             }
-            tc_mma(d, dAh, dBh, idesc, first ? 0u : 1u);
+            for (int h = 0; h < (kMN ? p.mh : 1); ++h) {  // half h: A MN groups 4h..4h+3
+              const uint64_t hoff = uint64_t(h * (kBM * kBK * 4)) >> 4;
+              const uint32_t dh = d + uint32_t(h * p.tmem_cols);
+              tc_mma(dh, dAh + hoff, dBh, idesc, first ? 0u : 1u);
+              tc_mma(dh, dAh + hoff, dBl, idesc, 1u);
+              tc_mma(dh, dAl + hoff, dBh, idesc, 1u);
+            }
             first = false;
-            tc_mma(d, dAh, dBl, idesc, 1u);
-            tc_mma(d, dAl, dBh, idesc, 1u);
           }
           tc_commit(&empty[s]);
         }
@@ -296,10 +306,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
       int m0, kc0, kc1, split;
       tile_chunks(tile, m0, kc0, kc1, split);
-      const int acc = it & 1;
-      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      const int acc0 = p.mh == 2 ? 0 : it & 1;
+      mbar_wait(&tfull[acc0], p.mh == 2 ? (it & 1) : ((it >> 1) & 1));
       tc_fence_after();
-      const int row0 = m0 + 32 * q;  // this warp's 32 accumulator rows (TMEM lanes 32q..)
+      for (int h = 0; h < p.mh; ++h) {
+      const int acc = acc0 + h;  // TMEM buffer: tile parity, or the tile's half
+      const int row0 = m0 + 128 * h + 32 * q;  // this warp's 32 rows (TMEM lanes 32q..)
       float* out_base = p.out + (kMN ? int64_t(split) * p.M * p.N : 0);
       float* st = stage_out + q * (32 * 36);
       // 32-column groups: TMEM -> registers (thread = row) -> ReLU / mask -> smem
@@ -371,8 +383,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       }
+      }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      mbar_arrive(&tempty[acc0]);
     }
   } else if (warp >= 8) {
     // ---------------- converters
@@ -456,26 +469,31 @@ CUtensorMap make_map(const float* base, uint64_t inner, uint64_t outer, uint64_t
   return m;
 }
 
+bool wgrad_m256() {  // QGNN_WGRAD_M256=0: 128-row tiles (A/B)
+  const char* e = std::getenv("QGNN_WGRAD_M256");
+  return !e || std::atoi(e) != 0;
+}
+
 int pow2_cols(int bn) {
   int c = 32;
   while (c < bn) c <<= 1;
   return c;
 }
 
-constexpr size_t kSmemBudget = 184 * 1024;  // + 18 KB epilogue staging
-int stages_for(int BN) {
-  const size_t stage = 2 * tc::kBM * tc::kBK * 4 + 2 * size_t(BN) * tc::kBK * 4;
+constexpr size_t kSmemBudget = 200 * 1024;  // + 18 KB epilogue staging (<= 227 KB)
+int stages_for(int BN, int mh = 1) {
+  const size_t stage = 2 * tc::kBM * tc::kBK * 4 * size_t(mh) + 2 * size_t(BN) * tc::kBK * 4;
   return int(std::max<size_t>(2, std::min<size_t>(tc::kMaxStages, kSmemBudget / stage)));
 }
-size_t smem_bytes(int BN) {
-  const size_t stage = 2 * tc::kBM * tc::kBK * 4 + 2 * size_t(BN) * tc::kBK * 4;
-  return size_t(stages_for(BN)) * stage + 1024 + 256 + 4 * 32 * 36 * sizeof(float);
+size_t smem_bytes(int BN, int mh = 1) {
+  const size_t stage = 2 * tc::kBM * tc::kBK * 4 * size_t(mh) + 2 * size_t(BN) * tc::kBK * 4;
+  return size_t(stages_for(BN, mh)) * stage + 1024 + 256 + 4 * 32 * 36 * sizeof(float);
 }
 
 template <bool kMN>
 void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo, const tc::Params& p,
             int num_sms, cudaStream_t s) {
-  const size_t sm = smem_bytes(p.BN);
+  const size_t sm = smem_bytes(p.BN, p.mh);
   static bool attr_set = false;
   if (!attr_set) {
     QGNN_CUDA(cudaFuncSetAttribute(tc::k_tc_gemm<kMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -521,6 +539,7 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
   p.relu = relu;
   p.mask = mask;
   p.ldm = ldm;
+  p.mh = 1;
   p.stages = stages_for(BN);
   launch<false>(ta, tb, tbl, p, ctx->num_sms, s);
 }
@@ -533,7 +552,9 @@ float* tc_gemm_wgrad_partials(qgnn_ctx* ctx, const float* A, int64_t lda, const 
                               cudaStream_t s) {
   QGNN_REQUIRE(N <= 256, QGNN_EINVAL, "tc_gemm_wgrad: N must be <= 256");
   const int BN = int(round_up(N, 32));
-  const int m_tiles = int(ceil_div(M, tc::kBM));
+  // 256-row tiles when M > 128 (the N operand streams once per 256 output rows)
+  const int mh = M > tc::kBM && wgrad_m256() ? 2 : 1;
+  const int m_tiles = int(ceil_div(M, tc::kBM * mh));
   const int k_chunks = int(ceil_div(std::max<int64_t>(n_rows, 1), tc::kBK));
   int splits = std::max(1, std::min(k_chunks, ctx->num_sms / std::max(1, m_tiles)));
   const int cps = int(ceil_div(k_chunks, splits));
@@ -558,7 +579,8 @@ float* tc_gemm_wgrad_partials(qgnn_ctx* ctx, const float* A, int64_t lda, const 
   p.relu = 0;
   p.mask = nullptr;
   p.ldm = 0;
-  p.stages = stages_for(BN);
+  p.mh = mh;
+  p.stages = stages_for(BN, mh);
   launch<true>(ta, tb, tb, p, ctx->num_sms, s);
   *splits_out = splits;
   return part;
