@@ -453,6 +453,144 @@ __global__ void __launch_bounds__(256, MINB) k_quantize_pack_f32(
   }
 }
 
+// Lean variant for dim % 4 == 0 (every production width): the profile of the
+// general kernel showed the integer ALU pipe at 64 % with ~116 instructions per
+// element (bounds checks, compare/select chains, divergence bookkeeping).
+// Here: no per-element bounds, extrema with FMNMX, the signed-zero search only
+// when the row holds a -0.0 (the first-occurrence rule can only differ then),
+// and per element one counter draw plus a branch-free fp64 decision whose
+// exactness is checked arithmetically (see quant_fast); flagged elements
+// (~1e-12, and never h == lo) take quant_exact.  Same codes and headers.
+template <int NV, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_quantize_pack_lean(
+    const float* __restrict__ values, int64_t ld, int dim, int64_t n,
+    const int32_t* __restrict__ rows, const uint32_t* __restrict__ ids,
+    const uint8_t* __restrict__ bits, const uint64_t* __restrict__ offsets,
+    const uint16_t* __restrict__ set_of, const uint64_t* __restrict__ set_keys,
+    uint8_t* __restrict__ out, float* __restrict__ win_lo, float* __restrict__ win_hi,
+    int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int nchunk = dim >> 2;
+  for (int64_t m = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; m < n;
+       m += wstride) {
+    const float* row = values + static_cast<int64_t>(rows[m]) * ld;
+    const int b = bits[m];
+    uint8_t* chunk = out + offsets[m];
+    float v[NV][4];
+    float lo = INFINITY, hi = -INFINITY;
+    bool finite = true, negz = false;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = lane + 32 * i;
+      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (c < nchunk) t = __ldg(reinterpret_cast<const float4*>(row) + c);
+      v[i][0] = t.x, v[i][1] = t.y, v[i][2] = t.z, v[i][3] = t.w;
+      if (c < nchunk) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          lo = fminf(lo, v[i][q]);
+          hi = fmaxf(hi, v[i][q]);
+          finite &= fabsf(v[i][q]) < INFINITY;
+          negz |= __float_as_uint(v[i][q]) == 0x80000000u;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    finite = __all_sync(0xffffffffu, finite);
+    // fminf/fmaxf may pick either signed zero; the reference keeps the first
+    // occurrence (quant.hpp:63-68), which only matters if a -0.0 is present
+    if (lo == 0.f || hi == 0.f) {
+      float z0 = 0.f;
+      if (__any_sync(0xffffffffu, negz)) z0 = first_zero_reg<NV>(v, lane, dim);
+      if (lo == 0.f) lo = z0;
+      if (hi == 0.f) hi = z0;
+    }
+    if (lane == 0 && win_lo) {  // trace.hpp:86-91 (update precedes encode, engine.hpp:487)
+      const float wl = win_lo[m], wh = win_hi[m];
+      win_lo[m] = lo < wl ? lo : wl;
+      win_hi[m] = wh < hi ? hi : wh;
+    }
+    if (b == 0) {  // BitMode::kFp: raw row (engine.hpp:473-481)
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int c = lane + 32 * i;
+        if (c < nchunk)
+          reinterpret_cast<float4*>(chunk)[c] = make_float4(v[i][0], v[i][1], v[i][2], v[i][3]);
+      }
+      continue;
+    }
+    if (b != 2 && b != 4 && b != 8) {
+      if (lane == 0) atomicOr(err, kErrBadWidth);
+      continue;
+    }
+    if (!finite) {
+      if (lane == 0) atomicOr(err, kErrNonFinite);
+      continue;
+    }
+    const double lo_d = lo, hi_d = hi;
+    const uint32_t levels = (1u << b) - 1;
+    const bool constant = hi_d == lo_d;
+    const double scale = constant ? 0.0 : (hi_d - lo_d) / static_cast<double>(levels);
+    if (lane == 0) {
+      uint4 h;
+      h.x = __float_as_uint(static_cast<float>(scale));
+      h.y = __float_as_uint(lo);
+      h.z = static_cast<uint32_t>(dim);
+      h.w = static_cast<uint32_t>(b);
+      *reinterpret_cast<uint4*>(chunk) = h;
+    }
+    uint8_t* payload = chunk + kHdrGpu;
+    const int padded = static_cast<int>(((packed_bytes(dim, b) + 15) / 16) * 16);
+    const int units = (padded * 2) >> (b == 8 ? 3 : b == 4 ? 2 : 1);
+    const uint64_t key = rng_fork(set_keys[set_of ? set_of[m] : 0], ids[m]);
+    const double rcp = constant ? 0.0 : __drcp_rn(scale);
+    const double x_hi = constant ? 0.0 : __ddiv_rn(__dsub_rn(hi_d, lo_d), scale);
+    constexpr double tol = 0x1.0p-40;
+#pragma unroll
+    for (int i = 0; i < NV + 1; ++i) {
+      const int c = lane + 32 * i;
+      if (c >= units) break;
+      uint32_t word = 0;
+      if (i < NV && c < nchunk && !constant) {
+        const uint64_t z0 = key + static_cast<uint64_t>(4 * c + 1) * kPhi;
+        bool slow = false;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float hq = v[i][q];
+          const double a = __dsub_rn(static_cast<double>(hq), lo_d);
+          const double u =
+              static_cast<double>(rng_mix(z0 + uint64_t(q) * kPhi) >> 11) * 0x1.0p-53;
+          const double x = hq == hi ? x_hi : __dmul_rn(a, rcp);
+          const double base = floor(x);
+          const double frac = __dsub_rn(x, base);
+          const uint32_t code = static_cast<uint32_t>(base) + (u < frac ? 1u : 0u);
+          word |= min(code, levels) << (q * b);
+          // x' within 2^-43 of x: the decision can only differ near a boundary
+          slow |= hq != hi && a != 0.0 &&
+                  (frac < tol || frac > 1.0 - tol || fabs(u - frac) < tol);
+        }
+        if (slow) {  // ~1e-12 per element: recompute the chunk exactly
+          const double lv = static_cast<double>(levels);
+          word = 0;
+          for (int q = 0; q < 4; ++q)
+            word |= quant_exact(v[i][q], lo_d, scale, lv, z0 + uint64_t(q) * kPhi) << (q * b);
+        }
+      }
+      if (b == 8)
+        reinterpret_cast<uint32_t*>(payload)[c] = word;
+      else if (b == 4)
+        reinterpret_cast<uint16_t*>(payload)[c] = static_cast<uint16_t>(word);
+      else
+        payload[c] = static_cast<uint8_t>(word);
+    }
+  }
+}
+
 // Decode counterpart: lane l writes the float4 chunks c = l + 32 i of the row.
 __global__ void __launch_bounds__(256) k_dequant_f32(
     const uint8_t* __restrict__ in, int64_t n, int dim, const uint8_t* __restrict__ bits,
@@ -577,9 +715,18 @@ int qgnn_quantize_pack(qgnn_ctx* ctx, const void* values, int dtype, int64_t ld,
       const char* e = std::getenv("QGNN_K1_MINB");  // occupancy target (measured best: 4)
       return e ? std::atoi(e) : 4;
     }();
-#define QGNN_K1_LAUNCH(NVV, MB)                                                                  \
-  k_quantize_pack_f32<NVV, MB><<<fblocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets, \
-                                                          set_of, set_keys, out, wl, wh, ctx->d_err)
+    static const bool lean = [] {
+      const char* e = std::getenv("QGNN_K1_LEAN");
+      return !e || std::atoi(e) != 0;
+    }();
+#define QGNN_K1_LAUNCH(NVV, MB)                                                                     \
+  if (lean && d % 4 == 0)                                                                           \
+    k_quantize_pack_lean<NVV, MB><<<fblocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets, \
+                                                             set_of, set_keys, out, wl, wh,         \
+                                                             ctx->d_err);                           \
+  else                                                                                              \
+    k_quantize_pack_f32<NVV, MB><<<fblocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,  \
+                                                            set_of, set_keys, out, wl, wh, ctx->d_err)
 #define QGNN_K1_NV(NVV)                 \
   if (minb >= 4)                        \
     QGNN_K1_LAUNCH(NVV, 4);             \

@@ -225,7 +225,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int k0 = kc * kBK;
           if (!kMN) {
             mbar_expect_tx(&full[s], a_bytes + 2 * b_bytes);
-            tma_load_2d(A, &tmA, &full[s], k0, m0);
+            for (int h = 0; h < p.mh; ++h)
+              tma_load_2d(A + h * (kBM * kBK * 4), &tmA, &full[s], k0, m0 + kBM * h);
             tma_load_2d(B, &tmB, &full[s], k0, 0);
             tma_load_2d(Blo, &tmBlo, &full[s], k0, 0);
           } else {
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               dBh = sdesc(bH + 1024 * j, 2048, 512, 1);
               dBl = sdesc(bL + 1024 * j, 2048, 512, 1);
             }
-            for (int h = 0; h < (kMN ? p.mh : 1); ++h) {  // half h: A MN groups 4h..4h+3
+            for (int h = 0; h < p.mh; ++h) {  // half h: rows 128h.. (MN groups 4h.. / SW64 atoms 16h..)
               const uint64_t hoff = uint64_t(h * (kBM * kBK * 4)) >> 4;
               const uint32_t dh = d + uint32_t(h * p.tmem_cols);
               tc_mma(dh, dAh + hoff, dBh, idesc, first ? 0u : 1u);
@@ -469,6 +470,11 @@ CUtensorMap make_map(const float* base, uint64_t inner, uint64_t outer, uint64_t
   return m;
 }
 
+bool gemm_m256() {  // QGNN_GEMM_M256=1: 256-row tiles for z = A W and dz W^T too (A/B)
+  const char* e = std::getenv("QGNN_GEMM_M256");
+  return e && std::atoi(e) != 0;
+}
+
 bool wgrad_m256() {  // QGNN_WGRAD_M256=0: 128-row tiles (A/B)
   const char* e = std::getenv("QGNN_WGRAD_M256");
   return !e || std::atoi(e) != 0;
@@ -539,8 +545,9 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
   p.relu = relu;
   p.mask = mask;
   p.ldm = ldm;
-  p.mh = 1;
-  p.stages = stages_for(BN);
+  p.mh = gemm_m256() && n_rows > tc::kBM ? 2 : 1;
+  p.m_tiles = int(ceil_div(n_rows, tc::kBM * p.mh));
+  p.stages = stages_for(BN, p.mh);
   launch<false>(ta, tb, tbl, p, ctx->num_sms, s);
 }
 
