@@ -8,11 +8,15 @@
 // TU is built with -ffp-contract=off, so plans, objectives and tie-breaks are
 // identical to the reference's solve_assignment.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <numeric>
 #include <optional>
+#include <string>
+#include <thread>
 
 #include "host.hpp"
 #include "qgnn_b200.h"
@@ -223,11 +227,123 @@ SolveResult group_and_order(const std::vector<PairStat>& pairs, int64_t group_si
   return plan;
 }
 
+// Exact solve (solve.hpp:264-309): every candidate makespan z (each pair's
+// reachable transfer times) gives each pair its min-variance assignment under
+// cap(z); the best (objective, variance, larger bits) wins.  Same caps, same
+// reconstruction, same evaluation order as the reference, but:
+//  * caps are non-decreasing in z, so each pair's cap advances by pointer
+//    instead of a binary search per candidate;
+//  * a pair is reconstructed only when its cap moves, and a candidate is
+//    evaluated only when some pair's bits actually changed (identical bits give
+//    an identical evaluation, which never beats the earlier candidate);
+//  * per-group variances for the three widths are tabulated once;
+//  * the candidate range is split over worker threads (each starts with binary
+//    searched caps) and merged in range order with the reference's tie-break.
+namespace {
+struct EvalCtx {
+  const SolveResult* plan;
+  const Cost* cm;
+  double lambda;
+  std::vector<double> var3;        // [group * 3 + bi] = variance_at(beta, 2/4/8)
+  std::vector<uint64_t> dimsum;    // per group (flat)
+  std::vector<size_t> pair_first;  // first flat group of each pair
+};
+
+Eval eval_bits(const EvalCtx& C, const std::vector<int>& bits) {  // == evaluate()
+  Eval ev;
+  const SolveResult& plan = *C.plan;
+  for (size_t i = 0; i < plan.pairs.size(); ++i) {
+    uint64_t pair_bits = 0;
+    for (size_t g = C.pair_first[i]; g < C.pair_first[i + 1]; ++g) {
+      const int b = bits[g];
+      ev.variance += C.var3[g * 3 + (b == 2 ? 0 : b == 4 ? 1 : 2)];
+      pair_bits += C.dimsum[g] * static_cast<uint64_t>(b);
+    }
+    const PlanPairG& pp = plan.pairs[i];
+    ev.z = std::max(ev.z, C.cm->seconds(pp.src, pp.dst, static_cast<double>(pair_bits)));
+  }
+  ev.objective = C.lambda * ev.variance + (1.0 - C.lambda) * ev.z;
+  return ev;
+}
+
+struct ScanBest {
+  bool have = false;
+  Eval best;
+  std::vector<int> bits;
+};
+
+void scan(const EvalCtx& C, const std::vector<Table>& tables, const std::vector<double>& cand,
+          size_t c0, size_t c1, ScanBest& out) {
+  if (c0 >= c1) return;
+  const SolveResult& plan = *C.plan;
+  const double inf = std::numeric_limits<double>::infinity();
+  const size_t P = tables.size();
+  // cap[i] = largest s <= smax with time_at(s) <= z (cap_for), or -1 if none
+  std::vector<int64_t> cap(P, -1);
+  std::vector<int64_t> done(P, -2);  // cap the bits below were built for
+  std::vector<int> bits(C.dimsum.size(), 0);
+  bool dirty = true;
+  for (size_t i = 0; i < P; ++i) {
+    const auto c = tables[i].cap_for(cand[c0]);
+    cap[i] = c ? int64_t(*c) : -1;
+  }
+  for (size_t ci = c0; ci < c1; ++ci) {
+    const double z = cand[ci];
+    bool feasible = true;
+    for (size_t i = 0; i < P; ++i) {
+      const Table& t = tables[i];
+      while (cap[i] < int64_t(t.smax) && t.time_at(uint64_t(cap[i] + 1)) <= z) ++cap[i];
+      if (cap[i] < 0 || t.mv(0, uint64_t(cap[i])) == inf) {
+        feasible = false;
+        continue;  // keep advancing the other caps
+      }
+      if (done[i] != cap[i]) {
+        std::vector<int> nb;
+        nb.reserve(plan.pairs[i].groups.size());
+        reconstruct(t, plan.pairs[i], uint64_t(cap[i]), nb);
+        done[i] = cap[i];
+        if (!std::equal(nb.begin(), nb.end(), bits.begin() + C.pair_first[i])) {
+          std::copy(nb.begin(), nb.end(), bits.begin() + C.pair_first[i]);
+          dirty = true;
+        }
+      }
+    }
+    if (!feasible || !dirty) continue;
+    dirty = false;
+    const Eval ev = eval_bits(C, bits);
+    if (!out.have || better(ev, bits, out.best, out.bits)) {
+      out.best = ev;
+      out.bits = bits;
+      out.have = true;
+    }
+  }
+}
+}  // namespace
+
 void solve_exact(SolveResult& plan, const Cost& cm, double lambda) {
   validate(plan, cm, lambda);
-  std::vector<Table> tables;
-  tables.reserve(plan.pairs.size());
-  for (const PlanPairG& pp : plan.pairs) tables.push_back(build_table(pp, cm));
+  // per-pair knapsack tables are independent: build them on worker threads
+  const size_t P = plan.pairs.size();
+  std::vector<Table> tables(P);
+  {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t W = std::min<size_t>(P, std::max(1u, std::min(16u, hw / 2)));
+    std::atomic<size_t> next{0};
+    std::vector<std::string> errs(W);
+    auto work = [&](size_t w) {
+      try {
+        for (size_t i = next++; i < P; i = next++) tables[i] = build_table(plan.pairs[i], cm);
+      } catch (const std::exception& e) {
+        errs[w] = e.what();
+      }
+    };
+    std::vector<std::thread> th;
+    for (size_t w = 1; w < W; ++w) th.emplace_back(work, w);
+    work(0);
+    for (auto& x : th) x.join();
+    for (const auto& e : errs)
+      QGNN_REQUIRE(e.empty(), QGNN_ERESOURCE, e);
+  }
   std::vector<double> cand;
   for (const Table& t : tables)
     for (uint64_t s = 0; s <= t.smax; ++s)
@@ -235,44 +351,44 @@ void solve_exact(SolveResult& plan, const Cost& cm, double lambda) {
   std::sort(cand.begin(), cand.end());
   cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
 
-  // The pair assignment is a function of its cap only: memoize per pair.
-  std::vector<std::optional<uint64_t>> last_cap(tables.size());
-  std::vector<std::vector<int>> last_bits(tables.size());
-  std::vector<int> best_bits, bits;
-  Eval best;
-  bool have = false;
-  SolveResult work = plan;
-  const double inf = std::numeric_limits<double>::infinity();
-  for (double z : cand) {
-    bits.clear();
-    bool feasible = true;
-    for (size_t i = 0; i < tables.size(); ++i) {
-      const auto cap = tables[i].cap_for(z);
-      if (!cap || tables[i].mv(0, *cap) == inf) {
-        feasible = false;
-        break;
-      }
-      if (!last_cap[i] || *last_cap[i] != *cap) {
-        last_bits[i].clear();
-        reconstruct(tables[i], plan.pairs[i], *cap, last_bits[i]);
-        last_cap[i] = cap;
-      }
-      bits.insert(bits.end(), last_bits[i].begin(), last_bits[i].end());
+  EvalCtx C;
+  C.plan = &plan;
+  C.cm = &cm;
+  C.lambda = lambda;
+  C.pair_first.push_back(0);
+  for (const PlanPairG& pp : plan.pairs) {
+    for (const Group& g : pp.groups) {
+      for (int bi = 0; bi < 3; ++bi) C.var3.push_back(variance_at(g.beta, kBits[bi]));
+      C.dimsum.push_back(g.dim_sum());
     }
-    if (!feasible) continue;
-    set_bits(work, bits);
-    const Eval ev = evaluate(work, cm, lambda);
-    if (!have || better(ev, bits, best, best_bits)) {
-      best = ev;
-      best_bits = bits;
-      have = true;
-    }
+    C.pair_first.push_back(C.dimsum.size());
   }
-  QGNN_REQUIRE(have, QGNN_EINVAL, "solve_assignment: no feasible assignment");
-  set_bits(plan, best_bits);
-  plan.objective = best.objective;
-  plan.variance = best.variance;
-  plan.z = best.z;
+
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  size_t T = std::min<size_t>(std::max<size_t>(1, cand.size() / 65536),
+                              std::max(1u, std::min(8u, hw / 4)));
+  if (const char* e = std::getenv("QGNN_SOLVE_THREADS"))  // tests: force the split
+    T = std::max<size_t>(1, std::min<size_t>(cand.size(), size_t(std::atoi(e))));
+  std::vector<ScanBest> part(T);
+  auto run = [&](size_t t) {
+    scan(C, tables, cand, cand.size() * t / T, cand.size() * (t + 1) / T, part[t]);
+  };
+  if (T == 1) {
+    run(0);
+  } else {
+    std::vector<std::thread> th;
+    for (size_t t = 0; t < T; ++t) th.emplace_back(run, t);
+    for (auto& x : th) x.join();
+  }
+  ScanBest best;
+  for (size_t t = 0; t < T; ++t)  // range order: earlier ranges win exact ties
+    if (part[t].have && (!best.have || better(part[t].best, part[t].bits, best.best, best.bits)))
+      best = std::move(part[t]);
+  QGNN_REQUIRE(best.have, QGNN_EINVAL, "solve_assignment: no feasible assignment");
+  set_bits(plan, best.bits);
+  plan.objective = best.best.objective;
+  plan.variance = best.best.variance;
+  plan.z = best.best.z;
 }
 
 void solve_brute(SolveResult& plan, const Cost& cm, double lambda) {

@@ -172,6 +172,40 @@ def test_solver_matches_reference_and_brute_force():  # test_assigner.cpp:228-24
     assert n_checked > 10
 
 
+@pytest.mark.skipif(not ref_available(), reason="compiled reference not present")
+@pytest.mark.parametrize("threads", ["1", "3"])
+def test_solver_large_instance_matches_reference(monkeypatch, threads):
+    """A larger instance (12 device pairs, ~12 groups each, mixed dims), scanned
+    on one and on several threads: plan, objective, variance and makespan must
+    equal the reference's exactly."""
+    import time
+    from oracle import ref
+    monkeypatch.setenv("QGNN_SOLVE_THREADS", threads)
+    rs = np.random.default_rng(7)
+    n_dev = 4
+    pairs = []
+    for s in range(n_dev):
+        for d in range(n_dev):
+            if s == d:
+                continue
+            msgs = []
+            for i in range(int(rs.integers(500, 700))):
+                lo = float(rs.normal())
+                msgs.append((i, int(rs.choice([100, 256, 47])), lo, lo + float(rs.exponential()),
+                             float(rs.uniform(0.1, 2.0))))
+            pairs.append((s, d, msgs))
+    theta = rs.uniform(1e-10, 1e-9, n_dev * n_dev)
+    gamma = rs.uniform(1e-5, 2e-5, n_dev * n_dev)
+    for lam in ((0.3,) if threads == "1" else (0.7,)):
+        t0 = time.time()
+        bits, ev = _solve(pairs, n_dev, theta, gamma, lam, 50)
+        t1 = time.time()
+        rbits, rev = ref.solve_instance(pairs, n_dev, theta, gamma, lam, 50)
+        t2 = time.time()
+        assert (bits == rbits).all() and (ev == rev).all(), lam
+        print(f"lambda {lam}: ours {t1 - t0:.3f} s, reference {t2 - t1:.3f} s")
+
+
 def test_solver_rejects_bad_instances():  # test_assigner.cpp:265-297
     pairs = [(0, 1, [(1, 4, 0.0, 1.0, 1.0)])]
     with pytest.raises(_lib.InvalidArgument):
