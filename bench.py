@@ -269,6 +269,15 @@ def impl_ours(args):
         _ = (m["train_loss"], m["val_acc"])
         e2e_dev.append(m["ms_total"])
     e2e_s = allmax((time.time() - t0) / n_e2e, world)
+    # the adaptive re-solve (host solver, every `period` epochs) is outside the
+    # per-epoch device time: run on to the next re-solve epoch and report it
+    resolve_s = None
+    if bit_mode == "adaptive":
+        for _ in range(60):
+            m2 = eng.run_epoch()
+            if m2["resolve_seconds"] > 0:
+                resolve_s = allmax(m2["resolve_seconds"], world)
+                break
     hbm, tflops, src = peaks()
     # roofline of the dominant kernel class
     dom = max((k for k in ks if k != "exchange"), key=lambda k: ks[k]["ms"])
@@ -340,6 +349,10 @@ def impl_ours(args):
                          "bytes_per_launch": d["bytes"] / max(1, d["launches"]),
                          "ms_per_launch": d["ms"] / max(1, d["launches"])},
             "quant_gbs": quant_gbs, "exchange_gbs": xchg,
+            "adaptive_resolve": ({"seconds": resolve_s, "period_epochs": 50,
+                                  "amortized_ms_per_epoch": resolve_s / 50 * 1e3,
+                                  "value_plus_amortized_s": dev_s + resolve_s / 50}
+                                 if resolve_s is not None else None),
             "kernels_ms_per_epoch": {k: v["ms"] / args.steps for k, v in ks.items()},
             "last_epoch": {k: m[k] for k in ("train_loss", "val_acc", "bytes_total",
                                              "ref_bytes_total", "msgs_b2", "msgs_b4",

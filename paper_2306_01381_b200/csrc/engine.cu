@@ -19,6 +19,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -1026,33 +1027,38 @@ void Engine<T>::arena_layout() {
 
 template <typename T>
 void Engine<T>::upload_key_meta(int k) {
+  // message lists never change: rows / ids / destinations (and the windows)
+  // are uploaded once; widths and wire offsets follow every plan
   const KeyInfo& K = keys_[k];
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
     const int64_t p = D.id;
     const View& V = D.view;
     auto& S = D.snd[k];
-    std::vector<int32_t> rows;
-    std::vector<uint32_t> ids;
     std::vector<uint8_t> bits;
     std::vector<uint64_t> off;
+    const bool fresh = !S.rows.p;
+    std::vector<int32_t> rows;
+    std::vector<uint32_t> ids;
     std::vector<uint16_t> set;
     S.q_begin.assign(P_ + 1, 0);
     for (int64_t q = 0; q < P_; ++q) {
-      S.q_begin[q] = int64_t(ids.size());
+      S.q_begin[q] = int64_t(bits.size());
       if (q == p) continue;
       const PairMsgs& m = msgs_[k][p][q];
       for (size_t i = 0; i < m.ids.size(); ++i) {
-        rows.push_back(K.bwd ? int32_t(V.device_slot_offset[q] + int64_t(i)) : V.gpu_row(m.ids[i]));
-        ids.push_back(m.ids[i]);
+        if (fresh) {
+          rows.push_back(K.bwd ? int32_t(V.device_slot_offset[q] + int64_t(i))
+                               : V.gpu_row(m.ids[i]));
+          ids.push_back(m.ids[i]);
+          set.push_back(uint16_t(q));
+        }
         bits.push_back(m.bits[i]);
         off.push_back(send_base_[k][p][q] + m.off[i]);
-        set.push_back(uint16_t(q));
       }
     }
-    S.q_begin[P_] = int64_t(ids.size());
-    const bool fresh = S.n != int64_t(ids.size()) || !S.rows.p;
-    S.n = int64_t(ids.size());
+    S.q_begin[P_] = int64_t(bits.size());
+    S.n = int64_t(bits.size());
     if (fresh) {
       S.rows.upload(rows);
       S.ids.upload(ids);
@@ -1068,42 +1074,47 @@ void Engine<T>::upload_key_meta(int k) {
     S.off.upload(off);
 
     auto& R = D.rcv[k];
+    const bool rfresh = !R.dst.p;
     std::vector<int32_t> dst;
     std::vector<uint8_t> rb;
     std::vector<uint64_t> ro;
     R.p_begin.assign(P_ + 1, 0);
     for (int64_t src = 0; src < P_; ++src) {
-      R.p_begin[src] = int64_t(dst.size());
+      R.p_begin[src] = int64_t(rb.size());
       if (src == p) continue;
       const PairMsgs& m = msgs_[k][src][p];
       for (size_t i = 0; i < m.ids.size(); ++i) {
-        dst.push_back(K.bwd ? V.gpu_row(m.ids[i]) : int32_t(V.device_slot_offset[src] + int64_t(i)));
+        if (rfresh)
+          dst.push_back(K.bwd ? V.gpu_row(m.ids[i])
+                              : int32_t(V.device_slot_offset[src] + int64_t(i)));
         rb.push_back(m.bits[i]);
         ro.push_back(recv_base_[k][p][src] + m.off[i]);
       }
     }
-    R.p_begin[P_] = int64_t(dst.size());
-    if (K.bwd && (R.n != int64_t(dst.size()) || !R.acc_ptr.p)) {
-      std::vector<int32_t> order(dst.size());
-      std::iota(order.begin(), order.end(), 0);
-      std::stable_sort(order.begin(), order.end(),
-                       [&](int32_t a, int32_t b) { return dst[a] < dst[b]; });  // keeps source order
-      std::vector<int32_t> rows, ptr{0};
-      for (size_t i = 0; i < order.size(); ++i) {
-        if (i == 0 || dst[order[i]] != dst[order[i - 1]]) {
-          if (i) ptr.push_back(int32_t(i));
-          rows.push_back(dst[order[i]]);
+    R.p_begin[P_] = int64_t(rb.size());
+    R.n = int64_t(rb.size());
+    if (rfresh) {
+      if (K.bwd) {  // destination rows with their messages in ascending source order
+        std::vector<int32_t> order(dst.size());
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int32_t a, int32_t b) { return dst[a] < dst[b]; });
+        std::vector<int32_t> rws, ptr{0};
+        for (size_t i = 0; i < order.size(); ++i) {
+          if (i == 0 || dst[order[i]] != dst[order[i - 1]]) {
+            if (i) ptr.push_back(int32_t(i));
+            rws.push_back(dst[order[i]]);
+          }
         }
+        ptr.push_back(int32_t(order.size()));
+        if (rws.empty()) ptr.assign(1, 0);
+        R.acc_rows.upload(rws);
+        R.acc_ptr.upload(ptr);
+        R.acc_msg.upload(order);
+        R.n_acc_rows = int64_t(rws.size());
       }
-      ptr.push_back(int32_t(order.size()));
-      if (rows.empty()) ptr.assign(1, 0);
-      R.acc_rows.upload(rows);
-      R.acc_ptr.upload(ptr);
-      R.acc_msg.upload(order);
-      R.n_acc_rows = int64_t(rows.size());
+      R.dst.upload(dst.empty() ? std::vector<int32_t>{0} : dst);
     }
-    if (R.n != int64_t(dst.size()) || !R.dst.p) R.dst.upload(dst);
-    R.n = int64_t(dst.size());
     R.bits.upload(rb);
     R.off.upload(ro);
   }
@@ -1766,6 +1777,7 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
       whi[k][p].assign(hi_all.begin() + p * stride, hi_all.begin() + (p + 1) * stride);
     }
   }
+  const auto t_win = std::chrono::steady_clock::now();
   // per key: stats -> group_and_order -> solve_assignment, concurrently (solve.hpp:343-350)
   Cost cm;
   cm.n = P_;
@@ -1774,67 +1786,94 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
   std::vector<std::future<SolveResult>> jobs(keys_.size());
   std::vector<char> has(keys_.size(), 0);
   for (size_t k = 0; k < keys_.size(); ++k) {
-    std::vector<PairStat> pairs;
-    for (int64_t p = 0; p < P_; ++p) {
-      int64_t base = 0;
-      for (int64_t q = 0; q < P_; ++q) {
-        if (p == q) continue;
-        const PairMsgs& m = msgs_[k][p][q];
-        if (m.ids.empty()) continue;
-        PairStat ps;
-        ps.src = uint32_t(p);
-        ps.dst = uint32_t(q);
-        int64_t mb = 0;
-        for (int64_t qq = 0; qq < q; ++qq)
-          if (qq != p) mb += int64_t(msgs_[k][p][qq].ids.size());
-        (void)base;
-        for (size_t i = 0; i < m.ids.size(); ++i) {
-          const double lo = double(wlo[k][p][mb + i]), hi = double(whi[k][p][mb + i]);
-          if (!(hi >= lo)) continue;  // traced (trace.hpp:93)
-          MsgStat st;
-          st.id = m.ids[i];
-          st.dim = uint64_t(keys_[k].dim);
-          st.lo = lo;
-          st.hi = hi;
-          st.asq = keys_[k].bwd ? 1.0 : rx_asq_[p][q][i];
-          ps.msgs.push_back(st);
+    for (int64_t p = 0; p < P_ && !has[k]; ++p)
+      for (int64_t q = 0; q < P_; ++q)
+        if (p != q && !msgs_[k][p][q].ids.empty()) has[k] = 1;
+    if (!has[k]) continue;
+    // stats (engine.hpp:135-165) -> group_and_order -> solve_assignment, one thread per key
+    jobs[k] = std::async(std::launch::async, [&, k]() {
+      const auto a = std::chrono::steady_clock::now();
+      std::vector<PairStat> pairs;
+      for (int64_t p = 0; p < P_; ++p) {
+        int64_t mb = 0;  // first message of pair (p, q) in p's send order
+        for (int64_t q = 0; q < P_; ++q) {
+          if (p == q) continue;
+          const PairMsgs& m = msgs_[k][p][q];
+          PairStat ps;
+          ps.src = uint32_t(p);
+          ps.dst = uint32_t(q);
+          for (size_t i = 0; i < m.ids.size(); ++i) {
+            const double lo = double(wlo[k][p][mb + int64_t(i)]);
+            const double hi = double(whi[k][p][mb + int64_t(i)]);
+            if (!(hi >= lo)) continue;  // traced (trace.hpp:93)
+            MsgStat st;
+            st.id = m.ids[i];
+            st.dim = uint64_t(keys_[k].dim);
+            st.lo = lo;
+            st.hi = hi;
+            st.asq = keys_[k].bwd ? 1.0 : rx_asq_[p][q][i];
+            ps.msgs.push_back(st);
+          }
+          mb += int64_t(m.ids.size());
+          if (!ps.msgs.empty()) pairs.push_back(std::move(ps));
         }
-        if (!ps.msgs.empty()) pairs.push_back(std::move(ps));
       }
-    }
-    if (pairs.empty()) continue;
-    has[k] = 1;
-    jobs[k] = std::async(std::launch::async, [pairs = std::move(pairs), &cm, this]() {
+      if (pairs.empty()) return SolveResult{};
+      const auto b = std::chrono::steady_clock::now();
       SolveResult r = group_and_order(pairs, s_.group_size);
+      const auto c = std::chrono::steady_clock::now();
       solve_exact(r, cm, s_.lambda);
+      if (std::getenv("QGNN_RESOLVE_PROFILE")) {
+        const auto d = std::chrono::steady_clock::now();
+        size_t ng = 0;
+        for (const auto& pp : r.pairs) ng += pp.groups.size();
+        std::fprintf(stderr,
+                     "[resolve] key %zu: stats %.3f s, group %.3f s, solve %.3f s, %zu pairs %zu "
+                     "groups\n",
+                     k, std::chrono::duration<double>(b - a).count(),
+                     std::chrono::duration<double>(c - b).count(),
+                     std::chrono::duration<double>(d - c).count(), r.pairs.size(), ng);
+      }
       return r;
     });
   }
-  // adopt: new bits for every message (all-8 default for untraced / absent pairs)
+  const auto t_stats = std::chrono::steady_clock::now();
+  // adopt: new bits for every message (all-8 default for untraced / absent pairs),
+  // one host thread per key; then the wire layout and the device metadata
   ++plan_version_;
-  for (size_t k = 0; k < keys_.size(); ++k) {
-    for (int64_t p = 0; p < P_; ++p)
-      for (int64_t q = 0; q < P_; ++q)
-        if (p != q) std::fill(msgs_[k][p][q].bits.begin(), msgs_[k][p][q].bits.end(), uint8_t(8));
-    if (!has[k]) continue;
-    SolveResult r = jobs[k].get();
-    for (const PlanPairG& pp : r.pairs) {
-      PairMsgs& m = msgs_[k][pp.src][pp.dst];
-      for (const Group& g : pp.groups)
-        for (uint32_t id : g.ids) {
-          auto it = std::lower_bound(m.ids.begin(), m.ids.end(), id);
-          m.bits[it - m.ids.begin()] = uint8_t(g.bits);
-        }
-    }
-  }
-  bits_dirty_ = true;
+  std::vector<std::future<void>> adopt(keys_.size());
   for (size_t k = 0; k < keys_.size(); ++k)
-    for (int64_t p = 0; p < P_; ++p)
-      for (int64_t q = 0; q < P_; ++q)
-        if (p != q) layout_pair(int(k), int(p), int(q));
+    adopt[k] = std::async(std::launch::async, [&, k] {
+      for (int64_t p = 0; p < P_; ++p)
+        for (int64_t q = 0; q < P_; ++q)
+          if (p != q)
+            std::fill(msgs_[k][p][q].bits.begin(), msgs_[k][p][q].bits.end(), uint8_t(8));
+      if (has[k]) {
+        SolveResult r = jobs[k].get();
+        for (const PlanPairG& pp : r.pairs) {
+          PairMsgs& m = msgs_[k][pp.src][pp.dst];
+          for (const Group& g : pp.groups)
+            for (uint32_t id : g.ids) {
+              auto it = std::lower_bound(m.ids.begin(), m.ids.end(), id);
+              m.bits[it - m.ids.begin()] = uint8_t(g.bits);
+            }
+        }
+      }
+      for (int64_t p = 0; p < P_; ++p)
+        for (int64_t q = 0; q < P_; ++q)
+          if (p != q) layout_pair(int(k), int(p), int(q));
+    });
+  for (auto& f : adopt) f.get();
+  bits_dirty_ = true;
   arena_layout();
+  std::vector<std::future<void>> meta(keys_.size());
+  for (size_t k = 0; k < keys_.size(); ++k)
+    meta[k] = std::async(std::launch::async, [&, k] {
+      QGNN_CUDA(cudaSetDevice(s_.device));
+      upload_key_meta(int(k));
+    });
+  for (auto& f : meta) f.get();
   for (size_t k = 0; k < keys_.size(); ++k) {
-    upload_key_meta(int(k));
     for (auto& up : parts_dev_) {  // reset windows (engine.hpp:855-860)
       auto& S = up->snd[k];
       if (S.n)
@@ -1845,6 +1884,10 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
   QGNN_CUDA(cudaStreamSynchronize(s_main_));
   resolve_seconds_ =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (std::getenv("QGNN_RESOLVE_PROFILE"))
+    std::fprintf(stderr, "[resolve] windows %.3f s, stats %.3f s, total %.3f s\n",
+                 std::chrono::duration<double>(t_win - t0).count(),
+                 std::chrono::duration<double>(t_stats - t_win).count(), resolve_seconds_);
 }
 
 template <typename T>
