@@ -257,6 +257,11 @@ enum {
   QGNN_K_COUNT
 };
 int qgnn_engine_kernel_stats(qgnn_engine* e, double* out, int n);
+/* Switch per-kernel event timing on/off between epochs.  With it off (and one
+ * GPU, fixed/adaptive widths) the steady-state epoch runs as one captured CUDA
+ * graph, re-captured when the plan or a workspace changes; with it on every
+ * kernel is launched eagerly between timing events. */
+int qgnn_engine_set_kstats(qgnn_engine* e, int on);
 
 /* NCCL bootstrap for world > 1: rank 0 creates the id, every rank passes it to
  * qgnn_engine_create.  128 bytes. */

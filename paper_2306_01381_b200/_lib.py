@@ -133,6 +133,7 @@ _SIGS = {
     "qgnn_engine_set_weights": (C.c_int, [vp, C.c_int, vp]),
     "qgnn_engine_info": (C.c_int, [vp, vp]),
     "qgnn_engine_kernel_stats": (C.c_int, [vp, vp, C.c_int]),
+    "qgnn_engine_set_kstats": (C.c_int, [vp, C.c_int]),
     "qgnn_nccl_unique_id": (C.c_int, [vp]),
     "qgnn_loopback_id": (C.c_int, [u64, vp]),
     # host extras (not in the reference API; setup / statistics)

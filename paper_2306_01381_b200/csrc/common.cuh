@@ -73,6 +73,9 @@ void dequant_rows_add_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n_rows, cons
                           const int32_t* ptr, const int32_t* msg, int dim, const uint8_t* bits,
                           const uint64_t* offsets, float* out, int64_t ld, const float* mask,
                           int64_t ldm, cudaStream_t s);
+// Adam with the bias corrections in device memory (captured epoch graphs, dense.cu)
+void adam_step_devbc(int dtype, void* p, void* m, void* v, const void* g, int64_t n, double lr,
+                     double beta1, double beta2, double eps, const double* bc, cudaStream_t s);
 // fp32 loss phase for the engine: CE over train rows + val/test hit counts (dense.cu)
 void loss_f32(qgnn_ctx* ctx, const float* logits, int64_t ld, int classes, const int32_t* labels,
               const int32_t* rows, int64_t n_train, int64_t n_val, int64_t n_test,
@@ -133,6 +136,9 @@ void dequant_rows_add_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n_rows, cons
                           const int32_t* ptr, const int32_t* msg, int dim, const uint8_t* bits,
                           const uint64_t* offsets, float* out, int64_t ld, const float* mask,
                           int64_t ldm, cudaStream_t s);
+// Adam with the bias corrections in device memory (captured epoch graphs, dense.cu)
+void adam_step_devbc(int dtype, void* p, void* m, void* v, const void* g, int64_t n, double lr,
+                     double beta1, double beta2, double eps, const double* bc, cudaStream_t s);
 // fp32 loss phase for the engine: CE over train rows + val/test hit counts (dense.cu)
 void loss_f32(qgnn_ctx* ctx, const float* logits, int64_t ld, int classes, const int32_t* labels,
               const int32_t* rows, int64_t n_train, int64_t n_val, int64_t n_test,

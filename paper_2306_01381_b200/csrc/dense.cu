@@ -407,6 +407,34 @@ __global__ void k_adam(T* __restrict__ p, T* __restrict__ m, T* __restrict__ v,
   }
 }
 
+// Same step with the bias corrections read from device memory (bc[0], bc[1]), so a
+// captured epoch graph picks up each epoch's values (engine).
+template <typename T>
+__global__ void k_adam_devbc(T* __restrict__ p, T* __restrict__ m, T* __restrict__ v,
+                             const T* __restrict__ g, int64_t n, T lr, T b1, T b2, T eps,
+                             const double* __restrict__ bc) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const T bc1 = static_cast<T>(bc[0]), bc2 = static_cast<T>(bc[1]);
+  const T gi = g[i];
+  if constexpr (sizeof(T) == 8) {
+    const double mi = __dadd_rn(__dmul_rn(b1, m[i]), __dmul_rn(__dsub_rn(1.0, b1), gi));
+    const double vi =
+        __dadd_rn(__dmul_rn(b2, v[i]), __dmul_rn(__dmul_rn(__dsub_rn(1.0, b2), gi), gi));
+    m[i] = mi;
+    v[i] = vi;
+    const double mhat = __ddiv_rn(mi, bc1);
+    const double vhat = __ddiv_rn(vi, bc2);
+    p[i] = __dsub_rn(p[i], __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps)));
+  } else {
+    const T mi = b1 * m[i] + (T(1) - b1) * gi;
+    const T vi = b2 * v[i] + (T(1) - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    p[i] -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+  }
+}
+
 inline dim3 grid1(int64_t n, int t) { return dim3(static_cast<unsigned>(ceil_div(n, t))); }
 
 // TMA needs a 16-byte aligned base and row pitch
@@ -625,5 +653,19 @@ void input_grad_masked_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const flo
                                        out, ldo, s);
     if (st2) throw Status(st2, qgnn_last_error());
   }
+}
+
+void adam_step_devbc(int dtype, void* p, void* m, void* v, const void* g, int64_t n, double lr,
+                     double beta1, double beta2, double eps, const double* bc, cudaStream_t s) {
+  if (n == 0) return;
+  if (dtype == QGNN_F64)
+    k_adam_devbc<double><<<grid1(n, 256), 256, 0, s>>>(
+        static_cast<double*>(p), static_cast<double*>(m), static_cast<double*>(v),
+        static_cast<const double*>(g), n, lr, beta1, beta2, eps, bc);
+  else
+    k_adam_devbc<float><<<grid1(n, 256), 256, 0, s>>>(
+        static_cast<float*>(p), static_cast<float*>(m), static_cast<float*>(v),
+        static_cast<const float*>(g), n, float(lr), float(beta1), float(beta2), float(eps), bc);
+  check_launch("adam_step");
 }
 }  // namespace qgnn_b200

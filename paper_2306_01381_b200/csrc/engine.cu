@@ -218,6 +218,7 @@ class EngineBase {
   virtual void set_weights(int l, const void* in) = 0;
   virtual void info(int64_t* out) = 0;
   virtual int kernel_stats(double* out, int n) = 0;
+  virtual void set_kstats(bool on) = 0;
 };
 
 template <typename T>
@@ -232,8 +233,32 @@ class Engine final : public EngineBase {
     finish_epoch(m);
   }
   void launch_epoch() override;
+  void set_kstats(bool on) override {
+    QGNN_REQUIRE(!in_flight_, QGNN_EPROTOCOL, "set_kstats: an epoch is in flight");
+    s_.kstats = on ? 1 : 0;
+  }
   void finish_epoch(qgnn_epoch_metrics* m) override;
   bool in_flight_ = false;
+  // CUDA graph of the steady-state epoch (one GPU, no pending feature upload):
+  // captured once per plan version / arena and replayed with one launch
+  struct EpochGraph {
+    cudaGraphExec_t exec = nullptr;
+    uint64_t plan = ~uint64_t(0);
+    void* arena = nullptr;
+    void* scratch = nullptr;  // context workspaces baked into the graph
+    void* gemm_b = nullptr;
+    std::vector<std::tuple<int, size_t, double>> ev_used;
+    int64_t launches = 0;
+    double gbytes[QGNN_K_COUNT] = {};
+  } graph_;
+  bool graphs_enabled() const {
+    const char* e = std::getenv("QGNN_GRAPH");
+    // per-kernel event timing (kstats) cannot time events recorded inside a graph
+    return (!e || std::atoi(e) != 0) && s_.world == 1 && s_.bit_mode != kUniform && !s_.kstats;
+  }
+  void epoch_body();
+  DBuf<double> adam_bc_;  // [2] bias corrections of this epoch's step
+  double* adam_bc_host_ = nullptr;
   void set_features(const void* f) override;
   void get_weights(int l, void* out) override;
   void set_weights(int l, const void* in) override;
@@ -810,6 +835,8 @@ Engine<T>::~Engine() {
   if (s_main_) cudaStreamDestroy(s_main_);
   if (s_comm_) cudaStreamDestroy(s_comm_);
   if (s_copy_) cudaStreamDestroy(s_copy_);
+  if (graph_.exec) cudaGraphExecDestroy(graph_.exec);
+  if (adam_bc_host_) cudaFreeHost(adam_bc_host_);
   for (auto e : ev_feat_)
     if (e) cudaEventDestroy(e);
   if (ev_feat_free_) cudaEventDestroy(ev_feat_free_);
@@ -1626,12 +1653,9 @@ void Engine<T>::step() {
   allgather_dev(wgrad_all_.p, (P_ / s_.world) * nparams_, s_main_);
   k_sum_parts<T><<<unsigned(ceil_div(nparams_, 256)), 256, 0, s_main_>>>(wgrad_all_.p, int(P_),
                                                                          nparams_, wsum_.p);
-  ++adam_t_;
-  const double b1 = 0.9, b2 = 0.999;
-  const double bc1 = 1.0 - std::pow(b1, double(adam_t_));
-  const double bc2 = 1.0 - std::pow(b2, double(adam_t_));
-  QGNN_CALL(qgnn_adam_step(ctx_, dtype_, w_.p, adam_m_.p, adam_v_.p, wsum_.p, nparams_, s_.lr, b1,
-                           b2, 1e-8, bc1, bc2, s_main_));
+  // bias corrections of step adam_t_ were staged by launch_epoch (adam_bc_)
+  adam_step_devbc(dtype_, w_.p, adam_m_.p, adam_v_.p, wsum_.p, nparams_, s_.lr, 0.9, 0.999, 1e-8,
+                  adam_bc_.p, s_main_);
   kend(QGNN_K_ELEMWISE, double(nparams_) * sizeof(T) * (P_ + 6), s_main_, 2);
 }
 
@@ -1645,7 +1669,61 @@ void Engine<T>::launch_epoch() {
   QGNN_CUDA(cudaSetDevice(s_.device));
   launches_ = 0;
   prepare_epoch();
+  // Adam step t = epoch: bias corrections staged through pinned memory
+  ++adam_t_;
+  if (!adam_bc_host_) {
+    QGNN_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&adam_bc_host_), 2 * sizeof(double),
+                            cudaHostAllocDefault));
+    adam_bc_.alloc(2);
+  }
+  QGNN_CUDA(cudaStreamSynchronize(s_main_));  // the pinned slot is free (previous epoch done)
+  adam_bc_host_[0] = 1.0 - std::pow(0.9, double(adam_t_));
+  adam_bc_host_[1] = 1.0 - std::pow(0.999, double(adam_t_));
+  QGNN_CUDA(cudaMemcpyAsync(adam_bc_.p, adam_bc_host_, 2 * sizeof(double), cudaMemcpyHostToDevice,
+                            s_main_));
   QGNN_CUDA(cudaEventRecord(ev_a_, s_main_));
+  const bool graph = graphs_enabled() && !feat_pending_ && epoch_ > 1;
+  if (graph && graph_.exec && graph_.plan == plan_version_ && graph_.arena == arena_.p &&
+      graph_.scratch == ctx_->scratch && graph_.gemm_b == ctx_->gemm_b) {
+    QGNN_CUDA(cudaGraphLaunch(graph_.exec, s_main_));  // replay: restore the host-side records
+    ev_used_ = graph_.ev_used;
+    launches_ = graph_.launches;
+    if (s_.kstats)
+      for (int c = 0; c < QGNN_K_COUNT; ++c) kst_[c].gbytes += graph_.gbytes[c];
+  } else if (graph) {
+    if (graph_.exec) QGNN_CUDA(cudaGraphExecDestroy(graph_.exec));
+    graph_ = EpochGraph{};
+    double gb0[QGNN_K_COUNT];
+    for (int c = 0; c < QGNN_K_COUNT; ++c) gb0[c] = kst_[c].gbytes;
+    cudaGraph_t g = nullptr;
+    QGNN_CUDA(cudaStreamBeginCapture(s_main_, cudaStreamCaptureModeRelaxed));
+    try {
+      epoch_body();
+    } catch (...) {
+      cudaStreamEndCapture(s_main_, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    QGNN_CUDA(cudaStreamEndCapture(s_main_, &g));
+    QGNN_CUDA(cudaGraphInstantiate(&graph_.exec, g, 0));
+    QGNN_CUDA(cudaGraphDestroy(g));
+    graph_.plan = plan_version_;
+    graph_.arena = arena_.p;
+    graph_.scratch = ctx_->scratch;
+    graph_.gemm_b = ctx_->gemm_b;
+    graph_.ev_used = ev_used_;
+    graph_.launches = launches_;
+    for (int c = 0; c < QGNN_K_COUNT; ++c) graph_.gbytes[c] = kst_[c].gbytes - gb0[c];
+    QGNN_CUDA(cudaGraphLaunch(graph_.exec, s_main_));
+  } else {
+    epoch_body();
+  }
+  QGNN_CUDA(cudaEventRecord(ev_b_, s_main_));
+  in_flight_ = true;
+}
+
+template <typename T>
+void Engine<T>::epoch_body() {
   for (int64_t l = 1; l <= L_; ++l) {
     if (l == L_ && tf_last_)
       forward_last_tf(int(l));
@@ -1661,8 +1739,6 @@ void Engine<T>::launch_epoch() {
   }
   backward_last();
   step();
-  QGNN_CUDA(cudaEventRecord(ev_b_, s_main_));
-  in_flight_ = true;
 }
 
 template <typename T>
@@ -1985,6 +2061,13 @@ int qgnn_engine_run_epoch(qgnn_engine* e, qgnn_epoch_metrics* m) {
   QGNN_API_BEGIN
   QGNN_REQUIRE(e && m, QGNN_EINVAL, "null engine");
   e->impl->run_epoch(m);
+  QGNN_API_END
+}
+
+int qgnn_engine_set_kstats(qgnn_engine* e, int on) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(e, QGNN_EINVAL, "null engine");
+  e->impl->set_kstats(on != 0);
   QGNN_API_END
 }
 

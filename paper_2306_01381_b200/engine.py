@@ -142,6 +142,10 @@ class Engine:
         check(lib.qgnn_engine_run_epoch(self._h, C.byref(m)))
         return m.as_dict()
 
+    def set_kstats(self, on: bool) -> None:
+        """Per-kernel event timing on/off (off: the epoch replays as a CUDA graph)."""
+        check(lib.qgnn_engine_set_kstats(self._h, int(bool(on))))
+
     def launch_epoch(self) -> None:
         """Enqueue one epoch and return (pair with finish_epoch)."""
         check(lib.qgnn_engine_launch_epoch(self._h))

@@ -165,3 +165,25 @@ def test_overlapped_feature_staging_is_identical(cuda):
     b.close()
     assert seq == ovl
     assert (wa == wb).all()
+
+
+@pytest.mark.parametrize("mode", ["fixed", "adaptive"])
+def test_graph_replay_matches_eager(cuda, monkeypatch, mode):
+    """The captured steady-state epoch (CUDA graph, re-captured when the adaptive
+    plan changes) trains exactly like eager launches."""
+    def run():
+        eng = Engine(GRAPH, [8, 12, 3], n_parts=4, bit_mode=mode, fixed_bits=4, seed=11,
+                     period=3, dtype="f32")
+        out = [(m["train_loss"], m["plan_version"]) for m in (eng.run_epoch() for _ in range(8))]
+        w = np.concatenate([x.reshape(-1) for x in eng.weights()])
+        eng.close()
+        return out, w
+
+    monkeypatch.setenv("QGNN_GRAPH", "0")
+    eager, we = run()
+    monkeypatch.setenv("QGNN_GRAPH", "1")
+    graph, wg = run()
+    assert eager == graph
+    assert (we == wg).all()
+    if mode == "adaptive":
+        assert graph[-1][1] > 1  # the plan changed while replaying
