@@ -250,7 +250,8 @@ class Engine final : public EngineBase {
     std::vector<std::tuple<int, size_t, double>> ev_used;
     int64_t launches = 0;
     double gbytes[QGNN_K_COUNT] = {};
-  } graph_;
+  } graphs_[2];  // [0]: steady state, [1]: first layer consumes a pending feature upload
+  bool capturing_ = false;
   bool graphs_enabled() const {
     const char* e = std::getenv("QGNN_GRAPH");
     // per-kernel event timing (kstats) cannot time events recorded inside a graph
@@ -835,7 +836,8 @@ Engine<T>::~Engine() {
   if (s_main_) cudaStreamDestroy(s_main_);
   if (s_comm_) cudaStreamDestroy(s_comm_);
   if (s_copy_) cudaStreamDestroy(s_copy_);
-  if (graph_.exec) cudaGraphExecDestroy(graph_.exec);
+  for (auto& g : graphs_)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   if (adam_bc_host_) cudaFreeHost(adam_bc_host_);
   for (auto e : ev_feat_)
     if (e) cudaEventDestroy(e);
@@ -930,7 +932,9 @@ __global__ void k_gather_rows4(const float4* __restrict__ feats, int64_t f4,
 template <typename T>
 void Engine<T>::gather_features(PartDev& D) {
   const int64_t F = dims_[0], ld = ld_of(F), no = D.view.num_owned;
-  QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_feat_[part_chunk_[D.id - p0_]], 0));
+  // inside a captured epoch the chunk events are recorded outside the graph
+  QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_feat_[part_chunk_[D.id - p0_]],
+                                capturing_ ? cudaEventWaitExternal : 0));
   if (sizeof(T) == 4 && F % 4 == 0)
     k_gather_rows4<<<unsigned(std::min<int64_t>(ceil_div(no, 8), int64_t(ctx_->num_sms) * 16)), 256,
                      0, s_main_>>>(reinterpret_cast<const float4*>(feat_all_.p), F / 4,
@@ -1334,7 +1338,8 @@ void Engine<T>::forward_layer(int l) {
     for (auto& up : parts_dev_) {
       if (feats) gather_features(*up);
       if (feats && up.get() == parts_dev_.back().get())
-        QGNN_CUDA(cudaEventRecord(ev_feat_free_, s_main_));  // staging matrix consumed
+        QGNN_CUDA(cudaEventRecordWithFlags(ev_feat_free_, s_main_,  // staging matrix consumed
+                                           capturing_ ? cudaEventRecordExternal : 0));
       quantize(*up, k, up->h[t].p, ldi);  // fwd_send (engine.hpp:566-588)
       central(*up);
     }
@@ -1682,12 +1687,14 @@ void Engine<T>::launch_epoch() {
   QGNN_CUDA(cudaMemcpyAsync(adam_bc_.p, adam_bc_host_, 2 * sizeof(double), cudaMemcpyHostToDevice,
                             s_main_));
   QGNN_CUDA(cudaEventRecord(ev_a_, s_main_));
-  const bool graph = graphs_enabled() && !feat_pending_ && epoch_ > 1;
+  const bool graph = graphs_enabled() && epoch_ > 1;
+  EpochGraph& graph_ = graphs_[feat_pending_ ? 1 : 0];
   if (graph && graph_.exec && graph_.plan == plan_version_ && graph_.arena == arena_.p &&
       graph_.scratch == ctx_->scratch && graph_.gemm_b == ctx_->gemm_b) {
     QGNN_CUDA(cudaGraphLaunch(graph_.exec, s_main_));  // replay: restore the host-side records
     ev_used_ = graph_.ev_used;
     launches_ = graph_.launches;
+    feat_pending_ = false;
     if (s_.kstats)
       for (int c = 0; c < QGNN_K_COUNT; ++c) kst_[c].gbytes += graph_.gbytes[c];
   } else if (graph) {
@@ -1697,13 +1704,16 @@ void Engine<T>::launch_epoch() {
     for (int c = 0; c < QGNN_K_COUNT; ++c) gb0[c] = kst_[c].gbytes;
     cudaGraph_t g = nullptr;
     QGNN_CUDA(cudaStreamBeginCapture(s_main_, cudaStreamCaptureModeRelaxed));
+    capturing_ = true;
     try {
       epoch_body();
     } catch (...) {
+      capturing_ = false;
       cudaStreamEndCapture(s_main_, &g);
       if (g) cudaGraphDestroy(g);
       throw;
     }
+    capturing_ = false;
     QGNN_CUDA(cudaStreamEndCapture(s_main_, &g));
     QGNN_CUDA(cudaGraphInstantiate(&graph_.exec, g, 0));
     QGNN_CUDA(cudaGraphDestroy(g));
