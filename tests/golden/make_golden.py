@@ -93,6 +93,13 @@ def main():
     ep, fw = ref.engine_run(ds, [8, 12, 3], 4, bit_mode=3, epochs=12, seed=11, period=5,
                             group_size=4, theta=3e-9, gamma=5e-5)
     g["eng_ad_epochs"], g["eng_ad_weights"] = ep, fw
+    # GraphSAGE-mean aggregation (coeffs.hpp kSageMean) and a 3-layer GCN
+    ep, fw = ref.engine_run(ds, [8, 12, 3], 4, bit_mode=1, fixed_bits=8, epochs=5, seed=11,
+                            period=5, sage=True)
+    g["eng_sage_epochs"], g["eng_sage_weights"] = ep, fw
+    ep, fw = ref.engine_run(ds, [8, 16, 16, 3], 4, bit_mode=1, fixed_bits=4, epochs=5, seed=11,
+                            period=5)
+    g["eng_l3_epochs"], g["eng_l3_weights"] = ep, fw
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **g)
     print("wrote", os.path.join(HERE, "golden.npz"), len(g), "arrays")
 

@@ -187,3 +187,23 @@ def test_graph_replay_matches_eager(cuda, monkeypatch, mode):
     assert (we == wg).all()
     if mode == "adaptive":
         assert graph[-1][1] > 1  # the plan changed while replaying
+
+
+@pytest.mark.parametrize("name,dims,sage,fb", [("sage", [8, 12, 3], True, 8),
+                                               ("l3", [8, 16, 16, 3], False, 4)])
+def test_engine_sage_and_three_layers_match_reference(cuda, name, dims, sage, fb):
+    """GraphSAGE-mean aggregation and a 3-layer GCN: fp64 reproduces the reference
+    trainer to 1e-12; the production fp32 path (transform-first last layer,
+    fused ReLU backward, CUDA graph) stays within 1e-4."""
+    ref = G[f"eng_{name}_epochs"]
+    for dtype, tol in (("f64", 1e-12), ("f32", 1e-4)):
+        eng = Engine(GRAPH, dims, n_parts=4, bit_mode="fixed", fixed_bits=fb, seed=11, period=5,
+                     sage=sage, dtype=dtype)
+        got = [eng.run_epoch() for _ in range(len(ref))]
+        w = np.concatenate([x.reshape(-1) for x in eng.weights()])
+        eng.close()
+        for e, m in enumerate(got):
+            assert _rel(m["train_loss"], ref[e, 0]) < tol, (dtype, e, m["train_loss"], ref[e, 0])
+            assert m["ref_bytes_total"] == ref[e, 3]
+        if dtype == "f64":
+            assert np.allclose(w, G[f"eng_{name}_weights"], rtol=1e-10, atol=1e-12)
