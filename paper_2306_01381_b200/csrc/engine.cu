@@ -382,7 +382,23 @@ class Engine final : public EngineBase {
   void upload_key_meta(int k);
   void compute_bits_uniform();
   void prepare_epoch();
-  void quantize(PartDev& P, int k, const T* src, int64_t ld);
+  void quantize(PartDev& P, int k, const T* src, int64_t ld, cudaStream_t st = nullptr);
+  // one GPU: encode / decode on the side stream, overlapping the compute stream
+  bool side_overlap() const { return s_.world == 1 && side_enabled(); }
+  static bool side_enabled() {
+    const char* e = std::getenv("QGNN_SIDE_STREAM");
+    return !e || std::atoi(e) != 0;
+  }
+  void fork_side() {  // s_comm_ continues after everything queued on s_main_
+    QGNN_CUDA(cudaEventRecord(ev_fork_, s_main_));
+    QGNN_CUDA(cudaStreamWaitEvent(s_comm_, ev_fork_, 0));
+  }
+  void join_side() {  // s_main_ continues after everything queued on s_comm_
+    QGNN_CUDA(cudaEventRecord(ev_join_, s_comm_));
+    QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_join_, 0));
+  }
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  void decode_halo(int k, int64_t din, int64_t ldi, cudaStream_t st);
   void exchange(int k);
   void forward_layer(int l);
   void forward_last_tf(int l);
@@ -442,7 +458,7 @@ class Engine final : public EngineBase {
   uint64_t msg_offset_send(int k, int p, int q) const { return send_base_[k][p][q]; }
   void arena_layout();
   // profiling
-  void kbegin(int cls);
+  void kbegin(int cls, cudaStream_t st = nullptr);
   void kend(int cls, double bytes, cudaStream_t s, int nk = 1, double gbytes = 0);
   void flush_kstats();
 
@@ -513,7 +529,7 @@ class Engine final : public EngineBase {
 
 // ------------------------------------------------------------ profiling ---
 template <typename T>
-void Engine<T>::kbegin(int cls) {
+void Engine<T>::kbegin(int cls, cudaStream_t st) {
   if (!s_.kstats) return;
   if (ev_next_ == ev_pool_.size()) {
     cudaEvent_t a, b;
@@ -522,7 +538,7 @@ void Engine<T>::kbegin(int cls) {
     ev_pool_.emplace_back(a, b);
   }
   cur_cls_ = cls;
-  QGNN_CUDA(cudaEventRecord(ev_pool_[ev_next_].first, s_main_));
+  QGNN_CUDA(cudaEventRecord(ev_pool_[ev_next_].first, st ? st : s_main_));
 }
 
 template <typename T>
@@ -591,6 +607,8 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
   QGNN_CUDA(cudaEventCreateWithFlags(&ev_c_, cudaEventDisableTiming));
   QGNN_CUDA(cudaEventCreateWithFlags(&ev_d_, cudaEventDisableTiming));
   QGNN_CUDA(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking));
+  QGNN_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+  QGNN_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   QGNN_CUDA(cudaEventCreateWithFlags(&ev_feat_free_, cudaEventDisableTiming));
   if (s.world > 1) {
     QGNN_REQUIRE(nccl_id, QGNN_EINVAL, "engine: world > 1 needs an NCCL unique id");
@@ -842,6 +860,8 @@ Engine<T>::~Engine() {
   for (auto e : ev_feat_)
     if (e) cudaEventDestroy(e);
   if (ev_feat_free_) cudaEventDestroy(ev_feat_free_);
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
   if (ctx_) qgnn_ctx_destroy(ctx_);
 }
 
@@ -1180,21 +1200,40 @@ void Engine<T>::prepare_epoch() {
 
 // ------------------------------------------------------------ data path ---
 template <typename T>
-void Engine<T>::quantize(PartDev& D, int k, const T* src, int64_t ld) {
+void Engine<T>::quantize(PartDev& D, int k, const T* src, int64_t ld, cudaStream_t sq) {
   auto& S = D.snd[k];
   if (S.n == 0) return;
+  if (!sq) sq = s_main_;
   const int64_t dim = keys_[k].dim;
-  kbegin(QGNN_K_QUANT);
+  kbegin(QGNN_K_QUANT, sq);
   const int st = qgnn_quantize_pack(ctx_, src, dtype_, ld, dim, S.n, S.rows.p, S.ids.p, S.bits.p,
                                     S.off.p, S.set.p, S.keys.p, s_.layout, arena_.p, S.wlo.p,
-                                    S.whi.p, s_main_);
+                                    S.whi.p, sq);
   if (st) throw Status(st, qgnn_last_error());
   // algorithmic bytes: rows read once per message + packed chunks + metadata
   double bytes = 0;
   for (int64_t q = 0; q < P_; ++q)
     if (q != D.id) bytes += double(msgs_[k][D.id][q].bytes);
   bytes += double(S.n) * (double(dim) * sizeof(T) + 4 + 4 + 1 + 8 + 2 + 2 * sizeof(T));
-  kend(QGNN_K_QUANT, bytes, s_main_);
+  kend(QGNN_K_QUANT, bytes, sq);
+}
+
+// receive (engine.hpp:607-618): decode every source straight into the halo
+template <typename T>
+void Engine<T>::decode_halo(int k, int64_t din, int64_t ldi, cudaStream_t st) {
+  for (auto& up : parts_dev_) {
+    PartDev& D = *up;
+    auto& R = D.rcv[k];
+    if (!R.n) continue;
+    kbegin(QGNN_K_DEQUANT, st);
+    const int rc = qgnn_dequant_scatter(ctx_, arena_.p, R.n, din, R.bits.p, R.off.p, s_.layout,
+                                        R.dst.p, 0, D.halo.p, dtype_, ldi, st);
+    if (rc) throw Status(rc, qgnn_last_error());
+    double bytes = double(R.n) * (din * sizeof(T) + 4 + 1 + 8);
+    for (int64_t src = 0; src < P_; ++src)
+      if (src != D.id) bytes += double(msgs_[k][src][D.id].bytes);
+    kend(QGNN_K_DEQUANT, bytes, st);
+  }
 }
 
 // Grouped point-to-point exchange of the remote pairs on the comm stream.
@@ -1334,35 +1373,32 @@ void Engine<T>::forward_layer(int l) {
   // soon as its rows exist; otherwise every encode precedes the exchange, which
   // the central rows then overlap.
   const bool feats = t == 0 && feat_pending_;
-  if (feats || s_.world == 1) {
-    for (auto& up : parts_dev_) {
-      if (feats) gather_features(*up);
-      if (feats && up.get() == parts_dev_.back().get())
-        QGNN_CUDA(cudaEventRecordWithFlags(ev_feat_free_, s_main_,  // staging matrix consumed
-                                           capturing_ ? cudaEventRecordExternal : 0));
-      quantize(*up, k, up->h[t].p, ldi);  // fwd_send (engine.hpp:566-588)
-      central(*up);
-    }
-    feat_pending_ = false;
-    exchange(k);
-  } else {
-    for (auto& up : parts_dev_) quantize(*up, k, up->h[t].p, ldi);  // fwd_send
-    exchange(k);
+  if (side_overlap() && !feats) {
+    // one GPU: encode + decode on the side stream while the central rows run
+    fork_side();
+    for (auto& up : parts_dev_) quantize(*up, k, up->h[t].p, ldi, s_comm_);  // fwd_send
+    decode_halo(k, din, ldi, s_comm_);
     for (auto& up : parts_dev_) central(*up);
-  }
-  wait_exchange();
-  // receive (engine.hpp:607-618): decode every source straight into the halo
-  for (auto& up : parts_dev_) {
-    PartDev& D = *up;
-    auto& R = D.rcv[k];
-    if (!R.n) continue;
-    kbegin(QGNN_K_DEQUANT);
-    QGNN_CALL(qgnn_dequant_scatter(ctx_, arena_.p, R.n, din, R.bits.p, R.off.p, s_.layout,
-                                   R.dst.p, 0, D.halo.p, dtype_, ldi, s_main_));
-    double bytes = double(R.n) * (din * sizeof(T) + 4 + 1 + 8);
-    for (int64_t src = 0; src < P_; ++src)
-      if (src != D.id) bytes += double(msgs_[k][src][D.id].bytes);
-    kend(QGNN_K_DEQUANT, bytes, s_main_);
+    join_side();
+  } else {
+    if (feats || s_.world == 1) {
+      for (auto& up : parts_dev_) {
+        if (feats) gather_features(*up);
+        if (feats && up.get() == parts_dev_.back().get())
+          QGNN_CUDA(cudaEventRecordWithFlags(ev_feat_free_, s_main_,  // staging matrix consumed
+                                             capturing_ ? cudaEventRecordExternal : 0));
+        quantize(*up, k, up->h[t].p, ldi);  // fwd_send (engine.hpp:566-588)
+        central(*up);
+      }
+      feat_pending_ = false;
+      exchange(k);
+    } else {
+      for (auto& up : parts_dev_) quantize(*up, k, up->h[t].p, ldi);  // fwd_send
+      exchange(k);
+      for (auto& up : parts_dev_) central(*up);
+    }
+    wait_exchange();
+    decode_halo(k, din, ldi, s_main_);
   }
   // marginal rows (engine.hpp:622-623)
   for (auto& up : parts_dev_) {
@@ -1452,9 +1488,14 @@ void Engine<T>::backward_layer(int l) {
                                 double(D.view.remote_nnz()) * (4 + sizeof(T) + din * sizeof(T)),
            s_main_, nk, double(D.view.remote_nnz()) * din * sizeof(T));
     }
-    quantize(D, k, D.partials.p, ldi);
+    if (!side_overlap()) quantize(D, k, D.partials.p, ldi);
   }
-  exchange(k);
+  if (side_overlap()) {  // one GPU: encode on the side stream during bwd_finish
+    fork_side();
+    for (auto& up : parts_dev_) quantize(*up, k, up->partials.p, ldi, s_comm_);
+  } else {
+    exchange(k);
+  }
   // bwd_finish (engine.hpp:690-740)
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
@@ -1487,7 +1528,10 @@ void Engine<T>::backward_layer(int l) {
                               double(no) * din * sizeof(T), s_main_, nk,
          double(D.view.local_nnz() + no) * din * sizeof(T));
   }
-  wait_exchange();
+  if (side_overlap())
+    join_side();
+  else
+    wait_exchange();
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
     scatter_add_all(D, k, din, ldi, mk ? D.h[t].p : nullptr);
@@ -1506,8 +1550,15 @@ void Engine<T>::forward_last_tf(int l) {
   const int64_t din = dims_[t], dout = dims_[l];
   const int64_t ldi = ld_of(din), ldo = ld_of(dout);
   const T* W = w_.p + woff_[t];
-  for (auto& up : parts_dev_) quantize(*up, k, up->h[t].p, ldi);
-  exchange(k);
+  const bool side = side_overlap();
+  if (side) {  // one GPU: encode + decode on the side stream during the owned-row work
+    fork_side();
+    for (auto& up : parts_dev_) quantize(*up, k, up->h[t].p, ldi, s_comm_);
+    decode_halo(k, din, ldi, s_comm_);
+  } else {
+    for (auto& up : parts_dev_) quantize(*up, k, up->h[t].p, ldi);
+    exchange(k);
+  }
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
     const int64_t no = D.view.num_owned, nc = D.view.n_central;
@@ -1524,18 +1575,11 @@ void Engine<T>::forward_last_tf(int l) {
                               double(no) * dout * sizeof(T), s_main_, nk,
          double(D.view.local_ptr[nc] + nc) * dout * sizeof(T));
   }
-  wait_exchange();
-  for (auto& up : parts_dev_) {
-    PartDev& D = *up;
-    auto& R = D.rcv[k];
-    if (!R.n) continue;
-    kbegin(QGNN_K_DEQUANT);
-    QGNN_CALL(qgnn_dequant_scatter(ctx_, arena_.p, R.n, din, R.bits.p, R.off.p, s_.layout,
-                                   R.dst.p, 0, D.halo.p, dtype_, ldi, s_main_));
-    double bytes = double(R.n) * (din * sizeof(T) + 4 + 1 + 8);
-    for (int64_t src = 0; src < P_; ++src)
-      if (src != D.id) bytes += double(msgs_[k][src][D.id].bytes);
-    kend(QGNN_K_DEQUANT, bytes, s_main_);
+  if (side) {
+    join_side();
+  } else {
+    wait_exchange();
+    decode_halo(k, din, ldi, s_main_);
   }
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
@@ -1585,9 +1629,14 @@ void Engine<T>::backward_last_tf(int l) {
                                       D.partials.p, ldi, s_main_));
       kend(QGNN_K_GEMM_DGRAD, double(nr) * (din + dout) * sizeof(T), s_main_, gemm_nk());
     }
-    quantize(D, k, D.partials.p, ldi);
+    if (!side_overlap()) quantize(D, k, D.partials.p, ldi);
   }
-  exchange(k);
+  if (side_overlap()) {  // one GPU: encode on the side stream during bwd_finish
+    fork_side();
+    for (auto& up : parts_dev_) quantize(*up, k, up->partials.p, ldi, s_comm_);
+  } else {
+    exchange(k);
+  }
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
     const int64_t no = D.view.num_owned, nr = D.view.num_remote;
@@ -1616,7 +1665,10 @@ void Engine<T>::backward_last_tf(int l) {
     kend(QGNN_K_GEMM_WGRAD, double(no + nr) * (din + dout) * sizeof(T), s_main_,
          (dtype_ == QGNN_F64 ? 1 : 2) * (nr ? 2 : 1));
   }
-  wait_exchange();
+  if (side_overlap())
+    join_side();
+  else
+    wait_exchange();
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
     scatter_add_all(D, k, din, ldi, mk ? D.h[t].p : nullptr);
