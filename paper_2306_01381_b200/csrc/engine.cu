@@ -384,7 +384,8 @@ class Engine final : public EngineBase {
   void prepare_epoch();
   void quantize(PartDev& P, int k, const T* src, int64_t ld, cudaStream_t st = nullptr);
   // one GPU: encode / decode on the side stream, overlapping the compute stream
-  bool side_overlap() const { return s_.world == 1 && side_enabled(); }
+  // (per-kernel timing runs serialised so each class's time is its own)
+  bool side_overlap() const { return s_.world == 1 && side_enabled() && !s_.kstats; }
   static bool side_enabled() {
     const char* e = std::getenv("QGNN_SIDE_STREAM");
     return !e || std::atoi(e) != 0;

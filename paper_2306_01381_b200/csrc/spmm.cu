@@ -352,6 +352,100 @@ __global__ void __launch_bounds__(256, 4) k_spmm_f32g(
   }
 }
 
+// Narrow rows, two float4 per lane: G = ceil(F/2) lanes per row, E = 32/G
+// lane groups, 4 steps per round (8 loads per lane in flight).  Per step a
+// warp issues the same index shuffles and address math as k_spmm_f32g but moves
+// twice the bytes per lane, so per gathered byte it issues ~half the
+// instructions (the 100- and 48-wide layers are issue-bound in k_spmm_f32g).
+__device__ __forceinline__ void grp2_gather(float4 (&acc)[2], const float* __restrict__ src,
+                                            int ld, int64_t beg, int64_t end,
+                                            const int32_t* __restrict__ col,
+                                            const float* __restrict__ alpha, int lane, int grp,
+                                            int E, bool act, bool has2) {
+  for (int64_t e0 = beg; e0 < end; e0 += 32) {
+    const int cnt = end - e0 < 32 ? static_cast<int>(end - e0) : 32;
+    int my_c = 0;
+    float my_a = 0.f;
+    if (lane < cnt) {
+      my_c = __ldg(col + e0 + lane);
+      my_a = __ldg(alpha + e0 + lane);
+    }
+    for (int j = 0; j < cnt; j += 4 * E) {
+      float4 v[4][2];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = j + u * E + grp;
+        const int c = __shfl_sync(0xffffffffu, my_c, k & 31);
+        const bool ok = act && k < cnt;
+        const float4* p = reinterpret_cast<const float4*>(src + int64_t(c) * ld);
+        v[u][0] = ok ? __ldg(p) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[u][1] = (ok && has2) ? __ldg(p + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float a = __shfl_sync(0xffffffffu, my_a, (j + u * E + grp) & 31);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          acc[h].x = fmaf(a, v[u][h].x, acc[h].x);
+          acc[h].y = fmaf(a, v[u][h].y, acc[h].y);
+          acc[h].z = fmaf(a, v[u][h].z, acc[h].z);
+          acc[h].w = fmaf(a, v[u][h].w, acc[h].w);
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 4) k_spmm_f32g2(
+    int dim, const float* __restrict__ x, int64_t ldx, const float* __restrict__ y, int64_t ldy,
+    const float* __restrict__ self_alpha, const int64_t* __restrict__ pa,
+    const int32_t* __restrict__ ca, const float* __restrict__ aa, const int64_t* __restrict__ pb,
+    const int32_t* __restrict__ cb, const float* __restrict__ ab, int64_t r0, int64_t n_rows,
+    float* __restrict__ out, int64_t ldo, int64_t hub_deg, const float* __restrict__ mask,
+    int64_t ldm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int F = dim >> 2, G = (F + 1) >> 1, E = 32 / G;
+  const int grp = lane / G, sub = lane - grp * G;
+  const bool act = grp < E;
+  const bool has2 = 2 * sub + 1 < F;
+  const int64_t r = r0 + int64_t(blockIdx.x) * 8 + warp;
+  if (r >= r0 + n_rows) return;
+  const int64_t ea0 = pa[r], ea1 = pa[r + 1];
+  const int64_t eb0 = pb ? pb[r] : 0, eb1 = pb ? pb[r + 1] : 0;
+  if ((ea1 - ea0) + (eb1 - eb0) > hub_deg) return;  // k_spmm_hubseg + k_spmm_hubred
+  float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+  const int cx = sub * 8;  // first float of this lane's two columns
+  grp2_gather(acc, x + cx, int(ldx), ea0, ea1, ca, aa, lane, grp, E, act, has2);
+  if (pb) grp2_gather(acc, y + cx, int(ldy), eb0, eb1, cb, ab, lane, grp, E, act, has2);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const float4 mine = acc[h];  // group g's partial -> group 0, g ascending
+    for (int g = 1; g < E; ++g) {
+      const int sl = (lane + g * G) & 31;
+      acc[h].x += __shfl_sync(0xffffffffu, mine.x, sl);
+      acc[h].y += __shfl_sync(0xffffffffu, mine.y, sl);
+      acc[h].z += __shfl_sync(0xffffffffu, mine.z, sl);
+      acc[h].w += __shfl_sync(0xffffffffu, mine.w, sl);
+    }
+  }
+  if (grp == 0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && !has2) break;
+      const int c = cx + 4 * h;
+      float4 o = acc[h];
+      if (self_alpha) {
+        const float sa = self_alpha[r];
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(x + r * ldx + c));
+        o = make_float4(fmaf(sa, xv.x, o.x), fmaf(sa, xv.y, o.y), fmaf(sa, xv.z, o.z),
+                        fmaf(sa, xv.w, o.w));
+      }
+      if (mask) o = relu_mask4(o, mask + r * ldm + c);
+      *reinterpret_cast<float4*>(out + r * ldo + c) = o;
+    }
+  }
+}
+
 // One CTA per hub row: 8 warps take contiguous eighths of the edge lists,
 // partial sums meet in shared memory and are added in warp order (deterministic).
 template <int NV>
@@ -451,6 +545,11 @@ static int split_wide() {
   return e ? std::atoi(e) : 0;
 }
 
+static bool two_per_lane() {  // QGNN_SPMM_G2=0: one float4 per lane (k_spmm_f32g)
+  const char* e = std::getenv("QGNN_SPMM_G2");
+  return !e || std::atoi(e) != 0;
+}
+
 static bool grouped_narrow() {  // QGNN_SPMM_GROUPED=0 selects the one-row-per-warp kernel
   const char* e = std::getenv("QGNN_SPMM_GROUPED");
   return !e || std::atoi(e) != 0;
@@ -482,9 +581,13 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
   const int parts = nv == 1 ? 1 : (nv == 2 && dim % 8 == 0 && sw) ? (sw == 2 ? -2 : 2) : 0;
   if (parts && grouped_narrow()) {
     const int np = parts < 0 ? -parts : parts;
-    k_spmm_f32g<<<unsigned(blocks * np), 256, 0, s>>>(dim / np, x, ldx, y, ldy, sa, pa, ca, aa, pb,
-                                                      cb, ab, row_begin, n_rows, out, ldo, hd, mask,
-                                                      ldm, parts);
+    if (parts == 1 && dim / 4 >= 5 && two_per_lane())
+      k_spmm_f32g2<<<unsigned(blocks), 256, 0, s>>>(dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab,
+                                                    row_begin, n_rows, out, ldo, hd, mask, ldm);
+    else
+      k_spmm_f32g<<<unsigned(blocks * np), 256, 0, s>>>(dim / np, x, ldx, y, ldy, sa, pa, ca, aa,
+                                                        pb, cb, ab, row_begin, n_rows, out, ldo, hd,
+                                                        mask, ldm, parts);
     if (hubs) {
       if (nv == 1)
         k_spmm_hubseg<1><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(
