@@ -54,6 +54,21 @@ __device__ __forceinline__ void vstore(T* p, const T (&v)[VEC]) {
   }
 }
 
+// acc += a * v on float4 as two packed fp32x2 FMAs (FFMA2: same rounding as four
+// FFMAs, half the issue slots — the narrow-row gathers are issue-bound)
+__device__ __forceinline__ void fma4(float4& acc, float a, const float4& v) {
+  unsigned long long c0, c1, v0, v1, aa;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(c0) : "f"(acc.x), "f"(acc.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(c1) : "f"(acc.z), "f"(acc.w));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(v0) : "f"(v.x), "f"(v.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(v1) : "f"(v.z), "f"(v.w));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c0) : "l"(aa), "l"(v0));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c1) : "l"(aa), "l"(v1));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(acc.x), "=f"(acc.y) : "l"(c0));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(acc.z), "=f"(acc.w) : "l"(c1));
+}
+
 template <typename T, int VEC, int NV>
 __device__ __forceinline__ void gather_edges(T (&acc)[NV][VEC], const T* __restrict__ src,
                                              int64_t ld, const int64_t beg, const int64_t end,
@@ -87,9 +102,16 @@ __device__ __forceinline__ void gather_edges(T (&acc)[NV][VEC], const T* __restr
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int i = 0; i < NV; ++i)
+        for (int i = 0; i < NV; ++i) {
+          if constexpr (sizeof(T) == 4 && VEC == 4) {
+            float4 ac = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+            fma4(ac, a[u], make_float4(v[u][i][0], v[u][i][1], v[u][i][2], v[u][i][3]));
+            acc[i][0] = ac.x, acc[i][1] = ac.y, acc[i][2] = ac.z, acc[i][3] = ac.w;
+          } else {
 #pragma unroll
-          for (int k = 0; k < VEC; ++k) acc[i][k] = Arith<T>::madd(a[u], v[u][i][k], acc[i][k]);
+            for (int k = 0; k < VEC; ++k) acc[i][k] = Arith<T>::madd(a[u], v[u][i][k], acc[i][k]);
+          }
+        }
     }
     for (; j < cnt; ++j) {
       const int c = __shfl_sync(0xffffffffu, my_c, j);
@@ -294,10 +316,7 @@ __device__ __forceinline__ void grp_gather(float4& acc, const float* __restrict_
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const float a = __shfl_sync(0xffffffffu, my_a, (j + u * E + grp) & 31);
-        acc.x = fmaf(a, v[u].x, acc.x);
-        acc.y = fmaf(a, v[u].y, acc.y);
-        acc.z = fmaf(a, v[u].z, acc.z);
-        acc.w = fmaf(a, v[u].w, acc.w);
+        fma4(acc, a, v[u]);
       }
     }
   }
@@ -385,12 +404,7 @@ __device__ __forceinline__ void grp2_gather(float4 (&acc)[2], const float* __res
       for (int u = 0; u < 4; ++u) {
         const float a = __shfl_sync(0xffffffffu, my_a, (j + u * E + grp) & 31);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          acc[h].x = fmaf(a, v[u][h].x, acc[h].x);
-          acc[h].y = fmaf(a, v[u][h].y, acc[h].y);
-          acc[h].z = fmaf(a, v[u][h].z, acc[h].z);
-          acc[h].w = fmaf(a, v[u][h].w, acc[h].w);
-        }
+        for (int h = 0; h < 2; ++h) fma4(acc[h], a, v[u][h]);
       }
     }
   }
