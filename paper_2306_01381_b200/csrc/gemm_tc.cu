@@ -13,8 +13,9 @@
 //   warp 2      TMEM allocator (2 x BN fp32 accumulator columns, double buffer)
 //   warps 4-7   epilogue: tcgen05.ld 32x32b -> ReLU -> global stores, while the
 //               MMA warp already accumulates the next tile in the other buffer
-//   warps 8-11  converters: split the landed fp32 tile into hi (in place) and
-//               lo (second buffer), fence.proxy.async, release the stage
+//   warps 8-11  converters: lo = x - tf32(x) of the landed fp32 tile into a
+//               second buffer (the MMA reads the tile itself as hi: kind::tf32
+//               ignores the low 13 mantissa bits), fence.proxy.async, release
 // Shapes: forward z = A W (A rows x din, K-major), input gradient dz W^T
 // (K-major, SWIZZLE_128B), weight gradient A^T B over rows (both operands
 // MN-major; 32-bit MN-major operands require the 128B swizzle with 32-byte
@@ -125,13 +126,16 @@ __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
-// in-place hi + separate lo for `n16` 16-byte vectors, strided over `nthr` threads
-__device__ __forceinline__ void split_tile(float4* buf, float4* lo, int n16, int t, int nthr) {
+// lo = x - tf32(x) for `n16` 16-byte vectors, strided over `nthr` threads.  The hi
+// part needs no copy: kind::tf32 reads only the top 19 bits of each 32-bit
+// operand (verified bit-identical against an explicit truncated copy,
+// profiles/chk_tc_trunc.py), so the landed fp32 tile is used as hi in place.
+__device__ __forceinline__ void split_tile(const float4* buf, float4* lo, int n16, int t,
+                                           int nthr) {
   for (int i = t; i < n16; i += nthr) {
-    float4 v = buf[i];
-    float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-    buf[i] = h;
-    lo[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+    const float4 v = buf[i];
+    lo[i] = make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z),
+                        v.w - tf32_hi(v.w));
   }
 }
 
