@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(256, (NV <= 2 ? 3 : 1)) k_spmm_f32(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nvec = dim >> 2;
   {
-    const int64_t r = r0 + int64_t(blockIdx.x) * 8 + warp;
+    const int64_t r = r0 + int64_t(blockIdx.x) * (blockDim.x >> 5) + warp;
     if (r >= r0 + n_rows) return;
     const int64_t ea0 = pa[r], ea1 = pa[r + 1];
     const int64_t eb0 = pb ? pb[r] : 0, eb1 = pb ? pb[r + 1] : 0;
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(256, 4) k_spmm_f32g2(
   const int grp = lane / G, sub = lane - grp * G;
   const bool act = grp < E;
   const bool has2 = 2 * sub + 1 < F;
-  const int64_t r = r0 + int64_t(blockIdx.x) * 8 + warp;
+  const int64_t r = r0 + int64_t(blockIdx.x) * (blockDim.x >> 5) + warp;
   if (r >= r0 + n_rows) return;
   const int64_t ea0 = pa[r], ea1 = pa[r + 1];
   const int64_t eb0 = pb ? pb[r] : 0, eb1 = pb ? pb[r + 1] : 0;
@@ -564,6 +564,12 @@ static bool two_per_lane() {  // QGNN_SPMM_G2=0: one float4 per lane (k_spmm_f32
   return !e || std::atoi(e) != 0;
 }
 
+static int spmm_tpb() {  // threads per block of the full-row kernel (QGNN_SPMM_TPB)
+  const char* e = std::getenv("QGNN_SPMM_TPB");
+  return e ? std::max(32, std::min(256, std::atoi(e))) : 64;  // small blocks: a straggler row
+                                                                  // holds 1 warp slot, not 8
+}
+
 static bool grouped_narrow() {  // QGNN_SPMM_GROUPED=0 selects the one-row-per-warp kernel
   const char* e = std::getenv("QGNN_SPMM_GROUPED");
   return !e || std::atoi(e) != 0;
@@ -582,7 +588,8 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
   const int64_t hd = hubs ? hp->hub_deg : (int64_t(1) << 62);
 #define QGNN_SPMM_CASE(NVV)                                                                    \
   case NVV:                                                                                    \
-    k_spmm_f32<NVV><<<unsigned(blocks), 256, 0, s>>>(dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, \
+    k_spmm_f32<NVV><<<unsigned(ceil_div(n_rows, spmm_tpb() / 32)), spmm_tpb(), 0, s>>>(         \
+                                                     dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, \
                                                      ab, row_begin, n_rows, out, ldo, hd, mask, ldm); \
     if (hubs) {                                                                                \
       k_spmm_hubseg<NVV><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(             \
@@ -596,8 +603,9 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
   if (parts && grouped_narrow()) {
     const int np = parts < 0 ? -parts : parts;
     if (parts == 1 && dim / 4 >= 5 && two_per_lane())
-      k_spmm_f32g2<<<unsigned(blocks), 256, 0, s>>>(dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab,
-                                                    row_begin, n_rows, out, ldo, hd, mask, ldm);
+      k_spmm_f32g2<<<unsigned(ceil_div(n_rows, spmm_tpb() / 32)), spmm_tpb(), 0, s>>>(
+          dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask,
+          ldm);
     else
       k_spmm_f32g<<<unsigned(blocks * np), 256, 0, s>>>(dim / np, x, ldx, y, ldy, sa, pa, ca, aa,
                                                         pb, cb, ab, row_begin, n_rows, out, ldo, hd,
