@@ -879,7 +879,7 @@ void dequant_rows_add_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n_rows, cons
                           int64_t ldm, cudaStream_t s) {
   if (n_rows == 0) return;
   QGNN_REQUIRE(dim <= 512, QGNN_EINVAL, "dequant_rows_add: dim must be <= 512");
-  k_dequant_rows_f32<<<unsigned(ceil_div(n_rows * 32, 256)), 256, 0, s>>>(
+  k_dequant_rows_f32<<<unsigned(ceil_div(n_rows * 32, 64)), 64, 0, s>>>(
       in, n_rows, rows, ptr, msg, dim, bits, offsets, out, ld, mask, ldm, ctx->d_err);
   check_launch("k_dequant_rows_f32");
 }

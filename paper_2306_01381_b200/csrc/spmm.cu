@@ -594,7 +594,7 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
     if (hubs) {                                                                                \
       k_spmm_hubseg<NVV><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(             \
           dim, x, ldx, y, ldy, ca, aa, cb, ab, hp->seg, hp->n_segs, hp->part, hp->ldp);        \
-      k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 256)), 256, 0, s>>>(                  \
+      k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 64)), 64, 0, s>>>(                  \
           dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask, ldm); \
     }                                                                                          \
     break;
@@ -617,7 +617,7 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
       else
         k_spmm_hubseg<2><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(
             dim, x, ldx, y, ldy, ca, aa, cb, ab, hp->seg, hp->n_segs, hp->part, hp->ldp);
-      k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 256)), 256, 0, s>>>(
+      k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 64)), 64, 0, s>>>(
           dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask,
           ldm);
     }
