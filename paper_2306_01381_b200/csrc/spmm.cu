@@ -377,12 +377,11 @@ __global__ void __launch_bounds__(256, 4) k_spmm_f32g(
 // twice the bytes per lane, so per gathered byte it issues ~half the
 // instructions (the 100- and 48-wide layers are issue-bound in k_spmm_f32g).
 __device__ __forceinline__ void grp2_gather(float4 (&acc)[2], const float* __restrict__ src,
-                                            int ld, int64_t beg, int64_t end,
-                                            const int32_t* __restrict__ col,
+                                            int ld, int n, const int32_t* __restrict__ col,
                                             const float* __restrict__ alpha, int lane, int grp,
                                             int E, bool act, bool has2) {
-  for (int64_t e0 = beg; e0 < end; e0 += 32) {
-    const int cnt = end - e0 < 32 ? static_cast<int>(end - e0) : 32;
+  for (int e0 = 0; e0 < n; e0 += 32) {
+    const int cnt = min(32, n - e0);
     int my_c = 0;
     float my_a = 0.f;
     if (lane < cnt) {
@@ -410,27 +409,41 @@ __device__ __forceinline__ void grp2_gather(float4 (&acc)[2], const float* __res
   }
 }
 
-__global__ void __launch_bounds__(256, 4) k_spmm_f32g2(
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_spmm_f32g2(
     int dim, const float* __restrict__ x, int64_t ldx, const float* __restrict__ y, int64_t ldy,
     const float* __restrict__ self_alpha, const int64_t* __restrict__ pa,
     const int32_t* __restrict__ ca, const float* __restrict__ aa, const int64_t* __restrict__ pb,
     const int32_t* __restrict__ cb, const float* __restrict__ ab, int64_t r0, int64_t n_rows,
     float* __restrict__ out, int64_t ldo, int64_t hub_deg, const float* __restrict__ mask,
-    int64_t ldm) {
+    int64_t ldm, const int64_t* __restrict__ seg, int64_t n_segs, float* __restrict__ part,
+    int64_t ldp) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int F = dim >> 2, G = (F + 1) >> 1, E = 32 / G;
   const int grp = lane / G, sub = lane - grp * G;
   const bool act = grp < E;
   const bool has2 = 2 * sub + 1 < F;
-  const int64_t r = r0 + int64_t(blockIdx.x) * (blockDim.x >> 5) + warp;
+  // warps [0, n_segs): hub segments into `part` (as k_spmm_wide); then the rows
+  const int64_t w = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp;
+  const bool is_seg = w < n_segs;
+  const int64_t r = is_seg ? -1 : r0 + (w - n_segs);
   if (r >= r0 + n_rows) return;
-  const int64_t ea0 = pa[r], ea1 = pa[r + 1];
-  const int64_t eb0 = pb ? pb[r] : 0, eb1 = pb ? pb[r + 1] : 0;
-  if ((ea1 - ea0) + (eb1 - eb0) > hub_deg) return;  // k_spmm_hubseg + k_spmm_hubred
+  int64_t ea0;  // edge ranges rebased to pointers + 32-bit counts
+  int na, nb;
+  if (is_seg) {
+    const int64_t* sg = seg + 4 * w;
+    ea0 = sg[0], na = int(sg[1] - ea0), nb = int(sg[3] - sg[2]);
+  } else {
+    ea0 = pa[r], na = int(pa[r + 1] - ea0), nb = pb ? int(pb[r + 1] - pb[r]) : 0;
+    if (na + nb > hub_deg) return;  // segments + k_spmm_hubred
+  }
   float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
   const int cx = sub * 8;  // first float of this lane's two columns
-  grp2_gather(acc, x + cx, int(ldx), ea0, ea1, ca, aa, lane, grp, E, act, has2);
-  if (pb) grp2_gather(acc, y + cx, int(ldy), eb0, eb1, cb, ab, lane, grp, E, act, has2);
+  grp2_gather(acc, x + cx, int(ldx), na, ca + ea0, aa + ea0, lane, grp, E, act, has2);
+  if (nb) {  // b range start re-read here rather than held across the first gather
+    const int64_t eb0 = is_seg ? seg[4 * w + 2] : pb[r];
+    grp2_gather(acc, y + cx, int(ldy), nb, cb + eb0, ab + eb0, lane, grp, E, act, has2);
+  }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const float4 mine = acc[h];  // group g's partial -> group 0, g ascending
@@ -448,6 +461,10 @@ __global__ void __launch_bounds__(256, 4) k_spmm_f32g2(
       if (h == 1 && !has2) break;
       const int c = cx + 4 * h;
       float4 o = acc[h];
+      if (is_seg) {
+        *reinterpret_cast<float4*>(part + w * ldp + c) = o;
+        continue;
+      }
       if (self_alpha) {
         const float sa = self_alpha[r];
         const float4 xv = __ldg(reinterpret_cast<const float4*>(x + r * ldx + c));
@@ -457,6 +474,94 @@ __global__ void __launch_bounds__(256, 4) k_spmm_f32g2(
       if (mask) o = relu_mask4(o, mask + r * ldm + c);
       *reinterpret_cast<float4*>(out + r * ldo + c) = o;
     }
+  }
+}
+
+// 256-wide rows (two float4 per lane, every lane active), register-lean: 32-bit
+// edge offsets within the row (pointers rebased once per row), no per-lane column
+// bounds, alphas shuffled after the loads — to fit 64 registers (32 warps/SM)
+// with the same 8 gathers per lane in flight as k_spmm_f32<2>.
+__device__ __forceinline__ void wide_gather(float4 (&acc)[2], const float* __restrict__ src,
+                                            int ld, int n, const int32_t* __restrict__ col,
+                                            const float* __restrict__ alpha, int lane) {
+  for (int e0 = 0; e0 < n; e0 += 32) {
+    const int cnt = min(32, n - e0);
+    int my_c = 0;
+    float my_a = 0.f;
+    if (lane < cnt) {
+      my_c = __ldg(col + e0 + lane);
+      my_a = __ldg(alpha + e0 + lane);
+    }
+    for (int j = 0; j < cnt; j += 4) {
+      float4 v[4][2];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = __shfl_sync(0xffffffffu, my_c, (j + u) & 31);
+        const float4* p = reinterpret_cast<const float4*>(src + int64_t(c) * ld) + lane;
+        const bool ok = j + u < cnt;
+        v[u][0] = ok ? __ldg(p) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[u][1] = ok ? __ldg(p + 32) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float a = __shfl_sync(0xffffffffu, my_a, (j + u) & 31);
+        fma4(acc[0], a, v[u][0]);
+        fma4(acc[1], a, v[u][1]);
+      }
+    }
+  }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(64, MINB) k_spmm_wide(
+    const float* __restrict__ x, int64_t ldx, const float* __restrict__ y, int64_t ldy,
+    const float* __restrict__ self_alpha, const int64_t* __restrict__ pa,
+    const int32_t* __restrict__ ca, const float* __restrict__ aa, const int64_t* __restrict__ pb,
+    const int32_t* __restrict__ cb, const float* __restrict__ ab, int64_t r0, int64_t n_rows,
+    float* __restrict__ out, int64_t ldo, int64_t hub_deg, const float* __restrict__ mask,
+    int64_t ldm, const int64_t* __restrict__ seg, int64_t n_segs, float* __restrict__ part,
+    int64_t ldp) {
+  // warps [0, n_segs) reduce hub segments into `part` (k_spmm_hubred finishes those
+  // rows); they take the lowest block ids so the long lists start first and overlap
+  // the ordinary rows instead of running as a separate tail launch
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t w = int64_t(blockIdx.x) * (blockDim.x >> 5) + warp;
+  const bool is_seg = w < n_segs;
+  const int64_t r = r0 + (w - n_segs);
+  if (!is_seg && r >= r0 + n_rows) return;
+  int64_t ea;
+  int na, nb;
+  if (is_seg) {
+    const int64_t* sg = seg + 4 * w;  // [a0, a1, b0, b1]
+    ea = sg[0], na = int(sg[1] - ea), nb = int(sg[3] - sg[2]);
+  } else {
+    ea = pa[r], na = int(pa[r + 1] - ea), nb = pb ? int(pb[r + 1] - pb[r]) : 0;
+    if (na + nb > hub_deg) return;  // segments + k_spmm_hubred
+  }
+  float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+  wide_gather(acc, x, int(ldx), na, ca + ea, aa + ea, lane);
+  if (nb) {  // b range start re-read here rather than held across the first gather
+    const int64_t eb = is_seg ? seg[4 * w + 2] : pb[r];
+    wide_gather(acc, y, int(ldy), nb, cb + eb, ab + eb, lane);
+  }
+  if (is_seg) {
+    float* dst = part + w * ldp + 4 * lane;
+    *reinterpret_cast<float4*>(dst) = acc[0];
+    *reinterpret_cast<float4*>(dst + 128) = acc[1];
+    return;
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = 4 * (lane + 32 * h);
+    float4 o = acc[h];
+    if (self_alpha) {
+      const float sa = self_alpha[r];
+      const float4 xv = __ldg(reinterpret_cast<const float4*>(x + r * ldx + c));
+      o = make_float4(fmaf(sa, xv.x, o.x), fmaf(sa, xv.y, o.y), fmaf(sa, xv.z, o.z),
+                      fmaf(sa, xv.w, o.w));
+    }
+    if (mask) o = relu_mask4(o, mask + r * ldm + c);
+    *reinterpret_cast<float4*>(out + r * ldo + c) = o;
   }
 }
 
@@ -570,6 +675,21 @@ static int spmm_tpb() {  // threads per block of the full-row kernel (QGNN_SPMM_
                                                                   // holds 1 warp slot, not 8
 }
 
+static int wide_lean() {  // QGNN_SPMM_WIDE=0: 256-wide rows via k_spmm_f32<2>
+  const char* e = std::getenv("QGNN_SPMM_WIDE");
+  return e ? std::atoi(e) : 1;
+}
+
+static int g2_minb() {  // QGNN_G2_MINB=3: 85-register k_spmm_f32g2 (no spills, 24 warps/SM)
+  const char* e = std::getenv("QGNN_G2_MINB");
+  return e ? std::atoi(e) : 4;
+}
+
+static bool merge_hubs() {  // QGNN_HUB_MERGE=0: hub segments as a separate k_spmm_hubseg launch
+  const char* e = std::getenv("QGNN_HUB_MERGE");
+  return !e || std::atoi(e) != 0;
+}
+
 static bool grouped_narrow() {  // QGNN_SPMM_GROUPED=0 selects the one-row-per-warp kernel
   const char* e = std::getenv("QGNN_SPMM_GROUPED");
   return !e || std::atoi(e) != 0;
@@ -602,14 +722,31 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
   const int parts = nv == 1 ? 1 : (nv == 2 && dim % 8 == 0 && sw) ? (sw == 2 ? -2 : 2) : 0;
   if (parts && grouped_narrow()) {
     const int np = parts < 0 ? -parts : parts;
-    if (parts == 1 && dim / 4 >= 5 && two_per_lane())
-      k_spmm_f32g2<<<unsigned(ceil_div(n_rows, spmm_tpb() / 32)), spmm_tpb(), 0, s>>>(
-          dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask,
-          ldm);
-    else
-      k_spmm_f32g<<<unsigned(blocks * np), 256, 0, s>>>(dim / np, x, ldx, y, ldy, sa, pa, ca, aa,
-                                                        pb, cb, ab, row_begin, n_rows, out, ldo, hd,
-                                                        mask, ldm, parts);
+    if (parts == 1 && dim / 4 >= 5 && two_per_lane()) {
+      const bool mg = hubs && merge_hubs();
+      const int64_t ns = mg ? hp->n_segs : 0;
+      if (hubs && !mg)
+        k_spmm_hubseg<1><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(
+            dim, x, ldx, y, ldy, ca, aa, cb, ab, hp->seg, hp->n_segs, hp->part, hp->ldp);
+      const unsigned nb2 = unsigned(ceil_div(ns + n_rows, spmm_tpb() / 32));
+      if (g2_minb() == 3)
+        k_spmm_f32g2<3><<<nb2, spmm_tpb(), 0, s>>>(
+            dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask,
+            ldm, hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0);
+      else
+        k_spmm_f32g2<4><<<nb2, spmm_tpb(), 0, s>>>(
+            dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask,
+            ldm, hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0);
+      if (hubs)
+        k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 64)), 64, 0, s>>>(
+            dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask,
+            ldm);
+      check_launch("k_spmm_f32g2");
+      return;
+    }
+    k_spmm_f32g<<<unsigned(blocks * np), 256, 0, s>>>(dim / np, x, ldx, y, ldy, sa, pa, ca, aa,
+                                                      pb, cb, ab, row_begin, n_rows, out, ldo, hd,
+                                                      mask, ldm, parts);
     if (hubs) {
       if (nv == 1)
         k_spmm_hubseg<1><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(
@@ -622,6 +759,23 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
           ldm);
     }
     check_launch("k_spmm_f32g");
+    return;
+  }
+  if (dim == 256 && wide_lean()) {
+    const bool mg = hubs && merge_hubs();
+    const int64_t ns = mg ? hp->n_segs : 0;
+    if (hubs && !mg)
+      k_spmm_hubseg<2><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(
+          dim, x, ldx, y, ldy, ca, aa, cb, ab, hp->seg, hp->n_segs, hp->part, hp->ldp);
+    k_spmm_wide<16><<<unsigned(ceil_div(ns + n_rows, 2)), 64, 0, s>>>(
+        x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask, ldm,
+        hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0);
+    if (hubs) {
+      k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 64)), 64, 0, s>>>(
+          dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask,
+          ldm);
+    }
+    check_launch("k_spmm_wide");
     return;
   }
   switch (nv) {
