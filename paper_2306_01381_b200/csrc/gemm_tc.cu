@@ -72,6 +72,25 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// Multicast variant: the box lands at the same smem offset in every CTA of
+// `mask` and completes tx bytes on each destination's barrier at `bar`'s offset.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                               int c0, int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::"
+      "cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" :::
+                   "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -85,6 +104,14 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
                : "memory");
+}
+// arrive once on the barrier at `bar`'s offset in every CTA of `mask`
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
 }
 __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                        uint32_t idesc, uint32_t accum) {
@@ -152,6 +179,9 @@ struct Params {
   int64_t ldm;
   int mh;  // M halves per tile (MN-major path): 2 = 256-row tiles, the two TMEM buffers hold
            // the two halves, so the N operand is read once per 256 output rows
+  int cs;  // K-major: CTAs per cluster sharing each B stage (1, 2, 4).  Rank r loads
+           // B rows [r BN/cs, (r+1) BN/cs) once and multicasts them to the cluster; a
+           // stage is refilled when every CTA's MMAs have drained it (empty count = cs)
 };
 
 // kMN = false: A K-major (tmA box {32, 128}), B/Blo K-major prepared (box {32, BN})
@@ -184,12 +214,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 128);
-      mbar_init(&empty[s], 1);
+      mbar_init(&conv[s], 4);  // one arrival per converter warp
+      mbar_init(&empty[s], uint32_t(p.cs));
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -201,8 +231,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (p.cs > 1) cluster_sync();  // peers' barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const uint16_t cmask = uint16_t((1u << p.cs) - 1u);
+  const int crank = p.cs > 1 ? int(cluster_rank()) : 0;
 
   auto tile_chunks = [&](int tile, int& m0, int& kc0, int& kc1, int& split) {
     const int mt = tile % p.m_tiles;
@@ -231,8 +264,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_expect_tx(&full[s], a_bytes + 2 * b_bytes);
             for (int h = 0; h < p.mh; ++h)
               tma_load_2d(A + h * (kBM * kBK * 4), &tmA, &full[s], k0, m0 + kBM * h);
-            tma_load_2d(B, &tmB, &full[s], k0, 0);
-            tma_load_2d(Blo, &tmBlo, &full[s], k0, 0);
+            if (p.cs == 1) {
+              tma_load_2d(B, &tmB, &full[s], k0, 0);
+              tma_load_2d(Blo, &tmBlo, &full[s], k0, 0);
+            } else {  // this rank's slice of B rows, to every CTA of the cluster
+              const int rows = p.BN / p.cs, off = crank * rows * kBK * 4;
+              tma_load_2d_mc(B + off, &tmB, &full[s], k0, crank * rows, cmask);
+              tma_load_2d_mc(Blo + off, &tmBlo, &full[s], k0, crank * rows, cmask);
+            }
           } else {
             mbar_expect_tx(&full[s], a_bytes + b_bytes);
             // 32-bit MN-major operands must use the 128B swizzle with 32-byte atoms
@@ -296,7 +335,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             first = false;
           }
-          tc_commit(&empty[s]);
+          if (p.cs == 1)
+            tc_commit(&empty[s]);
+          else
+            tc_commit_mc(&empty[s], cmask);  // frees stage s in every CTA's ring
         }
         __syncwarp();
         if (++s == kStages) s = 0, ph ^= 1;
@@ -390,7 +432,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc0]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc0]);
     }
   } else if (warp >= 8) {
     // ---------------- converters
@@ -409,13 +452,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           split_tile(reinterpret_cast<float4*>(st + 2 * a_bytes),
                      reinterpret_cast<float4*>(st + 2 * a_bytes + b_bytes), b_bytes / 16, t, 128);
         fence_proxy_async();
-        mbar_arrive(&conv[s]);
+        __syncwarp();
+        if ((t & 31) == 0) mbar_arrive(&conv[s]);
         if (++s == kStages) s = 0, ph ^= 1;
       }
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (p.cs > 1) cluster_sync();  // no peer still multicasting into / arriving on this CTA
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -479,6 +524,12 @@ bool gemm_m256() {  // QGNN_GEMM_M256=1: 256-row tiles for z = A W and dz W^T to
   return e && std::atoi(e) != 0;
 }
 
+int gemm_cluster() {  // QGNN_GEMM_CLUSTER: CTAs sharing each B stage (1, 2 or 4)
+  const char* e = std::getenv("QGNN_GEMM_CLUSTER");
+  const int v = e ? std::atoi(e) : 2;
+  return v == 4 ? 4 : v == 2 ? 2 : 1;
+}
+
 bool wgrad_m256() {  // QGNN_WGRAD_M256=0: 128-row tiles (A/B)
   const char* e = std::getenv("QGNN_WGRAD_M256");
   return !e || std::atoi(e) != 0;
@@ -511,8 +562,37 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo, 
     attr_set = true;
   }
   const int tiles = p.m_tiles * p.splits;
-  const int grid = std::max(1, std::min(tiles, num_sms));
-  tc::k_tc_gemm<kMN><<<grid, tc::kThreads, sm, s>>>(a, b, blo, p);
+  if (p.cs == 1) {
+    const int grid = std::max(1, std::min(tiles, num_sms));
+    tc::k_tc_gemm<kMN><<<grid, tc::kThreads, sm, s>>>(a, b, blo, p);
+  } else {
+    // every CTA of a cluster runs the same number of tiles (p.m_tiles is a multiple
+    // of cs; rows past M load as TMA zero fill and are not stored)
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(tc::kThreads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(p.cs);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    // persistent grid = the clusters that are co-resident (GPC sizes need not be
+    // multiples of cs, so this can be below num_sms / cs)
+    static int resident[2][5] = {};  // [kMN][cs], per process (one device per engine)
+    int& rc = resident[kMN ? 1 : 0][p.cs];
+    if (rc == 0) {
+      cfg.gridDim = dim3(unsigned(num_sms / p.cs * p.cs));
+      int n = 0;
+      QGNN_CUDA(cudaOccupancyMaxActiveClusters(&n, tc::k_tc_gemm<kMN>, &cfg));
+      rc = std::max(1, n);
+    }
+    const int grid = std::max(p.cs, std::min(tiles, rc * p.cs));
+    cfg.gridDim = dim3(unsigned(grid));
+    QGNN_CUDA(cudaLaunchKernelEx(&cfg, tc::k_tc_gemm<kMN>, a, b, blo, p));
+  }
   check_launch("k_tc_gemm");
 }
 }  // namespace
@@ -530,10 +610,12 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
                                                                         transpose_w, bhi, blo);
   const CUtensorMap ta = make_map(A, uint64_t(K), uint64_t(n_rows), uint64_t(lda), tc::kBK, tc::kBM,
                                   CU_TENSOR_MAP_SWIZZLE_64B);
-  const CUtensorMap tb = make_map(bhi, uint64_t(Kp), uint64_t(N), uint64_t(Kp), tc::kBK, uint32_t(BN),
-                                  CU_TENSOR_MAP_SWIZZLE_64B);
+  int cs = gemm_cluster();
+  while (cs > 1 && (BN % (8 * cs) != 0 || ceil_div(n_rows, tc::kBM) < 2 * cs)) cs >>= 1;
+  const CUtensorMap tb = make_map(bhi, uint64_t(Kp), uint64_t(N), uint64_t(Kp), tc::kBK,
+                                  uint32_t(BN / cs), CU_TENSOR_MAP_SWIZZLE_64B);
   const CUtensorMap tbl = make_map(blo, uint64_t(Kp), uint64_t(N), uint64_t(Kp), tc::kBK,
-                                   uint32_t(BN), CU_TENSOR_MAP_SWIZZLE_64B);
+                                   uint32_t(BN / cs), CU_TENSOR_MAP_SWIZZLE_64B);
   tc::Params p{};
   p.M = int(n_rows);
   p.N = N;
@@ -549,8 +631,10 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
   p.relu = relu;
   p.mask = mask;
   p.ldm = ldm;
-  p.mh = gemm_m256() && n_rows > tc::kBM ? 2 : 1;
+  p.mh = gemm_m256() && n_rows > tc::kBM && cs == 1 ? 2 : 1;
   p.m_tiles = int(ceil_div(n_rows, tc::kBM * p.mh));
+  p.cs = cs;
+  if (cs > 1) p.m_tiles = int(round_up(p.m_tiles, cs));
   p.stages = stages_for(BN, p.mh);
   launch<false>(ta, tb, tbl, p, ctx->num_sms, s);
 }
@@ -591,6 +675,7 @@ float* tc_gemm_wgrad_partials(qgnn_ctx* ctx, const float* A, int64_t lda, const 
   p.mask = nullptr;
   p.ldm = 0;
   p.mh = mh;
+  p.cs = 1;
   p.stages = stages_for(BN, mh);
   launch<true>(ta, tb, tb, p, ctx->num_sms, s);
   *splits_out = splits;
