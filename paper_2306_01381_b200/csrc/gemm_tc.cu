@@ -179,6 +179,8 @@ struct Params {
   int64_t ldm;
   int mh;  // M halves per tile (MN-major path): 2 = 256-row tiles, the two TMEM buffers hold
            // the two halves, so the N operand is read once per 256 output rows
+  int dbg;  // QGNN_GEMM_DEBUG bit mask for bottleneck isolation (results invalid when set):
+            // 1 = no MMAs, 2 = no output stores, 4 = no lo split
   int cs;  // K-major: CTAs per cluster sharing each B stage (1, 2, 4).  Rank r loads
            // B rows [r BN/cs, (r+1) BN/cs) once and multicasts them to the cluster; a
            // stage is refilled when every CTA's MMAs have drained it (empty count = cs)
@@ -329,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int h = 0; h < p.mh; ++h) {  // half h: rows 128h.. (MN groups 4h.. / SW64 atoms 16h..)
               const uint64_t hoff = uint64_t(h * (kBM * kBK * 4)) >> 4;
               const uint32_t dh = d + uint32_t(h * p.tmem_cols);
+              if (p.dbg & 1) continue;
               tc_mma(dh, dAh + hoff, dBh, idesc, first ? 0u : 1u);
               tc_mma(dh, dAh + hoff, dBl, idesc, 1u);
               tc_mma(dh, dAl + hoff, dBh, idesc, 1u);
@@ -418,6 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             v.z = mk[j].z > 0.f ? v.z : 0.f;
             v.w = mk[j].w > 0.f ? v.w : 0.f;
           }
+          if (p.dbg & 2) continue;
           float* o = out_base + int64_t(row) * p.ldo + cc;
           if (cc + 4 <= p.N && (p.ldo & 3) == 0) {
             *reinterpret_cast<float4*>(o) = v;
@@ -446,8 +450,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kc = kc0; kc < kc1; ++kc) {
         mbar_wait(&full[s], ph);
         uint8_t* st = smem + s * stage_bytes;
-        split_tile(reinterpret_cast<float4*>(st), reinterpret_cast<float4*>(st + a_bytes),
-                   a_bytes / 16, t, 128);
+        if (!(p.dbg & 4))
+          split_tile(reinterpret_cast<float4*>(st), reinterpret_cast<float4*>(st + a_bytes),
+                     a_bytes / 16, t, 128);
         if (kMN)
           split_tile(reinterpret_cast<float4*>(st + 2 * a_bytes),
                      reinterpret_cast<float4*>(st + 2 * a_bytes + b_bytes), b_bytes / 16, t, 128);
@@ -522,6 +527,11 @@ CUtensorMap make_map(const float* base, uint64_t inner, uint64_t outer, uint64_t
 bool gemm_m256() {  // QGNN_GEMM_M256=1: 256-row tiles for z = A W and dz W^T too (A/B)
   const char* e = std::getenv("QGNN_GEMM_M256");
   return e && std::atoi(e) != 0;
+}
+
+int gemm_debug() {
+  const char* e = std::getenv("QGNN_GEMM_DEBUG");
+  return e ? std::atoi(e) : 0;
 }
 
 int gemm_cluster() {  // QGNN_GEMM_CLUSTER: CTAs sharing each B stage (1, 2 or 4)
@@ -634,6 +644,7 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
   p.mh = gemm_m256() && n_rows > tc::kBM && cs == 1 ? 2 : 1;
   p.m_tiles = int(ceil_div(n_rows, tc::kBM * p.mh));
   p.cs = cs;
+  p.dbg = gemm_debug();
   if (cs > 1) p.m_tiles = int(round_up(p.m_tiles, cs));
   p.stages = stages_for(BN, p.mh);
   launch<false>(ta, tb, tbl, p, ctx->num_sms, s);
@@ -676,6 +687,7 @@ float* tc_gemm_wgrad_partials(qgnn_ctx* ctx, const float* A, int64_t lda, const 
   p.ldm = 0;
   p.mh = mh;
   p.cs = 1;
+  p.dbg = gemm_debug();
   p.stages = stages_for(BN, mh);
   launch<true>(ta, tb, tb, p, ctx->num_sms, s);
   *splits_out = splits;
