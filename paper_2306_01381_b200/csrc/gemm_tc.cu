@@ -180,7 +180,7 @@ struct Params {
   int mh;  // M halves per tile (MN-major path): 2 = 256-row tiles, the two TMEM buffers hold
            // the two halves, so the N operand is read once per 256 output rows
   int dbg;  // QGNN_GEMM_DEBUG bit mask for bottleneck isolation (results invalid when set):
-            // 1 = no MMAs, 2 = no output stores, 4 = no lo split
+            // 1 = no MMAs, 2 = no output stores, 4 = no lo split, 8 = TMA producer only
   int cs;  // K-major: CTAs per cluster sharing each B stage (1, 2, 4).  Rank r loads
            // B rows [r BN/cs, (r+1) BN/cs) once and multicasts them to the cluster; a
            // stage is refilled when every CTA's MMAs have drained it (empty count = cs)
@@ -247,7 +247,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     kc1 = min(p.k_chunks, kc0 + p.chunks_per_split);
   };
 
-  if (warp == 0) {
+  if ((p.dbg & 8) && warp != 0) {
+    // isolation: producer alone (it waits for its own loads before reusing a stage)
+  } else if (warp == 0) {
     // ---------------- TMA producer
     if (lane == 0) {
       int s = 0;
@@ -256,7 +258,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         int m0, kc0, kc1, split;
         tile_chunks(tile, m0, kc0, kc1, split);
         for (int kc = kc0; kc < kc1; ++kc) {
-          mbar_wait(&empty[s], ph ^ 1);
+          if (p.dbg & 8)
+            mbar_wait(&full[s], ph ^ 1);
+          else
+            mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * stage_bytes;
           uint8_t* A = st;
           uint8_t* B = st + 2 * a_bytes;
@@ -620,7 +625,7 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
                                                                         transpose_w, bhi, blo);
   const CUtensorMap ta = make_map(A, uint64_t(K), uint64_t(n_rows), uint64_t(lda), tc::kBK, tc::kBM,
                                   CU_TENSOR_MAP_SWIZZLE_64B);
-  int cs = gemm_cluster();
+  int cs = (gemm_debug() & 8) ? 1 : gemm_cluster();  // producer-only isolation is per CTA
   while (cs > 1 && (BN % (8 * cs) != 0 || ceil_div(n_rows, tc::kBM) < 2 * cs)) cs >>= 1;
   const CUtensorMap tb = make_map(bhi, uint64_t(Kp), uint64_t(N), uint64_t(Kp), tc::kBK,
                                   uint32_t(BN / cs), CU_TENSOR_MAP_SWIZZLE_64B);

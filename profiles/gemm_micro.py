@@ -34,8 +34,10 @@ DBG = os.environ.get("DBG", "0,1,2,4,3,7").split(",")
 
 def main():
     M = int(os.environ.get("M", 300_000))
-    for K, N in ((100, 256), (256, 256), (256, 48)):
-        for cl in ("1", "2"):
+    shapes = [tuple(int(v) for v in x.split("x")) for x in
+              os.environ.get("SHAPES", "100x256,256x256,256x48").split(",")]
+    for K, N in shapes:
+        for cl in os.environ.get("CLUSTERS", "1,2").split(","):
             for dbg in DBG:
                 os.environ["QGNN_GEMM_DEBUG"] = dbg
                 os.environ["QGNN_GEMM_CLUSTER"] = cl
