@@ -529,9 +529,14 @@ CUtensorMap make_map(const float* base, uint64_t inner, uint64_t outer, uint64_t
   return m;
 }
 
-bool gemm_m256() {  // QGNN_GEMM_M256=1: 256-row tiles for z = A W and dz W^T too (A/B)
+// 256-row tiles for the K-major path: the B stage is then loaded once per 256
+// output rows.  Default: only for narrow outputs (BN <= 64, e.g. the 47-class
+// layer: -12 % in profiles/gemm_micro_r1.txt); at BN = 256 the halved ring depth
+// and the lost TMEM double buffer cost more (+20 %).  QGNN_GEMM_M256=0/1 forces.
+bool gemm_m256(int bn) {
   const char* e = std::getenv("QGNN_GEMM_M256");
-  return e && std::atoi(e) != 0;
+  if (e) return std::atoi(e) != 0;
+  return bn <= 64;
 }
 
 int gemm_debug() {
@@ -625,7 +630,8 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
                                                                         transpose_w, bhi, blo);
   const CUtensorMap ta = make_map(A, uint64_t(K), uint64_t(n_rows), uint64_t(lda), tc::kBK, tc::kBM,
                                   CU_TENSOR_MAP_SWIZZLE_64B);
-  int cs = (gemm_debug() & 8) ? 1 : gemm_cluster();  // producer-only isolation is per CTA
+  const bool m256 = gemm_m256(BN) && n_rows > tc::kBM;
+  int cs = (gemm_debug() & 8) || m256 ? 1 : gemm_cluster();  // producer-only isolation is per CTA
   while (cs > 1 && (BN % (8 * cs) != 0 || ceil_div(n_rows, tc::kBM) < 2 * cs)) cs >>= 1;
   const CUtensorMap tb = make_map(bhi, uint64_t(Kp), uint64_t(N), uint64_t(Kp), tc::kBK,
                                   uint32_t(BN / cs), CU_TENSOR_MAP_SWIZZLE_64B);
@@ -646,7 +652,7 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
   p.relu = relu;
   p.mask = mask;
   p.ldm = ldm;
-  p.mh = gemm_m256() && n_rows > tc::kBM && cs == 1 ? 2 : 1;
+  p.mh = m256 ? 2 : 1;
   p.m_tiles = int(ceil_div(n_rows, tc::kBM * p.mh));
   p.cs = cs;
   p.dbg = gemm_debug();
