@@ -571,8 +571,9 @@ __global__ void __launch_bounds__(256, MINB) k_quantize_pack_lean(
           const uint32_t code = static_cast<uint32_t>(base) + (u < frac ? 1u : 0u);
           word |= min(code, levels) << (q * b);
           // x' within 2^-43 of x: the decision can only differ near a boundary
-          slow |= hq != hi && a != 0.0 &&
-                  (frac < tol || frac > 1.0 - tol || fabs(u - frac) < tol);
+          // non-short-circuit: predicate logic instead of a branch per element
+          slow |= (hq != hi) & (a != 0.0) &
+                  ((frac < tol) | (frac > 1.0 - tol) | (fabs(u - frac) < tol));
         }
         if (slow) {  // ~1e-12 per element: recompute the chunk exactly
           const double lv = static_cast<double>(levels);

@@ -114,6 +114,8 @@ struct HubPlan {
   const int64_t* seg = nullptr;      // [n_segs][4] = a_begin, a_end, b_begin, b_end
   float* part = nullptr;             // [n_segs][ldp] partial rows (workspace)
   int64_t ldp = 0;
+  const int32_t* order = nullptr;    // [n_order] non-hub rows of the range, degree-descending
+  int64_t n_order = 0;
 };
 // fp32 row-range SpMM with segmented hub rows (spmm.cu)
 void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y, int64_t ldy,

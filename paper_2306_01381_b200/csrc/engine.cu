@@ -311,7 +311,7 @@ class Engine final : public EngineBase {
     DBuf<double> ce_terms;
     // hub rows (slots) per SpMM call site, segmented (spmm.cu:k_spmm_hubseg)
     struct Hubs {
-      DBuf<int32_t> rows, seg_ptr;
+      DBuf<int32_t> rows, seg_ptr, order;
       DBuf<int64_t> seg;
       DBuf<float> part;
       HubPlan plan;
@@ -331,11 +331,15 @@ class Engine final : public EngineBase {
     constexpr int64_t kSeg = 256;
     std::vector<int32_t> rows, sptr{0};
     std::vector<int64_t> seg;
+    std::vector<std::pair<int64_t, int32_t>> by_deg;  // (-degree, row) of the non-hub rows
     for (int64_t r = r0; r < r1; ++r) {
       const int64_t a0 = pa[r], a1 = pa[r + 1];
       const int64_t b0 = pb ? (*pb)[r] : 0, b1 = pb ? (*pb)[r + 1] : 0;
       const int64_t deg = (a1 - a0) + (b1 - b0);
-      if (deg <= kHubDeg) continue;
+      if (deg <= kHubDeg) {
+        by_deg.emplace_back(-deg, int32_t(r));
+        continue;
+      }
       rows.push_back(int32_t(r));
       for (int64_t e = 0; e < deg; e += kSeg) {  // edge positions in the (a ++ b) list
         const int64_t f = std::min(deg, e + kSeg);
@@ -347,6 +351,13 @@ class Engine final : public EngineBase {
       }
       sptr.push_back(int32_t(seg.size() / 4));
     }
+    // degree-descending row order for the multi-row narrow kernel (spmm.cu:k_spmm_sorted)
+    std::sort(by_deg.begin(), by_deg.end());
+    std::vector<int32_t> order(by_deg.size());
+    for (size_t i = 0; i < by_deg.size(); ++i) order[i] = by_deg[i].second;
+    h.order.upload(order);
+    h.plan.order = order.empty() ? nullptr : h.order.p;
+    h.plan.n_order = int64_t(order.size());
     h.rows.upload(rows);
     h.seg_ptr.upload(sptr);
     h.seg.upload(seg);

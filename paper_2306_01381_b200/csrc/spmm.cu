@@ -477,6 +477,109 @@ __global__ void __launch_bounds__(256, MINB) k_spmm_f32g2(
   }
 }
 
+// Narrow rows (D <= 128), several rows per warp: G = ceil(F/2) lanes (two float4
+// each) own one row, R = 32/G rows per warp, no cross-group reduction.  Rows come
+// from HubPlan::order — the range's non-hub rows sorted by descending degree — so
+// the R rows of a warp have (nearly) the same length and the warp-uniform edge
+// loop wastes little; hub segments (256 edges) are the first units.  Per lane 4
+// edges x 2 float4 in flight; each step's 4 edge indices are loaded by 4 lanes of
+// the group and shuffled to the rest (G >= 4, i.e. D >= 28).
+__device__ __forceinline__ void sorted_gather(float4 (&acc)[2], const float* __restrict__ src,
+                                              int ld, int n, int nmax,
+                                              const int32_t* __restrict__ col,
+                                              const float* __restrict__ alpha, bool has2,
+                                              int sub, int base) {
+  for (int j = 0; j < nmax; j += 4) {
+    // lanes 0..3 of the group load the step's 4 edge indices, the group shuffles them
+    int my_c = 0;
+    float my_a = 0.f;
+    if (sub < 4 && j + sub < n) my_c = __ldg(col + j + sub), my_a = __ldg(alpha + j + sub);
+    int c[4];
+    float a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      c[u] = __shfl_sync(0xffffffffu, my_c, (base + u) & 31);
+      a[u] = __shfl_sync(0xffffffffu, my_a, (base + u) & 31);
+    }
+    float4 v[4][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float4* p = reinterpret_cast<const float4*>(src + int64_t(c[u]) * ld);
+      v[u][0] = v[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j + u < n) {
+        v[u][0] = __ldg(p);
+        if (has2) v[u][1] = __ldg(p + 1);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      fma4(acc[0], a[u], v[u][0]);
+      fma4(acc[1], a[u], v[u][1]);
+    }
+  }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(64, MINB) k_spmm_sorted(
+    int dim, const float* __restrict__ x, int64_t ldx, const float* __restrict__ y, int64_t ldy,
+    const float* __restrict__ self_alpha, const int64_t* __restrict__ pa,
+    const int32_t* __restrict__ ca, const float* __restrict__ aa, const int64_t* __restrict__ pb,
+    const int32_t* __restrict__ cb, const float* __restrict__ ab,
+    const int32_t* __restrict__ order, int64_t n_order, float* __restrict__ out, int64_t ldo,
+    const float* __restrict__ mask, int64_t ldm, const int64_t* __restrict__ seg, int64_t n_segs,
+    float* __restrict__ part, int64_t ldp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int F = dim >> 2, G = (F + 1) >> 1, R = 32 / G;
+  const int grp = lane / G, sub = lane - grp * G;
+  const bool act = grp < R;
+  const bool has2 = 2 * sub + 1 < F;
+  const int64_t u = (int64_t(blockIdx.x) * (blockDim.x >> 5) + warp) * R + grp;
+  const bool is_seg = u < n_segs;
+  const bool live = act && u < n_segs + n_order;
+  int64_t ea = 0, eb = 0, r = -1;
+  int na = 0, nb = 0;
+  if (live) {
+    if (is_seg) {
+      const int64_t* sg = seg + 4 * u;
+      ea = sg[0], na = int(sg[1] - ea), eb = sg[2], nb = int(sg[3] - eb);
+    } else {
+      r = order[u - n_segs];
+      ea = pa[r], na = int(pa[r + 1] - ea);
+      if (pb) eb = pb[r], nb = int(pb[r + 1] - eb);
+    }
+  }
+  int ma = na, mb = nb;  // warp-uniform trip counts (rows of a warp have ~equal degree)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ma = max(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+    mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+  }
+  float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+  const int cx = sub * 8;
+  // all lanes stay for the shuffles; dead lanes load nothing (n = 0)
+  sorted_gather(acc, x + cx, int(ldx), na, ma, ca + ea, aa + ea, has2, sub, grp * G);
+  if (mb) sorted_gather(acc, y + cx, int(ldy), nb, mb, cb + eb, ab + eb, has2, sub, grp * G);
+  if (!live) return;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (h == 1 && !has2) break;
+    const int c = cx + 4 * h;
+    float4 o = acc[h];
+    if (is_seg) {
+      *reinterpret_cast<float4*>(part + u * ldp + c) = o;
+      continue;
+    }
+    if (self_alpha) {
+      const float sa = self_alpha[r];
+      const float4 xv = __ldg(reinterpret_cast<const float4*>(x + r * ldx + c));
+      o = make_float4(fmaf(sa, xv.x, o.x), fmaf(sa, xv.y, o.y), fmaf(sa, xv.z, o.z),
+                      fmaf(sa, xv.w, o.w));
+    }
+    if (mask) o = relu_mask4(o, mask + r * ldm + c);
+    *reinterpret_cast<float4*>(out + r * ldo + c) = o;
+  }
+}
+
 // 256-wide rows (two float4 per lane, every lane active), register-lean: 32-bit
 // edge offsets within the row (pointers rebased once per row), no per-lane column
 // bounds, alphas shuffled after the loads — to fit 64 registers (32 warps/SM)
@@ -685,6 +788,16 @@ static int g2_minb() {  // QGNN_G2_MINB=3: 85-register k_spmm_f32g2 (no spills, 
   return e ? std::atoi(e) : 4;
 }
 
+static int sorted_rows() {  // QGNN_SPMM_SORTED=0: narrow rows via k_spmm_f32g2 (2: 64 regs)
+  const char* e = std::getenv("QGNN_SPMM_SORTED");
+  return e ? std::atoi(e) : 1;
+}
+
+static int sorted_max_dim() {  // widest rows sent to k_spmm_sorted (QGNN_SPMM_SORTED_MAXD)
+  const char* e = std::getenv("QGNN_SPMM_SORTED_MAXD");
+  return e ? std::atoi(e) : 64;
+}
+
 static bool merge_hubs() {  // QGNN_HUB_MERGE=0: hub segments as a separate k_spmm_hubseg launch
   const char* e = std::getenv("QGNN_HUB_MERGE");
   return !e || std::atoi(e) != 0;
@@ -718,6 +831,26 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
           dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask, ldm); \
     }                                                                                          \
     break;
+  if (hp && hp->order && dim <= sorted_max_dim() && dim / 4 >= 7 && sorted_rows()) {
+    const int G = (dim / 4 + 1) / 2, R = 32 / G;
+    const int64_t ns = hp->n_hubs > 0 ? hp->n_segs : 0;
+    const int64_t units = ns + hp->n_order;
+    const unsigned nb = unsigned(ceil_div(ceil_div(units, R), 2));
+    if (sorted_rows() == 2)
+      k_spmm_sorted<16><<<nb, 64, 0, s>>>(dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab,
+                                          hp->order, hp->n_order, out, ldo, mask, ldm, hp->seg, ns,
+                                          hp->part, hp->ldp);
+    else
+      k_spmm_sorted<12><<<nb, 64, 0, s>>>(dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab,
+                                          hp->order, hp->n_order, out, ldo, mask, ldm, hp->seg, ns,
+                                          hp->part, hp->ldp);
+    if (hp->n_hubs > 0)
+      k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 64)), 64, 0, s>>>(
+          dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask,
+          ldm);
+    check_launch("k_spmm_sorted");
+    return;
+  }
   const int sw = split_wide();
   const int parts = nv == 1 ? 1 : (nv == 2 && dim % 8 == 0 && sw) ? (sw == 2 ? -2 : 2) : 0;
   if (parts && grouped_narrow()) {

@@ -1,6 +1,7 @@
 """DRAM traffic per engine launch of each kernel class, from an ncu launch list
 taken with --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
-over ONE epoch (bench.py, 1 GPU).  Kernels are assigned to the engine's classes
+over ONE epoch (bench.py, 1 GPU; with two or more optimizer steps in the list the
+last complete epoch is used).  Kernels are assigned to the engine's classes
 by name and by phase (forward = before k_loss_f32).  Writes profiles/ncu_traffic.json
 {class: bytes per engine-level launch}, read by bench.py as roofline.traffic.
 
@@ -32,9 +33,13 @@ def main(path):
             continue
         d = launches.setdefault(r[idi], {"name": r[ki].split("(")[0].replace("void ", "")})
         d[r[ni]] = float(r[vi].replace(",", "")) * UNITS.get(r[ui], 1.0)
+    seq = list(launches.values())
+    adam = [i for i, d in enumerate(seq) if "k_adam" in d["name"]]
+    if len(adam) >= 2:  # one whole epoch: after the penultimate optimizer step up to the last
+        seq = seq[adam[-2] + 1:adam[-1] + 1]
     phase = "fwd"
     acc = collections.defaultdict(lambda: [0.0, 0.0])  # class -> [dram bytes, seconds]
-    for d in launches.values():
+    for d in seq:
         n = d["name"]
         if "k_loss_f32" in n:
             phase = "bwd"
