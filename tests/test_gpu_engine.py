@@ -123,6 +123,34 @@ def test_engine_wide_hub_rows_match(cuda, monkeypatch, split):
     assert np.abs(wb - wh).max() < 1e-4
 
 
+@pytest.mark.parametrize("hub_deg", [None, "2"])
+def test_engine_sorted_narrow_rows_match(cuda, monkeypatch, hub_deg):
+    """28..64-wide layers through the degree-sorted multi-row kernel (k_spmm_sorted:
+    R rows per warp, hub segments as its first units when hub_deg is set) give the
+    same run as the one-row-per-warp kernel (k_spmm_f32g2)."""
+    if hub_deg:
+        monkeypatch.setenv("QGNN_HUB_DEG", hub_deg)
+
+    def run():
+        eng = Engine(GRAPH, [8, 40, 48, 36, 3], n_parts=4, bit_mode="fixed", fixed_bits=8,
+                     seed=11, dtype="f32")
+        out = [eng.run_epoch()["train_loss"] for _ in range(3)]
+        w = np.concatenate([x.reshape(-1) for x in eng.weights()])
+        eng.close()
+        return out, w
+
+    monkeypatch.setenv("QGNN_SPMM_SORTED", "1")
+    srt, ws = run()
+    monkeypatch.setenv("QGNN_SPMM_SORTED", "0")
+    grp, wg = run()
+    for a, b in zip(srt, grp):
+        assert _rel(a, b) < 1e-5, (a, b)
+    assert np.abs(ws - wg).max() < 1e-4
+    # the two kernels sum in different orders: bit-identical weights would mean the
+    # sorted path was not taken
+    assert not (ws == wg).all()
+
+
 def test_engine_transform_first_last_layer(cuda, monkeypatch):
     """z = A(hW) for the narrowing last layer matches aggregate-then-transform (fp32)."""
     tf, wt = _run("fixed", 4, 4, "f32")
