@@ -181,6 +181,7 @@ struct Params {
            // the two halves, so the N operand is read once per 256 output rows
   int dbg;  // QGNN_GEMM_DEBUG bit mask for bottleneck isolation (results invalid when set):
             // 1 = no MMAs, 2 = no output stores, 4 = no lo split, 8 = TMA producer only
+  int bk;  // K elements per chunk: 16 (SW64, 64-byte rows) or 32 (SW128, K-major only)
   int cs;  // K-major: CTAs per cluster sharing each B stage (1, 2, 4).  Rank r loads
            // B rows [r BN/cs, (r+1) BN/cs) once and multicasts them to the cluster; a
            // stage is refilled when every CTA's MMAs have drained it (empty count = cs)
@@ -195,8 +196,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  const int a_bytes = kBM * kBK * 4 * p.mh;  // 8 KB per 128-row half
-  const int b_bytes = p.BN * kBK * 4;       // BN x 64 B
+  const int bk = kMN ? kBK : p.bk;
+  const int a_bytes = kBM * bk * 4 * p.mh;  // 8 / 16 KB per 128-row half
+  const int b_bytes = p.BN * bk * 4;       // BN x 64 / 128 B
   const int stage_bytes = 2 * a_bytes + 2 * b_bytes;
   const int kStages = p.stages;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * stage_bytes);
@@ -266,16 +268,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* A = st;
           uint8_t* B = st + 2 * a_bytes;
           uint8_t* Blo = B + b_bytes;
-          const int k0 = kc * kBK;
+          const int k0 = kc * bk;
           if (!kMN) {
             mbar_expect_tx(&full[s], a_bytes + 2 * b_bytes);
             for (int h = 0; h < p.mh; ++h)
-              tma_load_2d(A + h * (kBM * kBK * 4), &tmA, &full[s], k0, m0 + kBM * h);
+              tma_load_2d(A + h * (kBM * bk * 4), &tmA, &full[s], k0, m0 + kBM * h);
             if (p.cs == 1) {
               tma_load_2d(B, &tmB, &full[s], k0, 0);
               tma_load_2d(Blo, &tmBlo, &full[s], k0, 0);
             } else {  // this rank's slice of B rows, to every CTA of the cluster
-              const int rows = p.BN / p.cs, off = crank * rows * kBK * 4;
+              const int rows = p.BN / p.cs, off = crank * rows * bk * 4;
               tma_load_2d_mc(B + off, &tmB, &full[s], k0, crank * rows, cmask);
               tma_load_2d_mc(Blo + off, &tmBlo, &full[s], k0, crank * rows, cmask);
             }
@@ -320,13 +322,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t aH = smem_u32(st), aL = smem_u32(st + a_bytes);
           const uint32_t bH = smem_u32(st + 2 * a_bytes), bL = smem_u32(st + 2 * a_bytes + b_bytes);
 #pragma unroll
-          for (int j = 0; j < kBK / 8; ++j) {
+          for (int j = 0; j < bk / 8; ++j) {
             uint64_t dAh, dAl, dBh, dBl;
-            if (!kMN) {  // K-major SWIZZLE_64B: 8-row atoms of 64 B (SBO 512), +32 B per k-step
-              dAh = sdesc(aH + 32 * j, 16, 512, 4);
-              dAl = sdesc(aL + 32 * j, 16, 512, 4);
-              dBh = sdesc(bH + 32 * j, 16, 512, 4);
-              dBl = sdesc(bL + 32 * j, 16, 512, 4);
+            if (!kMN) {  // K-major SWIZZLE_64B / 128B: 8-row atoms of 64 / 128 B, +32 B per k-step
+              const uint32_t sbo = bk == 32 ? 1024 : 512, lay = bk == 32 ? 2 : 4;
+              dAh = sdesc(aH + 32 * j, 16, sbo, lay);
+              dAl = sdesc(aL + 32 * j, 16, sbo, lay);
+              dBh = sdesc(bH + 32 * j, 16, sbo, lay);
+              dBl = sdesc(bL + 32 * j, 16, sbo, lay);
             } else {  // MN-major BASE32B: 4-row K atoms (SBO 512 B), MN groups 2 KB (LBO)
               dAh = sdesc(aH + 1024 * j, 2048, 512, 1);
               dAl = sdesc(aL + 1024 * j, 2048, 512, 1);
@@ -334,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               dBl = sdesc(bL + 1024 * j, 2048, 512, 1);
             }
             for (int h = 0; h < p.mh; ++h) {  // half h: rows 128h.. (MN groups 4h.. / SW64 atoms 16h..)
-              const uint64_t hoff = uint64_t(h * (kBM * kBK * 4)) >> 4;
+              const uint64_t hoff = uint64_t(h * (kBM * bk * 4)) >> 4;
               const uint32_t dh = d + uint32_t(h * p.tmem_cols);
               if (p.dbg & 1) continue;
               tc_mma(dh, dAh + hoff, dBh, idesc, first ? 0u : 1u);
@@ -544,6 +547,11 @@ int gemm_debug() {
   return e ? std::atoi(e) : 0;
 }
 
+int gemm_bk() {  // QGNN_GEMM_BK=32: 128-byte K-major rows (SW128) for z = A W / dz W^T
+  const char* e = std::getenv("QGNN_GEMM_BK");
+  return e && std::atoi(e) == 32 ? 32 : 16;
+}
+
 int gemm_cluster() {  // QGNN_GEMM_CLUSTER: CTAs sharing each B stage (1, 2 or 4)
   const char* e = std::getenv("QGNN_GEMM_CLUSTER");
   const int v = e ? std::atoi(e) : 2;
@@ -562,19 +570,19 @@ int pow2_cols(int bn) {
 }
 
 constexpr size_t kSmemBudget = 200 * 1024;  // + 18 KB epilogue staging (<= 227 KB)
-int stages_for(int BN, int mh = 1) {
-  const size_t stage = 2 * tc::kBM * tc::kBK * 4 * size_t(mh) + 2 * size_t(BN) * tc::kBK * 4;
+int stages_for(int BN, int mh = 1, int bk = tc::kBK) {
+  const size_t stage = 2 * tc::kBM * bk * 4 * size_t(mh) + 2 * size_t(BN) * bk * 4;
   return int(std::max<size_t>(2, std::min<size_t>(tc::kMaxStages, kSmemBudget / stage)));
 }
-size_t smem_bytes(int BN, int mh = 1) {
-  const size_t stage = 2 * tc::kBM * tc::kBK * 4 * size_t(mh) + 2 * size_t(BN) * tc::kBK * 4;
-  return size_t(stages_for(BN, mh)) * stage + 1024 + 256 + 4 * 32 * 36 * sizeof(float);
+size_t smem_bytes(int BN, int mh = 1, int bk = tc::kBK) {
+  const size_t stage = 2 * tc::kBM * bk * 4 * size_t(mh) + 2 * size_t(BN) * bk * 4;
+  return size_t(stages_for(BN, mh, bk)) * stage + 1024 + 256 + 4 * 32 * 36 * sizeof(float);
 }
 
 template <bool kMN>
 void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo, const tc::Params& p,
             int num_sms, cudaStream_t s) {
-  const size_t sm = smem_bytes(p.BN, p.mh);
+  const size_t sm = smem_bytes(p.BN, p.mh, kMN ? tc::kBK : p.bk);
   static bool attr_set = false;
   if (!attr_set) {
     QGNN_CUDA(cudaFuncSetAttribute(tc::k_tc_gemm<kMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -628,15 +636,17 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
   float* blo = bhi + size_t(BN) * Kp;
   tc::k_prep_b<<<unsigned(ceil_div(int64_t(N) * Kp, 256)), 256, 0, s>>>(W, wcols, N, K, Kp,
                                                                         transpose_w, bhi, blo);
-  const CUtensorMap ta = make_map(A, uint64_t(K), uint64_t(n_rows), uint64_t(lda), tc::kBK, tc::kBM,
-                                  CU_TENSOR_MAP_SWIZZLE_64B);
+  const int bk = gemm_bk();
+  const CUtensorMapSwizzle swz = bk == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  const CUtensorMap ta = make_map(A, uint64_t(K), uint64_t(n_rows), uint64_t(lda), uint32_t(bk),
+                                  tc::kBM, swz);
   const bool m256 = gemm_m256(BN) && n_rows > tc::kBM;
   int cs = (gemm_debug() & 8) || m256 ? 1 : gemm_cluster();  // producer-only isolation is per CTA
   while (cs > 1 && (BN % (8 * cs) != 0 || ceil_div(n_rows, tc::kBM) < 2 * cs)) cs >>= 1;
-  const CUtensorMap tb = make_map(bhi, uint64_t(Kp), uint64_t(N), uint64_t(Kp), tc::kBK,
-                                  uint32_t(BN / cs), CU_TENSOR_MAP_SWIZZLE_64B);
-  const CUtensorMap tbl = make_map(blo, uint64_t(Kp), uint64_t(N), uint64_t(Kp), tc::kBK,
-                                   uint32_t(BN / cs), CU_TENSOR_MAP_SWIZZLE_64B);
+  const CUtensorMap tb = make_map(bhi, uint64_t(Kp), uint64_t(N), uint64_t(Kp), uint32_t(bk),
+                                  uint32_t(BN / cs), swz);
+  const CUtensorMap tbl = make_map(blo, uint64_t(Kp), uint64_t(N), uint64_t(Kp), uint32_t(bk),
+                                   uint32_t(BN / cs), swz);
   tc::Params p{};
   p.M = int(n_rows);
   p.N = N;
@@ -645,7 +655,8 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
   p.tmem_cols = pow2_cols(BN);
   p.m_tiles = int(ceil_div(n_rows, tc::kBM));
   p.splits = 1;
-  p.k_chunks = int(ceil_div(K, tc::kBK));
+  p.k_chunks = int(ceil_div(K, bk));
+  p.bk = bk;
   p.chunks_per_split = p.k_chunks;
   p.out = out;
   p.ldo = ldo;
@@ -657,7 +668,7 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
   p.cs = cs;
   p.dbg = gemm_debug();
   if (cs > 1) p.m_tiles = int(round_up(p.m_tiles, cs));
-  p.stages = stages_for(BN, p.mh);
+  p.stages = stages_for(BN, p.mh, bk);
   launch<false>(ta, tb, tbl, p, ctx->num_sms, s);
 }
 
@@ -698,6 +709,7 @@ float* tc_gemm_wgrad_partials(qgnn_ctx* ctx, const float* A, int64_t lda, const 
   p.ldm = 0;
   p.mh = mh;
   p.cs = 1;
+  p.bk = tc::kBK;
   p.dbg = gemm_debug();
   p.stages = stages_for(BN, mh);
   launch<true>(ta, tb, tb, p, ctx->num_sms, s);
