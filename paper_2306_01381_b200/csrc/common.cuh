@@ -118,7 +118,8 @@ struct HubPlan {
   int64_t n_order = 0;
 };
 // fp32 row-range SpMM with segmented hub rows (spmm.cu)
-void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y, int64_t ldy,
+// returns the number of kernels launched
+int spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y, int64_t ldy,
               const float* sa, const int64_t* pa, const int32_t* ca, const float* aa,
               const int64_t* pb, const int32_t* cb, const float* ab, int64_t row_begin,
               int64_t n_rows, float* out, int64_t ldo, const HubPlan* hp, cudaStream_t s,

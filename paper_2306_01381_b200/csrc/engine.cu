@@ -378,9 +378,8 @@ class Engine final : public EngineBase {
            const int32_t* cb, const T* ab, int64_t r0, int64_t n, T* out, int64_t ldo,
            const HubPlan* hubs, const T* mask = nullptr, int64_t ldm = 0) {
     if constexpr (sizeof(T) == 4) {
-      spmm_f32(ctx_, int(round_up(dim, 4)), x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, r0, n, out,
-               ldo, hubs, s_main_, mask, ldm);
-      return 1 + (hubs && hubs->n_hubs > 0 ? 2 : 0);
+      return spmm_f32(ctx_, int(round_up(dim, 4)), x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, r0,
+                      n, out, ldo, hubs, s_main_, mask, ldm);
     } else {
       const int st = qgnn_csr_aggregate(ctx_, dtype_, dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb,
                                         ab, nullptr, r0, n, out, ldo, s_main_);

@@ -809,12 +809,12 @@ static bool grouped_narrow() {  // QGNN_SPMM_GROUPED=0 selects the one-row-per-w
 }
 
 // fp32 row-range SpMM with optional hub list (rows with > hub_deg neighbours).
-void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y, int64_t ldy,
+int spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y, int64_t ldy,
               const float* sa, const int64_t* pa, const int32_t* ca, const float* aa,
               const int64_t* pb, const int32_t* cb, const float* ab, int64_t row_begin,
               int64_t n_rows, float* out, int64_t ldo, const HubPlan* hp, cudaStream_t s,
               const float* mask, int64_t ldm) {
-  if (n_rows <= 0) return;
+  if (n_rows <= 0) return 0;
   const int nv = int(ceil_div(dim / 4, 32));
   const int64_t blocks = ceil_div(n_rows, 8);
   const bool hubs = hp && hp->n_hubs > 0;
@@ -849,7 +849,7 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
           dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask,
           ldm);
     check_launch("k_spmm_sorted");
-    return;
+    return 1 + (hp->n_hubs > 0 ? 1 : 0);
   }
   const int sw = split_wide();
   const int parts = nv == 1 ? 1 : (nv == 2 && dim % 8 == 0 && sw) ? (sw == 2 ? -2 : 2) : 0;
@@ -875,7 +875,7 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
             dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask,
             ldm);
       check_launch("k_spmm_f32g2");
-      return;
+      return 1 + (hubs ? (mg ? 1 : 2) : 0);
     }
     k_spmm_f32g<<<unsigned(blocks * np), 256, 0, s>>>(dim / np, x, ldx, y, ldy, sa, pa, ca, aa,
                                                       pb, cb, ab, row_begin, n_rows, out, ldo, hd,
@@ -892,7 +892,7 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
           ldm);
     }
     check_launch("k_spmm_f32g");
-    return;
+    return 1 + (hubs ? 2 : 0);
   }
   if (dim == 256 && wide_lean()) {
     const bool mg = hubs && merge_hubs();
@@ -909,7 +909,7 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
           ldm);
     }
     check_launch("k_spmm_wide");
-    return;
+    return 1 + (hubs ? (mg ? 1 : 2) : 0);
   }
   switch (nv) {
     QGNN_SPMM_CASE(1)
@@ -923,6 +923,7 @@ void spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* 
   }
 #undef QGNN_SPMM_CASE
   check_launch("k_spmm_f32");
+  return 1 + (hubs ? 2 : 0);
 }
 
 inline int pick_nv(int64_t nvec) {
