@@ -157,12 +157,25 @@ __device__ __forceinline__ float tf32_hi(float x) {
 // part needs no copy: kind::tf32 reads only the top 19 bits of each 32-bit
 // operand (verified bit-identical against an explicit truncated copy,
 // profiles/chk_tc_trunc.py), so the landed fp32 tile is used as hi in place.
-__device__ __forceinline__ void split_tile(const float4* buf, float4* lo, int n16, int t,
-                                           int nthr) {
+__device__ __forceinline__ void st_shared4(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ float4 ld_shared4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+// buf / lo: shared-space byte addresses (explicit ld/st.shared, not generic)
+__device__ __forceinline__ void split_tile(uint32_t buf, uint32_t lo, int n16, int t, int nthr) {
   for (int i = t; i < n16; i += nthr) {
-    const float4 v = buf[i];
-    lo[i] = make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z),
-                        v.w - tf32_hi(v.w));
+    const float4 v = ld_shared4(buf + 16u * uint32_t(i));
+    st_shared4(lo + 16u * uint32_t(i), make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y),
+                                                   v.z - tf32_hi(v.z), v.w - tf32_hi(v.w)));
   }
 }
 
@@ -371,7 +384,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int acc = acc0 + h;  // TMEM buffer: tile parity, or the tile's half
       const int row0 = m0 + 128 * h + 32 * q;  // this warp's 32 rows (TMEM lanes 32q..)
       float* out_base = p.out + (kMN ? int64_t(split) * p.M * p.N : 0);
-      float* st = stage_out + q * (32 * 36);
+      // explicit shared-space accesses (the uintptr-aligned base would otherwise
+      // compile to generic LD/ST)
+      const uint32_t st_s = smem_u32(stage_out + q * (32 * 36));
       // 32-column groups: TMEM -> registers (thread = row) -> ReLU / mask -> smem
       // -> registers (8 lanes = one 128-byte row segment) -> coalesced stores
       for (int c0 = 0; c0 < p.BN; c0 += 32) {
@@ -414,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               v.z = v.z > 0.f ? v.z : 0.f;
               v.w = v.w > 0.f ? v.w : 0.f;
             }
-            *reinterpret_cast<float4*>(st + lane * 36 + 16 * h + i) = v;
+            st_shared4(st_s + 4u * uint32_t(lane * 36 + 16 * h + i), v);
           }
         __syncwarp();
 #pragma unroll
@@ -422,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int rr = 4 * j + (lane >> 3);
           const int row = row0 + rr;
           if (row >= p.M || cc >= p.N) continue;
-          float4 v = *reinterpret_cast<const float4*>(st + rr * 36 + 4 * (lane & 7));
+          float4 v = ld_shared4(st_s + 4u * uint32_t(rr * 36 + 4 * (lane & 7)));
           if (p.mask) {
             v.x = mk[j].x > 0.f ? v.x : 0.f;
             v.y = mk[j].y > 0.f ? v.y : 0.f;
@@ -459,11 +474,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&full[s], ph);
         uint8_t* st = smem + s * stage_bytes;
         if (!(p.dbg & 4))
-          split_tile(reinterpret_cast<float4*>(st), reinterpret_cast<float4*>(st + a_bytes),
-                     a_bytes / 16, t, 128);
+          split_tile(smem_u32(st), smem_u32(st + a_bytes), a_bytes / 16, t, 128);
         if (kMN)
-          split_tile(reinterpret_cast<float4*>(st + 2 * a_bytes),
-                     reinterpret_cast<float4*>(st + 2 * a_bytes + b_bytes), b_bytes / 16, t, 128);
+          split_tile(smem_u32(st + 2 * a_bytes), smem_u32(st + 2 * a_bytes + b_bytes),
+                     b_bytes / 16, t, 128);
         fence_proxy_async();
         __syncwarp();
         if ((t & 31) == 0) mbar_arrive(&conv[s]);
