@@ -91,6 +91,18 @@ struct qgnn_ctx {
   void* gemm_b = nullptr;        // pre-split weight operand of the tcgen05 GEMM
   size_t gemm_b_bytes = 0;
   int num_sms = 148;
+  // Reuse of the pre-split weight operand across consecutive GEMMs with the same
+  // weights (the P partitions of one layer).  Opt-in: an owner that knows when its
+  // weights change (the engine: Adam step, set_weights) sets b_reuse and bumps
+  // wgen on every change; plain C-ABI callers always re-split.
+  bool b_reuse = false;
+  uint64_t wgen = 0;
+  struct {
+    const void* W = nullptr;
+    const void* buf = nullptr;
+    int wcols = 0, N = 0, K = 0, transpose = -1;
+    uint64_t gen = ~uint64_t{0};
+  } bprep;
 };
 
 namespace qgnn_b200 {

@@ -607,6 +607,7 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
   root_ = rng_seed_key(s.seed);
   QGNN_CUDA(cudaSetDevice(s.device));
   QGNN_REQUIRE(qgnn_ctx_create(s.device, &ctx_) == QGNN_OK, QGNN_ECUDA, qgnn_last_error());
+  ctx_->b_reuse = true;  // private ctx: weights change only in step() / set_weights (wgen)
   int lo_pri = 0, hi_pri = 0;
   QGNN_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
   QGNN_CUDA(cudaStreamCreateWithPriority(&s_main_, cudaStreamNonBlocking, lo_pri));
@@ -1724,6 +1725,7 @@ void Engine<T>::step() {
   // bias corrections of step adam_t_ were staged by launch_epoch (adam_bc_)
   adam_step_devbc(dtype_, w_.p, adam_m_.p, adam_v_.p, wsum_.p, nparams_, s_.lr, 0.9, 0.999, 1e-8,
                   adam_bc_.p, s_main_);
+  ++ctx_->wgen;  // the next GEMM re-splits the updated weights
   kend(QGNN_K_ELEMWISE, double(nparams_) * sizeof(T) * (P_ + 6), s_main_, 2);
 }
 
@@ -1736,6 +1738,7 @@ void Engine<T>::launch_epoch() {
   ++epoch_;
   QGNN_CUDA(cudaSetDevice(s_.device));
   launches_ = 0;
+  ++ctx_->wgen;  // replayed graphs update the weights without running step() on the host
   prepare_epoch();
   // Adam step t = epoch: bias corrections staged through pinned memory
   ++adam_t_;
@@ -2053,6 +2056,7 @@ void Engine<T>::set_weights(int l, const void* in) {
   QGNN_REQUIRE(l >= 0 && l < L_, QGNN_EINVAL, "set_weights: bad layer");
   QGNN_CUDA(cudaMemcpy(w_.p + woff_[l], in, dims_[l] * dims_[l + 1] * sizeof(T),
                        cudaMemcpyHostToDevice));
+  ++ctx_->wgen;
 }
 
 template <typename T>

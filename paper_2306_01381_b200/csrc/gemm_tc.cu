@@ -648,8 +648,15 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
   const int Kp = int(round_up(K, 4));
   float* bhi = static_cast<float*>(ctx_gemm_b(ctx, size_t(2) * BN * Kp * sizeof(float)));
   float* blo = bhi + size_t(BN) * Kp;
-  tc::k_prep_b<<<unsigned(ceil_div(int64_t(N) * Kp, 256)), 256, 0, s>>>(W, wcols, N, K, Kp,
-                                                                        transpose_w, bhi, blo);
+  auto& bp = ctx->bprep;
+  const bool reuse = ctx->b_reuse && bp.W == W && bp.buf == bhi && bp.wcols == wcols &&
+                     bp.N == N && bp.K == K && bp.transpose == transpose_w && bp.gen == ctx->wgen;
+  if (!reuse) {  // same stream as every GEMM that reuses it: ordered before them
+    tc::k_prep_b<<<unsigned(ceil_div(int64_t(N) * Kp, 256)), 256, 0, s>>>(W, wcols, N, K, Kp,
+                                                                          transpose_w, bhi, blo);
+    bp.W = W, bp.buf = bhi, bp.wcols = wcols, bp.N = N, bp.K = K, bp.transpose = transpose_w;
+    bp.gen = ctx->wgen;
+  }
   const int bk = gemm_bk();
   const CUtensorMapSwizzle swz = bk == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   const CUtensorMap ta = make_map(A, uint64_t(K), uint64_t(n_rows), uint64_t(lda), uint32_t(bk),
