@@ -453,6 +453,58 @@ __global__ void __launch_bounds__(256, MINB) k_quantize_pack_f32(
   }
 }
 
+// Payload of one message from the row in registers (lane l holds float4 chunks
+// c = l + 32 i): per element one counter draw and the branch-free fp64 decision,
+// flagged elements (~1e-12) recomputed exactly; zero padding to 16 bytes.
+template <int NV>
+__device__ __forceinline__ void encode_payload(const float (&v)[NV][4], int lane, int dim, int b,
+                                               double lo_d, float hi, double scale, double rcp,
+                                               double x_hi, uint64_t key, uint8_t* payload) {
+  const int nchunk = dim >> 2;
+  const uint32_t levels = (1u << b) - 1;
+  const bool constant = scale == 0.0;
+  const int padded = static_cast<int>(((packed_bytes(dim, b) + 15) / 16) * 16);
+  const int units = (padded * 2) >> (b == 8 ? 3 : b == 4 ? 2 : 1);
+  constexpr double tol = 0x1.0p-40;
+#pragma unroll
+  for (int i = 0; i < NV + 1; ++i) {
+    const int c = lane + 32 * i;
+    if (c >= units) break;
+    uint32_t word = 0;
+    if (i < NV && c < nchunk && !constant) {
+      const uint64_t z0 = key + static_cast<uint64_t>(4 * c + 1) * kPhi;
+      bool slow = false;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float hq = v[i][q];
+        const double a = __dsub_rn(static_cast<double>(hq), lo_d);
+        const double u = static_cast<double>(rng_mix(z0 + uint64_t(q) * kPhi) >> 11) * 0x1.0p-53;
+        const double x = hq == hi ? x_hi : __dmul_rn(a, rcp);
+        const double base = floor(x);
+        const double frac = __dsub_rn(x, base);
+        const uint32_t code = static_cast<uint32_t>(base) + (u < frac ? 1u : 0u);
+        word |= min(code, levels) << (q * b);
+        // x' within 2^-43 of x: the decision can only differ near a boundary;
+        // non-short-circuit: predicate logic instead of a branch per element
+        slow |= (hq != hi) & (a != 0.0) &
+                ((frac < tol) | (frac > 1.0 - tol) | (fabs(u - frac) < tol));
+      }
+      if (slow) {  // ~1e-12 per element: recompute the chunk exactly
+        const double lv = static_cast<double>(levels);
+        word = 0;
+        for (int q = 0; q < 4; ++q)
+          word |= quant_exact(v[i][q], lo_d, scale, lv, z0 + uint64_t(q) * kPhi) << (q * b);
+      }
+    }
+    if (b == 8)
+      reinterpret_cast<uint32_t*>(payload)[c] = word;
+    else if (b == 4)
+      reinterpret_cast<uint16_t*>(payload)[c] = static_cast<uint16_t>(word);
+    else
+      payload[c] = static_cast<uint8_t>(word);
+  }
+}
+
 // Lean variant for dim % 4 == 0 (every production width): the profile of the
 // general kernel showed the integer ALU pipe at 64 % with ~116 instructions per
 // element (bounds checks, compare/select chains, divergence bookkeeping).
@@ -544,51 +596,10 @@ __global__ void __launch_bounds__(256, MINB) k_quantize_pack_lean(
       h.w = static_cast<uint32_t>(b);
       *reinterpret_cast<uint4*>(chunk) = h;
     }
-    uint8_t* payload = chunk + kHdrGpu;
-    const int padded = static_cast<int>(((packed_bytes(dim, b) + 15) / 16) * 16);
-    const int units = (padded * 2) >> (b == 8 ? 3 : b == 4 ? 2 : 1);
     const uint64_t key = rng_fork(set_keys[set_of ? set_of[m] : 0], ids[m]);
     const double rcp = constant ? 0.0 : __drcp_rn(scale);
     const double x_hi = constant ? 0.0 : __ddiv_rn(__dsub_rn(hi_d, lo_d), scale);
-    constexpr double tol = 0x1.0p-40;
-#pragma unroll
-    for (int i = 0; i < NV + 1; ++i) {
-      const int c = lane + 32 * i;
-      if (c >= units) break;
-      uint32_t word = 0;
-      if (i < NV && c < nchunk && !constant) {
-        const uint64_t z0 = key + static_cast<uint64_t>(4 * c + 1) * kPhi;
-        bool slow = false;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float hq = v[i][q];
-          const double a = __dsub_rn(static_cast<double>(hq), lo_d);
-          const double u =
-              static_cast<double>(rng_mix(z0 + uint64_t(q) * kPhi) >> 11) * 0x1.0p-53;
-          const double x = hq == hi ? x_hi : __dmul_rn(a, rcp);
-          const double base = floor(x);
-          const double frac = __dsub_rn(x, base);
-          const uint32_t code = static_cast<uint32_t>(base) + (u < frac ? 1u : 0u);
-          word |= min(code, levels) << (q * b);
-          // x' within 2^-43 of x: the decision can only differ near a boundary
-          // non-short-circuit: predicate logic instead of a branch per element
-          slow |= (hq != hi) & (a != 0.0) &
-                  ((frac < tol) | (frac > 1.0 - tol) | (fabs(u - frac) < tol));
-        }
-        if (slow) {  // ~1e-12 per element: recompute the chunk exactly
-          const double lv = static_cast<double>(levels);
-          word = 0;
-          for (int q = 0; q < 4; ++q)
-            word |= quant_exact(v[i][q], lo_d, scale, lv, z0 + uint64_t(q) * kPhi) << (q * b);
-        }
-      }
-      if (b == 8)
-        reinterpret_cast<uint32_t*>(payload)[c] = word;
-      else if (b == 4)
-        reinterpret_cast<uint16_t*>(payload)[c] = static_cast<uint16_t>(word);
-      else
-        payload[c] = static_cast<uint8_t>(word);
-    }
+    encode_payload<NV>(v, lane, dim, b, lo_d, hi, scale, rcp, x_hi, key, chunk + kHdrGpu);
   }
 }
 
