@@ -19,6 +19,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <chrono>
 #include <cmath>
@@ -165,6 +166,8 @@ struct LoopGroup {
   uint64_t gen = 0;
   std::vector<void*> engines, ptr;
   std::vector<cudaEvent_t> ev, ev2;
+  // per rank: (peer, p, q, bytes) of its grouped sends / receives, in issue order
+  std::vector<std::vector<std::array<int64_t, 4>>> sends, recvs;
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
     const uint64_t g = gen;
@@ -636,6 +639,8 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
         g->ptr.assign(s.world, nullptr);
         g->ev.assign(s.world, nullptr);
         g->ev2.assign(s.world, nullptr);
+        g->sends.assign(s.world, {});
+        g->recvs.assign(s.world, {});
       }
       QGNN_REQUIRE(g->world == s.world && !g->engines[s.rank], QGNN_EPROTOCOL,
                    "loopback group: world mismatch or rank already registered");
@@ -1259,27 +1264,58 @@ void Engine<T>::exchange(int k) {
     kbegin(QGNN_K_EXCHANGE);
     QGNN_CUDA(cudaEventRecord(ev_pool_[ev_next_].first, s_comm_));
   }
+  // Grouped p2p schedule.  Inside one NCCL group the i-th send A->B is matched
+  // with the i-th receive B<-A, so both sides enumerate a rank pair's messages in
+  // the same (source partition p, destination partition q) order.
+  std::vector<std::array<int64_t, 4>> sends, recvs;  // (peer rank, p, q, bytes)
+  for (int64_t p = p0_; p < p1_; ++p)
+    for (int64_t q = 0; q < P_; ++q) {
+      if (q >= p0_ && q < p1_) continue;
+      const uint64_t nb = msgs_[k][p][q].bytes;
+      if (nb) sends.push_back({q / ppr, p, q, int64_t(nb)});
+    }
+  for (int64_t p = 0; p < P_; ++p) {
+    if (p >= p0_ && p < p1_) continue;
+    for (int64_t q = p0_; q < p1_; ++q) {
+      const uint64_t nb = msgs_[k][p][q].bytes;
+      if (nb) recvs.push_back({p / ppr, p, q, int64_t(nb)});
+    }
+  }
   double bytes = 0;
+  for (const auto& e : sends) bytes += double(e[3]);
   if (loop_) {
     LoopGroup& G = *loop_;
     G.ev[s_.rank] = ev_q_;
+    G.sends[s_.rank] = sends;
+    G.recvs[s_.rank] = recvs;
     G.barrier();  // every rank's K1 enqueued; its receive regions free after ev_q_
+    // the NCCL matching rule, checked for every rank pair (by every rank, so all
+    // ranks agree on the outcome): b's receives from a, in order, are exactly
+    // a's sends to b, in order
+    bool match = true;
+    for (int a = 0; a < s_.world; ++a)
+      for (int b = 0; b < s_.world; ++b) {
+        if (a == b) continue;
+        std::vector<std::array<int64_t, 4>> sent, got;
+        for (const auto& e : G.sends[a])
+          if (e[0] == b) sent.push_back({e[1], e[2], e[3], 0});
+        for (const auto& e : G.recvs[b])
+          if (e[0] == a) got.push_back({e[1], e[2], e[3], 0});
+        match &= sent == got;
+      }
     for (int r = 0; r < s_.world; ++r)
       if (r != s_.rank) QGNN_CUDA(cudaStreamWaitEvent(s_comm_, G.ev[r], 0));
-    for (int64_t p = p0_; p < p1_; ++p)
-      for (int64_t q = 0; q < P_; ++q) {
-        if (q == p || (q >= p0_ && q < p1_)) continue;
-        const uint64_t nb = msgs_[k][p][q].bytes;
-        if (!nb) continue;
-        auto* peer = static_cast<Engine<T>*>(G.engines[q / ppr]);
-        QGNN_CUDA(cudaMemcpyAsync(peer->arena_.p + peer->recv_base_[k][q][p],
-                                  arena_.p + send_base_[k][p][q], nb, cudaMemcpyDeviceToDevice,
-                                  s_comm_));
-        bytes += double(nb);
-      }
+    for (const auto& e : sends) {
+      auto* peer = static_cast<Engine<T>*>(G.engines[e[0]]);
+      QGNN_CUDA(cudaMemcpyAsync(peer->arena_.p + peer->recv_base_[k][e[2]][e[1]],
+                                arena_.p + send_base_[k][e[1]][e[2]], size_t(e[3]),
+                                cudaMemcpyDeviceToDevice, s_comm_));
+    }
     QGNN_CUDA(cudaEventRecord(ev_x_, s_comm_));
     G.ev2[s_.rank] = ev_x_;
-    G.barrier();  // all copies enqueued
+    G.barrier();  // all copies enqueued (and every rank done reading G.sends)
+    QGNN_REQUIRE(match, QGNN_EPROTOCOL,
+                 "exchange: grouped send/receive order differs between ranks");
     peer_x_.clear();
     for (int r = 0; r < s_.world; ++r)
       if (r != s_.rank) peer_x_.push_back(G.ev2[r]);
@@ -1287,23 +1323,12 @@ void Engine<T>::exchange(int k) {
     return;
   }
   QGNN_NCCL(nccl().GroupStart());
-  for (int64_t p = p0_; p < p1_; ++p)
-    for (int64_t q = 0; q < P_; ++q) {
-      if (q == p || (q >= p0_ && q < p1_)) continue;
-      const uint64_t nb = msgs_[k][p][q].bytes;
-      if (!nb) continue;
-      QGNN_NCCL(nccl().Send(arena_.p + send_base_[k][p][q], nb, ncclUint8, int(q / ppr), comm_,
-                            s_comm_));
-      bytes += double(nb);
-    }
-  for (int64_t q = p0_; q < p1_; ++q)
-    for (int64_t p = 0; p < P_; ++p) {
-      if (p == q || (p >= p0_ && p < p1_)) continue;
-      const uint64_t nb = msgs_[k][p][q].bytes;
-      if (!nb) continue;
-      QGNN_NCCL(nccl().Recv(arena_.p + recv_base_[k][q][p], nb, ncclUint8, int(p / ppr), comm_,
-                            s_comm_));
-    }
+  for (const auto& e : sends)
+    QGNN_NCCL(nccl().Send(arena_.p + send_base_[k][e[1]][e[2]], size_t(e[3]), ncclUint8,
+                          int(e[0]), comm_, s_comm_));
+  for (const auto& e : recvs)
+    QGNN_NCCL(nccl().Recv(arena_.p + recv_base_[k][e[2]][e[1]], size_t(e[3]), ncclUint8,
+                          int(e[0]), comm_, s_comm_));
   QGNN_NCCL(nccl().GroupEnd());
   kend(QGNN_K_EXCHANGE, bytes, s_comm_, 0);
   QGNN_CUDA(cudaEventRecord(ev_x_, s_comm_));
