@@ -140,6 +140,29 @@ def test_dense_f32_against_fp64(cuda, din, dout):
     assert torch.equal(wg, wg2)
 
 
+@pytest.mark.parametrize("n", [129, 300, 5121, 33000])
+@pytest.mark.parametrize("din,dout", [(100, 256), (256, 256), (256, 47), (47, 256)])
+def test_dense_f32_tile_edges(cuda, n, din, dout):
+    """Row counts around the tile grid: odd tile counts (the 2-CTA cluster path pads
+    the row tiles to a multiple of 2: the padding tile is TMA zero fill and must
+    not be stored), single tiles (no cluster), 256-row tiles for narrow outputs."""
+    rs = np.random.default_rng(n + din * 7 + dout)
+    a = rs.standard_normal((n, din))
+    w = rs.standard_normal((din, dout)) / np.sqrt(din)
+    f = torch.float32
+    out = torch.full((n + 200, dout), -3.0, dtype=f, device=cuda)
+    ops.dense_forward(_t(a, f), _t(w, f), out[:n], relu=True)
+    o = out.cpu().numpy()
+    assert np.allclose(o[:n], np.maximum(a @ w, 0), rtol=1e-4, atol=1e-4)
+    assert (o[n:] == -3.0).all()
+    ig = torch.full((n + 200, din), -3.0, dtype=f, device=cuda)
+    dz = rs.standard_normal((n, dout))
+    ops.dense_input_grad(_t(dz, f), _t(w, f), ig[:n])
+    g = ig.cpu().numpy()
+    assert np.allclose(g[:n], dz @ w.T, rtol=1e-4, atol=1e-4)
+    assert (g[n:] == -3.0).all()
+
+
 def test_dense_row_subsets(cuda):
     rs = np.random.default_rng(3)
     n, din, dout = 1000, 64, 48
