@@ -128,6 +128,9 @@ struct HubPlan {
   int64_t ldp = 0;
   const int32_t* order = nullptr;    // [n_order] non-hub rows of the range, degree-descending
   int64_t n_order = 0;
+  // in-kernel hub reduction: the last segment of a hub to finish reduces it
+  const int32_t* seg_hub = nullptr;  // [n_segs] hub index of each segment
+  int32_t* cnt = nullptr;            // [n_hubs] arrivals; zero between launches
 };
 // fp32 row-range SpMM with segmented hub rows (spmm.cu)
 // returns the number of kernels launched

@@ -314,7 +314,7 @@ class Engine final : public EngineBase {
     DBuf<double> ce_terms;
     // hub rows (slots) per SpMM call site, segmented (spmm.cu:k_spmm_hubseg)
     struct Hubs {
-      DBuf<int32_t> rows, seg_ptr, order;
+      DBuf<int32_t> rows, seg_ptr, order, seg_hub, cnt;
       DBuf<int64_t> seg;
       DBuf<float> part;
       HubPlan plan;
@@ -334,6 +334,7 @@ class Engine final : public EngineBase {
     constexpr int64_t kSeg = 256;
     std::vector<int32_t> rows, sptr{0};
     std::vector<int64_t> seg;
+    std::vector<int32_t> seg_hub;  // hub index of each segment
     std::vector<std::pair<int64_t, int32_t>> by_deg;  // (-degree, row) of the non-hub rows
     for (int64_t r = r0; r < r1; ++r) {
       const int64_t a0 = pa[r], a1 = pa[r + 1];
@@ -353,6 +354,7 @@ class Engine final : public EngineBase {
         seg.push_back(b0 + std::max<int64_t>(0, f - la));
       }
       sptr.push_back(int32_t(seg.size() / 4));
+      seg_hub.resize(seg.size() / 4, int32_t(rows.size() - 1));
     }
     // degree-descending row order for the multi-row narrow kernel (spmm.cu:k_spmm_sorted)
     std::sort(by_deg.begin(), by_deg.end());
@@ -361,6 +363,10 @@ class Engine final : public EngineBase {
     h.order.upload(order);
     h.plan.order = order.empty() ? nullptr : h.order.p;
     h.plan.n_order = int64_t(order.size());
+    h.seg_hub.upload(seg_hub);
+    h.cnt.alloc(std::max<size_t>(1, rows.size()));  // zeroed
+    h.plan.seg_hub = h.seg_hub.p;
+    h.plan.cnt = h.cnt.p;
     h.rows.upload(rows);
     h.seg_ptr.upload(sptr);
     h.seg.upload(seg);

@@ -371,6 +371,51 @@ __global__ void __launch_bounds__(256, 4) k_spmm_f32g(
   }
 }
 
+// In-kernel hub reduction (replaces the k_spmm_hubred launch).  A lane group of
+// G lanes has just stored segment u's partial row; after a fence its leader counts
+// the arrival, and the group that brings the last segment of hub h reduces it:
+// out[r] = x[r]·α_rr + Σ_s part[s] in segment order, masked — the same arithmetic
+// and order as k_spmm_hubred, so the result does not depend on which group does
+// it.  The counter is reset by that group for the next launch (stream order).
+// All 32 lanes must call this (it shuffles); `mine` marks lanes of a segment unit.
+__device__ __noinline__ void hub_finish(bool mine, int64_t u, int sub, int G, int leader,
+                                           int dim, const float* __restrict__ x, int64_t ldx,
+                                           const float* __restrict__ self_alpha,
+                                           const int32_t* __restrict__ hubs,
+                                           const int32_t* __restrict__ seg_ptr,
+                                           const int32_t* __restrict__ seg_hub,
+                                           int32_t* __restrict__ cnt,
+                                           const float* __restrict__ part, int64_t ldp,
+                                           float* __restrict__ out, int64_t ldo,
+                                           const float* __restrict__ mask, int64_t ldm) {
+  __threadfence();  // this lane's partial stores before the arrival count
+  __syncwarp();
+  int last = 0, h = 0;
+  if (mine && sub == 0) {
+    h = seg_hub[u];
+    last = atomicAdd(cnt + h, 1) == seg_ptr[h + 1] - seg_ptr[h] - 1;
+  }
+  last = __shfl_sync(0xffffffffu, last, leader & 31);
+  h = __shfl_sync(0xffffffffu, h, leader & 31);
+  if (!(mine && last)) return;
+  __threadfence();  // the other groups' partials (their fences precede their counts)
+  const int64_t r = hubs[h];
+  const float sa = self_alpha ? self_alpha[r] : 0.f;
+  const int s0 = seg_ptr[h], s1 = seg_ptr[h + 1];
+  for (int c = sub * 4; c < dim; c += 4 * G) {
+    float4 v = self_alpha ? *reinterpret_cast<const float4*>(x + r * ldx + c)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+    v.x *= sa, v.y *= sa, v.z *= sa, v.w *= sa;
+    for (int sg = s0; sg < s1; ++sg) {
+      const float4 p = __ldcg(reinterpret_cast<const float4*>(part + int64_t(sg) * ldp + c));
+      v.x += p.x, v.y += p.y, v.z += p.z, v.w += p.w;
+    }
+    if (mask) v = relu_mask4(v, mask + r * ldm + c);
+    *reinterpret_cast<float4*>(out + r * ldo + c) = v;
+  }
+  if (sub == 0) cnt[h] = 0;
+}
+
 // Narrow rows, two float4 per lane: G = ceil(F/2) lanes per row, E = 32/G
 // lane groups, 4 steps per round (8 loads per lane in flight).  Per step a
 // warp issues the same index shuffles and address math as k_spmm_f32g but moves
@@ -417,7 +462,8 @@ __global__ void __launch_bounds__(256, MINB) k_spmm_f32g2(
     const int32_t* __restrict__ cb, const float* __restrict__ ab, int64_t r0, int64_t n_rows,
     float* __restrict__ out, int64_t ldo, int64_t hub_deg, const float* __restrict__ mask,
     int64_t ldm, const int64_t* __restrict__ seg, int64_t n_segs, float* __restrict__ part,
-    int64_t ldp) {
+    int64_t ldp, const int32_t* __restrict__ hubs, const int32_t* __restrict__ seg_ptr,
+    const int32_t* __restrict__ seg_hub, int32_t* __restrict__ cnt) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int F = dim >> 2, G = (F + 1) >> 1, E = 32 / G;
   const int grp = lane / G, sub = lane - grp * G;
@@ -475,6 +521,9 @@ __global__ void __launch_bounds__(256, MINB) k_spmm_f32g2(
       *reinterpret_cast<float4*>(out + r * ldo + c) = o;
     }
   }
+  if (is_seg && cnt)  // warp-uniform: the whole warp worked on segment w
+    hub_finish(true, w, lane, 32, 0, dim, x, ldx, self_alpha, hubs, seg_ptr, seg_hub, cnt, part,
+               ldp, out, ldo, mask, ldm);
 }
 
 // Narrow rows (D <= 128), several rows per warp: G = ceil(F/2) lanes (two float4
@@ -527,7 +576,8 @@ __global__ void __launch_bounds__(64, MINB) k_spmm_sorted(
     const int32_t* __restrict__ cb, const float* __restrict__ ab,
     const int32_t* __restrict__ order, int64_t n_order, float* __restrict__ out, int64_t ldo,
     const float* __restrict__ mask, int64_t ldm, const int64_t* __restrict__ seg, int64_t n_segs,
-    float* __restrict__ part, int64_t ldp) {
+    float* __restrict__ part, int64_t ldp, const int32_t* __restrict__ hubs, const int32_t* __restrict__ seg_ptr,
+    const int32_t* __restrict__ seg_hub, int32_t* __restrict__ cnt) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int F = dim >> 2, G = (F + 1) >> 1, R = 32 / G;
   const int grp = lane / G, sub = lane - grp * G;
@@ -559,6 +609,16 @@ __global__ void __launch_bounds__(64, MINB) k_spmm_sorted(
   // all lanes stay for the shuffles; dead lanes load nothing (n = 0)
   sorted_gather(acc, x + cx, int(ldx), na, ma, ca + ea, aa + ea, has2, sub, grp * G);
   if (mb) sorted_gather(acc, y + cx, int(ldy), nb, mb, cb + eb, ab + eb, has2, sub, grp * G);
+  if (n_segs && cnt) {  // kernel-uniform: segment partials, then the in-kernel hub finish
+    const bool mine = live && is_seg;
+    if (mine) {
+      *reinterpret_cast<float4*>(part + u * ldp + cx) = acc[0];
+      if (has2) *reinterpret_cast<float4*>(part + u * ldp + cx + 4) = acc[1];
+    }
+    hub_finish(mine, u, sub, G, grp * G, dim, x, ldx, self_alpha, hubs, seg_ptr, seg_hub, cnt,
+               part, ldp, out, ldo, mask, ldm);
+    if (is_seg) return;
+  }
   if (!live) return;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -623,7 +683,8 @@ __global__ void __launch_bounds__(64, MINB) k_spmm_wide(
     const int32_t* __restrict__ cb, const float* __restrict__ ab, int64_t r0, int64_t n_rows,
     float* __restrict__ out, int64_t ldo, int64_t hub_deg, const float* __restrict__ mask,
     int64_t ldm, const int64_t* __restrict__ seg, int64_t n_segs, float* __restrict__ part,
-    int64_t ldp) {
+    int64_t ldp, const int32_t* __restrict__ hubs, const int32_t* __restrict__ seg_ptr,
+    const int32_t* __restrict__ seg_hub, int32_t* __restrict__ cnt) {
   // warps [0, n_segs) reduce hub segments into `part` (k_spmm_hubred finishes those
   // rows); they take the lowest block ids so the long lists start first and overlap
   // the ordinary rows instead of running as a separate tail launch
@@ -651,6 +712,9 @@ __global__ void __launch_bounds__(64, MINB) k_spmm_wide(
     float* dst = part + w * ldp + 4 * lane;
     *reinterpret_cast<float4*>(dst) = acc[0];
     *reinterpret_cast<float4*>(dst + 128) = acc[1];
+    if (cnt)
+      hub_finish(true, w, lane, 32, 0, 256, x, ldx, self_alpha, hubs, seg_ptr, seg_hub, cnt, part,
+                 ldp, out, ldo, mask, ldm);
     return;
   }
 #pragma unroll
@@ -798,6 +862,11 @@ static int sorted_max_dim() {  // widest rows sent to k_spmm_sorted (QGNN_SPMM_S
   return e ? std::atoi(e) : 64;
 }
 
+static bool hub_finish_inline() {  // QGNN_HUB_FINISH=0: hub rows reduced by k_spmm_hubred
+  const char* e = std::getenv("QGNN_HUB_FINISH");
+  return !e || std::atoi(e) != 0;
+}
+
 static bool merge_hubs() {  // QGNN_HUB_MERGE=0: hub segments as a separate k_spmm_hubseg launch
   const char* e = std::getenv("QGNN_HUB_MERGE");
   return !e || std::atoi(e) != 0;
@@ -836,20 +905,23 @@ int spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y
     const int64_t ns = hp->n_hubs > 0 ? hp->n_segs : 0;
     const int64_t units = ns + hp->n_order;
     const unsigned nb = unsigned(ceil_div(ceil_div(units, R), 2));
+    int32_t* cnt = ns && hp->cnt && hub_finish_inline() ? hp->cnt : nullptr;
     if (sorted_rows() == 2)
       k_spmm_sorted<16><<<nb, 64, 0, s>>>(dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab,
                                           hp->order, hp->n_order, out, ldo, mask, ldm, hp->seg, ns,
-                                          hp->part, hp->ldp);
+                                          hp->part, hp->ldp, hp->hubs, hp->seg_ptr, hp->seg_hub,
+                                          cnt);
     else
       k_spmm_sorted<12><<<nb, 64, 0, s>>>(dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab,
                                           hp->order, hp->n_order, out, ldo, mask, ldm, hp->seg, ns,
-                                          hp->part, hp->ldp);
-    if (hp->n_hubs > 0)
+                                          hp->part, hp->ldp, hp->hubs, hp->seg_ptr, hp->seg_hub,
+                                          cnt);
+    if (hp->n_hubs > 0 && !cnt)
       k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 64)), 64, 0, s>>>(
           dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask,
           ldm);
     check_launch("k_spmm_sorted");
-    return 1 + (hp->n_hubs > 0 ? 1 : 0);
+    return 1 + (hp->n_hubs > 0 && !cnt ? 1 : 0);
   }
   const int sw = split_wide();
   const int parts = nv == 1 ? 1 : (nv == 2 && dim % 8 == 0 && sw) ? (sw == 2 ? -2 : 2) : 0;
@@ -862,20 +934,26 @@ int spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y
         k_spmm_hubseg<1><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(
             dim, x, ldx, y, ldy, ca, aa, cb, ab, hp->seg, hp->n_segs, hp->part, hp->ldp);
       const unsigned nb2 = unsigned(ceil_div(ns + n_rows, spmm_tpb() / 32));
+      int32_t* cnt = ns && hp->cnt && hub_finish_inline() ? hp->cnt : nullptr;
+      const int32_t* hh = hubs ? hp->hubs : nullptr;
+      const int32_t* hsp = hubs ? hp->seg_ptr : nullptr;
+      const int32_t* hsh = hubs ? hp->seg_hub : nullptr;
       if (g2_minb() == 3)
         k_spmm_f32g2<3><<<nb2, spmm_tpb(), 0, s>>>(
             dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask,
-            ldm, hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0);
+            ldm, hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0, hh,
+            hsp, hsh, cnt);
       else
         k_spmm_f32g2<4><<<nb2, spmm_tpb(), 0, s>>>(
             dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask,
-            ldm, hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0);
-      if (hubs)
+            ldm, hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0, hh,
+            hsp, hsh, cnt);
+      if (hubs && !cnt)
         k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 64)), 64, 0, s>>>(
             dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask,
             ldm);
       check_launch("k_spmm_f32g2");
-      return 1 + (hubs ? (mg ? 1 : 2) : 0);
+      return 1 + (hubs ? (cnt ? 0 : mg ? 1 : 2) : 0);
     }
     k_spmm_f32g<<<unsigned(blocks * np), 256, 0, s>>>(dim / np, x, ldx, y, ldy, sa, pa, ca, aa,
                                                       pb, cb, ab, row_begin, n_rows, out, ldo, hd,
@@ -900,16 +978,18 @@ int spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y
     if (hubs && !mg)
       k_spmm_hubseg<2><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(
           dim, x, ldx, y, ldy, ca, aa, cb, ab, hp->seg, hp->n_segs, hp->part, hp->ldp);
+    int32_t* cnt = ns && hp->cnt && hub_finish_inline() ? hp->cnt : nullptr;
     k_spmm_wide<16><<<unsigned(ceil_div(ns + n_rows, 2)), 64, 0, s>>>(
         x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask, ldm,
-        hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0);
-    if (hubs) {
+        hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0,
+        hubs ? hp->hubs : nullptr, hubs ? hp->seg_ptr : nullptr, hubs ? hp->seg_hub : nullptr, cnt);
+    if (hubs && !cnt) {
       k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 64)), 64, 0, s>>>(
           dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask,
           ldm);
     }
     check_launch("k_spmm_wide");
-    return 1 + (hubs ? (mg ? 1 : 2) : 0);
+    return 1 + (hubs ? (cnt ? 0 : mg ? 1 : 2) : 0);
   }
   switch (nv) {
     QGNN_SPMM_CASE(1)
