@@ -139,8 +139,17 @@ __global__ void k_splitk_reduce(const float* __restrict__ part, int splits, int6
                                 float* __restrict__ out, int accumulate) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= mn) return;
+  // the adds stay in z order (bit-identical); unrolling keeps 8 loads in flight
   float s = 0.f;
-  for (int z = 0; z < splits; ++z) s += part[static_cast<int64_t>(z) * mn + i];
+  int z = 0;
+  for (; z + 8 <= splits; z += 8) {
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __ldcs(part + static_cast<int64_t>(z + j) * mn + i);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += v[j];
+  }
+  for (; z < splits; ++z) s += __ldcs(part + static_cast<int64_t>(z) * mn + i);
   out[i] = accumulate ? out[i] + s : s;
 }
 
