@@ -405,9 +405,12 @@ class Engine final : public EngineBase {
   // one GPU: encode / decode on the side stream, overlapping the compute stream
   // (per-kernel timing runs serialised so each class's time is its own)
   bool side_overlap() const { return s_.world == 1 && side_enabled() && !s_.kstats; }
+  // K1/K3 on a side stream alongside the central rows (QGNN_SIDE_STREAM=1).  Off by
+  // default since the SpMM/GEMM kernels saturate the GPU: in the captured graph the
+  // concurrent encode/decode cost 1.6 ms/epoch more than running it in line.
   static bool side_enabled() {
     const char* e = std::getenv("QGNN_SIDE_STREAM");
-    return !e || std::atoi(e) != 0;
+    return e && std::atoi(e) != 0;
   }
   void fork_side() {  // s_comm_ continues after everything queued on s_main_
     QGNN_CUDA(cudaEventRecord(ev_fork_, s_main_));

@@ -151,6 +151,19 @@ def test_engine_sorted_narrow_rows_match(cuda, monkeypatch, hub_deg):
     assert not (ws == wg).all()
 
 
+@pytest.mark.parametrize("graph", ["0", "1"])
+def test_side_stream_is_identical(cuda, monkeypatch, graph):
+    """K1/K3 on the side stream (QGNN_SIDE_STREAM=1, overlapped with the central rows)
+    give bit-identical training to the in-line schedule."""
+    monkeypatch.setenv("QGNN_GRAPH", graph)
+    monkeypatch.setenv("QGNN_SIDE_STREAM", "0")
+    a, wa = _run("fixed", 4, 4, "f32")
+    monkeypatch.setenv("QGNN_SIDE_STREAM", "1")
+    b, wb = _run("fixed", 4, 4, "f32")
+    assert [m["train_loss"] for m in a] == [m["train_loss"] for m in b]
+    assert (wa == wb).all()
+
+
 def test_engine_transform_first_last_layer(cuda, monkeypatch):
     """z = A(hW) for the narrowing last layer matches aggregate-then-transform (fp32)."""
     tf, wt = _run("fixed", 4, 4, "f32")
