@@ -263,6 +263,11 @@ class Engine final : public EngineBase {
   void epoch_body();
   DBuf<double> adam_bc_;  // [2] bias corrections of this epoch's step
   double* adam_bc_host_ = nullptr;
+  // adaptive re-solve: trace windows of all keys gathered here once per period
+  // (persistent device buffer for the cross-rank gather, pinned host copy)
+  DBuf<T> win_dev_;
+  T* win_host_ = nullptr;
+  size_t win_cap_ = 0;
   void set_features(const void* f) override;
   void get_weights(int l, void* out) override;
   void set_weights(int l, const void* in) override;
@@ -883,6 +888,7 @@ Engine<T>::~Engine() {
   for (auto& g : graphs_)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (adam_bc_host_) cudaFreeHost(adam_bc_host_);
+  if (win_host_) cudaFreeHost(win_host_);
   for (auto e : ev_feat_)
     if (e) cudaEventDestroy(e);
   if (ev_feat_free_) cudaEventDestroy(ev_feat_free_);
@@ -1926,11 +1932,10 @@ template <typename T>
 void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
   if (s_.period <= 0 || epoch_ % uint64_t(s_.period) != 0) return;
   const auto t0 = std::chrono::steady_clock::now();
-  // windows of every sender partition (all ranks)
-  std::vector<std::vector<std::vector<double>>> wlo(keys_.size()), whi(keys_.size());
+  // windows of every sender partition (all ranks): key k's lo values of partition p
+  // at win_host_[koff[k] + p * stride[k] + i], its hi values half a buffer later
+  std::vector<int64_t> stride(keys_.size()), koff(keys_.size() + 1, 0);
   for (size_t k = 0; k < keys_.size(); ++k) {
-    wlo[k].assign(P_, {});
-    whi[k].assign(P_, {});
     int64_t maxn = 0;
     for (int64_t p = 0; p < P_; ++p) {
       int64_t n = 0;
@@ -1938,31 +1943,44 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
         if (q != p) n += int64_t(msgs_[k][p][q].ids.size());
       maxn = std::max(maxn, n);
     }
+    stride[k] = std::max<int64_t>(1, maxn);
+    koff[k + 1] = koff[k] + P_ * stride[k];
+  }
+  const size_t half = size_t(koff[keys_.size()]);
+  if (win_cap_ < 2 * half) {  // grows once (message lists are fixed after setup)
+    if (win_host_) QGNN_CUDA(cudaFreeHost(win_host_));
+    QGNN_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&win_host_), 2 * half * sizeof(T),
+                            cudaHostAllocDefault));
+    if (s_.world > 1) win_dev_.alloc(2 * half, false);
+    win_cap_ = 2 * half;
+  }
+  for (size_t k = 0; k < keys_.size(); ++k) {
     const int64_t ppr = P_ / s_.world;
-    std::vector<T> lo_all(P_ * std::max<int64_t>(1, maxn)), hi_all(lo_all.size());
-    DBuf<T> dlo, dhi;
-    dlo.alloc(lo_all.size());
-    dhi.alloc(lo_all.size());
-    const int64_t stride = std::max<int64_t>(1, maxn);
     for (auto& up : parts_dev_) {
       auto& S = up->snd[k];
-      if (S.n) {
-        QGNN_CUDA(cudaMemcpyAsync(dlo.p + up->id * stride, S.wlo.p, S.n * sizeof(T),
+      if (!S.n) continue;
+      const size_t o = size_t(koff[k] + up->id * stride[k]);
+      if (s_.world == 1) {  // straight into the pinned host copy
+        QGNN_CUDA(cudaMemcpyAsync(win_host_ + o, S.wlo.p, S.n * sizeof(T), cudaMemcpyDeviceToHost,
+                                  s_main_));
+        QGNN_CUDA(cudaMemcpyAsync(win_host_ + half + o, S.whi.p, S.n * sizeof(T),
+                                  cudaMemcpyDeviceToHost, s_main_));
+      } else {
+        QGNN_CUDA(cudaMemcpyAsync(win_dev_.p + o, S.wlo.p, S.n * sizeof(T),
                                   cudaMemcpyDeviceToDevice, s_main_));
-        QGNN_CUDA(cudaMemcpyAsync(dhi.p + up->id * stride, S.whi.p, S.n * sizeof(T),
+        QGNN_CUDA(cudaMemcpyAsync(win_dev_.p + half + o, S.whi.p, S.n * sizeof(T),
                                   cudaMemcpyDeviceToDevice, s_main_));
       }
     }
-    allgather_dev(dlo.p, ppr * stride, s_main_);
-    allgather_dev(dhi.p, ppr * stride, s_main_);
-    QGNN_CUDA(cudaStreamSynchronize(s_main_));
-    QGNN_CUDA(cudaMemcpy(lo_all.data(), dlo.p, lo_all.size() * sizeof(T), cudaMemcpyDeviceToHost));
-    QGNN_CUDA(cudaMemcpy(hi_all.data(), dhi.p, hi_all.size() * sizeof(T), cudaMemcpyDeviceToHost));
-    for (int64_t p = 0; p < P_; ++p) {
-      wlo[k][p].assign(lo_all.begin() + p * stride, lo_all.begin() + (p + 1) * stride);
-      whi[k][p].assign(hi_all.begin() + p * stride, hi_all.begin() + (p + 1) * stride);
+    if (s_.world > 1) {
+      allgather_dev(win_dev_.p + koff[k], ppr * stride[k], s_main_);
+      allgather_dev(win_dev_.p + half + koff[k], ppr * stride[k], s_main_);
     }
   }
+  if (s_.world > 1)
+    QGNN_CUDA(cudaMemcpyAsync(win_host_, win_dev_.p, 2 * half * sizeof(T), cudaMemcpyDeviceToHost,
+                              s_main_));
+  QGNN_CUDA(cudaStreamSynchronize(s_main_));
   const auto t_win = std::chrono::steady_clock::now();
   // per key: stats -> group_and_order -> solve_assignment, concurrently (solve.hpp:343-350)
   Cost cm;
@@ -1989,8 +2007,9 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
           ps.src = uint32_t(p);
           ps.dst = uint32_t(q);
           for (size_t i = 0; i < m.ids.size(); ++i) {
-            const double lo = double(wlo[k][p][mb + int64_t(i)]);
-            const double hi = double(whi[k][p][mb + int64_t(i)]);
+            const size_t w = size_t(koff[k] + p * stride[k] + mb + int64_t(i));
+            const double lo = double(win_host_[w]);
+            const double hi = double(win_host_[half + w]);
             if (!(hi >= lo)) continue;  // traced (trace.hpp:93)
             MsgStat st;
             st.id = m.ids[i];
@@ -2023,7 +2042,6 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
       return r;
     });
   }
-  const auto t_stats = std::chrono::steady_clock::now();
   // adopt: new bits for every message (all-8 default for untraced / absent pairs),
   // one host thread per key; then the wire layout and the device metadata
   ++plan_version_;
@@ -2050,8 +2068,10 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
           if (p != q) layout_pair(int(k), int(p), int(q));
     });
   for (auto& f : adopt) f.get();
+  const auto t_adopt = std::chrono::steady_clock::now();
   bits_dirty_ = true;
   arena_layout();
+  const auto t_arena = std::chrono::steady_clock::now();
   std::vector<std::future<void>> meta(keys_.size());
   for (size_t k = 0; k < keys_.size(); ++k)
     meta[k] = std::async(std::launch::async, [&, k] {
@@ -2059,6 +2079,7 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
       upload_key_meta(int(k));
     });
   for (auto& f : meta) f.get();
+  const auto t_meta = std::chrono::steady_clock::now();
   for (size_t k = 0; k < keys_.size(); ++k) {
     for (auto& up : parts_dev_) {  // reset windows (engine.hpp:855-860)
       auto& S = up->snd[k];
@@ -2071,9 +2092,13 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
   resolve_seconds_ =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (std::getenv("QGNN_RESOLVE_PROFILE"))
-    std::fprintf(stderr, "[resolve] windows %.3f s, stats %.3f s, total %.3f s\n",
+    std::fprintf(stderr,
+                 "[resolve] windows %.3f s, solve+adopt %.3f s, arena %.3f s, upload %.3f s, "
+                 "total %.3f s\n",
                  std::chrono::duration<double>(t_win - t0).count(),
-                 std::chrono::duration<double>(t_stats - t_win).count(), resolve_seconds_);
+                 std::chrono::duration<double>(t_adopt - t_win).count(),
+                 std::chrono::duration<double>(t_arena - t_adopt).count(),
+                 std::chrono::duration<double>(t_meta - t_arena).count(), resolve_seconds_);
 }
 
 template <typename T>

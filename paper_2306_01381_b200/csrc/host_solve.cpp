@@ -200,9 +200,10 @@ SolveResult group_and_order(const std::vector<PairStat>& pairs, int64_t group_si
       QGNN_REQUIRE(m.asq > 0.0, QGNN_EINVAL, "stats: sum_alpha_sq must be > 0");
     }
   }
-  SolveResult plan;
-  for (const PairStat& p : pairs) {
-    if (p.msgs.empty()) continue;
+  // pairs are independent: grouped on worker threads, kept in input order
+  std::vector<PlanPairG> out(pairs.size());
+  auto one = [&](size_t pi) {
+    const PairStat& p = pairs[pi];
     std::vector<std::pair<double, const MsgStat*>> order;
     order.reserve(p.msgs.size());
     for (const MsgStat& m : p.msgs) order.emplace_back(compute_beta(m), &m);
@@ -222,8 +223,24 @@ SolveResult group_and_order(const std::vector<PairStat>& pairs, int64_t group_si
       }
       pp.groups.push_back(std::move(g));
     }
-    plan.pairs.push_back(std::move(pp));
-  }
+    out[pi] = std::move(pp);
+  };
+  size_t nthr = std::max<size_t>(1, std::min<size_t>(pairs.size(),
+                                                      std::thread::hardware_concurrency() / 2));
+  if (const char* e = std::getenv("QGNN_SOLVE_THREADS"))
+    nthr = std::max<size_t>(1, std::min<size_t>(pairs.size(), size_t(std::atoi(e))));
+  std::atomic<size_t> next{0};
+  auto worker = [&] {
+    for (size_t i; (i = next.fetch_add(1)) < pairs.size();)
+      if (!pairs[i].msgs.empty()) one(i);
+  };
+  std::vector<std::thread> th;
+  for (size_t t = 1; t < nthr; ++t) th.emplace_back(worker);
+  worker();
+  for (auto& t : th) t.join();
+  SolveResult plan;
+  for (size_t i = 0; i < pairs.size(); ++i)
+    if (!pairs[i].msgs.empty()) plan.pairs.push_back(std::move(out[i]));
   return plan;
 }
 
