@@ -2017,6 +2017,7 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
             st.lo = lo;
             st.hi = hi;
             st.asq = keys_[k].bwd ? 1.0 : rx_asq_[p][q][i];
+            st.pos = uint32_t(i);
             ps.msgs.push_back(st);
           }
           mb += int64_t(m.ids.size());
@@ -2057,10 +2058,7 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
         for (const PlanPairG& pp : r.pairs) {
           PairMsgs& m = msgs_[k][pp.src][pp.dst];
           for (const Group& g : pp.groups)
-            for (uint32_t id : g.ids) {
-              auto it = std::lower_bound(m.ids.begin(), m.ids.end(), id);
-              m.bits[it - m.ids.begin()] = uint8_t(g.bits);
-            }
+            for (uint32_t i : g.pos) m.bits[i] = uint8_t(g.bits);  // stats carried positions
         }
       }
       for (int64_t p = 0; p < P_; ++p)

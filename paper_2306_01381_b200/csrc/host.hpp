@@ -70,6 +70,7 @@ struct MsgStat {
   uint32_t id = 0;
   uint64_t dim = 0;
   double lo = 0, hi = 0, asq = 0;
+  uint32_t pos = 0;  // caller's index of the message (carried into Group::pos)
 };
 struct PairStat {
   uint32_t src = 0, dst = 0;
@@ -77,6 +78,7 @@ struct PairStat {
 };
 struct Group {
   std::vector<uint32_t> ids;
+  std::vector<uint32_t> pos;  // MsgStat::pos of each id
   std::vector<uint64_t> dims;
   double beta = 0;
   int bits = 8;

@@ -218,6 +218,7 @@ SolveResult group_and_order(const std::vector<PairStat>& pairs, int64_t group_si
       Group g;
       for (size_t j = i; j < std::min(order.size(), i + static_cast<size_t>(group_size)); ++j) {
         g.ids.push_back(order[j].second->id);
+        g.pos.push_back(order[j].second->pos);
         g.dims.push_back(order[j].second->dim);
         g.beta += order[j].first;
       }
