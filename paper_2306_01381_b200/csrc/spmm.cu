@@ -371,6 +371,14 @@ __global__ void __launch_bounds__(256, 4) k_spmm_f32g(
   }
 }
 
+// 32-byte read-only load (LDG.E.256 on sm_100): two consecutive float4 of a row
+__device__ __forceinline__ void ldg256(const float* p, float4& a, float4& b) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z),
+                 "=f"(b.w)
+               : "l"(p));
+}
+
 // In-kernel hub reduction (replaces the k_spmm_hubred launch).  A lane group of
 // G lanes has just stored segment u's partial row; after a fence its leader counts
 // the arrival, and the group that brings the last segment of hub h reduces it:
@@ -424,7 +432,7 @@ __device__ __noinline__ void hub_finish(bool mine, int64_t u, int sub, int G, in
 __device__ __forceinline__ void grp2_gather(float4 (&acc)[2], const float* __restrict__ src,
                                             int ld, int n, const int32_t* __restrict__ col,
                                             const float* __restrict__ alpha, int lane, int grp,
-                                            int E, bool act, bool has2) {
+                                            int E, bool act, bool has2, bool v8) {
   for (int e0 = 0; e0 < n; e0 += 32) {
     const int cnt = min(32, n - e0);
     int my_c = 0;
@@ -441,8 +449,15 @@ __device__ __forceinline__ void grp2_gather(float4 (&acc)[2], const float* __res
         const int c = __shfl_sync(0xffffffffu, my_c, k & 31);
         const bool ok = act && k < cnt;
         const float4* p = reinterpret_cast<const float4*>(src + int64_t(c) * ld);
-        v[u][0] = ok ? __ldg(p) : make_float4(0.f, 0.f, 0.f, 0.f);
-        v[u][1] = (ok && has2) ? __ldg(p + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[u][0] = v[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ok) {
+          if (v8 && has2) {  // adjacent float4 pair: one 32-byte load
+            ldg256(reinterpret_cast<const float*>(p), v[u][0], v[u][1]);
+          } else {
+            v[u][0] = __ldg(p);
+            if (has2) v[u][1] = __ldg(p + 1);
+          }
+        }
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -463,7 +478,7 @@ __global__ void __launch_bounds__(256, MINB) k_spmm_f32g2(
     float* __restrict__ out, int64_t ldo, int64_t hub_deg, const float* __restrict__ mask,
     int64_t ldm, const int64_t* __restrict__ seg, int64_t n_segs, float* __restrict__ part,
     int64_t ldp, const int32_t* __restrict__ hubs, const int32_t* __restrict__ seg_ptr,
-    const int32_t* __restrict__ seg_hub, int32_t* __restrict__ cnt) {
+    const int32_t* __restrict__ seg_hub, int32_t* __restrict__ cnt, bool v8) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int F = dim >> 2, G = (F + 1) >> 1, E = 32 / G;
   const int grp = lane / G, sub = lane - grp * G;
@@ -485,10 +500,10 @@ __global__ void __launch_bounds__(256, MINB) k_spmm_f32g2(
   }
   float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
   const int cx = sub * 8;  // first float of this lane's two columns
-  grp2_gather(acc, x + cx, int(ldx), na, ca + ea0, aa + ea0, lane, grp, E, act, has2);
+  grp2_gather(acc, x + cx, int(ldx), na, ca + ea0, aa + ea0, lane, grp, E, act, has2, v8);
   if (nb) {  // b range start re-read here rather than held across the first gather
     const int64_t eb0 = is_seg ? seg[4 * w + 2] : pb[r];
-    grp2_gather(acc, y + cx, int(ldy), nb, cb + eb0, ab + eb0, lane, grp, E, act, has2);
+    grp2_gather(acc, y + cx, int(ldy), nb, cb + eb0, ab + eb0, lane, grp, E, act, has2, v8);
   }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -537,7 +552,7 @@ __device__ __forceinline__ void sorted_gather(float4 (&acc)[2], const float* __r
                                               int ld, int n, int nmax,
                                               const int32_t* __restrict__ col,
                                               const float* __restrict__ alpha, bool has2,
-                                              int sub, int base) {
+                                              int sub, int base, bool v8) {
   for (int j = 0; j < nmax; j += 4) {
     // lanes 0..3 of the group load the step's 4 edge indices, the group shuffles them
     int my_c = 0;
@@ -556,8 +571,12 @@ __device__ __forceinline__ void sorted_gather(float4 (&acc)[2], const float* __r
       const float4* p = reinterpret_cast<const float4*>(src + int64_t(c[u]) * ld);
       v[u][0] = v[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (j + u < n) {
-        v[u][0] = __ldg(p);
-        if (has2) v[u][1] = __ldg(p + 1);
+        if (v8 && has2) {  // the lane's two float4 are adjacent: one 32-byte load
+          ldg256(reinterpret_cast<const float*>(p), v[u][0], v[u][1]);
+        } else {
+          v[u][0] = __ldg(p);
+          if (has2) v[u][1] = __ldg(p + 1);
+        }
       }
     }
 #pragma unroll
@@ -577,7 +596,7 @@ __global__ void __launch_bounds__(64, MINB) k_spmm_sorted(
     const int32_t* __restrict__ order, int64_t n_order, float* __restrict__ out, int64_t ldo,
     const float* __restrict__ mask, int64_t ldm, const int64_t* __restrict__ seg, int64_t n_segs,
     float* __restrict__ part, int64_t ldp, const int32_t* __restrict__ hubs, const int32_t* __restrict__ seg_ptr,
-    const int32_t* __restrict__ seg_hub, int32_t* __restrict__ cnt) {
+    const int32_t* __restrict__ seg_hub, int32_t* __restrict__ cnt, bool v8) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int F = dim >> 2, G = (F + 1) >> 1, R = 32 / G;
   const int grp = lane / G, sub = lane - grp * G;
@@ -607,8 +626,8 @@ __global__ void __launch_bounds__(64, MINB) k_spmm_sorted(
   float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
   const int cx = sub * 8;
   // all lanes stay for the shuffles; dead lanes load nothing (n = 0)
-  sorted_gather(acc, x + cx, int(ldx), na, ma, ca + ea, aa + ea, has2, sub, grp * G);
-  if (mb) sorted_gather(acc, y + cx, int(ldy), nb, mb, cb + eb, ab + eb, has2, sub, grp * G);
+  sorted_gather(acc, x + cx, int(ldx), na, ma, ca + ea, aa + ea, has2, sub, grp * G, v8);
+  if (mb) sorted_gather(acc, y + cx, int(ldy), nb, mb, cb + eb, ab + eb, has2, sub, grp * G, v8);
   if (n_segs && cnt) {  // kernel-uniform: segment partials, then the in-kernel hub finish
     const bool mine = live && is_seg;
     if (mine) {
@@ -644,6 +663,7 @@ __global__ void __launch_bounds__(64, MINB) k_spmm_sorted(
 // edge offsets within the row (pointers rebased once per row), no per-lane column
 // bounds, alphas shuffled after the loads — to fit 64 registers (32 warps/SM)
 // with the same 8 gathers per lane in flight as k_spmm_f32<2>.
+template <bool V8>
 __device__ __forceinline__ void wide_gather(float4 (&acc)[2], const float* __restrict__ src,
                                             int ld, int n, const int32_t* __restrict__ col,
                                             const float* __restrict__ alpha, int lane) {
@@ -660,10 +680,15 @@ __device__ __forceinline__ void wide_gather(float4 (&acc)[2], const float* __res
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int c = __shfl_sync(0xffffffffu, my_c, (j + u) & 31);
-        const float4* p = reinterpret_cast<const float4*>(src + int64_t(c) * ld) + lane;
         const bool ok = j + u < cnt;
-        v[u][0] = ok ? __ldg(p) : make_float4(0.f, 0.f, 0.f, 0.f);
-        v[u][1] = ok ? __ldg(p + 32) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (V8) {  // lane owns columns 8 lane .. 8 lane + 7: one 32-byte load
+          v[u][0] = v[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (ok) ldg256(src + int64_t(c) * ld + 8 * lane, v[u][0], v[u][1]);
+        } else {
+          const float4* p = reinterpret_cast<const float4*>(src + int64_t(c) * ld) + lane;
+          v[u][0] = ok ? __ldg(p) : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[u][1] = ok ? __ldg(p + 32) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -675,7 +700,7 @@ __device__ __forceinline__ void wide_gather(float4 (&acc)[2], const float* __res
   }
 }
 
-template <int MINB>
+template <int MINB, bool V8>
 __global__ void __launch_bounds__(64, MINB) k_spmm_wide(
     const float* __restrict__ x, int64_t ldx, const float* __restrict__ y, int64_t ldy,
     const float* __restrict__ self_alpha, const int64_t* __restrict__ pa,
@@ -703,15 +728,15 @@ __global__ void __launch_bounds__(64, MINB) k_spmm_wide(
     if (na + nb > hub_deg) return;  // segments + k_spmm_hubred
   }
   float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
-  wide_gather(acc, x, int(ldx), na, ca + ea, aa + ea, lane);
+  wide_gather<V8>(acc, x, int(ldx), na, ca + ea, aa + ea, lane);
   if (nb) {  // b range start re-read here rather than held across the first gather
     const int64_t eb = is_seg ? seg[4 * w + 2] : pb[r];
-    wide_gather(acc, y, int(ldy), nb, cb + eb, ab + eb, lane);
+    wide_gather<V8>(acc, y, int(ldy), nb, cb + eb, ab + eb, lane);
   }
   if (is_seg) {
-    float* dst = part + w * ldp + 4 * lane;
-    *reinterpret_cast<float4*>(dst) = acc[0];
-    *reinterpret_cast<float4*>(dst + 128) = acc[1];
+    float* dst = part + w * ldp;
+    *reinterpret_cast<float4*>(dst + (V8 ? 8 * lane : 4 * lane)) = acc[0];
+    *reinterpret_cast<float4*>(dst + (V8 ? 8 * lane + 4 : 4 * lane + 128)) = acc[1];
     if (cnt)
       hub_finish(true, w, lane, 32, 0, 256, x, ldx, self_alpha, hubs, seg_ptr, seg_hub, cnt, part,
                  ldp, out, ldo, mask, ldm);
@@ -719,7 +744,7 @@ __global__ void __launch_bounds__(64, MINB) k_spmm_wide(
   }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const int c = 4 * (lane + 32 * h);
+    const int c = V8 ? 8 * lane + 4 * h : 4 * (lane + 32 * h);
     float4 o = acc[h];
     if (self_alpha) {
       const float sa = self_alpha[r];
@@ -867,6 +892,11 @@ static bool hub_finish_inline() {  // QGNN_HUB_FINISH=0: hub rows reduced by k_s
   return !e || std::atoi(e) != 0;
 }
 
+static bool load256() {  // QGNN_SPMM_LD256=0: 16-byte gathers only
+  const char* e = std::getenv("QGNN_SPMM_LD256");
+  return !e || std::atoi(e) != 0;
+}
+
 static bool merge_hubs() {  // QGNN_HUB_MERGE=0: hub segments as a separate k_spmm_hubseg launch
   const char* e = std::getenv("QGNN_HUB_MERGE");
   return !e || std::atoi(e) != 0;
@@ -906,16 +936,18 @@ int spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y
     const int64_t units = ns + hp->n_order;
     const unsigned nb = unsigned(ceil_div(ceil_div(units, R), 2));
     int32_t* cnt = ns && hp->cnt && hub_finish_inline() ? hp->cnt : nullptr;
+    const bool v8 = load256() && (reinterpret_cast<uintptr_t>(x) & 31) == 0 && ldx % 8 == 0 &&
+                    (!y || ((reinterpret_cast<uintptr_t>(y) & 31) == 0 && ldy % 8 == 0));
     if (sorted_rows() == 2)
       k_spmm_sorted<16><<<nb, 64, 0, s>>>(dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab,
                                           hp->order, hp->n_order, out, ldo, mask, ldm, hp->seg, ns,
                                           hp->part, hp->ldp, hp->hubs, hp->seg_ptr, hp->seg_hub,
-                                          cnt);
+                                          cnt, v8);
     else
       k_spmm_sorted<12><<<nb, 64, 0, s>>>(dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab,
                                           hp->order, hp->n_order, out, ldo, mask, ldm, hp->seg, ns,
                                           hp->part, hp->ldp, hp->hubs, hp->seg_ptr, hp->seg_hub,
-                                          cnt);
+                                          cnt, v8);
     if (hp->n_hubs > 0 && !cnt)
       k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 64)), 64, 0, s>>>(
           dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask,
@@ -938,16 +970,18 @@ int spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y
       const int32_t* hh = hubs ? hp->hubs : nullptr;
       const int32_t* hsp = hubs ? hp->seg_ptr : nullptr;
       const int32_t* hsh = hubs ? hp->seg_hub : nullptr;
+      const bool v8 = load256() && (reinterpret_cast<uintptr_t>(x) & 31) == 0 && ldx % 8 == 0 &&
+                      (!y || ((reinterpret_cast<uintptr_t>(y) & 31) == 0 && ldy % 8 == 0));
       if (g2_minb() == 3)
         k_spmm_f32g2<3><<<nb2, spmm_tpb(), 0, s>>>(
             dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask,
             ldm, hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0, hh,
-            hsp, hsh, cnt);
+            hsp, hsh, cnt, v8);
       else
         k_spmm_f32g2<4><<<nb2, spmm_tpb(), 0, s>>>(
             dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask,
             ldm, hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0, hh,
-            hsp, hsh, cnt);
+            hsp, hsh, cnt, v8);
       if (hubs && !cnt)
         k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 64)), 64, 0, s>>>(
             dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask,
@@ -979,10 +1013,21 @@ int spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y
       k_spmm_hubseg<2><<<unsigned(ceil_div(hp->n_segs * 32, 256)), 256, 0, s>>>(
           dim, x, ldx, y, ldy, ca, aa, cb, ab, hp->seg, hp->n_segs, hp->part, hp->ldp);
     int32_t* cnt = ns && hp->cnt && hub_finish_inline() ? hp->cnt : nullptr;
-    k_spmm_wide<16><<<unsigned(ceil_div(ns + n_rows, 2)), 64, 0, s>>>(
-        x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask, ldm,
-        hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0,
-        hubs ? hp->hubs : nullptr, hubs ? hp->seg_ptr : nullptr, hubs ? hp->seg_hub : nullptr, cnt);
+    // 32-byte loads need 32-byte aligned rows (engine buffers: ld multiple of 8 floats)
+    const bool v8 = load256() && (reinterpret_cast<uintptr_t>(x) & 31) == 0 && ldx % 8 == 0 &&
+                    (!y || ((reinterpret_cast<uintptr_t>(y) & 31) == 0 && ldy % 8 == 0));
+    if (v8)
+      k_spmm_wide<16, true><<<unsigned(ceil_div(ns + n_rows, 2)), 64, 0, s>>>(
+          x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask, ldm,
+          hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0,
+          hubs ? hp->hubs : nullptr, hubs ? hp->seg_ptr : nullptr, hubs ? hp->seg_hub : nullptr,
+          cnt);
+    else
+      k_spmm_wide<16, false><<<unsigned(ceil_div(ns + n_rows, 2)), 64, 0, s>>>(
+          x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask, ldm,
+          hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0,
+          hubs ? hp->hubs : nullptr, hubs ? hp->seg_ptr : nullptr, hubs ? hp->seg_hub : nullptr,
+          cnt);
     if (hubs && !cnt) {
       k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 64)), 64, 0, s>>>(
           dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask,
