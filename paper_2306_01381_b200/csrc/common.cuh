@@ -97,6 +97,7 @@ struct qgnn_ctx {
   // wgen on every change; plain C-ABI callers always re-split.
   bool b_reuse = false;
   uint64_t wgen = 0;
+  int last_gemm_launches = 0;  // kernels the last tc_gemm_rows call launched (1 or 2)
   struct {
     const void* W = nullptr;
     const void* buf = nullptr;

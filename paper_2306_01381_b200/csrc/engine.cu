@@ -435,7 +435,9 @@ class Engine final : public EngineBase {
   // fp32 + GPU wire layout: ReLU backward folded into the producers of dh (masked by h)
   bool relu_fused() const { return sizeof(T) == 4 && s_.layout == QGNN_WIRE_GPU; }
   bool dh_masked_ = false;  // dh already carries the ReLU-backward mask of its layer
-  int gemm_nk() const { return (sizeof(T) == 4 && use_tc_gemm()) ? 2 : 1; }
+  int gemm_nk() const {  // kernels of the last dense_forward / input_grad call
+    return (sizeof(T) == 4 && use_tc_gemm()) ? std::max(1, ctx_->last_gemm_launches) : 1;
+  }
   void loss_phase();
   void backward_layer(int l);
   void backward_last();

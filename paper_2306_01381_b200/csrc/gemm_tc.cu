@@ -651,6 +651,7 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
   auto& bp = ctx->bprep;
   const bool reuse = ctx->b_reuse && bp.W == W && bp.buf == bhi && bp.wcols == wcols &&
                      bp.N == N && bp.K == K && bp.transpose == transpose_w && bp.gen == ctx->wgen;
+  ctx->last_gemm_launches = reuse ? 1 : 2;
   if (!reuse) {  // same stream as every GEMM that reuses it: ordered before them
     tc::k_prep_b<<<unsigned(ceil_div(int64_t(N) * Kp, 256)), 256, 0, s>>>(W, wcols, N, K, Kp,
                                                                           transpose_w, bhi, blo);
