@@ -132,6 +132,7 @@ struct HubPlan {
   // in-kernel hub reduction: the last segment of a hub to finish reduces it
   const int32_t* seg_hub = nullptr;  // [n_segs] hub index of each segment
   int32_t* cnt = nullptr;            // [n_hubs] arrivals; zero between launches
+  double avg_deg = 0;                // mean (a + b) degree of the range's rows
 };
 // fp32 row-range SpMM with segmented hub rows (spmm.cu)
 // returns the number of kernels launched

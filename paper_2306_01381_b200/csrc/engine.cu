@@ -341,10 +341,12 @@ class Engine final : public EngineBase {
     std::vector<int64_t> seg;
     std::vector<int32_t> seg_hub;  // hub index of each segment
     std::vector<std::pair<int64_t, int32_t>> by_deg;  // (-degree, row) of the non-hub rows
+    int64_t total_deg = 0;
     for (int64_t r = r0; r < r1; ++r) {
       const int64_t a0 = pa[r], a1 = pa[r + 1];
       const int64_t b0 = pb ? (*pb)[r] : 0, b1 = pb ? (*pb)[r + 1] : 0;
       const int64_t deg = (a1 - a0) + (b1 - b0);
+      total_deg += deg;
       if (deg <= kHubDeg) {
         by_deg.emplace_back(-deg, int32_t(r));
         continue;
@@ -368,6 +370,7 @@ class Engine final : public EngineBase {
     h.order.upload(order);
     h.plan.order = order.empty() ? nullptr : h.order.p;
     h.plan.n_order = int64_t(order.size());
+    h.plan.avg_deg = r1 > r0 ? double(total_deg) / double(r1 - r0) : 0.0;
     h.seg_hub.upload(seg_hub);
     h.cnt.alloc(std::max<size_t>(1, rows.size()));  // zeroed
     h.plan.seg_hub = h.seg_hub.p;

@@ -757,6 +757,74 @@ __global__ void __launch_bounds__(64, MINB) k_spmm_wide(
   }
 }
 
+// 256-wide rows of low degree (the remote-partial rows: ~1 edge each), two rows
+// per warp: a half-warp owns a row (16 lanes x 16 columns, two 32-byte loads per
+// edge), so twice the rows' dependent index -> gather chains are in flight.
+// Hub rows are left to k_spmm_wide's segments; no shuffles, halves run freely.
+__device__ __forceinline__ void half_gather(float4 (&acc)[4], const float* __restrict__ src,
+                                            int ld, int n, const int32_t* __restrict__ col,
+                                            const float* __restrict__ alpha, int c0) {
+  for (int e = 0; e < n; e += 2) {
+    float4 v[2][4];
+    float a[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      a[u] = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[u][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e + u < n) {
+        const int c = __ldg(col + e + u);
+        a[u] = __ldg(alpha + e + u);
+        const float* p = src + int64_t(c) * ld + c0;
+        ldg256(p, v[u][0], v[u][1]);
+        ldg256(p + 8, v[u][2], v[u][3]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) fma4(acc[q], a[u], v[u][q]);
+  }
+}
+
+__global__ void __launch_bounds__(64, 16) k_spmm_wide_half(
+    const float* __restrict__ x, int64_t ldx, const float* __restrict__ y, int64_t ldy,
+    const float* __restrict__ self_alpha, const int64_t* __restrict__ pa,
+    const int32_t* __restrict__ ca, const float* __restrict__ aa, const int64_t* __restrict__ pb,
+    const int32_t* __restrict__ cb, const float* __restrict__ ab, int64_t r0, int64_t n_rows,
+    float* __restrict__ out, int64_t ldo, int64_t hub_deg, const float* __restrict__ mask,
+    int64_t ldm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int hl = lane & 15;
+  const int64_t r = r0 + (int64_t(blockIdx.x) * (blockDim.x >> 5) + warp) * 2 + (lane >> 4);
+  if (r >= r0 + n_rows) return;
+  const int64_t ea = pa[r];
+  const int na = int(pa[r + 1] - ea), nb = pb ? int(pb[r + 1] - pb[r]) : 0;
+  if (na + nb > hub_deg) return;  // k_spmm_wide's segments + in-kernel finish
+  const int c0 = 16 * hl;         // this lane's 16 columns
+  float4 acc[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  half_gather(acc, x, int(ldx), na, ca + ea, aa + ea, c0);
+  if (nb) {
+    const int64_t eb = pb[r];
+    half_gather(acc, y, int(ldy), nb, cb + eb, ab + eb, c0);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = c0 + 4 * q;
+    float4 o = acc[q];
+    if (self_alpha) {
+      const float sa = self_alpha[r];
+      const float4 xv = __ldg(reinterpret_cast<const float4*>(x + r * ldx + c));
+      o = make_float4(fmaf(sa, xv.x, o.x), fmaf(sa, xv.y, o.y), fmaf(sa, xv.z, o.z),
+                      fmaf(sa, xv.w, o.w));
+    }
+    if (mask) o = relu_mask4(o, mask + r * ldm + c);
+    *reinterpret_cast<float4*>(out + r * ldo + c) = o;
+  }
+}
+
 // One CTA per hub row: 8 warps take contiguous eighths of the edge lists,
 // partial sums meet in shared memory and are added in warp order (deterministic).
 template <int NV>
@@ -897,6 +965,11 @@ static bool load256() {  // QGNN_SPMM_LD256=0: 16-byte gathers only
   return !e || std::atoi(e) != 0;
 }
 
+static double half_rows_deg() {  // QGNN_SPMM_HALF_DEG: mean degree below which 256-wide
+  const char* e = std::getenv("QGNN_SPMM_HALF_DEG");  // ranges run two rows per warp
+  return e ? std::atof(e) : 4.0;
+}
+
 static bool merge_hubs() {  // QGNN_HUB_MERGE=0: hub segments as a separate k_spmm_hubseg launch
   const char* e = std::getenv("QGNN_HUB_MERGE");
   return !e || std::atoi(e) != 0;
@@ -1016,6 +1089,21 @@ int spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y
     // 32-byte loads need 32-byte aligned rows (engine buffers: ld multiple of 8 floats)
     const bool v8 = load256() && (reinterpret_cast<uintptr_t>(x) & 31) == 0 && ldx % 8 == 0 &&
                     (!y || ((reinterpret_cast<uintptr_t>(y) & 31) == 0 && ldy % 8 == 0));
+    if (v8 && hp && hp->avg_deg < half_rows_deg()) {
+      // low-degree rows: two per warp; hub segments (if any) through k_spmm_wide
+      k_spmm_wide_half<<<unsigned(ceil_div(n_rows, 4)), 64, 0, s>>>(
+          x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask, ldm);
+      if (ns)
+        k_spmm_wide<16, true><<<unsigned(ceil_div(ns, 2)), 64, 0, s>>>(
+            x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, 0, out, ldo, hd, mask, ldm,
+            hp->seg, ns, hp->part, hp->ldp, hp->hubs, hp->seg_ptr, hp->seg_hub, cnt);
+      if (hubs && !cnt)
+        k_spmm_hubred<<<unsigned(ceil_div(hp->n_hubs * 32, 64)), 64, 0, s>>>(
+            dim, x, ldx, sa, hp->hubs, hp->seg_ptr, hp->n_hubs, hp->part, hp->ldp, out, ldo, mask,
+            ldm);
+      check_launch("k_spmm_wide_half");
+      return 1 + (ns ? 1 : 0) + (hubs && !cnt ? 1 : 0);
+    }
     if (v8)
       k_spmm_wide<16, true><<<unsigned(ceil_div(ns + n_rows, 2)), 64, 0, s>>>(
           x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask, ldm,
