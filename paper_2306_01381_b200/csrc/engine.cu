@@ -416,6 +416,10 @@ class Engine final : public EngineBase {
   // K1/K3 on a side stream alongside the central rows (QGNN_SIDE_STREAM=1).  Off by
   // default since the SpMM/GEMM kernels saturate the GPU: in the captured graph the
   // concurrent encode/decode cost 1.6 ms/epoch more than running it in line.
+  static bool merge_gemm_enabled() {  // QGNN_MERGE_GEMM=0: separate central / marginal GEMMs
+    const char* e = std::getenv("QGNN_MERGE_GEMM");
+    return !e || std::atoi(e) != 0;
+  }
   static bool side_enabled() {
     const char* e = std::getenv("QGNN_SIDE_STREAM");
     return e && std::atoi(e) != 0;
@@ -1409,6 +1413,10 @@ void Engine<T>::forward_layer(int l) {
   const int64_t din = dims_[t], dout = dims_[l];
   const int64_t ldi = ld_of(din), ldo = ld_of(dout);
   const int relu = l < L_ ? 1 : 0;
+  // One GPU, in-line schedule: nothing overlaps the central rows, so each
+  // partition's transform runs once over central + marginal rows (contiguous in
+  // hagg) after its marginal aggregation: one GEMM launch instead of two.
+  const bool one_gemm = s_.world == 1 && !side_overlap() && merge_gemm_enabled();
   // central rows (engine.hpp:598-605): during the exchange
   auto central = [&](PartDev& D) {
     const int64_t nc = D.view.n_central;
@@ -1420,6 +1428,7 @@ void Engine<T>::forward_layer(int l) {
     kend(QGNN_K_SPMM_FWD, nc * (16.0 + 2 * din * sizeof(T)) + nnz * (4 + sizeof(T)) +
                               double(D.view.num_owned) * din * sizeof(T), s_main_, nk,
          (nnz + nc) * din * sizeof(T));
+    if (one_gemm) return;
     kbegin(QGNN_K_GEMM_FWD);
     QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
                                  nullptr, 0, nc, relu, D.h[l].p, ldo, s_main_));
@@ -1461,6 +1470,12 @@ void Engine<T>::forward_layer(int l) {
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
     const int64_t nc = D.view.n_central, nm = D.view.n_marginal;
+    if (one_gemm && !nm && nc) {  // all rows central: their deferred transform
+      kbegin(QGNN_K_GEMM_FWD);
+      QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
+                                   nullptr, 0, nc, relu, D.h[l].p, ldo, s_main_));
+      kend(QGNN_K_GEMM_FWD, double(nc) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+    }
     if (!nm) continue;
     kbegin(QGNN_K_SPMM_FWD);
     const int nk = spmm(din, D.h[t].p, ldi, D.halo.p, ldi, D.self_alpha.p, D.lptr.p, D.lcol.p,
@@ -1471,10 +1486,11 @@ void Engine<T>::forward_layer(int l) {
     kend(QGNN_K_SPMM_FWD, nm * (24.0 + 2 * din * sizeof(T)) + nnz * (4 + sizeof(T)) +
                               double(D.view.num_remote) * din * sizeof(T), s_main_, nk,
          (nnz + nm) * din * sizeof(T));
+    const int64_t g0 = one_gemm ? 0 : nc, gn = one_gemm ? nc + nm : nm;
     kbegin(QGNN_K_GEMM_FWD);
     QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
-                                 nullptr, nc, nm, relu, D.h[l].p, ldo, s_main_));
-    kend(QGNN_K_GEMM_FWD, double(nm) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+                                 nullptr, g0, gn, relu, D.h[l].p, ldo, s_main_));
+    kend(QGNN_K_GEMM_FWD, double(gn) * (din + dout) * sizeof(T), s_main_, gemm_nk());
   }
 }
 
