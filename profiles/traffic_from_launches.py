@@ -17,7 +17,9 @@ UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "
          "us": 1e-6, "usecond": 1e-6, "ms": 1e-3,
          "msecond": 1e-3}
 # engine-level launches (kend calls) per class per epoch for the bench workload (P = 8, 3 layers)
-KENDS = {"spmm_fwd": 48, "spmm_bwd": 16, "partials": 16, "quant": 40, "gemm_fwd": 48}
+# (one GPU: the forward GEMM runs once per partition over central + marginal rows for the
+# aggregate-then-transform layers, twice for the transform-first one: 8 + 8 + 16)
+KENDS = {"spmm_fwd": 48, "spmm_bwd": 16, "partials": 16, "quant": 40, "gemm_fwd": 32}
 
 
 def main(path):
