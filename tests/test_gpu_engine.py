@@ -164,6 +164,17 @@ def test_side_stream_is_identical(cuda, monkeypatch, graph):
     assert (wa == wb).all()
 
 
+def test_merged_forward_gemm_is_identical(cuda, monkeypatch):
+    """One forward GEMM per partition over central + marginal rows (QGNN_MERGE_GEMM=1,
+    one GPU) gives bit-identical training to separate central / marginal GEMMs."""
+    monkeypatch.setenv("QGNN_MERGE_GEMM", "0")
+    a, wa = _run("fixed", 8, 3, "f32")
+    monkeypatch.setenv("QGNN_MERGE_GEMM", "1")
+    b, wb = _run("fixed", 8, 3, "f32")
+    assert [m["train_loss"] for m in a] == [m["train_loss"] for m in b]
+    assert (wa == wb).all()
+
+
 def test_engine_transform_first_last_layer(cuda, monkeypatch):
     """z = A(hW) for the narrowing last layer matches aggregate-then-transform (fp32)."""
     tf, wt = _run("fixed", 4, 4, "f32")
