@@ -140,60 +140,101 @@ def bcast_bytes(b, world, rank):
 
 
 # ------------------------------------------------------------------ CPU side ---
-def reference_sample(scale_div):
-    """Bounded sample for the reference CPU engine: the same generator and shape
-    family scaled down by `scale_div` in nodes and edges (same degree, dims, P)."""
-    from paper_2306_01381_b200.engine import generate_planted
+# The reference arm and cpu_baseline load only synth/ (input generation shared
+# with the GPU arm) and oracle/_ref (the unmodified reference headers compiled
+# by oracle/Makefile) -- never the product package.
+def workload_graph(scale_div=1):
+    """The bench graph (scale_div == 1) or a bounded sample of it: the same
+    generator and shape family scaled down by `scale_div` in nodes and edges
+    (same degree law, dims, P and planted blocks)."""
+    from synth import generate_planted
     w = WORKLOAD
-    n = w["nodes"] // scale_div
-    e = w["n_edges"] // scale_div
-    g = generate_planted(n, e, w["feat"], w["classes"], w["parts"], w["cross_frac"],
-                         gamma=w["gamma"], seed=w["seed"])
-    g["features"] = g["features"].astype(np.float64)
-    return g
+    return generate_planted(w["nodes"] // scale_div, w["n_edges"] // scale_div, w["feat"],
+                            w["classes"], w["parts"], w["cross_frac"], gamma=w["gamma"],
+                            seed=w["seed"])
 
 
-def run_reference_epochs(g, epochs, threads=True):
-    """The compiled reference Engine (oracle/_ref, trainer/engine.hpp) — kThreads,
-    one host thread per partition; returns per-epoch seconds."""
+def run_reference_epochs(g, epochs, bit_mode="adaptive"):
+    """The compiled reference Engine (oracle/_ref: trainer/engine.hpp, unmodified)
+    in ExecMode::kThreads (one host thread per partition), partitioned like the
+    GPU arm: planted owner map -> partitions_from_owner (partition.hpp:39).
+    Returns (per-epoch seconds of Engine::run, setup seconds, epoch metrics)."""
     from oracle import ref
     w = WORKLOAD
     dims = [w["feat"], w["hidden"], w["hidden"], w["classes"]]
-    ep, _ = ref.engine_run(g, dims, w["parts"], bit_mode=3, epochs=epochs, seed=7,
-                           group_size=2000, period=50, threads=threads,
-                           theta=1.0 / (900e9 * 8), gamma=2e-5)
-    return ep[:, 9], ep
+    g = dict(g)
+    g["features"] = np.ascontiguousarray(g["features"], np.float64)  # fp32-representable
+    times = np.zeros(2)
+    ep, _ = ref.engine_run(g, dims, w["parts"], bit_mode=BIT_CODES[bit_mode], fixed_bits=8,
+                           epochs=epochs, seed=7, group_size=2000, period=50, threads=True,
+                           theta=1.0 / (900e9 * 8), gamma=2e-5, owner=g["owner"], times=times)
+    return times[1] / epochs, times[0], ep
+
+
+BIT_CODES = {"fp": 0, "fixed": 1, "uniform": 2, "adaptive": 3}
+
+
+def cpu_baseline_sample(bit_mode, div=16, epochs=2):
+    """cpu_baseline: the reference engine on a bounded 1/div sample of the
+    workload (same generator, owner map, dims, P), Engine::run seconds per
+    epoch (setup excluded) scaled by div (epoch work is linear in nodes and
+    nnz: SpMM + dense rows)."""
+    g = workload_graph(div)
+    per, setup, ep = run_reference_epochs(g, epochs, bit_mode)
+    return {"value": per * div, "unit": "s", "cores": REF_THREADS, "kind": "reference",
+            "sample": f"reference Engine (oracle/_ref, kThreads: {REF_THREADS} partitions = "
+                      f"{REF_THREADS} threads, planted owner map -> partitions_from_owner) on "
+                      f"the bench generator scaled 1/{div} ({len(g['adj_ptr']) - 1} nodes, "
+                      f"{int(g['adj_ptr'][-1])} CSR nnz); {epochs} epochs, "
+                      f"{per:.3f} s/epoch of Engine::run (setup {setup:.2f} s excluded) "
+                      f"x {div}",
+            "sample_epoch_s": per, "scale": div, "sample_train_loss": float(ep[-1, 0])}
+
+
+REF_THREADS = 8  # kThreads: one host thread per partition (engine.hpp:356-380)
+
+
+def _peak_rss_gb():
+    import resource
+    return resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6
 
 
 def impl_reference(args):
+    """--impl reference: the reference's own CPU engine on the FULL bench
+    workload (same graph, partitions, dims, bit mode), timed per epoch over
+    Engine::run with setup excluded.  A full epoch takes ~1-2 minutes on 8
+    host threads, so the arm times min(K, --ref-epochs) epochs and no warm-up
+    (the CPU engine has no JIT, graph capture or cache to warm); both counts
+    are reported as run."""
     rank, world, _ = dist_setup()
     if rank != 0:
         return
-    div = 64
-    g = reference_sample(div)
-    n_cores = os.cpu_count()
-    k = max(1, args.steps)
-    wu = max(0, args.warmup)
-    # one engine run of W+K epochs; the reference reports mean wall s/epoch
     t0 = time.time()
-    per, _ = run_reference_epochs(g, wu + k)
-    wall = time.time() - t0
-    sample_epoch = float(wall / (wu + k))
-    value = sample_epoch * div  # linear in nodes and nnz (dense + SpMM dominate)
+    g = workload_graph(1)
+    t_gen = time.time() - t0
+    k = max(1, min(args.steps, args.ref_epochs))
+    per, setup, ep = run_reference_epochs(g, k, args.bit_mode)
+    value = per
     line = {"metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus, "steps": k,
-            "warmup": wu, "ms_per_step": value * 1e3, "higher_is_better": False,
+            "warmup": 0, "steps_requested": args.steps, "warmup_requested": args.warmup,
+            "ms_per_step": value * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference", "config": config_dict(args.gpus, "adaptive"),
-            "cpu_baseline": {"value": value, "unit": "s", "cores": min(8, n_cores),
+            "impl": "reference", "config": config_dict(args.gpus, args.bit_mode),
+            "cpu_baseline": {"value": value, "unit": "s", "cores": REF_THREADS,
                              "kind": "reference",
-                             "sample": f"reference Engine (kThreads, 8 partitions = 8 threads, "
-                                       f"BFS partition_graph) on the same generator scaled "
-                                       f"1/{div} ({g['adj_ptr'].shape[0]-1} nodes, "
-                                       f"{g['adj_ptr'][-1]} nnz); {wu}+{k} epochs, "
-                                       f"{sample_epoch:.3f} s/epoch x {div} (linear in nodes "
-                                       f"and nnz)"},
+                             "sample": f"full workload ({len(g['adj_ptr']) - 1} nodes, "
+                                       f"{int(g['adj_ptr'][-1])} CSR nnz): reference Engine "
+                                       f"(oracle/_ref, kThreads = {REF_THREADS} threads, "
+                                       f"partitions_from_owner on the planted owner map), "
+                                       f"{k} epoch(s) of Engine::run; setup {setup:.1f} s and "
+                                       f"graph generation {t_gen:.1f} s excluded",
+                             "host_cpus": os.cpu_count(),
+                             "peak_rss_gb": _peak_rss_gb()},
             "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "last_epoch": {"train_loss": float(ep[-1, 0]), "val_acc": float(ep[-1, 1]),
+                           "bytes_total": int(ep[-1, 3]), "msgs_b8": int(ep[-1, 6])},
+            "setup_s": {"generate": t_gen, "engine": setup}}
     print(json.dumps(line), flush=True)
 
 
@@ -201,13 +242,12 @@ def impl_reference(args):
 def impl_ours(args):
     rank, world, local = dist_setup()
     import torch
-    from paper_2306_01381_b200.engine import Engine, generate_planted, nccl_unique_id
+    from paper_2306_01381_b200.engine import Engine, nccl_unique_id
     torch.cuda.set_device(local)
     w = WORKLOAD
     assert w["parts"] % world == 0, "P must be a multiple of the GPU count"
     t0 = time.time()
-    g = generate_planted(w["nodes"], w["n_edges"], w["feat"], w["classes"], w["parts"],
-                         w["cross_frac"], gamma=w["gamma"], seed=w["seed"])
+    g = workload_graph(1)
     t_gen = time.time() - t0
     nid = bcast_bytes(nccl_unique_id() if (world > 1 and rank == 0) else None, world, rank)
     bit_mode = args.bit_mode
@@ -324,16 +364,7 @@ def impl_ours(args):
     cpu = None
     if world == 1 and not args.no_cpu:
         try:
-            div = 64
-            gs = reference_sample(div)
-            t0 = time.time()
-            per, _ = run_reference_epochs(gs, 1)
-            cpu_s = time.time() - t0
-            cpu = {"value": cpu_s * div, "unit": "s", "cores": min(8, os.cpu_count()),
-                   "kind": "reference",
-                   "sample": f"reference Engine (oracle/_ref, kThreads: 8 partitions = 8 "
-                             f"threads, BFS partition_graph) 1 epoch on the same generator "
-                             f"scaled 1/{div}; {cpu_s:.2f} s x {div} (linear in nodes, nnz)"}
+            cpu = cpu_baseline_sample(bit_mode)
         except Exception as exc:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {exc}"}
@@ -392,6 +423,8 @@ def main():
     ap.add_argument("--bit-mode", default="adaptive",
                     choices=["adaptive", "fixed", "fp", "uniform"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-epochs", type=int, default=2,
+                    help="reference arm: full-size epochs timed (min with --steps)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":

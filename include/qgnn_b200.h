@@ -64,7 +64,8 @@ uint64_t qgnn_packed_bytes(uint64_t count, int bits);
 /* QGNN_WIRE_REF: 25 + ceil(count*bits/8)  (byte-identical to append_chunk).
  * QGNN_WIRE_GPU: 16-byte header {f32 scale, f32 zero, u32 count, u8 bits, 3 pad}
  *                + payload padded to a 16-byte multiple.
- * bits == 0 denotes a raw full-precision row (BitMode::kFp): count * elem bytes. */
+ * bits == 0 denotes a raw full-precision row (BitMode::kFp): count * elem bytes
+ * (QGNN_WIRE_GPU pads it to a 16-byte multiple so every chunk stays 16-aligned). */
 uint64_t qgnn_chunk_wire_bytes(uint64_t count, int bits, int layout, int dtype);
 
 /* encode_message_set's wire order (codec.hpp:56-69): width groups 2,4,8, caller
@@ -109,6 +110,30 @@ int qgnn_csr_aggregate(qgnn_ctx* ctx, int dtype, int64_t dim, const void* x, int
                        const int32_t* col_a, const void* alpha_a, const int64_t* ptr_b,
                        const int32_t* col_b, const void* alpha_b, const int32_t* rows,
                        int64_t row_begin, int64_t n_rows, void* out, int64_t ld_out, void* stream);
+
+/* Production fp32 K4 for one CSR row range — the kernels the engine runs at
+ * scale (spmm.cu: 256-wide, grouped <= 128-wide and degree-sorted <= 64-wide
+ * row kernels, hub rows split into 256-edge segments and reduced in segment
+ * order inside the launch).  The plan is built once per (CSR, row range) on
+ * the host from HOST copies of ptr_a / ptr_b (rows [row_begin, row_begin +
+ * n_rows)); rows with more than hub_deg neighbours become hub segments;
+ * max_dim bounds `dim` of later runs.  A run computes the same sum as
+ * qgnn_csr_aggregate (F32, fused multiply-add) with [dev] arrays; x / y /
+ * out / mask rows must be 16-byte aligned with ld a multiple of 4 and the
+ * columns in [dim, round_up(dim, 4)) zero.  mask != NULL applies the ReLU
+ * backward (layer_backward_rows, model.hpp:128-153) to the result:
+ * out[r][c] = mask[r][c] > 0 ? sum : 0. */
+typedef struct qgnn_spmm_plan qgnn_spmm_plan;
+int qgnn_spmm_plan_create(qgnn_ctx* ctx, const int64_t* ptr_a, const int64_t* ptr_b,
+                          int64_t row_begin, int64_t n_rows, int64_t max_dim, int64_t hub_deg,
+                          qgnn_spmm_plan** out);
+int qgnn_spmm_plan_run(qgnn_spmm_plan* plan, int64_t dim, const float* x, int64_t ld_x,
+                       const float* y, int64_t ld_y, const float* self_alpha,
+                       const int64_t* ptr_a, const int32_t* col_a, const float* alpha_a,
+                       const int64_t* ptr_b, const int32_t* col_b, const float* alpha_b,
+                       const float* mask, int64_t ld_mask, float* out, int64_t ld_out,
+                       void* stream);
+int qgnn_spmm_plan_destroy(qgnn_spmm_plan* plan);
 
 /* ---- K5 dense transform: model.hpp:90-170, matrix.hpp:51-65 --------------------
  * forward:      out[r] = act(A[r] W)            W: din x dout row-major (layer_forward_rows)
@@ -198,7 +223,10 @@ typedef struct {
   int32_t layout;          /* QGNN_WIRE_GPU or QGNN_WIRE_REF */
   int32_t rank, world;     /* process rank / count; parts are split contiguously */
   int32_t device;          /* CUDA device of this rank */
-  int32_t overlap;         /* 1: central compute on its own stream during the exchange */
+  int32_t overlap;         /* 0: the compute stream waits for each exchange before the
+                              central rows (serialized); 1 (default): central SpMM + GEMM
+                              overlap the exchange on the comm stream; 2: one GPU, K1/K3
+                              also on a side stream next to the central rows */
   int32_t kstats;          /* 1: time every kernel class with CUDA events (bench roofline) */
 } qgnn_settings;
 
@@ -210,7 +238,10 @@ typedef struct {
   uint64_t msgs_b2, msgs_b4, msgs_b8, msgs_fp;
   uint64_t plan_version;
   double ms_total;           /* device time of the epoch (CUDA events) */
-  double ms_quant, ms_exchange, ms_central, ms_marginal, ms_backward, ms_step;
+  /* per kernel class, this epoch (settings.kstats = 1; 0 otherwise): K1 quantize,
+   * exchange (comm stream), K3 dequantize, K4 SpMM (all variants), K5 GEMMs,
+   * everything else (ReLU, loss, all-gather sum + Adam) */
+  double ms_quant, ms_exchange, ms_dequant, ms_spmm, ms_gemm, ms_other;
   double resolve_seconds;    /* host solver time if a re-solve ran */
 } qgnn_epoch_metrics;
 

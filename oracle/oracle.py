@@ -281,7 +281,7 @@ class _Ref:
         L.ref_engine_run.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                      C.c_double, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                      C.c_uint64, C.c_int, C.c_double, C.c_double, C.c_double,
-                                     C.c_void_p, C.c_void_p]
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
 
     def _chk(self, st):
         if st:
@@ -457,7 +457,10 @@ class _Ref:
     # engine -----------------------------------------------------------------
     def engine_run(self, g, dims, n_parts, bit_mode=1, fixed_bits=8, epochs=3, seed=7,
                    sage=False, lam=0.5, group_size=4, period=50, threads=False, theta=3e-9,
-                   gamma=5e-5, lr=0.01):
+                   gamma=5e-5, lr=0.01, owner=None, times=None):
+        """Reference Engine::run.  owner: planted owner map -> the Engine
+        partitions with partitions_from_owner (else partition_graph, BFS).
+        times: optional float64[2] <- (setup seconds, run seconds)."""
         h = self.L.ref_dataset_from_arrays(
             _p(g["adj_ptr"]), _p(g["adj"]), C.c_uint64(len(g["adj_ptr"]) - 1),
             _p(np.ascontiguousarray(g["features"], np.float64)),
@@ -468,10 +471,12 @@ class _Ref:
             ep = np.zeros((epochs, 10), np.float64)
             total = sum(int(dims[i]) * int(dims[i + 1]) for i in range(len(dims) - 1))
             fw = np.zeros(total, np.float64)
+            own = None if owner is None else np.ascontiguousarray(owner, np.uint32)
             self._chk(self.L.ref_engine_run(h, _p(d), len(d), int(sage), int(bit_mode),
                                             int(fixed_bits), lam, group_size, period, epochs,
                                             seed, n_parts, int(threads), theta, gamma, lr,
-                                            _p(ep), _p(fw)))
+                                            _p(ep), _p(fw),
+                                            _p(own), _p(times)))
             return ep, fw
         finally:
             self.L.ref_dataset_free(h)

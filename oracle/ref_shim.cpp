@@ -24,7 +24,25 @@
 #include "qgnn/quantcodec/rng.hpp"
 #include "qgnn/tensorops/aggregate.hpp"
 #include "qgnn/tensorops/model.hpp"
+
+// Partitioner interposition for the Engine (engine.hpp:212 calls
+// partition_graph).  When ref_engine_run is given an owner map, the Engine
+// partitions with the reference's own partitions_from_owner
+// (partition.hpp:39-84, the halo-layout API SURVEY.md §8e names for the
+// planted-block configs) instead of the BFS partition_graph; with no owner
+// map it calls partition_graph unchanged.  Only the one call token is
+// redirected; the header text is untouched.
+namespace qgnn::shim_hook {
+inline const std::vector<uint32_t>* g_owner = nullptr;
+inline std::vector<Partition> partition_graph(const Graph& g, std::size_t n_parts,
+                                              uint64_t seed) {
+  if (g_owner) return qgnn::partitions_from_owner(g, *g_owner, n_parts);
+  return qgnn::partition_graph(g, n_parts, seed);
+}
+}  // namespace qgnn::shim_hook
+#define partition_graph shim_hook::partition_graph
 #include "qgnn/trainer/engine.hpp"
+#undef partition_graph
 
 using namespace qgnn;
 
@@ -471,10 +489,15 @@ int ref_solve_instance(uint64_t n_pairs, const uint32_t* pair_src, const uint32_
 // reports per-epoch (loss, val_acc, test_acc, bytes_total, msgs_b2, msgs_b4,
 // msgs_b8, msgs_fp, plan_version, wall_seconds) and final weights.
 // bit_mode: 0 fp, 1 fixed, 2 uniform, 3 adaptive.  threads != 0 -> kThreads.
+// owner != NULL: partitions_from_owner(g, owner) instead of partition_graph
+// (see shim_hook above).  times_out (optional, 2 doubles): Engine
+// construction seconds and run() seconds (epoch_out[.., 9] = run() / epochs,
+// setup excluded).
 int ref_engine_run(void* dataset, const uint64_t* dims, int n_dims, int sage, int bit_mode,
                    int fixed_bits, double lambda, uint64_t group_size, uint64_t period,
                    uint64_t epochs, uint64_t seed, uint64_t n_parts, int threads, double theta,
-                   double gamma, double lr, double* epoch_out, double* final_weights) {
+                   double gamma, double lr, double* epoch_out, double* final_weights,
+                   const uint32_t* owner, double* times_out) {
   GUARD({
     const Graph& g = static_cast<RefDataset*>(dataset)->g;
     TrainSettings s;
@@ -492,11 +515,23 @@ int ref_engine_run(void* dataset, const uint64_t* dims, int n_dims, int sage, in
     s.n_parts = n_parts;
     s.exec = threads ? ExecMode::kThreads : ExecMode::kRoundRobin;
     s.cost = CostModel::uniform(n_parts, theta, gamma);
-    Engine eng(g, s);
+    std::vector<uint32_t> own;
+    if (owner) own.assign(owner, owner + g.num_nodes);
+    const auto ts = std::chrono::steady_clock::now();
+    shim_hook::g_owner = owner ? &own : nullptr;
+    struct Reset {
+      ~Reset() { shim_hook::g_owner = nullptr; }
+    } reset;
+    Engine eng(g, s);  // setup(): partition, coefficients, views, model init
+    shim_hook::g_owner = nullptr;
     const auto t0 = std::chrono::steady_clock::now();
     const TrainResult res = eng.run();
     const double wall =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (times_out) {
+      times_out[0] = std::chrono::duration<double>(t0 - ts).count();  // Engine construction
+      times_out[1] = wall;                                             // run(): all epochs
+    }
     for (std::size_t e = 0; e < res.epochs.size(); ++e) {
       const EpochMetrics& m = res.epochs[e];
       double* o = epoch_out + e * 10;

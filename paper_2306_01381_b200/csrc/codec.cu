@@ -28,7 +28,10 @@ __host__ __device__ inline uint64_t packed_bytes(uint64_t count, int b) {
   return (count * static_cast<uint64_t>(b) + 7) / 8;
 }
 __host__ __device__ inline uint64_t chunk_bytes(uint64_t count, int b, int layout, int elem) {
-  if (b == 0) return count * static_cast<uint64_t>(elem);
+  if (b == 0) {  // raw row; GPU layout pads it to 16 bytes so every chunk stays 16-aligned
+    const uint64_t raw = count * static_cast<uint64_t>(elem);
+    return layout == QGNN_WIRE_REF ? raw : (raw + 15) / 16 * 16;
+  }
   if (layout == QGNN_WIRE_REF) return kHdrRef + packed_bytes(count, b);
   return kHdrGpu + ((packed_bytes(count, b) + 15) / 16) * 16;
 }
@@ -815,7 +818,8 @@ __global__ void __launch_bounds__(256) k_dequant_rows_f32(
   const int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (g >= n_rows) return;
   const int nchunk = (dim + 3) >> 2;
-  constexpr int kMaxC = 4;  // float4 chunks per lane: dim <= 512
+  constexpr int kMaxC = 4;  // float4 chunks per lane: 512 columns per grid.y slice
+  const int cbase = blockIdx.y * 128;
   float4 acc[kMaxC];
 #pragma unroll
   for (int i = 0; i < kMaxC; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -827,7 +831,7 @@ __global__ void __launch_bounds__(256) k_dequant_rows_f32(
       const float4* src = reinterpret_cast<const float4*>(chunk);
 #pragma unroll
       for (int i = 0; i < kMaxC; ++i) {
-        const int c = lane + 32 * i;
+        const int c = cbase + lane + 32 * i;
         if (c < nchunk) {
           const float4 v = src[c];
           acc[i].x += v.x, acc[i].y += v.y, acc[i].z += v.z, acc[i].w += v.w;
@@ -845,7 +849,7 @@ __global__ void __launch_bounds__(256) k_dequant_rows_f32(
     const uint32_t cmask = (1u << b) - 1;
 #pragma unroll
     for (int i = 0; i < kMaxC; ++i) {
-      const int c = lane + 32 * i;
+      const int c = cbase + lane + 32 * i;
       if (c >= nchunk) continue;
       uint32_t word;
       if (b == 8)
@@ -863,7 +867,7 @@ __global__ void __launch_bounds__(256) k_dequant_rows_f32(
   const int64_t r = rows[g];
 #pragma unroll
   for (int i = 0; i < kMaxC; ++i) {
-    const int c = lane + 32 * i;
+    const int c = cbase + lane + 32 * i;
     if (c >= nchunk) continue;
     float4 a = acc[i];
     if (mask) {
@@ -890,8 +894,8 @@ void dequant_rows_add_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n_rows, cons
                           const uint64_t* offsets, float* out, int64_t ld, const float* mask,
                           int64_t ldm, cudaStream_t s) {
   if (n_rows == 0) return;
-  QGNN_REQUIRE(dim <= 512, QGNN_EINVAL, "dequant_rows_add: dim must be <= 512");
-  k_dequant_rows_f32<<<unsigned(ceil_div(n_rows * 32, 64)), 64, 0, s>>>(
+  const dim3 grid(unsigned(ceil_div(n_rows * 32, 64)), unsigned(ceil_div(dim, 512)));
+  k_dequant_rows_f32<<<grid, 64, 0, s>>>(
       in, n_rows, rows, ptr, msg, dim, bits, offsets, out, ld, mask, ldm, ctx->d_err);
   check_launch("k_dequant_rows_f32");
 }

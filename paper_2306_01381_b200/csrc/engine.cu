@@ -128,6 +128,76 @@ struct DBuf {
   }
 };
 
+// Row-range plan of the production fp32 SpMM (spmm.cu:spmm_f32): rows with
+// more than hub_deg neighbours (a + b lists) are split into 256-edge segments
+// (reduced in segment order by the last-arriving segment, or k_spmm_hubred),
+// the other rows are listed by descending degree for the multi-row narrow
+// kernel (k_spmm_sorted).  maxd: widest row the partial-row workspace holds
+// (0: no workspace, fp64 engines).
+struct Hubs {
+DBuf<int32_t> rows, seg_ptr, order, seg_hub, cnt;
+DBuf<int64_t> seg;
+DBuf<float> part;
+HubPlan plan;
+};
+
+inline void build_hub_plan(Hubs& h, const int64_t* pa, const int64_t* pb, int64_t r0, int64_t r1,
+                         int64_t maxd, int64_t kHubDeg) {
+  constexpr int64_t kSeg = 256;
+  std::vector<int32_t> rows, sptr{0};
+  std::vector<int64_t> seg;
+  std::vector<int32_t> seg_hub;  // hub index of each segment
+  std::vector<std::pair<int64_t, int32_t>> by_deg;  // (-degree, row) of the non-hub rows
+  int64_t total_deg = 0;
+  for (int64_t r = r0; r < r1; ++r) {
+    const int64_t a0 = pa[r], a1 = pa[r + 1];
+    const int64_t b0 = pb ? pb[r] : 0, b1 = pb ? pb[r + 1] : 0;
+    const int64_t deg = (a1 - a0) + (b1 - b0);
+    total_deg += deg;
+    if (deg <= kHubDeg) {
+      by_deg.emplace_back(-deg, int32_t(r));
+      continue;
+    }
+    rows.push_back(int32_t(r));
+    for (int64_t e = 0; e < deg; e += kSeg) {  // edge positions in the (a ++ b) list
+      const int64_t f = std::min(deg, e + kSeg);
+      const int64_t la = a1 - a0;
+      seg.push_back(a0 + std::min(e, la));
+      seg.push_back(a0 + std::min(f, la));
+      seg.push_back(b0 + std::max<int64_t>(0, e - la));
+      seg.push_back(b0 + std::max<int64_t>(0, f - la));
+    }
+    sptr.push_back(int32_t(seg.size() / 4));
+    seg_hub.resize(seg.size() / 4, int32_t(rows.size() - 1));
+  }
+  // degree-descending row order for the multi-row narrow kernel (spmm.cu:k_spmm_sorted)
+  std::sort(by_deg.begin(), by_deg.end());
+  std::vector<int32_t> order(by_deg.size());
+  for (size_t i = 0; i < by_deg.size(); ++i) order[i] = by_deg[i].second;
+  h.order.upload(order);
+  h.plan.order = order.empty() ? nullptr : h.order.p;
+  h.plan.n_order = int64_t(order.size());
+  h.plan.avg_deg = r1 > r0 ? double(total_deg) / double(r1 - r0) : 0.0;
+  h.seg_hub.upload(seg_hub);
+  h.cnt.alloc(std::max<size_t>(1, rows.size()));  // zeroed
+  h.plan.seg_hub = h.seg_hub.p;
+  h.plan.cnt = h.cnt.p;
+  h.rows.upload(rows);
+  h.seg_ptr.upload(sptr);
+  h.seg.upload(seg);
+  const int64_t n_segs = int64_t(seg.size() / 4);
+  if (maxd > 0) h.part.alloc(std::max<int64_t>(1, n_segs) * maxd, false);
+  h.plan.hub_deg = kHubDeg;
+  h.plan.n_hubs = int64_t(rows.size());
+  h.plan.n_segs = n_segs;
+  h.plan.hubs = h.rows.p;
+  h.plan.seg_ptr = h.seg_ptr.p;
+  h.plan.seg = h.seg.p;
+  h.plan.part = reinterpret_cast<float*>(h.part.p);
+  h.plan.ldp = maxd;
+}
+
+
 // ------------------------------------------------------ small kernels ----
 template <typename T>
 __global__ void k_sum_parts(const T* __restrict__ all, int parts, int64_t n, T* __restrict__ out) {
@@ -318,12 +388,7 @@ class Engine final : public EngineBase {
     DBuf<unsigned long long> correct;   // [2]
     DBuf<double> ce_terms;
     // hub rows (slots) per SpMM call site, segmented (spmm.cu:k_spmm_hubseg)
-    struct Hubs {
-      DBuf<int32_t> rows, seg_ptr, order, seg_hub, cnt;
-      DBuf<int64_t> seg;
-      DBuf<float> part;
-      HubPlan plan;
-    } hub_fc, hub_fm, hub_bwd, hub_part;
+    Hubs hub_fc, hub_fm, hub_bwd, hub_part;
   };
 
   int64_t ld_of(int64_t d) const { return round_up(d, 8); }
@@ -336,58 +401,8 @@ class Engine final : public EngineBase {
   template <typename H>
   void build_hubs(H& h, const std::vector<int64_t>& pa, const std::vector<int64_t>* pb, int64_t r0,
                   int64_t r1, int64_t maxd) {
-    constexpr int64_t kSeg = 256;
-    std::vector<int32_t> rows, sptr{0};
-    std::vector<int64_t> seg;
-    std::vector<int32_t> seg_hub;  // hub index of each segment
-    std::vector<std::pair<int64_t, int32_t>> by_deg;  // (-degree, row) of the non-hub rows
-    int64_t total_deg = 0;
-    for (int64_t r = r0; r < r1; ++r) {
-      const int64_t a0 = pa[r], a1 = pa[r + 1];
-      const int64_t b0 = pb ? (*pb)[r] : 0, b1 = pb ? (*pb)[r + 1] : 0;
-      const int64_t deg = (a1 - a0) + (b1 - b0);
-      total_deg += deg;
-      if (deg <= kHubDeg) {
-        by_deg.emplace_back(-deg, int32_t(r));
-        continue;
-      }
-      rows.push_back(int32_t(r));
-      for (int64_t e = 0; e < deg; e += kSeg) {  // edge positions in the (a ++ b) list
-        const int64_t f = std::min(deg, e + kSeg);
-        const int64_t la = a1 - a0;
-        seg.push_back(a0 + std::min(e, la));
-        seg.push_back(a0 + std::min(f, la));
-        seg.push_back(b0 + std::max<int64_t>(0, e - la));
-        seg.push_back(b0 + std::max<int64_t>(0, f - la));
-      }
-      sptr.push_back(int32_t(seg.size() / 4));
-      seg_hub.resize(seg.size() / 4, int32_t(rows.size() - 1));
-    }
-    // degree-descending row order for the multi-row narrow kernel (spmm.cu:k_spmm_sorted)
-    std::sort(by_deg.begin(), by_deg.end());
-    std::vector<int32_t> order(by_deg.size());
-    for (size_t i = 0; i < by_deg.size(); ++i) order[i] = by_deg[i].second;
-    h.order.upload(order);
-    h.plan.order = order.empty() ? nullptr : h.order.p;
-    h.plan.n_order = int64_t(order.size());
-    h.plan.avg_deg = r1 > r0 ? double(total_deg) / double(r1 - r0) : 0.0;
-    h.seg_hub.upload(seg_hub);
-    h.cnt.alloc(std::max<size_t>(1, rows.size()));  // zeroed
-    h.plan.seg_hub = h.seg_hub.p;
-    h.plan.cnt = h.cnt.p;
-    h.rows.upload(rows);
-    h.seg_ptr.upload(sptr);
-    h.seg.upload(seg);
-    const int64_t n_segs = int64_t(seg.size() / 4);
-    if constexpr (sizeof(T) == 4) h.part.alloc(std::max<int64_t>(1, n_segs) * maxd, false);
-    h.plan.hub_deg = kHubDeg;
-    h.plan.n_hubs = int64_t(rows.size());
-    h.plan.n_segs = n_segs;
-    h.plan.hubs = h.rows.p;
-    h.plan.seg_ptr = h.seg_ptr.p;
-    h.plan.seg = h.seg.p;
-    h.plan.part = reinterpret_cast<float*>(h.part.p);
-    h.plan.ldp = maxd;
+    build_hub_plan(h, pa.data(), pb ? pb->data() : nullptr, r0, r1, sizeof(T) == 4 ? maxd : 0,
+                   kHubDeg);
   }
 
   int spmm(int64_t dim, const T* x, int64_t ldx, const T* y, int64_t ldy, const T* sa,
@@ -412,7 +427,9 @@ class Engine final : public EngineBase {
   void quantize(PartDev& P, int k, const T* src, int64_t ld, cudaStream_t st = nullptr);
   // one GPU: encode / decode on the side stream, overlapping the compute stream
   // (per-kernel timing runs serialised so each class's time is its own)
-  bool side_overlap() const { return s_.world == 1 && side_enabled() && !s_.kstats; }
+  bool side_overlap() const {
+    return s_.world == 1 && (side_enabled() || s_.overlap >= 2) && !s_.kstats;
+  }
   // K1/K3 on a side stream alongside the central rows (QGNN_SIDE_STREAM=1).  Off by
   // default since the SpMM/GEMM kernels saturate the GPU: in the captured graph the
   // concurrent encode/decode cost 1.6 ms/epoch more than running it in line.
@@ -1344,6 +1361,7 @@ void Engine<T>::exchange(int k) {
     for (int r = 0; r < s_.world; ++r)
       if (r != s_.rank) peer_x_.push_back(G.ev2[r]);
     kend(QGNN_K_EXCHANGE, bytes, s_comm_, 0);
+    if (s_.overlap == 0) wait_exchange();
     return;
   }
   QGNN_NCCL(nccl().GroupStart());
@@ -1356,6 +1374,7 @@ void Engine<T>::exchange(int k) {
   QGNN_NCCL(nccl().GroupEnd());
   kend(QGNN_K_EXCHANGE, bytes, s_comm_, 0);
   QGNN_CUDA(cudaEventRecord(ev_x_, s_comm_));
+  if (s_.overlap == 0) wait_exchange();  // serialized schedule: nothing overlaps the exchange
 }
 
 // Receivers wait for the exchange of the current key: NCCL completes on our comm
@@ -1365,6 +1384,10 @@ void Engine<T>::wait_exchange() {
   if (s_.world == 1) return;
   if (loop_) {
     for (cudaEvent_t e : peer_x_) QGNN_CUDA(cudaStreamWaitEvent(s_main_, e, 0));
+    // and for this rank's own outgoing copies: every key's send regions start at
+    // arena offset 0, so the next K1 on s_main_ must not overwrite them while
+    // s_comm_ is still reading them
+    QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_x_, 0));
     return;
   }
   QGNN_CUDA(cudaStreamWaitEvent(s_main_, ev_x_, 0));
@@ -1398,6 +1421,7 @@ void Engine<T>::allgather_dev(X* base, int64_t slice, cudaStream_t st) {
   G.barrier();
   for (int r = 0; r < s_.world; ++r)
     if (r != s_.rank) QGNN_CUDA(cudaStreamWaitEvent(st, G.ev2[r], 0));
+  QGNN_CUDA(cudaStreamWaitEvent(st, ev_d_, 0));  // our own slice has been read out
 }
 
 #define QGNN_CALL(x)                                 \
@@ -1425,8 +1449,8 @@ void Engine<T>::forward_layer(int l) {
     const int nk = spmm(din, D.h[t].p, ldi, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
                         D.lafwd.p, nullptr, nullptr, nullptr, 0, nc, D.hagg[t].p, ldi, &D.hub_fc.plan);
     const double nnz = double(D.view.local_ptr[nc]);
-    kend(QGNN_K_SPMM_FWD, nc * (16.0 + 2 * din * sizeof(T)) + nnz * (4 + sizeof(T)) +
-                              double(D.view.num_owned) * din * sizeof(T), s_main_, nk,
+    kend(QGNN_K_SPMM_FWD, nc * (16.0 + din * sizeof(T)) + nnz * (4 + sizeof(T)) +
+                              double(D.view.src_rows_central) * din * sizeof(T), s_main_, nk,
          (nnz + nc) * din * sizeof(T));
     if (one_gemm) return;
     kbegin(QGNN_K_GEMM_FWD);
@@ -1483,8 +1507,9 @@ void Engine<T>::forward_layer(int l) {
                         &D.hub_fm.plan);
     const double nnz = double(D.view.local_ptr[nc + nm] - D.view.local_ptr[nc]) +
                        double(D.view.remote_nnz());
-    kend(QGNN_K_SPMM_FWD, nm * (24.0 + 2 * din * sizeof(T)) + nnz * (4 + sizeof(T)) +
-                              double(D.view.num_remote) * din * sizeof(T), s_main_, nk,
+    kend(QGNN_K_SPMM_FWD, nm * (24.0 + din * sizeof(T)) + nnz * (4 + sizeof(T)) +
+                              double(D.view.src_rows_marginal + D.view.src_slots_marginal) *
+                                  din * sizeof(T), s_main_, nk,
          (nnz + nm) * din * sizeof(T));
     const int64_t g0 = one_gemm ? 0 : nc, gn = one_gemm ? nc + nm : nm;
     kbegin(QGNN_K_GEMM_FWD);
@@ -1558,7 +1583,8 @@ void Engine<T>::backward_layer(int l) {
                           nullptr, nullptr, nullptr, 0, D.view.num_remote, D.partials.p, ldi,
                           &D.hub_part.plan);
       kend(QGNN_K_PARTIALS, double(D.view.num_remote) * (8 + din * sizeof(T)) +
-                                double(D.view.remote_nnz()) * (4 + sizeof(T) + din * sizeof(T)),
+                                double(D.view.remote_nnz()) * (4 + sizeof(T)) +
+                                double(D.view.n_marginal) * din * sizeof(T),
            s_main_, nk, double(D.view.remote_nnz()) * din * sizeof(T));
     }
     if (!side_overlap()) quantize(D, k, D.partials.p, ldi);
@@ -1596,9 +1622,9 @@ void Engine<T>::backward_layer(int l) {
     const int nk = spmm(din, D.gbar.p, ldi, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
                         D.labwd.p, nullptr, nullptr, nullptr, 0, no, D.dh_next.p, ldi, &D.hub_bwd.plan,
                         mk ? D.h[t].p : nullptr, ldi);
-    kend(QGNN_K_SPMM_BWD, no * (16.0 + 2 * din * sizeof(T)) +
+    kend(QGNN_K_SPMM_BWD, no * (16.0 + (mk ? 2 : 1) * din * sizeof(T)) +
                               double(D.view.local_nnz()) * (4 + sizeof(T)) +
-                              double(no) * din * sizeof(T), s_main_, nk,
+                              double(D.view.src_rows_all) * din * sizeof(T), s_main_, nk,
          double(D.view.local_nnz() + no) * din * sizeof(T));
   }
   if (side_overlap())
@@ -1643,9 +1669,9 @@ void Engine<T>::forward_last_tf(int l) {
     kbegin(QGNN_K_SPMM_FWD);
     const int nk = spmm(dout, D.dz.p, ldo, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
                         D.lafwd.p, nullptr, nullptr, nullptr, 0, nc, D.h[l].p, ldo, &D.hub_fc.plan);
-    kend(QGNN_K_SPMM_FWD, nc * (16.0 + 2 * dout * sizeof(T)) +
+    kend(QGNN_K_SPMM_FWD, nc * (16.0 + dout * sizeof(T)) +
                               double(D.view.local_ptr[nc]) * (4 + sizeof(T)) +
-                              double(no) * dout * sizeof(T), s_main_, nk,
+                              double(D.view.src_rows_central) * dout * sizeof(T), s_main_, nk,
          double(D.view.local_ptr[nc] + nc) * dout * sizeof(T));
   }
   if (side) {
@@ -1670,8 +1696,9 @@ void Engine<T>::forward_last_tf(int l) {
                         &D.hub_fm.plan);
     const double nnz = double(D.view.local_ptr[nc + nm] - D.view.local_ptr[nc]) +
                        double(D.view.remote_nnz());
-    kend(QGNN_K_SPMM_FWD, nm * (24.0 + 2 * dout * sizeof(T)) + nnz * (4 + sizeof(T)) +
-                              double(nr) * dout * sizeof(T), s_main_, nk,
+    kend(QGNN_K_SPMM_FWD, nm * (24.0 + dout * sizeof(T)) + nnz * (4 + sizeof(T)) +
+                              double(D.view.src_rows_marginal + D.view.src_slots_marginal) *
+                                  dout * sizeof(T), s_main_, nk,
          (nnz + nm) * dout * sizeof(T));
   }
 }
@@ -1695,7 +1722,8 @@ void Engine<T>::backward_last_tf(int l) {
       const int nk = spmm(dout, D.dh.p, ldo, nullptr, 0, nullptr, D.sptr.p, D.srow.p, D.salpha.p,
                           nullptr, nullptr, nullptr, 0, nr, D.gpart.p, ldo, &D.hub_part.plan);
       kend(QGNN_K_PARTIALS, double(nr) * (8 + dout * sizeof(T)) +
-                                double(D.view.remote_nnz()) * (4 + sizeof(T) + dout * sizeof(T)),
+                                double(D.view.remote_nnz()) * (4 + sizeof(T)) +
+                                double(D.view.n_marginal) * dout * sizeof(T),
            s_main_, nk, double(D.view.remote_nnz()) * dout * sizeof(T));
       kbegin(QGNN_K_GEMM_DGRAD);
       QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, D.gpart.p, ldo, W, din, dout, nullptr, 0, nr,
@@ -1716,9 +1744,9 @@ void Engine<T>::backward_last_tf(int l) {
     kbegin(QGNN_K_SPMM_BWD);
     const int nk = spmm(dout, D.dh.p, ldo, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
                         D.labwd.p, nullptr, nullptr, nullptr, 0, no, D.gbar.p, ldo, &D.hub_bwd.plan);
-    kend(QGNN_K_SPMM_BWD, no * (16.0 + 2 * dout * sizeof(T)) +
+    kend(QGNN_K_SPMM_BWD, no * (16.0 + dout * sizeof(T)) +
                               double(D.view.local_nnz()) * (4 + sizeof(T)) +
-                              double(no) * dout * sizeof(T), s_main_, nk,
+                              double(D.view.src_rows_all) * dout * sizeof(T), s_main_, nk,
          double(D.view.local_nnz() + no) * dout * sizeof(T));
     kbegin(QGNN_K_GEMM_DGRAD);
     if constexpr (sizeof(T) == 4)
@@ -1886,7 +1914,11 @@ void Engine<T>::finish_epoch(qgnn_epoch_metrics* m) {
   float ms = 0;
   QGNN_CUDA(cudaEventElapsedTime(&ms, ev_a_, ev_b_));
   QGNN_CALL(qgnn_ctx_check(ctx_, s_main_));
+  double kms0[QGNN_K_COUNT];
+  for (int c = 0; c < QGNN_K_COUNT; ++c) kms0[c] = kst_[c].ms;
   flush_kstats();
+  double kms[QGNN_K_COUNT];
+  for (int c = 0; c < QGNN_K_COUNT; ++c) kms[c] = kst_[c].ms - kms0[c];
   launches_last_ = launches_;
 
   // loss / accuracy (engine.hpp:393-397, 803-849)
@@ -1940,7 +1972,12 @@ void Engine<T>::finish_epoch(qgnn_epoch_metrics* m) {
   em.msgs_b8 = msgs_b_[2];
   em.msgs_fp = msgs_b_[3];
   em.ms_total = ms;
-  em.ms_quant = kst_[QGNN_K_QUANT].ms;
+  em.ms_quant = kms[QGNN_K_QUANT];
+  em.ms_exchange = kms[QGNN_K_EXCHANGE];
+  em.ms_dequant = kms[QGNN_K_DEQUANT];
+  em.ms_spmm = kms[QGNN_K_SPMM_FWD] + kms[QGNN_K_SPMM_BWD] + kms[QGNN_K_PARTIALS];
+  em.ms_gemm = kms[QGNN_K_GEMM_FWD] + kms[QGNN_K_GEMM_DGRAD] + kms[QGNN_K_GEMM_WGRAD];
+  em.ms_other = kms[QGNN_K_ELEMWISE];
   resolve_seconds_ = 0;
   if (s_.bit_mode == kAdaptive) adaptive_round(&em);
   em.plan_version = plan_version_;
@@ -2285,6 +2322,64 @@ int qgnn_nccl_unique_id(void* out128) {
   ncclUniqueId id;
   QGNN_NCCL(nccl().GetUniqueId(&id));
   std::memcpy(out128, &id, sizeof(id));
+  QGNN_API_END
+}
+
+// ---- production SpMM plan (aggregate.hpp:94-165 at scale) ----------------------
+struct qgnn_spmm_plan {
+  qgnn_ctx* ctx = nullptr;
+  int64_t row_begin = 0, n_rows = 0, max_dim = 0;
+  qgnn_b200::Hubs hubs;
+};
+
+int qgnn_spmm_plan_create(qgnn_ctx* ctx, const int64_t* ptr_a, const int64_t* ptr_b,
+                          int64_t row_begin, int64_t n_rows, int64_t max_dim, int64_t hub_deg,
+                          qgnn_spmm_plan** out) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(ctx && out && ptr_a, QGNN_EINVAL, "spmm_plan_create: null argument");
+  QGNN_REQUIRE(row_begin >= 0 && n_rows >= 0 && max_dim > 0 && hub_deg >= 1, QGNN_EINVAL,
+               "spmm_plan_create: bad sizes");
+  auto* p = new qgnn_spmm_plan;
+  p->ctx = ctx;
+  p->row_begin = row_begin;
+  p->n_rows = n_rows;
+  p->max_dim = round_up(max_dim, 8);
+  try {
+    build_hub_plan(p->hubs, ptr_a, ptr_b, row_begin, row_begin + n_rows, p->max_dim, hub_deg);
+  } catch (...) {
+    delete p;
+    throw;
+  }
+  *out = p;
+  QGNN_API_END
+}
+
+int qgnn_spmm_plan_destroy(qgnn_spmm_plan* p) {
+  delete p;
+  return QGNN_OK;
+}
+
+int qgnn_spmm_plan_run(qgnn_spmm_plan* p, int64_t dim, const float* x, int64_t ld_x,
+                       const float* y, int64_t ld_y, const float* self_alpha,
+                       const int64_t* ptr_a, const int32_t* col_a, const float* alpha_a,
+                       const int64_t* ptr_b, const int32_t* col_b, const float* alpha_b,
+                       const float* mask, int64_t ld_mask, float* out, int64_t ld_out,
+                       void* stream) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(p, QGNN_EINVAL, "spmm_plan_run: null plan");
+  QGNN_REQUIRE(dim > 0 && dim <= p->max_dim, QGNN_EINVAL, "spmm_plan_run: dim exceeds the plan");
+  const int64_t d4 = round_up(dim, 4);
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  QGNN_REQUIRE(ld_x % 4 == 0 && ld_out % 4 == 0 && d4 <= ld_x && d4 <= ld_out && al16(x) &&
+                   al16(out) && (!ptr_b || (ld_y % 4 == 0 && d4 <= ld_y && al16(y))) &&
+                   (!mask || (ld_mask % 4 == 0 && d4 <= ld_mask && al16(mask))),
+               QGNN_EINVAL,
+               "spmm_plan_run: fp32 rows must be 16-byte aligned with ld a multiple of 4 "
+               "columns covering round_up(dim, 4) (zero padded)");
+  if (p->n_rows == 0) return QGNN_OK;
+  spmm_f32(p->ctx, int(d4), x, ld_x, y, ld_y, self_alpha, ptr_a, col_a, alpha_a, ptr_b, col_b,
+           alpha_b, p->row_begin, p->n_rows, out, ld_out, &p->hubs.plan,
+           static_cast<cudaStream_t>(stream), mask, ld_mask);
   QGNN_API_END
 }
 

@@ -57,6 +57,8 @@ struct View {
   int32_t gpu_row(uint32_t node) const;
   std::vector<uint32_t> owned_sorted;   // == Part::owned
   std::vector<int32_t> owned_gpu_row;   // GPU row of owned_sorted[i]
+  // distinct source rows per SpMM call site (self rows included; §8d bytes)
+  int64_t src_rows_central = 0, src_rows_marginal = 0, src_rows_all = 0, src_slots_marginal = 0;
   int64_t local_nnz() const { return static_cast<int64_t>(local_col.size()); }
   int64_t remote_nnz() const { return static_cast<int64_t>(remote_slot.size()); }
 };

@@ -18,25 +18,12 @@ import numpy as np
 from . import _lib
 from ._lib import F32, F64, WIRE_GPU, WIRE_REF, check, lib
 
+# input generation lives outside the product (shared by both bench arms)
+from synth import generate_planted  # noqa: F401
+
 BIT_MODES = {"fp": 0, "fixed": 1, "uniform": 2, "adaptive": 3}
 KCLASSES = ["quant", "dequant", "spmm_fwd", "spmm_bwd", "partials", "gemm_fwd", "gemm_dgrad",
             "gemm_wgrad", "elemwise", "exchange"]
-
-
-def generate_planted(nodes: int, n_edges: int, feat: int, classes: int, blocks: int,
-                     cross_frac: float, gamma: float = 2.5, sep: float = 1.0, seed: int = 1):
-    """Planted-block power-law graph (host C++, csrc/host_graph.cpp:gen_planted)."""
-    g = dict(adj_ptr=np.zeros(nodes + 1, np.int64), adj=np.zeros(2 * n_edges, np.int32),
-             features=np.zeros((nodes, feat), np.float32), labels=np.zeros(nodes, np.int32),
-             train=np.zeros(nodes, np.uint8), val=np.zeros(nodes, np.uint8),
-             test=np.zeros(nodes, np.uint8))
-    check(lib.qgnn_generate_planted(nodes, n_edges, feat, classes, blocks, cross_frac, gamma, sep,
-                                    seed, g["adj_ptr"].ctypes.data, g["adj"].ctypes.data,
-                                    g["features"].ctypes.data, g["labels"].ctypes.data,
-                                    g["train"].ctypes.data, g["val"].ctypes.data,
-                                    g["test"].ctypes.data))
-    g["owner"] = (np.arange(nodes, dtype=np.int64) // (-(-nodes // blocks))).astype(np.uint32)
-    return g
 
 
 def partition_stats(g, owner, n_parts):
@@ -82,7 +69,7 @@ class Engine:
                  group_size: int = 4, period: int = 50, lr: float = 0.01, theta: float = 3e-9,
                  gamma: float = 5e-5, dtype: str = "f32", layout: Optional[int] = None,
                  owner=None, rank: int = 0, world: int = 1, device: int = 0,
-                 nccl_id: Optional[bytes] = None, kstats: bool = False):
+                 nccl_id: Optional[bytes] = None, kstats: bool = False, overlap: int = 1):
         s = _lib.Settings()
         s.sage = int(sage)
         s.n_dims = len(dims)
@@ -101,7 +88,7 @@ class Engine:
         s.dtype = F64 if dtype == "f64" else F32
         s.layout = (WIRE_REF if dtype == "f64" else WIRE_GPU) if layout is None else layout
         s.rank, s.world, s.device = rank, world, device
-        s.overlap = 1
+        s.overlap = int(overlap)
         s.kstats = int(kstats)
         self.settings = s
         self.dims = list(dims)

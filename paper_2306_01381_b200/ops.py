@@ -152,6 +152,40 @@ def csr_aggregate(x, ptr_a, col_a, alpha_a, out, self_alpha=None, y=None, ptr_b=
     return out
 
 
+class SpmmPlan:
+    """Production fp32 K4 over one CSR row range (qgnn_spmm_plan_*): the
+    engine's kernels, hub segmentation and degree-sorted narrow rows.
+    ``ptr_a``/``ptr_b`` are host (numpy int64) row pointers; runs take device
+    tensors."""
+
+    def __init__(self, ptr_a, row_begin, n_rows, max_dim, ptr_b=None, hub_deg=128):
+        self._pa = np.ascontiguousarray(ptr_a, np.int64)
+        self._pb = None if ptr_b is None else np.ascontiguousarray(ptr_b, np.int64)
+        h = C.c_void_p()
+        check(lib.qgnn_spmm_plan_create(ctx(), self._pa.ctypes.data,
+                                        None if self._pb is None else self._pb.ctypes.data,
+                                        row_begin, n_rows, max_dim, hub_deg, C.byref(h)))
+        self._h = h
+
+    def run(self, dim, x, ptr_a, col_a, alpha_a, out, self_alpha=None, y=None, ptr_b=None,
+            col_b=None, alpha_b=None, mask=None):
+        check(lib.qgnn_spmm_plan_run(self._h, dim, _ptr(x), x.stride(0), _ptr(y),
+                                     y.stride(0) if y is not None else 0, _ptr(self_alpha),
+                                     _ptr(ptr_a), _ptr(col_a), _ptr(alpha_a), _ptr(ptr_b),
+                                     _ptr(col_b), _ptr(alpha_b), _ptr(mask),
+                                     mask.stride(0) if mask is not None else 0, _ptr(out),
+                                     out.stride(0), _stream()))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.qgnn_spmm_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
 # ---- model.hpp / matrix.hpp ---------------------------------------------------------
 def dense_forward(a, w, out, relu=True, rows=None, row_begin=0, n_rows=None):
     if n_rows is None:

@@ -59,6 +59,7 @@ def test_chunk_sizes_ref_and_gpu_layout():
     assert lib.qgnn_chunk_wire_bytes(256, 8, _lib.WIRE_GPU, 0) == 16 + 256
     assert lib.qgnn_chunk_wire_bytes(100, 2, _lib.WIRE_GPU, 0) == 16 + 32
     assert lib.qgnn_chunk_wire_bytes(100, 0, _lib.WIRE_GPU, 0) == 400
+    assert lib.qgnn_chunk_wire_bytes(10, 0, _lib.WIRE_GPU, 0) == 48  # raw rows padded to 16 B
     assert lib.qgnn_chunk_wire_bytes(100, 0, _lib.WIRE_REF, 1) == 800
 
 
