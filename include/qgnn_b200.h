@@ -80,21 +80,39 @@ int qgnn_wire_layout(const int32_t* bits, int64_t n, int64_t dim, int layout, in
  * and writes its chunk at out + offsets[i].  bits[i] == 0 copies the raw row
  * (fp mode, engine.hpp:473-481).  win_lo/win_hi (optional, dtype, [n]) fold
  * the row extrema into the message's trace window (trace.hpp:86-91).
- * set_of == NULL means every message belongs to set 0.  [dev] for all arrays. */
+ * set_of == NULL means every message belongs to set 0.  [dev] for all arrays.
+ * envelope (QGNN_WIRE_GPU): source id | plan version << 8 (each mod 256); the
+ * chunk header records (source, set index = destination, version) — the
+ * routing fields of the reference's ExchangePayload (engine.hpp:530-541). */
 int qgnn_quantize_pack(qgnn_ctx* ctx, const void* values, int dtype, int64_t ld, int64_t dim,
                        int64_t n, const int32_t* rows, const uint32_t* ids, const uint8_t* bits,
                        const uint64_t* offsets, const uint16_t* set_of, const uint64_t* set_keys,
-                       int layout, uint8_t* out, void* win_lo, void* win_hi, void* stream);
+                       int layout, uint8_t* out, void* win_lo, void* win_hi, uint32_t envelope,
+                       void* stream);
+
+/* decode_message_set's index checks (codec.hpp:82-95), host side: the n
+ * entries in wire order (bits[k], offsets[k], dims[k]) must tile [0, n_bytes)
+ * contiguously with qgnn_chunk_wire_bytes each and total_bytes == n_bytes.
+ * Fails with QGNN_EDECODE and the reference's message ("message set: byte
+ * count mismatch", "... index offsets not contiguous", "chunk: truncated
+ * payload", "message set: trailing bytes").  The per-chunk width / count check
+ * against the index runs on the device in K3. */
+int qgnn_decode_validate(const uint8_t* bits, const uint64_t* offsets, const uint64_t* dims,
+                         int64_t n, int layout, int dtype, uint64_t total_bytes,
+                         uint64_t n_bytes);
 
 /* ---- K3 unpack + dequantize + scatter: quant.hpp:92-99, codec.hpp:80-96 --------
  * Decodes message i's chunk at in + offsets[i] (validating width and count
  * against bits[i] / dim — DecodeError semantics) and stores (accumulate == 0,
  * engine.hpp:607-618) or adds (accumulate == 1, engine.hpp:729-733) the values
- * into row dst_rows[i] of `out` (dst_rows == NULL: row i). */
+ * into row dst_rows[i] of `out` (dst_rows == NULL: row i).  expect_envelope
+ * (optional [dev] [n], QGNN_WIRE_GPU): source | destination << 8 | plan
+ * version << 16 expected of each chunk; a mismatch is latched as QGNN_EPROTOCOL
+ * ("misrouted payload" / "plan version skew", engine.hpp:530-541). */
 int qgnn_dequant_scatter(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int64_t dim,
                          const uint8_t* bits, const uint64_t* offsets, int layout,
                          const int32_t* dst_rows, int accumulate, void* out, int dtype,
-                         int64_t ld, void* stream);
+                         int64_t ld, const uint32_t* expect_envelope, void* stream);
 
 /* ---- K4 CSR aggregation: aggregate.hpp:94-165 ----------------------------------
  * For each listed row r (rows != NULL: rows[k]; else row_begin + k):
@@ -185,6 +203,27 @@ int qgnn_exchange_plan(const int64_t* adj_ptr, const int32_t* adj, int64_t n,
                        int bits, int bwd, int layout, int dtype, uint64_t* send_bytes,
                        uint64_t* recv_bytes);
 
+/* ---- K2 exchange: ring_all2all / comm_seconds (commsim/exchange.hpp:45-78,
+ * trainer/engine.hpp:507-522) and the mailbox send / take (engine.hpp:502,
+ * :528-529) ------------------------------------------------------------------
+ * One rank of a group of `world` ranks.  id128 = qgnn_nccl_unique_id (NCCL
+ * over NVLink / NVSwitch; NULL allowed for world == 1) or qgnn_loopback_id
+ * (ranks as threads of one process on one device: tests). */
+typedef struct qgnn_comm qgnn_comm;
+int qgnn_comm_create(const void* id128, int world, int rank, int device, qgnn_comm** out);
+int qgnn_comm_destroy(qgnn_comm* comm);
+/* Irregular all-to-all of packed payloads in one grouped send/receive: this
+ * rank sends send_bytes[r] bytes from send + send_off[r] to rank r and
+ * receives recv_bytes[r] bytes into recv + recv_off[r] (host arrays [world];
+ * [dev] buffers; r == rank is a device copy).  Sizes come from
+ * qgnn_exchange_plan, so both sides agree without a handshake
+ * (negotiate_buffers, plan.hpp:140-154); the loopback transport checks the
+ * agreement and fails with QGNN_EPROTOCOL like engine.hpp:546-550.
+ * Asynchronous on `stream`. */
+int qgnn_exchange(qgnn_comm* comm, const void* send, const uint64_t* send_off,
+                  const uint64_t* send_bytes, void* recv, const uint64_t* recv_off,
+                  const uint64_t* recv_bytes, void* stream);
+
 /* ---- host: assigner (assigner/solve.hpp) ---------------------------------------
  * One instance = one tensor key across device pairs.  Messages are flat,
  * grouped by pair: pair p has pair_count[p] messages (id, dim, lo, hi,
@@ -228,6 +267,9 @@ typedef struct {
                               overlap the exchange on the comm stream; 2: one GPU, K1/K3
                               also on a side stream next to the central rows */
   int32_t kstats;          /* 1: time every kernel class with CUDA events (bench roofline) */
+  int32_t transport;       /* world == 1 only: 0 zero copy between the partitions of the
+                              GPU (default); 1 every pair through NCCL self send/receive
+                              (the multi-GPU exchange path, run and timed on one device) */
 } qgnn_settings;
 
 typedef struct {

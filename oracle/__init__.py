@@ -13,4 +13,4 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline
 leg may import this package; the product (``paper_2306_01381_b200``) never
 does.
 """
-from .oracle import port, ref, ref_available, build  # noqa: F401
+from .oracle import RefError, build, port, ref, ref_available  # noqa: F401

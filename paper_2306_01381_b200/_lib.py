@@ -67,7 +67,7 @@ class Settings(C.Structure):
                 ("n_parts", C.c_int64), ("lr", C.c_double), ("theta", C.c_double),
                 ("gamma", C.c_double), ("dtype", C.c_int32), ("layout", C.c_int32),
                 ("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32),
-                ("overlap", C.c_int32), ("kstats", C.c_int32)]
+                ("overlap", C.c_int32), ("kstats", C.c_int32), ("transport", C.c_int32)]
 
 
 class EpochMetrics(C.Structure):
@@ -99,9 +99,10 @@ _SIGS = {
     "qgnn_chunk_wire_bytes": (u64, [u64, C.c_int, C.c_int, C.c_int]),
     "qgnn_wire_layout": (C.c_int, [vp, i64, i64, C.c_int, C.c_int, vp, vp, C.POINTER(u64)]),
     "qgnn_quantize_pack": (C.c_int, [vp, vp, C.c_int, i64, i64, i64, vp, vp, vp, vp, vp, vp,
-                                     C.c_int, vp, vp, vp, vp]),
+                                     C.c_int, vp, vp, vp, u32, vp]),
+    "qgnn_decode_validate": (C.c_int, [vp, vp, vp, i64, C.c_int, C.c_int, u64, u64]),
     "qgnn_dequant_scatter": (C.c_int, [vp, vp, i64, i64, vp, vp, C.c_int, vp, C.c_int, vp,
-                                       C.c_int, i64, vp]),
+                                       C.c_int, i64, vp, vp]),
     "qgnn_csr_aggregate": (C.c_int, [vp, C.c_int, i64, vp, i64, vp, i64, vp, vp, vp, vp, vp, vp,
                                      vp, vp, i64, i64, vp, i64, vp]),
     "qgnn_spmm_plan_create": (C.c_int, [vp, vp, vp, i64, i64, i64, i64, C.POINTER(vp)]),
@@ -123,6 +124,9 @@ _SIGS = {
     "qgnn_compute_coeffs": (C.c_int, [vp, vp, i64, C.c_int, vp, vp]),
     "qgnn_exchange_plan": (C.c_int, [vp, vp, i64, vp, i64, C.c_int, C.c_int, i64, C.c_int,
                                      C.c_int, C.c_int, C.c_int, vp, vp]),
+    "qgnn_comm_create": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+    "qgnn_comm_destroy": (C.c_int, [vp]),
+    "qgnn_exchange": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "qgnn_solve_instance": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, dbl, i64,
                                       C.c_int, vp, vp]),
     "qgnn_fit_affine": (C.c_int, [vp, vp, i64, vp, vp]),

@@ -22,6 +22,18 @@
 namespace qgnn_b200 {
 
 constexpr int kHdrGpu = 16;
+
+// GPU-layout chunk envelope (header word 3 above the width byte): source
+// partition, destination partition and plan version, each mod 256 — the
+// per-message form of the reference payload's routing fields (source, target,
+// plan_version; engine.hpp:530-541).  `env` = source | version << 8;
+// the destination is the message's set index.
+__device__ __forceinline__ uint32_t env_word(int b, uint32_t env, const uint16_t* set_of,
+                                             int64_t m) {
+  const uint32_t dst = set_of ? set_of[m] : 0u;
+  return static_cast<uint32_t>(b) | (env & 0xffu) << 8 | (dst & 0xffu) << 16 |
+         ((env >> 8) & 0xffu) << 24;
+}
 constexpr int kHdrRef = 25;
 
 __host__ __device__ inline uint64_t packed_bytes(uint64_t count, int b) {
@@ -91,7 +103,7 @@ __global__ void __launch_bounds__(256) k_quantize_pack(
     const uint32_t* __restrict__ ids, const uint8_t* __restrict__ bits,
     const uint64_t* __restrict__ offsets, const uint16_t* __restrict__ set_of,
     const uint64_t* __restrict__ set_keys, int layout, uint8_t* __restrict__ out,
-    T* __restrict__ win_lo, T* __restrict__ win_hi, int* __restrict__ err) {
+    T* __restrict__ win_lo, T* __restrict__ win_hi, int* __restrict__ err, uint32_t env) {
   const int lane = threadIdx.x & 31;
   const int64_t m = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (m >= n) return;
@@ -132,7 +144,7 @@ __global__ void __launch_bounds__(256) k_quantize_pack(
       h.x = __float_as_uint(static_cast<float>(scale));
       h.y = __float_as_uint(static_cast<float>(lo_d));
       h.z = static_cast<uint32_t>(dim);
-      h.w = static_cast<uint32_t>(b);
+      h.w = env_word(b, env, set_of, m);
       *reinterpret_cast<uint4*>(chunk) = h;
     }
     payload = chunk + kHdrGpu;
@@ -190,7 +202,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_dequant_scatter(
     const uint8_t* __restrict__ in, int64_t n, int dim, const uint8_t* __restrict__ bits,
     const uint64_t* __restrict__ offsets, int layout, const int32_t* __restrict__ dst_rows,
-    int accumulate, T* __restrict__ out, int64_t ld, int* __restrict__ err) {
+    int accumulate, T* __restrict__ out, int64_t ld, int* __restrict__ err,
+    const uint32_t* __restrict__ expect) {
   const int lane = threadIdx.x & 31;
   const int64_t m = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (m >= n) return;
@@ -216,6 +229,10 @@ __global__ void __launch_bounds__(256) k_dequant_scatter(
     count = h.z;
     hb = static_cast<int>(h.w & 0xff);
     payload = chunk + kHdrGpu;
+    if (expect && (h.w >> 8) != expect[m]) {  // engine.hpp:530-541
+      if (lane == 0) atomicOr(err, kErrProtocol);
+      return;
+    }
   } else {
     hb = chunk[0];
     count = load_u64_bytes(chunk + 1);
@@ -336,7 +353,7 @@ __global__ void __launch_bounds__(256, MINB) k_quantize_pack_f32(
     const uint8_t* __restrict__ bits, const uint64_t* __restrict__ offsets,
     const uint16_t* __restrict__ set_of, const uint64_t* __restrict__ set_keys,
     uint8_t* __restrict__ out, float* __restrict__ win_lo, float* __restrict__ win_hi,
-    int* __restrict__ err) {
+    int* __restrict__ err, uint32_t env) {
   const int lane = threadIdx.x & 31;
   const int64_t wstride = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   for (int64_t m = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; m < n;
@@ -404,7 +421,7 @@ __global__ void __launch_bounds__(256, MINB) k_quantize_pack_f32(
     h.x = __float_as_uint(static_cast<float>(scale));
     h.y = __float_as_uint(lo);
     h.z = static_cast<uint32_t>(dim);
-    h.w = static_cast<uint32_t>(b);
+    h.w = env_word(b, env, set_of, m);
     *reinterpret_cast<uint4*>(chunk) = h;
   }
   uint8_t* payload = chunk + kHdrGpu;
@@ -523,7 +540,7 @@ __global__ void __launch_bounds__(256, MINB) k_quantize_pack_lean(
     const uint8_t* __restrict__ bits, const uint64_t* __restrict__ offsets,
     const uint16_t* __restrict__ set_of, const uint64_t* __restrict__ set_keys,
     uint8_t* __restrict__ out, float* __restrict__ win_lo, float* __restrict__ win_hi,
-    int* __restrict__ err) {
+    int* __restrict__ err, uint32_t env) {
   const int lane = threadIdx.x & 31;
   const int64_t wstride = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const int nchunk = dim >> 2;
@@ -596,7 +613,7 @@ __global__ void __launch_bounds__(256, MINB) k_quantize_pack_lean(
       h.x = __float_as_uint(static_cast<float>(scale));
       h.y = __float_as_uint(lo);
       h.z = static_cast<uint32_t>(dim);
-      h.w = static_cast<uint32_t>(b);
+      h.w = env_word(b, env, set_of, m);
       *reinterpret_cast<uint4*>(chunk) = h;
     }
     const uint64_t key = rng_fork(set_keys[set_of ? set_of[m] : 0], ids[m]);
@@ -610,7 +627,8 @@ __global__ void __launch_bounds__(256, MINB) k_quantize_pack_lean(
 __global__ void __launch_bounds__(256) k_dequant_f32(
     const uint8_t* __restrict__ in, int64_t n, int dim, const uint8_t* __restrict__ bits,
     const uint64_t* __restrict__ offsets, const int32_t* __restrict__ dst_rows, int accumulate,
-    float* __restrict__ out, int64_t ld, int* __restrict__ err, const float* __restrict__ mask,
+    float* __restrict__ out, int64_t ld, int* __restrict__ err, const uint32_t* __restrict__ expect,
+    const float* __restrict__ mask,
     int64_t ldm) {
   const int lane = threadIdx.x & 31;
   const int64_t wstride = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -632,6 +650,10 @@ __global__ void __launch_bounds__(256) k_dequant_f32(
   const uint4 h = *reinterpret_cast<const uint4*>(chunk);
   if (static_cast<int>(h.w & 0xff) != b || h.z != static_cast<uint32_t>(dim)) {
     if (lane == 0) atomicOr(err, kErrDecode);
+    continue;
+  }
+  if (expect && (h.w >> 8) != expect[m]) {  // misrouted / plan-version skew (engine.hpp:530-541)
+    if (lane == 0) atomicOr(err, kErrProtocol);
     continue;
   }
   const float sc = __uint_as_float(h.x), zp = __uint_as_float(h.y);
@@ -706,10 +728,32 @@ int qgnn_wire_layout(const int32_t* bits, int64_t n, int64_t dim, int layout, in
   QGNN_API_END
 }
 
+int qgnn_decode_validate(const uint8_t* bits, const uint64_t* offsets, const uint64_t* dims,
+                         int64_t n, int layout, int dtype, uint64_t total_bytes,
+                         uint64_t n_bytes) {
+  QGNN_API_BEGIN
+  const int elem = dtype == QGNN_F64 ? 8 : 4;
+  QGNN_REQUIRE(n_bytes == total_bytes, QGNN_EDECODE, "message set: byte count mismatch");
+  uint64_t expect = 0;
+  for (int64_t k = 0; k < n; ++k) {
+    QGNN_REQUIRE(offsets[k] == expect, QGNN_EDECODE, "message set: index offsets not contiguous");
+    const int b = bits[k];
+    QGNN_REQUIRE(b == 2 || b == 4 || b == 8 || b == 0, QGNN_EDECODE, "chunk: bad bit width");
+    const uint64_t cb = chunk_bytes(dims[k], b, layout, elem);
+    QGNN_REQUIRE(b == 0 || offsets[k] + (layout == QGNN_WIRE_REF ? kHdrRef : kHdrGpu) <= n_bytes,
+                 QGNN_EDECODE, "chunk: truncated header");
+    QGNN_REQUIRE(offsets[k] + cb <= n_bytes, QGNN_EDECODE, "chunk: truncated payload");
+    expect = offsets[k] + cb;
+  }
+  QGNN_REQUIRE(expect == n_bytes, QGNN_EDECODE, "message set: trailing bytes");
+  QGNN_API_END
+}
+
 int qgnn_quantize_pack(qgnn_ctx* ctx, const void* values, int dtype, int64_t ld, int64_t dim,
                        int64_t n, const int32_t* rows, const uint32_t* ids, const uint8_t* bits,
                        const uint64_t* offsets, const uint16_t* set_of, const uint64_t* set_keys,
-                       int layout, uint8_t* out, void* win_lo, void* win_hi, void* stream) {
+                       int layout, uint8_t* out, void* win_lo, void* win_hi, uint32_t envelope,
+                       void* stream) {
   QGNN_API_BEGIN
   QGNN_REQUIRE(ctx, QGNN_EINVAL, "quantize_pack: null context");
   QGNN_REQUIRE(dim > 0, QGNN_EINVAL, "quantize: empty input");
@@ -738,10 +782,11 @@ int qgnn_quantize_pack(qgnn_ctx* ctx, const void* values, int dtype, int64_t ld,
   if (lean && d % 4 == 0)                                                                           \
     k_quantize_pack_lean<NVV, MB><<<fblocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets, \
                                                              set_of, set_keys, out, wl, wh,         \
-                                                             ctx->d_err);                           \
+                                                             ctx->d_err, envelope);                 \
   else                                                                                              \
     k_quantize_pack_f32<NVV, MB><<<fblocks, threads, 0, s>>>(v, ld, d, n, rows, ids, bits, offsets,  \
-                                                            set_of, set_keys, out, wl, wh, ctx->d_err)
+                                                            set_of, set_keys, out, wl, wh, ctx->d_err, \
+                                                            envelope)
 #define QGNN_K1_NV(NVV)                 \
   if (minb >= 4)                        \
     QGNN_K1_LAUNCH(NVV, 4);             \
@@ -764,12 +809,12 @@ int qgnn_quantize_pack(qgnn_ctx* ctx, const void* values, int dtype, int64_t ld,
     k_quantize_pack<double><<<blocks, threads, 0, s>>>(
         static_cast<const double*>(values), ld, static_cast<int>(dim), n, rows, ids, bits, offsets,
         set_of, set_keys, layout, out, static_cast<double*>(win_lo), static_cast<double*>(win_hi),
-        ctx->d_err);
+        ctx->d_err, envelope);
   else
     k_quantize_pack<float><<<blocks, threads, 0, s>>>(
         static_cast<const float*>(values), ld, static_cast<int>(dim), n, rows, ids, bits, offsets,
         set_of, set_keys, layout, out, static_cast<float*>(win_lo), static_cast<float*>(win_hi),
-        ctx->d_err);
+        ctx->d_err, envelope);
   check_launch("k_quantize_pack");
   QGNN_API_END
 }
@@ -777,7 +822,7 @@ int qgnn_quantize_pack(qgnn_ctx* ctx, const void* values, int dtype, int64_t ld,
 int qgnn_dequant_scatter(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int64_t dim,
                          const uint8_t* bits, const uint64_t* offsets, int layout,
                          const int32_t* dst_rows, int accumulate, void* out, int dtype,
-                         int64_t ld, void* stream) {
+                         int64_t ld, const uint32_t* expect_envelope, void* stream) {
   QGNN_API_BEGIN
   QGNN_REQUIRE(ctx, QGNN_EINVAL, "dequant_scatter: null context");
   if (n == 0) return QGNN_OK;
@@ -789,15 +834,19 @@ int qgnn_dequant_scatter(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int64_t di
   if (fast)
     k_dequant_f32<<<std::min<int64_t>(blocks, int64_t(ctx->num_sms) * 16), threads, 0, s>>>(
         in, n, static_cast<int>(dim), bits, offsets, dst_rows, accumulate, static_cast<float*>(out),
-        ld, ctx->d_err, nullptr, 0);
+        ld, ctx->d_err, layout == QGNN_WIRE_GPU ? expect_envelope : nullptr, nullptr, 0);
   else if (dtype == QGNN_F64)
     k_dequant_scatter<double><<<blocks, threads, 0, s>>>(in, n, static_cast<int>(dim), bits,
                                                          offsets, layout, dst_rows, accumulate,
-                                                         static_cast<double*>(out), ld, ctx->d_err);
+                                                         static_cast<double*>(out), ld, ctx->d_err,
+                                                         layout == QGNN_WIRE_GPU ? expect_envelope
+                                                                                 : nullptr);
   else
     k_dequant_scatter<float><<<blocks, threads, 0, s>>>(in, n, static_cast<int>(dim), bits,
                                                         offsets, layout, dst_rows, accumulate,
-                                                        static_cast<float*>(out), ld, ctx->d_err);
+                                                        static_cast<float*>(out), ld, ctx->d_err,
+                                                        layout == QGNN_WIRE_GPU ? expect_envelope
+                                                                                : nullptr);
   check_launch("k_dequant_scatter");
   QGNN_API_END
 }
@@ -813,7 +862,7 @@ __global__ void __launch_bounds__(256) k_dequant_rows_f32(
     const int32_t* __restrict__ ptr, const int32_t* __restrict__ msg, int dim,
     const uint8_t* __restrict__ bits, const uint64_t* __restrict__ offsets,
     float* __restrict__ out, int64_t ld, const float* __restrict__ mask, int64_t ldm,
-    int* __restrict__ err) {
+    int* __restrict__ err, const uint32_t* __restrict__ expect) {
   const int lane = threadIdx.x & 31;
   const int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (g >= n_rows) return;
@@ -842,6 +891,10 @@ __global__ void __launch_bounds__(256) k_dequant_rows_f32(
     const uint4 h = *reinterpret_cast<const uint4*>(chunk);
     if (static_cast<int>(h.w & 0xff) != b || h.z != static_cast<uint32_t>(dim)) {
       if (lane == 0) atomicOr(err, kErrDecode);
+      continue;
+    }
+    if (expect && (h.w >> 8) != expect[m]) {
+      if (lane == 0) atomicOr(err, kErrProtocol);
       continue;
     }
     const float sc = __uint_as_float(h.x), zp = __uint_as_float(h.y);
@@ -892,22 +945,23 @@ __global__ void __launch_bounds__(256) k_dequant_rows_f32(
 void dequant_rows_add_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n_rows, const int32_t* rows,
                           const int32_t* ptr, const int32_t* msg, int dim, const uint8_t* bits,
                           const uint64_t* offsets, float* out, int64_t ld, const float* mask,
-                          int64_t ldm, cudaStream_t s) {
+                          int64_t ldm, const uint32_t* expect, cudaStream_t s) {
   if (n_rows == 0) return;
   const dim3 grid(unsigned(ceil_div(n_rows * 32, 64)), unsigned(ceil_div(dim, 512)));
   k_dequant_rows_f32<<<grid, 64, 0, s>>>(
-      in, n_rows, rows, ptr, msg, dim, bits, offsets, out, ld, mask, ldm, ctx->d_err);
+      in, n_rows, rows, ptr, msg, dim, bits, offsets, out, ld, mask, ldm, ctx->d_err, expect);
   check_launch("k_dequant_rows_f32");
 }
 
 // fp32 GPU-layout decode + scatter-add with the ReLU-backward mask (engine)
 void dequant_add_masked_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int dim,
                             const uint8_t* bits, const uint64_t* offsets, const int32_t* dst_rows,
-                            float* out, int64_t ld, const float* mask, int64_t ldm, cudaStream_t s) {
+                            float* out, int64_t ld, const float* mask, int64_t ldm,
+                            const uint32_t* expect, cudaStream_t s) {
   if (n == 0) return;
   const int64_t blocks = ceil_div(n * 32, 256);
   k_dequant_f32<<<std::min<int64_t>(blocks, int64_t(ctx->num_sms) * 16), 256, 0, s>>>(
-      in, n, dim, bits, offsets, dst_rows, 1, out, ld, ctx->d_err, mask, ldm);
+      in, n, dim, bits, offsets, dst_rows, 1, out, ld, ctx->d_err, expect, mask, ldm);
   check_launch("k_dequant_f32");
 }
 }  // namespace qgnn_b200

@@ -18,6 +18,8 @@ enum : int {
   kErrDecode = 2,      // chunk width/count/index mismatch -> QGNN_EDECODE  (codec.hpp:82-95)
   kErrBadWidth = 4,    // bit width not in {2,4,8}         -> QGNN_EINVAL   (quant.hpp:61)
   kErrLabel = 8,       // label out of range               -> QGNN_EINVAL   (model.hpp:185)
+  kErrProtocol = 16,   // chunk envelope (source, target, plan version) differs from the
+                       // receiver's expectation           -> QGNN_EPROTOCOL (engine.hpp:530-541)
 };
 
 #define QGNN_CUDA(call)                                                                  \
@@ -61,7 +63,8 @@ struct Ctx;  // defined in ctx.cu
 // fp32 GPU-layout decode + scatter-add, ReLU-backward mask by h (codec.cu)
 void dequant_add_masked_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int dim,
                             const uint8_t* bits, const uint64_t* offsets, const int32_t* dst_rows,
-                            float* out, int64_t ld, const float* mask, int64_t ldm, cudaStream_t s);
+                            float* out, int64_t ld, const float* mask, int64_t ldm,
+                            const uint32_t* expect, cudaStream_t s);
 // fp32 input gradient out = A W^T for rows [row_begin, row_begin + n_rows) with the
 // ReLU-backward mask by h folded into the epilogue (dense.cu)
 void input_grad_masked_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int64_t din,
@@ -72,7 +75,7 @@ void input_grad_masked_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const flo
 void dequant_rows_add_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n_rows, const int32_t* rows,
                           const int32_t* ptr, const int32_t* msg, int dim, const uint8_t* bits,
                           const uint64_t* offsets, float* out, int64_t ld, const float* mask,
-                          int64_t ldm, cudaStream_t s);
+                          int64_t ldm, const uint32_t* expect, cudaStream_t s);
 // Adam with the bias corrections in device memory (captured epoch graphs, dense.cu)
 void adam_step_devbc(int dtype, void* p, void* m, void* v, const void* g, int64_t n, double lr,
                      double beta1, double beta2, double eps, const double* bc, cudaStream_t s);
@@ -144,7 +147,8 @@ int spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y
 // fp32 GPU-layout decode + scatter-add, ReLU-backward mask by h (codec.cu)
 void dequant_add_masked_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int dim,
                             const uint8_t* bits, const uint64_t* offsets, const int32_t* dst_rows,
-                            float* out, int64_t ld, const float* mask, int64_t ldm, cudaStream_t s);
+                            float* out, int64_t ld, const float* mask, int64_t ldm,
+                            const uint32_t* expect, cudaStream_t s);
 // fp32 input gradient out = A W^T for rows [row_begin, row_begin + n_rows) with the
 // ReLU-backward mask by h folded into the epilogue (dense.cu)
 void input_grad_masked_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int64_t din,
@@ -155,7 +159,7 @@ void input_grad_masked_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const flo
 void dequant_rows_add_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n_rows, const int32_t* rows,
                           const int32_t* ptr, const int32_t* msg, int dim, const uint8_t* bits,
                           const uint64_t* offsets, float* out, int64_t ld, const float* mask,
-                          int64_t ldm, cudaStream_t s);
+                          int64_t ldm, const uint32_t* expect, cudaStream_t s);
 // Adam with the bias corrections in device memory (captured epoch graphs, dense.cu)
 void adam_step_devbc(int dtype, void* p, void* m, void* v, const void* g, int64_t n, double lr,
                      double beta1, double beta2, double eps, const double* bc, cudaStream_t s);

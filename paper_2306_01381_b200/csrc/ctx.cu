@@ -84,6 +84,10 @@ int status_from_error_word(int w, std::string& msg) {
     msg = "message set: chunk disagrees with index";
     return QGNN_EDECODE;
   }
+  if (w & kErrProtocol) {
+    msg = "exchange: misrouted payload or plan version skew";
+    return QGNN_EPROTOCOL;
+  }
   return QGNN_OK;
 }
 

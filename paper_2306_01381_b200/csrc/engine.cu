@@ -45,6 +45,7 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -72,6 +73,7 @@ static NcclApi& nccl() {
   api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
   api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
   api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+  api.CommInitAll = reinterpret_cast<decltype(api.CommInitAll)>(sym("ncclCommInitAll"));
   api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
   api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
   api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
@@ -380,6 +382,9 @@ class Engine final : public EngineBase {
       // backward keys: destination rows with their incoming messages in ascending
       // source order (one fused scatter-add launch instead of one per source)
       DBuf<int32_t> acc_rows, acc_ptr, acc_msg;
+      // expected chunk envelope per message (source | destination << 8 |
+      // plan version << 16, each mod 256; GPU layout): checked by K3
+      DBuf<uint32_t> env;
       int64_t n_acc_rows = 0;
     };
     std::vector<SendMeta> snd;
@@ -420,6 +425,8 @@ class Engine final : public EngineBase {
     }
   }
   void build_messages();
+  void negotiate_sizes();
+  DBuf<uint64_t> neg_;
   void layout_pair(int k, int p, int q);
   void upload_key_meta(int k);
   void compute_bits_uniform();
@@ -428,7 +435,7 @@ class Engine final : public EngineBase {
   // one GPU: encode / decode on the side stream, overlapping the compute stream
   // (per-kernel timing runs serialised so each class's time is its own)
   bool side_overlap() const {
-    return s_.world == 1 && (side_enabled() || s_.overlap >= 2) && !s_.kstats;
+    return zero_copy() && (side_enabled() || s_.overlap >= 2) && !s_.kstats;
   }
   // K1/K3 on a side stream alongside the central rows (QGNN_SIDE_STREAM=1).  Off by
   // default since the SpMM/GEMM kernels saturate the GPU: in the captured graph the
@@ -475,10 +482,11 @@ class Engine final : public EngineBase {
     for (int64_t src = 0; src < P_; ++src)
       if (src != D.id) wire += double(msgs_[k][src][D.id].bytes);
     if constexpr (sizeof(T) == 4) {
-      if (s_.layout == QGNN_WIRE_GPU && din <= 512) {
+      if (s_.layout == QGNN_WIRE_GPU) {
         kbegin(QGNN_K_DEQUANT);
         dequant_rows_add_f32(ctx_, arena_.p, R.n_acc_rows, R.acc_rows.p, R.acc_ptr.p, R.acc_msg.p,
-                             int(din), R.bits.p, R.off.p, D.dh_next.p, ldi, mask, ldi, s_main_);
+                             int(din), R.bits.p, R.off.p, D.dh_next.p, ldi, mask, ldi, R.env.p,
+                             s_main_);
         kend(QGNN_K_DEQUANT, double(R.n_acc_rows) * 2 * din * sizeof(T) + double(R.n) * 13 + wire,
              s_main_);
         return;
@@ -499,12 +507,14 @@ class Engine final : public EngineBase {
     if constexpr (sizeof(T) == 4) {
       if (s_.layout == QGNN_WIRE_GPU) {
         dequant_add_masked_f32(ctx_, arena_.p, e - b, int(din), R.bits.p + b, R.off.p + b,
-                               R.dst.p + b, D.dh_next.p, ldi, mask, ldi, s_main_);
+                               R.dst.p + b, D.dh_next.p, ldi, mask, ldi,
+                               R.env.p ? R.env.p + b : nullptr, s_main_);
         return;
       }
     }
     const int st = qgnn_dequant_scatter(ctx_, arena_.p, e - b, din, R.bits.p + b, R.off.p + b,
-                                        s_.layout, R.dst.p + b, 1, D.dh_next.p, dtype_, ldi, s_main_);
+                                        s_.layout, R.dst.p + b, 1, D.dh_next.p, dtype_, ldi,
+                                        R.env.p ? R.env.p + b : nullptr, s_main_);
     if (st) throw Status(st, qgnn_last_error());
   }
   void step();
@@ -525,6 +535,21 @@ class Engine final : public EngineBase {
   cudaStream_t s_main_ = nullptr, s_comm_ = nullptr;
   cudaEvent_t ev_a_ = nullptr, ev_b_ = nullptr, ev_x_ = nullptr, ev_q_ = nullptr;
   ncclComm_t comm_ = nullptr;
+  // one GPU: route same-GPU pairs through NCCL self send/receive instead of
+  // zero copy (settings.transport = 1): the multi-GPU exchange code path,
+  // exercised and timed on a single device
+  bool self_xfer_ = false;
+  bool zero_copy() const { return s_.world == 1 && !self_xfer_; }
+  // K1 chunk envelope of sender partition p: source | plan version << 8 (GPU layout)
+  uint32_t envelope(int p) const {
+    return s_.layout == QGNN_WIRE_GPU
+               ? (uint32_t(p + env_skew_src_) & 0xffu) |
+                     (uint32_t(plan_version_ + env_skew_ver_) & 0xffu) << 8
+               : 0u;
+  }
+  // test hook (QGNN_TEST_ENVELOPE=source|version): senders stamp a wrong source
+  // or plan version, which the receivers' K3 must reject (ProtocolError)
+  int env_skew_src_ = 0, env_skew_ver_ = 0;
   std::shared_ptr<LoopGroup> loop_;     // loopback transport (tests), else NCCL
   cudaEvent_t ev_c_ = nullptr, ev_d_ = nullptr;
   std::vector<cudaEvent_t> peer_x_;     // loopback: peers' exchange-done events
@@ -691,6 +716,10 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
       std::memcpy(&id, nccl_id, sizeof(id));
       QGNN_NCCL(nccl().CommInitRank(&comm_, s.world, id, s.rank));
     }
+  } else if (s.transport == 1) {
+    self_xfer_ = true;
+    const int dev = s.device;  // one-rank communicator: no bootstrap network needed
+    QGNN_NCCL(nccl().CommInitAll(&comm_, 1, &dev));
   }
 
   // partition (engine.hpp:212) and coefficients (:213)
@@ -708,6 +737,10 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
     global_test_ += test[v] != 0;
   }
   QGNN_REQUIRE(global_train_ > 0, QGNN_EINVAL, "engine: empty train mask");
+  if (const char* e = std::getenv("QGNN_TEST_ENVELOPE")) {
+    env_skew_src_ = std::string(e) == "source" ? 1 : 0;
+    env_skew_ver_ = std::string(e) == "version" ? 1 : 0;
+  }
 
   // keys: forward t = 0..L-1, backward t = 1..L-1 (engine.hpp:345-352)
   for (int64_t t = 0; t < L_; ++t) keys_.push_back({int(t), false, dims_[t], uint64_t(2 * t)});
@@ -878,6 +911,55 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
   build_messages();
   for (size_t k = 0; k < keys_.size(); ++k) upload_key_meta(int(k));
   QGNN_CUDA(cudaDeviceSynchronize());
+  negotiate_sizes();
+}
+
+// negotiate_buffers (plan.hpp:140-154) across ranks: every rank derives every
+// pair's wire bytes from its own copy of the plan; the senders' figures are
+// all-gathered and each receiver checks its incoming pairs against them
+// (ProtocolError "negotiated buffer size mismatch", engine.hpp:546-547).  Runs
+// at construction and after every plan adoption, never inside an epoch.
+template <typename T>
+void Engine<T>::negotiate_sizes() {
+  if (s_.world == 1) return;
+  const int64_t K = int64_t(keys_.size()), ppr = P_ / s_.world;
+  const int64_t slice = K * ppr * P_ + 1;  // + the plan version
+  std::vector<uint64_t> all(size_t(slice * s_.world), 0);
+  uint64_t* mine = all.data() + s_.rank * slice;
+  for (int64_t k = 0; k < K; ++k)
+    for (int64_t p = p0_; p < p1_; ++p)
+      for (int64_t q = 0; q < P_; ++q)
+        if (q != p) mine[(k * ppr + (p - p0_)) * P_ + q] = msgs_[k][p][q].bytes;
+  mine[slice - 1] = plan_version_;
+  if (const char* e = std::getenv("QGNN_TEST_NEGOTIATE"))  // test hook: rank 1 disagrees
+    if (std::atoi(e) == 1 && s_.rank == 1) mine[0] += 16;
+  neg_.alloc(size_t(slice * s_.world), false);
+  QGNN_CUDA(cudaMemcpyAsync(neg_.p, all.data(), all.size() * sizeof(uint64_t),
+                            cudaMemcpyHostToDevice, s_main_));
+  allgather_dev(neg_.p, slice, s_main_);
+  QGNN_CUDA(cudaStreamSynchronize(s_main_));
+  QGNN_CUDA(cudaMemcpy(all.data(), neg_.p, all.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  bool ok = true;
+  for (int r = 0; r < s_.world; ++r) {
+    const uint64_t* theirs = all.data() + r * slice;
+    ok &= theirs[slice - 1] == plan_version_;
+    for (int64_t k = 0; k < K; ++k)
+      for (int64_t p = r * ppr; p < (r + 1) * ppr; ++p)
+        for (int64_t q = p0_; q < p1_; ++q)
+          if (q != p) ok &= theirs[(k * ppr + (p - r * ppr)) * P_ + q] == msgs_[k][p][q].bytes;
+  }
+  // every rank learns every rank's verdict, so all of them fail together
+  // (a lone failing rank would leave its peers waiting in the next exchange)
+  std::vector<uint64_t> verdict(s_.world, 0);
+  verdict[s_.rank] = ok ? 1 : 0;
+  QGNN_CUDA(cudaMemcpyAsync(neg_.p, verdict.data(), verdict.size() * sizeof(uint64_t),
+                            cudaMemcpyHostToDevice, s_main_));
+  allgather_dev(neg_.p, 1, s_main_);
+  QGNN_CUDA(cudaStreamSynchronize(s_main_));
+  QGNN_CUDA(cudaMemcpy(verdict.data(), neg_.p, verdict.size() * sizeof(uint64_t),
+                       cudaMemcpyDeviceToHost));
+  for (uint64_t v : verdict) ok &= v == 1;
+  QGNN_REQUIRE(ok, QGNN_EPROTOCOL, "exchange: negotiated buffer size mismatch");
 }
 
 template <typename T>
@@ -888,6 +970,9 @@ Engine<T>::~Engine() {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
   }
+  // captured graphs may hold NCCL kernels of comm_: release them first
+  for (auto& g : graphs_)
+    if (g.exec) cudaGraphExecDestroy(g.exec), g.exec = nullptr;
   if (comm_) nccl().CommDestroy(comm_);
   if (loop_) {
     std::lock_guard<std::mutex> lk(g_loop_mu);
@@ -1119,7 +1204,7 @@ void Engine<T>::arena_layout() {
     for (int64_t q = p0_; q < p1_; ++q)
       for (int64_t p = 0; p < P_; ++p) {
         if (p == q) continue;
-        if (p >= p0_ && p < p1_)
+        if (p >= p0_ && p < p1_ && !self_xfer_)
           recv_base_[k][q][p] = send_base_[k][p][q];  // zero copy on the same GPU
         else {
           recv_base_[k][q][p] = o;
@@ -1187,6 +1272,8 @@ void Engine<T>::upload_key_meta(int k) {
     std::vector<int32_t> dst;
     std::vector<uint8_t> rb;
     std::vector<uint64_t> ro;
+    std::vector<uint32_t> env;
+    const bool gpu_layout = s_.layout == QGNN_WIRE_GPU;
     R.p_begin.assign(P_ + 1, 0);
     for (int64_t src = 0; src < P_; ++src) {
       R.p_begin[src] = int64_t(rb.size());
@@ -1198,6 +1285,9 @@ void Engine<T>::upload_key_meta(int k) {
                               : int32_t(V.device_slot_offset[src] + int64_t(i)));
         rb.push_back(m.bits[i]);
         ro.push_back(recv_base_[k][p][src] + m.off[i]);
+        if (gpu_layout)  // the receiver's expectation: (src, this partition, its plan version)
+          env.push_back((uint32_t(src) & 0xffu) | (uint32_t(p) & 0xffu) << 8 |
+                        (uint32_t(plan_version_) & 0xffu) << 16);
       }
     }
     R.p_begin[P_] = int64_t(rb.size());
@@ -1226,6 +1316,7 @@ void Engine<T>::upload_key_meta(int k) {
     }
     R.bits.upload(rb);
     R.off.upload(ro);
+    if (gpu_layout) R.env.upload(env);
   }
 }
 
@@ -1266,7 +1357,7 @@ void Engine<T>::quantize(PartDev& D, int k, const T* src, int64_t ld, cudaStream
   kbegin(QGNN_K_QUANT, sq);
   const int st = qgnn_quantize_pack(ctx_, src, dtype_, ld, dim, S.n, S.rows.p, S.ids.p, S.bits.p,
                                     S.off.p, S.set.p, S.keys.p, s_.layout, arena_.p, S.wlo.p,
-                                    S.whi.p, sq);
+                                    S.whi.p, envelope(D.id), sq);
   if (st) throw Status(st, qgnn_last_error());
   // algorithmic bytes: rows read once per message + packed chunks + metadata
   double bytes = 0;
@@ -1285,7 +1376,7 @@ void Engine<T>::decode_halo(int k, int64_t din, int64_t ldi, cudaStream_t st) {
     if (!R.n) continue;
     kbegin(QGNN_K_DEQUANT, st);
     const int rc = qgnn_dequant_scatter(ctx_, arena_.p, R.n, din, R.bits.p, R.off.p, s_.layout,
-                                        R.dst.p, 0, D.halo.p, dtype_, ldi, st);
+                                        R.dst.p, 0, D.halo.p, dtype_, ldi, R.env.p, st);
     if (rc) throw Status(rc, qgnn_last_error());
     double bytes = double(R.n) * (din * sizeof(T) + 4 + 1 + 8);
     for (int64_t src = 0; src < P_; ++src)
@@ -1297,7 +1388,7 @@ void Engine<T>::decode_halo(int k, int64_t din, int64_t ldi, cudaStream_t st) {
 // Grouped point-to-point exchange of the remote pairs on the comm stream.
 template <typename T>
 void Engine<T>::exchange(int k) {
-  if (s_.world == 1) return;  // every pair is on this GPU: zero-copy
+  if (zero_copy()) return;  // every pair is on this GPU: zero-copy
   QGNN_CUDA(cudaEventRecord(ev_q_, s_main_));
   QGNN_CUDA(cudaStreamWaitEvent(s_comm_, ev_q_, 0));
   const int64_t ppr = P_ / s_.world;
@@ -1309,15 +1400,18 @@ void Engine<T>::exchange(int k) {
   // with the i-th receive B<-A, so both sides enumerate a rank pair's messages in
   // the same (source partition p, destination partition q) order.
   std::vector<std::array<int64_t, 4>> sends, recvs;  // (peer rank, p, q, bytes)
+  // self_xfer_ (one GPU, QGNN transport "nccl"): same-GPU pairs go through NCCL
+  // self send/receive too, into their own receive regions
   for (int64_t p = p0_; p < p1_; ++p)
     for (int64_t q = 0; q < P_; ++q) {
-      if (q >= p0_ && q < p1_) continue;
+      if (q == p || (q >= p0_ && q < p1_ && !self_xfer_)) continue;
       const uint64_t nb = msgs_[k][p][q].bytes;
       if (nb) sends.push_back({q / ppr, p, q, int64_t(nb)});
     }
   for (int64_t p = 0; p < P_; ++p) {
-    if (p >= p0_ && p < p1_) continue;
+    if (p >= p0_ && p < p1_ && !self_xfer_) continue;
     for (int64_t q = p0_; q < p1_; ++q) {
+      if (q == p) continue;
       const uint64_t nb = msgs_[k][p][q].bytes;
       if (nb) recvs.push_back({p / ppr, p, q, int64_t(nb)});
     }
@@ -1381,7 +1475,7 @@ void Engine<T>::exchange(int k) {
 // stream; loopback copies were issued on the senders' comm streams.
 template <typename T>
 void Engine<T>::wait_exchange() {
-  if (s_.world == 1) return;
+  if (zero_copy()) return;
   if (loop_) {
     for (cudaEvent_t e : peer_x_) QGNN_CUDA(cudaStreamWaitEvent(s_main_, e, 0));
     // and for this rank's own outgoing copies: every key's send regions start at
@@ -1440,7 +1534,7 @@ void Engine<T>::forward_layer(int l) {
   // One GPU, in-line schedule: nothing overlaps the central rows, so each
   // partition's transform runs once over central + marginal rows (contiguous in
   // hagg) after its marginal aggregation: one GEMM launch instead of two.
-  const bool one_gemm = s_.world == 1 && !side_overlap() && merge_gemm_enabled();
+  const bool one_gemm = zero_copy() && !side_overlap() && merge_gemm_enabled();
   // central rows (engine.hpp:598-605): during the exchange
   auto central = [&](PartDev& D) {
     const int64_t nc = D.view.n_central;
@@ -1471,7 +1565,7 @@ void Engine<T>::forward_layer(int l) {
     for (auto& up : parts_dev_) central(*up);
     join_side();
   } else {
-    if (feats || s_.world == 1) {
+    if (feats || zero_copy()) {
       for (auto& up : parts_dev_) {
         if (feats) gather_features(*up);
         if (feats && up.get() == parts_dev_.back().get())
@@ -2135,6 +2229,7 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
       upload_key_meta(int(k));
     });
   for (auto& f : meta) f.get();
+  negotiate_sizes();
   const auto t_meta = std::chrono::steady_clock::now();
   for (size_t k = 0; k < keys_.size(); ++k) {
     for (auto& up : parts_dev_) {  // reset windows (engine.hpp:855-860)
@@ -2380,6 +2475,138 @@ int qgnn_spmm_plan_run(qgnn_spmm_plan* p, int64_t dim, const float* x, int64_t l
   spmm_f32(p->ctx, int(d4), x, ld_x, y, ld_y, self_alpha, ptr_a, col_a, alpha_a, ptr_b, col_b,
            alpha_b, p->row_begin, p->n_rows, out, ld_out, &p->hubs.plan,
            static_cast<cudaStream_t>(stream), mask, ld_mask);
+  QGNN_API_END
+}
+
+// ---- standalone exchange (exchange.hpp:45-78; engine.hpp:502, :528-529) ----------
+struct qgnn_comm {
+  int world = 1, rank = 0, device = 0;
+  ncclComm_t nccl = nullptr;
+  std::shared_ptr<qgnn_b200::LoopGroup> loop;
+  cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+};
+
+int qgnn_comm_create(const void* id128, int world, int rank, int device, qgnn_comm** out) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(out && world >= 1 && rank >= 0 && rank < world, QGNN_EINVAL,
+               "comm_create: bad rank / world");
+  QGNN_CUDA(cudaSetDevice(device));
+  auto c = std::make_unique<qgnn_comm>();
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  QGNN_CUDA(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
+  QGNN_CUDA(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+  if (id128 && std::memcmp(id128, kLoopMagic, 8) == 0) {
+    uint64_t key;
+    std::memcpy(&key, static_cast<const char*>(id128) + 8, 8);
+    key ^= 0x636f6d6d00000000ull;  // separate namespace from engine loopback groups
+    std::lock_guard<std::mutex> lk(g_loop_mu);
+    auto& g = g_loops[key];
+    if (!g) {
+      g = std::make_shared<LoopGroup>();
+      g->world = world;
+      g->engines.assign(world, nullptr);
+      g->ptr.assign(world, nullptr);
+      g->ev.assign(world, nullptr);
+      g->ev2.assign(world, nullptr);
+      g->sends.assign(world, {});
+      g->recvs.assign(world, {});
+    }
+    QGNN_REQUIRE(g->world == world && !g->engines[rank], QGNN_EPROTOCOL,
+                 "comm_create: loopback world mismatch or rank already registered");
+    g->engines[rank] = c.get();
+    c->loop = g;
+  } else {
+    if (id128) {
+      ncclUniqueId id;
+      std::memcpy(&id, id128, sizeof(id));
+      QGNN_NCCL(nccl().CommInitRank(&c->nccl, world, id, rank));
+    } else {
+      QGNN_REQUIRE(world == 1, QGNN_EINVAL, "comm_create: world > 1 needs an id");
+      QGNN_NCCL(nccl().CommInitAll(&c->nccl, 1, &device));
+    }
+  }
+  *out = c.release();
+  QGNN_API_END
+}
+
+int qgnn_comm_destroy(qgnn_comm* c) {
+  if (!c) return QGNN_OK;
+  if (c->nccl) nccl().CommDestroy(c->nccl);
+  if (c->loop) {
+    std::lock_guard<std::mutex> lk(g_loop_mu);
+    c->loop->engines[c->rank] = nullptr;
+    bool empty = true;
+    for (void* e : c->loop->engines) empty &= e == nullptr;
+    if (empty)
+      for (auto it = g_loops.begin(); it != g_loops.end(); ++it)
+        if (it->second == c->loop) {
+          g_loops.erase(it);
+          break;
+        }
+  }
+  if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+  if (c->ev_done) cudaEventDestroy(c->ev_done);
+  delete c;
+  return QGNN_OK;
+}
+
+int qgnn_exchange(qgnn_comm* c, const void* send, const uint64_t* send_off,
+                  const uint64_t* send_bytes, void* recv, const uint64_t* recv_off,
+                  const uint64_t* recv_bytes, void* stream) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(c && send_off && send_bytes && recv_off && recv_bytes, QGNN_EINVAL,
+               "exchange: null argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const auto* sb = static_cast<const uint8_t*>(send);
+  auto* rb = static_cast<uint8_t*>(recv);
+  const int W = c->world, me = c->rank;
+  if (c->nccl) {
+    // one NCCL group: every pair's send and receive posted together, so the
+    // transfers to all peers proceed concurrently over NVLink / NVSwitch
+    QGNN_NCCL(nccl().GroupStart());
+    for (int r = 0; r < W; ++r)
+      if (send_bytes[r])
+        QGNN_NCCL(nccl().Send(sb + send_off[r], size_t(send_bytes[r]), ncclUint8, r, c->nccl, st));
+    for (int r = 0; r < W; ++r)
+      if (recv_bytes[r])
+        QGNN_NCCL(nccl().Recv(rb + recv_off[r], size_t(recv_bytes[r]), ncclUint8, r, c->nccl, st));
+    QGNN_NCCL(nccl().GroupEnd());
+    return QGNN_OK;
+  }
+  // in-process loopback: receivers pull from the senders' buffers (device copies)
+  LoopGroup& G = *c->loop;
+  std::vector<std::array<int64_t, 4>> mine(W);
+  for (int r = 0; r < W; ++r)
+    mine[r] = {int64_t(send_off[r]), int64_t(send_bytes[r]), int64_t(recv_off[r]),
+               int64_t(recv_bytes[r])};
+  QGNN_CUDA(cudaEventRecord(c->ev_ready, st));
+  G.ptr[me] = const_cast<uint8_t*>(sb);
+  G.ev[me] = c->ev_ready;
+  G.sends[me] = mine;
+  G.barrier();
+  // ProtocolError (engine.hpp:546-550): negotiated sizes must agree pairwise
+  bool match = true;
+  for (int a = 0; a < W; ++a)
+    for (int b = 0; b < W; ++b) match &= G.sends[a][b][1] == G.sends[b][a][3];
+  if (match)
+    for (int r = 0; r < W; ++r) {
+      const int64_t nb = G.sends[r][me][1];
+      if (!nb) continue;
+      if (r != me) QGNN_CUDA(cudaStreamWaitEvent(st, G.ev[r], 0));
+      QGNN_CUDA(cudaMemcpyAsync(rb + recv_off[r], static_cast<uint8_t*>(G.ptr[r]) + G.sends[r][me][0],
+                                size_t(nb), cudaMemcpyDeviceToDevice, st));
+    }
+  QGNN_CUDA(cudaEventRecord(c->ev_done, st));
+  G.ev2[me] = c->ev_done;
+  G.barrier();  // every rank's pulls enqueued
+  // our send buffer may be reused once every receiver has copied out of it
+  for (int r = 0; r < W; ++r)
+    if (r != me && G.sends[me][r][1]) QGNN_CUDA(cudaStreamWaitEvent(st, G.ev2[r], 0));
+  G.barrier();  // nobody reads G.* of this call after here
+  QGNN_REQUIRE(match, QGNN_EPROTOCOL,
+               "exchange: send/receive sizes disagree between ranks (negotiate_buffers)");
   QGNN_API_END
 }
 

@@ -69,7 +69,8 @@ class Engine:
                  group_size: int = 4, period: int = 50, lr: float = 0.01, theta: float = 3e-9,
                  gamma: float = 5e-5, dtype: str = "f32", layout: Optional[int] = None,
                  owner=None, rank: int = 0, world: int = 1, device: int = 0,
-                 nccl_id: Optional[bytes] = None, kstats: bool = False, overlap: int = 1):
+                 nccl_id: Optional[bytes] = None, kstats: bool = False, overlap: int = 1,
+                 transport: str = "zero_copy"):
         s = _lib.Settings()
         s.sage = int(sage)
         s.n_dims = len(dims)
@@ -89,6 +90,7 @@ class Engine:
         s.layout = (WIRE_REF if dtype == "f64" else WIRE_GPU) if layout is None else layout
         s.rank, s.world, s.device = rank, world, device
         s.overlap = int(overlap)
+        s.transport = {"zero_copy": 0, "nccl": 1}[transport]
         s.kstats = int(kstats)
         self.settings = s
         self.dims = list(dims)

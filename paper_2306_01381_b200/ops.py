@@ -77,13 +77,13 @@ def wire_layout(bits: np.ndarray, dim: int, layout: int = WIRE_GPU, dtype: int =
 
 # ---- codec.hpp / quant.hpp ----------------------------------------------------------
 def quantize_pack(values, rows, ids, bits, offsets, set_keys, out, layout=WIRE_GPU, set_of=None,
-                  win_lo=None, win_hi=None, check_errors=True):
+                  win_lo=None, win_hi=None, check_errors=True, envelope=0):
     """K1 over arbitrary (row, id, width, offset) message lists."""
     dim = values.shape[1]
     check(lib.qgnn_quantize_pack(ctx(), _ptr(values), _dtype(values), values.stride(0), dim,
                                  rows.numel(), _ptr(rows), _ptr(ids), _ptr(bits), _ptr(offsets),
                                  _ptr(set_of), _ptr(set_keys), layout, _ptr(out), _ptr(win_lo),
-                                 _ptr(win_hi), _stream()))
+                                 _ptr(win_hi), envelope, _stream()))
     if check_errors:
         sync_check()
     return out
@@ -114,22 +114,37 @@ def encode_message_set(values: torch.Tensor, rows, ids, bits, set_key: int,
 
 
 def dequant_scatter(wire, bits, offsets, dim, out, dst_rows=None, accumulate=False,
-                    layout=WIRE_GPU, check_errors=True):
+                    layout=WIRE_GPU, check_errors=True, expect_envelope=None):
     """K3: decode_message_set (codec.hpp:80-96) fused with the halo scatter."""
     n = bits.numel()
     check(lib.qgnn_dequant_scatter(ctx(), _ptr(wire), n, dim, _ptr(bits), _ptr(offsets), layout,
                                    _ptr(dst_rows), int(accumulate), _ptr(out), _dtype(out),
-                                   out.stride(0), _stream()))
+                                   out.stride(0), _ptr(expect_envelope), _stream()))
     if check_errors:
         sync_check()
     return out
 
 
+def validate_index(bits, offsets, dim, n_bytes: int, total: Optional[int] = None,
+                   layout: int = WIRE_GPU, dtype: int = F32) -> None:
+    """decode_message_set's index checks (qgnn_decode_validate, codec.hpp:82-95):
+    raises DecodeError like the reference."""
+    b = np.ascontiguousarray(bits, np.uint8)
+    o = np.ascontiguousarray(offsets, np.uint64)
+    d = np.full(len(b), dim, np.uint64)
+    check(lib.qgnn_decode_validate(b.ctypes.data, o.ctypes.data, d.ctypes.data, len(b), layout,
+                                   dtype, n_bytes if total is None else total, n_bytes))
+
+
 def decode_message_set(wire: torch.Tensor, bits, offsets, dim: int, dtype=torch.float32,
-                       layout: int = WIRE_GPU):
-    """decode_message_set: rows in index (wire) order."""
+                       layout: int = WIRE_GPU, total: Optional[int] = None):
+    """decode_message_set: rows in index (wire) order.  ``total`` is the
+    index's total_bytes (default: the wire length); the index is validated on
+    the host first, each chunk against its entry on the device."""
     dev = wire.device
     n = len(bits)
+    validate_index(bits, offsets, dim, wire.numel(), total, layout,
+                   F64 if dtype == torch.float64 else F32)
     out = torch.zeros((max(1, n), dim), dtype=dtype, device=dev)
     bits_t = torch.as_tensor(np.ascontiguousarray(bits, np.uint8), device=dev)
     off_t = torch.as_tensor(np.ascontiguousarray(offsets, np.uint64).view(np.int64), device=dev)
@@ -180,6 +195,41 @@ class SpmmPlan:
     def close(self):
         if getattr(self, "_h", None):
             lib.qgnn_spmm_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+# ---- exchange.hpp / engine.hpp mailbox ------------------------------------------------
+class Comm:
+    """One rank of an exchange group (qgnn_comm_*): NCCL (id from
+    engine.nccl_unique_id(), or None for world 1) or the in-process loopback
+    transport (engine.loopback_id(group), ranks as threads)."""
+
+    def __init__(self, world: int = 1, rank: int = 0, id128: Optional[bytes] = None,
+                 device: Optional[int] = None):
+        if device is None:
+            device = torch.cuda.current_device()
+        idbuf = None if id128 is None else (C.c_char * 128).from_buffer_copy(id128)
+        h = C.c_void_p()
+        check(lib.qgnn_comm_create(None if idbuf is None else C.cast(idbuf, C.c_void_p), world,
+                                   rank, device, C.byref(h)))
+        self._h, self.world, self.rank = h, world, rank
+
+    def exchange(self, send: torch.Tensor, send_off, send_bytes, recv: torch.Tensor, recv_off,
+                 recv_bytes):
+        """Grouped point-to-point all-to-all-v (qgnn_exchange) on the current stream."""
+        arr = [np.ascontiguousarray(a, np.uint64) for a in (send_off, send_bytes, recv_off,
+                                                           recv_bytes)]
+        assert all(len(a) == self.world for a in arr)
+        check(lib.qgnn_exchange(self._h, _ptr(send), arr[0].ctypes.data, arr[1].ctypes.data,
+                                _ptr(recv), arr[2].ctypes.data, arr[3].ctypes.data, _stream()))
+        return recv
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.qgnn_comm_destroy(self._h)
             self._h = None
 
     def __del__(self):

@@ -237,3 +237,40 @@ def test_fit_affine():  # cost_model.hpp:78-109, test_commsim.cpp:65-99
     with pytest.raises(_lib.InvalidArgument):
         x1 = np.array([1.0, 1.0])
         check(lib.qgnn_fit_affine(x1.ctypes.data, y.ctypes.data, 2, C.byref(th), C.byref(ga)))
+
+
+def _validate(bits, off, dim, n_bytes, total, layout=_lib.WIRE_REF, dtype=_lib.F64):
+    b = np.ascontiguousarray(bits, np.uint8)
+    o = np.ascontiguousarray(off, np.uint64)
+    d = np.ascontiguousarray(dim, np.uint64)
+    st = lib.qgnn_decode_validate(b.ctypes.data, o.ctypes.data, d.ctypes.data, len(b), layout,
+                                  dtype, total, n_bytes)
+    return st, lib.qgnn_last_error().decode()
+
+
+def test_decode_index_validation_matches_reference():
+    """qgnn_decode_validate raises DecodeError with the reference's own message
+    (codec.hpp:82-95, quant.hpp:122-133) on every corrupt-index case of
+    test_quantcodec.cpp:389-420; the clean index passes."""
+    G = GOLDEN
+    wire, bits, dim, off = G["enc_wire"], G["enc_idx_bits"], G["enc_idx_dim"], G["enc_idx_off"]
+    n = len(wire)
+    assert _validate(bits, off, dim, n, n)[0] == _lib.OK
+    gap = off.copy()
+    gap[1] += 1
+    short = wire[:-3]
+    cases = {  # name: (bits, off, dim, bytes, total, reference message)
+        "total": (bits, off, dim, wire, n + 1, "message set: byte count mismatch"),
+        "gap": (bits, gap, dim, wire, n, "message set: index offsets not contiguous"),
+        "trailing": (bits[:-1], off[:-1], dim[:-1], wire, n, "message set: trailing bytes"),
+        "truncated": (bits, off, dim, short, len(short), "chunk: truncated payload"),
+    }
+    for name, (b, o, d, w, total, msg) in cases.items():
+        st, got = _validate(b, o, d, len(w), total)
+        assert st == _lib.EDECODE and got == msg, (name, got)
+        if ref_available():
+            from oracle import RefError, ref
+            idx = dict(id=G["enc_idx_id"][:len(b)], bits=b, off=o, dim=d)
+            with pytest.raises(RefError) as ei:
+                ref.decode_message_set(w, idx, total)
+            assert msg in str(ei.value), (name, str(ei.value))

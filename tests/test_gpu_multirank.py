@@ -82,3 +82,16 @@ def test_world_split_planted_graph(cuda):
         for ms, w in _run_world(g, world, 3, **kw):
             assert [m["train_loss"] for m in ms] == [m["train_loss"] for m in base_ms]
             assert (w == base_w).all()
+
+
+def test_negotiated_size_mismatch_is_protocol_error(cuda, monkeypatch):
+    """Every rank checks its incoming pairs against the senders' all-gathered
+    sizes (negotiate_buffers, plan.hpp:140-154): a disagreeing rank makes every
+    rank fail with ProtocolError (engine.hpp:546-547)."""
+    from paper_2306_01381_b200._lib import ProtocolError
+    monkeypatch.setenv("QGNN_TEST_NEGOTIATE", "1")
+    kw = dict(dims=[8, 12, 3], n_parts=4, bit_mode="fixed", fixed_bits=4, seed=11)
+    with pytest.raises(AssertionError) as ei:
+        _run_world(GRAPH, 2, 1, **kw)
+    assert "negotiated buffer size mismatch" in str(ei.value)
+    assert str(ei.value).count("ProtocolError") >= 2  # both ranks fail together
