@@ -623,6 +623,306 @@ __global__ void __launch_bounds__(256, MINB) k_quantize_pack_lean(
   }
 }
 
+// ------------------------------------------------------------ grouped K1 ---
+// Production K1 (fp32 rows, GPU layout).  G = 2^lg lanes own one message (G *
+// EPL >= dim) and a warp carries 32 / G messages, so lane j holds the EPL
+// contiguous elements [j*EPL, (j+1)*EPL): its payload is one contiguous run of
+// EPL*b/8 bytes (16 B at 8 bits -> one 128-bit store), and the per-message
+// scalars (key fork, S, 1/S) are amortized over EPL elements per lane instead
+// of 4-8 (D = 256: 2 messages per warp; D = 100: 4).
+//
+// Element decision in fp32 with a proven error bound, exact fallback.  The
+// reference computes x = RN(RN(h - lo) / S) in fp64 (quant.hpp:81-87).  Here
+// x_f = RN_f(RN_f(h - lo) * RN_f(1/S)) with |x_f - x| <= 3.01 * 2^-24 * x, so
+// for x <= levels the distance is below dl = levels * 2^-22.  With frac_f =
+// x_f - floor(x_f) (exact) inside (dl, 1 - dl), floor(x) == floor(x_f) and
+// |frac - frac_f| < dl; the draw's top 23 bits give u_f <= u < u_f + 2^-23, so
+// (u < frac) == (u_f < frac_f) whenever |u_f - frac_f| > dl + 2^-22.  Only
+// elements failing that test (~4 * dl: 2e-4 at 8 bits) or equal to hi with a
+// non-integral x_hi take quant_fast/quant_exact, the fp64 path of the lean
+// kernel (so every code is the reference's).  h == lo gives a = 0: code 0,
+// never flagged.  The top 23 bits of the draw are bits 41..63 of the second
+// multiply: the final xorshift (z ^ z >> 31) does not touch them, and only the
+// high word of that product is formed.  32-bit form: 14 integer ops.
+__device__ __forceinline__ uint32_t draw_top32(uint32_t lo, uint32_t hi) {  // z = key+(e+2)phi
+  const uint32_t tl = lo ^ __funnelshift_r(lo, hi, 30);  // z ^= z >> 30
+  const uint32_t th = hi ^ (hi >> 30);
+  const uint64_t w = static_cast<uint64_t>(tl) * 0x1ce4e5b9u;  // z *= 0xbf58476d1ce4e5b9
+  const uint32_t ml = static_cast<uint32_t>(w);
+  const uint32_t mh = static_cast<uint32_t>(w >> 32) + tl * 0xbf58476du + th * 0x1ce4e5b9u;
+  const uint32_t sl = ml ^ __funnelshift_r(ml, mh, 27);  // z ^= z >> 27
+  const uint32_t sh = mh ^ (mh >> 27);
+  return __umulhi(sl, 0x133111ebu) + sl * 0x94d049bbu + sh * 0x133111ebu;  // hi(z * C2)
+}
+
+__device__ __noinline__ uint32_t quant_slow(float h, float lo, float hi, uint32_t levels,
+                                            uint64_t z0, int q) {
+  const uint64_t z = z0 + static_cast<uint64_t>(q - 1) * kPhi;  // counter e0 + q + 1
+  QRow R;
+  R.lo = lo;
+  R.scale = (static_cast<double>(hi) - R.lo) / static_cast<double>(levels);
+  R.rcp = __drcp_rn(R.scale);
+  R.x_hi = __ddiv_rn(__dsub_rn(static_cast<double>(hi), R.lo), R.scale);
+  R.hi = hi;
+  R.levels = levels;
+  bool sl;
+  const uint32_t c = quant_fast(h, R, z, sl);
+  return sl ? quant_exact(h, R.lo, R.scale, static_cast<double>(levels), z) : c;
+}
+
+__device__ __forceinline__ float fmin_nan(float a, float b) {  // NaN-propagating min
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+// 4 byte containers (codes < 2^b) -> 4*b packed bits, LSB first
+// (flagged elements hold arbitrary bytes until patched: mask them to the width)
+__device__ __forceinline__ uint32_t pack4x4(uint32_t w) {
+  w &= 0x0f0f0f0fu;
+  w = (w | (w >> 4)) & 0x00ff00ffu;
+  return (w | (w >> 8)) & 0xffffu;
+}
+__device__ __forceinline__ uint32_t pack4x2(uint32_t w) {
+  w &= 0x03030303u;
+  w = (w | (w >> 6)) & 0x000f000fu;
+  return (w | (w >> 12)) & 0xffu;
+}
+
+template <int EPL, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_quantize_pack_grp(
+    const float* __restrict__ values, int64_t ld, int dim, int64_t n, int lg,
+    const int32_t* __restrict__ rows, const uint32_t* __restrict__ ids,
+    const uint8_t* __restrict__ bits, const uint64_t* __restrict__ offsets,
+    const uint16_t* __restrict__ set_of, const uint64_t* __restrict__ set_keys,
+    uint8_t* __restrict__ out, float* __restrict__ win_lo, float* __restrict__ win_hi,
+    int* __restrict__ err, uint32_t env) {
+  constexpr int CPL = EPL / 4;  // float4 chunks per lane
+  constexpr int NW = EPL / 4;   // byte-container words per lane
+  const int lane = threadIdx.x & 31;
+  const int G = 1 << lg;
+  const int j = lane & (G - 1);
+  const int mpw = 32 >> lg;
+  const unsigned gm = G == 32 ? 0xffffffffu : ((1u << G) - 1u) << (lane & ~(G - 1));
+  const int nchunk = (dim + 3) >> 2;
+  const int e0 = j * EPL;
+  const int nvalid = min(max(dim - e0, 0), EPL);  // valid elements of this lane
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarp = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t base = warp * mpw; base < n; base += nwarp * mpw) {
+    int64_t m = base + (lane >> lg);
+    const bool live = m < n;
+    if (!live) m = n - 1;  // idle group: recompute the last message, store nothing
+    const float* row = values + static_cast<int64_t>(rows[m]) * ld;
+    float v[EPL];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const int c = j * CPL + k;
+      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (c < nchunk) t = __ldg(reinterpret_cast<const float4*>(row) + c);
+      v[4 * k] = t.x, v[4 * k + 1] = t.y, v[4 * k + 2] = t.z, v[4 * k + 3] = t.w;
+    }
+    if (nvalid < EPL && nvalid > 0) {  // tail lane: pad with a valid element
+#pragma unroll
+      for (int q = 1; q < EPL; ++q)
+        if (q >= nvalid) v[q] = v[0];
+    }
+    // extrema; NaN propagates into lo, +-inf shows in lo/hi: finite <=> both finite
+    float lo = INFINITY, hi = -INFINITY;
+    bool negz = false;
+    if (nvalid > 0) {
+#pragma unroll
+      for (int q = 0; q < EPL; ++q) {
+        lo = fmin_nan(lo, v[q]);
+        hi = fmaxf(hi, v[q]);
+        negz |= __float_as_uint(v[q]) == 0x80000000u;
+      }
+    }
+    for (int o = G >> 1; o > 0; o >>= 1) {
+      lo = fmin_nan(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const bool finite = fabsf(lo) < INFINITY && fabsf(hi) < INFINITY;
+    negz = (__ballot_sync(0xffffffffu, negz) & gm) != 0;
+    // first-occurrence signed zero (quant.hpp:63-68); only when a -0.0 is present
+    const bool needz = negz && (lo == 0.f || hi == 0.f);
+    if (__any_sync(0xffffffffu, needz)) {
+      int zk = 0x7fffffff;  // (index << 1) | sign of this lane's first zero
+#pragma unroll
+      for (int q = EPL - 1; q >= 0; --q)
+        if (q < nvalid && v[q] == 0.f) zk = ((e0 + q) << 1) | int(__float_as_uint(v[q]) >> 31);
+      for (int o = G >> 1; o > 0; o >>= 1) zk = min(zk, __shfl_xor_sync(0xffffffffu, zk, o));
+      if (needz) {
+        const float z0 = (zk & 1) ? -0.f : 0.f;
+        if (lo == 0.f) lo = z0;
+        if (hi == 0.f) hi = z0;
+      }
+    }
+    if (!live) continue;
+    if (j == 0 && win_lo) {  // trace.hpp:86-91 (update precedes encode, engine.hpp:487)
+      const float wl = win_lo[m], wh = win_hi[m];
+      win_lo[m] = lo < wl ? lo : wl;
+      win_hi[m] = wh < hi ? hi : wh;
+    }
+    const int b = bits[m];
+    uint8_t* chunk = out + offsets[m];
+    if (b == 0) {  // BitMode::kFp: raw row (engine.hpp:473-481)
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        const int c = j * CPL + k;
+        if (c < nchunk)
+          reinterpret_cast<float4*>(chunk)[c] =
+              make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+      }
+      continue;
+    }
+    if (b != 2 && b != 4 && b != 8) {
+      if (j == 0) atomicOr(err, kErrBadWidth);
+      continue;
+    }
+    if (!finite) {
+      if (j == 0) atomicOr(err, kErrNonFinite);
+      continue;
+    }
+    const double lo_d = lo, hi_d = hi;
+    const uint32_t levels = (1u << b) - 1;
+    const bool constant = hi_d == lo_d;
+    const double scale = constant ? 0.0 : (hi_d - lo_d) / static_cast<double>(levels);
+    if (j == 0) {
+      uint4 h;
+      h.x = __float_as_uint(static_cast<float>(scale));
+      h.y = __float_as_uint(lo);
+      h.z = static_cast<uint32_t>(dim);
+      h.w = env_word(b, env, set_of, m);
+      *reinterpret_cast<uint4*>(chunk) = h;
+    }
+    uint32_t w8[NW];  // codes in byte containers, element q in byte q & 3 of word q >> 2
+#pragma unroll
+    for (int k = 0; k < NW; ++k) w8[k] = 0;
+    // elements left to the exact path: bit q = element e0 + q (patched after the stores)
+    uint32_t slow = 0, hib = 0, Tb = 0, Ab = 0;
+    uint64_t z0 = 0;
+    bool f32ok = true;
+    if (!constant && nvalid > 0) {  // hi == lo: S = 0, zero payload, no draws (quant.hpp:74-78)
+      if (nvalid < EPL) {  // tail lane: padding elements encode as h == lo (code 0)
+#pragma unroll
+        for (int q = 1; q < EPL; ++q)
+          if (q >= nvalid) v[q] = lo;
+      }
+      const uint64_t key = rng_fork(set_keys[set_of ? set_of[m] : 0], ids[m]);
+      // h == hi has x = x_hi exactly: code = floor(x_hi) + (u < frac_hi).  With
+      // K = frac_hi * 2^23 and k the draw's top 23 bits, u < frac_hi <=> k < floor(K)
+      // unless K is fractional and k == floor(K) (probability 2^-23: exact path).
+      const double x_hi = __ddiv_rn(__dsub_rn(hi_d, lo_d), scale);
+      const double hbd = floor(x_hi);
+      if (hbd < static_cast<double>(levels)) {
+        const double K = __dmul_rn(__dsub_rn(x_hi, hbd), 8388608.0);
+        const double Kf = floor(K);
+        hib = static_cast<uint32_t>(hbd);
+        Tb = 0x3f800000u | static_cast<uint32_t>(Kf);
+        Ab = K != Kf ? Tb : 0u;
+      } else {
+        hib = levels;  // min(floor(x_hi) + inc, levels) = levels
+      }
+      f32ok = scale >= 0x1.0p-100 && scale <= 0x1.0p+100;
+      const float rf = __double2float_rn(__drcp_rn(scale));
+      const float dl = static_cast<float>(levels) * 0x1.0p-22f;
+      const float hw = 0.5f - dl - 0x1.0p-24f;  // |fr - 1/2| > hw  <=>  dl <= fr <= 1 - dl
+      const float dd = dl + 0x1.0p-22f;
+      z0 = key + static_cast<uint64_t>(e0 + 2) * kPhi;  // pre-mix state, counter e0 + 1
+#pragma unroll
+      for (int k = 0; k < NW; ++k) {
+        uint32_t c4[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int q = 4 * k + r;
+          const uint64_t zq = z0 + static_cast<uint64_t>(q) * kPhi;
+          const uint32_t top = draw_top32(static_cast<uint32_t>(zq), static_cast<uint32_t>(zq >> 32));
+          const float u = __uint_as_float(__funnelshift_r(top, 0x7fu, 9)) - 1.f;  // u_f in [0,1)
+          const float h = v[q];
+          const float a = h - lo;
+          const float x = a * rf;
+          const float mm = __fadd_rz(x, 8388608.f);  // 2^23 + floor(x) for 0 <= x < 2^23
+          const float fr = x - (mm - 8388608.f);
+          const float d = u - fr;
+          // low byte: floor(x) + (u < fr), the sign of d (d = +0 when equal)
+          c4[r] = __float_as_uint(mm) + (__float_as_uint(d) >> 31);
+          const bool s = ((a != 0.f) & ((fabsf(fr - 0.5f) > hw) | (fabsf(d) <= dd))) | (h == hi);
+          if (s) slow |= 1u << q;
+        }
+        w8[k] = __byte_perm(__byte_perm(c4[0], c4[1], 0x0040), __byte_perm(c4[2], c4[3], 0x0040),
+                            0x5410);
+      }
+      if (!f32ok) slow = nvalid == 32 ? 0xffffffffu : (1u << nvalid) - 1u;
+    }
+    // LSB-first payload, zero padded to 16 bytes; the lane's run is EPL*b/8 bytes
+    uint8_t* payload = chunk + kHdrGpu;
+    const int pb = static_cast<int>(((packed_bytes(dim, b) + 15) / 16) * 16);
+    if (b == 8) {
+#pragma unroll
+      for (int k = 0; k < NW; k += 4) {
+        const int off = e0 + 4 * k;
+        if (off < pb)
+          *reinterpret_cast<uint4*>(payload + off) = make_uint4(w8[k], w8[k + 1], w8[k + 2], w8[k + 3]);
+      }
+    } else if (b == 4) {
+      uint32_t p[NW / 2];
+#pragma unroll
+      for (int k = 0; k < NW / 2; ++k) p[k] = pack4x4(w8[2 * k]) | pack4x4(w8[2 * k + 1]) << 16;
+      const int off = e0 / 2;
+      if constexpr (NW / 2 == 2) {
+        if (off < pb) *reinterpret_cast<uint2*>(payload + off) = make_uint2(p[0], p[1]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < NW / 2; k += 4)
+          if (off + 4 * k < pb)
+            *reinterpret_cast<uint4*>(payload + off + 4 * k) = make_uint4(p[k], p[k + 1], p[k + 2], p[k + 3]);
+      }
+    } else {
+      uint32_t p[NW / 4];
+#pragma unroll
+      for (int k = 0; k < NW / 4; ++k)
+        p[k] = pack4x2(w8[4 * k]) | pack4x2(w8[4 * k + 1]) << 8 | pack4x2(w8[4 * k + 2]) << 16 |
+               pack4x2(w8[4 * k + 3]) << 24;
+      const int off = e0 / 4;
+      if constexpr (NW / 4 == 1) {
+        if (off < pb) *reinterpret_cast<uint32_t*>(payload + off) = p[0];
+      } else {
+        if (off < pb) *reinterpret_cast<uint2*>(payload + off) = make_uint2(p[0], p[1]);
+      }
+    }
+    // lanes cover G*EPL*b/8 bytes; the rest of the 16-byte padding (small dims)
+    for (int off = G * EPL * b / 8 + 4 * j; off < pb; off += 4 * G)
+      *reinterpret_cast<uint32_t*>(payload + off) = 0u;
+    // flagged elements (h == hi, ~2e-4 near a decision boundary, or every element
+    // when S is outside the fp32 window): exact code patched into the payload this
+    // lane just wrote (its own bytes; same-thread order)
+    while (slow) {
+      const int q = __ffs(slow) - 1;
+      slow &= slow - 1;
+      const float h = row[e0 + q];
+      uint32_t c;
+      const uint32_t ub = f32ok && h == hi
+                              ? __funnelshift_r(draw_top32(static_cast<uint32_t>(z0 + q * kPhi),
+                                                           static_cast<uint32_t>((z0 + q * kPhi) >> 32)),
+                                                0x7fu, 9)
+                              : 0u;
+      if (ub != 0u && ub != Ab)
+        c = min(hib + (ub < Tb ? 1u : 0u), levels);
+      else
+        c = quant_slow(h, lo, hi, levels, z0, q);
+      const int e = e0 + q;
+      if (b == 8) {
+        payload[e] = static_cast<uint8_t>(c);
+      } else {
+        const int sh = b == 4 ? (e & 1) * 4 : (e & 3) * 2;
+        uint8_t* p = payload + (b == 4 ? e >> 1 : e >> 2);
+        *p = static_cast<uint8_t>((*p & ~(levels << sh)) | (c << sh));
+      }
+    }
+  }
+}
+
 // Decode counterpart: lane l writes the float4 chunks c = l + 32 i of the row.
 __global__ void __launch_bounds__(256) k_dequant_f32(
     const uint8_t* __restrict__ in, int64_t n, int dim, const uint8_t* __restrict__ bits,
@@ -763,7 +1063,34 @@ int qgnn_quantize_pack(qgnn_ctx* ctx, const void* values, int dtype, int64_t ld,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool fast = dtype == QGNN_F32 && layout == QGNN_WIRE_GPU && ld % 4 == 0 &&
                     (reinterpret_cast<uintptr_t>(values) & 15) == 0 && dim <= 1024;
-  if (fast) {
+  static const int grp = [] {
+    const char* e = std::getenv("QGNN_K1_GRP");  // 0: the round-1 lean kernel
+    return e ? std::atoi(e) : 1;
+  }();
+  if (fast && grp) {
+    static const int epl_env = [] {
+      const char* e = std::getenv("QGNN_K1_EPL");  // 16 or 32 elements per lane (default 32)
+      return e ? std::atoi(e) : 32;
+    }();
+    const int epl = (epl_env == 16 && dim <= 512) ? 16 : 32;
+    int lg = 0;
+    while ((int64_t(1) << lg) * epl < dim) ++lg;
+    const int64_t per_cta = (256 / 32) * (32 >> lg);  // messages per CTA per sweep
+    const int minb = epl == 16 ? 4 : 3;
+    const int64_t gblocks = std::min<int64_t>(ceil_div(n, per_cta), int64_t(ctx->num_sms) * minb);
+    auto* v = static_cast<const float*>(values);
+    auto* wl = static_cast<float*>(win_lo);
+    auto* wh = static_cast<float*>(win_hi);
+    const int d = static_cast<int>(dim);
+    if (epl == 16)
+      k_quantize_pack_grp<16, 4><<<gblocks, 256, 0, s>>>(v, ld, d, n, lg, rows, ids, bits, offsets,
+                                                        set_of, set_keys, out, wl, wh, ctx->d_err,
+                                                        envelope);
+    else
+      k_quantize_pack_grp<32, 3><<<gblocks, 256, 0, s>>>(v, ld, d, n, lg, rows, ids, bits, offsets,
+                                                        set_of, set_keys, out, wl, wh, ctx->d_err,
+                                                        envelope);
+  } else if (fast) {
     const int64_t fblocks = std::min<int64_t>(blocks, int64_t(ctx->num_sms) * 16);
     const int nv = static_cast<int>(ceil_div(ceil_div(dim, 4), 32));
     auto* v = static_cast<const float*>(values);

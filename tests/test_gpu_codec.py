@@ -215,3 +215,81 @@ def test_fast_path_codes_exact_on_adversarial_rows(cuda):
         s_, z_, p = port.quantize(X[i].astype(np.float64), int(bits[i]), port.fork(key, int(ids[i])))
         bad += int(not (w[o + 16:o + 16 + len(p)] == p).all())
     assert bad == 0
+
+
+K1_DIMS = [4, 12, 16, 20, 36, 64, 68, 100, 128, 256, 260, 500, 512, 516, 602, 1000, 1024]
+
+
+def _k1_rows(rs, kind, n, d, lv):
+    if kind == "gauss":
+        return rs.standard_normal((n, d))
+    if kind == "negzero":  # post-ReLU rows holding -0.0: first-occurrence signed zero
+        x = np.maximum(rs.standard_normal((n, d)), 0.0)
+        x[rs.random((n, d)) < 0.2] = -0.0
+        x[::5] = -0.0
+        x[1::5, 0] = 0.0
+        return x
+    if kind == "lattice":  # x = (h - lo) / S exactly integral, and one-ulp-scale noise
+        x = rs.integers(0, lv + 1, (n, d)) * 0.375 - 1.5
+        x[1::2] += rs.standard_normal((n // 2, d)) * 1e-7
+        return x
+    if kind == "tiny":
+        return rs.standard_normal((n, d)) * 1e-30
+    if kind == "huge":  # S > 2^100: the fp32 decision is off, every element exact
+        return rs.standard_normal((n, d)) * 1e36
+    x = np.repeat(rs.standard_normal((n, 1)), d, 1)  # constant rows: S = 0, no draws
+    x[::2, rs.integers(0, d)] += 1.0
+    return x
+
+
+@pytest.mark.parametrize("d", K1_DIMS)
+def test_k1_grouped_kernel_bit_exact(cuda, d):
+    """Production K1 (grouped lanes, fp32 decision with exact fallback) at every
+    lane-group shape: codes, headers and zero padding equal the oracle's."""
+    rs = np.random.default_rng(5000 + d)
+    ld = (d + 7) // 8 * 8
+    for kind in ("gauss", "negzero", "lattice", "tiny", "huge", "const"):
+        n = 48
+        bits = np.array([(2, 4, 8)[k % 3] for k in range(n)], np.int32)
+        x32 = np.zeros((n, ld), np.float32)
+        for b in (2, 4, 8):
+            sel = bits == b
+            x32[sel, :d] = _k1_rows(rs, kind, int(sel.sum()), d, (1 << b) - 1)
+        x32[:, d:] = np.nan  # row padding is never read as data
+        xt = torch.as_tensor(x32, device=cuda)[:, :d]
+        ids = (rs.permutation(50000)[:n] * 2 + 1).astype(np.uint32)
+        key = port.stream(11, 2, 3, 0, 1, 2)
+        wire, idx = ops.encode_message_set(xt, np.arange(n), ids, bits, key, layout=WIRE_GPU)
+        w = wire.cpu().numpy()
+        for k in range(n):
+            i = idx["pos"][k]
+            o = int(idx["off"][k])
+            b = int(bits[i])
+            s, z, p = port.quantize(x32[i, :d].astype(np.float64), b, port.fork(key, int(ids[i])))
+            hdr = w[o:o + 16]
+            assert hdr[:4].view(np.float32)[0] == np.float32(s), (kind, k)
+            assert hdr[4:8].view(np.float32)[0] == np.float32(z), (kind, k)
+            assert hdr[8:12].view(np.uint32)[0] == d and hdr[12] == b
+            nb = len(p)
+            assert (w[o + 16:o + 16 + nb] == p).all(), (kind, k, b)
+            assert (w[o + 16 + nb:o + 16 + ((nb + 15) // 16) * 16] == 0).all(), (kind, k, b)
+
+
+def test_k1_production_matches_round1_kernel_at_scale(cuda):
+    """400k messages per (dim, width): the grouped K1 writes the same wire bytes
+    as the round-1 lean kernel (itself bit-exact against the oracle above) --
+    catches rare-path bugs (flagged elements, patching) the small sets miss."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = os.path.join(root, "profiles", "k1_bench.py")
+
+    def digests(env):
+        out = subprocess.run([sys.executable, script, "400000"], capture_output=True, text=True,
+                             env={**os.environ, **env}, timeout=600, check=True).stdout
+        return [line.split("sha=")[1].strip() for line in out.splitlines() if "sha=" in line]
+
+    ref = digests({"QGNN_K1_GRP": "0"})
+    assert len(ref) == 6
+    assert digests({"QGNN_K1_GRP": "1"}) == ref
+    assert digests({"QGNN_K1_GRP": "1", "QGNN_K1_EPL": "16"}) == ref
