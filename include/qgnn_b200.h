@@ -203,6 +203,54 @@ int qgnn_exchange_plan(const int64_t* adj_ptr, const int32_t* adj, int64_t n,
                        int bits, int bwd, int layout, int dtype, uint64_t* send_bytes,
                        uint64_t* recv_bytes);
 
+/* partitions_from_owner (partition.hpp:39-84): one handle per device p in
+ * out[0..n_parts).  Lists (QGNN_PART_*) are ascending node ids exactly as the
+ * reference's Partition: owned / central / marginal, remote_in[q] (nodes owned
+ * by q that p consumes), remote_out[q] (owned nodes q consumes).  Any n_parts. */
+typedef struct qgnn_partition qgnn_partition;
+enum { QGNN_PART_OWNED = 0, QGNN_PART_CENTRAL = 1, QGNN_PART_MARGINAL = 2,
+       QGNN_PART_REMOTE_IN = 3, QGNN_PART_REMOTE_OUT = 4 };
+int qgnn_partitions_from_owner(const int64_t* adj_ptr, const int32_t* adj, int64_t n,
+                               const uint32_t* owner, int64_t n_parts, qgnn_partition** out);
+/* *ids stays valid until qgnn_partition_destroy; q is used by REMOTE_IN/OUT. */
+int qgnn_partition_list(const qgnn_partition* part, int which, int64_t q, const uint32_t** ids,
+                        int64_t* len);
+int qgnn_partition_destroy(qgnn_partition* part);
+
+/* DeviceAggView::build (tensorops/aggregate.hpp:41-89) with compute_coeffs
+ * (coeffs.hpp:30-45; sage = AggMode::kSageMean) for partition `part` of the
+ * owner map: the reference's row order (owned ascending) and slot order
+ * (remote_in by ascending source, ids ascending).  The GPU engine uses its own
+ * central-first layout of the same view internally. */
+typedef struct qgnn_agg_view qgnn_agg_view;
+typedef struct {
+  int64_t num_owned, num_remote, local_nnz, remote_nnz, n_parts, n_central, n_marginal;
+  const double* self_alpha;                    /* [num_owned] */
+  const int64_t* local_ptr;                    /* [num_owned + 1] */
+  const uint32_t* local_row;                   /* [local_nnz] owned-row index */
+  const double* local_alpha_fwd;               /* [local_nnz] */
+  const double* local_alpha_bwd;               /* [local_nnz] */
+  const int64_t* remote_ptr;                   /* [num_owned + 1] */
+  const uint32_t* remote_slot;                 /* [remote_nnz] */
+  const double* remote_alpha;                  /* [remote_nnz] */
+  const uint32_t* slot_node;                   /* [num_remote] */
+  const uint32_t* slot_owner;                  /* [num_remote] */
+  const int64_t* device_slot_offset;           /* [n_parts + 1] */
+  const uint32_t* central_rows;                /* [n_central] */
+  const uint32_t* marginal_rows;               /* [n_marginal] */
+} qgnn_agg_view_arrays;
+int qgnn_agg_view_build(const int64_t* adj_ptr, const int32_t* adj, int64_t n,
+                        const uint32_t* owner, const qgnn_partition* part, int sage,
+                        qgnn_agg_view** out);
+int qgnn_agg_view_arrays_get(const qgnn_agg_view* view, qgnn_agg_view_arrays* out);
+int qgnn_agg_view_destroy(qgnn_agg_view* view);
+
+/* BitWidthPlan::Lookup::bits_for (assigner/plan.hpp:60-72) over one
+ * (key, src, dst) entry list (ids ascending, bits parallel): out[k] = bits of
+ * query[k]; an unknown id fails with QGNN_EINVAL "plan: unknown message id". */
+int qgnn_plan_bits_for(const uint32_t* ids, const int32_t* bits, int64_t n,
+                       const uint32_t* query, int64_t n_query, int32_t* out);
+
 /* ---- K2 exchange: ring_all2all / comm_seconds (commsim/exchange.hpp:45-78,
  * trainer/engine.hpp:507-522) and the mailbox send / take (engine.hpp:502,
  * :528-529) ------------------------------------------------------------------

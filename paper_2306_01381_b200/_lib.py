@@ -86,6 +86,17 @@ class EpochMetrics(C.Structure):
 
 
 # name -> (restype, argtypes)
+class AggViewArrays(C.Structure):
+    """qgnn_agg_view_arrays (include/qgnn_b200.h): DeviceAggView, aggregate.hpp:17-90."""
+    _fields_ = [(k, C.c_int64) for k in ("num_owned", "num_remote", "local_nnz", "remote_nnz",
+                                          "n_parts", "n_central", "n_marginal")] + \
+               [(k, C.c_void_p) for k in ("self_alpha", "local_ptr", "local_row",
+                                           "local_alpha_fwd", "local_alpha_bwd", "remote_ptr",
+                                           "remote_slot", "remote_alpha", "slot_node",
+                                           "slot_owner", "device_slot_offset", "central_rows",
+                                           "marginal_rows")]
+
+
 _SIGS = {
     "qgnn_last_error": (C.c_char_p, []),
     "qgnn_version": (C.c_char_p, []),
@@ -124,6 +135,13 @@ _SIGS = {
     "qgnn_compute_coeffs": (C.c_int, [vp, vp, i64, C.c_int, vp, vp]),
     "qgnn_exchange_plan": (C.c_int, [vp, vp, i64, vp, i64, C.c_int, C.c_int, i64, C.c_int,
                                      C.c_int, C.c_int, C.c_int, vp, vp]),
+    "qgnn_partitions_from_owner": (C.c_int, [vp, vp, i64, vp, i64, vp]),
+    "qgnn_partition_list": (C.c_int, [vp, C.c_int, i64, C.POINTER(vp), C.POINTER(i64)]),
+    "qgnn_partition_destroy": (C.c_int, [vp]),
+    "qgnn_agg_view_build": (C.c_int, [vp, vp, i64, vp, vp, C.c_int, C.POINTER(vp)]),
+    "qgnn_agg_view_arrays_get": (C.c_int, [vp, C.POINTER(AggViewArrays)]),
+    "qgnn_agg_view_destroy": (C.c_int, [vp]),
+    "qgnn_plan_bits_for": (C.c_int, [vp, vp, i64, vp, i64, vp]),
     "qgnn_comm_create": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
     "qgnn_comm_destroy": (C.c_int, [vp]),
     "qgnn_exchange": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),

@@ -81,10 +81,13 @@ std::vector<uint32_t> partition_owner_bfs(const int64_t* ptr, const int32_t* adj
   return owner;
 }
 
-// partition.hpp:39-84 — consumer sets as per-node bitmasks (P <= 64).
+// partition.hpp:39-84.  Each node's consumer set (the other partitions owning
+// one of its neighbours) is a short ascending list in a CSR, so any P works;
+// remote_out[q] of p is filled in ascending node order and remote_in[q] of p
+// is q's remote_out[p] (the nodes q owns that p consumes).
 std::vector<Part> partitions_from_owner(const int64_t* ptr, const int32_t* adj, int64_t n,
                                         const uint32_t* owner, int64_t n_parts) {
-  QGNN_REQUIRE(n_parts >= 1 && n_parts <= 64, QGNN_EINVAL, "partitions: 1..64 parts supported");
+  QGNN_REQUIRE(n_parts >= 1, QGNN_EINVAL, "partitions: n_parts must be positive");
   std::vector<Part> parts(n_parts);
   for (int64_t p = 0; p < n_parts; ++p) {
     parts[p].id = static_cast<uint32_t>(p);
@@ -95,25 +98,41 @@ std::vector<Part> partitions_from_owner(const int64_t* ptr, const int32_t* adj, 
     QGNN_REQUIRE(owner[v] < n_parts, QGNN_EINVAL, "owner id out of range");
     parts[owner[v]].owned.push_back(static_cast<uint32_t>(v));
   }
-  std::vector<uint64_t> consumers(n, 0);
-  parallel_for(n, [&](int64_t v) {
-    uint64_t m = 0;
-    for (int64_t e = ptr[v]; e < ptr[v + 1]; ++e) {
-      const uint32_t q = owner[adj[e]];
-      if (q != owner[v]) m |= uint64_t{1} << q;
+  // consumers of v: distinct owner[u] != owner[v] over v's neighbours
+  std::vector<int64_t> cptr(n + 1, 0);
+  std::vector<std::vector<uint32_t>> cbuf(std::max<int64_t>(1, std::min<int64_t>(
+      n, std::max(1u, std::thread::hardware_concurrency()))));
+  const int64_t nb = static_cast<int64_t>(cbuf.size()), chunk = (n + nb - 1) / std::max<int64_t>(1, nb);
+  parallel_for(nb, [&](int64_t w) {
+    std::vector<uint32_t> tmp;
+    for (int64_t v = w * chunk; v < std::min(n, (w + 1) * chunk); ++v) {
+      tmp.clear();
+      for (int64_t e = ptr[v]; e < ptr[v + 1]; ++e) {
+        const uint32_t q = owner[adj[e]];
+        if (q != owner[v]) tmp.push_back(q);
+      }
+      std::sort(tmp.begin(), tmp.end());
+      tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+      cptr[v + 1] = static_cast<int64_t>(tmp.size());
+      cbuf[w].insert(cbuf[w].end(), tmp.begin(), tmp.end());
     }
-    consumers[v] = m;
+  });
+  for (int64_t v = 0; v < n; ++v) cptr[v + 1] += cptr[v];
+  std::vector<uint32_t> cons(cptr[n]);
+  parallel_for(nb, [&](int64_t w) {
+    const int64_t v0 = std::min(n, w * chunk);
+    if (!cbuf[w].empty()) std::copy(cbuf[w].begin(), cbuf[w].end(), cons.begin() + cptr[v0]);
   });
   parallel_for(n_parts, [&](int64_t p) {
     Part& P = parts[p];
-    for (uint32_t v : P.owned) (consumers[v] ? P.marginal : P.central).push_back(v);
-    for (int64_t q = 0; q < n_parts; ++q) {
-      if (q == p) continue;
-      for (uint32_t v : P.owned)
-        if (consumers[v] >> q & 1) P.remote_out[q].push_back(v);
-      for (uint32_t u : parts[q].owned)
-        if (consumers[u] >> p & 1) P.remote_in[q].push_back(u);
+    for (uint32_t v : P.owned) {
+      (cptr[v + 1] > cptr[v] ? P.marginal : P.central).push_back(v);
+      for (int64_t k = cptr[v]; k < cptr[v + 1]; ++k) P.remote_out[cons[k]].push_back(v);
     }
+  });
+  parallel_for(n_parts, [&](int64_t p) {
+    for (int64_t q = 0; q < n_parts; ++q)
+      if (q != p) parts[p].remote_in[q] = parts[q].remote_out[p];
   });
   return parts;
 }
@@ -349,6 +368,170 @@ int qgnn_partition_stats(const int64_t* adj_ptr, const int32_t* adj, int64_t n,
     out[5 * p + 2] = static_cast<int64_t>(parts[p].marginal.size());
     out[5 * p + 3] = halo;
     out[5 * p + 4] = outm;
+  }
+  QGNN_API_END
+}
+
+
+// ---- partitions_from_owner / DeviceAggView::build / Lookup::bits_for ---------
+}  // extern "C"
+
+struct qgnn_partition {
+  Part part;
+};
+
+struct qgnn_agg_view {
+  std::vector<double> self_alpha, local_alpha_fwd, local_alpha_bwd, remote_alpha;
+  std::vector<int64_t> local_ptr, remote_ptr, device_slot_offset;
+  std::vector<uint32_t> local_row, remote_slot, slot_node, slot_owner, central_rows, marginal_rows;
+  int64_t num_owned = 0, num_remote = 0;
+};
+
+extern "C" {
+
+int qgnn_partitions_from_owner(const int64_t* adj_ptr, const int32_t* adj, int64_t n,
+                               const uint32_t* owner, int64_t n_parts, qgnn_partition** out) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(out, QGNN_EINVAL, "partitions: null output");
+  auto parts = partitions_from_owner(adj_ptr, adj, n, owner, n_parts);
+  for (int64_t p = 0; p < n_parts; ++p) out[p] = new qgnn_partition{std::move(parts[p])};
+  QGNN_API_END
+}
+
+int qgnn_partition_destroy(qgnn_partition* part) {
+  delete part;
+  return QGNN_OK;
+}
+
+int qgnn_partition_list(const qgnn_partition* part, int which, int64_t q, const uint32_t** ids,
+                        int64_t* len) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(part && ids && len, QGNN_EINVAL, "partition_list: null argument");
+  const Part& P = part->part;
+  const std::vector<uint32_t>* v = nullptr;
+  switch (which) {
+    case QGNN_PART_OWNED: v = &P.owned; break;
+    case QGNN_PART_CENTRAL: v = &P.central; break;
+    case QGNN_PART_MARGINAL: v = &P.marginal; break;
+    case QGNN_PART_REMOTE_IN:
+    case QGNN_PART_REMOTE_OUT:
+      QGNN_REQUIRE(q >= 0 && q < static_cast<int64_t>(P.remote_in.size()), QGNN_EINVAL,
+                   "partition_list: device out of range");
+      v = which == QGNN_PART_REMOTE_IN ? &P.remote_in[q] : &P.remote_out[q];
+      break;
+    default:
+      QGNN_REQUIRE(false, QGNN_EINVAL, "partition_list: unknown list");
+  }
+  *ids = v->data();
+  *len = static_cast<int64_t>(v->size());
+  QGNN_API_END
+}
+
+// DeviceAggView::build (aggregate.hpp:41-89) in the reference's row order (owned
+// ascending): slots concatenate remote_in by ascending source; per owned row the
+// adjacency is split into same-device (local) and cross-device (remote) entries
+// in adjacency order; rows with a remote entry are marginal.
+int qgnn_agg_view_build(const int64_t* adj_ptr, const int32_t* adj, int64_t n,
+                        const uint32_t* owner, const qgnn_partition* part, int sage,
+                        qgnn_agg_view** out) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(part && out && owner, QGNN_EINVAL, "agg_view: null argument");
+  const Part& P = part->part;
+  const uint32_t me = P.id;
+  const int64_t n_parts = static_cast<int64_t>(P.remote_in.size());
+  std::vector<double> alpha, self_alpha;
+  compute_coeffs(adj_ptr, adj, n, sage != 0, alpha, self_alpha);
+  auto* V = new qgnn_agg_view;
+  V->num_owned = static_cast<int64_t>(P.owned.size());
+  V->device_slot_offset.assign(n_parts + 1, 0);
+  for (int64_t q = 0; q < n_parts; ++q) {
+    V->device_slot_offset[q] = static_cast<int64_t>(V->slot_node.size());
+    for (uint32_t k : P.remote_in[q]) {
+      V->slot_node.push_back(k);
+      V->slot_owner.push_back(static_cast<uint32_t>(q));
+    }
+  }
+  V->device_slot_offset[n_parts] = static_cast<int64_t>(V->slot_node.size());
+  V->num_remote = static_cast<int64_t>(V->slot_node.size());
+  auto row_of = [&](uint32_t v) {  // owned ascending: binary search
+    return static_cast<uint32_t>(std::lower_bound(P.owned.begin(), P.owned.end(), v) - P.owned.begin());
+  };
+  auto slot_of = [&](uint32_t u) {  // slots of source q are ascending ids
+    const uint32_t q = owner[u];
+    const auto& in = P.remote_in[q];
+    return static_cast<uint32_t>(V->device_slot_offset[q] +
+                                 (std::lower_bound(in.begin(), in.end(), u) - in.begin()));
+  };
+  V->local_ptr.assign(V->num_owned + 1, 0);
+  V->remote_ptr.assign(V->num_owned + 1, 0);
+  V->self_alpha.resize(V->num_owned);
+  for (int64_t i = 0; i < V->num_owned; ++i) {
+    const uint32_t v = P.owned[i];
+    V->self_alpha[i] = self_alpha[v];
+    bool has_remote = false;
+    for (int64_t e = adj_ptr[v]; e < adj_ptr[v + 1]; ++e) {
+      const uint32_t u = static_cast<uint32_t>(adj[e]);
+      if (owner[u] == me) {
+        V->local_row.push_back(row_of(u));
+        V->local_alpha_fwd.push_back(alpha[e]);
+        // coeffs.of(g, v, u): u's adjacency entry for v (graph.hpp sorted lists)
+        const int32_t* b = adj + adj_ptr[u];
+        const int32_t* f = std::lower_bound(b, adj + adj_ptr[u + 1], static_cast<int32_t>(v));
+        V->local_alpha_bwd.push_back(alpha[adj_ptr[u] + (f - b)]);
+      } else {
+        V->remote_slot.push_back(slot_of(u));
+        V->remote_alpha.push_back(alpha[e]);
+        has_remote = true;
+      }
+    }
+    V->local_ptr[i + 1] = static_cast<int64_t>(V->local_row.size());
+    V->remote_ptr[i + 1] = static_cast<int64_t>(V->remote_slot.size());
+    (has_remote ? V->marginal_rows : V->central_rows).push_back(static_cast<uint32_t>(i));
+  }
+  *out = V;
+  QGNN_API_END
+}
+
+int qgnn_agg_view_destroy(qgnn_agg_view* view) {
+  delete view;
+  return QGNN_OK;
+}
+
+int qgnn_agg_view_arrays_get(const qgnn_agg_view* v, qgnn_agg_view_arrays* a) {
+  QGNN_API_BEGIN
+  QGNN_REQUIRE(v && a, QGNN_EINVAL, "agg_view: null argument");
+  a->num_owned = v->num_owned;
+  a->num_remote = v->num_remote;
+  a->local_nnz = static_cast<int64_t>(v->local_row.size());
+  a->remote_nnz = static_cast<int64_t>(v->remote_slot.size());
+  a->n_parts = static_cast<int64_t>(v->device_slot_offset.size()) - 1;
+  a->n_central = static_cast<int64_t>(v->central_rows.size());
+  a->n_marginal = static_cast<int64_t>(v->marginal_rows.size());
+  a->self_alpha = v->self_alpha.data();
+  a->local_ptr = v->local_ptr.data();
+  a->local_row = v->local_row.data();
+  a->local_alpha_fwd = v->local_alpha_fwd.data();
+  a->local_alpha_bwd = v->local_alpha_bwd.data();
+  a->remote_ptr = v->remote_ptr.data();
+  a->remote_slot = v->remote_slot.data();
+  a->remote_alpha = v->remote_alpha.data();
+  a->slot_node = v->slot_node.data();
+  a->slot_owner = v->slot_owner.data();
+  a->device_slot_offset = v->device_slot_offset.data();
+  a->central_rows = v->central_rows.data();
+  a->marginal_rows = v->marginal_rows.data();
+  QGNN_API_END
+}
+
+// BitWidthPlan::Lookup::bits_for (plan.hpp:60-72) for one (key, src, dst)
+// entry list: ids ascending, bits parallel.  Unknown ids fail like the reference.
+int qgnn_plan_bits_for(const uint32_t* ids, const int32_t* bits, int64_t n,
+                       const uint32_t* query, int64_t n_query, int32_t* out) {
+  QGNN_API_BEGIN
+  for (int64_t k = 0; k < n_query; ++k) {
+    const uint32_t* it = std::lower_bound(ids, ids + n, query[k]);
+    QGNN_REQUIRE(it != ids + n && *it == query[k], QGNN_EINVAL, "plan: unknown message id");
+    out[k] = bits[it - ids];
   }
   QGNN_API_END
 }

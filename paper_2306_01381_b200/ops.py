@@ -296,3 +296,90 @@ def adam_step(p, m, v, g, t, lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8):
     check(lib.qgnn_adam_step(ctx(), _dtype(p), _ptr(p), _ptr(m), _ptr(v), _ptr(g), p.numel(), lr,
                              beta1, beta2, eps, bc1, bc2, _stream()))
     return p
+
+
+# ---- graphcore/partition.hpp, tensorops/aggregate.hpp, assigner/plan.hpp (host) -------------
+def partitions_from_owner(adj_ptr, adj, owner, n_parts: int):
+    """partitions_from_owner (partition.hpp:39-84) through the C-ABI: one dict
+    per device with owned / central / marginal and remote_in[q] / remote_out[q]
+    (ascending node ids, like Partition)."""
+    adj_ptr = np.ascontiguousarray(adj_ptr, np.int64)
+    adj = np.ascontiguousarray(adj, np.int32)
+    owner = np.ascontiguousarray(owner, np.uint32)
+    hs = (C.c_void_p * n_parts)()
+    check(lib.qgnn_partitions_from_owner(adj_ptr.ctypes.data, adj.ctypes.data, len(owner),
+                                         owner.ctypes.data, n_parts, hs))
+
+    def lst(h, which, q=0):
+        p, n = C.c_void_p(), C.c_int64()
+        check(lib.qgnn_partition_list(h, which, q, C.byref(p), C.byref(n)))
+        if n.value == 0:
+            return np.zeros(0, np.uint32)
+        return np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint32)), (n.value,)).copy()
+
+    out = []
+    try:
+        for h in hs:
+            out.append(dict(owned=lst(h, 0), central=lst(h, 1), marginal=lst(h, 2),
+                            remote_in=[lst(h, 3, q) for q in range(n_parts)],
+                            remote_out=[lst(h, 4, q) for q in range(n_parts)]))
+    finally:
+        for h in hs:
+            lib.qgnn_partition_destroy(h)
+    return out
+
+
+def agg_view(adj_ptr, adj, owner, n_parts: int, device: int, sage: bool = False):
+    """DeviceAggView::build (aggregate.hpp:41-89) for `device` of the owner map,
+    reference row / slot order, as numpy arrays."""
+    adj_ptr = np.ascontiguousarray(adj_ptr, np.int64)
+    adj = np.ascontiguousarray(adj, np.int32)
+    owner = np.ascontiguousarray(owner, np.uint32)
+    hs = (C.c_void_p * n_parts)()
+    check(lib.qgnn_partitions_from_owner(adj_ptr.ctypes.data, adj.ctypes.data, len(owner),
+                                         owner.ctypes.data, n_parts, hs))
+    view = C.c_void_p()
+    try:
+        check(lib.qgnn_agg_view_build(adj_ptr.ctypes.data, adj.ctypes.data, len(owner),
+                                      owner.ctypes.data, hs[device], int(sage), C.byref(view)))
+    finally:
+        for h in hs:
+            lib.qgnn_partition_destroy(h)
+    try:
+        a = _lib.AggViewArrays()
+        check(lib.qgnn_agg_view_arrays_get(view, C.byref(a)))
+
+        def arr(ptr, n, ct, dt):
+            if n == 0:
+                return np.zeros(0, dt)
+            return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ct)), (n,)).astype(dt)
+
+        no, nr, ln, rn = a.num_owned, a.num_remote, a.local_nnz, a.remote_nnz
+        return dict(num_owned=no, num_remote=nr,
+                    self_alpha=arr(a.self_alpha, no, C.c_double, np.float64),
+                    local_ptr=arr(a.local_ptr, no + 1, C.c_int64, np.int64),
+                    local_row=arr(a.local_row, ln, C.c_uint32, np.int64),
+                    local_alpha_fwd=arr(a.local_alpha_fwd, ln, C.c_double, np.float64),
+                    local_alpha_bwd=arr(a.local_alpha_bwd, ln, C.c_double, np.float64),
+                    remote_ptr=arr(a.remote_ptr, no + 1, C.c_int64, np.int64),
+                    remote_slot=arr(a.remote_slot, rn, C.c_uint32, np.int64),
+                    remote_alpha=arr(a.remote_alpha, rn, C.c_double, np.float64),
+                    slot_node=arr(a.slot_node, nr, C.c_uint32, np.uint32),
+                    slot_owner=arr(a.slot_owner, nr, C.c_uint32, np.uint32),
+                    device_slot_offset=arr(a.device_slot_offset, a.n_parts + 1, C.c_int64,
+                                           np.int64),
+                    central=arr(a.central_rows, a.n_central, C.c_uint32, np.int64),
+                    marginal=arr(a.marginal_rows, a.n_marginal, C.c_uint32, np.int64))
+    finally:
+        lib.qgnn_agg_view_destroy(view)
+
+
+def plan_bits_for(ids, bits, query):
+    """BitWidthPlan::Lookup::bits_for (plan.hpp:60-72) over one pair's sorted entries."""
+    ids = np.ascontiguousarray(ids, np.uint32)
+    bits = np.ascontiguousarray(bits, np.int32)
+    query = np.ascontiguousarray(query, np.uint32)
+    out = np.zeros(max(1, len(query)), np.int32)
+    check(lib.qgnn_plan_bits_for(ids.ctypes.data, bits.ctypes.data, len(ids), query.ctypes.data,
+                                 len(query), out.ctypes.data))
+    return out[:len(query)]

@@ -274,3 +274,45 @@ def test_decode_index_validation_matches_reference():
             with pytest.raises(RefError) as ei:
                 ref.decode_message_set(w, idx, total)
             assert msg in str(ei.value), (name, str(ei.value))
+
+
+@pytest.mark.skipif(not ref_available(), reason="compiled reference not present")
+@pytest.mark.parametrize("n_parts", [2, 8, 70])
+def test_partitions_and_views_match_reference(n_parts):
+    """partitions_from_owner (partition.hpp:39-84) and DeviceAggView::build
+    (aggregate.hpp:41-89) through the C-ABI equal the compiled reference's, for
+    BFS and random owner maps, GCN and SAGE coefficients (P = 70 > 64 too)."""
+    from oracle import ref
+    from paper_2306_01381_b200 import ops
+    g = ref.generate_dataset("cite", nodes=2500, classes=8, feature_dim=4, attach_edges=6, seed=5)
+    ptr, adj = g["adj_ptr"], g["adj"]
+    rs = np.random.default_rng(n_parts)
+    owners = [ref.partition_owner(ptr, adj, n_parts, 7),
+              rs.integers(0, n_parts, len(ptr) - 1).astype(np.uint32)]
+    for owner in owners:
+        parts = ops.partitions_from_owner(ptr, adj, owner, n_parts)
+        for dev in sorted({0, n_parts // 2, n_parts - 1}):
+            for sage in (False, True):
+                rv = ref.view(ptr, adj, owner, n_parts, dev, sage=sage).v
+                P = parts[dev]
+                assert (P["owned"] == rv["owned"]).all()
+                for q in range(n_parts):
+                    assert (P["remote_in"][q] == rv["remote_in"][q]).all(), q
+                    assert (P["remote_out"][q] == rv["remote_out"][q]).all(), q
+                v = ops.agg_view(ptr, adj, owner, n_parts, dev, sage=sage)
+                assert (P["owned"][v["central"]] == P["central"]).all()
+                assert (P["owned"][v["marginal"]] == P["marginal"]).all()
+                for k in ("self_alpha", "local_ptr", "local_row", "local_alpha_fwd",
+                          "local_alpha_bwd", "remote_ptr", "remote_slot", "remote_alpha",
+                          "slot_node", "slot_owner", "device_slot_offset", "central",
+                          "marginal"):
+                    assert np.array_equal(v[k], rv[k].astype(v[k].dtype)), (k, dev, sage)
+
+
+def test_plan_bits_for_lookup():  # plan.hpp:60-72
+    from paper_2306_01381_b200 import InvalidArgument, ops
+    ids = np.array([3, 9, 10, 44], np.uint32)
+    bits = np.array([2, 8, 4, 8], np.int32)
+    assert list(ops.plan_bits_for(ids, bits, [44, 3, 10, 9])) == [8, 2, 4, 8]
+    with pytest.raises(InvalidArgument, match="unknown message id"):
+        ops.plan_bits_for(ids, bits, [5])
