@@ -33,8 +33,21 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = dict(nodes=2449029, n_edges=61859140, feat=100, hidden=256, classes=47, parts=8,
-                cross_frac=0.0085, gamma=2.8, seed=1)
+# BASELINE.json configs: planted-block power-law graphs of the
+# named shapes; cross_frac calibrated (scratch runs of qgnn_partition_stats on
+# the full graphs) to the paper's remote ratios (halo / owned).  At N = 1 all
+# P partitions live on one GPU; at N > 1 they spread over the GPUs.
+CONFIGS = {
+    2: dict(name="Reddit-shaped", nodes=232965, n_edges=57307946, feat=602, hidden=256,
+            classes=41, parts=4, cross_frac=0.0016, gamma=2.8, seed=1, sage=False),
+    3: dict(name="Yelp-shaped", nodes=716847, n_edges=6977410, feat=300, hidden=256,
+            classes=100, parts=8, cross_frac=0.0218, gamma=2.8, seed=1, sage=True),
+    4: dict(name="ogbn-products-shaped", nodes=2449029, n_edges=61859140, feat=100, hidden=256,
+            classes=47, parts=8, cross_frac=0.0085, gamma=2.8, seed=1, sage=False),
+    5: dict(name="AmazonProducts-shaped", nodes=1569960, n_edges=132169734, feat=200,
+            hidden=256, classes=107, parts=8, cross_frac=0.0034, gamma=2.8, seed=1, sage=True),
+}
+WORKLOAD = CONFIGS[4]  # the north-star configuration (BASELINE configs[3])
 METRIC = "full-graph GCN epoch time (s)"
 # random-row gather ceiling measured on B200 by profiles/gather_probe.cu
 # (L2-resident table, 256-512 B rows): the bound of a gather-form SpMM
@@ -53,14 +66,21 @@ def peaks():
         return 6650.0, 1590.0, "fallback"
 
 
-def config_dict(n_gpus, bit_mode):
+def bit_desc(args):
+    return f"fixed:{args.bits}" if args.bit_mode == "fixed" else args.bit_mode
+
+
+def config_dict(n_gpus, args):
     w = WORKLOAD
-    return {"workload": "ogbn-products-shaped planted-block power-law graph, 3-layer GCN "
-                        "hidden 256, P=8 partitions, AdaQP " + bit_mode + " bit-width",
+    model = "GraphSAGE-mean" if w["sage"] else "GCN"
+    return {"workload": f"{w['name']} planted-block power-law graph, 3-layer {model} hidden "
+                        f"{w['hidden']}, P={w['parts']} partitions, AdaQP {bit_desc(args)} "
+                        f"bit-width", "baseline_config": args.config,
             "nodes": w["nodes"], "csr_nnz": 2 * w["n_edges"], "features": w["feat"],
             "hidden": w["hidden"], "classes": w["classes"], "partitions": w["parts"],
+            "model": model, "cross_frac": w["cross_frac"],
             "parallelism": f"graph-partition dp{n_gpus} ({w['parts'] // n_gpus} partitions/GPU)",
-            "bit_mode": bit_mode, "l2": "inputs larger than L2 (no flush)"}
+            "bit_mode": bit_desc(args), "l2": "inputs larger than L2 (no flush)"}
 
 
 class ClockSampler:
@@ -154,7 +174,7 @@ def workload_graph(scale_div=1):
                             seed=w["seed"])
 
 
-def run_reference_epochs(g, epochs, bit_mode="adaptive"):
+def run_reference_epochs(g, epochs, bit_mode="adaptive", bits=8):
     """The compiled reference Engine (oracle/_ref: trainer/engine.hpp, unmodified)
     in ExecMode::kThreads (one host thread per partition), partitioned like the
     GPU arm: planted owner map -> partitions_from_owner (partition.hpp:39).
@@ -165,8 +185,9 @@ def run_reference_epochs(g, epochs, bit_mode="adaptive"):
     g = dict(g)
     g["features"] = np.ascontiguousarray(g["features"], np.float64)  # fp32-representable
     times = np.zeros(2)
-    ep, _ = ref.engine_run(g, dims, w["parts"], bit_mode=BIT_CODES[bit_mode], fixed_bits=8,
-                           epochs=epochs, seed=7, group_size=2000, period=50, threads=True,
+    ep, _ = ref.engine_run(g, dims, w["parts"], bit_mode=BIT_CODES[bit_mode], fixed_bits=bits,
+                           epochs=epochs, seed=7, sage=w["sage"], group_size=2000, period=50,
+                           threads=True,
                            theta=1.0 / (900e9 * 8), gamma=2e-5, owner=g["owner"], times=times)
     return times[1] / epochs, times[0], ep
 
@@ -174,13 +195,13 @@ def run_reference_epochs(g, epochs, bit_mode="adaptive"):
 BIT_CODES = {"fp": 0, "fixed": 1, "uniform": 2, "adaptive": 3}
 
 
-def cpu_baseline_sample(bit_mode, div=16, epochs=2):
+def cpu_baseline_sample(bit_mode, bits=8, div=16, epochs=2):
     """cpu_baseline: the reference engine on a bounded 1/div sample of the
     workload (same generator, owner map, dims, P), Engine::run seconds per
     epoch (setup excluded) scaled by div (epoch work is linear in nodes and
     nnz: SpMM + dense rows)."""
     g = workload_graph(div)
-    per, setup, ep = run_reference_epochs(g, epochs, bit_mode)
+    per, setup, ep = run_reference_epochs(g, epochs, bit_mode, bits)
     return {"value": per * div, "unit": "s", "cores": REF_THREADS, "kind": "reference",
             "sample": f"reference Engine (oracle/_ref, kThreads: {REF_THREADS} partitions = "
                       f"{REF_THREADS} threads, planted owner map -> partitions_from_owner) on "
@@ -213,13 +234,13 @@ def impl_reference(args):
     g = workload_graph(1)
     t_gen = time.time() - t0
     k = max(1, min(args.steps, args.ref_epochs))
-    per, setup, ep = run_reference_epochs(g, k, args.bit_mode)
+    per, setup, ep = run_reference_epochs(g, k, args.bit_mode, args.bits)
     value = per
     line = {"metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus, "steps": k,
             "warmup": 0, "steps_requested": args.steps, "warmup_requested": args.warmup,
             "ms_per_step": value * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference", "config": config_dict(args.gpus, args.bit_mode),
+            "impl": "reference", "config": config_dict(args.gpus, args),
             "cpu_baseline": {"value": value, "unit": "s", "cores": REF_THREADS,
                              "kind": "reference",
                              "sample": f"full workload ({len(g['adj_ptr']) - 1} nodes, "
@@ -253,7 +274,8 @@ def impl_ours(args):
     bit_mode = args.bit_mode
     t0 = time.time()
     eng = Engine(g, [w["feat"], w["hidden"], w["hidden"], w["classes"]], n_parts=w["parts"],
-                 bit_mode=bit_mode, fixed_bits=8, seed=7, group_size=2000, period=50,
+                 bit_mode=bit_mode, fixed_bits=args.bits, seed=7, sage=w["sage"],
+                 group_size=2000, period=50,
                  theta=1.0 / (900e9 * 8), gamma=2e-5, dtype="f32", owner=g["owner"], rank=rank,
                  world=world, device=local, nccl_id=nid, kstats=True)
     t_setup = time.time() - t0
@@ -364,14 +386,14 @@ def impl_ours(args):
     cpu = None
     if world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_baseline_sample(bit_mode)
+            cpu = cpu_baseline_sample(bit_mode, args.bits)
         except Exception as exc:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {exc}"}
     line = {"metric": METRIC, "value": dev_s, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_s * 1e3,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": config_dict(world, bit_mode),
+            "data": "synthetic", "config": config_dict(world, args),
             "wall_s_per_step": wall_s,
             # SURVEY 8(d) asks for the median epoch too (value is the mean of the K steps)
             "median_ms_per_step": med_ms,
@@ -422,11 +444,17 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--bit-mode", default="adaptive",
                     choices=["adaptive", "fixed", "fp", "uniform"])
+    ap.add_argument("--bits", type=int, default=8, choices=[2, 4, 8],
+                    help="width of --bit-mode fixed")
+    ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS),
+                    help="BASELINE.json config (4 = the north-star ogbn-products shape)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-epochs", type=int, default=2,
                     help="reference arm: full-size epochs timed (min with --steps)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    global WORKLOAD
+    WORKLOAD = CONFIGS[args.config]
     if args.impl == "reference":
         impl_reference(args)
     else:
