@@ -137,13 +137,31 @@ struct HubPlan {
   int32_t* cnt = nullptr;            // [n_hubs] arrivals; zero between launches
   double avg_deg = 0;                // mean (a + b) degree of the range's rows
 };
+// Forward halo rows read straight from the exchange arena:
+// remote slot s is message s of the receive list, its chunk at arena + off[s]
+// with width bits[s]; the marginal SpMM dequantizes the 8 columns a lane needs
+// in registers (code * S + Z, the value K3 would have stored) instead of
+// reading a materialised fp32 halo row.  Headers are checked like K3 (width,
+// count -> kErrDecode; envelope env[s] -> kErrProtocol).
+struct PackedHalo {
+  const uint8_t* arena = nullptr;
+  const uint64_t* off = nullptr;
+  const uint8_t* bits = nullptr;
+  const uint32_t* env = nullptr;
+  int dim = 0;
+  int* err = nullptr;
+};
 // fp32 row-range SpMM with segmented hub rows (spmm.cu)
-// returns the number of kernels launched
+// returns the number of kernels launched.  pk != nullptr: the b range (remote
+// CSR) gathers from the packed arena instead of y (spmm_packed_ok must hold).
 int spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y, int64_t ldy,
               const float* sa, const int64_t* pa, const int32_t* ca, const float* aa,
               const int64_t* pb, const int32_t* cb, const float* ab, int64_t row_begin,
               int64_t n_rows, float* out, int64_t ldo, const HubPlan* hp, cudaStream_t s,
-              const float* mask = nullptr, int64_t ldm = 0);
+              const float* mask = nullptr, int64_t ldm = 0, const PackedHalo* pk = nullptr);
+// whether spmm_f32 runs this range through a kernel with a packed-halo variant
+// (the grouped <= 128-wide and the 256-wide row kernels, 32-byte aligned rows)
+bool spmm_packed_ok(int dim, const HubPlan* hp, const float* x, int64_t ldx);
 // fp32 GPU-layout decode + scatter-add, ReLU-backward mask by h (codec.cu)
 void dequant_add_masked_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int dim,
                             const uint8_t* bits, const uint64_t* offsets, const int32_t* dst_rows,

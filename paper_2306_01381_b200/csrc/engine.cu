@@ -413,10 +413,11 @@ class Engine final : public EngineBase {
   int spmm(int64_t dim, const T* x, int64_t ldx, const T* y, int64_t ldy, const T* sa,
            const int64_t* pa, const int32_t* ca, const T* aa, const int64_t* pb,
            const int32_t* cb, const T* ab, int64_t r0, int64_t n, T* out, int64_t ldo,
-           const HubPlan* hubs, const T* mask = nullptr, int64_t ldm = 0) {
+           const HubPlan* hubs, const T* mask = nullptr, int64_t ldm = 0,
+           const PackedHalo* pk = nullptr) {
     if constexpr (sizeof(T) == 4) {
       return spmm_f32(ctx_, int(round_up(dim, 4)), x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, r0,
-                      n, out, ldo, hubs, s_main_, mask, ldm);
+                      n, out, ldo, hubs, s_main_, mask, ldm, pk);
     } else {
       const int st = qgnn_csr_aggregate(ctx_, dtype_, dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb,
                                         ab, nullptr, r0, n, out, ldo, s_main_);
@@ -458,6 +459,11 @@ class Engine final : public EngineBase {
   }
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   void decode_halo(int k, int64_t din, int64_t ldi, cudaStream_t st);
+  // §8f rank 1: forward key k's marginal SpMM reads the halo rows straight from
+  // the exchange arena (no K3 store, no fp32 halo) when every partition's
+  // marginal range runs through a kernel with a packed variant (fp32, GPU layout)
+  bool packed_fwd(int k, int64_t din, int64_t ldi);
+  PackedHalo packed_halo(PartDev& D, int k, int64_t din);
   void exchange(int k);
   void forward_layer(int l);
   void forward_last_tf(int l);
@@ -1525,6 +1531,37 @@ void Engine<T>::allgather_dev(X* base, int64_t slice, cudaStream_t st) {
   } while (0)
 
 template <typename T>
+bool Engine<T>::packed_fwd(int k, int64_t din, int64_t ldi) {
+  if constexpr (sizeof(T) != 4) {
+    return false;
+  } else {
+    static const bool on = [] {
+      const char* e = std::getenv("QGNN_PACKED_HALO");  // 0: K3 into the fp32 halo (round 1)
+      return !e || std::atoi(e) != 0;
+    }();
+    if (!on || s_.layout != QGNN_WIRE_GPU || keys_[k].bwd) return false;
+    for (auto& up : parts_dev_)
+      if (up->view.n_marginal &&
+          !spmm_packed_ok(int(round_up(din, 4)), &up->hub_fm.plan, up->h[k].p, ldi))
+        return false;
+    return true;
+  }
+}
+
+template <typename T>
+PackedHalo Engine<T>::packed_halo(PartDev& D, int k, int64_t din) {
+  auto& R = D.rcv[k];
+  PackedHalo pk;
+  pk.arena = arena_.p;
+  pk.off = R.off.p;
+  pk.bits = R.bits.p;
+  pk.env = R.env.p;
+  pk.dim = int(din);
+  pk.err = ctx_->d_err;
+  return pk;
+}
+
+template <typename T>
 void Engine<T>::forward_layer(int l) {
   const int t = l - 1;
   const int k = t;  // forward key index
@@ -1557,11 +1594,12 @@ void Engine<T>::forward_layer(int l) {
   // soon as its rows exist; otherwise every encode precedes the exchange, which
   // the central rows then overlap.
   const bool feats = t == 0 && feat_pending_;
+  const bool pkd = packed_fwd(k, din, ldi);  // no K3: the marginal SpMM decodes in registers
   if (side_overlap() && !feats) {
     // one GPU: encode + decode on the side stream while the central rows run
     fork_side();
     for (auto& up : parts_dev_) quantize(*up, k, up->h[t].p, ldi, s_comm_);  // fwd_send
-    decode_halo(k, din, ldi, s_comm_);
+    if (!pkd) decode_halo(k, din, ldi, s_comm_);
     for (auto& up : parts_dev_) central(*up);
     join_side();
   } else {
@@ -1582,7 +1620,7 @@ void Engine<T>::forward_layer(int l) {
       for (auto& up : parts_dev_) central(*up);
     }
     wait_exchange();
-    decode_halo(k, din, ldi, s_main_);
+    if (!pkd) decode_halo(k, din, ldi, s_main_);
   }
   // marginal rows (engine.hpp:622-623)
   for (auto& up : parts_dev_) {
@@ -1596,14 +1634,23 @@ void Engine<T>::forward_layer(int l) {
     }
     if (!nm) continue;
     kbegin(QGNN_K_SPMM_FWD);
-    const int nk = spmm(din, D.h[t].p, ldi, D.halo.p, ldi, D.self_alpha.p, D.lptr.p, D.lcol.p,
-                        D.lafwd.p, D.rptr.p, D.rslot.p, D.ralpha.p, nc, nm, D.hagg[t].p, ldi,
-                        &D.hub_fm.plan);
+    const PackedHalo pk = pkd ? packed_halo(D, k, din) : PackedHalo{};
+    const int nk = spmm(din, D.h[t].p, ldi, pkd ? nullptr : D.halo.p, ldi, D.self_alpha.p, D.lptr.p,
+                        D.lcol.p, D.lafwd.p, D.rptr.p, D.rslot.p, D.ralpha.p, nc, nm,
+                        D.hagg[t].p, ldi, &D.hub_fm.plan, nullptr, 0, pkd ? &pk : nullptr);
     const double nnz = double(D.view.local_ptr[nc + nm] - D.view.local_ptr[nc]) +
                        double(D.view.remote_nnz());
+    // remote source rows: fp32 halo rows, or their packed chunks (+ offset, width)
+    double slot_bytes = double(din * sizeof(T));
+    if (pkd && D.rcv[k].n) {
+      double in = 0;
+      for (int64_t src = 0; src < P_; ++src)
+        if (src != D.id) in += double(msgs_[k][src][D.id].bytes);
+      slot_bytes = in / double(D.rcv[k].n) + 9;
+    }
     kend(QGNN_K_SPMM_FWD, nm * (24.0 + din * sizeof(T)) + nnz * (4 + sizeof(T)) +
-                              double(D.view.src_rows_marginal + D.view.src_slots_marginal) *
-                                  din * sizeof(T), s_main_, nk,
+                              double(D.view.src_rows_marginal) * din * sizeof(T) +
+                              double(D.view.src_slots_marginal) * slot_bytes, s_main_, nk,
          (nnz + nm) * din * sizeof(T));
     const int64_t g0 = one_gemm ? 0 : nc, gn = one_gemm ? nc + nm : nm;
     kbegin(QGNN_K_GEMM_FWD);

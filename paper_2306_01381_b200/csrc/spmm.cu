@@ -379,6 +379,54 @@ __device__ __forceinline__ void ldg256(const float* p, float4& a, float4& b) {
                : "l"(p));
 }
 
+// ---- packed halo rows -------------------------------------------
+// The 8 columns [c0, c0 + 8) of remote slot `slot`, dequantized from its chunk in
+// the exchange arena exactly as K3 (k_dequant_f32) would have stored them:
+// fmaf(code, S, Z), columns >= dim zero (K3 leaves the halo padding zero).
+__device__ __forceinline__ void packed_row8(const PackedHalo& pk, int slot, int c0, float4& a,
+                                            float4& b) {
+  a = b = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int bw = __ldg(pk.bits + slot);
+  const uint8_t* ch = pk.arena + __ldg(pk.off + slot);
+  if (bw == 0) {  // BitMode::kFp: raw fp32 row, padded to 16 bytes
+    const float* f = reinterpret_cast<const float*>(ch);
+    if (c0 < pk.dim) a = __ldg(reinterpret_cast<const float4*>(f + c0));
+    if (c0 + 4 < pk.dim) b = __ldg(reinterpret_cast<const float4*>(f + c0 + 4));
+    return;
+  }
+  const uint4 h = __ldg(reinterpret_cast<const uint4*>(ch));
+  if (static_cast<int>(h.w & 0xffu) != bw || h.z != static_cast<uint32_t>(pk.dim)) {
+    atomicOr(pk.err, kErrDecode);  // chunk disagrees with the index (codec.hpp:90-91)
+    return;
+  }
+  if (pk.env && (h.w >> 8) != __ldg(pk.env + slot)) {
+    atomicOr(pk.err, kErrProtocol);  // misrouted payload / plan-version skew (engine.hpp:530-541)
+    return;
+  }
+  const float sc = __uint_as_float(h.x), zp = __uint_as_float(h.y);
+  const uint8_t* pl = ch + 16;
+  uint32_t code[8];
+  if (bw == 8) {
+    const uint2 q = __ldg(reinterpret_cast<const uint2*>(pl + c0));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) code[i] = (q.x >> (8 * i)) & 0xffu, code[4 + i] = (q.y >> (8 * i)) & 0xffu;
+  } else if (bw == 4) {
+    const uint32_t q = __ldg(reinterpret_cast<const uint32_t*>(pl + (c0 >> 1)));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) code[i] = (q >> (4 * i)) & 0xfu;
+  } else {
+    const uint32_t q = __ldg(reinterpret_cast<const uint16_t*>(pl + (c0 >> 2)));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) code[i] = (q >> (2 * i)) & 0x3u;
+  }
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    v[i] = c0 + i < pk.dim ? fmaf(static_cast<float>(code[i]), sc, zp) : 0.f;
+  a = make_float4(v[0], v[1], v[2], v[3]);
+  b = make_float4(v[4], v[5], v[6], v[7]);
+}
+
 // In-kernel hub reduction (replaces the k_spmm_hubred launch).  A lane group of
 // G lanes has just stored segment u's partial row; after a fence its leader counts
 // the arrival, and the group that brings the last segment of hub h reduces it:
@@ -469,7 +517,39 @@ __device__ __forceinline__ void grp2_gather(float4 (&acc)[2], const float* __res
   }
 }
 
-template <int MINB>
+// grp2_gather with the rows read from the packed arena (lane columns cx..cx+7)
+__device__ __forceinline__ void grp2_gather_pk(float4 (&acc)[2], const PackedHalo& pk, int cx,
+                                               int n, const int32_t* __restrict__ col,
+                                               const float* __restrict__ alpha, int lane, int grp,
+                                               int E, bool act) {
+  for (int e0 = 0; e0 < n; e0 += 32) {
+    const int cnt = min(32, n - e0);
+    int my_c = 0;
+    float my_a = 0.f;
+    if (lane < cnt) {
+      my_c = __ldg(col + e0 + lane);
+      my_a = __ldg(alpha + e0 + lane);
+    }
+    for (int j = 0; j < cnt; j += 4 * E) {
+      float4 v[4][2];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = j + u * E + grp;
+        const int c = __shfl_sync(0xffffffffu, my_c, k & 31);
+        v[u][0] = v[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (act && k < cnt) packed_row8(pk, c, cx, v[u][0], v[u][1]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float a = __shfl_sync(0xffffffffu, my_a, (j + u * E + grp) & 31);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) fma4(acc[h], a, v[u][h]);
+      }
+    }
+  }
+}
+
+template <int MINB, bool PK = false>
 __global__ void __launch_bounds__(256, MINB) k_spmm_f32g2(
     int dim, const float* __restrict__ x, int64_t ldx, const float* __restrict__ y, int64_t ldy,
     const float* __restrict__ self_alpha, const int64_t* __restrict__ pa,
@@ -478,7 +558,8 @@ __global__ void __launch_bounds__(256, MINB) k_spmm_f32g2(
     float* __restrict__ out, int64_t ldo, int64_t hub_deg, const float* __restrict__ mask,
     int64_t ldm, const int64_t* __restrict__ seg, int64_t n_segs, float* __restrict__ part,
     int64_t ldp, const int32_t* __restrict__ hubs, const int32_t* __restrict__ seg_ptr,
-    const int32_t* __restrict__ seg_hub, int32_t* __restrict__ cnt, bool v8) {
+    const int32_t* __restrict__ seg_hub, int32_t* __restrict__ cnt, bool v8,
+    PackedHalo pk = PackedHalo{}) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int F = dim >> 2, G = (F + 1) >> 1, E = 32 / G;
   const int grp = lane / G, sub = lane - grp * G;
@@ -503,7 +584,10 @@ __global__ void __launch_bounds__(256, MINB) k_spmm_f32g2(
   grp2_gather(acc, x + cx, int(ldx), na, ca + ea0, aa + ea0, lane, grp, E, act, has2, v8);
   if (nb) {  // b range start re-read here rather than held across the first gather
     const int64_t eb0 = is_seg ? seg[4 * w + 2] : pb[r];
-    grp2_gather(acc, y + cx, int(ldy), nb, cb + eb0, ab + eb0, lane, grp, E, act, has2, v8);
+    if constexpr (PK)
+      grp2_gather_pk(acc, pk, cx, nb, cb + eb0, ab + eb0, lane, grp, E, act);
+    else
+      grp2_gather(acc, y + cx, int(ldy), nb, cb + eb0, ab + eb0, lane, grp, E, act, has2, v8);
   }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -700,7 +784,37 @@ __device__ __forceinline__ void wide_gather(float4 (&acc)[2], const float* __res
   }
 }
 
-template <int MINB, bool V8>
+// wide_gather with the rows read from the packed arena (lane columns 8 lane .. +7)
+__device__ __forceinline__ void wide_gather_pk(float4 (&acc)[2], const PackedHalo& pk, int n,
+                                               const int32_t* __restrict__ col,
+                                               const float* __restrict__ alpha, int lane) {
+  for (int e0 = 0; e0 < n; e0 += 32) {
+    const int cnt = min(32, n - e0);
+    int my_c = 0;
+    float my_a = 0.f;
+    if (lane < cnt) {
+      my_c = __ldg(col + e0 + lane);
+      my_a = __ldg(alpha + e0 + lane);
+    }
+    for (int j = 0; j < cnt; j += 4) {
+      float4 v[4][2];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = __shfl_sync(0xffffffffu, my_c, (j + u) & 31);
+        v[u][0] = v[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j + u < cnt) packed_row8(pk, c, 8 * lane, v[u][0], v[u][1]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float a = __shfl_sync(0xffffffffu, my_a, (j + u) & 31);
+        fma4(acc[0], a, v[u][0]);
+        fma4(acc[1], a, v[u][1]);
+      }
+    }
+  }
+}
+
+template <int MINB, bool V8, bool PK = false>
 __global__ void __launch_bounds__(64, MINB) k_spmm_wide(
     const float* __restrict__ x, int64_t ldx, const float* __restrict__ y, int64_t ldy,
     const float* __restrict__ self_alpha, const int64_t* __restrict__ pa,
@@ -709,7 +823,8 @@ __global__ void __launch_bounds__(64, MINB) k_spmm_wide(
     float* __restrict__ out, int64_t ldo, int64_t hub_deg, const float* __restrict__ mask,
     int64_t ldm, const int64_t* __restrict__ seg, int64_t n_segs, float* __restrict__ part,
     int64_t ldp, const int32_t* __restrict__ hubs, const int32_t* __restrict__ seg_ptr,
-    const int32_t* __restrict__ seg_hub, int32_t* __restrict__ cnt) {
+    const int32_t* __restrict__ seg_hub, int32_t* __restrict__ cnt, PackedHalo pk = PackedHalo{}) {
+  static_assert(!PK || V8, "packed rows use the 8-columns-per-lane layout");
   // warps [0, n_segs) reduce hub segments into `part` (k_spmm_hubred finishes those
   // rows); they take the lowest block ids so the long lists start first and overlap
   // the ordinary rows instead of running as a separate tail launch
@@ -731,7 +846,10 @@ __global__ void __launch_bounds__(64, MINB) k_spmm_wide(
   wide_gather<V8>(acc, x, int(ldx), na, ca + ea, aa + ea, lane);
   if (nb) {  // b range start re-read here rather than held across the first gather
     const int64_t eb = is_seg ? seg[4 * w + 2] : pb[r];
-    wide_gather<V8>(acc, y, int(ldy), nb, cb + eb, ab + eb, lane);
+    if constexpr (PK)
+      wide_gather_pk(acc, pk, nb, cb + eb, ab + eb, lane);
+    else
+      wide_gather<V8>(acc, y, int(ldy), nb, cb + eb, ab + eb, lane);
   }
   if (is_seg) {
     float* dst = part + w * ldp;
@@ -787,13 +905,39 @@ __device__ __forceinline__ void half_gather(float4 (&acc)[4], const float* __res
   }
 }
 
+__device__ __forceinline__ void half_gather_pk(float4 (&acc)[4], const PackedHalo& pk, int n,
+                                               const int32_t* __restrict__ col,
+                                               const float* __restrict__ alpha, int c0) {
+  for (int e = 0; e < n; e += 2) {
+    float4 v[2][4];
+    float a[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      a[u] = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[u][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e + u < n) {
+        const int c = __ldg(col + e + u);
+        a[u] = __ldg(alpha + e + u);
+        packed_row8(pk, c, c0, v[u][0], v[u][1]);
+        packed_row8(pk, c, c0 + 8, v[u][2], v[u][3]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) fma4(acc[q], a[u], v[u][q]);
+  }
+}
+
+template <bool PK = false>
 __global__ void __launch_bounds__(64, 16) k_spmm_wide_half(
     const float* __restrict__ x, int64_t ldx, const float* __restrict__ y, int64_t ldy,
     const float* __restrict__ self_alpha, const int64_t* __restrict__ pa,
     const int32_t* __restrict__ ca, const float* __restrict__ aa, const int64_t* __restrict__ pb,
     const int32_t* __restrict__ cb, const float* __restrict__ ab, int64_t r0, int64_t n_rows,
     float* __restrict__ out, int64_t ldo, int64_t hub_deg, const float* __restrict__ mask,
-    int64_t ldm) {
+    int64_t ldm, PackedHalo pk = PackedHalo{}) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int hl = lane & 15;
   const int64_t r = r0 + (int64_t(blockIdx.x) * (blockDim.x >> 5) + warp) * 2 + (lane >> 4);
@@ -808,7 +952,10 @@ __global__ void __launch_bounds__(64, 16) k_spmm_wide_half(
   half_gather(acc, x, int(ldx), na, ca + ea, aa + ea, c0);
   if (nb) {
     const int64_t eb = pb[r];
-    half_gather(acc, y, int(ldy), nb, cb + eb, ab + eb, c0);
+    if constexpr (PK)
+      half_gather_pk(acc, pk, nb, cb + eb, ab + eb, c0);
+    else
+      half_gather(acc, y, int(ldy), nb, cb + eb, ab + eb, c0);
   }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -981,12 +1128,23 @@ static bool grouped_narrow() {  // QGNN_SPMM_GROUPED=0 selects the one-row-per-w
 }
 
 // fp32 row-range SpMM with optional hub list (rows with > hub_deg neighbours).
+bool spmm_packed_ok(int dim, const HubPlan* hp, const float* x, int64_t ldx) {
+  if (hp && hp->order && dim <= sorted_max_dim() && dim / 4 >= 7 && sorted_rows()) return false;
+  if (hp && hp->n_hubs > 0 && !merge_hubs()) return false;
+  const int nv = int(ceil_div(dim / 4, 32));
+  if (nv == 1) return grouped_narrow() && dim / 4 >= 5 && two_per_lane();
+  const bool v8 = load256() && (reinterpret_cast<uintptr_t>(x) & 31) == 0 && ldx % 8 == 0;
+  return dim == 256 && wide_lean() && split_wide() == 0 && v8;
+}
+
 int spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y, int64_t ldy,
               const float* sa, const int64_t* pa, const int32_t* ca, const float* aa,
               const int64_t* pb, const int32_t* cb, const float* ab, int64_t row_begin,
               int64_t n_rows, float* out, int64_t ldo, const HubPlan* hp, cudaStream_t s,
-              const float* mask, int64_t ldm) {
+              const float* mask, int64_t ldm, const PackedHalo* pk) {
   if (n_rows <= 0) return 0;
+  if (pk && !spmm_packed_ok(dim, hp, x, ldx))
+    throw Status(QGNN_EINVAL, "spmm_f32: no packed-halo kernel for this row range");
   const int nv = int(ceil_div(dim / 4, 32));
   const int64_t blocks = ceil_div(n_rows, 8);
   const bool hubs = hp && hp->n_hubs > 0;
@@ -1045,7 +1203,12 @@ int spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y
       const int32_t* hsh = hubs ? hp->seg_hub : nullptr;
       const bool v8 = load256() && (reinterpret_cast<uintptr_t>(x) & 31) == 0 && ldx % 8 == 0 &&
                       (!y || ((reinterpret_cast<uintptr_t>(y) & 31) == 0 && ldy % 8 == 0));
-      if (g2_minb() == 3)
+      if (pk)
+        k_spmm_f32g2<4, true><<<nb2, spmm_tpb(), 0, s>>>(
+            dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask,
+            ldm, hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0, hh,
+            hsp, hsh, cnt, v8, *pk);
+      else if (g2_minb() == 3)
         k_spmm_f32g2<3><<<nb2, spmm_tpb(), 0, s>>>(
             dim, x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask,
             ldm, hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0, hh,
@@ -1091,9 +1254,18 @@ int spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y
                     (!y || ((reinterpret_cast<uintptr_t>(y) & 31) == 0 && ldy % 8 == 0));
     if (v8 && hp && hp->avg_deg < half_rows_deg()) {
       // low-degree rows: two per warp; hub segments (if any) through k_spmm_wide
-      k_spmm_wide_half<<<unsigned(ceil_div(n_rows, 4)), 64, 0, s>>>(
-          x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask, ldm);
-      if (ns)
+      if (pk)
+        k_spmm_wide_half<true><<<unsigned(ceil_div(n_rows, 4)), 64, 0, s>>>(
+            x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask, ldm,
+            *pk);
+      else
+        k_spmm_wide_half<<<unsigned(ceil_div(n_rows, 4)), 64, 0, s>>>(
+            x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask, ldm);
+      if (ns && pk)
+        k_spmm_wide<16, true, true><<<unsigned(ceil_div(ns, 2)), 64, 0, s>>>(
+            x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, 0, out, ldo, hd, mask, ldm,
+            hp->seg, ns, hp->part, hp->ldp, hp->hubs, hp->seg_ptr, hp->seg_hub, cnt, *pk);
+      else if (ns)
         k_spmm_wide<16, true><<<unsigned(ceil_div(ns, 2)), 64, 0, s>>>(
             x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, 0, out, ldo, hd, mask, ldm,
             hp->seg, ns, hp->part, hp->ldp, hp->hubs, hp->seg_ptr, hp->seg_hub, cnt);
@@ -1104,7 +1276,13 @@ int spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y
       check_launch("k_spmm_wide_half");
       return 1 + (ns ? 1 : 0) + (hubs && !cnt ? 1 : 0);
     }
-    if (v8)
+    if (pk)
+      k_spmm_wide<16, true, true><<<unsigned(ceil_div(ns + n_rows, 2)), 64, 0, s>>>(
+          x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask, ldm,
+          hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0,
+          hubs ? hp->hubs : nullptr, hubs ? hp->seg_ptr : nullptr, hubs ? hp->seg_hub : nullptr,
+          cnt, *pk);
+    else if (v8)
       k_spmm_wide<16, true><<<unsigned(ceil_div(ns + n_rows, 2)), 64, 0, s>>>(
           x, ldx, y, ldy, sa, pa, ca, aa, pb, cb, ab, row_begin, n_rows, out, ldo, hd, mask, ldm,
           hubs ? hp->seg : nullptr, ns, hubs ? hp->part : nullptr, hubs ? hp->ldp : 0,
