@@ -385,16 +385,30 @@ __device__ __forceinline__ void ldg256(const float* p, float4& a, float4& b) {
 // fmaf(code, S, Z), columns >= dim zero (K3 leaves the halo padding zero).
 __device__ __forceinline__ void packed_row8(const PackedHalo& pk, int slot, int c0, float4& a,
                                             float4& b) {
-  a = b = make_float4(0.f, 0.f, 0.f, 0.f);
+  // off / width first (independent), then header and payload together: two
+  // dependent round trips, like slot -> row for an fp32 halo row plus one
   const int bw = __ldg(pk.bits + slot);
   const uint8_t* ch = pk.arena + __ldg(pk.off + slot);
-  if (bw == 0) {  // BitMode::kFp: raw fp32 row, padded to 16 bytes
+  const uint8_t* pl = ch + 16;
+  uint2 q = make_uint2(0u, 0u);
+  float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra;
+  uint4 h = make_uint4(0u, 0u, 0u, 0u);
+  if (bw == 0) {  // BitMode::kFp: raw fp32 row (no header), padded to 16 bytes
     const float* f = reinterpret_cast<const float*>(ch);
-    if (c0 < pk.dim) a = __ldg(reinterpret_cast<const float4*>(f + c0));
-    if (c0 + 4 < pk.dim) b = __ldg(reinterpret_cast<const float4*>(f + c0 + 4));
-    return;
+    if (c0 < pk.dim) ra = __ldg(reinterpret_cast<const float4*>(f + c0));
+    if (c0 + 4 < pk.dim) rb = __ldg(reinterpret_cast<const float4*>(f + c0 + 4));
+  } else {
+    h = __ldg(reinterpret_cast<const uint4*>(ch));
+    if (bw == 8)
+      q = __ldg(reinterpret_cast<const uint2*>(pl + c0));
+    else if (bw == 4)
+      q.x = __ldg(reinterpret_cast<const uint32_t*>(pl + (c0 >> 1)));
+    else
+      q.x = __ldg(reinterpret_cast<const uint16_t*>(pl + (c0 >> 2)));
   }
-  const uint4 h = __ldg(reinterpret_cast<const uint4*>(ch));
+  a = ra, b = rb;
+  if (bw == 0) return;
+  a = b = make_float4(0.f, 0.f, 0.f, 0.f);
   if (static_cast<int>(h.w & 0xffu) != bw || h.z != static_cast<uint32_t>(pk.dim)) {
     atomicOr(pk.err, kErrDecode);  // chunk disagrees with the index (codec.hpp:90-91)
     return;
@@ -404,25 +418,15 @@ __device__ __forceinline__ void packed_row8(const PackedHalo& pk, int slot, int 
     return;
   }
   const float sc = __uint_as_float(h.x), zp = __uint_as_float(h.y);
-  const uint8_t* pl = ch + 16;
-  uint32_t code[8];
-  if (bw == 8) {
-    const uint2 q = __ldg(reinterpret_cast<const uint2*>(pl + c0));
-#pragma unroll
-    for (int i = 0; i < 4; ++i) code[i] = (q.x >> (8 * i)) & 0xffu, code[4 + i] = (q.y >> (8 * i)) & 0xffu;
-  } else if (bw == 4) {
-    const uint32_t q = __ldg(reinterpret_cast<const uint32_t*>(pl + (c0 >> 1)));
-#pragma unroll
-    for (int i = 0; i < 8; ++i) code[i] = (q >> (4 * i)) & 0xfu;
-  } else {
-    const uint32_t q = __ldg(reinterpret_cast<const uint16_t*>(pl + (c0 >> 2)));
-#pragma unroll
-    for (int i = 0; i < 8; ++i) code[i] = (q >> (2 * i)) & 0x3u;
-  }
+  const int sh = bw == 8 ? 8 : bw;  // bits per code
+  const uint32_t m = (1u << sh) - 1u;
   float v[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-    v[i] = c0 + i < pk.dim ? fmaf(static_cast<float>(code[i]), sc, zp) : 0.f;
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t code = bw == 8 ? ((i < 4 ? q.x : q.y) >> (8 * (i & 3))) & 0xffu
+                                  : (q.x >> (sh * i)) & m;
+    v[i] = c0 + i < pk.dim ? fmaf(static_cast<float>(code), sc, zp) : 0.f;
+  }
   a = make_float4(v[0], v[1], v[2], v[3]);
   b = make_float4(v[4], v[5], v[6], v[7]);
 }
