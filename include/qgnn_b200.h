@@ -318,6 +318,10 @@ typedef struct {
   int32_t transport;       /* world == 1 only: 0 zero copy between the partitions of the
                               GPU (default); 1 every pair through NCCL self send/receive
                               (the multi-GPU exchange path, run and timed on one device) */
+  int32_t layer_norm;      /* TrainSettings::layer_norm (engine.hpp:42): LN after every
+                              layer's transform (model.hpp:62-73, 108-112) */
+  double dropout;          /* TrainSettings::dropout (engine.hpp:43): inverted dropout on
+                              the hidden layers' outputs (model.hpp:114-119) */
 } qgnn_settings;
 
 typedef struct {

@@ -281,7 +281,8 @@ class _Ref:
         L.ref_engine_run.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                      C.c_double, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                      C.c_uint64, C.c_int, C.c_double, C.c_double, C.c_double,
-                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                     C.c_double]
 
     def _chk(self, st):
         if st:
@@ -457,7 +458,7 @@ class _Ref:
     # engine -----------------------------------------------------------------
     def engine_run(self, g, dims, n_parts, bit_mode=1, fixed_bits=8, epochs=3, seed=7,
                    sage=False, lam=0.5, group_size=4, period=50, threads=False, theta=3e-9,
-                   gamma=5e-5, lr=0.01, owner=None, times=None):
+                   gamma=5e-5, lr=0.01, owner=None, times=None, layer_norm=False, dropout=0.0):
         """Reference Engine::run.  owner: planted owner map -> the Engine
         partitions with partitions_from_owner (else partition_graph, BFS).
         times: optional float64[2] <- (setup seconds, run seconds)."""
@@ -476,7 +477,7 @@ class _Ref:
                                             int(fixed_bits), lam, group_size, period, epochs,
                                             seed, n_parts, int(threads), theta, gamma, lr,
                                             _p(ep), _p(fw),
-                                            _p(own), _p(times)))
+                                            _p(own), _p(times), int(layer_norm), float(dropout)))
             return ep, fw
         finally:
             self.L.ref_dataset_free(h)

@@ -492,12 +492,12 @@ int ref_solve_instance(uint64_t n_pairs, const uint32_t* pair_src, const uint32_
 // owner != NULL: partitions_from_owner(g, owner) instead of partition_graph
 // (see shim_hook above).  times_out (optional, 2 doubles): Engine
 // construction seconds and run() seconds (epoch_out[.., 9] = run() / epochs,
-// setup excluded).
+// setup excluded).  layer_norm / dropout: TrainSettings::layer_norm / dropout.
 int ref_engine_run(void* dataset, const uint64_t* dims, int n_dims, int sage, int bit_mode,
                    int fixed_bits, double lambda, uint64_t group_size, uint64_t period,
                    uint64_t epochs, uint64_t seed, uint64_t n_parts, int threads, double theta,
                    double gamma, double lr, double* epoch_out, double* final_weights,
-                   const uint32_t* owner, double* times_out) {
+                   const uint32_t* owner, double* times_out, int layer_norm, double dropout) {
   GUARD({
     const Graph& g = static_cast<RefDataset*>(dataset)->g;
     TrainSettings s;
@@ -515,6 +515,8 @@ int ref_engine_run(void* dataset, const uint64_t* dims, int n_dims, int sage, in
     s.n_parts = n_parts;
     s.exec = threads ? ExecMode::kThreads : ExecMode::kRoundRobin;
     s.cost = CostModel::uniform(n_parts, theta, gamma);
+    s.layer_norm = layer_norm != 0;  // TrainSettings (engine.hpp:42-43)
+    s.dropout = dropout;
     std::vector<uint32_t> own;
     if (owner) own.assign(owner, owner + g.num_nodes);
     const auto ts = std::chrono::steady_clock::now();

@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libqgnn_b200.so")
+# QGNN_LIB: an alternative build of the same library (A/B experiments only)
+LIB_PATH = os.environ.get("QGNN_LIB") or os.path.join(_HERE, "_lib", "libqgnn_b200.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "qgnn_b200.h")
 
 OK, EINVAL, EDECODE, EPROTOCOL, ERESOURCE, EDIVERGED, EIO, ECUDA, ENCCL = range(9)
@@ -67,7 +68,8 @@ class Settings(C.Structure):
                 ("n_parts", C.c_int64), ("lr", C.c_double), ("theta", C.c_double),
                 ("gamma", C.c_double), ("dtype", C.c_int32), ("layout", C.c_int32),
                 ("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32),
-                ("overlap", C.c_int32), ("kstats", C.c_int32), ("transport", C.c_int32)]
+                ("overlap", C.c_int32), ("kstats", C.c_int32), ("transport", C.c_int32),
+                ("layer_norm", C.c_int32), ("dropout", C.c_double)]
 
 
 class EpochMetrics(C.Structure):

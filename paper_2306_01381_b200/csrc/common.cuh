@@ -137,6 +137,24 @@ struct HubPlan {
   int32_t* cnt = nullptr;            // [n_hubs] arrivals; zero between launches
   double avg_deg = 0;                // mean (a + b) degree of the range's rows
 };
+// Per-row activation chain with LayerNorm / dropout (chain.cu; model.hpp:62-153)
+struct ChainArgs {
+  int ln = 0;                 // layer_norm
+  int relu = 0;               // Activation::kRelu
+  double keep = 1.0;          // 1 - dropout (1: no dropout on this layer)
+  uint64_t keep_thr = 0;      // ceil(keep * 2^53): draw >> 11 below it keeps the element
+  const uint64_t* drop_key = nullptr;  // [dev] RngStream key of fork({0x4, epoch, l, device})
+  const int32_t* ref_row = nullptr;    // GPU row -> reference owned-row index
+};
+
+template <typename T>
+void chain_forward(const T* z, T* act, int64_t ld, T* h, int64_t ldh, T* inv_std, int dout,
+                   int64_t r0, int64_t n, const ChainArgs& c, cudaStream_t s);
+template <typename T>
+void chain_backward(const T* dh, int64_t lddh, const T* act, int64_t ld, const T* h, int64_t ldh,
+                    const T* inv_std, T* dz, int64_t lddz, int dout, int64_t r0, int64_t n,
+                    const ChainArgs& c, cudaStream_t s);
+
 // Forward halo rows read straight from the exchange arena:
 // remote slot s is message s of the receive list, its chunk at arena + off[s]
 // with width bits[s]; the marginal SpMM dequantizes the 8 columns a lane needs

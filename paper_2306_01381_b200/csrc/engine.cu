@@ -355,6 +355,8 @@ class Engine final : public EngineBase {
     DBuf<int32_t> lcol, rslot, srow;
     DBuf<T> lafwd, labwd, ralpha, salpha, self_alpha;
     DBuf<int32_t> labels, train_rows, val_rows, test_rows, loss_rows, ref_order;
+    DBuf<int32_t> ref_row;            // GPU row -> reference row (dropout coordinates)
+    std::vector<DBuf<T>> act, istd;   // chain: act_in (y or z) and LN inv_std per layer
     int64_t n_train = 0, n_val = 0, n_test = 0;
     // activations
     std::vector<DBuf<T>> h, hagg;  // h[0..L], hagg[0..L-1]
@@ -470,7 +472,27 @@ class Engine final : public EngineBase {
   void backward_last_tf(int l);
   bool tf_last_ = false;  // last layer aggregates after the transform (fp32, dout < din)
   // fp32 + GPU wire layout: ReLU backward folded into the producers of dh (masked by h)
-  bool relu_fused() const { return sizeof(T) == 4 && s_.layout == QGNN_WIRE_GPU; }
+  bool relu_fused() const { return sizeof(T) == 4 && s_.layout == QGNN_WIRE_GPU && !chain_; }
+  // LayerNorm / dropout (TrainSettings::layer_norm, dropout; model.hpp:62-153): the
+  // transform writes act[t], chain.cu turns it into h[l] and back-propagates
+  bool chain_ = false;
+  bool chain_layer(int64_t l) const {  // layer l (1-based) runs the explicit chain
+    return chain_ && (s_.layer_norm || l < L_);
+  }
+  ChainArgs chain_args(const PartDev& D, int64_t l) const {
+    ChainArgs c;
+    c.ln = s_.layer_norm;
+    c.relu = l < L_ ? 1 : 0;
+    if (s_.dropout > 0.0 && l < L_) {
+      c.keep = 1.0 - s_.dropout;
+      c.keep_thr = uint64_t(std::ceil(std::ldexp(c.keep, 53)));
+      c.drop_key = drop_keys_.p + (D.id - p0_) * L_ + l;
+      c.ref_row = D.ref_row.p;
+    }
+    return c;
+  }
+  DBuf<uint64_t> drop_keys_;        // [local parts][L + 1] fork({0x4, epoch, l, device}) keys
+  uint64_t* drop_keys_host_ = nullptr;
   bool dh_masked_ = false;  // dh already carries the ReLU-backward mask of its layer
   int gemm_nk() const {  // kernels of the last dense_forward / input_grad call
     return (sizeof(T) == 4 && use_tc_gemm()) ? std::max(1, ctx_->last_gemm_launches) : 1;
@@ -674,6 +696,8 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
   tf_last_ = sizeof(T) == 4 && L_ >= 2 && s.dims[L_] < s.dims[L_ - 1];
   if (const char* e = std::getenv("QGNN_TF_LAST")) tf_last_ = tf_last_ && std::atoi(e) != 0;
   if (const char* e = std::getenv("QGNN_HUB_DEG")) kHubDeg = std::max<int64_t>(1, std::atoll(e));
+  QGNN_REQUIRE(s.dropout >= 0.0 && s.dropout < 1.0, QGNN_EINVAL, "engine: dropout must be in [0, 1)");
+  chain_ = s.layer_norm != 0 || s.dropout > 0.0;
   dims_.assign(s.dims, s.dims + s.n_dims);
   p0_ = s.rank * (P_ / s.world);
   p1_ = p0_ + P_ / s.world;
@@ -850,6 +874,16 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
     D.dz.alloc(no * maxd);
     D.gbar.alloc(no * maxd);
     if (tf_last_) D.gpart.alloc(std::max<int64_t>(1, nr) * ld_of(dims_[L_]));
+    if (chain_) {  // act_in per layer (+ inv_std with LN), GPU -> reference rows for dropout
+      D.act.resize(L_);
+      D.istd.resize(L_);
+      for (int64_t t = 0; t < L_; ++t) {
+        if (!chain_layer(t + 1)) continue;
+        D.act[t].alloc(no * ld_of(dims_[t + 1]));
+        if (s_.layer_norm) D.istd[t].alloc(std::max<int64_t>(1, no));
+      }
+      if (s_.dropout > 0.0) D.ref_row.upload(V.ref_row);
+    }
     D.loss.alloc(1);
     D.correct.alloc(2);
     D.ce_terms.alloc(std::max<int64_t>(1, D.n_train));
@@ -971,6 +1005,7 @@ void Engine<T>::negotiate_sizes() {
 template <typename T>
 Engine<T>::~Engine() {
   cudaDeviceSynchronize();
+  if (drop_keys_host_) cudaFreeHost(drop_keys_host_);
   parts_dev_.clear();
   for (auto& e : ev_pool_) {
     cudaEventDestroy(e.first);
@@ -1572,6 +1607,22 @@ void Engine<T>::forward_layer(int l) {
   // partition's transform runs once over central + marginal rows (contiguous in
   // hagg) after its marginal aggregation: one GEMM launch instead of two.
   const bool one_gemm = zero_copy() && !side_overlap() && merge_gemm_enabled();
+  // layer_forward_rows (model.hpp:90-124) for rows [r0, r0 + n): the GEMM with the
+  // ReLU epilogue, or (LayerNorm / dropout) z -> act[t], then the chain -> h[l]
+  const bool chain = chain_layer(l);
+  auto transform = [&](PartDev& D, int64_t r0, int64_t n) {
+    kbegin(QGNN_K_GEMM_FWD);
+    QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
+                                 nullptr, r0, n, chain ? 0 : relu,
+                                 chain ? D.act[t].p : D.h[l].p, ldo, s_main_));
+    kend(QGNN_K_GEMM_FWD, double(n) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+    if (!chain) return;
+    kbegin(QGNN_K_ELEMWISE);
+    chain_forward<T>(D.act[t].p, D.act[t].p, ldo, D.h[l].p, ldo,
+                     s_.layer_norm ? D.istd[t].p : nullptr, int(dout), r0, n, chain_args(D, l),
+                     s_main_);
+    kend(QGNN_K_ELEMWISE, double(n) * dout * sizeof(T) * 3, s_main_);
+  };
   // central rows (engine.hpp:598-605): during the exchange
   auto central = [&](PartDev& D) {
     const int64_t nc = D.view.n_central;
@@ -1584,10 +1635,7 @@ void Engine<T>::forward_layer(int l) {
                               double(D.view.src_rows_central) * din * sizeof(T), s_main_, nk,
          (nnz + nc) * din * sizeof(T));
     if (one_gemm) return;
-    kbegin(QGNN_K_GEMM_FWD);
-    QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
-                                 nullptr, 0, nc, relu, D.h[l].p, ldo, s_main_));
-    kend(QGNN_K_GEMM_FWD, double(nc) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+    transform(D, 0, nc);
   };
   // With features still in flight (first layer after set_features) or with no
   // remote exchange (one GPU), each partition's encode and central rows run as
@@ -1626,12 +1674,7 @@ void Engine<T>::forward_layer(int l) {
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
     const int64_t nc = D.view.n_central, nm = D.view.n_marginal;
-    if (one_gemm && !nm && nc) {  // all rows central: their deferred transform
-      kbegin(QGNN_K_GEMM_FWD);
-      QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
-                                   nullptr, 0, nc, relu, D.h[l].p, ldo, s_main_));
-      kend(QGNN_K_GEMM_FWD, double(nc) * (din + dout) * sizeof(T), s_main_, gemm_nk());
-    }
+    if (one_gemm && !nm && nc) transform(D, 0, nc);  // all rows central: deferred transform
     if (!nm) continue;
     kbegin(QGNN_K_SPMM_FWD);
     const PackedHalo pk = pkd ? packed_halo(D, k, din) : PackedHalo{};
@@ -1653,10 +1696,7 @@ void Engine<T>::forward_layer(int l) {
                               double(D.view.src_slots_marginal) * slot_bytes, s_main_, nk,
          (nnz + nm) * din * sizeof(T));
     const int64_t g0 = one_gemm ? 0 : nc, gn = one_gemm ? nc + nm : nm;
-    kbegin(QGNN_K_GEMM_FWD);
-    QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
-                                 nullptr, g0, gn, relu, D.h[l].p, ldo, s_main_));
-    kend(QGNN_K_GEMM_FWD, double(gn) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+    transform(D, g0, gn);
   }
 }
 
@@ -1701,13 +1741,25 @@ void Engine<T>::backward_layer(int l) {
   // and this layer's producers of dh_next are masked by h[t] (relu_mask4)
   const bool relu = l < L_ && !dh_masked_;
   const bool mk = relu_fused() && t >= 1;
+  // LayerNorm / dropout: layer_backward_rows as chain.cu (dz from dh, act_in, h, inv_std)
+  const bool chain = chain_layer(l);
+  auto chain_bwd = [&](PartDev& D, int64_t r0, int64_t n) {
+    kbegin(QGNN_K_ELEMWISE);
+    chain_backward<T>(D.dh.p, ldo, D.act[t].p, ldo, D.h[l].p, ldo,
+                      s_.layer_norm ? D.istd[t].p : nullptr, D.dz.p, ldo, int(dout), r0, n,
+                      chain_args(D, l), s_main_);
+    kend(QGNN_K_ELEMWISE, double(n) * dout * sizeof(T) * 4, s_main_);
+  };
   const T* W = w_.p + woff_[t];
   // bwd_send (engine.hpp:661-688): marginal chain, remote partials, encode
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
     const int64_t nc = D.view.n_central, nm = D.view.n_marginal;
     const T* dz = D.dh.p;
-    if (relu) {
+    if (chain) {
+      chain_bwd(D, nc, nm);
+      dz = D.dz.p;
+    } else if (relu) {
       kbegin(QGNN_K_ELEMWISE);
       QGNN_CALL(qgnn_relu_backward(ctx_, dtype_, D.h[l].p, ldo, D.dh.p, ldo, dout, nc, nm, D.dz.p,
                                    ldo, s_main_));
@@ -1741,7 +1793,10 @@ void Engine<T>::backward_layer(int l) {
     PartDev& D = *up;
     const int64_t nc = D.view.n_central, no = D.view.num_owned;
     const T* dz = D.dh.p;
-    if (relu) {
+    if (chain) {
+      chain_bwd(D, 0, nc);
+      dz = D.dz.p;
+    } else if (relu) {
       kbegin(QGNN_K_ELEMWISE);
       QGNN_CALL(qgnn_relu_backward(ctx_, dtype_, D.h[l].p, ldo, D.dh.p, ldo, dout, 0, nc, D.dz.p,
                                    ldo, s_main_));
@@ -1791,6 +1846,9 @@ void Engine<T>::forward_last_tf(int l) {
   const int64_t ldi = ld_of(din), ldo = ld_of(dout);
   const T* W = w_.p + woff_[t];
   const bool side = side_overlap();
+  // LayerNorm on the last layer: the aggregation lands in act[t] = z, the chain
+  // writes h[l] = LN(z) (model.hpp:108-112; linear, no dropout on the last layer)
+  const bool chain = chain_layer(l);
   if (side) {  // one GPU: encode + decode on the side stream during the owned-row work
     fork_side();
     for (auto& up : parts_dev_) quantize(*up, k, up->h[t].p, ldi, s_comm_);
@@ -1809,7 +1867,8 @@ void Engine<T>::forward_last_tf(int l) {
     if (!nc) continue;
     kbegin(QGNN_K_SPMM_FWD);
     const int nk = spmm(dout, D.dz.p, ldo, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
-                        D.lafwd.p, nullptr, nullptr, nullptr, 0, nc, D.h[l].p, ldo, &D.hub_fc.plan);
+                        D.lafwd.p, nullptr, nullptr, nullptr, 0, nc,
+                        chain ? D.act[t].p : D.h[l].p, ldo, &D.hub_fc.plan);
     kend(QGNN_K_SPMM_FWD, nc * (16.0 + dout * sizeof(T)) +
                               double(D.view.local_ptr[nc]) * (4 + sizeof(T)) +
                               double(D.view.src_rows_central) * dout * sizeof(T), s_main_, nk,
@@ -1833,8 +1892,8 @@ void Engine<T>::forward_last_tf(int l) {
     }
     kbegin(QGNN_K_SPMM_FWD);
     const int nk = spmm(dout, D.dz.p, ldo, D.partials.p, ldo, D.self_alpha.p, D.lptr.p, D.lcol.p,
-                        D.lafwd.p, D.rptr.p, D.rslot.p, D.ralpha.p, nc, nm, D.h[l].p, ldo,
-                        &D.hub_fm.plan);
+                        D.lafwd.p, D.rptr.p, D.rslot.p, D.ralpha.p, nc, nm,
+                        chain ? D.act[t].p : D.h[l].p, ldo, &D.hub_fm.plan);
     const double nnz = double(D.view.local_ptr[nc + nm] - D.view.local_ptr[nc]) +
                        double(D.view.remote_nnz());
     kend(QGNN_K_SPMM_FWD, nm * (24.0 + dout * sizeof(T)) + nnz * (4 + sizeof(T)) +
@@ -1842,6 +1901,14 @@ void Engine<T>::forward_last_tf(int l) {
                                   dout * sizeof(T), s_main_, nk,
          (nnz + nm) * dout * sizeof(T));
   }
+  if (chain)
+    for (auto& up : parts_dev_) {
+      PartDev& D = *up;
+      kbegin(QGNN_K_ELEMWISE);
+      chain_forward<T>(D.act[t].p, D.act[t].p, ldo, D.h[l].p, ldo, D.istd[t].p, int(dout), 0,
+                       D.view.num_owned, chain_args(D, l), s_main_);
+      kend(QGNN_K_ELEMWISE, double(D.view.num_owned) * dout * sizeof(T) * 3, s_main_);
+    }
 }
 
 // Backward of the transform-first last layer: g = A^T dz (dout-wide), then
@@ -1855,13 +1922,24 @@ void Engine<T>::backward_last_tf(int l) {
   const int64_t ldi = ld_of(din), ldo = ld_of(dout);
   const T* W = w_.p + woff_[t];
   const bool mk = relu_fused() && t >= 1;  // ReLU backward of layer t folded into dh_next's producers
+  // LayerNorm on the last layer: dz = LN'(dh) first (dropout is never on the last layer)
+  const bool chain = chain_layer(l);
+  if (chain)
+    for (auto& up : parts_dev_) {
+      PartDev& D = *up;
+      kbegin(QGNN_K_ELEMWISE);
+      chain_backward<T>(D.dh.p, ldo, D.act[t].p, ldo, D.h[l].p, ldo, D.istd[t].p, D.dz.p, ldo,
+                        int(dout), 0, D.view.num_owned, chain_args(D, l), s_main_);
+      kend(QGNN_K_ELEMWISE, double(D.view.num_owned) * dout * sizeof(T) * 4, s_main_);
+    }
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
     const int64_t nr = D.view.num_remote;
     if (nr) {
       kbegin(QGNN_K_PARTIALS);
-      const int nk = spmm(dout, D.dh.p, ldo, nullptr, 0, nullptr, D.sptr.p, D.srow.p, D.salpha.p,
-                          nullptr, nullptr, nullptr, 0, nr, D.gpart.p, ldo, &D.hub_part.plan);
+      const int nk = spmm(dout, chain ? D.dz.p : D.dh.p, ldo, nullptr, 0, nullptr, D.sptr.p,
+                          D.srow.p, D.salpha.p, nullptr, nullptr, nullptr, 0, nr, D.gpart.p, ldo,
+                          &D.hub_part.plan);
       kend(QGNN_K_PARTIALS, double(nr) * (8 + dout * sizeof(T)) +
                                 double(D.view.remote_nnz()) * (4 + sizeof(T)) +
                                 double(D.view.n_marginal) * dout * sizeof(T),
@@ -1883,8 +1961,9 @@ void Engine<T>::backward_last_tf(int l) {
     PartDev& D = *up;
     const int64_t no = D.view.num_owned, nr = D.view.num_remote;
     kbegin(QGNN_K_SPMM_BWD);
-    const int nk = spmm(dout, D.dh.p, ldo, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
-                        D.labwd.p, nullptr, nullptr, nullptr, 0, no, D.gbar.p, ldo, &D.hub_bwd.plan);
+    const int nk = spmm(dout, chain ? D.dz.p : D.dh.p, ldo, nullptr, 0, D.self_alpha.p, D.lptr.p,
+                        D.lcol.p, D.labwd.p, nullptr, nullptr, nullptr, 0, no, D.gbar.p, ldo,
+                        &D.hub_bwd.plan);
     kend(QGNN_K_SPMM_BWD, no * (16.0 + dout * sizeof(T)) +
                               double(D.view.local_nnz()) * (4 + sizeof(T)) +
                               double(D.view.src_rows_all) * dout * sizeof(T), s_main_, nk,
@@ -1929,7 +2008,14 @@ void Engine<T>::backward_last() {
     PartDev& D = *up;
     const int64_t no = D.view.num_owned;
     const T* dz = D.dh.p;
-    if (relu) {
+    if (chain_layer(1)) {  // LayerNorm / dropout of layer 1 (chain.cu)
+      kbegin(QGNN_K_ELEMWISE);
+      chain_backward<T>(D.dh.p, ldo, D.act[0].p, ldo, D.h[1].p, ldo,
+                        s_.layer_norm ? D.istd[0].p : nullptr, D.dz.p, ldo, int(dout), 0, no,
+                        chain_args(D, 1), s_main_);
+      kend(QGNN_K_ELEMWISE, double(no) * dout * sizeof(T) * 4, s_main_);
+      dz = D.dz.p;
+    } else if (relu) {
       kbegin(QGNN_K_ELEMWISE);
       QGNN_CALL(qgnn_relu_backward(ctx_, dtype_, D.h[1].p, ldo, D.dh.p, ldo, dout, 0, no, D.dz.p,
                                    ldo, s_main_));
@@ -1982,6 +2068,22 @@ void Engine<T>::launch_epoch() {
   adam_bc_host_[1] = 1.0 - std::pow(0.999, double(adam_t_));
   QGNN_CUDA(cudaMemcpyAsync(adam_bc_.p, adam_bc_host_, 2 * sizeof(double), cudaMemcpyHostToDevice,
                             s_main_));
+  if (s_.dropout > 0.0) {  // dropout streams root.fork({0x4, epoch, l, device}) (engine.hpp:600)
+    const int64_t nloc = p1_ - p0_;
+    if (!drop_keys_host_) {
+      QGNN_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&drop_keys_host_),
+                              nloc * L_ * sizeof(uint64_t), cudaHostAllocDefault));
+      drop_keys_.alloc(nloc * L_);
+    }
+    for (int64_t p = p0_; p < p1_; ++p)
+      for (int64_t l = 0; l < L_; ++l) {
+        uint64_t key = root_;
+        for (uint64_t c : {uint64_t(0x4), epoch_, uint64_t(l), uint64_t(p)}) key = rng_fork(key, c);
+        drop_keys_host_[(p - p0_) * L_ + l] = key;
+      }
+    QGNN_CUDA(cudaMemcpyAsync(drop_keys_.p, drop_keys_host_, nloc * L_ * sizeof(uint64_t),
+                              cudaMemcpyHostToDevice, s_main_));
+  }
   QGNN_CUDA(cudaEventRecord(ev_a_, s_main_));
   const bool graph = graphs_enabled() && epoch_ > 1;
   EpochGraph& graph_ = graphs_[feat_pending_ ? 1 : 0];

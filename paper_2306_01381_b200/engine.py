@@ -70,7 +70,7 @@ class Engine:
                  gamma: float = 5e-5, dtype: str = "f32", layout: Optional[int] = None,
                  owner=None, rank: int = 0, world: int = 1, device: int = 0,
                  nccl_id: Optional[bytes] = None, kstats: bool = False, overlap: int = 1,
-                 transport: str = "zero_copy"):
+                 transport: str = "zero_copy", layer_norm: bool = False, dropout: float = 0.0):
         s = _lib.Settings()
         s.sage = int(sage)
         s.n_dims = len(dims)
@@ -92,6 +92,8 @@ class Engine:
         s.overlap = int(overlap)
         s.transport = {"zero_copy": 0, "nccl": 1}[transport]
         s.kstats = int(kstats)
+        s.layer_norm = int(layer_norm)
+        s.dropout = float(dropout)
         self.settings = s
         self.dims = list(dims)
         self.np_dtype = np.float64 if dtype == "f64" else np.float32
