@@ -245,6 +245,18 @@ int qgnn_agg_view_build(const int64_t* adj_ptr, const int32_t* adj, int64_t n,
 int qgnn_agg_view_arrays_get(const qgnn_agg_view* view, qgnn_agg_view_arrays* out);
 int qgnn_agg_view_destroy(qgnn_agg_view* view);
 
+/* GPU-side setup: the same two builders computed on `device`
+ * from a device-resident copy of the graph — per-node consumer sets and every
+ * per-edge pass (local/remote split with the fp64 coefficients, remote-CSR
+ * transpose) run as kernels; outputs are identical to qgnn_partitions_from_owner /
+ * qgnn_agg_view_build (same handles, same accessors, same destroy calls). */
+int qgnn_partitions_from_owner_gpu(const int64_t* adj_ptr, const int32_t* adj, int64_t n,
+                                   const uint32_t* owner, int64_t n_parts, int device,
+                                   qgnn_partition** out);
+int qgnn_agg_view_build_gpu(const int64_t* adj_ptr, const int32_t* adj, int64_t n,
+                            const uint32_t* owner, const qgnn_partition* part, int sage,
+                            int device, qgnn_agg_view** out);
+
 /* BitWidthPlan::Lookup::bits_for (assigner/plan.hpp:60-72) over one
  * (key, src, dst) entry list (ids ascending, bits parallel): out[k] = bits of
  * query[k]; an unknown id fails with QGNN_EINVAL "plan: unknown message id". */

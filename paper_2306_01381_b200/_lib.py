@@ -138,6 +138,8 @@ _SIGS = {
     "qgnn_exchange_plan": (C.c_int, [vp, vp, i64, vp, i64, C.c_int, C.c_int, i64, C.c_int,
                                      C.c_int, C.c_int, C.c_int, vp, vp]),
     "qgnn_partitions_from_owner": (C.c_int, [vp, vp, i64, vp, i64, vp]),
+    "qgnn_partitions_from_owner_gpu": (C.c_int, [vp, vp, i64, vp, i64, C.c_int, vp]),
+    "qgnn_agg_view_build_gpu": (C.c_int, [vp, vp, i64, vp, vp, C.c_int, C.c_int, C.POINTER(vp)]),
     "qgnn_partition_list": (C.c_int, [vp, C.c_int, i64, C.POINTER(vp), C.POINTER(i64)]),
     "qgnn_partition_destroy": (C.c_int, [vp]),
     "qgnn_agg_view_build": (C.c_int, [vp, vp, i64, vp, vp, C.c_int, C.POINTER(vp)]),

@@ -34,7 +34,9 @@
 #include <vector>
 
 #include "common.cuh"
+#include "dbuf.cuh"
 #include "host.hpp"
+#include "setup.cuh"
 #include "rng.cuh"
 
 namespace qgnn_b200 {
@@ -91,44 +93,6 @@ static NcclApi& nccl() {
     if (r_ != ncclSuccess)                                                               \
       throw ::qgnn_b200::Status(QGNN_ENCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
   } while (0)
-
-// ---------------------------------------------------------- device buffer ---
-template <typename X>
-struct DBuf {
-  X* p = nullptr;
-  size_t n = 0;
-  DBuf() = default;
-  DBuf(const DBuf&) = delete;
-  DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
-  DBuf& operator=(DBuf&& o) noexcept {
-    std::swap(p, o.p);
-    std::swap(n, o.n);
-    return *this;
-  }
-  ~DBuf() {
-    if (p) cudaFree(p);
-  }
-  void alloc(size_t count, bool zero = true) {
-    if (count <= n && p) {
-      if (zero) QGNN_CUDA(cudaMemset(p, 0, count * sizeof(X)));
-      QGNN_CUDA(cudaDeviceSynchronize());
-      return;
-    }
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = count;
-    QGNN_CUDA(cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(X)));
-    if (zero) QGNN_CUDA(cudaMemset(p, 0, std::max<size_t>(1, count) * sizeof(X)));
-    // legacy-stream memsets/copies do not order against our non-blocking streams
-    QGNN_CUDA(cudaDeviceSynchronize());
-  }
-  void upload(const std::vector<X>& v) {
-    alloc(v.size(), false);
-    if (!v.empty()) QGNN_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(X), cudaMemcpyHostToDevice));
-    QGNN_CUDA(cudaDeviceSynchronize());
-  }
-};
 
 // Row-range plan of the production fp32 SpMM (spmm.cu:spmm_f32): rows with
 // more than hub_deg neighbours (a + b lists) are split into 256-edge segments
@@ -427,6 +391,18 @@ class Engine final : public EngineBase {
       return 1;
     }
   }
+  // f(i) for every hosted partition on its own host thread (setup and plan
+  // uploads: per-partition host loops, uploads and allocations are independent)
+  template <typename F>
+  void par_parts(F&& f) {
+    std::vector<std::future<void>> jobs;
+    for (size_t i = 0; i < parts_dev_.size(); ++i)
+      jobs.push_back(std::async(std::launch::async, [&, i] {
+        QGNN_CUDA(cudaSetDevice(s_.device));
+        f(i);
+      }));
+    for (auto& j : jobs) j.get();
+  }
   void build_messages();
   void negotiate_sizes();
   DBuf<uint64_t> neg_;
@@ -615,8 +591,6 @@ class Engine final : public EngineBase {
   KStat kst_[QGNN_K_COUNT];
   int cur_cls_ = -1;
   int64_t launches_ = 0, launches_last_ = 0;
-  T* pinned_ = nullptr;
-  size_t pinned_elems_ = 0;
   DBuf<T> feat_all_;  // node-ordered features (pinned-input fast path)
   // async feature upload: node-range chunks on s_copy_, one event per chunk;
   // partition p's gather waits for the chunk holding its largest node id
@@ -757,9 +731,34 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
     owner_.assign(owner, owner + n);
   else
     owner_ = partition_owner_bfs(ptr, adj, n, P_, s.seed);
-  parts_ = partitions_from_owner(ptr, adj, n, owner_.data(), P_);
+  // §8f rank 3: consumer sets, coefficients, views and Σα² weights on the GPU
+  // (QGNN_GPU_SETUP=0: the host builders of host_graph.cpp; identical outputs)
+  const bool gpu_setup = [] {
+    const char* e = std::getenv("QGNN_GPU_SETUP");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool prof = std::getenv("QGNN_SETUP_PROFILE") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!prof) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[qgnn setup] %-22s %8.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
+  phase("streams / comm");
+  std::unique_ptr<GraphDev> gdev;
   std::vector<double> alpha, self_alpha;
-  compute_coeffs(ptr, adj, n, s.sage != 0, alpha, self_alpha);
+  if (gpu_setup) {
+    gdev = std::make_unique<GraphDev>(ptr, adj, n, owner_.data(), P_, s_main_);
+    phase("graph upload");
+    parts_ = partitions_from_owner_gpu(*gdev, owner_.data());
+    phase("partitions (gpu)");
+  } else {
+    parts_ = partitions_from_owner(ptr, adj, n, owner_.data(), P_);
+    compute_coeffs(ptr, adj, n, s.sage != 0, alpha, self_alpha);
+    phase("partitions+coeffs (host)");
+  }
 
   for (int64_t v = 0; v < n; ++v) {
     global_train_ += train[v] != 0;
@@ -778,7 +777,15 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
 
   // views of hosted partitions (parallel)
   parts_dev_.resize(p1_ - p0_);
-  {
+  std::vector<ViewDev<T>> vdev(size_t(p1_ - p0_));
+  if (gpu_setup) {
+    for (int64_t i = 0; i < p1_ - p0_; ++i) {
+      parts_dev_[i] = std::make_unique<PartDev>();
+      parts_dev_[i]->id = int(p0_ + i);
+      build_view_gpu<T>(*gdev, parts_[p0_ + i], s.sage != 0, true, parts_dev_[i]->view, vdev[i],
+                        false);
+    }
+  } else {
     std::vector<std::future<View>> futs;
     for (int64_t p = p0_; p < p1_; ++p)
       futs.push_back(std::async(std::launch::async, [&, p] {
@@ -791,8 +798,11 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
     }
   }
 
+  phase("views");
   // forward-statistics weights of every pair (engine.hpp:262-273), for adaptive
-  if (s.bit_mode == kAdaptive) {
+  if (s.bit_mode == kAdaptive && gpu_setup) {
+    rx_asq_ = rx_alpha_sq_gpu(*gdev, parts_, s.sage != 0);
+  } else if (s.bit_mode == kAdaptive) {
     rx_asq_.assign(P_, std::vector<std::vector<double>>(P_));
     for (int64_t p = 0; p < P_; ++p)
       for (int64_t q = 0; q < P_; ++q) {
@@ -814,22 +824,39 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
       }
   }
 
-  // device state per hosted partition
-  for (auto& up : parts_dev_) {
-    PartDev& D = *up;
+  phase("rx alpha^2");
+  gdev.reset();  // the device copy of the graph is only needed for setup
+  // device state per hosted partition (partitions on worker threads)
+  par_parts([&](size_t ip) {
+    PartDev& D = *parts_dev_[ip];
     const View& V = D.view;
-    auto tocast = [](const std::vector<double>& v) { return std::vector<T>(v.begin(), v.end()); };
-    D.lptr.upload(V.local_ptr);
-    D.lcol.upload(V.local_col);
-    D.lafwd.upload(tocast(V.local_afwd));
-    D.labwd.upload(tocast(V.local_abwd));
-    D.rptr.upload(V.remote_ptr);
-    D.rslot.upload(V.remote_slot);
-    D.ralpha.upload(tocast(V.remote_alpha));
-    D.sptr.upload(V.slot_ptr);
-    D.srow.upload(V.slot_row);
-    D.salpha.upload(tocast(V.slot_alpha));
-    D.self_alpha.upload(tocast(V.self_alpha));
+    if (gpu_setup) {  // built in place on the device
+      ViewDev<T>& vd = vdev[ip];
+      D.lptr = std::move(vd.lptr);
+      D.lcol = std::move(vd.lcol);
+      D.lafwd = std::move(vd.lafwd);
+      D.labwd = std::move(vd.labwd);
+      D.rptr = std::move(vd.rptr);
+      D.rslot = std::move(vd.rslot);
+      D.ralpha = std::move(vd.ralpha);
+      D.sptr = std::move(vd.sptr);
+      D.srow = std::move(vd.srow);
+      D.salpha = std::move(vd.salpha);
+      D.self_alpha = std::move(vd.self_alpha);
+    } else {
+      auto tocast = [](const std::vector<double>& v) { return std::vector<T>(v.begin(), v.end()); };
+      D.lptr.upload(V.local_ptr);
+      D.lcol.upload(V.local_col);
+      D.lafwd.upload(tocast(V.local_afwd));
+      D.labwd.upload(tocast(V.local_abwd));
+      D.rptr.upload(V.remote_ptr);
+      D.rslot.upload(V.remote_slot);
+      D.ralpha.upload(tocast(V.remote_alpha));
+      D.sptr.upload(V.slot_ptr);
+      D.srow.upload(V.slot_row);
+      D.salpha.upload(tocast(V.slot_alpha));
+      D.self_alpha.upload(tocast(V.self_alpha));
+    }
     std::vector<int32_t> lab(V.num_owned), tr, va, te;
     for (int64_t g = 0; g < V.num_owned; ++g) {
       const uint32_t node = V.row_node[g];
@@ -895,7 +922,7 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
     }
     D.snd.resize(keys_.size());
     D.rcv.resize(keys_.size());
-  }
+  });
   {  // feature-upload chunks: boundaries at each local partition's largest node id
     std::vector<int64_t> ends;
     for (auto& up : parts_dev_) {
@@ -919,6 +946,7 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
       part_chunk_.push_back(c);
     }
   }
+  phase("device state / hubs");
   set_features(features);
   if (feat_pending_) {  // construction consumes the features right away
     for (auto& up : parts_dev_) gather_features(*up);
@@ -948,10 +976,14 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
   wsum_.alloc(nparams_);
 
   plan_version_ = s.bit_mode == kAdaptive ? 1 : 0;
+  phase("features / weights");
   build_messages();
+  phase("message lists");
   for (size_t k = 0; k < keys_.size(); ++k) upload_key_meta(int(k));
+  phase("message metadata");
   QGNN_CUDA(cudaDeviceSynchronize());
   negotiate_sizes();
+  phase("sync / negotiate");
 }
 
 // negotiate_buffers (plan.hpp:140-154) across ranks: every rank derives every
@@ -1029,7 +1061,6 @@ Engine<T>::~Engine() {
   }
   if (ev_c_) cudaEventDestroy(ev_c_);
   if (ev_d_) cudaEventDestroy(ev_d_);
-  if (pinned_) cudaFreeHost(pinned_);
   if (ev_a_) cudaEventDestroy(ev_a_);
   if (ev_b_) cudaEventDestroy(ev_b_);
   if (ev_x_) cudaEventDestroy(ev_x_);
@@ -1062,63 +1093,31 @@ __global__ void k_gather_rows(const T* __restrict__ feats, int64_t F, const int3
 
 template <typename T>
 void Engine<T>::set_features(const void* f) {
-  const int64_t F = dims_[0], ld = ld_of(F);
+  const int64_t F = dims_[0];
   const T* src = static_cast<const T*>(f);
   cudaPointerAttributes attr{};
   const bool pinned = cudaPointerGetAttributes(&attr, f) == cudaSuccess &&
                       (attr.type == cudaMemoryTypeHost || attr.type == cudaMemoryTypeDevice);
   cudaGetLastError();
-  if (pinned) {
-    // node-range chunks copied asynchronously on s_copy_ (after the previous
-    // epoch's readers of feat_all_); the epoch's first layer gathers partition
-    // p into row order as soon as p's chunk has landed (gather_features), so
-    // the upload overlaps the first layer's work.  The caller keeps `f` alive
-    // until the next run_epoch returns.
-    if (!feat_all_.p || feat_all_.n < size_t(n_nodes_ * F)) feat_all_.alloc(n_nodes_ * F, false);
-    // the staging matrix is free once the last epoch's gathers have read it
-    // (ev_feat_free_ is recorded after them), so this copy may overlap the
-    // rest of an epoch that is still in flight
-    QGNN_CUDA(cudaStreamWaitEvent(s_copy_, ev_feat_free_, 0));
-    for (size_t c = 0; c + 1 < feat_bounds_.size(); ++c) {
-      const int64_t a = feat_bounds_[c], b = feat_bounds_[c + 1];
-      QGNN_CUDA(cudaMemcpyAsync(feat_all_.p + a * F, src + a * F, size_t(b - a) * F * sizeof(T),
-                                cudaMemcpyDefault, s_copy_));
-      QGNN_CUDA(cudaEventRecord(ev_feat_[c], s_copy_));
-    }
-    feat_pending_ = true;
-    return;
+  // node-range chunks copied asynchronously on s_copy_ (after the previous
+  // epoch's readers of feat_all_); the epoch's first layer gathers partition
+  // p into row order as soon as p's chunk has landed (gather_features), so
+  // the upload overlaps the first layer's work.  A pinned `f` must stay alive
+  // until the next run_epoch returns; a pageable one is consumed before
+  // set_features returns (the copies from it are synchronous).
+  if (!feat_all_.p || feat_all_.n < size_t(n_nodes_ * F)) feat_all_.alloc(n_nodes_ * F, false);
+  // the staging matrix is free once the last epoch's gathers have read it
+  // (ev_feat_free_ is recorded after them), so this copy may overlap the
+  // rest of an epoch that is still in flight
+  QGNN_CUDA(cudaStreamWaitEvent(s_copy_, ev_feat_free_, 0));
+  for (size_t c = 0; c + 1 < feat_bounds_.size(); ++c) {
+    const int64_t a = feat_bounds_[c], b = feat_bounds_[c + 1];
+    QGNN_CUDA(cudaMemcpyAsync(feat_all_.p + a * F, src + a * F, size_t(b - a) * F * sizeof(T),
+                              cudaMemcpyDefault, s_copy_));
+    QGNN_CUDA(cudaEventRecord(ev_feat_[c], s_copy_));
   }
-  size_t total = 0;
-  for (auto& up : parts_dev_) total += size_t(up->view.num_owned * ld);
-  if (total > pinned_elems_) {
-    if (pinned_) cudaFreeHost(pinned_);
-    QGNN_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&pinned_), total * sizeof(T), cudaHostAllocDefault));
-    std::memset(pinned_, 0, total * sizeof(T));
-    pinned_elems_ = total;
-  }
-  // pageable input: gather rows into partition order on host threads, then one
-  // pinned H2D per partition
-  std::vector<std::future<void>> jobs;
-  size_t o = 0;
-  for (auto& up : parts_dev_) {
-    PartDev* D = up.get();
-    T* dst = pinned_ + o;
-    o += size_t(D->view.num_owned * ld);
-    jobs.push_back(std::async(std::launch::async, [D, dst, src, F, ld] {
-      const int64_t no = D->view.num_owned;
-      for (int64_t g = 0; g < no; ++g)
-        std::memcpy(dst + g * ld, src + int64_t(D->view.row_node[g]) * F, F * sizeof(T));
-    }));
-  }
-  o = 0;
-  for (size_t i = 0; i < parts_dev_.size(); ++i) {
-    jobs[i].get();
-    PartDev& D = *parts_dev_[i];
-    QGNN_CUDA(cudaMemcpyAsync(D.h[0].p, pinned_ + o, D.view.num_owned * ld * sizeof(T),
-                              cudaMemcpyHostToDevice, s_main_));
-    o += size_t(D.view.num_owned * ld);
-  }
-  QGNN_CUDA(cudaStreamSynchronize(s_main_));
+  if (!pinned) QGNN_CUDA(cudaStreamSynchronize(s_copy_));
+  feat_pending_ = true;
 }
 
 // warp per row, 16-byte vectors (rows of F % 4 == 0 fp32 features)
@@ -1168,20 +1167,27 @@ void Engine<T>::recount_bits() {
 template <typename T>
 void Engine<T>::build_messages() {
   msgs_.assign(keys_.size(), std::vector<std::vector<PairMsgs>>(P_, std::vector<PairMsgs>(P_)));
-  for (size_t k = 0; k < keys_.size(); ++k)
-    for (int64_t p = 0; p < P_; ++p)
-      for (int64_t q = 0; q < P_; ++q) {
-        if (p == q) continue;
-        PairMsgs& m = msgs_[k][p][q];
-        m.ids = keys_[k].bwd ? parts_[p].remote_in[q] : parts_[p].remote_out[q];
-        const uint8_t b = s_.bit_mode == kFp ? 0 : s_.bit_mode == kFixed ? uint8_t(s_.fixed_bits) : 8;
-        m.bits.assign(m.ids.size(), b);  // adaptive: initial all-8 plan (plan.hpp:104-126)
-      }
+  // (key, source) rows of the pair table on host threads
+  auto rows = [&](auto&& f) {
+    std::vector<std::future<void>> jobs;
+    for (size_t k = 0; k < keys_.size(); ++k)
+      for (int64_t p = 0; p < P_; ++p) jobs.push_back(std::async(std::launch::async, f, k, p));
+    for (auto& j : jobs) j.get();
+  };
+  rows([&](size_t k, int64_t p) {
+    for (int64_t q = 0; q < P_; ++q) {
+      if (p == q) continue;
+      PairMsgs& m = msgs_[k][p][q];
+      m.ids = keys_[k].bwd ? parts_[p].remote_in[q] : parts_[p].remote_out[q];
+      const uint8_t b = s_.bit_mode == kFp ? 0 : s_.bit_mode == kFixed ? uint8_t(s_.fixed_bits) : 8;
+      m.bits.assign(m.ids.size(), b);  // adaptive: initial all-8 plan (plan.hpp:104-126)
+    }
+  });
   if (s_.bit_mode == kUniform) compute_bits_uniform();
-  for (size_t k = 0; k < keys_.size(); ++k)
-    for (int64_t p = 0; p < P_; ++p)
-      for (int64_t q = 0; q < P_; ++q)
-        if (p != q) layout_pair(int(k), int(p), int(q));
+  rows([&](size_t k, int64_t p) {
+    for (int64_t q = 0; q < P_; ++q)
+      if (p != q) layout_pair(int(k), int(p), int(q));
+  });
   arena_layout();
   bits_dirty_ = true;
 }
@@ -1265,8 +1271,8 @@ void Engine<T>::upload_key_meta(int k) {
   // message lists never change: rows / ids / destinations (and the windows)
   // are uploaded once; widths and wire offsets follow every plan
   const KeyInfo& K = keys_[k];
-  for (auto& up : parts_dev_) {
-    PartDev& D = *up;
+  par_parts([&](size_t ip) {
+    PartDev& D = *parts_dev_[ip];
     const int64_t p = D.id;
     const View& V = D.view;
     auto& S = D.snd[k];
@@ -1358,7 +1364,7 @@ void Engine<T>::upload_key_meta(int k) {
     R.bits.upload(rb);
     R.off.upload(ro);
     if (gpu_layout) R.env.upload(env);
-  }
+  });
 }
 
 template <typename T>

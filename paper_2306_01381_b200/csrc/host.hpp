@@ -59,8 +59,9 @@ struct View {
   std::vector<int32_t> owned_gpu_row;   // GPU row of owned_sorted[i]
   // distinct source rows per SpMM call site (self rows included; §8d bytes)
   int64_t src_rows_central = 0, src_rows_marginal = 0, src_rows_all = 0, src_slots_marginal = 0;
-  int64_t local_nnz() const { return static_cast<int64_t>(local_col.size()); }
-  int64_t remote_nnz() const { return static_cast<int64_t>(remote_slot.size()); }
+  // (the GPU setup keeps the edge arrays on the device only: counts from the pointers)
+  int64_t local_nnz() const { return local_ptr.empty() ? 0 : local_ptr.back(); }
+  int64_t remote_nnz() const { return remote_ptr.empty() ? 0 : remote_ptr.back(); }
 };
 
 View build_view(const int64_t* ptr, const int32_t* adj, int64_t n, const Part& part,
@@ -110,3 +111,14 @@ void solve_brute(SolveResult& plan, const Cost& cm, double lambda);   // solve.h
 double uniform_expected_variance(const std::vector<PairStat>& pairs);  // solve.hpp:313-326
 
 }  // namespace qgnn_b200
+
+// C-ABI handles (include/qgnn_b200.h): a partition and a reference-order view
+struct qgnn_partition {
+  qgnn_b200::Part part;
+};
+struct qgnn_agg_view {
+  std::vector<double> self_alpha, local_alpha_fwd, local_alpha_bwd, remote_alpha;
+  std::vector<int64_t> local_ptr, remote_ptr, device_slot_offset;
+  std::vector<uint32_t> local_row, remote_slot, slot_node, slot_owner, central_rows, marginal_rows;
+  int64_t num_owned = 0, num_remote = 0;
+};

@@ -376,17 +376,6 @@ int qgnn_partition_stats(const int64_t* adj_ptr, const int32_t* adj, int64_t n,
 // ---- partitions_from_owner / DeviceAggView::build / Lookup::bits_for ---------
 }  // extern "C"
 
-struct qgnn_partition {
-  Part part;
-};
-
-struct qgnn_agg_view {
-  std::vector<double> self_alpha, local_alpha_fwd, local_alpha_bwd, remote_alpha;
-  std::vector<int64_t> local_ptr, remote_ptr, device_slot_offset;
-  std::vector<uint32_t> local_row, remote_slot, slot_node, slot_owner, central_rows, marginal_rows;
-  int64_t num_owned = 0, num_remote = 0;
-};
-
 extern "C" {
 
 int qgnn_partitions_from_owner(const int64_t* adj_ptr, const int32_t* adj, int64_t n,

@@ -299,16 +299,27 @@ def adam_step(p, m, v, g, t, lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8):
 
 
 # ---- graphcore/partition.hpp, tensorops/aggregate.hpp, assigner/plan.hpp (host) -------------
-def partitions_from_owner(adj_ptr, adj, owner, n_parts: int):
+def _partition_handles(adj_ptr, adj, owner, n_parts, gpu_device):
+    hs = (C.c_void_p * n_parts)()
+    if gpu_device is None:
+        check(lib.qgnn_partitions_from_owner(adj_ptr.ctypes.data, adj.ctypes.data, len(owner),
+                                             owner.ctypes.data, n_parts, hs))
+    else:  # consumer sets on the device
+        check(lib.qgnn_partitions_from_owner_gpu(adj_ptr.ctypes.data, adj.ctypes.data,
+                                                 len(owner), owner.ctypes.data, n_parts,
+                                                 gpu_device, hs))
+    return hs
+
+
+def partitions_from_owner(adj_ptr, adj, owner, n_parts: int, gpu_device: Optional[int] = None):
     """partitions_from_owner (partition.hpp:39-84) through the C-ABI: one dict
     per device with owned / central / marginal and remote_in[q] / remote_out[q]
-    (ascending node ids, like Partition)."""
+    (ascending node ids, like Partition).  gpu_device: build on that GPU
+    (qgnn_partitions_from_owner_gpu) instead of the host."""
     adj_ptr = np.ascontiguousarray(adj_ptr, np.int64)
     adj = np.ascontiguousarray(adj, np.int32)
     owner = np.ascontiguousarray(owner, np.uint32)
-    hs = (C.c_void_p * n_parts)()
-    check(lib.qgnn_partitions_from_owner(adj_ptr.ctypes.data, adj.ctypes.data, len(owner),
-                                         owner.ctypes.data, n_parts, hs))
+    hs = _partition_handles(adj_ptr, adj, owner, n_parts, gpu_device)
 
     def lst(h, which, q=0):
         p, n = C.c_void_p(), C.c_int64()
@@ -329,19 +340,25 @@ def partitions_from_owner(adj_ptr, adj, owner, n_parts: int):
     return out
 
 
-def agg_view(adj_ptr, adj, owner, n_parts: int, device: int, sage: bool = False):
+def agg_view(adj_ptr, adj, owner, n_parts: int, device: int, sage: bool = False,
+             gpu_device: Optional[int] = None):
     """DeviceAggView::build (aggregate.hpp:41-89) for `device` of the owner map,
-    reference row / slot order, as numpy arrays."""
+    reference row / slot order, as numpy arrays.  gpu_device: partitions and
+    view built on that GPU (qgnn_*_gpu) instead of the host."""
     adj_ptr = np.ascontiguousarray(adj_ptr, np.int64)
     adj = np.ascontiguousarray(adj, np.int32)
     owner = np.ascontiguousarray(owner, np.uint32)
-    hs = (C.c_void_p * n_parts)()
-    check(lib.qgnn_partitions_from_owner(adj_ptr.ctypes.data, adj.ctypes.data, len(owner),
-                                         owner.ctypes.data, n_parts, hs))
+    hs = _partition_handles(adj_ptr, adj, owner, n_parts, gpu_device)
     view = C.c_void_p()
     try:
-        check(lib.qgnn_agg_view_build(adj_ptr.ctypes.data, adj.ctypes.data, len(owner),
-                                      owner.ctypes.data, hs[device], int(sage), C.byref(view)))
+        if gpu_device is None:
+            check(lib.qgnn_agg_view_build(adj_ptr.ctypes.data, adj.ctypes.data, len(owner),
+                                          owner.ctypes.data, hs[device], int(sage),
+                                          C.byref(view)))
+        else:
+            check(lib.qgnn_agg_view_build_gpu(adj_ptr.ctypes.data, adj.ctypes.data, len(owner),
+                                              owner.ctypes.data, hs[device], int(sage),
+                                              gpu_device, C.byref(view)))
     finally:
         for h in hs:
             lib.qgnn_partition_destroy(h)
