@@ -195,8 +195,6 @@ struct Params {
   int dbg;  // QGNN_GEMM_DEBUG bit mask for bottleneck isolation (results invalid when set):
             // 1 = no MMAs, 2 = no output stores, 4 = no lo split, 8 = TMA producer only
   int bk;  // K elements per chunk: 16 (SW64, 64-byte rows) or 32 (SW128, K-major only)
-  int bsplit;  // K-major: 1 = only the fp32 B tile is loaded and the converters split its
-               // lo part in shared memory (B TMA bytes halved); 0 = pre-split hi / lo copies
   int cs;  // K-major: CTAs per cluster sharing each B stage (1, 2, 4).  Rank r loads
            // B rows [r BN/cs, (r+1) BN/cs) once and multicasts them to the cluster; a
            // stage is refilled when every CTA's MMAs have drained it (empty count = cs)
@@ -285,16 +283,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* Blo = B + b_bytes;
           const int k0 = kc * bk;
           if (!kMN) {
-            mbar_expect_tx(&full[s], a_bytes + (p.bsplit ? 1 : 2) * b_bytes);
+            mbar_expect_tx(&full[s], a_bytes + 2 * b_bytes);
             for (int h = 0; h < p.mh; ++h)
               tma_load_2d(A + h * (kBM * bk * 4), &tmA, &full[s], k0, m0 + kBM * h);
             if (p.cs == 1) {
               tma_load_2d(B, &tmB, &full[s], k0, 0);
-              if (!p.bsplit) tma_load_2d(Blo, &tmBlo, &full[s], k0, 0);
+              tma_load_2d(Blo, &tmBlo, &full[s], k0, 0);
             } else {  // this rank's slice of B rows, to every CTA of the cluster
               const int rows = p.BN / p.cs, off = crank * rows * bk * 4;
               tma_load_2d_mc(B + off, &tmB, &full[s], k0, crank * rows, cmask);
-              if (!p.bsplit) tma_load_2d_mc(Blo + off, &tmBlo, &full[s], k0, crank * rows, cmask);
+              tma_load_2d_mc(Blo + off, &tmBlo, &full[s], k0, crank * rows, cmask);
             }
           } else {
             mbar_expect_tx(&full[s], a_bytes + b_bytes);
@@ -477,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* st = smem + s * stage_bytes;
         if (!(p.dbg & 4))
           split_tile(smem_u32(st), smem_u32(st + a_bytes), a_bytes / 16, t, 128);
-        if (kMN || p.bsplit)  // B lo = x - tf32(x) of the landed B tile (same bits as k_prep_b's)
+        if (kMN)
           split_tile(smem_u32(st + 2 * a_bytes), smem_u32(st + 2 * a_bytes + b_bytes),
                      b_bytes / 16, t, 128);
         fence_proxy_async();
@@ -507,10 +505,9 @@ __global__ void k_prep_b(const float* __restrict__ W, int wcols, int N, int K, i
   const int n = int(i / Kp), k = int(i % Kp);
   float x = 0.f;
   if (k < K) x = transpose ? W[int64_t(k) * wcols + n] : W[int64_t(n) * wcols + k];
-  // hi is stored unrounded: kind::tf32 reads only its top 19 bits (= tf32_hi(x)),
-  // and the in-smem split (Params::bsplit) needs x itself to form lo
-  bhi[i] = x;
-  blo[i] = x - tf32_hi(x);
+  const float h = tf32_hi(x);
+  bhi[i] = h;
+  blo[i] = x - h;
 }
 
 }  // namespace tc
@@ -567,11 +564,6 @@ int gemm_debug() {
 int gemm_bk() {  // QGNN_GEMM_BK=32: 128-byte K-major rows (SW128) for z = A W / dz W^T
   const char* e = std::getenv("QGNN_GEMM_BK");
   return e && std::atoi(e) == 32 ? 32 : 16;
-}
-
-bool gemm_bsplit() {  // QGNN_GEMM_BSPLIT=0: load pre-split B hi / lo copies (round 1)
-  const char* e = std::getenv("QGNN_GEMM_BSPLIT");
-  return !e || std::atoi(e) != 0;
 }
 
 int gemm_cluster() {  // QGNN_GEMM_CLUSTER: CTAs sharing each B stage (1, 2 or 4)
@@ -696,7 +688,6 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
   p.mh = m256 ? 2 : 1;
   p.m_tiles = int(ceil_div(n_rows, tc::kBM * p.mh));
   p.cs = cs;
-  p.bsplit = gemm_bsplit() ? 1 : 0;
   p.dbg = gemm_debug();
   if (cs > 1) p.m_tiles = int(round_up(p.m_tiles, cs));
   p.stages = stages_for(BN, p.mh, bk);

@@ -211,27 +211,3 @@ def test_loss_adam_relu(cuda):
     dz = torch.zeros((50, 9), dtype=torch.float64, device=cuda)
     ops.relu_backward(_t(act), _t(dh), dz)
     assert (dz.cpu().numpy() == np.where(act <= 0, 0, dh)).all()
-
-
-@pytest.mark.parametrize("cluster", ["1", "2"])
-@pytest.mark.parametrize("din,dout", [(100, 256), (256, 256), (256, 47), (47, 256), (602, 256)])
-def test_dense_f32_smem_b_split_bit_identical(cuda, monkeypatch, cluster, din, dout):
-    """K-major GEMM with B's lo part split in shared memory by the converter warps
-    (QGNN_GEMM_BSPLIT=1, default) is bit-identical to loading the pre-split
-    hi / lo copies (=0): same truncation, same products, same order."""
-    rs = np.random.default_rng(din + dout)
-    n = 3000
-    a = _t(rs.standard_normal((n, din)), torch.float32)
-    w = _t(rs.standard_normal((din, dout)) / np.sqrt(din), torch.float32)
-    dz = _t(rs.standard_normal((n, dout)), torch.float32)
-    monkeypatch.setenv("QGNN_GEMM_CLUSTER", cluster)
-    res = []
-    for bs in ("0", "1"):
-        monkeypatch.setenv("QGNN_GEMM_BSPLIT", bs)
-        out = torch.zeros((n, dout), device=cuda)
-        ops.dense_forward(a, w, out, relu=True)
-        ig = torch.zeros((n, din), device=cuda)
-        ops.dense_input_grad(dz, w, ig)
-        res.append((out, ig))
-    assert torch.equal(res[0][0], res[1][0])
-    assert torch.equal(res[0][1], res[1][1])
