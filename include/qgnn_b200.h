@@ -327,9 +327,13 @@ typedef struct {
                               overlap the exchange on the comm stream; 2: one GPU, K1/K3
                               also on a side stream next to the central rows */
   int32_t kstats;          /* 1: time every kernel class with CUDA events (bench roofline) */
-  int32_t transport;       /* world == 1 only: 0 zero copy between the partitions of the
-                              GPU (default); 1 every pair through NCCL self send/receive
-                              (the multi-GPU exchange path, run and timed on one device) */
+  int32_t transport;       /* world == 1: 0 zero copy between the partitions of the GPU
+                              (default); 1 every pair through NCCL self send/receive (the
+                              multi-GPU exchange path, run and timed on one device).
+                              world > 1: 0 grouped NCCL send/receive (default); 2 peer
+                              store — K1 writes each remote pair's chunks straight into
+                              the receiver's arena (CUDA IPC / peer memory over NVLink),
+                              ordered by ready / consumed flags, no exchange copies */
   int32_t layer_norm;      /* TrainSettings::layer_norm (engine.hpp:42): LN after every
                               layer's transform (model.hpp:62-73, 108-112) */
   double dropout;          /* TrainSettings::dropout (engine.hpp:43): inverted dropout on

@@ -6,6 +6,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "qgnn_b200.h"
 #include "status.hpp"
@@ -93,6 +94,9 @@ struct qgnn_ctx {
   size_t scratch_bytes = 0;
   void* gemm_b = nullptr;        // pre-split weight operand of the tcgen05 GEMM
   size_t gemm_b_bytes = 0;
+  // outgrown workspaces, freed with the context: a cudaFree while kernels run would
+  // synchronize the whole device (and deadlock peer-store ranks sharing one GPU)
+  std::vector<void*> retired;
   int num_sms = 148;
   // Reuse of the pre-split weight operand across consecutive GEMMs with the same
   // weights (the P partitions of one layer).  Opt-in: an owner that knows when its

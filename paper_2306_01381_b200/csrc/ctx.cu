@@ -39,7 +39,7 @@ int status_from_exception() {
 
 void* ctx_scratch(qgnn_ctx* ctx, size_t bytes) {
   if (bytes <= ctx->scratch_bytes) return ctx->scratch;
-  if (ctx->scratch) QGNN_CUDA(cudaFree(ctx->scratch));
+  if (ctx->scratch) ctx->retired.push_back(ctx->scratch);
   ctx->scratch = nullptr;
   ctx->scratch_bytes = 0;
   QGNN_CUDA(cudaMalloc(&ctx->scratch, bytes));
@@ -49,7 +49,7 @@ void* ctx_scratch(qgnn_ctx* ctx, size_t bytes) {
 
 void* ctx_gemm_b(qgnn_ctx* ctx, size_t bytes) {
   if (bytes <= ctx->gemm_b_bytes) return ctx->gemm_b;
-  if (ctx->gemm_b) QGNN_CUDA(cudaFree(ctx->gemm_b));
+  if (ctx->gemm_b) ctx->retired.push_back(ctx->gemm_b);
   ctx->gemm_b = nullptr;
   ctx->gemm_b_bytes = 0;
   QGNN_CUDA(cudaMalloc(&ctx->gemm_b, bytes));
@@ -128,6 +128,7 @@ int qgnn_ctx_destroy(qgnn_ctx* ctx) {
   if (ctx->d_err) cudaFree(ctx->d_err);
   if (ctx->scratch) cudaFree(ctx->scratch);
   if (ctx->gemm_b) cudaFree(ctx->gemm_b);
+  for (void* p : ctx->retired) cudaFree(p);
   delete ctx;
   QGNN_API_END
 }

@@ -216,6 +216,34 @@ struct LoopGroup {
     }
   }
 };
+// Peer-store flags.  signal: every prior write of this stream (the K1 stores into
+// peer arenas, or the reads of the receive regions) is ordered before the flag
+// store (kernel boundary + system fence, release at system scope).  wait: acquire
+// at system scope; gives up after 30 s with a ProtocolError instead of hanging.
+__global__ void k_p2p_signal(uint64_t* const* __restrict__ dst, int n, uint64_t v) {
+  const int i = threadIdx.x;
+  if (i >= n || !dst[i]) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst[i]), "l"(v) : "memory");
+}
+__global__ void k_p2p_wait(const uint64_t* __restrict__ flags, int n, int skip, uint64_t v,
+                           int* err) {
+  const int i = threadIdx.x;
+  if (i >= n || i == skip) return;
+  uint64_t t0, t, x;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(flags + i) : "memory");
+    if (x >= v) break;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 30000000000ull) {
+      atomicOr(err, kErrProtocol);
+      break;
+    }
+    __nanosleep(200);
+  }
+}
+
 static std::mutex g_loop_mu;
 static std::map<uint64_t, std::shared_ptr<LoopGroup>> g_loops;
 constexpr char kLoopMagic[8] = {'Q', 'G', 'N', 'N', 'L', 'O', 'O', 'P'};
@@ -572,6 +600,25 @@ class Engine final : public EngineBase {
   // msgs_[k][p][q]
   std::vector<std::vector<std::vector<PairMsgs>>> msgs_;
   std::vector<std::vector<std::vector<uint64_t>>> send_base_, recv_base_;
+  // ---- peer-store transport (settings.transport = 2, world > 1):
+  // K1 stores each remote pair's chunks straight into the receiver's arena (peer
+  // memory over NVLink: CUDA IPC across processes, plain device pointers between
+  // in-process loopback ranks), so the exchange moves no bytes of its own.  The
+  // arena layout is plan-independent (worst-case widths), every rank derives every
+  // rank's receive offsets, and per-rank flags at the arena's tail order the stores:
+  // flags[0, world) = exchanges whose stores peer r has finished (ready), flags[world,
+  // 2 world) = exchanges peer r has finished reading (consumed).
+  bool p2p_ = false;
+  bool send_open_ = false;       // this exchange's consumed-wait / ready-signal pending
+  uint64_t xseq_ = 0;            // exchanges completed (identical on every rank)
+  std::vector<uint8_t*> peer_arena_;                       // [world] (own = arena_.p)
+  std::vector<uint64_t> flags_off_;                        // [world] flag block offsets
+  std::vector<std::vector<std::vector<uint64_t>>> p2p_recv_;  // [k][q][p] in q's arena
+  std::vector<bool> ipc_opened_;
+  DBuf<uint64_t*> sig_ready_, sig_cons_;  // peers' flag words this rank writes
+  void p2p_layout();
+  void p2p_connect();
+  void p2p_begin_send();
   DBuf<uint8_t> arena_;
   size_t arena_bytes_ = 0;
   std::vector<std::unique_ptr<PartDev>> parts_dev_;
@@ -720,6 +767,7 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
       std::memcpy(&id, nccl_id, sizeof(id));
       QGNN_NCCL(nccl().CommInitRank(&comm_, s.world, id, s.rank));
     }
+    p2p_ = s.transport == 2;
   } else if (s.transport == 1) {
     self_xfer_ = true;
     const int dev = s.device;  // one-rank communicator: no bootstrap network needed
@@ -978,6 +1026,7 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
   plan_version_ = s.bit_mode == kAdaptive ? 1 : 0;
   phase("features / weights");
   build_messages();
+  if (p2p_) p2p_connect();
   phase("message lists");
   for (size_t k = 0; k < keys_.size(); ++k) upload_key_meta(int(k));
   phase("message metadata");
@@ -1063,6 +1112,8 @@ Engine<T>::~Engine() {
   if (ev_d_) cudaEventDestroy(ev_d_);
   if (ev_a_) cudaEventDestroy(ev_a_);
   if (ev_b_) cudaEventDestroy(ev_b_);
+  for (size_t r = 0; r < ipc_opened_.size(); ++r)
+    if (ipc_opened_[r]) cudaIpcCloseMemHandle(peer_arena_[r]);
   if (ev_x_) cudaEventDestroy(ev_x_);
   if (ev_q_) cudaEventDestroy(ev_q_);
   if (s_main_) cudaStreamDestroy(s_main_);
@@ -1236,6 +1287,10 @@ void Engine<T>::compute_bits_uniform() {
 // same arena (they are processed one after another on the same streams).
 template <typename T>
 void Engine<T>::arena_layout() {
+  if (p2p_) {
+    p2p_layout();
+    return;
+  }
   send_base_.assign(keys_.size(), std::vector<std::vector<uint64_t>>(P_, std::vector<uint64_t>(P_, 0)));
   recv_base_ = send_base_;
   size_t need = 0;
@@ -1264,6 +1319,115 @@ void Engine<T>::arena_layout() {
     arena_.alloc(std::max<size_t>(need, 256), true);
     arena_bytes_ = std::max<size_t>(need, 256);
   }
+}
+
+// Peer-store layout, identical on every rank: per rank r, send regions of its
+// same-rank pairs (zero copy) then receive regions of remote sources, all keys
+// sharing one region (exchanges are sequential and the consumed flags order
+// reuse), each pair sized for its widest possible plan so no plan change moves or
+// grows an arena; then 2 * world flag words.
+template <typename T>
+void Engine<T>::p2p_layout() {
+  const int64_t K = int64_t(keys_.size()), ppr = P_ / s_.world;
+  const int wb = s_.bit_mode == kFp ? 0 : s_.bit_mode == kFixed ? s_.fixed_bits : 8;
+  auto worst = [&](int64_t k, int64_t p, int64_t q) {
+    return uint64_t(msgs_[k][p][q].ids.size()) *
+           qgnn_chunk_wire_bytes(uint64_t(keys_[k].dim), wb, s_.layout, dtype_);
+  };
+  auto al = [](uint64_t x) { return (x + 255) / 256 * 256; };
+  send_base_.assign(K, std::vector<std::vector<uint64_t>>(P_, std::vector<uint64_t>(P_, 0)));
+  recv_base_ = send_base_;
+  p2p_recv_ = send_base_;
+  flags_off_.assign(s_.world, 0);
+  for (int r = 0; r < s_.world; ++r) {
+    const int64_t a = r * ppr, b = a + ppr;
+    uint64_t need = 0;
+    for (int64_t k = 0; k < K; ++k) {
+      uint64_t o = 0;
+      for (int64_t p = a; p < b; ++p)
+        for (int64_t q = a; q < b; ++q) {
+          if (q == p) continue;
+          if (r == s_.rank) send_base_[k][p][q] = recv_base_[k][q][p] = o;
+          o = al(o + worst(k, p, q));
+        }
+      for (int64_t q = a; q < b; ++q)
+        for (int64_t p = 0; p < P_; ++p) {
+          if (p >= a && p < b) continue;
+          p2p_recv_[k][q][p] = o;
+          if (r == s_.rank) recv_base_[k][q][p] = o;
+          o = al(o + worst(k, p, q));
+        }
+      need = std::max(need, o);
+    }
+    flags_off_[r] = al(need);
+  }
+  const size_t bytes = flags_off_[s_.rank] + size_t(2 * s_.world) * sizeof(uint64_t);
+  if (!arena_.p) {  // zeroed: all flags start at 0
+    arena_.alloc(bytes, true);
+    arena_bytes_ = bytes;
+  }
+  QGNN_REQUIRE(bytes <= arena_bytes_, QGNN_EPROTOCOL, "peer-store arena cannot grow");
+}
+
+// Map every peer's arena: the loopback group's engines directly, other processes
+// through CUDA IPC handles all-gathered over NCCL.  Then the flag words this rank
+// signals: slot `rank` of every peer's ready block and of its consumed block.
+template <typename T>
+void Engine<T>::p2p_connect() {
+  const int W = s_.world;
+  peer_arena_.assign(W, nullptr);
+  ipc_opened_.assign(W, false);
+  peer_arena_[s_.rank] = arena_.p;
+  if (loop_) {
+    LoopGroup& G = *loop_;
+    G.barrier();  // every rank's arena exists
+    for (int r = 0; r < W; ++r) peer_arena_[r] = static_cast<Engine<T>*>(G.engines[r])->arena_.p;
+    G.barrier();
+  } else {
+    cudaIpcMemHandle_t h;
+    QGNN_CUDA(cudaIpcGetMemHandle(&h, arena_.p));
+    constexpr int64_t kH = sizeof(cudaIpcMemHandle_t);
+    DBuf<uint8_t> hs;
+    hs.alloc(size_t(kH * W), true);
+    QGNN_CUDA(cudaMemcpy(hs.p + kH * s_.rank, &h, kH, cudaMemcpyHostToDevice));
+    allgather_dev(hs.p, kH, s_main_);
+    QGNN_CUDA(cudaStreamSynchronize(s_main_));
+    std::vector<cudaIpcMemHandle_t> all(W);
+    QGNN_CUDA(cudaMemcpy(all.data(), hs.p, size_t(kH * W), cudaMemcpyDeviceToHost));
+    for (int r = 0; r < W; ++r) {
+      if (r == s_.rank) continue;
+      void* p = nullptr;
+      QGNN_CUDA(cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess));
+      peer_arena_[r] = static_cast<uint8_t*>(p);
+      ipc_opened_[r] = true;
+    }
+  }
+  std::vector<uint64_t*> rd(W, nullptr), cs(W, nullptr);
+  for (int r = 0; r < W; ++r) {
+    if (r == s_.rank) continue;
+    auto* f = reinterpret_cast<uint64_t*>(peer_arena_[r] + flags_off_[r]);
+    rd[r] = f + s_.rank;
+    cs[r] = f + W + s_.rank;
+  }
+  sig_ready_.upload(rd);
+  sig_cons_.upload(cs);
+}
+
+// Before this rank's first K1 store of the next exchange: publish that every
+// earlier exchange has been read here (the consumers precede this in stream
+// order), then wait until every peer has read the previous one out of the
+// regions these stores overwrite.
+template <typename T>
+void Engine<T>::p2p_begin_send() {
+  const int W = s_.world;
+  k_p2p_signal<<<1, 32 * unsigned(ceil_div(W, 32)), 0, s_main_>>>(sig_cons_.p, W, xseq_);
+  check_launch("k_p2p_signal");
+  auto* flags = reinterpret_cast<const uint64_t*>(arena_.p + flags_off_[s_.rank]);
+  k_p2p_wait<<<1, 32 * unsigned(ceil_div(W, 32)), 0, s_main_>>>(flags + W, W, s_.rank, xseq_,
+                                                                  ctx_->d_err);
+  check_launch("k_p2p_wait");
+  launches_ += 2;
+  send_open_ = true;
 }
 
 template <typename T>
@@ -1295,7 +1459,13 @@ void Engine<T>::upload_key_meta(int k) {
           set.push_back(uint16_t(q));
         }
         bits.push_back(m.bits[i]);
-        off.push_back(send_base_[k][p][q] + m.off[i]);
+        const int64_t rq = q / (P_ / s_.world);
+        if (p2p_ && rq != s_.rank)  // straight into the receiver's arena (64-bit wrap)
+          off.push_back(uint64_t(reinterpret_cast<uintptr_t>(peer_arena_[rq])) +
+                        p2p_recv_[k][q][p] + m.off[i] -
+                        uint64_t(reinterpret_cast<uintptr_t>(arena_.p)));
+        else
+          off.push_back(send_base_[k][p][q] + m.off[i]);
       }
     }
     S.q_begin[P_] = int64_t(bits.size());
@@ -1397,6 +1567,7 @@ void Engine<T>::prepare_epoch() {
 // ------------------------------------------------------------ data path ---
 template <typename T>
 void Engine<T>::quantize(PartDev& D, int k, const T* src, int64_t ld, cudaStream_t sq) {
+  if (p2p_ && !send_open_) p2p_begin_send();
   auto& S = D.snd[k];
   if (S.n == 0) return;
   if (!sq) sq = s_main_;
@@ -1436,6 +1607,17 @@ void Engine<T>::decode_halo(int k, int64_t din, int64_t ldi, cudaStream_t st) {
 template <typename T>
 void Engine<T>::exchange(int k) {
   if (zero_copy()) return;  // every pair is on this GPU: zero-copy
+  if (p2p_) {  // the stores are done: tell every peer (no bytes move here)
+    if (!send_open_) p2p_begin_send();
+    ++xseq_;
+    k_p2p_signal<<<1, 32 * unsigned(ceil_div(s_.world, 32)), 0, s_main_>>>(sig_ready_.p,
+                                                                          s_.world, xseq_);
+    check_launch("k_p2p_signal");
+    ++launches_;
+    send_open_ = false;
+    if (s_.overlap == 0) wait_exchange();
+    return;
+  }
   QGNN_CUDA(cudaEventRecord(ev_q_, s_main_));
   QGNN_CUDA(cudaStreamWaitEvent(s_comm_, ev_q_, 0));
   const int64_t ppr = P_ / s_.world;
@@ -1523,6 +1705,14 @@ void Engine<T>::exchange(int k) {
 template <typename T>
 void Engine<T>::wait_exchange() {
   if (zero_copy()) return;
+  if (p2p_) {  // every peer's stores of this exchange have landed here
+    auto* flags = reinterpret_cast<const uint64_t*>(arena_.p + flags_off_[s_.rank]);
+    k_p2p_wait<<<1, 32 * unsigned(ceil_div(s_.world, 32)), 0, s_main_>>>(flags, s_.world, s_.rank,
+                                                                        xseq_, ctx_->d_err);
+    check_launch("k_p2p_wait");
+    ++launches_;
+    return;
+  }
   if (loop_) {
     for (cudaEvent_t e : peer_x_) QGNN_CUDA(cudaStreamWaitEvent(s_main_, e, 0));
     // and for this rank's own outgoing copies: every key's send regions start at
@@ -2090,6 +2280,10 @@ void Engine<T>::launch_epoch() {
     QGNN_CUDA(cudaMemcpyAsync(drop_keys_.p, drop_keys_host_, nloc * L_ * sizeof(uint64_t),
                               cudaMemcpyHostToDevice, s_main_));
   }
+  // peer-store ranks sharing one GPU (loopback tests): the host-side uploads above
+  // synchronize the whole device, so no rank may queue a flag wait of this epoch
+  // until every rank is past them (separate GPUs need no such barrier)
+  if (p2p_ && loop_) loop_->barrier();
   QGNN_CUDA(cudaEventRecord(ev_a_, s_main_));
   const bool graph = graphs_enabled() && epoch_ > 1;
   EpochGraph& graph_ = graphs_[feat_pending_ ? 1 : 0];

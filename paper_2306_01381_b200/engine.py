@@ -90,7 +90,7 @@ class Engine:
         s.layout = (WIRE_REF if dtype == "f64" else WIRE_GPU) if layout is None else layout
         s.rank, s.world, s.device = rank, world, device
         s.overlap = int(overlap)
-        s.transport = {"zero_copy": 0, "nccl": 1}[transport]
+        s.transport = {"zero_copy": 0, "nccl": 1, "p2p": 2}[transport]
         s.kstats = int(kstats)
         s.layer_norm = int(layer_norm)
         s.dropout = float(dropout)

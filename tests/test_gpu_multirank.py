@@ -61,6 +61,39 @@ def test_world_split_is_bit_identical(cuda, world, mode, dtype):
         assert (w == base_w).all()
 
 
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("mode,dtype", [("fixed", "f32"), ("uniform", "f32"), ("fp", "f64"),
+                                        ("adaptive", "f32")])
+def test_peer_store_is_bit_identical(cuda, world, mode, dtype):
+    """Peer-store transport (K1 writes straight into the receivers' arenas, ready /
+    consumed flags instead of exchange copies; SURVEY §8f rank 1 at N > 1): the
+    same bits as one rank, across plan changes (adaptive re-solves every 2 epochs)."""
+    kw = dict(dims=[8, 12, 3], n_parts=4, bit_mode=mode, fixed_bits=4, seed=11, dtype=dtype,
+              period=2)
+    (base_ms, base_w), = _run_world(GRAPH, 1, 5, **kw)
+    res = _run_world(GRAPH, world, 5, transport="p2p", **kw)
+    for ms, w in res:
+        assert [m["train_loss"] for m in ms] == [m["train_loss"] for m in base_ms]
+        assert [m["val_acc"] for m in ms] == [m["val_acc"] for m in base_ms]
+        assert [m["bytes_total"] for m in ms] == [m["bytes_total"] for m in base_ms]
+        assert [m["plan_version"] for m in ms] == [m["plan_version"] for m in base_ms]
+        assert (w == base_w).all()
+
+
+def test_peer_store_planted_graph(cuda):
+    """Peer stores on the production kernels (256-wide fused receive, 8 partitions
+    over 4 ranks) and the planted owner map."""
+    g = generate_planted(20000, 200000, 32, 8, 8, 0.02, gamma=2.8, seed=4)
+    kw = dict(dims=[32, 256, 8], n_parts=8, bit_mode="adaptive", seed=3, period=2,
+              owner=g["owner"])
+    (base_ms, base_w), = _run_world(g, 1, 4, **kw)
+    for world in (2, 4):
+        res = _run_world(g, world, 4, transport="p2p", **kw)
+        for ms, w in res:
+            assert [m["train_loss"] for m in ms] == [m["train_loss"] for m in base_ms]
+            assert (w == base_w).all()
+
+
 def test_world_split_adaptive_matches_reference(cuda):
     """Adaptive re-solves gather trace windows across ranks: same plans, same losses."""
     kw = dict(dims=[8, 12, 3], n_parts=4, bit_mode="adaptive", seed=11, period=5, dtype="f64")
