@@ -80,7 +80,12 @@ def config_dict(n_gpus, args):
             "hidden": w["hidden"], "classes": w["classes"], "partitions": w["parts"],
             "model": model, "cross_frac": w["cross_frac"],
             "parallelism": f"graph-partition dp{n_gpus} ({w['parts'] // n_gpus} partitions/GPU)",
-            "bit_mode": bit_desc(args), "l2": "inputs larger than L2 (no flush)"}
+            "bit_mode": bit_desc(args), "l2": "inputs larger than L2 (no flush)",
+            "transport": {"auto": "zero copy" if n_gpus == 1 else "nccl grouped send/recv",
+                          "nccl": "nccl self send/recv" if n_gpus == 1 else
+                          "nccl grouped send/recv",
+                          "p2p": "peer store (K1 -> receiver arena)"}[
+                              getattr(args, "transport", "auto")]}
 
 
 class ClockSampler:
@@ -260,6 +265,15 @@ def impl_reference(args):
 
 
 # ------------------------------------------------------------------ GPU side ---
+def transport_of(args, world):
+    if args.transport == "p2p":
+        assert world > 1, "--transport p2p needs N > 1 (one GPU is zero copy)"
+        return "p2p"
+    if args.transport == "nccl" and world == 1:
+        return "nccl"
+    return "zero_copy"  # engine default: zero copy on one GPU, NCCL send/recv across GPUs
+
+
 def impl_ours(args):
     rank, world, local = dist_setup()
     import torch
@@ -277,7 +291,8 @@ def impl_ours(args):
                  bit_mode=bit_mode, fixed_bits=args.bits, seed=7, sage=w["sage"],
                  group_size=2000, period=50,
                  theta=1.0 / (900e9 * 8), gamma=2e-5, dtype="f32", owner=g["owner"], rank=rank,
-                 world=world, device=local, nccl_id=nid, kstats=True)
+                 world=world, device=local, nccl_id=nid, kstats=True,
+                 transport=transport_of(args, world))
     t_setup = time.time() - t0
     info = eng.info()
     # production mode: no per-kernel events, the steady-state epoch replays as a
@@ -448,6 +463,11 @@ def main():
                     help="width of --bit-mode fixed")
     ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS),
                     help="BASELINE.json config (4 = the north-star ogbn-products shape)")
+    ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "p2p"],
+                    help="auto: zero copy on one GPU, grouped NCCL send/recv across GPUs; "
+                         "nccl on one GPU: every pair through NCCL self send/recv (the "
+                         "multi-GPU exchange path timed on one device); p2p (N > 1): K1 "
+                         "stores straight into the receivers' arenas over peer memory")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-epochs", type=int, default=2,
                     help="reference arm: full-size epochs timed (min with --steps)")
