@@ -188,23 +188,3 @@ class Engine:
         return {KCLASSES[i]: dict(ms=out[4 * i], launches=int(out[4 * i + 1]),
                                   bytes=out[4 * i + 2], gathered=out[4 * i + 3])
                 for i in range(n)}
-
-
-def smoke_epoch():
-    """Tiny fp32 engine run (2 partitions, quantized 8-bit exchange) on cuda:0."""
-    from oracle import port  # checker only
-    g = generate_planted(2000, 12000, 16, 4, 2, 0.05, seed=3)
-    eng = Engine(g, [16, 32, 32, 4], n_parts=2, bit_mode="fixed", fixed_bits=8, seed=5)
-    m1 = eng.run_epoch()
-    m2 = eng.run_epoch()
-    assert np.isfinite(m1["train_loss"]) and m2["train_loss"] < m1["train_loss"] * 1.5
-    assert m1["bytes_total"] > 0 and m1["msgs_b8"] > 0
-    # initial weights follow GnnModel::init (model.hpp:27-41) exactly
-    eng2 = Engine(g, [16, 32, 32, 4], n_parts=2, bit_mode="fixed", seed=5)
-    w0 = eng2.weights()[0]
-    key = port.stream(5, 0x77, 0)
-    a = np.sqrt(6.0 / 48)
-    exp = np.array([(2.0 * port.draw_double(key, i + 1) - 1.0) * a for i in range(16 * 32)])
-    assert np.allclose(w0.reshape(-1), exp.astype(np.float32))
-    eng.close()
-    eng2.close()
