@@ -21,6 +21,8 @@ enum : int {
   kErrLabel = 8,       // label out of range               -> QGNN_EINVAL   (model.hpp:185)
   kErrProtocol = 16,   // chunk envelope (source, target, plan version) differs from the
                        // receiver's expectation           -> QGNN_EPROTOCOL (engine.hpp:530-541)
+  kErrMissing = 32,    // peer-store flag wait timed out: a payload never arrived
+                       //                                  -> QGNN_EPROTOCOL (engine.hpp:530)
 };
 
 #define QGNN_CUDA(call)                                                                  \

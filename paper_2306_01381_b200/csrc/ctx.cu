@@ -80,6 +80,10 @@ int status_from_error_word(int w, std::string& msg) {
     msg = "loss: label out of range";
     return QGNN_EINVAL;
   }
+  if (w & kErrMissing) {  // a missing payload also explains any decode error after it
+    msg = "exchange: missing payload (peer-store flags not received in time)";
+    return QGNN_EPROTOCOL;
+  }
   if (w & kErrDecode) {
     msg = "message set: chunk disagrees with index";
     return QGNN_EDECODE;

@@ -31,6 +31,7 @@
 #include <mutex>
 #include <memory>
 #include <numeric>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -57,6 +58,8 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
 };
 
 static NcclApi& nccl() {
@@ -83,6 +86,9 @@ static NcclApi& nccl() {
   api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
   api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
   api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  api.CommGetAsyncError =
+      reinterpret_cast<decltype(api.CommGetAsyncError)>(sym("ncclCommGetAsyncError"));
+  api.CommAbort = reinterpret_cast<decltype(api.CommAbort)>(sym("ncclCommAbort"));
   api.h = h;
   return api;
 }
@@ -219,7 +225,8 @@ struct LoopGroup {
 // Peer-store flags.  signal: every prior write of this stream (the K1 stores into
 // peer arenas, or the reads of the receive regions) is ordered before the flag
 // store (kernel boundary + system fence, release at system scope).  wait: acquire
-// at system scope; gives up after 30 s with a ProtocolError instead of hanging.
+// at system scope; gives up after QGNN_P2P_TIMEOUT_MS (30 s) with a ProtocolError
+// ("missing payload") instead of hanging the GPU.
 __global__ void k_p2p_signal(uint64_t* const* __restrict__ dst, int n, uint64_t v) {
   const int i = threadIdx.x;
   if (i >= n || !dst[i]) return;
@@ -227,7 +234,7 @@ __global__ void k_p2p_signal(uint64_t* const* __restrict__ dst, int n, uint64_t 
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst[i]), "l"(v) : "memory");
 }
 __global__ void k_p2p_wait(const uint64_t* __restrict__ flags, int n, int skip, uint64_t v,
-                           int* err) {
+                           uint64_t timeout_ns, int* err) {
   const int i = threadIdx.x;
   if (i >= n || i == skip) return;
   uint64_t t0, t, x;
@@ -236,8 +243,8 @@ __global__ void k_p2p_wait(const uint64_t* __restrict__ flags, int n, int skip, 
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(flags + i) : "memory");
     if (x >= v) break;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 30000000000ull) {
-      atomicOr(err, kErrProtocol);
+    if (t - t0 > timeout_ns) {  // ProtocolError "exchange: missing payload" (engine.hpp:530)
+      atomicOr(err, kErrMissing);
       break;
     }
     __nanosleep(200);
@@ -586,6 +593,7 @@ class Engine final : public EngineBase {
   cudaEvent_t ev_c_ = nullptr, ev_d_ = nullptr;
   std::vector<cudaEvent_t> peer_x_;     // loopback: peers' exchange-done events
   DBuf<double> dloss_;
+  DBuf<uint64_t> dstat_;  // per-rank epoch status, all-gathered in finish_epoch
   DBuf<unsigned long long> dcorr_;
   template <typename X>
   void allgather_dev(X* base, int64_t slice, cudaStream_t s);
@@ -616,9 +624,14 @@ class Engine final : public EngineBase {
   std::vector<std::vector<std::vector<uint64_t>>> p2p_recv_;  // [k][q][p] in q's arena
   std::vector<bool> ipc_opened_;
   DBuf<uint64_t*> sig_ready_, sig_cons_;  // peers' flag words this rank writes
+  void watchdog_wait(cudaEvent_t ev);
   void p2p_layout();
   void p2p_connect();
   void p2p_begin_send();
+  static uint64_t p2p_timeout_ns() {
+    const char* e = std::getenv("QGNN_P2P_TIMEOUT_MS");
+    return uint64_t(e ? std::max(1L, std::atol(e)) : 30000L) * 1000000ull;
+  }
   DBuf<uint8_t> arena_;
   size_t arena_bytes_ = 0;
   std::vector<std::unique_ptr<PartDev>> parts_dev_;
@@ -1424,7 +1437,7 @@ void Engine<T>::p2p_begin_send() {
   check_launch("k_p2p_signal");
   auto* flags = reinterpret_cast<const uint64_t*>(arena_.p + flags_off_[s_.rank]);
   k_p2p_wait<<<1, 32 * unsigned(ceil_div(W, 32)), 0, s_main_>>>(flags + W, W, s_.rank, xseq_,
-                                                                  ctx_->d_err);
+                                                                  p2p_timeout_ns(), ctx_->d_err);
   check_launch("k_p2p_wait");
   launches_ += 2;
   send_open_ = true;
@@ -1610,8 +1623,12 @@ void Engine<T>::exchange(int k) {
   if (p2p_) {  // the stores are done: tell every peer (no bytes move here)
     if (!send_open_) p2p_begin_send();
     ++xseq_;
-    k_p2p_signal<<<1, 32 * unsigned(ceil_div(s_.world, 32)), 0, s_main_>>>(sig_ready_.p,
-                                                                          s_.world, xseq_);
+    // test hook (QGNN_TEST_P2P_DROP=r): rank r never publishes its first exchange
+    const char* de = std::getenv("QGNN_TEST_P2P_DROP");
+    const int drop = de ? std::atoi(de) : -1;
+    if (!(drop == s_.rank && xseq_ == 1))
+      k_p2p_signal<<<1, 32 * unsigned(ceil_div(s_.world, 32)), 0, s_main_>>>(sig_ready_.p,
+                                                                            s_.world, xseq_);
     check_launch("k_p2p_signal");
     ++launches_;
     send_open_ = false;
@@ -1707,8 +1724,8 @@ void Engine<T>::wait_exchange() {
   if (zero_copy()) return;
   if (p2p_) {  // every peer's stores of this exchange have landed here
     auto* flags = reinterpret_cast<const uint64_t*>(arena_.p + flags_off_[s_.rank]);
-    k_p2p_wait<<<1, 32 * unsigned(ceil_div(s_.world, 32)), 0, s_main_>>>(flags, s_.world, s_.rank,
-                                                                        xseq_, ctx_->d_err);
+    k_p2p_wait<<<1, 32 * unsigned(ceil_div(s_.world, 32)), 0, s_main_>>>(
+        flags, s_.world, s_.rank, xseq_, p2p_timeout_ns(), ctx_->d_err);
     check_launch("k_p2p_wait");
     ++launches_;
     return;
@@ -2349,14 +2366,73 @@ void Engine<T>::epoch_body() {
   step();
 }
 
+// Watchdog: wait for the epoch's end event by polling, checking the
+// NCCL communicator's asynchronous error state; after QGNN_WATCHDOG_S (600 s) or on
+// an NCCL error the communicator is aborted (releasing the peers' collectives) and
+// the epoch fails with ProtocolError / NCCL error instead of hanging the process.
+template <typename T>
+void Engine<T>::watchdog_wait(cudaEvent_t ev) {
+  static const double limit_s = [] {
+    const char* e = std::getenv("QGNN_WATCHDOG_S");
+    return e ? std::max(0.001, std::atof(e)) : 600.0;
+  }();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0;; ++spin) {
+    const cudaError_t q = cudaEventQuery(ev);
+    if (q == cudaSuccess) return;
+    if (q != cudaErrorNotReady) QGNN_CUDA(q);
+    if (comm_) {
+      ncclResult_t ar = ncclSuccess;
+      if (nccl().CommGetAsyncError(comm_, &ar) == ncclSuccess && ar != ncclSuccess &&
+          ar != ncclInProgress) {
+        nccl().CommAbort(comm_);
+        comm_ = nullptr;
+        throw Status(QGNN_ENCCL, std::string("watchdog: NCCL error: ") + nccl().GetErrorString(ar));
+      }
+    }
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el > limit_s) {
+      if (comm_) {
+        nccl().CommAbort(comm_);
+        comm_ = nullptr;
+      }
+      throw Status(QGNN_EPROTOCOL, "watchdog: epoch " + std::to_string(epoch_) +
+                                       " did not complete within " + std::to_string(limit_s) + " s");
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
 template <typename T>
 void Engine<T>::finish_epoch(qgnn_epoch_metrics* m) {
   QGNN_REQUIRE(in_flight_, QGNN_EPROTOCOL, "finish_epoch: no epoch in flight");
   in_flight_ = false;
-  QGNN_CUDA(cudaEventSynchronize(ev_b_));
+  watchdog_wait(ev_b_);
   float ms = 0;
   QGNN_CUDA(cudaEventElapsedTime(&ms, ev_a_, ev_b_));
-  QGNN_CALL(qgnn_ctx_check(ctx_, s_main_));
+  // device-detected errors: with world > 1 every rank learns every rank's status
+  // before anyone throws (a lone failing rank would leave its peers waiting in the
+  // loss all-gather and the next exchange)
+  const int st = qgnn_ctx_check(ctx_, s_main_);
+  const std::string st_msg = st ? qgnn_last_error() : "";
+  if (s_.world > 1) {
+    std::vector<uint64_t> all(s_.world, 0);
+    all[s_.rank] = uint64_t(st);
+    if (!dstat_.p) dstat_.alloc(s_.world);
+    QGNN_CUDA(cudaMemcpyAsync(dstat_.p, all.data(), all.size() * sizeof(uint64_t),
+                              cudaMemcpyHostToDevice, s_main_));
+    allgather_dev(dstat_.p, 1, s_main_);
+    QGNN_CUDA(cudaStreamSynchronize(s_main_));
+    QGNN_CUDA(cudaMemcpy(all.data(), dstat_.p, all.size() * sizeof(uint64_t),
+                         cudaMemcpyDeviceToHost));
+    if (st) throw Status(st, st_msg);
+    for (int r = 0; r < s_.world; ++r)
+      if (all[r])
+        throw Status(QGNN_EPROTOCOL, "exchange: peer rank " + std::to_string(r) +
+                                         " failed this epoch (status " + std::to_string(all[r]) + ")");
+  } else if (st) {
+    throw Status(st, st_msg);
+  }
   double kms0[QGNN_K_COUNT];
   for (int c = 0; c < QGNN_K_COUNT; ++c) kms0[c] = kst_[c].ms;
   flush_kstats();

@@ -94,6 +94,43 @@ def test_peer_store_planted_graph(cuda):
             assert (w == base_w).all()
 
 
+def test_peer_store_missing_payload_is_protocol_error(cuda, monkeypatch):
+    """A rank whose stores never get published (fault injection: rank 1 drops its
+    first ready flag) makes its peer's flag wait time out and the epoch fail with
+    ProtocolError "missing payload" (engine.hpp:530) instead of hanging the GPU
+    (both threads return well within the join timeout)."""
+    from paper_2306_01381_b200._lib import ProtocolError
+    monkeypatch.setenv("QGNN_TEST_P2P_DROP", "1")
+    monkeypatch.setenv("QGNN_P2P_TIMEOUT_MS", "300")
+    gid = _GROUP[0]
+    _GROUP[0] += 1
+    nid = loopback_id(gid)
+    errs = [None, None]
+    engines = [None, None]
+
+    def worker(r):
+        try:
+            engines[r] = Engine(GRAPH, dims=[8, 12, 3], n_parts=4, bit_mode="fixed", fixed_bits=8,
+                                seed=11, dtype="f32", rank=r, world=2, nccl_id=nid,
+                                transport="p2p")
+            engines[r].run_epoch()
+        except Exception as e:  # noqa: BLE001 - inspected below
+            errs[r] = e
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    for e in engines:
+        if e is not None:
+            e.close()
+    assert isinstance(errs[0], ProtocolError) and "missing payload" in str(errs[0]), errs
+    # the sender is stalled behind the receiver's late consumed flag: it may time out
+    # too, but only ever with the same ProtocolError
+    assert errs[1] is None or isinstance(errs[1], ProtocolError), errs
+
+
 def test_world_split_adaptive_matches_reference(cuda):
     """Adaptive re-solves gather trace windows across ranks: same plans, same losses."""
     kw = dict(dims=[8, 12, 3], n_parts=4, bit_mode="adaptive", seed=11, period=5, dtype="f64")
