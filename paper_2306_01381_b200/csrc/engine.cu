@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <array>
@@ -254,6 +255,19 @@ __global__ void k_p2p_wait(const uint64_t* __restrict__ flags, int n, int skip, 
 static std::mutex g_loop_mu;
 static std::map<uint64_t, std::shared_ptr<LoopGroup>> g_loops;
 constexpr char kLoopMagic[8] = {'Q', 'G', 'N', 'N', 'L', 'O', 'O', 'P'};
+
+// NVTX phase ranges (SURVEY §5 tracing): host-side ranges around each layer's
+// enqueue, the loss, the step and the adaptive re-solve; header-only NVTX 3, a no-op
+// unless a profiler is attached (inside a replayed CUDA graph they appear only while
+// the graph is captured).
+struct NvtxRange {
+  NvtxRange(const char* what, int64_t idx) {
+    char buf[64];
+    std::snprintf(buf, sizeof(buf), "%s %lld", what, static_cast<long long>(idx));
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // ------------------------------------------------------------ engine ----
 enum BitMode { kFp = 0, kFixed = 1, kUniform = 2, kAdaptive = 3 };
@@ -2350,18 +2364,24 @@ void Engine<T>::launch_epoch() {
 template <typename T>
 void Engine<T>::epoch_body() {
   for (int64_t l = 1; l <= L_; ++l) {
+    NvtxRange r("qgnn fwd layer", l);
     if (l == L_ && tf_last_)
       forward_last_tf(int(l));
     else
       forward_layer(int(l));
   }
-  loss_phase();
+  {
+    NvtxRange r("qgnn loss", 0);
+    loss_phase();
+  }
   for (int64_t l = L_; l >= 2; --l) {
+    NvtxRange r("qgnn bwd layer", l);
     if (l == L_ && tf_last_)
       backward_last_tf(int(l));
     else
       backward_layer(int(l));
   }
+  NvtxRange r("qgnn bwd layer 1 + allreduce/Adam", 1);
   backward_last();
   step();
 }
@@ -2507,6 +2527,7 @@ void Engine<T>::finish_epoch(qgnn_epoch_metrics* m) {
 // gather_stats (engine.hpp:135-165) + reassignment_round (solve.hpp:337-363) + adopt_plan (:851-861)
 template <typename T>
 void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
+  NvtxRange nv("qgnn adaptive re-solve, epoch", int64_t(epoch_));
   if (s_.period <= 0 || epoch_ % uint64_t(s_.period) != 0) return;
   const auto t0 = std::chrono::steady_clock::now();
   // windows of every sender partition (all ranks): key k's lo values of partition p
