@@ -469,7 +469,7 @@ int qgnn_dense_forward(qgnn_ctx* ctx, int dtype, const void* A, int64_t lda, con
     k_dfwd_exact<<<grid1(n_rows * dout, 256), 256, 0, s>>>(
         static_cast<const double*>(A), lda, static_cast<const double*>(W), int(din), int(dout),
         rows, row_begin, n_rows, relu, static_cast<double*>(out), ld_out);
-  } else if (!rows && use_tc_gemm() && dout <= 256 && tma_ok(A, lda, row_begin)) {
+  } else if (!rows && use_tc_gemm() && din <= 4096 && tma_ok(A, lda, row_begin)) {
     tc_gemm_rows(ctx, static_cast<const float*>(A) + row_begin * lda, lda,
                  static_cast<const float*>(W), int(dout), int(dout), int(din), 1, n_rows, relu,
                  static_cast<float*>(out) + row_begin * ld_out, ld_out, s);
@@ -496,7 +496,7 @@ int qgnn_dense_input_grad(qgnn_ctx* ctx, int dtype, const void* A, int64_t lda, 
     k_dgrad_exact<<<grid1(n_rows * din, 256), 256, 0, s>>>(
         static_cast<const double*>(A), lda, static_cast<const double*>(W), int(din), int(dout),
         rows, row_begin, n_rows, static_cast<double*>(out), ld_out);
-  } else if (!rows && use_tc_gemm() && din <= 256 && tma_ok(A, lda, row_begin)) {
+  } else if (!rows && use_tc_gemm() && dout <= 4096 && tma_ok(A, lda, row_begin)) {
     tc_gemm_rows(ctx, static_cast<const float*>(A) + row_begin * lda, lda,
                  static_cast<const float*>(W), int(dout), int(din), int(dout), 0, n_rows, 0,
                  static_cast<float*>(out) + row_begin * ld_out, ld_out, s);
@@ -649,7 +649,7 @@ void input_grad_masked_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const flo
                            int64_t dout, int64_t row_begin, int64_t n_rows, float* out,
                            int64_t ldo, const float* mask, int64_t ldm, cudaStream_t s) {
   if (n_rows == 0) return;
-  if (use_tc_gemm() && din <= 256 && tma_ok(A, lda, row_begin)) {
+  if (use_tc_gemm() && dout <= 4096 && tma_ok(A, lda, row_begin)) {
     tc_gemm_rows(ctx, A + row_begin * lda, lda, W, int(dout), int(din), int(dout), 0, n_rows, 0,
                  out + row_begin * ldo, ldo, s, mask ? mask + row_begin * ldm : nullptr, ldm);
     return;

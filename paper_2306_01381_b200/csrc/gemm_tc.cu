@@ -640,9 +640,33 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo, 
 }  // namespace
 
 // C[rows x N] = A[rows x K] B  with B(n,k) from W (see k_prep_b); relu optional.
+namespace {
+void tc_gemm_block(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int wcols, int N,
+                   int K, int transpose_w, int64_t n_rows, int relu, float* out, int64_t ldo,
+                   cudaStream_t s, const float* mask, int64_t ldm);
+}  // namespace
+
+// Outputs wider than one TMEM tile (N > 256) run as 256-column blocks of B.
 void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int wcols, int N,
                   int K, int transpose_w, int64_t n_rows, int relu, float* out, int64_t ldo,
                   cudaStream_t s, const float* mask, int64_t ldm) {
+  QGNN_REQUIRE(K <= 4096, QGNN_EINVAL, "tc_gemm: K must be <= 4096");
+  int launches = 0;
+  for (int n0 = 0; n0 < N; n0 += 256) {
+    const int nb = std::min(256, N - n0);
+    // B(n, k) = W[k][n] (transpose_w) or W[n][k]: block n0 starts n0 columns / rows in
+    const float* Wb = transpose_w ? W + n0 : W + int64_t(n0) * wcols;
+    tc_gemm_block(ctx, A, lda, Wb, wcols, nb, K, transpose_w, n_rows, relu, out + n0, ldo, s,
+                  mask ? mask + n0 : nullptr, ldm);
+    launches += ctx->last_gemm_launches;
+  }
+  ctx->last_gemm_launches = launches;
+}
+
+namespace {
+void tc_gemm_block(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int wcols, int N,
+                   int K, int transpose_w, int64_t n_rows, int relu, float* out, int64_t ldo,
+                   cudaStream_t s, const float* mask, int64_t ldm) {
   QGNN_REQUIRE(N <= 256 && K <= 4096, QGNN_EINVAL, "tc_gemm: N must be <= 256");
   const int BN = int(round_up(N, 16));
   const int Kp = int(round_up(K, 4));
@@ -693,6 +717,8 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
   p.stages = stages_for(BN, p.mh, bk);
   launch<false>(ta, tb, tbl, p, ctx->num_sms, s);
 }
+
+}  // namespace
 
 // Partial tiles of out[M x N] = A[rows x M]^T B[rows x N], split-K over rows:
 // returns the workspace holding *splits consecutive M x N partial products

@@ -163,6 +163,25 @@ def test_dense_f32_tile_edges(cuda, n, din, dout):
     assert (g[n:] == -3.0).all()
 
 
+@pytest.mark.parametrize("din,dout", [(602, 300), (300, 602), (128, 512)])
+def test_dense_f32_wide_outputs(cuda, din, dout):
+    """Outputs wider than one TMEM tile (N > 256: 602-wide input gradients of the
+    Reddit-shaped first layer, hidden 512) run on the tcgen05 path as 256-column
+    blocks of B: same tolerance as the single-block shapes."""
+    rs = np.random.default_rng(din * 7 + dout)
+    n = 3000
+    a = rs.standard_normal((n, din))
+    w = rs.standard_normal((din, dout)) / np.sqrt(din)
+    f = torch.float32
+    out = torch.zeros((n, dout), dtype=f, device=cuda)
+    ops.dense_forward(_t(a, f), _t(w, f), out, relu=True)
+    assert np.allclose(out.cpu().numpy(), np.maximum(a @ w, 0), rtol=1e-4, atol=1e-4)
+    dz = rs.standard_normal((n, dout))
+    ig = torch.zeros((n, din), dtype=f, device=cuda)
+    ops.dense_input_grad(_t(dz, f), _t(w, f), ig)
+    assert np.allclose(ig.cpu().numpy(), dz @ w.T, rtol=1e-4, atol=1e-4)
+
+
 def test_dense_row_subsets(cuda):
     rs = np.random.default_rng(3)
     n, din, dout = 1000, 64, 48
