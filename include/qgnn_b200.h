@@ -257,6 +257,30 @@ int qgnn_agg_view_build_gpu(const int64_t* adj_ptr, const int32_t* adj, int64_t 
                             const uint32_t* owner, const qgnn_partition* part, int sage,
                             int device, qgnn_agg_view** out);
 
+/* load_dataset (cli/synth.hpp:184-205) of a dataset directory written by the
+ * reference's save_dataset (edges.txt, features.bin, labels.txt,
+ * {train,val,test}_mask.txt, meta.json; formats graph.hpp:80-200).  The edge list
+ * is parsed on host threads and build_graph's symmetric, deduplicated, sorted CSR
+ * (graph.hpp:59-78) is built on `device` (radix sort of the directed pairs; device
+ * < 0: on the host).  features = the stored f64 matrix, features_f32 = the same
+ * rounded to fp32 (the production engine's input).  Errors: QGNN_EIO (IoError,
+ * same messages), QGNN_EINVAL (edge endpoint out of range, overlapping masks). */
+typedef struct qgnn_dataset qgnn_dataset;
+typedef struct {
+  int64_t nodes, nnz, feature_dim, classes;
+  const int64_t* adj_ptr;       /* [nodes + 1] */
+  const int32_t* adj;           /* [nnz] */
+  const double* features;       /* [nodes x feature_dim] as stored */
+  const float* features_f32;    /* [nodes x feature_dim] */
+  const int32_t* labels;        /* [nodes] */
+  const uint8_t* train;         /* [nodes] */
+  const uint8_t* val;
+  const uint8_t* test;
+} qgnn_dataset_arrays;
+int qgnn_dataset_load(const char* dir, int device, qgnn_dataset** out);
+int qgnn_dataset_arrays_get(const qgnn_dataset* d, qgnn_dataset_arrays* out);
+int qgnn_dataset_destroy(qgnn_dataset* d);
+
 /* BitWidthPlan::Lookup::bits_for (assigner/plan.hpp:60-72) over one
  * (key, src, dst) entry list (ids ascending, bits parallel): out[k] = bits of
  * query[k]; an unknown id fails with QGNN_EINVAL "plan: unknown message id". */

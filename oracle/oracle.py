@@ -269,6 +269,9 @@ class _Ref:
                                               C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
                                               C.c_void_p]
         L.ref_dataset_free.argtypes = [C.c_void_p]
+        L.ref_dataset_save.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_dataset_load.restype = C.c_void_p
+        L.ref_dataset_load.argtypes = [C.c_char_p]
         L.ref_dataset_sizes.argtypes = [C.c_void_p] * 4
         L.ref_dataset_export.argtypes = [C.c_void_p] * 8
         L.ref_view_build.restype = C.c_void_p
@@ -368,6 +371,30 @@ class _Ref:
                          p_inter=0.001, attach_edges=4, same_class_bias=0.8, sep=1.0, seed=1):
         h = self.L.ref_generate_dataset(1 if kind == "cite" else 0, nodes, classes, feature_dim,
                                         p_intra, p_inter, attach_edges, same_class_bias, sep, seed)
+        if not h:
+            raise RefError(1, self.L.ref_last_error().decode())
+        try:
+            return self._export(h)
+        finally:
+            self.L.ref_dataset_free(h)
+
+    def generate_and_save(self, dir, kind="sbm", nodes=1000, classes=4, feature_dim=32,
+                          p_intra=0.01, p_inter=0.001, attach_edges=4, same_class_bias=0.8,
+                          sep=1.0, seed=1):
+        """generate_dataset then the reference's save_dataset (cli/synth.hpp:153-182)."""
+        h = self.L.ref_generate_dataset(1 if kind == "cite" else 0, nodes, classes, feature_dim,
+                                        p_intra, p_inter, attach_edges, same_class_bias, sep, seed)
+        if not h:
+            raise RefError(1, self.L.ref_last_error().decode())
+        try:
+            self._chk(self.L.ref_dataset_save(h, str(dir).encode()))
+            return self._export(h)
+        finally:
+            self.L.ref_dataset_free(h)
+
+    def load_dataset(self, dir):
+        """The reference's load_dataset (cli/synth.hpp:184-205) as arrays."""
+        h = self.L.ref_dataset_load(str(dir).encode())
         if not h:
             raise RefError(1, self.L.ref_last_error().decode())
         try:

@@ -213,6 +213,24 @@ void* ref_generate_dataset(int kind, uint64_t nodes, uint64_t classes, uint64_t 
 
 void ref_dataset_free(void* d) { delete static_cast<RefDataset*>(d); }
 
+// save_dataset / load_dataset (cli/synth.hpp:153-205)
+int ref_dataset_save(void* d, const char* dir) {
+  try {
+    save_dataset(static_cast<RefDataset*>(d)->g, dir);
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+void* ref_dataset_load(const char* dir) {
+  try {
+    return new RefDataset{load_dataset(dir)};
+  } catch (...) {
+    map_exc();
+    return nullptr;
+  }
+}
+
 // sizes: nodes, nnz, feature cols
 void ref_dataset_sizes(void* d, uint64_t* nodes, uint64_t* nnz, uint64_t* fdim) {
   const Graph& g = static_cast<RefDataset*>(d)->g;

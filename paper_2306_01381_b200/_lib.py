@@ -99,6 +99,13 @@ class AggViewArrays(C.Structure):
                                            "marginal_rows")]
 
 
+class DatasetArrays(C.Structure):
+    """qgnn_dataset_arrays (include/qgnn_b200.h): load_dataset, cli/synth.hpp:184-205."""
+    _fields_ = [(k, C.c_int64) for k in ("nodes", "nnz", "feature_dim", "classes")] + \
+               [(k, C.c_void_p) for k in ("adj_ptr", "adj", "features", "features_f32",
+                                           "labels", "train", "val", "test")]
+
+
 _SIGS = {
     "qgnn_last_error": (C.c_char_p, []),
     "qgnn_version": (C.c_char_p, []),
@@ -139,6 +146,9 @@ _SIGS = {
                                      C.c_int, C.c_int, C.c_int, vp, vp]),
     "qgnn_partitions_from_owner": (C.c_int, [vp, vp, i64, vp, i64, vp]),
     "qgnn_partitions_from_owner_gpu": (C.c_int, [vp, vp, i64, vp, i64, C.c_int, vp]),
+    "qgnn_dataset_load": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(vp)]),
+    "qgnn_dataset_arrays_get": (C.c_int, [vp, vp]),
+    "qgnn_dataset_destroy": (C.c_int, [vp]),
     "qgnn_agg_view_build_gpu": (C.c_int, [vp, vp, i64, vp, vp, C.c_int, C.c_int, C.POINTER(vp)]),
     "qgnn_partition_list": (C.c_int, [vp, C.c_int, i64, C.POINTER(vp), C.POINTER(i64)]),
     "qgnn_partition_destroy": (C.c_int, [vp]),

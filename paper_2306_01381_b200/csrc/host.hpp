@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <map>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace qgnn_b200 {
@@ -63,6 +64,12 @@ struct View {
   int64_t local_nnz() const { return local_ptr.empty() ? 0 : local_ptr.back(); }
   int64_t remote_nnz() const { return remote_ptr.empty() ? 0 : remote_ptr.back(); }
 };
+
+// build_graph (graph.hpp:59-78): symmetrize, drop self loops, sort and deduplicate
+// every adjacency list.  device >= 0: radix sort of the directed pairs on that GPU
+// (setup.cu); device < 0: on the host.
+void build_graph_csr(int64_t n, const std::vector<std::pair<uint32_t, uint32_t>>& edges,
+                     int device, std::vector<int64_t>& ptr, std::vector<int32_t>& adj);
 
 View build_view(const int64_t* ptr, const int32_t* adj, int64_t n, const Part& part,
                 int64_t n_parts, const std::vector<double>& alpha,

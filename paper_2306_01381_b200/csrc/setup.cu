@@ -9,6 +9,7 @@
 // are identical to host_graph.cpp's builders (tests/test_gpu_setup.py).
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
 
 #include <algorithm>
 #include <cstring>
@@ -209,6 +210,25 @@ __global__ void k_rx_asq(const int64_t* __restrict__ ptr, const int32_t* __restr
   }
 }
 
+// build_graph: both directions of every non-loop edge as (u << 32 | v) keys; loops
+// become the all-ones key, sorted last and dropped
+__global__ void k_edge_keys(const uint2* __restrict__ e, int64_t m, uint64_t* __restrict__ keys) {
+  for (int64_t i = gthread(); i < m; i += nthreads()) {
+    const uint2 uv = e[i];
+    const bool loop = uv.x == uv.y;
+    keys[2 * i] = loop ? ~0ull : (uint64_t(uv.x) << 32 | uv.y);
+    keys[2 * i + 1] = loop ? ~0ull : (uint64_t(uv.y) << 32 | uv.x);
+  }
+}
+__global__ void k_csr_from_keys(const uint64_t* __restrict__ keys, int64_t m,
+                                int64_t* __restrict__ cnt, int32_t* __restrict__ adj) {
+  for (int64_t i = gthread(); i < m; i += nthreads()) {
+    const uint64_t k = keys[i];
+    adj[i] = int32_t(uint32_t(k));
+    atomicAdd(reinterpret_cast<unsigned long long*>(cnt + (k >> 32) + 1), 1ull);
+  }
+}
+
 // counts written at p[1..n] (p[0] = 0) -> inclusive scan in place
 void scan_counts(int64_t* p, int64_t n, cudaStream_t st) {
   if (n <= 0) return;
@@ -230,7 +250,82 @@ std::vector<X> download(const X* p, int64_t n, cudaStream_t st) {
   QGNN_CUDA(cudaStreamSynchronize(st));
   return h;
 }
+
 }  // namespace
+
+void build_graph_csr(int64_t n, const std::vector<std::pair<uint32_t, uint32_t>>& edges,
+                     int device, std::vector<int64_t>& ptr, std::vector<int32_t>& adj) {
+  const int64_t m = int64_t(edges.size());
+  if (device < 0) {  // host: per-node sort + unique, like the reference
+    std::vector<std::vector<int32_t>> lists(size_t(std::max<int64_t>(0, n)));
+    for (const auto& e : edges) {
+      if (e.first == e.second) continue;
+      lists[e.first].push_back(int32_t(e.second));
+      lists[e.second].push_back(int32_t(e.first));
+    }
+    ptr.assign(size_t(n + 1), 0);
+    adj.clear();
+    for (int64_t v = 0; v < n; ++v) {
+      auto& l = lists[size_t(v)];
+      std::sort(l.begin(), l.end());
+      l.erase(std::unique(l.begin(), l.end()), l.end());
+      ptr[size_t(v + 1)] = ptr[size_t(v)] + int64_t(l.size());
+      adj.insert(adj.end(), l.begin(), l.end());
+    }
+    return;
+  }
+  QGNN_CUDA(cudaSetDevice(device));
+  QGNN_REQUIRE(2 * m < (int64_t(1) << 31), QGNN_EINVAL, "dataset: more than 2^30 edges");
+  cudaStream_t st = nullptr;
+  QGNN_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct Guard {
+    cudaStream_t s;
+    ~Guard() { cudaStreamDestroy(s); }
+  } guard{st};
+  DBuf<uint2> e;
+  e.alloc(size_t(std::max<int64_t>(1, m)), false);
+  if (m) QGNN_CUDA(cudaMemcpy(e.p, edges.data(), size_t(m) * sizeof(uint2), cudaMemcpyHostToDevice));
+  DBuf<uint64_t> k0, k1;
+  k0.alloc(size_t(std::max<int64_t>(1, 2 * m)), false);
+  k1.alloc(size_t(std::max<int64_t>(1, 2 * m)), false);
+  int64_t u = 0;
+  if (m) {
+    k_edge_keys<<<grid_for(m), kThreads, 0, st>>>(e.p, m, k0.p);
+    check_launch("k_edge_keys");
+    size_t bytes = 0;
+    QGNN_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, k0.p, k1.p, int(2 * m), 0, 64, st));
+    DBuf<uint8_t> tmp;
+    tmp.alloc(std::max<size_t>(1, bytes), false);
+    QGNN_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, bytes, k0.p, k1.p, int(2 * m), 0, 64, st));
+    DBuf<int> nu;
+    nu.alloc(1, true);
+    size_t b2 = 0;
+    QGNN_CUDA(cub::DeviceSelect::Unique(nullptr, b2, k1.p, k0.p, nu.p, int(2 * m), st));
+    DBuf<uint8_t> tmp2;
+    tmp2.alloc(std::max<size_t>(1, b2), false);
+    QGNN_CUDA(cub::DeviceSelect::Unique(tmp2.p, b2, k1.p, k0.p, nu.p, int(2 * m), st));
+    int nuh = 0;
+    QGNN_CUDA(cudaMemcpyAsync(&nuh, nu.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    QGNN_CUDA(cudaStreamSynchronize(st));
+    u = nuh;
+    if (u > 0) {  // the loop sentinel sorts last
+      uint64_t last = 0;
+      QGNN_CUDA(cudaMemcpy(&last, k0.p + (u - 1), sizeof(uint64_t), cudaMemcpyDeviceToHost));
+      if (last == ~0ull) --u;
+    }
+  }
+  DBuf<int64_t> cnt;
+  cnt.alloc(size_t(n + 1), true);
+  DBuf<int32_t> a;
+  a.alloc(size_t(std::max<int64_t>(1, u)), false);
+  if (u) {
+    k_csr_from_keys<<<grid_for(u), kThreads, 0, st>>>(k0.p, u, cnt.p, a.p);
+    check_launch("k_csr_from_keys");
+    scan_counts(cnt.p, n, st);
+  }
+  ptr = download(cnt.p, n + 1, st);
+  adj = download(a.p, u, st);
+}
 
 GraphDev::GraphDev(const int64_t* ptr_h, const int32_t* adj_h, int64_t n_, const uint32_t* owner_h,
                    int64_t n_parts_, cudaStream_t s)

@@ -56,6 +56,35 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def load_dataset(path, device: Optional[int] = 0) -> dict:
+    """The reference's dataset directory (load_dataset, cli/synth.hpp:184-205) through
+    qgnn_dataset_load: CSR built on `device` (None: on the host), features as fp32
+    (``features``) and as stored (``features_f64``); the dict feeds :class:`Engine`."""
+    h = C.c_void_p()
+    check(lib.qgnn_dataset_load(str(path).encode(), -1 if device is None else int(device),
+                                C.byref(h)))
+    try:
+        a = _lib.DatasetArrays()
+        check(lib.qgnn_dataset_arrays_get(h, C.byref(a)))
+        n, e, f = a.nodes, a.nnz, a.feature_dim
+
+        def arr(p, cnt, ct, dt):
+            if cnt == 0:
+                return np.zeros(0, dt)
+            return np.ctypeslib.as_array(C.cast(p, C.POINTER(ct)), (cnt,)).astype(dt)
+
+        return dict(adj_ptr=arr(a.adj_ptr, n + 1, C.c_int64, np.int64),
+                    adj=arr(a.adj, e, C.c_int32, np.int32),
+                    features=arr(a.features_f32, n * f, C.c_float, np.float32).reshape(n, f),
+                    features_f64=arr(a.features, n * f, C.c_double, np.float64).reshape(n, f),
+                    labels=arr(a.labels, n, C.c_int32, np.int32),
+                    train=arr(a.train, n, C.c_uint8, np.uint8),
+                    val=arr(a.val, n, C.c_uint8, np.uint8),
+                    test=arr(a.test, n, C.c_uint8, np.uint8), classes=int(a.classes))
+    finally:
+        lib.qgnn_dataset_destroy(h)
+
+
 def loopback_id(group: int) -> bytes:
     """Id for the in-process loopback transport (one thread per rank, one GPU)."""
     buf = (C.c_char * 128)()
@@ -97,7 +126,9 @@ class Engine:
         self.settings = s
         self.dims = list(dims)
         self.np_dtype = np.float64 if dtype == "f64" else np.float32
-        feats = np.ascontiguousarray(graph["features"], self.np_dtype)
+        # a loaded dataset carries the stored f64 features next to the fp32 ones
+        src = graph.get("features_f64", graph["features"]) if dtype == "f64" else graph["features"]
+        feats = np.ascontiguousarray(src, self.np_dtype)
         self._keep = dict(
             ptr=np.ascontiguousarray(graph["adj_ptr"], np.int64),
             adj=np.ascontiguousarray(graph["adj"], np.int32), feats=feats,
