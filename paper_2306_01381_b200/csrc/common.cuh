@@ -69,10 +69,17 @@ void dequant_add_masked_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int dim
                             float* out, int64_t ld, const float* mask, int64_t ldm,
                             const uint32_t* expect, cudaStream_t s);
 // fp32 input gradient out = A W^T for rows [row_begin, row_begin + n_rows) with the
-// ReLU-backward mask by h folded into the epilogue (dense.cu)
+// ReLU-backward mask by h folded into the epilogue (dense.cu); mbits (optional): the
+// same mask as 1[h > 0] bit words written by dense_forward_bits_f32 (row pitch ldmb)
 void input_grad_masked_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int64_t din,
                            int64_t dout, int64_t row_begin, int64_t n_rows, float* out,
-                           int64_t ldo, const float* mask, int64_t ldm, cudaStream_t s);
+                           int64_t ldo, const float* mask, int64_t ldm, cudaStream_t s,
+                           const uint32_t* mbits = nullptr, int64_t ldmb = 0);
+// qgnn_dense_forward (fp32, ReLU) that also writes 1[out > 0] as 32-column bit words of
+// each row (row pitch ldb words) when it runs on the tcgen05 path; false: no bits
+bool dense_forward_bits_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W,
+                            int64_t din, int64_t dout, int64_t row_begin, int64_t n_rows,
+                            float* out, int64_t ldo, uint32_t* bits, int64_t ldb, cudaStream_t s);
 // backward scatter-add in one launch: destination rows with their incoming
 // messages in ascending source order, decoded + summed per row (codec.cu)
 void dequant_rows_add_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n_rows, const int32_t* rows,
@@ -120,9 +127,13 @@ namespace qgnn_b200 {
 void* ctx_scratch(qgnn_ctx* ctx, size_t bytes);
 void* ctx_gemm_b(qgnn_ctx* ctx, size_t bytes);
 // tcgen05 GEMMs (gemm_tc.cu)
+// bits_out: with relu, 1[out > 0] of every output row as 32-column words (row pitch
+// ldbo words); bits_in: ReLU-backward mask given as such words instead of `mask`
 void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int wcols, int N,
                   int K, int transpose_w, int64_t n_rows, int relu, float* out, int64_t ldo,
-                  cudaStream_t s, const float* mask = nullptr, int64_t ldm = 0);
+                  cudaStream_t s, const float* mask = nullptr, int64_t ldm = 0,
+                  uint32_t* bits_out = nullptr, int64_t ldbo = 0,
+                  const uint32_t* bits_in = nullptr, int64_t ldbi = 0);
 float* tc_gemm_wgrad_partials(qgnn_ctx* ctx, const float* A, int64_t lda, const float* B,
                               int64_t ldb, int M, int N, int64_t n_rows, int* splits_out,
                               cudaStream_t s);
@@ -191,11 +202,6 @@ void dequant_add_masked_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int dim
                             const uint8_t* bits, const uint64_t* offsets, const int32_t* dst_rows,
                             float* out, int64_t ld, const float* mask, int64_t ldm,
                             const uint32_t* expect, cudaStream_t s);
-// fp32 input gradient out = A W^T for rows [row_begin, row_begin + n_rows) with the
-// ReLU-backward mask by h folded into the epilogue (dense.cu)
-void input_grad_masked_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int64_t din,
-                           int64_t dout, int64_t row_begin, int64_t n_rows, float* out,
-                           int64_t ldo, const float* mask, int64_t ldm, cudaStream_t s);
 // backward scatter-add in one launch: destination rows with their incoming
 // messages in ascending source order, decoded + summed per row (codec.cu)
 void dequant_rows_add_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n_rows, const int32_t* rows,

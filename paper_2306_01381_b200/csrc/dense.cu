@@ -647,11 +647,17 @@ int qgnn_adam_step(qgnn_ctx* ctx, int dtype, void* p, void* m, void* v, const vo
 namespace qgnn_b200 {
 void input_grad_masked_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int64_t din,
                            int64_t dout, int64_t row_begin, int64_t n_rows, float* out,
-                           int64_t ldo, const float* mask, int64_t ldm, cudaStream_t s) {
+                           int64_t ldo, const float* mask, int64_t ldm, cudaStream_t s,
+                           const uint32_t* mbits, int64_t ldmb) {
   if (n_rows == 0) return;
   if (use_tc_gemm() && dout <= 4096 && tma_ok(A, lda, row_begin)) {
-    tc_gemm_rows(ctx, A + row_begin * lda, lda, W, int(dout), int(din), int(dout), 0, n_rows, 0,
-                 out + row_begin * ldo, ldo, s, mask ? mask + row_begin * ldm : nullptr, ldm);
+    if (mask && mbits)  // 32 B of bits per 256-wide row instead of the 1 KB activation row
+      tc_gemm_rows(ctx, A + row_begin * lda, lda, W, int(dout), int(din), int(dout), 0, n_rows,
+                   0, out + row_begin * ldo, ldo, s, nullptr, 0, nullptr, 0,
+                   mbits + row_begin * ldmb, ldmb);
+    else
+      tc_gemm_rows(ctx, A + row_begin * lda, lda, W, int(dout), int(din), int(dout), 0, n_rows,
+                   0, out + row_begin * ldo, ldo, s, mask ? mask + row_begin * ldm : nullptr, ldm);
     return;
   }
   const int st = qgnn_dense_input_grad(ctx, QGNN_F32, A, lda, W, din, dout, nullptr, row_begin,
@@ -662,6 +668,21 @@ void input_grad_masked_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const flo
                                        out, ldo, s);
     if (st2) throw Status(st2, qgnn_last_error());
   }
+}
+
+bool dense_forward_bits_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W,
+                            int64_t din, int64_t dout, int64_t row_begin, int64_t n_rows,
+                            float* out, int64_t ldo, uint32_t* bits, int64_t ldb, cudaStream_t s) {
+  if (n_rows == 0) return true;
+  if (use_tc_gemm() && din <= 4096 && tma_ok(A, lda, row_begin)) {
+    tc_gemm_rows(ctx, A + row_begin * lda, lda, W, int(dout), int(dout), int(din), 1, n_rows, 1,
+                 out + row_begin * ldo, ldo, s, nullptr, 0, bits + row_begin * ldb, ldb);
+    return true;
+  }
+  const int st = qgnn_dense_forward(ctx, QGNN_F32, A, lda, W, din, dout, nullptr, row_begin,
+                                    n_rows, 1, out, ldo, s);
+  if (st) throw Status(st, qgnn_last_error());
+  return false;
 }
 
 void adam_step_devbc(int dtype, void* p, void* m, void* v, const void* g, int64_t n, double lr,

@@ -376,6 +376,11 @@ class Engine final : public EngineBase {
     DBuf<T> halo, partials, dh, dh_next, dz, gbar;
     DBuf<T> gpart;  // transform-first last layer: backward_remote_partials of dz
     DBuf<int32_t> row_node_d;  // GPU row -> node id (feature gather)
+    // 1[h[L-1] > 0] as 32-column bit words, written by layer L-1's forward GEMM and read
+    // as the transform-first last layer's ReLU-backward mask (32 B per 256-wide row
+    // instead of the 1 KB activation row); rows covered this epoch
+    DBuf<uint32_t> hbits;
+    int64_t hbits_rows = 0;
     // per key: sender metadata
     struct SendMeta {
       DBuf<int32_t> rows;
@@ -498,6 +503,11 @@ class Engine final : public EngineBase {
   bool tf_last_ = false;  // last layer aggregates after the transform (fp32, dout < din)
   // fp32 + GPU wire layout: ReLU backward folded into the producers of dh (masked by h)
   bool relu_fused() const { return sizeof(T) == 4 && s_.layout == QGNN_WIRE_GPU && !chain_; }
+  int64_t hbits_ld() const { return ceil_div(dims_[L_ - 1], 32); }  // words per row of hbits
+  static bool mask_bits_enabled() {  // QGNN_MASK_BITS=0: float activation rows as the mask
+    const char* e = std::getenv("QGNN_MASK_BITS");
+    return !e || std::atoi(e) != 0;
+  }
   // LayerNorm / dropout (TrainSettings::layer_norm, dropout; model.hpp:62-153): the
   // transform writes act[t], chain.cu turns it into h[l] and back-propagates
   bool chain_ = false;
@@ -976,6 +986,7 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
     D.dz.alloc(no * maxd);
     D.gbar.alloc(no * maxd);
     if (tf_last_) D.gpart.alloc(std::max<int64_t>(1, nr) * ld_of(dims_[L_]));
+    if (tf_last_ && relu_fused()) D.hbits.alloc(std::max<int64_t>(1, no) * hbits_ld(), false);
     if (chain_) {  // act_in per layer (+ inv_std with LN), GPU -> reference rows for dropout
       D.act.resize(L_);
       D.istd.resize(L_);
@@ -1837,11 +1848,27 @@ void Engine<T>::forward_layer(int l) {
   // layer_forward_rows (model.hpp:90-124) for rows [r0, r0 + n): the GEMM with the
   // ReLU epilogue, or (LayerNorm / dropout) z -> act[t], then the chain -> h[l]
   const bool chain = chain_layer(l);
+  // the mask of the transform-first last layer's backward as bits (hbits)
+  const bool bits = tf_last_ && relu_fused() && l == L_ - 1 && relu && !chain &&
+                    mask_bits_enabled();
+  if constexpr (sizeof(T) == 4)
+    if (bits)
+      for (auto& up : parts_dev_) up->hbits_rows = 0;
   auto transform = [&](PartDev& D, int64_t r0, int64_t n) {
     kbegin(QGNN_K_GEMM_FWD);
-    QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
-                                 nullptr, r0, n, chain ? 0 : relu,
-                                 chain ? D.act[t].p : D.h[l].p, ldo, s_main_));
+    bool done = false;
+    if constexpr (sizeof(T) == 4) {
+      if (bits) {
+        if (dense_forward_bits_f32(ctx_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout, r0, n,
+                                   D.h[l].p, ldo, D.hbits.p, hbits_ld(), s_main_))
+          D.hbits_rows += n;
+        done = true;
+      }
+    }
+    if (!done)
+      QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
+                                   nullptr, r0, n, chain ? 0 : relu,
+                                   chain ? D.act[t].p : D.h[l].p, ldo, s_main_));
     kend(QGNN_K_GEMM_FWD, double(n) * (din + dout) * sizeof(T), s_main_, gemm_nk());
     if (!chain) return;
     kbegin(QGNN_K_ELEMWISE);
@@ -2198,7 +2225,9 @@ void Engine<T>::backward_last_tf(int l) {
     kbegin(QGNN_K_GEMM_DGRAD);
     if constexpr (sizeof(T) == 4)
       input_grad_masked_f32(ctx_, D.gbar.p, ldo, W, din, dout, 0, no, D.dh_next.p, ldi,
-                            mk ? D.h[t].p : nullptr, ldi, s_main_);
+                            mk ? D.h[t].p : nullptr, ldi, s_main_,
+                            mk && D.hbits_rows == no && t == L_ - 1 ? D.hbits.p : nullptr,
+                            hbits_ld());
     else
       QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, D.gbar.p, ldo, W, din, dout, nullptr, 0, no,
                                       D.dh_next.p, ldi, s_main_));

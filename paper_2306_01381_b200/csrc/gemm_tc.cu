@@ -195,6 +195,10 @@ struct Params {
   int dbg;  // QGNN_GEMM_DEBUG bit mask for bottleneck isolation (results invalid when set):
             // 1 = no MMAs, 2 = no output stores, 4 = no lo split, 8 = TMA producer only
   int bk;  // K elements per chunk: 16 (SW64, 64-byte rows) or 32 (SW128, K-major only)
+  uint32_t* bits_out;        // relu: 1[out > 0] as 32-column words per row (pitch ldbo)
+  int64_t ldbo;
+  const uint32_t* bits_in;   // ReLU-backward mask as such words (pitch ldbi), or mask
+  int64_t ldbi;
   int cs;  // K-major: CTAs per cluster sharing each B stage (1, 2, 4).  Rank r loads
            // B rows [r BN/cs, (r+1) BN/cs) once and multicasts them to the cluster; a
            // stage is refilled when every CTA's MMAs have drained it (empty count = cs)
@@ -393,6 +397,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int cc = c0 + 4 * (lane & 7);
         // ReLU-backward mask of this lane's 8 output segments, loaded up front
         float4 mk[8];
+        uint32_t mb[8];  // bits_in: this lane's 4 columns of each of its 8 rows
+        if (p.bits_in) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int row = row0 + 4 * j + (lane >> 3);
+            mb[j] = row < p.M ? (__ldg(p.bits_in + int64_t(row) * p.ldbi + (c0 >> 5)) >>
+                                 (4 * (lane & 7))) : 0xfu;
+          }
+        }
         if (p.mask) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -417,6 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                (uint32_t(32 * q) << 16),
                            r[1]);
         tmem_wait_ld();
+        uint32_t bw = 0;  // bits_out: 1[v > 0] of this thread's row, columns c0 .. c0 + 31
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -429,8 +443,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               v.z = v.z > 0.f ? v.z : 0.f;
               v.w = v.w > 0.f ? v.w : 0.f;
             }
+            bw |= (v.x > 0.f ? 1u : 0u) << (16 * h + i) | (v.y > 0.f ? 2u : 0u) << (16 * h + i) |
+                  (v.z > 0.f ? 4u : 0u) << (16 * h + i) | (v.w > 0.f ? 8u : 0u) << (16 * h + i);
             st_shared4(st_s + 4u * uint32_t(lane * 36 + 16 * h + i), v);
           }
+        if (p.bits_out && row0 + lane < p.M && !(p.dbg & 2))
+          p.bits_out[int64_t(row0 + lane) * p.ldbo + (c0 >> 5)] = bw;
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -443,6 +461,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             v.y = mk[j].y > 0.f ? v.y : 0.f;
             v.z = mk[j].z > 0.f ? v.z : 0.f;
             v.w = mk[j].w > 0.f ? v.w : 0.f;
+          }
+          if (p.bits_in) {
+            v.x = (mb[j] & 1u) ? v.x : 0.f;
+            v.y = (mb[j] & 2u) ? v.y : 0.f;
+            v.z = (mb[j] & 4u) ? v.z : 0.f;
+            v.w = (mb[j] & 8u) ? v.w : 0.f;
           }
           if (p.dbg & 2) continue;
           float* o = out_base + int64_t(row) * p.ldo + cc;
@@ -643,13 +667,15 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo, 
 namespace {
 void tc_gemm_block(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int wcols, int N,
                    int K, int transpose_w, int64_t n_rows, int relu, float* out, int64_t ldo,
-                   cudaStream_t s, const float* mask, int64_t ldm);
+                   cudaStream_t s, const float* mask, int64_t ldm, uint32_t* bits_out,
+                   int64_t ldbo, const uint32_t* bits_in, int64_t ldbi);
 }  // namespace
 
 // Outputs wider than one TMEM tile (N > 256) run as 256-column blocks of B.
 void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int wcols, int N,
                   int K, int transpose_w, int64_t n_rows, int relu, float* out, int64_t ldo,
-                  cudaStream_t s, const float* mask, int64_t ldm) {
+                  cudaStream_t s, const float* mask, int64_t ldm, uint32_t* bits_out,
+                  int64_t ldbo, const uint32_t* bits_in, int64_t ldbi) {
   QGNN_REQUIRE(K <= 4096, QGNN_EINVAL, "tc_gemm: K must be <= 4096");
   int launches = 0;
   for (int n0 = 0; n0 < N; n0 += 256) {
@@ -657,7 +683,8 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
     // B(n, k) = W[k][n] (transpose_w) or W[n][k]: block n0 starts n0 columns / rows in
     const float* Wb = transpose_w ? W + n0 : W + int64_t(n0) * wcols;
     tc_gemm_block(ctx, A, lda, Wb, wcols, nb, K, transpose_w, n_rows, relu, out + n0, ldo, s,
-                  mask ? mask + n0 : nullptr, ldm);
+                  mask ? mask + n0 : nullptr, ldm, bits_out ? bits_out + n0 / 32 : nullptr, ldbo,
+                  bits_in ? bits_in + n0 / 32 : nullptr, ldbi);
     launches += ctx->last_gemm_launches;
   }
   ctx->last_gemm_launches = launches;
@@ -666,7 +693,8 @@ void tc_gemm_rows(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, in
 namespace {
 void tc_gemm_block(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, int wcols, int N,
                    int K, int transpose_w, int64_t n_rows, int relu, float* out, int64_t ldo,
-                   cudaStream_t s, const float* mask, int64_t ldm) {
+                   cudaStream_t s, const float* mask, int64_t ldm, uint32_t* bits_out,
+                   int64_t ldbo, const uint32_t* bits_in, int64_t ldbi) {
   QGNN_REQUIRE(N <= 256 && K <= 4096, QGNN_EINVAL, "tc_gemm: N must be <= 256");
   const int BN = int(round_up(N, 16));
   const int Kp = int(round_up(K, 4));
@@ -709,6 +737,10 @@ void tc_gemm_block(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, i
   p.relu = relu;
   p.mask = mask;
   p.ldm = ldm;
+  p.bits_out = relu ? bits_out : nullptr;
+  p.ldbo = ldbo;
+  p.bits_in = bits_in;
+  p.ldbi = ldbi;
   p.mh = m256 ? 2 : 1;
   p.m_tiles = int(ceil_div(n_rows, tc::kBM * p.mh));
   p.cs = cs;

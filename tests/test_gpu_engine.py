@@ -164,6 +164,28 @@ def test_side_stream_is_identical(cuda, monkeypatch, graph):
     assert (wa == wb).all()
 
 
+@pytest.mark.parametrize("dims", [[8, 12, 3], [8, 40, 300, 3]])
+def test_mask_bits_is_identical(cuda, monkeypatch, dims):
+    """The transform-first last layer's ReLU-backward mask read as 1[h > 0] bit words
+    written by the previous layer's GEMM epilogue (QGNN_MASK_BITS=1, default) gives
+    bit-identical training to reading the activation rows (=0); 300 columns span two
+    256-column GEMM blocks and a partial bit word."""
+    def run():
+        eng = Engine(GRAPH, dims, n_parts=4, bit_mode="fixed", fixed_bits=8, seed=11,
+                     dtype="f32")
+        out = [eng.run_epoch()["train_loss"] for _ in range(3)]
+        w = np.concatenate([x.reshape(-1) for x in eng.weights()])
+        eng.close()
+        return out, w
+
+    monkeypatch.setenv("QGNN_MASK_BITS", "0")
+    a, wa = run()
+    monkeypatch.setenv("QGNN_MASK_BITS", "1")
+    b, wb = run()
+    assert a == b
+    assert (wa == wb).all()
+
+
 def test_merged_forward_gemm_is_identical(cuda, monkeypatch):
     """One forward GEMM per partition over central + marginal rows (QGNN_MERGE_GEMM=1,
     one GPU) gives bit-identical training to separate central / marginal GEMMs."""
