@@ -940,9 +940,14 @@ __global__ void __launch_bounds__(256) k_dequant_f32(
   const int nchunk = (dim + 3) >> 2;
   if (b == 0) {
     const float* src = reinterpret_cast<const float*>(chunk);
-    const float* hm = mask ? mask + (dst_rows ? static_cast<int64_t>(dst_rows[m]) : m) * ldm : nullptr;
+    const int64_t mr = dst_rows ? static_cast<int64_t>(dst_rows[m]) : m;
     for (int j = lane; j < dim; j += 32) {
-      const float v = hm && !(hm[j] > 0.f) ? 0.f : src[j];
+      bool keep = true;
+      if (mask)
+        keep = ldm < 0 ? ((__ldg(reinterpret_cast<const uint32_t*>(mask) + mr * (-ldm) + (j >> 5)) >>
+                           (j & 31)) & 1u) != 0
+                       : mask[mr * ldm + j] > 0.f;
+      const float v = keep ? src[j] : 0.f;
       dst[j] = accumulate ? dst[j] + v : v;
     }
     continue;
@@ -971,12 +976,12 @@ __global__ void __launch_bounds__(256) k_dequant_f32(
 #pragma unroll
     for (int q = 0; q < 4; ++q) r[q] = fmaf(static_cast<float>((word >> (q * b)) & cmask), sc, zp);
     if (mask) {  // ReLU backward folded into the scatter-add (see spmm.cu:relu_mask4)
-      const float4 hm = __ldg(reinterpret_cast<const float4*>(
-          mask + (dst_rows ? static_cast<int64_t>(dst_rows[m]) : m) * ldm + 4 * c));
-      r[0] = hm.x > 0.f ? r[0] : 0.f;
-      r[1] = hm.y > 0.f ? r[1] : 0.f;
-      r[2] = hm.z > 0.f ? r[2] : 0.f;
-      r[3] = hm.w > 0.f ? r[3] : 0.f;
+      const uint32_t mb =
+          relu_bits4(mask, ldm, dst_rows ? static_cast<int64_t>(dst_rows[m]) : m, 4 * c);
+      r[0] = (mb & 1u) ? r[0] : 0.f;
+      r[1] = (mb & 2u) ? r[1] : 0.f;
+      r[2] = (mb & 4u) ? r[2] : 0.f;
+      r[3] = (mb & 8u) ? r[3] : 0.f;
     }
     if (4 * c + 3 < dim) {
       float4* d4 = reinterpret_cast<float4*>(dst) + c;
@@ -1250,13 +1255,7 @@ __global__ void __launch_bounds__(256) k_dequant_rows_f32(
     const int c = cbase + lane + 32 * i;
     if (c >= nchunk) continue;
     float4 a = acc[i];
-    if (mask) {
-      const float4 hm = __ldg(reinterpret_cast<const float4*>(mask + r * ldm + 4 * c));
-      a.x = hm.x > 0.f ? a.x : 0.f;
-      a.y = hm.y > 0.f ? a.y : 0.f;
-      a.z = hm.z > 0.f ? a.z : 0.f;
-      a.w = hm.w > 0.f ? a.w : 0.f;
-    }
+    if (mask) a = apply_bits4(a, relu_bits4(mask, ldm, r, 4 * c));
     float* o = out + r * ld + 4 * c;
     if (4 * c + 3 < dim) {
       float4 p = *reinterpret_cast<float4*>(o);

@@ -61,6 +61,24 @@ struct Arith<float> {
   __device__ __forceinline__ static float mul(float a, float x) { return a * x; }
 };
 
+// ReLU-backward mask of the 4 columns [c, c + 4) of row r as bits 0..3: the
+// activation row itself (ldm > 0 floats per row: h > 0) or 1[h > 0] bit words
+// written by the forward GEMM epilogue (ldm < 0: -ldm 32-bit words per row, the
+// pointer reinterpreted) -- 32 B instead of 1 KB per 256-wide row.
+__device__ __forceinline__ uint32_t relu_bits4(const float* __restrict__ m, int64_t ldm, int64_t r,
+                                               int64_t c) {
+  if (ldm < 0)
+    return (__ldg(reinterpret_cast<const uint32_t*>(m) + r * (-ldm) + (c >> 5)) >> (c & 31)) &
+           0xfu;
+  const float4 h = __ldg(reinterpret_cast<const float4*>(m + r * ldm + c));
+  return (h.x > 0.f ? 1u : 0u) | (h.y > 0.f ? 2u : 0u) | (h.z > 0.f ? 4u : 0u) |
+         (h.w > 0.f ? 8u : 0u);
+}
+__device__ __forceinline__ float4 apply_bits4(float4 v, uint32_t b) {
+  return make_float4((b & 1u) ? v.x : 0.f, (b & 2u) ? v.y : 0.f, (b & 4u) ? v.z : 0.f,
+                     (b & 8u) ? v.w : 0.f);
+}
+
 struct Ctx;  // defined in ctx.cu
 
 // fp32 GPU-layout decode + scatter-add, ReLU-backward mask by h (codec.cu)

@@ -376,11 +376,11 @@ class Engine final : public EngineBase {
     DBuf<T> halo, partials, dh, dh_next, dz, gbar;
     DBuf<T> gpart;  // transform-first last layer: backward_remote_partials of dz
     DBuf<int32_t> row_node_d;  // GPU row -> node id (feature gather)
-    // 1[h[L-1] > 0] as 32-column bit words, written by layer L-1's forward GEMM and read
-    // as the transform-first last layer's ReLU-backward mask (32 B per 256-wide row
-    // instead of the 1 KB activation row); rows covered this epoch
-    DBuf<uint32_t> hbits;
-    int64_t hbits_rows = 0;
+    // 1[h[l] > 0] as 32-column bit words per hidden layer l, written by layer l's
+    // forward GEMM epilogue and read as layer l + 1's ReLU-backward mask (32 B per
+    // 256-wide row instead of the 1 KB activation row); rows covered this epoch
+    std::vector<DBuf<uint32_t>> hbits;
+    std::vector<int64_t> hbits_rows;
     // per key: sender metadata
     struct SendMeta {
       DBuf<int32_t> rows;
@@ -503,7 +503,14 @@ class Engine final : public EngineBase {
   bool tf_last_ = false;  // last layer aggregates after the transform (fp32, dout < din)
   // fp32 + GPU wire layout: ReLU backward folded into the producers of dh (masked by h)
   bool relu_fused() const { return sizeof(T) == 4 && s_.layout == QGNN_WIRE_GPU && !chain_; }
-  int64_t hbits_ld() const { return ceil_div(dims_[L_ - 1], 32); }  // words per row of hbits
+  int64_t hbits_ld(int64_t l) const { return ceil_div(dims_[l], 32); }  // words per row
+  // layer t's ReLU-backward mask: its bit words when this epoch's forward wrote them
+  // for every row (ldm < 0 selects them in the kernels), else the activation rows
+  std::pair<const T*, int64_t> relu_mask(PartDev& D, int64_t t, int64_t ldi) {
+    if (!D.hbits.empty() && D.hbits_rows[t] == D.view.num_owned)
+      return {reinterpret_cast<const T*>(D.hbits[t].p), -hbits_ld(t)};
+    return {D.h[t].p, ldi};
+  }
   static bool mask_bits_enabled() {  // QGNN_MASK_BITS=0: float activation rows as the mask
     const char* e = std::getenv("QGNN_MASK_BITS");
     return !e || std::atoi(e) != 0;
@@ -538,7 +545,8 @@ class Engine final : public EngineBase {
   // bwd_finish scatter-add (engine.hpp:718-738) of every received partial into dh_next.
   // fp32 + GPU layout: one launch, warp per destination row summing its messages
   // in ascending source order; otherwise one exact-order launch per source.
-  void scatter_add_all(PartDev& D, int k, int64_t din, int64_t ldi, const T* mask) {
+  void scatter_add_all(PartDev& D, int k, int64_t din, int64_t ldi, const T* mask,
+                       int64_t ldm) {
     auto& R = D.rcv[k];
     if (!R.n) return;
     double wire = 0;
@@ -548,7 +556,7 @@ class Engine final : public EngineBase {
       if (s_.layout == QGNN_WIRE_GPU) {
         kbegin(QGNN_K_DEQUANT);
         dequant_rows_add_f32(ctx_, arena_.p, R.n_acc_rows, R.acc_rows.p, R.acc_ptr.p, R.acc_msg.p,
-                             int(din), R.bits.p, R.off.p, D.dh_next.p, ldi, mask, ldi, R.env.p,
+                             int(din), R.bits.p, R.off.p, D.dh_next.p, ldi, mask, ldm, R.env.p,
                              s_main_);
         kend(QGNN_K_DEQUANT, double(R.n_acc_rows) * 2 * din * sizeof(T) + double(R.n) * 13 + wire,
              s_main_);
@@ -559,18 +567,19 @@ class Engine final : public EngineBase {
       const int64_t b = R.p_begin[src], e = R.p_begin[src + 1];
       if (e == b) continue;
       kbegin(QGNN_K_DEQUANT);
-      dequant_add(D, R, b, e, din, ldi, mask);
+      dequant_add(D, R, b, e, din, ldi, mask, ldm);
       kend(QGNN_K_DEQUANT, double(e - b) * (2 * din * sizeof(T) + 13) +
                                double(msgs_[k][src][D.id].bytes), s_main_);
     }
   }
   // ascending-source scatter-add of decoded rows [b, e) of R into dh_next (mask: fp32 ReLU bwd)
   template <typename R_>
-  void dequant_add(PartDev& D, R_& R, int64_t b, int64_t e, int64_t din, int64_t ldi, const T* mask) {
+  void dequant_add(PartDev& D, R_& R, int64_t b, int64_t e, int64_t din, int64_t ldi, const T* mask,
+                   int64_t ldm) {
     if constexpr (sizeof(T) == 4) {
       if (s_.layout == QGNN_WIRE_GPU) {
         dequant_add_masked_f32(ctx_, arena_.p, e - b, int(din), R.bits.p + b, R.off.p + b,
-                               R.dst.p + b, D.dh_next.p, ldi, mask, ldi,
+                               R.dst.p + b, D.dh_next.p, ldi, mask, ldm,
                                R.env.p ? R.env.p + b : nullptr, s_main_);
         return;
       }
@@ -986,7 +995,11 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
     D.dz.alloc(no * maxd);
     D.gbar.alloc(no * maxd);
     if (tf_last_) D.gpart.alloc(std::max<int64_t>(1, nr) * ld_of(dims_[L_]));
-    if (tf_last_ && relu_fused()) D.hbits.alloc(std::max<int64_t>(1, no) * hbits_ld(), false);
+    if (relu_fused() && mask_bits_enabled()) {
+      D.hbits.resize(L_);
+      D.hbits_rows.assign(L_, 0);
+      for (int64_t l = 1; l < L_; ++l) D.hbits[l].alloc(std::max<int64_t>(1, no) * hbits_ld(l), false);
+    }
     if (chain_) {  // act_in per layer (+ inv_std with LN), GPU -> reference rows for dropout
       D.act.resize(L_);
       D.istd.resize(L_);
@@ -1848,20 +1861,19 @@ void Engine<T>::forward_layer(int l) {
   // layer_forward_rows (model.hpp:90-124) for rows [r0, r0 + n): the GEMM with the
   // ReLU epilogue, or (LayerNorm / dropout) z -> act[t], then the chain -> h[l]
   const bool chain = chain_layer(l);
-  // the mask of the transform-first last layer's backward as bits (hbits)
-  const bool bits = tf_last_ && relu_fused() && l == L_ - 1 && relu && !chain &&
-                    mask_bits_enabled();
+  // the next layer's ReLU-backward mask as bits (hbits)
+  const bool bits = relu_fused() && l < L_ && relu && !chain && mask_bits_enabled();
   if constexpr (sizeof(T) == 4)
     if (bits)
-      for (auto& up : parts_dev_) up->hbits_rows = 0;
+      for (auto& up : parts_dev_) up->hbits_rows[l] = 0;
   auto transform = [&](PartDev& D, int64_t r0, int64_t n) {
     kbegin(QGNN_K_GEMM_FWD);
     bool done = false;
     if constexpr (sizeof(T) == 4) {
       if (bits) {
         if (dense_forward_bits_f32(ctx_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout, r0, n,
-                                   D.h[l].p, ldo, D.hbits.p, hbits_ld(), s_main_))
-          D.hbits_rows += n;
+                                   D.h[l].p, ldo, D.hbits[l].p, hbits_ld(l), s_main_))
+          D.hbits_rows[l] += n;
         done = true;
       }
     }
@@ -2071,7 +2083,8 @@ void Engine<T>::backward_layer(int l) {
     kbegin(QGNN_K_SPMM_BWD);
     const int nk = spmm(din, D.gbar.p, ldi, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
                         D.labwd.p, nullptr, nullptr, nullptr, 0, no, D.dh_next.p, ldi, &D.hub_bwd.plan,
-                        mk ? D.h[t].p : nullptr, ldi);
+                        mk ? relu_mask(D, t, ldi).first : nullptr,
+                        mk ? relu_mask(D, t, ldi).second : 0);
     kend(QGNN_K_SPMM_BWD, no * (16.0 + (mk ? 2 : 1) * din * sizeof(T)) +
                               double(D.view.local_nnz()) * (4 + sizeof(T)) +
                               double(D.view.src_rows_all) * din * sizeof(T), s_main_, nk,
@@ -2083,7 +2096,8 @@ void Engine<T>::backward_layer(int l) {
     wait_exchange();
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
-    scatter_add_all(D, k, din, ldi, mk ? D.h[t].p : nullptr);
+    scatter_add_all(D, k, din, ldi, mk ? relu_mask(D, t, ldi).first : nullptr,
+                    mk ? relu_mask(D, t, ldi).second : ldi);
     std::swap(D.dh, D.dh_next);
   }
   dh_masked_ = mk;
@@ -2226,8 +2240,8 @@ void Engine<T>::backward_last_tf(int l) {
     if constexpr (sizeof(T) == 4)
       input_grad_masked_f32(ctx_, D.gbar.p, ldo, W, din, dout, 0, no, D.dh_next.p, ldi,
                             mk ? D.h[t].p : nullptr, ldi, s_main_,
-                            mk && D.hbits_rows == no && t == L_ - 1 ? D.hbits.p : nullptr,
-                            hbits_ld());
+                            mk && relu_mask(D, t, ldi).second < 0 ? D.hbits[t].p : nullptr,
+                            mk ? hbits_ld(t) : 0);
     else
       QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, D.gbar.p, ldo, W, din, dout, nullptr, 0, no,
                                       D.dh_next.p, ldi, s_main_));
@@ -2248,7 +2262,8 @@ void Engine<T>::backward_last_tf(int l) {
     wait_exchange();
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
-    scatter_add_all(D, k, din, ldi, mk ? D.h[t].p : nullptr);
+    scatter_add_all(D, k, din, ldi, mk ? relu_mask(D, t, ldi).first : nullptr,
+                    mk ? relu_mask(D, t, ldi).second : ldi);
     std::swap(D.dh, D.dh_next);
   }
   dh_masked_ = mk;

@@ -211,18 +211,7 @@ void launch_csr(int nv, int dim, const T* x, int64_t ldx, const T* y, int64_t ld
 // dh, so every contribution to dh (SpMM rows, decoded remote partials, the
 // transform-first input gradient) can be masked by the layer's activation h
 // before it is stored or added (model.hpp:128-153).
-__device__ __forceinline__ void relu_mask4(float (&v)[4], const float* __restrict__ m) {
-  const float4 h = __ldg(reinterpret_cast<const float4*>(m));
-  v[0] = h.x > 0.f ? v[0] : 0.f;
-  v[1] = h.y > 0.f ? v[1] : 0.f;
-  v[2] = h.z > 0.f ? v[2] : 0.f;
-  v[3] = h.w > 0.f ? v[3] : 0.f;
-}
-__device__ __forceinline__ float4 relu_mask4(float4 v, const float* __restrict__ m) {
-  const float4 h = __ldg(reinterpret_cast<const float4*>(m));
-  return make_float4(h.x > 0.f ? v.x : 0.f, h.y > 0.f ? v.y : 0.f, h.z > 0.f ? v.z : 0.f,
-                     h.w > 0.f ? v.w : 0.f);
-}
+// (common.cuh: relu_bits4 / apply_bits4 read either form of the mask)
 
 // ----------------------------------------------------------------- F32 v2 ---
 // Production fp32 SpMM over a contiguous row range.  Warp w of block b owns
@@ -278,7 +267,11 @@ __global__ void __launch_bounds__(256, (NV <= 2 ? 3 : 1)) k_spmm_f32(
     for (int i = 0; i < NV; ++i) {
       const int cv = lane + 32 * i;
       if (cv >= nvec) continue;
-      if (mask) relu_mask4(acc[i], mask + r * ldm + cv * 4);
+      if (mask) {
+        const uint32_t mb = relu_bits4(mask, ldm, r, cv * 4);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q] = (mb >> q & 1u) ? acc[i][q] : 0.f;
+      }
       vstore<float, 4>(out + r * ldo + cv * 4, acc[i]);
     }
   }
@@ -366,7 +359,7 @@ __global__ void __launch_bounds__(256, 4) k_spmm_f32g(
       o = make_float4(fmaf(sa, xv.x, acc.x), fmaf(sa, xv.y, acc.y), fmaf(sa, xv.z, acc.z),
                       fmaf(sa, xv.w, acc.w));
     }
-    if (mask) o = relu_mask4(o, mask + r * ldm + sub * 4);
+    if (mask) o = apply_bits4(o, relu_bits4(mask, ldm, r, sub * 4));
     *reinterpret_cast<float4*>(out + r * ldo + sub * 4) = o;
   }
 }
@@ -470,7 +463,7 @@ __device__ __noinline__ void hub_finish(bool mine, int64_t u, int sub, int G, in
       const float4 p = __ldcg(reinterpret_cast<const float4*>(part + int64_t(sg) * ldp + c));
       v.x += p.x, v.y += p.y, v.z += p.z, v.w += p.w;
     }
-    if (mask) v = relu_mask4(v, mask + r * ldm + c);
+    if (mask) v = apply_bits4(v, relu_bits4(mask, ldm, r, c));
     *reinterpret_cast<float4*>(out + r * ldo + c) = v;
   }
   if (sub == 0) cnt[h] = 0;
@@ -620,7 +613,7 @@ __global__ void __launch_bounds__(256, MINB) k_spmm_f32g2(
         o = make_float4(fmaf(sa, xv.x, o.x), fmaf(sa, xv.y, o.y), fmaf(sa, xv.z, o.z),
                         fmaf(sa, xv.w, o.w));
       }
-      if (mask) o = relu_mask4(o, mask + r * ldm + c);
+      if (mask) o = apply_bits4(o, relu_bits4(mask, ldm, r, c));
       *reinterpret_cast<float4*>(out + r * ldo + c) = o;
     }
   }
@@ -742,7 +735,7 @@ __global__ void __launch_bounds__(64, MINB) k_spmm_sorted(
       o = make_float4(fmaf(sa, xv.x, o.x), fmaf(sa, xv.y, o.y), fmaf(sa, xv.z, o.z),
                       fmaf(sa, xv.w, o.w));
     }
-    if (mask) o = relu_mask4(o, mask + r * ldm + c);
+    if (mask) o = apply_bits4(o, relu_bits4(mask, ldm, r, c));
     *reinterpret_cast<float4*>(out + r * ldo + c) = o;
   }
 }
@@ -874,7 +867,7 @@ __global__ void __launch_bounds__(64, MINB) k_spmm_wide(
       o = make_float4(fmaf(sa, xv.x, o.x), fmaf(sa, xv.y, o.y), fmaf(sa, xv.z, o.z),
                       fmaf(sa, xv.w, o.w));
     }
-    if (mask) o = relu_mask4(o, mask + r * ldm + c);
+    if (mask) o = apply_bits4(o, relu_bits4(mask, ldm, r, c));
     *reinterpret_cast<float4*>(out + r * ldo + c) = o;
   }
 }
@@ -971,7 +964,7 @@ __global__ void __launch_bounds__(64, 16) k_spmm_wide_half(
       o = make_float4(fmaf(sa, xv.x, o.x), fmaf(sa, xv.y, o.y), fmaf(sa, xv.z, o.z),
                       fmaf(sa, xv.w, o.w));
     }
-    if (mask) o = relu_mask4(o, mask + r * ldm + c);
+    if (mask) o = apply_bits4(o, relu_bits4(mask, ldm, r, c));
     *reinterpret_cast<float4*>(out + r * ldo + c) = o;
   }
 }
@@ -1063,7 +1056,7 @@ __global__ void __launch_bounds__(256) k_spmm_hubred(
       const float4 p = *reinterpret_cast<const float4*>(part + int64_t(s) * ldp + c);
       v.x += p.x, v.y += p.y, v.z += p.z, v.w += p.w;
     }
-    if (mask) v = relu_mask4(v, mask + r * ldm + c);
+    if (mask) v = apply_bits4(v, relu_bits4(mask, ldm, r, c));
     *reinterpret_cast<float4*>(out + r * ldo + c) = v;
   }
 }

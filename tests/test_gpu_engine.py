@@ -164,12 +164,13 @@ def test_side_stream_is_identical(cuda, monkeypatch, graph):
     assert (wa == wb).all()
 
 
-@pytest.mark.parametrize("dims", [[8, 12, 3], [8, 40, 300, 3]])
+@pytest.mark.parametrize("dims", [[8, 12, 3], [8, 40, 300, 3], [8, 36, 44, 12]])
 def test_mask_bits_is_identical(cuda, monkeypatch, dims):
-    """The transform-first last layer's ReLU-backward mask read as 1[h > 0] bit words
-    written by the previous layer's GEMM epilogue (QGNN_MASK_BITS=1, default) gives
-    bit-identical training to reading the activation rows (=0); 300 columns span two
-    256-column GEMM blocks and a partial bit word."""
+    """The ReLU-backward masks read as 1[h > 0] bit words written by each hidden
+    layer's GEMM epilogue (QGNN_MASK_BITS=1, default: SpMM backward, scatter-add and
+    the transform-first input gradient) give bit-identical training to reading the
+    activation rows (=0); 300 columns span two 256-column GEMM blocks and a partial
+    bit word, [8, 36, 44, 12] has no transform-first layer."""
     def run():
         eng = Engine(GRAPH, dims, n_parts=4, bit_mode="fixed", fixed_bits=8, seed=11,
                      dtype="f32")
