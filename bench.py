@@ -66,6 +66,15 @@ def peaks():
         return 6650.0, 1590.0, "fallback"
 
 
+def bf16_burst():
+    """Dense bf16 TF/s measured on this pool (burst: a kernel timed alone)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"])
+    except Exception:
+        return 2250.0
+
+
 def bit_desc(args):
     return f"fixed:{args.bits}" if args.bit_mode == "fixed" else args.bit_mode
 
@@ -387,7 +396,12 @@ def impl_ours(args):
         e = {"ms_per_epoch": v["ms"] / n_prof, "launches_per_epoch": v["launches"] / n_prof,
              "gbs": v["bytes"] / (v["ms"] / 1e3) / 1e9}
         e["frac_hbm"] = e["gbs"] / hbm
-        if v.get("gathered"):
+        if v.get("gathered") and k.startswith("gemm"):
+            # GEMM classes carry their tensor work (3 TF32 products per 3xTF32 MMA) in the
+            # fourth stat: rate vs the TF32 dense rate = half the measured bf16 peak
+            e["tensor_tflops"] = v["gathered"] / (v["ms"] / 1e3) / 1e12
+            e["frac_tf32_peak"] = e["tensor_tflops"] / (bf16_burst() / 2.0)
+        elif v.get("gathered"):
             e["gather_gbs"] = v["gathered"] / (v["ms"] / 1e3) / 1e9
             e["frac_gather_ceiling"] = e["gather_gbs"] / GATHER_CEILING_GBS
         per_class[k] = e

@@ -536,6 +536,11 @@ class Engine final : public EngineBase {
   DBuf<uint64_t> drop_keys_;        // [local parts][L + 1] fork({0x4, epoch, l, device}) keys
   uint64_t* drop_keys_host_ = nullptr;
   bool dh_masked_ = false;  // dh already carries the ReLU-backward mask of its layer
+  // tensor-pipe work of a GEMM over n rows: 2 n din dout per product, three TF32
+  // products (3xTF32) on the fp32 path (reported per GEMM class next to the bytes)
+  double gemm_flops(double n, int64_t din, int64_t dout) const {
+    return 2.0 * n * double(din) * double(dout) * (sizeof(T) == 4 ? 3.0 : 1.0);
+  }
   int gemm_nk() const {  // kernels of the last dense_forward / input_grad call
     return (sizeof(T) == 4 && use_tc_gemm()) ? std::max(1, ctx_->last_gemm_launches) : 1;
   }
@@ -1881,7 +1886,8 @@ void Engine<T>::forward_layer(int l) {
       QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.hagg[t].p, ldi, w_.p + woff_[t], din, dout,
                                    nullptr, r0, n, chain ? 0 : relu,
                                    chain ? D.act[t].p : D.h[l].p, ldo, s_main_));
-    kend(QGNN_K_GEMM_FWD, double(n) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+    kend(QGNN_K_GEMM_FWD, double(n) * (din + dout) * sizeof(T), s_main_, gemm_nk(),
+         gemm_flops(double(n), din, dout));
     if (!chain) return;
     kbegin(QGNN_K_ELEMWISE);
     chain_forward<T>(D.act[t].p, D.act[t].p, ldo, D.h[l].p, ldo,
@@ -2035,7 +2041,8 @@ void Engine<T>::backward_layer(int l) {
     kbegin(QGNN_K_GEMM_DGRAD);
     QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, dz, ldo, W, din, dout, nullptr, nc, nm, D.gbar.p,
                                     ldi, s_main_));
-    kend(QGNN_K_GEMM_DGRAD, double(nm) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+    kend(QGNN_K_GEMM_DGRAD, double(nm) * (din + dout) * sizeof(T), s_main_, gemm_nk(),
+         gemm_flops(double(nm), din, dout));
     if (D.view.num_remote) {
       kbegin(QGNN_K_PARTIALS);
       const int nk = spmm(din, D.gbar.p, ldi, nullptr, 0, nullptr, D.sptr.p, D.srow.p, D.salpha.p,
@@ -2072,14 +2079,15 @@ void Engine<T>::backward_layer(int l) {
     kbegin(QGNN_K_GEMM_DGRAD);
     QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, dz, ldo, W, din, dout, nullptr, 0, nc, D.gbar.p,
                                     ldi, s_main_));
-    kend(QGNN_K_GEMM_DGRAD, double(nc) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+    kend(QGNN_K_GEMM_DGRAD, double(nc) * (din + dout) * sizeof(T), s_main_, gemm_nk(),
+         gemm_flops(double(nc), din, dout));
     kbegin(QGNN_K_GEMM_WGRAD);
     T* wg = wgrad_all_.p + D.id * nparams_ + woff_[t];
     QGNN_CALL(qgnn_dense_weight_grad(ctx_, dtype_, D.hagg[t].p, ldi, dz, ldo, din, dout,
                                      dtype_ == QGNN_F64 ? D.ref_order.p : nullptr, 0, no, 0, wg,
                                      s_main_));
     kend(QGNN_K_GEMM_WGRAD, double(no) * (din + dout) * sizeof(T), s_main_,
-         dtype_ == QGNN_F64 ? 1 : 2);
+         dtype_ == QGNN_F64 ? 1 : 2, gemm_flops(double(no), din, dout));
     kbegin(QGNN_K_SPMM_BWD);
     const int nk = spmm(din, D.gbar.p, ldi, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
                         D.labwd.p, nullptr, nullptr, nullptr, 0, no, D.dh_next.p, ldi, &D.hub_bwd.plan,
@@ -2131,7 +2139,8 @@ void Engine<T>::forward_last_tf(int l) {
     kbegin(QGNN_K_GEMM_FWD);
     QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.h[t].p, ldi, W, din, dout, nullptr, 0, no, 0,
                                  D.dz.p, ldo, s_main_));
-    kend(QGNN_K_GEMM_FWD, double(no) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+    kend(QGNN_K_GEMM_FWD, double(no) * (din + dout) * sizeof(T), s_main_, gemm_nk(),
+         gemm_flops(double(no), din, dout));
     if (!nc) continue;
     kbegin(QGNN_K_SPMM_FWD);
     const int nk = spmm(dout, D.dz.p, ldo, nullptr, 0, D.self_alpha.p, D.lptr.p, D.lcol.p,
@@ -2156,7 +2165,8 @@ void Engine<T>::forward_last_tf(int l) {
       kbegin(QGNN_K_GEMM_FWD);
       QGNN_CALL(qgnn_dense_forward(ctx_, dtype_, D.halo.p, ldi, W, din, dout, nullptr, 0, nr, 0,
                                    D.partials.p, ldo, s_main_));
-      kend(QGNN_K_GEMM_FWD, double(nr) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+      kend(QGNN_K_GEMM_FWD, double(nr) * (din + dout) * sizeof(T), s_main_, gemm_nk(),
+         gemm_flops(double(nr), din, dout));
     }
     kbegin(QGNN_K_SPMM_FWD);
     const int nk = spmm(dout, D.dz.p, ldo, D.partials.p, ldo, D.self_alpha.p, D.lptr.p, D.lcol.p,
@@ -2215,7 +2225,8 @@ void Engine<T>::backward_last_tf(int l) {
       kbegin(QGNN_K_GEMM_DGRAD);
       QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, D.gpart.p, ldo, W, din, dout, nullptr, 0, nr,
                                       D.partials.p, ldi, s_main_));
-      kend(QGNN_K_GEMM_DGRAD, double(nr) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+      kend(QGNN_K_GEMM_DGRAD, double(nr) * (din + dout) * sizeof(T), s_main_, gemm_nk(),
+         gemm_flops(double(nr), din, dout));
     }
     if (!side_overlap()) quantize(D, k, D.partials.p, ldi);
   }
@@ -2245,7 +2256,8 @@ void Engine<T>::backward_last_tf(int l) {
     else
       QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, D.gbar.p, ldo, W, din, dout, nullptr, 0, no,
                                       D.dh_next.p, ldi, s_main_));
-    kend(QGNN_K_GEMM_DGRAD, double(no) * (din + dout) * sizeof(T), s_main_, gemm_nk());
+    kend(QGNN_K_GEMM_DGRAD, double(no) * (din + dout) * sizeof(T), s_main_, gemm_nk(),
+         gemm_flops(double(no), din, dout));
     kbegin(QGNN_K_GEMM_WGRAD);
     T* wg = wgrad_all_.p + D.id * nparams_ + woff_[t];
     QGNN_CALL(qgnn_dense_weight_grad(ctx_, dtype_, D.h[t].p, ldi, D.gbar.p, ldo, din, dout, nullptr,
@@ -2254,7 +2266,7 @@ void Engine<T>::backward_last_tf(int l) {
       QGNN_CALL(qgnn_dense_weight_grad(ctx_, dtype_, D.halo.p, ldi, D.gpart.p, ldo, din, dout,
                                        nullptr, 0, nr, 1, wg, s_main_));
     kend(QGNN_K_GEMM_WGRAD, double(no + nr) * (din + dout) * sizeof(T), s_main_,
-         (dtype_ == QGNN_F64 ? 1 : 2) * (nr ? 2 : 1));
+         (dtype_ == QGNN_F64 ? 1 : 2) * (nr ? 2 : 1), gemm_flops(double(no + nr), din, dout));
   }
   if (side_overlap())
     join_side();
@@ -2298,7 +2310,7 @@ void Engine<T>::backward_last() {
                                      dtype_ == QGNN_F64 ? D.ref_order.p : nullptr, 0, no, 0,
                                      wgrad_all_.p + D.id * nparams_ + woff_[0], s_main_));
     kend(QGNN_K_GEMM_WGRAD, double(no) * (din + dout) * sizeof(T), s_main_,
-         dtype_ == QGNN_F64 ? 1 : 2);
+         dtype_ == QGNN_F64 ? 1 : 2, gemm_flops(double(no), din, dout));
   }
 }
 
