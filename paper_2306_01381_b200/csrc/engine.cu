@@ -2453,10 +2453,14 @@ void Engine<T>::watchdog_wait(cudaEvent_t ev) {
     return e ? std::max(0.001, std::atof(e)) : 600.0;
   }();
   const auto t0 = std::chrono::steady_clock::now();
-  for (int spin = 0;; ++spin) {
+  for (uint64_t spin = 0;; ++spin) {
     const cudaError_t q = cudaEventQuery(ev);
     if (q == cudaSuccess) return;
     if (q != cudaErrorNotReady) QGNN_CUDA(q);
+    if ((spin & 255) != 0) {
+      std::this_thread::yield();
+      continue;
+    }
     if (comm_) {
       ncclResult_t ar = ncclSuccess;
       if (nccl().CommGetAsyncError(comm_, &ar) == ncclSuccess && ar != ncclSuccess &&
@@ -2475,7 +2479,12 @@ void Engine<T>::watchdog_wait(cudaEvent_t ev) {
       throw Status(QGNN_EPROTOCOL, "watchdog: epoch " + std::to_string(epoch_) +
                                        " did not complete within " + std::to_string(limit_s) + " s");
     }
-    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    // spin like cudaEventSynchronize's default (epoch-end latency enters the e2e
+    // wall time); after a second, back off to 100 us naps
+    if (el > 1.0)
+      std::this_thread::sleep_for(std::chrono::microseconds(100));
+    else
+      std::this_thread::yield();
   }
 }
 
