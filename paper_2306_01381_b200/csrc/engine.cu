@@ -477,6 +477,10 @@ class Engine final : public EngineBase {
     const char* e = std::getenv("QGNN_MERGE_GEMM");
     return !e || std::atoi(e) != 0;
   }
+  static bool one_dgrad_enabled() {  // QGNN_ONE_DGRAD=0: split input gradients (A/B only)
+    const char* e = std::getenv("QGNN_ONE_DGRAD");
+    return !e || std::atoi(e) != 0;
+  }
   static bool side_enabled() {
     const char* e = std::getenv("QGNN_SIDE_STREAM");
     return e && std::atoi(e) != 0;
@@ -2023,10 +2027,15 @@ void Engine<T>::backward_layer(int l) {
     kend(QGNN_K_ELEMWISE, double(n) * dout * sizeof(T) * 4, s_main_);
   };
   const T* W = w_.p + woff_[t];
+  // One GPU, in-line schedule (nothing overlaps the exchange): the input gradient of
+  // the central rows runs in the same GEMM launch as the marginal rows' (bit-identical)
+  const bool one_dgrad = zero_copy() && !side_overlap() && merge_gemm_enabled() && !chain &&
+                         !relu && one_dgrad_enabled();
   // bwd_send (engine.hpp:661-688): marginal chain, remote partials, encode
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
     const int64_t nc = D.view.n_central, nm = D.view.n_marginal;
+    const int64_t g0 = one_dgrad ? 0 : nc, gn = one_dgrad ? nc + nm : nm;
     const T* dz = D.dh.p;
     if (chain) {
       chain_bwd(D, nc, nm);
@@ -2039,10 +2048,10 @@ void Engine<T>::backward_layer(int l) {
       dz = D.dz.p;
     }
     kbegin(QGNN_K_GEMM_DGRAD);
-    QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, dz, ldo, W, din, dout, nullptr, nc, nm, D.gbar.p,
+    QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, dz, ldo, W, din, dout, nullptr, g0, gn, D.gbar.p,
                                     ldi, s_main_));
-    kend(QGNN_K_GEMM_DGRAD, double(nm) * (din + dout) * sizeof(T), s_main_, gemm_nk(),
-         gemm_flops(double(nm), din, dout));
+    kend(QGNN_K_GEMM_DGRAD, double(gn) * (din + dout) * sizeof(T), s_main_, gemm_nk(),
+         gemm_flops(double(gn), din, dout));
     if (D.view.num_remote) {
       kbegin(QGNN_K_PARTIALS);
       const int nk = spmm(din, D.gbar.p, ldi, nullptr, 0, nullptr, D.sptr.p, D.srow.p, D.salpha.p,
@@ -2076,11 +2085,13 @@ void Engine<T>::backward_layer(int l) {
       kend(QGNN_K_ELEMWISE, double(nc) * dout * sizeof(T) * 3, s_main_);
       dz = D.dz.p;
     }
-    kbegin(QGNN_K_GEMM_DGRAD);
-    QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, dz, ldo, W, din, dout, nullptr, 0, nc, D.gbar.p,
-                                    ldi, s_main_));
-    kend(QGNN_K_GEMM_DGRAD, double(nc) * (din + dout) * sizeof(T), s_main_, gemm_nk(),
-         gemm_flops(double(nc), din, dout));
+    if (!one_dgrad) {
+      kbegin(QGNN_K_GEMM_DGRAD);
+      QGNN_CALL(qgnn_dense_input_grad(ctx_, dtype_, dz, ldo, W, din, dout, nullptr, 0, nc,
+                                      D.gbar.p, ldi, s_main_));
+      kend(QGNN_K_GEMM_DGRAD, double(nc) * (din + dout) * sizeof(T), s_main_, gemm_nk(),
+           gemm_flops(double(nc), din, dout));
+    }
     kbegin(QGNN_K_GEMM_WGRAD);
     T* wg = wgrad_all_.p + D.id * nparams_ + woff_[t];
     QGNN_CALL(qgnn_dense_weight_grad(ctx_, dtype_, D.hagg[t].p, ldi, dz, ldo, din, dout,

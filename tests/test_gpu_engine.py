@@ -188,8 +188,9 @@ def test_mask_bits_is_identical(cuda, monkeypatch, dims):
 
 
 def test_merged_forward_gemm_is_identical(cuda, monkeypatch):
-    """One forward GEMM per partition over central + marginal rows (QGNN_MERGE_GEMM=1,
-    one GPU) gives bit-identical training to separate central / marginal GEMMs."""
+    """One forward GEMM and one input-gradient GEMM per partition and layer over central
+    + marginal rows (QGNN_MERGE_GEMM=1, one GPU) give bit-identical training to separate
+    central / marginal GEMMs."""
     monkeypatch.setenv("QGNN_MERGE_GEMM", "0")
     a, wa = _run("fixed", 8, 3, "f32")
     monkeypatch.setenv("QGNN_MERGE_GEMM", "1")
