@@ -388,7 +388,7 @@ class Engine final : public EngineBase {
       DBuf<uint8_t> bits;
       DBuf<uint64_t> off;
       DBuf<uint16_t> set;
-      DBuf<uint64_t> keys;  // [P]
+      uint64_t* keys = nullptr;  // [P] view into Engine::keys_all_
       DBuf<T> wlo, whi;
       int64_t n = 0;
       std::vector<int64_t> q_begin;  // [P+1] message ranges per destination
@@ -409,8 +409,8 @@ class Engine final : public EngineBase {
     };
     std::vector<SendMeta> snd;
     std::vector<RecvMeta> rcv;
-    DBuf<double> loss;                  // [1]
-    DBuf<unsigned long long> correct;   // [2]
+    double* loss = nullptr;               // [1] view into Engine::epoch_out_
+    unsigned long long* correct = nullptr;  // [2] view into Engine::epoch_out_
     DBuf<double> ce_terms;
     // hub rows (slots) per SpMM call site, segmented (spmm.cu:k_spmm_hubseg)
     Hubs hub_fc, hub_fm, hub_bwd, hub_part;
@@ -636,6 +636,10 @@ class Engine final : public EngineBase {
   std::vector<cudaEvent_t> peer_x_;     // loopback: peers' exchange-done events
   DBuf<double> dloss_;
   DBuf<uint64_t> dstat_;  // per-rank epoch status, all-gathered in finish_epoch
+  DBuf<uint64_t> keys_all_;      // [key][hosted partition][destination] RNG set keys
+  uint64_t* keys_host_ = nullptr;  // pinned staging of keys_all_
+  DBuf<uint64_t> epoch_out_;     // [hosted partitions] loss (f64 bits), then [2 x] hit counts
+  uint64_t* epoch_out_host_ = nullptr;  // pinned readback of epoch_out_
   DBuf<unsigned long long> dcorr_;
   template <typename X>
   void allgather_dev(X* base, int64_t slice, cudaStream_t s);
@@ -1019,8 +1023,7 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
       }
       if (s_.dropout > 0.0) D.ref_row.upload(V.ref_row);
     }
-    D.loss.alloc(1);
-    D.correct.alloc(2);
+    // loss / hit counts and RNG set keys: views into per-rank buffers (constructor, below)
     D.ce_terms.alloc(std::max<int64_t>(1, D.n_train));
     if constexpr (sizeof(T) == 4) {
       build_hubs(D.hub_fc, V.local_ptr, nullptr, 0, V.n_central, maxd);
@@ -1085,6 +1088,20 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
 
   plan_version_ = s.bit_mode == kAdaptive ? 1 : 0;
   phase("features / weights");
+  {  // per-epoch key uploads and loss / hit-count readbacks: one copy each
+    const size_t np = parts_dev_.size();
+    keys_all_.alloc(std::max<size_t>(1, keys_.size() * np * size_t(P_)), true);
+    QGNN_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&keys_host_),
+                            std::max<size_t>(1, keys_.size() * np * size_t(P_)) * sizeof(uint64_t),
+                            cudaHostAllocDefault));
+    epoch_out_.alloc(std::max<size_t>(1, 3 * np), true);
+    QGNN_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&epoch_out_host_),
+                            std::max<size_t>(1, 3 * np) * sizeof(uint64_t), cudaHostAllocDefault));
+    for (size_t i = 0; i < np; ++i) {
+      parts_dev_[i]->loss = reinterpret_cast<double*>(epoch_out_.p + i);
+      parts_dev_[i]->correct = reinterpret_cast<unsigned long long*>(epoch_out_.p + np + 2 * i);
+    }
+  }
   build_messages();
   if (p2p_) p2p_connect();
   phase("message lists");
@@ -1174,6 +1191,8 @@ Engine<T>::~Engine() {
   if (ev_b_) cudaEventDestroy(ev_b_);
   for (size_t r = 0; r < ipc_opened_.size(); ++r)
     if (ipc_opened_[r]) cudaIpcCloseMemHandle(peer_arena_[r]);
+  if (keys_host_) cudaFreeHost(keys_host_);
+  if (epoch_out_host_) cudaFreeHost(epoch_out_host_);
   if (ev_x_) cudaEventDestroy(ev_x_);
   if (ev_q_) cudaEventDestroy(ev_q_);
   if (s_main_) cudaStreamDestroy(s_main_);
@@ -1534,7 +1553,7 @@ void Engine<T>::upload_key_meta(int k) {
       S.rows.upload(rows);
       S.ids.upload(ids);
       S.set.upload(set);
-      S.keys.alloc(P_);
+      S.keys = keys_all_.p + (size_t(k) * parts_dev_.size() + size_t(p - p0_)) * size_t(P_);
       S.wlo.alloc(std::max<int64_t>(1, S.n), false);
       S.whi.alloc(std::max<int64_t>(1, S.n), false);
       if (S.n)
@@ -1608,19 +1627,23 @@ void Engine<T>::prepare_epoch() {
     arena_layout();
     for (size_t k = 0; k < keys_.size(); ++k) upload_key_meta(int(k));
   }
-  // RNG stream of each encoded set: root.fork({0x2, epoch, key_code, src, dst}) (engine.hpp:497)
-  for (size_t k = 0; k < keys_.size(); ++k)
-    for (auto& up : parts_dev_) {
-      std::vector<uint64_t> ks(P_, 0);
-      for (int64_t q = 0; q < P_; ++q) {
-        uint64_t key = root_;
-        for (uint64_t c : {uint64_t(0x2), epoch_, keys_[k].code, uint64_t(up->id), uint64_t(q)})
-          key = rng_fork(key, c);
-        ks[q] = key;
-      }
-      QGNN_CUDA(cudaMemcpyAsync(up->snd[k].keys.p, ks.data(), P_ * sizeof(uint64_t),
-                                cudaMemcpyHostToDevice, s_main_));
-    }
+  // RNG stream of each encoded set: root.fork({0x2, epoch, key_code, src, dst}) (engine.hpp:497),
+  // every key x hosted partition x destination staged in pinned memory, one copy (the
+  // previous epoch, and with it its copy, has finished: finish_epoch waited for it)
+  {
+    const size_t np = parts_dev_.size();
+    for (size_t k = 0; k < keys_.size(); ++k)
+      for (size_t i = 0; i < np; ++i)
+        for (int64_t q = 0; q < P_; ++q) {
+          uint64_t key = root_;
+          for (uint64_t c : {uint64_t(0x2), epoch_, keys_[k].code, uint64_t(parts_dev_[i]->id),
+                             uint64_t(q)})
+            key = rng_fork(key, c);
+          keys_host_[(k * np + i) * size_t(P_) + size_t(q)] = key;
+        }
+    QGNN_CUDA(cudaMemcpyAsync(keys_all_.p, keys_host_, keys_.size() * np * P_ * sizeof(uint64_t),
+                              cudaMemcpyHostToDevice, s_main_));
+  }
   if (bits_dirty_) recount_bits();  // widths change only with the plan (or per epoch, uniform)
 }
 
@@ -1634,7 +1657,7 @@ void Engine<T>::quantize(PartDev& D, int k, const T* src, int64_t ld, cudaStream
   const int64_t dim = keys_[k].dim;
   kbegin(QGNN_K_QUANT, sq);
   const int st = qgnn_quantize_pack(ctx_, src, dtype_, ld, dim, S.n, S.rows.p, S.ids.p, S.bits.p,
-                                    S.off.p, S.set.p, S.keys.p, s_.layout, arena_.p, S.wlo.p,
+                                    S.off.p, S.set.p, S.keys, s_.layout, arena_.p, S.wlo.p,
                                     S.whi.p, envelope(D.id), sq);
   if (st) throw Status(st, qgnn_last_error());
   // algorithmic bytes: rows read once per message + packed chunks + metadata
@@ -1983,25 +2006,25 @@ void Engine<T>::loss_phase() {
   for (auto& up : parts_dev_) {
     PartDev& D = *up;
     QGNN_CUDA(cudaMemsetAsync(D.dh.p, 0, D.view.num_owned * ldc * sizeof(T), s_main_));
-    QGNN_CUDA(cudaMemsetAsync(D.loss.p, 0, sizeof(double), s_main_));
-    QGNN_CUDA(cudaMemsetAsync(D.correct.p, 0, 2 * sizeof(unsigned long long), s_main_));
+    QGNN_CUDA(cudaMemsetAsync(D.loss, 0, sizeof(double), s_main_));
+    QGNN_CUDA(cudaMemsetAsync(D.correct, 0, 2 * sizeof(unsigned long long), s_main_));
     kbegin(QGNN_K_ELEMWISE);
     if constexpr (sizeof(T) == 4) {
       loss_f32(ctx_, D.h[L_].p, ldc, int(C), D.labels.p, D.loss_rows.p, D.n_train, D.n_val,
-               D.n_test, 1.0 / double(global_train_), D.dh.p, ldc, D.loss.p, D.correct.p, s_main_);
+               D.n_test, 1.0 / double(global_train_), D.dh.p, ldc, D.loss, D.correct, s_main_);
       kend(QGNN_K_ELEMWISE, double(D.view.num_owned) * C * sizeof(T) * 2, s_main_, 2);
       continue;
     }
     if (D.n_train)
       QGNN_CALL(qgnn_masked_ce(ctx_, dtype_, D.h[L_].p, ldc, C, D.labels.p, D.train_rows.p,
-                               D.n_train, 1.0 / double(global_train_), D.dh.p, ldc, D.loss.p,
+                               D.n_train, 1.0 / double(global_train_), D.dh.p, ldc, D.loss,
                                s_main_));
     if (D.n_val)
       QGNN_CALL(qgnn_count_correct(ctx_, dtype_, D.h[L_].p, ldc, C, D.labels.p, D.val_rows.p,
-                                   D.n_val, D.correct.p, s_main_));
+                                   D.n_val, D.correct, s_main_));
     if (D.n_test)
       QGNN_CALL(qgnn_count_correct(ctx_, dtype_, D.h[L_].p, ldc, C, D.labels.p, D.test_rows.p,
-                                   D.n_test, D.correct.p + 1, s_main_));
+                                   D.n_test, D.correct + 1, s_main_));
     kend(QGNN_K_ELEMWISE, double(D.view.num_owned) * C * sizeof(T) * 2, s_main_,
          (D.n_train ? 2 : 0) + (D.n_val ? 1 : 0) + (D.n_test ? 1 : 0));
   }
@@ -2539,10 +2562,16 @@ void Engine<T>::finish_epoch(qgnn_epoch_metrics* m) {
   // loss / accuracy (engine.hpp:393-397, 803-849)
   std::vector<double> loss(P_, 0.0);
   std::vector<unsigned long long> corr(2 * P_, 0);
-  for (auto& up : parts_dev_) {
-    QGNN_CUDA(cudaMemcpy(&loss[up->id], up->loss.p, sizeof(double), cudaMemcpyDeviceToHost));
-    QGNN_CUDA(cudaMemcpy(&corr[2 * up->id], up->correct.p, 2 * sizeof(unsigned long long),
-                         cudaMemcpyDeviceToHost));
+  {  // one readback of every hosted partition's loss and hit counts
+    const size_t np = parts_dev_.size();
+    QGNN_CUDA(cudaMemcpyAsync(epoch_out_host_, epoch_out_.p, 3 * np * sizeof(uint64_t),
+                              cudaMemcpyDeviceToHost, s_main_));
+    QGNN_CUDA(cudaStreamSynchronize(s_main_));
+    for (size_t i = 0; i < np; ++i) {
+      const int id = parts_dev_[i]->id;
+      std::memcpy(&loss[id], epoch_out_host_ + i, sizeof(double));
+      std::memcpy(&corr[2 * id], epoch_out_host_ + np + 2 * i, 2 * sizeof(unsigned long long));
+    }
   }
   if (s_.world > 1) {  // every rank fills its partitions' slots, then all-gather
     if (!dloss_.p) {
