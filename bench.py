@@ -216,9 +216,9 @@ def cpu_baseline_sample(bit_mode, bits=8, div=16, epochs=2):
     nnz: SpMM + dense rows)."""
     g = workload_graph(div)
     per, setup, ep = run_reference_epochs(g, epochs, bit_mode, bits)
-    return {"value": per * div, "unit": "s", "cores": REF_THREADS, "kind": "reference",
-            "sample": f"reference Engine (oracle/_ref, kThreads: {REF_THREADS} partitions = "
-                      f"{REF_THREADS} threads, planted owner map -> partitions_from_owner) on "
+    return {"value": per * div, "unit": "s", "cores": ref_threads(), "kind": "reference",
+            "sample": f"reference Engine (oracle/_ref, kThreads: {ref_threads()} partitions = "
+                      f"{ref_threads()} threads, planted owner map -> partitions_from_owner) on "
                       f"the bench generator scaled 1/{div} ({len(g['adj_ptr']) - 1} nodes, "
                       f"{int(g['adj_ptr'][-1])} CSR nnz); {epochs} epochs, "
                       f"{per:.3f} s/epoch of Engine::run (setup {setup:.2f} s excluded) "
@@ -226,7 +226,8 @@ def cpu_baseline_sample(bit_mode, bits=8, div=16, epochs=2):
             "sample_epoch_s": per, "scale": div, "sample_train_loss": float(ep[-1, 0])}
 
 
-REF_THREADS = 8  # kThreads: one host thread per partition (engine.hpp:356-380)
+def ref_threads():  # kThreads: one host thread per partition (engine.hpp:356-380)
+    return WORKLOAD["parts"]
 
 
 def _peak_rss_gb():
@@ -255,11 +256,11 @@ def impl_reference(args):
             "ms_per_step": value * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference", "config": config_dict(args.gpus, args),
-            "cpu_baseline": {"value": value, "unit": "s", "cores": REF_THREADS,
+            "cpu_baseline": {"value": value, "unit": "s", "cores": ref_threads(),
                              "kind": "reference",
                              "sample": f"full workload ({len(g['adj_ptr']) - 1} nodes, "
                                        f"{int(g['adj_ptr'][-1])} CSR nnz): reference Engine "
-                                       f"(oracle/_ref, kThreads = {REF_THREADS} threads, "
+                                       f"(oracle/_ref, kThreads = {ref_threads()} threads, "
                                        f"partitions_from_owner on the planted owner map), "
                                        f"{k} epoch(s) of Engine::run; setup {setup:.1f} s and "
                                        f"graph generation {t_gen:.1f} s excluded",
