@@ -590,10 +590,10 @@ int gemm_bk() {  // QGNN_GEMM_BK=32: 128-byte K-major rows (SW128) for z = A W /
   return e && std::atoi(e) == 32 ? 32 : 16;
 }
 
-int gemm_cluster() {  // QGNN_GEMM_CLUSTER: CTAs sharing each B stage (1, 2 or 4)
+int gemm_cluster() {  // QGNN_GEMM_CLUSTER: CTAs sharing each B stage (1, 2, 4 or 8)
   const char* e = std::getenv("QGNN_GEMM_CLUSTER");
   const int v = e ? std::atoi(e) : 2;
-  return v == 4 ? 4 : v == 2 ? 2 : 1;
+  return v == 8 ? 8 : v == 4 ? 4 : v == 2 ? 2 : 1;
 }
 
 bool wgrad_m256() {  // QGNN_WGRAD_M256=0: 128-row tiles (A/B)
@@ -647,7 +647,7 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo, 
     cfg.numAttrs = 1;
     // persistent grid = the clusters that are co-resident (GPC sizes need not be
     // multiples of cs, so this can be below num_sms / cs)
-    static int resident[2][5] = {};  // [kMN][cs], per process (one device per engine)
+    static int resident[2][9] = {};  // [kMN][cs], per process (one device per engine)
     int& rc = resident[kMN ? 1 : 0][p.cs];
     if (rc == 0) {
       cfg.gridDim = dim3(unsigned(num_sms / p.cs * p.cs));
