@@ -1268,6 +1268,55 @@ __global__ void __launch_bounds__(256) k_dequant_rows_f32(
   }
 }
 
+// Chunk words for the packed-halo gathers (PackedHalo::direct): offset / 16 and the
+// width code of message idx[e], one word per gather entry, rebuilt with every plan.
+__global__ void k_encode_chunk_words(const int32_t* __restrict__ idx, int64_t n,
+                                     const uint64_t* __restrict__ off,
+                                     const uint8_t* __restrict__ bits, int32_t* __restrict__ out) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t m = idx[e];
+    const int b = bits[m];
+    const uint32_t code = b == 8 ? 3u : b == 4 ? 2u : b == 2 ? 1u : 0u;
+    out[e] = static_cast<int32_t>(static_cast<uint32_t>(off[m] >> 4) | code << 30);
+  }
+}
+void encode_chunk_words(const int32_t* idx, int64_t n, const uint64_t* off, const uint8_t* bits,
+                        int32_t* out, cudaStream_t s) {
+  if (n <= 0) return;
+  k_encode_chunk_words<<<unsigned(std::min<int64_t>(ceil_div(n, 256), 148 * 32)), 256, 0, s>>>(
+      idx, n, off, bits, out);
+  check_launch("k_encode_chunk_words");
+}
+
+// Once per received message: the header's width and count against the index
+// (DecodeError, codec.hpp:82-95) and its envelope against the receiver's
+// expectation (ProtocolError, engine.hpp:530-541) — the checks the slot-indexed
+// gather made per entry.
+__global__ void k_check_chunk_headers(const uint8_t* __restrict__ arena,
+                                      const uint64_t* __restrict__ off,
+                                      const uint8_t* __restrict__ bits,
+                                      const uint32_t* __restrict__ env, int64_t n, int dim,
+                                      int* __restrict__ err) {
+  for (int64_t m = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; m < n;
+       m += int64_t(gridDim.x) * blockDim.x) {
+    const int b = bits[m];
+    if (b == 0) continue;  // raw rows carry no header
+    const uint4 h = __ldg(reinterpret_cast<const uint4*>(arena + off[m]));
+    if (static_cast<int>(h.w & 0xffu) != b || h.z != static_cast<uint32_t>(dim))
+      atomicOr(err, kErrDecode);
+    else if (env && (h.w >> 8) != env[m])
+      atomicOr(err, kErrProtocol);
+  }
+}
+void check_chunk_headers(const uint8_t* arena, const uint64_t* off, const uint8_t* bits,
+                         const uint32_t* env, int64_t n, int dim, int* err, cudaStream_t s) {
+  if (n <= 0) return;
+  k_check_chunk_headers<<<unsigned(std::min<int64_t>(ceil_div(n, 256), 148 * 32)), 256, 0, s>>>(
+      arena, off, bits, env, n, dim, err);
+  check_launch("k_check_chunk_headers");
+}
+
 void dequant_rows_add_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n_rows, const int32_t* rows,
                           const int32_t* ptr, const int32_t* msg, int dim, const uint8_t* bits,
                           const uint64_t* offsets, float* out, int64_t ld, const float* mask,

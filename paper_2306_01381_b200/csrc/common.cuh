@@ -203,7 +203,19 @@ struct PackedHalo {
   const uint32_t* env = nullptr;
   int dim = 0;
   int* err = nullptr;
+  // direct: the b-range column entries are chunk words (offset / 16 in bits 0..29,
+  // width code 0 / 2 / 4 / 8 -> 0..3 in bits 30..31; encode_chunk_words) instead of
+  // slot indices, so a gather reaches its chunk in one dependent round trip; the
+  // headers are validated once per message by check_chunk_headers instead
+  bool direct = false;
 };
+// chunk words of the packed-halo gathers: out[e] = word of message idx[e] (engine.cu)
+void encode_chunk_words(const int32_t* idx, int64_t n, const uint64_t* off, const uint8_t* bits,
+                        int32_t* out, cudaStream_t s);
+// header checks of n received chunks (width, count, envelope) -> DecodeError /
+// ProtocolError in the error word, once per message (codec.hpp:82-95, engine.hpp:530-541)
+void check_chunk_headers(const uint8_t* arena, const uint64_t* off, const uint8_t* bits,
+                         const uint32_t* env, int64_t n, int dim, int* err, cudaStream_t s);
 // fp32 row-range SpMM with segmented hub rows (spmm.cu)
 // returns the number of kernels launched.  pk != nullptr: the b range (remote
 // CSR) gathers from the packed arena instead of y (spmm_packed_ok must hold).

@@ -406,6 +406,10 @@ class Engine final : public EngineBase {
       // plan version << 16, each mod 256; GPU layout): checked by K3
       DBuf<uint32_t> env;
       int64_t n_acc_rows = 0;
+      // forward keys (fp32 GPU layout): chunk word of every remote CSR entry (offset /
+      // 16 + width code of the entry's message), rebuilt with every plan, so the
+      // marginal SpMM reaches each packed halo row in one dependent round trip
+      DBuf<int32_t> words;
     };
     std::vector<SendMeta> snd;
     std::vector<RecvMeta> rcv;
@@ -475,6 +479,10 @@ class Engine final : public EngineBase {
   // concurrent encode/decode cost 1.6 ms/epoch more than running it in line.
   static bool merge_gemm_enabled() {  // QGNN_MERGE_GEMM=0: separate central / marginal GEMMs
     const char* e = std::getenv("QGNN_MERGE_GEMM");
+    return !e || std::atoi(e) != 0;
+  }
+  static bool direct_words_enabled() {  // QGNN_CHUNK_WORDS=0: slot-indexed packed gathers
+    const char* e = std::getenv("QGNN_CHUNK_WORDS");
     return !e || std::atoi(e) != 0;
   }
   static bool one_dgrad_enabled() {  // QGNN_ONE_DGRAD=0: split input gradients (A/B only)
@@ -1613,6 +1621,12 @@ void Engine<T>::upload_key_meta(int k) {
     R.bits.upload(rb);
     R.off.upload(ro);
     if (gpu_layout) R.env.upload(env);
+    if constexpr (sizeof(T) == 4) {
+      if (gpu_layout && !K.bwd && direct_words_enabled() && V.remote_nnz() > 0) {
+        if (!R.words.p) R.words.alloc(size_t(V.remote_nnz()), false);
+        encode_chunk_words(D.rslot.p, V.remote_nnz(), R.off.p, R.bits.p, R.words.p, s_main_);
+      }
+    }
   });
 }
 
@@ -1876,6 +1890,10 @@ PackedHalo Engine<T>::packed_halo(PartDev& D, int k, int64_t din) {
   pk.env = R.env.p;
   pk.dim = int(din);
   pk.err = ctx_->d_err;
+  pk.direct = R.words.p != nullptr;
+  if (pk.direct)  // the entries are chunk words: the headers are checked here, once each
+    check_chunk_headers(arena_.p, R.off.p, R.bits.p, R.env.p, R.n, int(din), ctx_->d_err,
+                        s_main_);
   return pk;
 }
 
@@ -1978,7 +1996,8 @@ void Engine<T>::forward_layer(int l) {
     kbegin(QGNN_K_SPMM_FWD);
     const PackedHalo pk = pkd ? packed_halo(D, k, din) : PackedHalo{};
     const int nk = spmm(din, D.h[t].p, ldi, pkd ? nullptr : D.halo.p, ldi, D.self_alpha.p, D.lptr.p,
-                        D.lcol.p, D.lafwd.p, D.rptr.p, D.rslot.p, D.ralpha.p, nc, nm,
+                        D.lcol.p, D.lafwd.p, D.rptr.p,
+                        pkd && pk.direct ? D.rcv[k].words.p : D.rslot.p, D.ralpha.p, nc, nm,
                         D.hagg[t].p, ldi, &D.hub_fm.plan, nullptr, 0, pkd ? &pk : nullptr);
     const double nnz = double(D.view.local_ptr[nc + nm] - D.view.local_ptr[nc]) +
                        double(D.view.remote_nnz());

@@ -380,8 +380,16 @@ __device__ __forceinline__ void packed_row8(const PackedHalo& pk, int slot, int 
                                             float4& b) {
   // off / width first (independent), then header and payload together: two
   // dependent round trips, like slot -> row for an fp32 halo row plus one
-  const int bw = __ldg(pk.bits + slot);
-  const uint8_t* ch = pk.arena + __ldg(pk.off + slot);
+  int bw;
+  const uint8_t* ch;
+  if (pk.direct) {  // slot is the chunk word: no index round trip
+    const uint32_t w = static_cast<uint32_t>(slot);
+    bw = (0x8420 >> (4 * (w >> 30))) & 0xf;  // code 0..3 -> width 0, 2, 4, 8
+    ch = pk.arena + (static_cast<uint64_t>(w & 0x3fffffffu) << 4);
+  } else {
+    bw = __ldg(pk.bits + slot);
+    ch = pk.arena + __ldg(pk.off + slot);
+  }
   const uint8_t* pl = ch + 16;
   uint2 q = make_uint2(0u, 0u);
   float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra;
@@ -402,11 +410,11 @@ __device__ __forceinline__ void packed_row8(const PackedHalo& pk, int slot, int 
   a = ra, b = rb;
   if (bw == 0) return;
   a = b = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (static_cast<int>(h.w & 0xffu) != bw || h.z != static_cast<uint32_t>(pk.dim)) {
+  if (!pk.direct && (static_cast<int>(h.w & 0xffu) != bw || h.z != static_cast<uint32_t>(pk.dim))) {
     atomicOr(pk.err, kErrDecode);  // chunk disagrees with the index (codec.hpp:90-91)
     return;
   }
-  if (pk.env && (h.w >> 8) != __ldg(pk.env + slot)) {
+  if (!pk.direct && pk.env && (h.w >> 8) != __ldg(pk.env + slot)) {
     atomicOr(pk.err, kErrProtocol);  // misrouted payload / plan-version skew (engine.hpp:530-541)
     return;
   }
