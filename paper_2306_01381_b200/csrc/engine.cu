@@ -1913,9 +1913,8 @@ void Engine<T>::forward_layer(int l) {
   const bool chain = chain_layer(l);
   // the next layer's ReLU-backward mask as bits (hbits)
   const bool bits = relu_fused() && l < L_ && relu && !chain && mask_bits_enabled();
-  if constexpr (sizeof(T) == 4)
-    if (bits)
-      for (auto& up : parts_dev_) up->hbits_rows[l] = 0;
+  for (auto& up : parts_dev_)  // this epoch's bits of h[l] are valid once every row is written
+    if (!up->hbits_rows.empty()) up->hbits_rows[l] = 0;
   auto transform = [&](PartDev& D, int64_t r0, int64_t n) {
     kbegin(QGNN_K_GEMM_FWD);
     bool done = false;
