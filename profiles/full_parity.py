@@ -1,12 +1,13 @@
 """Parity at the FULL bench workload (BASELINE configs[3]: 2.45 M nodes, 123.7 M CSR
-nnz, 3-layer GCN hidden 256, P = 8, adaptive bits): the compiled reference Engine
+nnz, 3-layer GCN hidden 256, P = 8, adaptive bits; or another BASELINE config
+at full size): the compiled reference Engine
 (oracle/_ref, fp64, kThreads) and the production fp32 GPU engine on the same graph,
 owner map, seed and settings, epoch by epoch.  North-star tolerances: losses within
 1e-4 relative, accuracies within 0.3 %; wire bytes (reference layout) and per-width
 message counts identical.  Evidence script (run on the GPU box, ~4 min, ~75 GB host
-RAM for the reference); writes gpurun_out/full_parity_cfg4.json.
+RAM for the reference at config 4); writes gpurun_out/full_parity_cfg<N>.json.
 
-    python profiles/full_parity_cfg4.py [epochs]
+    python profiles/full_parity.py [epochs] [config]   (config 2, 3, 4 or 5)
 """
 import json
 import os
@@ -23,12 +24,15 @@ from paper_2306_01381_b200.engine import Engine  # noqa: E402
 
 def main():
     epochs = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+    cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+    bench.WORKLOAD = bench.CONFIGS[cfg]
     w = bench.WORKLOAD
     g = bench.workload_graph(1)
     dims = [w["feat"], w["hidden"], w["hidden"], w["classes"]]
     t0 = time.time()
     eng = Engine(g, dims, n_parts=w["parts"], bit_mode="adaptive", seed=7, group_size=2000,
-                 period=50, theta=1.0 / (900e9 * 8), gamma=2e-5, dtype="f32", owner=g["owner"])
+                 period=50, theta=1.0 / (900e9 * 8), gamma=2e-5, dtype="f32", owner=g["owner"],
+                 sage=w["sage"])
     gpu = [eng.run_epoch() for _ in range(epochs)]
     eng.close()
     t_gpu = time.time() - t0
@@ -53,12 +57,12 @@ def main():
         ok &= r["pass"]
         rows.append(r)
     out = dict(workload=bench.config_dict(1, type("A", (), {"bit_mode": "adaptive", "bits": 8,
-                                                           "config": 4})()),
+                                                           "config": cfg})()),
                epochs=rows, all_pass=ok, gpu_seconds=t_gpu, reference_seconds=t_ref,
                reference_s_per_epoch=per, reference_setup_s=setup,
                tolerances="loss 1e-4 relative, accuracy 0.3 %, wire bytes and per-width counts exact")
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", "full_parity_cfg4.json"), "w") as f:
+    with open(os.path.join(ROOT, "gpurun_out", f"full_parity_cfg{cfg}.json"), "w") as f:
         json.dump(out, f, indent=1)
     print(json.dumps(out, indent=1))
 
