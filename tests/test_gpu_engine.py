@@ -187,6 +187,24 @@ def test_mask_bits_is_identical(cuda, monkeypatch, dims):
     assert (wa == wb).all()
 
 
+def test_engine_wide_hidden_layers_match_reference(cuda):
+    """Hidden layers wider than every specialised path (600 and 530 columns): the
+    generic wide SpMM, GEMM outputs split into 256-column blocks, the backward
+    scatter-add over more than 512 columns (grid.y slices), 19-word mask bits and
+    K1 on 600-wide rows — fp32 losses within 1e-4 and accuracies within 0.3 % of the
+    compiled reference Engine (trainer/engine.hpp) on its test graph."""
+    from oracle import ref
+    dims = [8, 600, 530, 3]
+    ep, _ = ref.engine_run(GRAPH, dims, 4, bit_mode=1, fixed_bits=8, epochs=4, seed=11)
+    eng = Engine(GRAPH, dims, n_parts=4, bit_mode="fixed", fixed_bits=8, seed=11, dtype="f32")
+    got = [eng.run_epoch() for _ in range(4)]
+    eng.close()
+    for e, m in enumerate(got):
+        assert _rel(m["train_loss"], ep[e, 0]) < 1e-4, (e, m["train_loss"], ep[e, 0])
+        assert abs(m["val_acc"] - ep[e, 1]) <= 0.003 and abs(m["test_acc"] - ep[e, 2]) <= 0.003
+        assert m["ref_bytes_total"] == ep[e, 3]
+
+
 def test_merged_forward_gemm_is_identical(cuda, monkeypatch):
     """One forward GEMM and one input-gradient GEMM per partition and layer over central
     + marginal rows (QGNN_MERGE_GEMM=1, one GPU) give bit-identical training to separate
