@@ -37,7 +37,7 @@ namespace tc {
 constexpr int kBM = 128;
 constexpr int kBK = 16;         // fp32 K elements per chunk (64-byte K-major rows)
 constexpr int kMaxStages = 6;   // ring depth is chosen per launch from the smem budget
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;  // 16 warps: warps 12-15 are the optional second epilogue group
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -199,6 +199,9 @@ struct Params {
   int64_t ldbo;
   const uint32_t* bits_in;   // ReLU-backward mask as such words (pitch ldbi), or mask
   int64_t ldbi;
+  int epi2;  // K-major: a second epilogue warp group (warps 12-15) drains the upper half
+             // of each tile's columns (wide outputs of short-K products, where the
+             // epilogue, not the MMA, paces the tile)
   int cs;  // K-major: CTAs per cluster sharing each B stage (1, 2, 4).  Rank r loads
            // B rows [r BN/cs, (r+1) BN/cs) once and multicasts them to the cluster; a
            // stage is refilled when every CTA's MMAs have drained it (empty count = cs)
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+      mbar_init(&tempty[a], p.epi2 ? 8 : 4);  // one arrival per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -374,9 +377,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) tc_commit(&tfull[acc]);
       __syncwarp();
     }
-  } else if (warp >= 4 && warp < 8) {
-    // ---------------- epilogue
+  } else if ((warp >= 4 && warp < 8) || (warp >= 12 && p.epi2 && !kMN)) {
+    // ---------------- epilogue (group 0: warps 4-7; with epi2, group 1: warps 12-15
+    // takes the upper half of the 32-column groups)
     const int q = warp & 3;
+    const int grp = warp >= 12 ? 1 : 0;
+    const int ngrp = (p.BN + 31) / 32;
+    const int cg0 = p.epi2 ? (grp ? (ngrp + 1) / 2 : 0) : 0;
+    const int cg1 = p.epi2 ? (grp ? ngrp : (ngrp + 1) / 2) : ngrp;
     int it = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
       int m0, kc0, kc1, split;
@@ -390,10 +398,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       float* out_base = p.out + (kMN ? int64_t(split) * p.M * p.N : 0);
       // explicit shared-space accesses (the uintptr-aligned base would otherwise
       // compile to generic LD/ST)
-      const uint32_t st_s = smem_u32(stage_out + q * (32 * 36));
+      const uint32_t st_s = smem_u32(stage_out + (4 * grp + q) * (32 * 36));
       // 32-column groups: TMEM -> registers (thread = row) -> ReLU / mask -> smem
       // -> registers (8 lanes = one 128-byte row segment) -> coalesced stores
-      for (int c0 = 0; c0 < p.BN; c0 += 32) {
+      for (int c0 = 32 * cg0; c0 < 32 * cg1; c0 += 32) {
         const int cc = c0 + 4 * (lane & 7);
         // ReLU-backward mask of this lane's 8 output segments, loaded up front
         float4 mk[8];
@@ -486,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc0]);
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 8 && warp < 12) {
     // ---------------- converters
     const int t = threadIdx.x - 256;
     int s = 0;
@@ -590,6 +598,11 @@ int gemm_bk() {  // QGNN_GEMM_BK=32: 128-byte K-major rows (SW128) for z = A W /
   return e && std::atoi(e) == 32 ? 32 : 16;
 }
 
+bool gemm_epi2() {  // QGNN_GEMM_EPI2=0: one epilogue warp group for every shape
+  const char* e = std::getenv("QGNN_GEMM_EPI2");
+  return !e || std::atoi(e) != 0;
+}
+
 int gemm_cluster() {  // QGNN_GEMM_CLUSTER: CTAs sharing each B stage (1, 2, 4 or 8)
   const char* e = std::getenv("QGNN_GEMM_CLUSTER");
   const int v = e ? std::atoi(e) : 2;
@@ -608,19 +621,22 @@ int pow2_cols(int bn) {
 }
 
 constexpr size_t kSmemBudget = 200 * 1024;  // + 18 KB epilogue staging (<= 227 KB)
-int stages_for(int BN, int mh = 1, int bk = tc::kBK) {
+constexpr size_t kStaging = 4 * 32 * 36 * sizeof(float);  // one epilogue group's blocks
+// the second epilogue group's staging comes out of the ring's budget
+int stages_for(int BN, int mh = 1, int bk = tc::kBK, int epi2 = 0) {
   const size_t stage = 2 * tc::kBM * bk * 4 * size_t(mh) + 2 * size_t(BN) * bk * 4;
-  return int(std::max<size_t>(2, std::min<size_t>(tc::kMaxStages, kSmemBudget / stage)));
+  const size_t budget = kSmemBudget - (epi2 ? kStaging : 0);
+  return int(std::max<size_t>(2, std::min<size_t>(tc::kMaxStages, budget / stage)));
 }
-size_t smem_bytes(int BN, int mh = 1, int bk = tc::kBK) {
+size_t smem_bytes(int BN, int mh = 1, int bk = tc::kBK, int epi2 = 0) {
   const size_t stage = 2 * tc::kBM * bk * 4 * size_t(mh) + 2 * size_t(BN) * bk * 4;
-  return size_t(stages_for(BN, mh, bk)) * stage + 1024 + 256 + 4 * 32 * 36 * sizeof(float);
+  return size_t(stages_for(BN, mh, bk, epi2)) * stage + 1024 + 256 + (epi2 ? 2 : 1) * kStaging;
 }
 
 template <bool kMN>
 void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo, const tc::Params& p,
             int num_sms, cudaStream_t s) {
-  const size_t sm = smem_bytes(p.BN, p.mh, kMN ? tc::kBK : p.bk);
+  const size_t sm = smem_bytes(p.BN, p.mh, kMN ? tc::kBK : p.bk, p.epi2);
   static bool attr_set = false;
   if (!attr_set) {
     QGNN_CUDA(cudaFuncSetAttribute(tc::k_tc_gemm<kMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -746,7 +762,8 @@ void tc_gemm_block(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, i
   p.cs = cs;
   p.dbg = gemm_debug();
   if (cs > 1) p.m_tiles = int(round_up(p.m_tiles, cs));
-  p.stages = stages_for(BN, p.mh, bk);
+  p.epi2 = gemm_epi2() && p.k_chunks <= 8 && BN >= 128 && !(p.dbg & 8) ? 1 : 0;
+  p.stages = stages_for(BN, p.mh, bk, p.epi2);
   launch<false>(ta, tb, tbl, p, ctx->num_sms, s);
 }
 
