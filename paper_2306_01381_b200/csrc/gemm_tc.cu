@@ -199,6 +199,8 @@ struct Params {
   int64_t ldbo;
   const uint32_t* bits_in;   // ReLU-backward mask as such words (pitch ldbi), or mask
   int64_t ldbi;
+  int conv2;  // warps 12-15 join the converters (8 warps split each landed tile): the
+              // weight gradient, whose converters split both operands of every chunk
   int epi2;  // K-major: a second epilogue warp group (warps 12-15) drains the upper half
              // of each tile's columns (wide outputs of short-K products, where the
              // epilogue, not the MMA, paces the tile)
@@ -238,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 4);  // one arrival per converter warp
+      mbar_init(&conv[s], p.conv2 ? 8 : 4);  // one arrival per converter warp
       mbar_init(&empty[s], uint32_t(p.cs));
     }
     for (int a = 0; a < 2; ++a) {
@@ -494,9 +496,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc0]);
     }
-  } else if (warp >= 8 && warp < 12) {
-    // ---------------- converters
-    const int t = threadIdx.x - 256;
+  } else if ((warp >= 8 && warp < 12) || (warp >= 12 && p.conv2)) {
+    // ---------------- converters (warps 8-11, with conv2 also 12-15)
+    const int t = threadIdx.x - 256;  // 0..127, or 0..255 with conv2
+    const int nthr = p.conv2 ? 256 : 128;
     int s = 0;
     uint32_t ph = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -506,10 +509,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&full[s], ph);
         uint8_t* st = smem + s * stage_bytes;
         if (!(p.dbg & 4))
-          split_tile(smem_u32(st), smem_u32(st + a_bytes), a_bytes / 16, t, 128);
+          split_tile(smem_u32(st), smem_u32(st + a_bytes), a_bytes / 16, t, nthr);
         if (kMN)
           split_tile(smem_u32(st + 2 * a_bytes), smem_u32(st + 2 * a_bytes + b_bytes),
-                     b_bytes / 16, t, 128);
+                     b_bytes / 16, t, nthr);
         fence_proxy_async();
         __syncwarp();
         if ((t & 31) == 0) mbar_arrive(&conv[s]);
@@ -596,6 +599,11 @@ int gemm_debug() {
 int gemm_bk() {  // QGNN_GEMM_BK=32: 128-byte K-major rows (SW128) for z = A W / dz W^T
   const char* e = std::getenv("QGNN_GEMM_BK");
   return e && std::atoi(e) == 32 ? 32 : 16;
+}
+
+bool gemm_conv2() {  // QGNN_GEMM_CONV2=0: four converter warps for the weight gradient too
+  const char* e = std::getenv("QGNN_GEMM_CONV2");
+  return !e || std::atoi(e) != 0;
 }
 
 bool gemm_epi2() {  // QGNN_GEMM_EPI2=0: one epilogue warp group for every shape
@@ -763,6 +771,7 @@ void tc_gemm_block(qgnn_ctx* ctx, const float* A, int64_t lda, const float* W, i
   p.dbg = gemm_debug();
   if (cs > 1) p.m_tiles = int(round_up(p.m_tiles, cs));
   p.epi2 = gemm_epi2() && p.k_chunks <= 8 && BN >= 128 && !(p.dbg & 8) ? 1 : 0;
+  p.conv2 = 0;  // K-major rings are not conversion-paced (profiles/ab_gemm_conv2_r2.txt)
   p.stages = stages_for(BN, p.mh, bk, p.epi2);
   launch<false>(ta, tb, tbl, p, ctx->num_sms, s);
 }
@@ -808,6 +817,7 @@ float* tc_gemm_wgrad_partials(qgnn_ctx* ctx, const float* A, int64_t lda, const 
   p.cs = 1;
   p.bk = tc::kBK;
   p.dbg = gemm_debug();
+  p.conv2 = gemm_conv2() ? 1 : 0;
   p.stages = stages_for(BN, mh);
   launch<true>(ta, tb, tb, p, ctx->num_sms, s);
   *splits_out = splits;
