@@ -608,6 +608,7 @@ class Engine final : public EngineBase {
   }
   void step();
   void adaptive_round(qgnn_epoch_metrics* m);
+  size_t window_layout(std::vector<int64_t>& stride, std::vector<int64_t>& koff);
   uint64_t msg_offset_send(int k, int p, int q) const { return send_base_[k][p][q]; }
   void arena_layout();
   // profiling
@@ -1117,6 +1118,10 @@ Engine<T>::Engine(const qgnn_settings& s, int64_t n, const int64_t* ptr, const i
   phase("message metadata");
   QGNN_CUDA(cudaDeviceSynchronize());
   negotiate_sizes();
+  if (s_.bit_mode == kAdaptive) {  // the re-solve's pinned window buffer
+    std::vector<int64_t> stride, koff;
+    window_layout(stride, koff);
+  }
   phase("sync / negotiate");
 }
 
@@ -2647,15 +2652,14 @@ void Engine<T>::finish_epoch(qgnn_epoch_metrics* m) {
   *m = em;
 }
 
-// gather_stats (engine.hpp:135-165) + reassignment_round (solve.hpp:337-363) + adopt_plan (:851-861)
+// Host layout of the trace windows the re-solve reads (every sender partition,
+// all ranks): key k's lo values of partition p at win_host_[koff[k] + p *
+// stride[k] + i], its hi values half a buffer later.  The message lists are
+// fixed after setup, so the pinned buffer is allocated once, at construction.
 template <typename T>
-void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
-  NvtxRange nv("qgnn adaptive re-solve, epoch", int64_t(epoch_));
-  if (s_.period <= 0 || epoch_ % uint64_t(s_.period) != 0) return;
-  const auto t0 = std::chrono::steady_clock::now();
-  // windows of every sender partition (all ranks): key k's lo values of partition p
-  // at win_host_[koff[k] + p * stride[k] + i], its hi values half a buffer later
-  std::vector<int64_t> stride(keys_.size()), koff(keys_.size() + 1, 0);
+size_t Engine<T>::window_layout(std::vector<int64_t>& stride, std::vector<int64_t>& koff) {
+  stride.assign(keys_.size(), 0);
+  koff.assign(keys_.size() + 1, 0);
   for (size_t k = 0; k < keys_.size(); ++k) {
     int64_t maxn = 0;
     for (int64_t p = 0; p < P_; ++p) {
@@ -2668,13 +2672,24 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
     koff[k + 1] = koff[k] + P_ * stride[k];
   }
   const size_t half = size_t(koff[keys_.size()]);
-  if (win_cap_ < 2 * half) {  // grows once (message lists are fixed after setup)
+  if (win_cap_ < 2 * half) {
     if (win_host_) QGNN_CUDA(cudaFreeHost(win_host_));
     QGNN_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&win_host_), 2 * half * sizeof(T),
                             cudaHostAllocDefault));
     if (s_.world > 1) win_dev_.alloc(2 * half, false);
     win_cap_ = 2 * half;
   }
+  return half;
+}
+
+// gather_stats (engine.hpp:135-165) + reassignment_round (solve.hpp:337-363) + adopt_plan (:851-861)
+template <typename T>
+void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
+  NvtxRange nv("qgnn adaptive re-solve, epoch", int64_t(epoch_));
+  if (s_.period <= 0 || epoch_ % uint64_t(s_.period) != 0) return;
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<int64_t> stride, koff;
+  const size_t half = window_layout(stride, koff);
   for (size_t k = 0; k < keys_.size(); ++k) {
     const int64_t ppr = P_ / s_.world;
     for (auto& up : parts_dev_) {
@@ -2727,6 +2742,7 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
           PairStat ps;
           ps.src = uint32_t(p);
           ps.dst = uint32_t(q);
+          ps.msgs.reserve(m.ids.size());
           for (size_t i = 0; i < m.ids.size(); ++i) {
             const size_t w = size_t(koff[k] + p * stride[k] + mb + int64_t(i));
             const double lo = double(win_host_[w]);
@@ -2814,11 +2830,12 @@ void Engine<T>::adaptive_round(qgnn_epoch_metrics*) {
   if (std::getenv("QGNN_RESOLVE_PROFILE"))
     std::fprintf(stderr,
                  "[resolve] windows %.3f s, solve+adopt %.3f s, arena %.3f s, upload %.3f s, "
-                 "total %.3f s\n",
+                 "total %.3f s (%u host threads)\n",
                  std::chrono::duration<double>(t_win - t0).count(),
                  std::chrono::duration<double>(t_adopt - t_win).count(),
                  std::chrono::duration<double>(t_arena - t_adopt).count(),
-                 std::chrono::duration<double>(t_meta - t_arena).count(), resolve_seconds_);
+                 std::chrono::duration<double>(t_meta - t_arena).count(), resolve_seconds_,
+                 std::thread::hardware_concurrency());
 }
 
 template <typename T>

@@ -85,18 +85,31 @@ bool better(const Eval& a, const std::vector<int>& ba, const Eval& b, const std:
   return ba > bb;
 }
 
-// Per-pair knapsack over scaled bit totals (solve.hpp:125-194).  minvar is
-// stored flat, row j = groups j.. with capacity c.
+// Per-pair knapsack over scaled bit totals (solve.hpp:125-194).  The
+// reference fills a dense (groups + 1) x (smax + 1) table of least variances
+// (148 MB over the 56 pairs of the bench's re-solve); each row is a step
+// function of the capacity c whose steps sit at achievable bit totals, so row
+// j is kept as its frontier: ascending totals with strictly decreasing
+// variance, mv(j, c) = the value of the last entry <= c.  Every entry's value
+// is var(bits) + value of a row-(j+1) entry, added in the reference's order,
+// and rounding is monotone, so min over the entries <= c equals the dense
+// cell bit for bit.
 struct Table {
   double theta = 0, gamma = 0;
   uint64_t unit = 1, smax = 0;
   size_t n = 0;
   std::vector<uint64_t> w;  // [j*3 + bi]
-  std::vector<double> minvar;  // [(j) * (smax+1) + c], j in [0, n]
-  std::vector<char> reachable;
-  double mv(size_t j, uint64_t c) const { return minvar[j * (smax + 1) + c]; }
+  std::vector<std::vector<uint64_t>> fw;  // frontier totals of row j, j in [0, n]
+  std::vector<std::vector<double>> fv;    // their least variances (strictly decreasing)
+  std::vector<uint64_t> reach;            // every achievable total, ascending
+  double mv(size_t j, uint64_t c) const {
+    const auto& r = fw[j];
+    const auto it = std::upper_bound(r.begin(), r.end(), c);
+    return it == r.begin() ? std::numeric_limits<double>::infinity()
+                           : fv[j][size_t(it - r.begin()) - 1];
+  }
   double time_at(uint64_t s) const { return theta * static_cast<double>(s * unit) + gamma; }
-  std::optional<uint64_t> cap_for(double z) const {
+  std::optional<uint64_t> cap_for(double z) const {  // solve.hpp:137-148
     if (time_at(0) > z) return std::nullopt;
     uint64_t lo = 0, hi = smax;
     while (lo < hi) {
@@ -107,6 +120,11 @@ struct Table {
         hi = mid - 1;
     }
     return lo;
+  }
+  // largest achievable total <= c, or -1
+  int64_t reach_below(uint64_t c) const {
+    const auto it = std::upper_bound(reach.begin(), reach.end(), c);
+    return it == reach.begin() ? -1 : int64_t(*(it - 1));
   }
 };
 
@@ -123,46 +141,43 @@ Table build_table(const PlanPairG& pp, const Cost& cm) {
     for (int bi = 0; bi < 3; ++bi) t.w[j * 3 + bi] = pp.groups[j].dim_sum() * kBits[bi] / t.unit;
     t.smax += t.w[j * 3 + 2];
   }
-  QGNN_REQUIRE((t.n + 1) * (t.smax + 1) <= (uint64_t{1} << 31), QGNN_ERESOURCE,
-               "solve_assignment: knapsack table too large (raise group_size)");
-  const double inf = std::numeric_limits<double>::infinity();
-  const size_t W = t.smax + 1;
-  t.minvar.assign((t.n + 1) * W, inf);
-  std::fill(t.minvar.begin() + t.n * W, t.minvar.end(), 0.0);
+  t.fw.resize(t.n + 1);
+  t.fv.resize(t.n + 1);
+  t.fw[t.n] = {0};  // no groups left: variance 0 at every capacity
+  t.fv[t.n] = {0.0};
+  std::vector<std::pair<uint64_t, double>> e;
   for (size_t j = t.n; j-- > 0;) {
-    const double* below = &t.minvar[(j + 1) * W];
-    double* row = &t.minvar[j * W];
-    double var[3];
-    for (int bi = 0; bi < 3; ++bi) var[bi] = variance_at(pp.groups[j].beta, kBits[bi]);
-    for (uint64_t c = 0; c <= t.smax; ++c) {
-      double best = inf;
-      for (int bi = 2; bi >= 0; --bi) {  // prefer larger bits on ties
-        const uint64_t wt = t.w[j * 3 + bi];
-        if (wt > c) continue;
-        const double b = below[c - wt];
-        if (b == inf) continue;
-        const double v = var[bi] + b;
-        if (v < best) best = v;
+    const auto& bw = t.fw[j + 1];
+    const auto& bv = t.fv[j + 1];
+    e.clear();
+    for (int bi = 0; bi < 3; ++bi) {
+      const double var = variance_at(pp.groups[j].beta, kBits[bi]);
+      for (size_t k = 0; k < bw.size(); ++k) e.emplace_back(bw[k] + t.w[j * 3 + bi], var + bv[k]);
+    }
+    std::sort(e.begin(), e.end());
+    double best = std::numeric_limits<double>::infinity();
+    for (const auto& [wt, v] : e)
+      if (v < best) {  // first entry of a total is its least value
+        t.fw[j].push_back(wt);
+        t.fv[j].push_back(v);
+        best = v;
       }
-      row[c] = best;
-    }
   }
-  t.reachable.assign(W, 0);
-  t.reachable[0] = 1;
-  std::vector<char> next(W);
+  t.reach = {0};
+  std::vector<uint64_t> next;
   for (size_t j = 0; j < t.n; ++j) {
-    std::fill(next.begin(), next.end(), 0);
-    for (uint64_t s = 0; s <= t.smax; ++s) {
-      if (!t.reachable[s]) continue;
-      for (int bi = 0; bi < 3; ++bi) next[s + t.w[j * 3 + bi]] = 1;
-    }
-    t.reachable.swap(next);
+    next.clear();
+    for (int bi = 0; bi < 3; ++bi)
+      for (uint64_t s : t.reach) next.push_back(s + t.w[j * 3 + bi]);
+    std::sort(next.begin(), next.end());
+    next.erase(std::unique(next.begin(), next.end()), next.end());
+    t.reach.swap(next);
   }
   return t;
 }
 
 // greedy largest-bits walk consistent with the minima (solve.hpp:197-214)
-void reconstruct(const Table& t, const PlanPairG& pp, uint64_t cap, std::vector<int>& out) {
+void reconstruct(const Table& t, const PlanPairG& pp, uint64_t cap, int* out) {
   uint64_t c = cap;
   const double inf = std::numeric_limits<double>::infinity();
   for (size_t j = 0; j < pp.groups.size(); ++j) {
@@ -178,7 +193,7 @@ void reconstruct(const Table& t, const PlanPairG& pp, uint64_t cap, std::vector<
         break;
       }
     }
-    out.push_back(pick);
+    out[j] = pick;
   }
 }
 }  // namespace
@@ -189,6 +204,43 @@ double compute_beta(const MsgStat& m) {  // trace.hpp:71-74
   const double range = m.hi - m.lo;
   return m.asq * static_cast<double>(m.dim) * range * range / 6.0;
 }
+
+namespace {
+// Stable LSD radix sort by descending value of non-negative doubles (11-bit
+// digits over the IEEE pattern, constant digits skipped).
+template <typename K>
+void radix_sort_desc(std::vector<K>& v) {
+  const size_t n = v.size();
+  if (n < 2) return;
+  std::vector<K> tmp(n);
+  std::vector<uint64_t> key(n), ktmp(n);
+  for (size_t i = 0; i < n; ++i) {
+    uint64_t b;
+    std::memcpy(&b, &v[i].beta, 8);
+    key[i] = ~b;
+  }
+  constexpr int kDig = 11, kB = 1 << kDig;
+  std::vector<uint32_t> cnt(kB);
+  for (int sh = 0; sh < 64; sh += kDig) {
+    std::fill(cnt.begin(), cnt.end(), 0u);
+    for (size_t i = 0; i < n; ++i) ++cnt[(key[i] >> sh) & (kB - 1)];
+    if (cnt[(key[0] >> sh) & (kB - 1)] == n) continue;  // one digit value: order unchanged
+    uint32_t s = 0;
+    for (auto& c : cnt) {
+      const uint32_t t = c;
+      c = s;
+      s += t;
+    }
+    for (size_t i = 0; i < n; ++i) {
+      const uint32_t d = cnt[(key[i] >> sh) & (kB - 1)]++;
+      tmp[d] = v[i];
+      ktmp[d] = key[i];
+    }
+    v.swap(tmp);
+    key.swap(ktmp);
+  }
+}
+}  // namespace
 
 SolveResult group_and_order(const std::vector<PairStat>& pairs, int64_t group_size) {
   QGNN_REQUIRE(group_size > 0, QGNN_EINVAL, "group_and_order: group_size must be > 0");
@@ -201,26 +253,51 @@ SolveResult group_and_order(const std::vector<PairStat>& pairs, int64_t group_si
     }
   }
   // pairs are independent: grouped on worker threads, kept in input order
+  // (beta desc, id asc) as in the reference's stable_sort.  Messages arrive in
+  // ascending id (the engine's send order), so a stable LSD radix sort on the
+  // descending-beta bit pattern gives that order directly (beta >= 0: the IEEE
+  // pattern is monotone); any other input — unsorted ids, a NaN or -0 beta —
+  // keeps the reference's stable_sort call.
+  struct Key {
+    double beta;
+    uint32_t id, idx;
+  };
   std::vector<PlanPairG> out(pairs.size());
   auto one = [&](size_t pi) {
     const PairStat& p = pairs[pi];
-    std::vector<std::pair<double, const MsgStat*>> order;
-    order.reserve(p.msgs.size());
-    for (const MsgStat& m : p.msgs) order.emplace_back(compute_beta(m), &m);
-    std::stable_sort(order.begin(), order.end(), [](const auto& a, const auto& b) {
-      if (a.first != b.first) return a.first > b.first;
-      return a.second->id < b.second->id;
-    });
+    const size_t n = p.msgs.size();
+    std::vector<Key> order(n);
+    bool radix = true;
+    for (size_t i = 0; i < n; ++i) {
+      order[i] = {compute_beta(p.msgs[i]), p.msgs[i].id, uint32_t(i)};
+      radix &= !std::signbit(order[i].beta) && !std::isnan(order[i].beta) &&
+               (i == 0 || p.msgs[i - 1].id < p.msgs[i].id);
+    }
+    if (radix) {
+      radix_sort_desc(order);
+    } else {
+      std::stable_sort(order.begin(), order.end(), [](const Key& a, const Key& b) {
+        if (a.beta != b.beta) return a.beta > b.beta;
+        return a.id < b.id;
+      });
+    }
     PlanPairG pp;
     pp.src = p.src;
     pp.dst = p.dst;
-    for (size_t i = 0; i < order.size(); i += static_cast<size_t>(group_size)) {
+    const size_t gs = static_cast<size_t>(group_size);
+    pp.groups.reserve((n + gs - 1) / gs);
+    for (size_t i = 0; i < n; i += gs) {
+      const size_t e = std::min(n, i + gs);
       Group g;
-      for (size_t j = i; j < std::min(order.size(), i + static_cast<size_t>(group_size)); ++j) {
-        g.ids.push_back(order[j].second->id);
-        g.pos.push_back(order[j].second->pos);
-        g.dims.push_back(order[j].second->dim);
-        g.beta += order[j].first;
+      g.ids.reserve(e - i);
+      g.pos.reserve(e - i);
+      g.dims.reserve(e - i);
+      for (size_t j = i; j < e; ++j) {
+        const MsgStat& m = p.msgs[order[j].idx];
+        g.ids.push_back(m.id);
+        g.pos.push_back(m.pos);
+        g.dims.push_back(m.dim);
+        g.beta += order[j].beta;
       }
       pp.groups.push_back(std::move(g));
     }
@@ -249,9 +326,10 @@ SolveResult group_and_order(const std::vector<PairStat>& pairs, int64_t group_si
 // reachable transfer times) gives each pair its min-variance assignment under
 // cap(z); the best (objective, variance, larger bits) wins.  Same caps, same
 // reconstruction, same evaluation order as the reference, but:
-//  * caps are non-decreasing in z, so each pair's cap advances by pointer
-//    instead of a binary search per candidate;
-//  * a pair is reconstructed only when its cap moves, and a candidate is
+//  * knapsack rows are frontiers (Table), and a pair's cap is tracked as the
+//    largest achievable total under it; with theta >= 0 that index only
+//    advances (a pointer instead of a binary search per candidate);
+//  * a pair is reconstructed only when that total moves, and a candidate is
 //    evaluated only when some pair's bits actually changed (identical bits give
 //    an identical evaluation, which never beats the earlier candidate);
 //  * per-group variances for the three widths are tabulated once;
@@ -290,36 +368,44 @@ struct ScanBest {
   std::vector<int> bits;
 };
 
+// k[i] indexes the largest achievable total of pair i that fits the budget
+// (reach_below(cap_for(z))), -1 if none (then mv(0, cap) is infinite: the
+// candidate is infeasible).  Every step of every row sits at an achievable
+// total, so the greedy walk gives the same bits anywhere between two
+// consecutive totals: a pair is rebuilt only when its k moves.
 void scan(const EvalCtx& C, const std::vector<Table>& tables, const std::vector<double>& cand,
-          size_t c0, size_t c1, ScanBest& out) {
+          size_t c0, size_t c1, bool monotone, ScanBest& out) {
   if (c0 >= c1) return;
   const SolveResult& plan = *C.plan;
-  const double inf = std::numeric_limits<double>::infinity();
   const size_t P = tables.size();
-  // cap[i] = largest s <= smax with time_at(s) <= z (cap_for), or -1 if none
-  std::vector<int64_t> cap(P, -1);
-  std::vector<int64_t> done(P, -2);  // cap the bits below were built for
-  std::vector<int> bits(C.dimsum.size(), 0);
+  auto locate = [&](const Table& t, double z) -> int64_t {
+    const auto c = t.cap_for(z);
+    if (!c) return -1;
+    return int64_t(std::upper_bound(t.reach.begin(), t.reach.end(), *c) - t.reach.begin()) - 1;
+  };
+  std::vector<int64_t> k(P, -1), done(P, -2);
+  std::vector<int> bits(C.dimsum.size(), 0), nb;
   bool dirty = true;
-  for (size_t i = 0; i < P; ++i) {
-    const auto c = tables[i].cap_for(cand[c0]);
-    cap[i] = c ? int64_t(*c) : -1;
-  }
+  for (size_t i = 0; i < P; ++i) k[i] = locate(tables[i], cand[c0]);
   for (size_t ci = c0; ci < c1; ++ci) {
     const double z = cand[ci];
     bool feasible = true;
     for (size_t i = 0; i < P; ++i) {
       const Table& t = tables[i];
-      while (cap[i] < int64_t(t.smax) && t.time_at(uint64_t(cap[i] + 1)) <= z) ++cap[i];
-      if (cap[i] < 0 || t.mv(0, uint64_t(cap[i])) == inf) {
+      if (!monotone)
+        k[i] = locate(t, z);
+      else  // time_at non-decreasing: the index only advances
+        while (k[i] + 1 < int64_t(t.reach.size()) && t.time_at(t.reach[size_t(k[i] + 1)]) <= z)
+          ++k[i];
+      if (k[i] < 0) {
         feasible = false;
-        continue;  // keep advancing the other caps
+        continue;  // keep advancing the other pairs
       }
-      if (done[i] != cap[i]) {
-        std::vector<int> nb;
-        nb.reserve(plan.pairs[i].groups.size());
-        reconstruct(t, plan.pairs[i], uint64_t(cap[i]), nb);
-        done[i] = cap[i];
+      if (done[i] != k[i]) {
+        const size_t ng = plan.pairs[i].groups.size();
+        nb.resize(ng);
+        reconstruct(t, plan.pairs[i], t.reach[size_t(k[i])], nb.data());
+        done[i] = k[i];
         if (!std::equal(nb.begin(), nb.end(), bits.begin() + C.pair_first[i])) {
           std::copy(nb.begin(), nb.end(), bits.begin() + C.pair_first[i]);
           dirty = true;
@@ -363,9 +449,11 @@ void solve_exact(SolveResult& plan, const Cost& cm, double lambda) {
       QGNN_REQUIRE(e.empty(), QGNN_ERESOURCE, e);
   }
   std::vector<double> cand;
-  for (const Table& t : tables)
-    for (uint64_t s = 0; s <= t.smax; ++s)
-      if (t.reachable[s]) cand.push_back(t.time_at(s));
+  bool monotone = true;
+  for (const Table& t : tables) {
+    monotone &= t.theta >= 0.0 && std::isfinite(t.theta) && std::isfinite(t.gamma);
+    for (uint64_t s : t.reach) cand.push_back(t.time_at(s));
+  }
   std::sort(cand.begin(), cand.end());
   cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
 
@@ -389,7 +477,7 @@ void solve_exact(SolveResult& plan, const Cost& cm, double lambda) {
     T = std::max<size_t>(1, std::min<size_t>(cand.size(), size_t(std::atoi(e))));
   std::vector<ScanBest> part(T);
   auto run = [&](size_t t) {
-    scan(C, tables, cand, cand.size() * t / T, cand.size() * (t + 1) / T, part[t]);
+    scan(C, tables, cand, cand.size() * t / T, cand.size() * (t + 1) / T, monotone, part[t]);
   };
   if (T == 1) {
     run(0);

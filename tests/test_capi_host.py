@@ -207,6 +207,85 @@ def test_solver_large_instance_matches_reference(monkeypatch, threads):
         print(f"lambda {lam}: ours {t1 - t0:.3f} s, reference {t2 - t1:.3f} s")
 
 
+@pytest.mark.skipif(not ref_available(), reason="compiled reference not present")
+def test_solver_frontier_tables_tie_cases_match_reference():
+    """The knapsack rows are kept as frontiers and each pair is rebuilt only when
+    its largest achievable total under the budget moves (host_solve.cpp).  Cases
+    that stress that: equal group variances (ties between widths and between
+    groups), lambda 0 and 1, theta = 0 (every budget equal), negative theta
+    (non-monotone budgets: the binary-searched caps), ragged last groups
+    (small gcd units), and ids in and out of ascending order (the grouping's
+    radix and stable_sort paths)."""
+    from oracle import ref
+    rs = np.random.default_rng(99)
+    n_ok = n_raise = 0
+    for trial in range(80):
+        n_dev = int(rs.integers(2, 5))
+        tie = trial % 2 == 0
+        pairs = []
+        for s in range(n_dev):
+            for d in range(n_dev):
+                if s == d or rs.random() < 0.2:
+                    continue
+                n = int(rs.integers(1, 40))
+                msgs = []
+                for i in range(n):
+                    lo = 0.0 if tie else float(rs.normal())
+                    hi = lo + (1.0 if tie else float(rs.exponential()))
+                    dim = int(rs.choice([4, 8] if tie else [3, 47, 100, 256]))
+                    msgs.append((i, dim, lo, hi, 1.0 if tie else float(rs.uniform(0.1, 2.0))))
+                if trial % 3 == 0:  # ids out of order: the grouping's stable_sort path
+                    msgs = [msgs[j] for j in rs.permutation(len(msgs))]
+                pairs.append((s, d, msgs))
+        if not pairs:
+            continue
+        kind = trial % 4
+        theta = (np.zeros(n_dev * n_dev) if kind == 1 else
+                 rs.uniform(-3e-4, 1e-3, n_dev * n_dev) if kind == 3 else
+                 rs.uniform(1e-5, 1e-3, n_dev * n_dev))
+        gamma = rs.uniform(0, 1e-2, n_dev * n_dev)
+        lam = float(rs.choice([0.0, 0.25, 0.5, 1.0]))
+        gs = int(rs.integers(1, 9))
+        try:
+            rbits, rev = ref.solve_instance(pairs, n_dev, theta, gamma, lam, gs)
+        except Exception as e:  # e.g. negative theta: no budget admits any total
+            with pytest.raises(_lib.InvalidArgument, match=str(e).split(": ", 1)[-1]):
+                _solve(pairs, n_dev, theta, gamma, lam, gs)
+            n_raise += 1
+            continue
+        bits, ev = _solve(pairs, n_dev, theta, gamma, lam, gs)
+        assert (bits == rbits).all() and (ev == rev).all(), trial
+        n_ok += 1
+    assert n_ok > 40
+
+
+@pytest.mark.skipif(not ref_available(), reason="compiled reference not present")
+def test_solver_bench_shaped_instance_matches_reference():
+    """The bench's re-solve shape (8 partitions: 56 pairs of 2000-5000
+    messages, one width per pair, groups of 500 with ragged last groups) with
+    slow enough links that all three widths are chosen."""
+    from oracle import ref
+    rs = np.random.default_rng(5)
+    n_dev = 8
+    pairs = []
+    for s in range(n_dev):
+        for d in range(n_dev):
+            if s == d:
+                continue
+            dim = int(rs.choice([100, 256, 47]))
+            lo = rs.normal(size=int(rs.integers(2000, 5000)))
+            hi = lo + rs.exponential(size=lo.size)
+            asq = rs.uniform(0.1, 2.0, lo.size)
+            pairs.append((s, d, [(i, dim, float(lo[i]), float(hi[i]), float(asq[i]))
+                                 for i in range(lo.size)]))
+    theta = np.full(n_dev * n_dev, 1e-5)
+    gamma = np.full(n_dev * n_dev, 2e-5)
+    bits, ev = _solve(pairs, n_dev, theta, gamma, 0.01, 500)
+    rbits, rev = ref.solve_instance(pairs, n_dev, theta, gamma, 0.01, 500)
+    assert (bits == rbits).all() and (ev == rev).all()
+    assert set(np.unique(bits)) == {2, 4, 8}
+
+
 def test_solver_rejects_bad_instances():  # test_assigner.cpp:265-297
     pairs = [(0, 1, [(1, 4, 0.0, 1.0, 1.0)])]
     with pytest.raises(_lib.InvalidArgument):
