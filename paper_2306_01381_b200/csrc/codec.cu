@@ -632,18 +632,23 @@ __global__ void __launch_bounds__(256, MINB) k_quantize_pack_lean(
 // of 4-8 (D = 256: 2 messages per warp; D = 100: 4).
 //
 // Element decision in fp32 with a proven error bound, exact fallback.  The
-// reference computes x = RN(RN(h - lo) / S) in fp64 (quant.hpp:81-87).  Here
-// x_f = RN_f(RN_f(h - lo) * RN_f(1/S)) with |x_f - x| <= 3.01 * 2^-24 * x, so
-// for x <= levels the distance is below dl = levels * 2^-22.  With frac_f =
-// x_f - floor(x_f) (exact) inside (dl, 1 - dl), floor(x) == floor(x_f) and
-// |frac - frac_f| < dl; the draw's top 23 bits give u_f <= u < u_f + 2^-23, so
-// (u < frac) == (u_f < frac_f) whenever |u_f - frac_f| > dl + 2^-22.  Only
-// elements failing that test (~4 * dl: 2e-4 at 8 bits) or equal to hi with a
-// non-integral x_hi take quant_fast/quant_exact, the fp64 path of the lean
-// kernel (so every code is the reference's).  h == lo gives a = 0: code 0,
-// never flagged.  The top 23 bits of the draw are bits 41..63 of the second
-// multiply: the final xorshift (z ^ z >> 31) does not touch them, and only the
-// high word of that product is formed.  32-bit form: 14 integer ops.
+// reference computes x = RN(RN(h - lo) / S) in fp64 and code = min(floor(x) +
+// (u < frac(x)), levels) (quant.hpp:81-87); that is ceil(T) - 1 for T = x + 1 - u.
+// Here (YD, the default) y = fma_f(RN_f(h - lo), RN_f(1/S), 1 - u_f) with u_f
+// the draw's top 23 bits (u_f <= u < u_f + 2^-23, and 1 - u_f exact), so
+// |y - T| <= 2.01 * 2^-24 * levels + ulp(y) / 2 + 2^-23 < 4.6e-5 < 2^-14 at 8
+// bits.  t = RZ_f(512 + y) holds floor(y * 2^14) in its mantissa: code =
+// floor(y) = t >> 14, exact whenever y's fraction is at least 2^-13 away from
+// 0 and 1 (then T is not an integer and floor(T) == floor(y), and floor(y) <=
+// levels); the rest (4 * 2^-14 = 2.4e-4 of the elements, lattice points and
+// u_f = 0 among them) take quant_fast / quant_exact, the fp64 path of the lean
+// kernel, so every code is the reference's.  h == lo (y = 1 - u_f) and h == hi
+// (x next to levels) need no special case.  The x-domain form (YD = false,
+// QGNN_K1_YDOM=0) decides floor(x_f) and u_f < frac(x_f) separately with the
+// bound dl = levels * 2^-22 and special-cases h == hi.  The top 23 bits of the
+// draw are bits 41..63 of the second multiply: the final xorshift (z ^ z >> 31)
+// does not touch them, and only the high word of that product is formed.
+// 32-bit form: 14 integer ops.
 __device__ __forceinline__ uint32_t draw_top32(uint32_t lo, uint32_t hi) {  // z = key+(e+2)phi
   const uint32_t tl = lo ^ __funnelshift_r(lo, hi, 30);  // z ^= z >> 30
   const uint32_t th = hi ^ (hi >> 30);
@@ -689,7 +694,7 @@ __device__ __forceinline__ uint32_t pack4x2(uint32_t w) {
   return (w | (w >> 12)) & 0xffu;
 }
 
-template <int EPL, int MINB>
+template <int EPL, int MINB, bool YD>
 __global__ void __launch_bounds__(256, MINB) k_quantize_pack_grp(
     const float* __restrict__ values, int64_t ld, int dim, int64_t n, int lg,
     const int32_t* __restrict__ rows, const uint32_t* __restrict__ ids,
@@ -810,6 +815,36 @@ __global__ void __launch_bounds__(256, MINB) k_quantize_pack_grp(
           if (q >= nvalid) v[q] = lo;
       }
       const uint64_t key = rng_fork(set_keys[set_of ? set_of[m] : 0], ids[m]);
+      f32ok = scale >= 0x1.0p-100 && scale <= 0x1.0p+100;
+      const float rf = __double2float_rn(__drcp_rn(scale));
+      z0 = key + static_cast<uint64_t>(e0 + 2) * kPhi;  // pre-mix state, counter e0 + 1
+      if constexpr (YD) {
+#pragma unroll
+        for (int k = 0; k < NW; ++k) {
+          uint32_t c4[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int q = 4 * k + r;
+            const uint64_t zq = z0 + static_cast<uint64_t>(q) * kPhi;
+            const uint32_t top = draw_top32(static_cast<uint32_t>(zq), static_cast<uint32_t>(zq >> 32));
+            const float vv = 2.f - __uint_as_float(__funnelshift_r(top, 0x7fu, 9));  // 1 - u_f
+            const float y = __fmaf_rn(v[q] - lo, rf, vv);
+            const uint32_t t = __float_as_uint(__fadd_rz(y, 512.f));  // 512 + floor(y * 2^14) / 2^14
+            c4[r] = t >> 14;                                        // floor(y) in the low byte
+            if (((t + 2u) & 0x3fffu) < 4u) slow |= 1u << q;         // within 2^-13 of an integer
+          }
+          w8[k] = __byte_perm(__byte_perm(c4[0], c4[1], 0x0040), __byte_perm(c4[2], c4[3], 0x0040),
+                              0x5410);
+        }
+        if (nvalid < EPL) {  // tail lane: padding bytes are zero, never patched
+#pragma unroll
+          for (int k = 0; k < NW; ++k) {
+            const int nb = nvalid - 4 * k;
+            w8[k] &= nb >= 4 ? 0xffffffffu : nb <= 0 ? 0u : (1u << (8 * nb)) - 1u;
+          }
+          slow &= (1u << nvalid) - 1u;
+        }
+      } else {
       // h == hi has x = x_hi exactly: code = floor(x_hi) + (u < frac_hi).  With
       // K = frac_hi * 2^23 and k the draw's top 23 bits, u < frac_hi <=> k < floor(K)
       // unless K is fractional and k == floor(K) (probability 2^-23: exact path).
@@ -824,12 +859,9 @@ __global__ void __launch_bounds__(256, MINB) k_quantize_pack_grp(
       } else {
         hib = levels;  // min(floor(x_hi) + inc, levels) = levels
       }
-      f32ok = scale >= 0x1.0p-100 && scale <= 0x1.0p+100;
-      const float rf = __double2float_rn(__drcp_rn(scale));
       const float dl = static_cast<float>(levels) * 0x1.0p-22f;
       const float hw = 0.5f - dl - 0x1.0p-24f;  // |fr - 1/2| > hw  <=>  dl <= fr <= 1 - dl
       const float dd = dl + 0x1.0p-22f;
-      z0 = key + static_cast<uint64_t>(e0 + 2) * kPhi;  // pre-mix state, counter e0 + 1
 #pragma unroll
       for (int k = 0; k < NW; ++k) {
         uint32_t c4[4];
@@ -852,6 +884,7 @@ __global__ void __launch_bounds__(256, MINB) k_quantize_pack_grp(
         }
         w8[k] = __byte_perm(__byte_perm(c4[0], c4[1], 0x0040), __byte_perm(c4[2], c4[3], 0x0040),
                             0x5410);
+      }
       }
       if (!f32ok) slow = nvalid == 32 ? 0xffffffffu : (1u << nvalid) - 1u;
     }
@@ -902,7 +935,7 @@ __global__ void __launch_bounds__(256, MINB) k_quantize_pack_grp(
       slow &= slow - 1;
       const float h = row[e0 + q];
       uint32_t c;
-      const uint32_t ub = f32ok && h == hi
+      const uint32_t ub = !YD && f32ok && h == hi
                               ? __funnelshift_r(draw_top32(static_cast<uint32_t>(z0 + q * kPhi),
                                                            static_cast<uint32_t>((z0 + q * kPhi) >> 32)),
                                                 0x7fu, 9)
@@ -1087,14 +1120,26 @@ int qgnn_quantize_pack(qgnn_ctx* ctx, const void* values, int dtype, int64_t ld,
     auto* wl = static_cast<float*>(win_lo);
     auto* wh = static_cast<float*>(win_hi);
     const int d = static_cast<int>(dim);
-    if (epl == 16)
-      k_quantize_pack_grp<16, 4><<<gblocks, 256, 0, s>>>(v, ld, d, n, lg, rows, ids, bits, offsets,
-                                                        set_of, set_keys, out, wl, wh, ctx->d_err,
-                                                        envelope);
-    else
-      k_quantize_pack_grp<32, 3><<<gblocks, 256, 0, s>>>(v, ld, d, n, lg, rows, ids, bits, offsets,
-                                                        set_of, set_keys, out, wl, wh, ctx->d_err,
-                                                        envelope);
+    static const bool yd = [] {  // QGNN_K1_YDOM=0: the x-domain decision (round 2 first cut)
+      const char* e = std::getenv("QGNN_K1_YDOM");
+      return !e || std::atoi(e) != 0;
+    }();
+#define QGNN_K1_GRP(E, MB, Y)                                                                       \
+  k_quantize_pack_grp<E, MB, Y><<<gblocks, 256, 0, s>>>(v, ld, d, n, lg, rows, ids, bits, offsets,  \
+                                                       set_of, set_keys, out, wl, wh, ctx->d_err,  \
+                                                       envelope)
+    if (epl == 16) {
+      if (yd)
+        QGNN_K1_GRP(16, 4, true);
+      else
+        QGNN_K1_GRP(16, 4, false);
+    } else {
+      if (yd)
+        QGNN_K1_GRP(32, 3, true);
+      else
+        QGNN_K1_GRP(32, 3, false);
+    }
+#undef QGNN_K1_GRP
   } else if (fast) {
     const int64_t fblocks = std::min<int64_t>(blocks, int64_t(ctx->num_sms) * 16);
     const int nv = static_cast<int>(ceil_div(ceil_div(dim, 4), 32));
