@@ -1234,9 +1234,17 @@ namespace qgnn_b200 {
 // Backward scatter-add, one launch: warp per destination row; the row's
 // incoming chunks (ascending source, engine.hpp:720-734) are decoded and summed
 // in registers, masked by the ReLU of h (when given) and added to out once.
-__global__ void __launch_bounds__(256) k_dequant_rows_f32(
+// The kernel is a chain of dependent loads (row list -> message -> offset ->
+// chunk), so everything that does not depend on the messages — the destination
+// row and its mask bits — is loaded before the chain starts, and a chunk's
+// header and payload are loaded together (the payload is used only if the
+// header checks pass; its bytes lie inside the arena either way).  KC float4
+// chunks per lane: 128 * KC columns per grid.y slice.
+template <int KC>
+__global__ void __launch_bounds__(64) k_dequant_rows_f32(
     const uint8_t* __restrict__ in, int64_t n_rows, const int32_t* __restrict__ rows,
-    const int32_t* __restrict__ ptr, const int32_t* __restrict__ msg, int dim,
+    const int32_t* __restrict__ ptr, const int32_t* __restrict__ msg,
+    const int32_t* __restrict__ words, int dim,
     const uint8_t* __restrict__ bits, const uint64_t* __restrict__ offsets,
     float* __restrict__ out, int64_t ld, const float* __restrict__ mask, int64_t ldm,
     int* __restrict__ err, const uint32_t* __restrict__ expect) {
@@ -1244,15 +1252,38 @@ __global__ void __launch_bounds__(256) k_dequant_rows_f32(
   const int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (g >= n_rows) return;
   const int nchunk = (dim + 3) >> 2;
-  constexpr int kMaxC = 4;  // float4 chunks per lane: 512 columns per grid.y slice
-  const int cbase = blockIdx.y * 128;
+  constexpr int kMaxC = KC;
+  const int cbase = blockIdx.y * 32 * KC;
+  const int64_t r = rows[g];
+  const int j0 = ptr[g], j1 = ptr[g + 1];
+  float4 prev[kMaxC];
+  uint32_t mb[kMaxC];
+#pragma unroll
+  for (int i = 0; i < kMaxC; ++i) {
+    const int c = cbase + lane + 32 * i;
+    prev[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    mb[i] = 0xfu;
+    if (c < nchunk && 4 * c + 3 < dim) {
+      prev[i] = *reinterpret_cast<const float4*>(out + r * ld + 4 * c);
+      if (mask) mb[i] = relu_bits4(mask, ldm, r, 4 * c);
+    }
+  }
   float4 acc[kMaxC];
 #pragma unroll
   for (int i = 0; i < kMaxC; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int j = ptr[g]; j < ptr[g + 1]; ++j) {
-    const int m = msg[j];
-    const uint8_t* chunk = in + offsets[m];
-    const int b = bits[m];
+  for (int j = j0; j < j1; ++j) {
+    int m = -1;
+    const uint8_t* chunk;
+    int b;
+    if (words) {  // chunk word: offset / 16 and width code, one load (rebuilt per plan)
+      const uint32_t w = static_cast<uint32_t>(words[j]);
+      chunk = in + (static_cast<uint64_t>(w & 0x3fffffffu) << 4);
+      b = (0x8420 >> (4 * (w >> 30))) & 0xf;  // code 0..3 -> width 0, 2, 4, 8
+    } else {
+      m = msg[j];
+      chunk = in + offsets[m];
+      b = bits[m];
+    }
     if (b == 0) {  // raw fp32 row (BitMode::kFp)
       const float4* src = reinterpret_cast<const float4*>(chunk);
 #pragma unroll
@@ -1266,47 +1297,51 @@ __global__ void __launch_bounds__(256) k_dequant_rows_f32(
       continue;
     }
     const uint4 h = *reinterpret_cast<const uint4*>(chunk);
+    const uint8_t* payload = chunk + kHdrGpu;
+    uint32_t word[kMaxC];
+#pragma unroll
+    for (int i = 0; i < kMaxC; ++i) {
+      const int c = cbase + lane + 32 * i;
+      word[i] = 0;
+      if (c < nchunk)
+        word[i] = b == 8 ? reinterpret_cast<const uint32_t*>(payload)[c]
+                : b == 4 ? reinterpret_cast<const uint16_t*>(payload)[c]
+                         : payload[c];
+    }
     if (static_cast<int>(h.w & 0xff) != b || h.z != static_cast<uint32_t>(dim)) {
       if (lane == 0) atomicOr(err, kErrDecode);
       continue;
     }
-    if (expect && (h.w >> 8) != expect[m]) {
+    if (expect && (h.w >> 8) != expect[m < 0 ? msg[j] : m]) {
       if (lane == 0) atomicOr(err, kErrProtocol);
       continue;
     }
     const float sc = __uint_as_float(h.x), zp = __uint_as_float(h.y);
-    const uint8_t* payload = chunk + kHdrGpu;
     const uint32_t cmask = (1u << b) - 1;
 #pragma unroll
     for (int i = 0; i < kMaxC; ++i) {
       const int c = cbase + lane + 32 * i;
       if (c >= nchunk) continue;
-      uint32_t word;
-      if (b == 8)
-        word = reinterpret_cast<const uint32_t*>(payload)[c];
-      else if (b == 4)
-        word = reinterpret_cast<const uint16_t*>(payload)[c];
-      else
-        word = payload[c];
-      acc[i].x += fmaf(static_cast<float>(word & cmask), sc, zp);
-      acc[i].y += fmaf(static_cast<float>((word >> b) & cmask), sc, zp);
-      acc[i].z += fmaf(static_cast<float>((word >> (2 * b)) & cmask), sc, zp);
-      acc[i].w += fmaf(static_cast<float>((word >> (3 * b)) & cmask), sc, zp);
+      const uint32_t w = word[i];
+      acc[i].x += fmaf(static_cast<float>(w & cmask), sc, zp);
+      acc[i].y += fmaf(static_cast<float>((w >> b) & cmask), sc, zp);
+      acc[i].z += fmaf(static_cast<float>((w >> (2 * b)) & cmask), sc, zp);
+      acc[i].w += fmaf(static_cast<float>((w >> (3 * b)) & cmask), sc, zp);
     }
   }
-  const int64_t r = rows[g];
 #pragma unroll
   for (int i = 0; i < kMaxC; ++i) {
     const int c = cbase + lane + 32 * i;
     if (c >= nchunk) continue;
-    float4 a = acc[i];
-    if (mask) a = apply_bits4(a, relu_bits4(mask, ldm, r, 4 * c));
     float* o = out + r * ld + 4 * c;
     if (4 * c + 3 < dim) {
-      float4 p = *reinterpret_cast<float4*>(o);
+      const float4 a = apply_bits4(acc[i], mb[i]);
+      float4 p = prev[i];
       p.x += a.x, p.y += a.y, p.z += a.z, p.w += a.w;
       *reinterpret_cast<float4*>(o) = p;
     } else {
+      float4 a = acc[i];
+      if (mask) a = apply_bits4(a, relu_bits4(mask, ldm, r, 4 * c));
       const float av[4] = {a.x, a.y, a.z, a.w};
       for (int q = 0; q < 4 && 4 * c + q < dim; ++q) o[q] += av[q];
     }
@@ -1363,13 +1398,20 @@ void check_chunk_headers(const uint8_t* arena, const uint64_t* off, const uint8_
 }
 
 void dequant_rows_add_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n_rows, const int32_t* rows,
-                          const int32_t* ptr, const int32_t* msg, int dim, const uint8_t* bits,
+                          const int32_t* ptr, const int32_t* msg, const int32_t* words, int dim,
+                          const uint8_t* bits,
                           const uint64_t* offsets, float* out, int64_t ld, const float* mask,
                           int64_t ldm, const uint32_t* expect, cudaStream_t s) {
   if (n_rows == 0) return;
-  const dim3 grid(unsigned(ceil_div(n_rows * 32, 64)), unsigned(ceil_div(dim, 512)));
-  k_dequant_rows_f32<<<grid, 64, 0, s>>>(
-      in, n_rows, rows, ptr, msg, dim, bits, offsets, out, ld, mask, ldm, ctx->d_err, expect);
+  if (dim <= 256) {
+    const dim3 grid(unsigned(ceil_div(n_rows * 32, 64)), 1);
+    k_dequant_rows_f32<2><<<grid, 64, 0, s>>>(
+        in, n_rows, rows, ptr, msg, words, dim, bits, offsets, out, ld, mask, ldm, ctx->d_err, expect);
+  } else {
+    const dim3 grid(unsigned(ceil_div(n_rows * 32, 64)), unsigned(ceil_div(dim, 512)));
+    k_dequant_rows_f32<4><<<grid, 64, 0, s>>>(
+        in, n_rows, rows, ptr, msg, words, dim, bits, offsets, out, ld, mask, ldm, ctx->d_err, expect);
+  }
   check_launch("k_dequant_rows_f32");
 }
 

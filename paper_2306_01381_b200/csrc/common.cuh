@@ -100,8 +100,11 @@ bool dense_forward_bits_f32(qgnn_ctx* ctx, const float* A, int64_t lda, const fl
                             float* out, int64_t ldo, uint32_t* bits, int64_t ldb, cudaStream_t s);
 // backward scatter-add in one launch: destination rows with their incoming
 // messages in ascending source order, decoded + summed per row (codec.cu)
+// words (optional): chunk word of every entry (encode_chunk_words over msg), so an
+// entry costs one load instead of message -> offset / width
 void dequant_rows_add_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n_rows, const int32_t* rows,
-                          const int32_t* ptr, const int32_t* msg, int dim, const uint8_t* bits,
+                          const int32_t* ptr, const int32_t* msg, const int32_t* words, int dim,
+                          const uint8_t* bits,
                           const uint64_t* offsets, float* out, int64_t ld, const float* mask,
                           int64_t ldm, const uint32_t* expect, cudaStream_t s);
 // Adam with the bias corrections in device memory (captured epoch graphs, dense.cu)
@@ -227,23 +230,4 @@ int spmm_f32(qgnn_ctx* ctx, int dim, const float* x, int64_t ldx, const float* y
 // whether spmm_f32 runs this range through a kernel with a packed-halo variant
 // (the grouped <= 128-wide and the 256-wide row kernels, 32-byte aligned rows)
 bool spmm_packed_ok(int dim, const HubPlan* hp, const float* x, int64_t ldx);
-// fp32 GPU-layout decode + scatter-add, ReLU-backward mask by h (codec.cu)
-void dequant_add_masked_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n, int dim,
-                            const uint8_t* bits, const uint64_t* offsets, const int32_t* dst_rows,
-                            float* out, int64_t ld, const float* mask, int64_t ldm,
-                            const uint32_t* expect, cudaStream_t s);
-// backward scatter-add in one launch: destination rows with their incoming
-// messages in ascending source order, decoded + summed per row (codec.cu)
-void dequant_rows_add_f32(qgnn_ctx* ctx, const uint8_t* in, int64_t n_rows, const int32_t* rows,
-                          const int32_t* ptr, const int32_t* msg, int dim, const uint8_t* bits,
-                          const uint64_t* offsets, float* out, int64_t ld, const float* mask,
-                          int64_t ldm, const uint32_t* expect, cudaStream_t s);
-// Adam with the bias corrections in device memory (captured epoch graphs, dense.cu)
-void adam_step_devbc(int dtype, void* p, void* m, void* v, const void* g, int64_t n, double lr,
-                     double beta1, double beta2, double eps, const double* bc, cudaStream_t s);
-// fp32 loss phase for the engine: CE over train rows + val/test hit counts (dense.cu)
-void loss_f32(qgnn_ctx* ctx, const float* logits, int64_t ld, int classes, const int32_t* labels,
-              const int32_t* rows, int64_t n_train, int64_t n_val, int64_t n_test,
-              double inv_denom, float* grad, int64_t ldg, double* loss_acc,
-              unsigned long long* correct, cudaStream_t s);
 }  // namespace qgnn_b200

@@ -41,6 +41,11 @@ struct DBuf {
     // legacy-stream memsets/copies do not order against our non-blocking streams
     QGNN_CUDA(cudaDeviceSynchronize());
   }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
   void upload(const std::vector<X>& v) {
     alloc(v.size(), false);
     if (!v.empty()) QGNN_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(X), cudaMemcpyHostToDevice));

@@ -485,6 +485,10 @@ class Engine final : public EngineBase {
     const char* e = std::getenv("QGNN_CHUNK_WORDS");
     return !e || std::atoi(e) != 0;
   }
+  static bool k3_words_enabled() {  // QGNN_K3_WORDS=0: message-indexed backward scatter-add
+    const char* e = std::getenv("QGNN_K3_WORDS");
+    return !e || std::atoi(e) != 0;
+  }
   static bool one_dgrad_enabled() {  // QGNN_ONE_DGRAD=0: split input gradients (A/B only)
     const char* e = std::getenv("QGNN_ONE_DGRAD");
     return !e || std::atoi(e) != 0;
@@ -573,8 +577,8 @@ class Engine final : public EngineBase {
       if (s_.layout == QGNN_WIRE_GPU) {
         kbegin(QGNN_K_DEQUANT);
         dequant_rows_add_f32(ctx_, arena_.p, R.n_acc_rows, R.acc_rows.p, R.acc_ptr.p, R.acc_msg.p,
-                             int(din), R.bits.p, R.off.p, D.dh_next.p, ldi, mask, ldm, R.env.p,
-                             s_main_);
+                             R.words.p, int(din), R.bits.p, R.off.p, D.dh_next.p, ldi, mask, ldm,
+                             R.env.p, s_main_);
         kend(QGNN_K_DEQUANT, double(R.n_acc_rows) * 2 * din * sizeof(T) + double(R.n) * 13 + wire,
              s_main_);
         return;
@@ -1627,9 +1631,16 @@ void Engine<T>::upload_key_meta(int k) {
     R.off.upload(ro);
     if (gpu_layout) R.env.upload(env);
     if constexpr (sizeof(T) == 4) {
-      if (gpu_layout && !K.bwd && direct_words_enabled() && V.remote_nnz() > 0) {
+      // chunk words hold offset / 16 in 30 bits: arenas up to 16 GiB
+      const bool words = gpu_layout && direct_words_enabled() && arena_bytes_ <= (size_t(1) << 34);
+      if (words && !K.bwd && V.remote_nnz() > 0) {
         if (!R.words.p) R.words.alloc(size_t(V.remote_nnz()), false);
         encode_chunk_words(D.rslot.p, V.remote_nnz(), R.off.p, R.bits.p, R.words.p, s_main_);
+      } else if (words && K.bwd && R.n > 0 && k3_words_enabled()) {  // per scatter-add entry
+        if (!R.words.p) R.words.alloc(size_t(R.n), false);
+        encode_chunk_words(R.acc_msg.p, R.n, R.off.p, R.bits.p, R.words.p, s_main_);
+      } else {
+        R.words.release();  // slot-indexed gathers / message-indexed scatter-add
       }
     }
   });
