@@ -1240,8 +1240,10 @@ namespace qgnn_b200 {
 // header and payload are loaded together (the payload is used only if the
 // header checks pass; its bytes lie inside the arena either way).  KC float4
 // chunks per lane: 128 * KC columns per grid.y slice.
+// 24 CTAs (48 warps) per SM: 38 registers, +40 % warps in flight for the load
+// chains over the unconstrained 49 (profiles/ab_k3_occ_r2.txt)
 template <int KC>
-__global__ void __launch_bounds__(64) k_dequant_rows_f32(
+__global__ void __launch_bounds__(64, 24) k_dequant_rows_f32(
     const uint8_t* __restrict__ in, int64_t n_rows, const int32_t* __restrict__ rows,
     const int32_t* __restrict__ ptr, const int32_t* __restrict__ msg,
     const int32_t* __restrict__ words, int dim,
