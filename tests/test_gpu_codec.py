@@ -217,7 +217,8 @@ def test_fast_path_codes_exact_on_adversarial_rows(cuda):
     assert bad == 0
 
 
-K1_DIMS = [4, 12, 16, 20, 36, 64, 68, 100, 128, 256, 260, 500, 512, 516, 602, 1000, 1024]
+K1_DIMS = [3, 4, 5, 12, 13, 16, 20, 36, 47, 64, 68, 100, 101, 128, 256, 260, 500, 512, 516, 602,
+           1000, 1024]
 
 
 def _k1_rows(rs, kind, n, d, lv):
@@ -293,3 +294,4 @@ def test_k1_production_matches_round1_kernel_at_scale(cuda):
     assert len(ref) == 6
     assert digests({"QGNN_K1_GRP": "1"}) == ref
     assert digests({"QGNN_K1_GRP": "1", "QGNN_K1_EPL": "16"}) == ref
+    assert digests({"QGNN_K1_GRP": "1", "QGNN_K1_YDOM": "0"}) == ref  # the x-domain form
